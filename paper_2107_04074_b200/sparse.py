@@ -1,0 +1,208 @@
+"""Sparse unit rows and the CSR ``Dataset`` the iteration loop consumes.
+
+API mirror of the reference (/root/reference/pkg/src/spkmeans/sparse.py):
+``SparseVector`` (22-67), ``dot_sparse_sparse`` (70-77),
+``dot_sparse_dense`` (80-87), ``normalize`` (90-98) and ``Dataset``
+(101-156).  Unlike the reference, ``Dataset`` is CSR-first: it keeps one
+set of flat arrays (int64 indptr, int32 indices, float64 values) and only
+builds per-row ``SparseVector`` objects on demand, because per-row Python
+objects are the reference's scalability wall at 10^5-10^7 rows
+(SURVEY.md §2.1 row 4).  ``Dataset.from_csr`` is the scalable entry point.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from .errors import DimensionMismatchError, ZeroNormError
+
+
+@dataclass(frozen=True)
+class SparseVector:
+    """One row: strictly increasing indices, explicit zeros removed."""
+
+    indices: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        idx = np.asarray(self.indices, dtype=np.int64)
+        val = np.asarray(self.values, dtype=np.float64)
+        if idx.ndim != 1 or idx.shape != val.shape:
+            raise ValueError("indices and values must be 1-D and equal length")
+        nz = val != 0.0
+        if not nz.all():
+            idx, val = idx[nz], val[nz]
+        if idx.size:
+            if idx[0] < 0:
+                raise ValueError("negative index")
+            if idx.size > 1 and np.any(idx[1:] <= idx[:-1]):
+                raise ValueError("indices must be strictly increasing")
+        idx.setflags(write=False)
+        val.setflags(write=False)
+        object.__setattr__(self, "indices", idx)
+        object.__setattr__(self, "values", val)
+
+    @property
+    def nnz(self) -> int:
+        return int(self.indices.size)
+
+    def norm(self) -> float:
+        return float(np.sqrt(np.dot(self.values, self.values)))
+
+    def normalized(self) -> "SparseVector":
+        nrm = self.norm()
+        if nrm == 0.0:
+            raise ZeroNormError()
+        return SparseVector(self.indices, self.values / nrm)
+
+    def densify(self, dim: int) -> np.ndarray:
+        if self.indices.size and self.indices[-1] >= dim:
+            raise DimensionMismatchError(f"index {int(self.indices[-1])} exceeds dimensionality {dim}")
+        out = np.zeros(dim)
+        out[self.indices] = self.values
+        return out
+
+
+def dot_sparse_sparse(x: SparseVector, y: SparseVector) -> float:
+    _, xi, yi = np.intersect1d(x.indices, y.indices, assume_unique=True, return_indices=True)
+    return float(np.dot(x.values[xi], y.values[yi])) if xi.size else 0.0
+
+
+def dot_sparse_dense(x: SparseVector, c: np.ndarray) -> float:
+    if x.indices.size and x.indices[-1] >= c.shape[0]:
+        raise DimensionMismatchError(f"index {int(x.indices[-1])} exceeds dense length {c.shape[0]}")
+    return float(np.dot(x.values, c[x.indices])) if x.indices.size else 0.0
+
+
+def normalize(v):
+    if isinstance(v, SparseVector):
+        return v.normalized()
+    v = np.asarray(v, dtype=np.float64)
+    nrm = float(np.linalg.norm(v))
+    if nrm == 0.0:
+        raise ZeroNormError()
+    return v / nrm
+
+
+def _row_norms(indptr, data):
+    sq = np.square(data)
+    n = indptr.size - 1
+    out = np.zeros(n)
+    nonempty = indptr[1:] > indptr[:-1]
+    if sq.size:
+        out[nonempty] = np.add.reduceat(sq, indptr[:-1][nonempty])
+    return np.sqrt(out)
+
+
+class Dataset:
+    """Unit-normalised sparse rows held as one CSR.
+
+    ``indptr`` int64[n+1], ``indices`` int32[nnz] (sorted within a row),
+    ``data`` float64[nnz].  Zero rows are rejected with their row numbers
+    (reference sparse.py:117-134).
+    """
+
+    def __init__(self, indptr, indices, data, dim: int, _checked: bool = False):
+        self.indptr = np.ascontiguousarray(indptr, dtype=np.int64)
+        self.indices = np.ascontiguousarray(indices, dtype=np.int32)
+        self.data = np.ascontiguousarray(data, dtype=np.float64)
+        self.dim = int(dim)
+        self.n = int(self.indptr.size - 1)
+        self._rows = None
+        self._csr = None
+        self._device_cache = {}
+
+    # -- construction ------------------------------------------------------
+    @classmethod
+    def from_rows(cls, rows, dim=None, normalize_rows=True) -> "Dataset":
+        rows = list(rows)
+        if not rows:
+            raise ValueError("dataset must contain at least one row")
+        max_idx = max((int(r.indices[-1]) for r in rows if r.nnz), default=-1)
+        if dim is None:
+            dim = max_idx + 1
+        elif max_idx >= dim:
+            raise DimensionMismatchError(f"row index {max_idx} exceeds declared dimensionality {dim}")
+        bad = [i for i, r in enumerate(rows) if r.nnz == 0 or r.norm() == 0.0]
+        if bad:
+            raise ZeroNormError(rows=bad)
+        if normalize_rows:
+            rows = [r.normalized() for r in rows]
+        indptr = np.zeros(len(rows) + 1, np.int64)
+        indptr[1:] = np.cumsum([r.nnz for r in rows])
+        indices = np.concatenate([r.indices for r in rows]).astype(np.int32)
+        data = np.concatenate([r.values for r in rows])
+        ds = cls(indptr, indices, data, dim)
+        ds._rows = tuple(rows)
+        return ds
+
+    @classmethod
+    def from_csr(cls, indptr, indices, data, dim, normalize_rows=True,
+                 check_sorted=True) -> "Dataset":
+        """Scalable constructor from flat CSR arrays (vectorised checks)."""
+        indptr = np.asarray(indptr, dtype=np.int64)
+        indices = np.asarray(indices, dtype=np.int64)
+        data = np.asarray(data, dtype=np.float64)
+        if indptr.size < 2:
+            raise ValueError("dataset must contain at least one row")
+        if indices.size and (indices.min() < 0):
+            raise ValueError("negative index")
+        if indices.size and indices.max() >= dim:
+            raise DimensionMismatchError(f"row index {int(indices.max())} exceeds declared dimensionality {dim}")
+        if check_sorted and indices.size > 1:
+            same_row = np.ones(indices.size - 1, bool)
+            starts = indptr[1:-1]
+            starts = starts[(starts > 0) & (starts < indices.size)]
+            same_row[starts - 1] = False
+            if np.any((indices[1:] <= indices[:-1]) & same_row):
+                raise ValueError("indices must be strictly increasing within a row")
+        if np.any(data == 0.0):
+            keep = data != 0.0
+            rowid = np.repeat(np.arange(indptr.size - 1), np.diff(indptr))
+            counts = np.bincount(rowid[keep], minlength=indptr.size - 1)
+            indptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+            indices, data = indices[keep], data[keep]
+        norms = _row_norms(indptr, data)
+        bad = np.nonzero(norms == 0.0)[0]
+        if bad.size:
+            raise ZeroNormError(rows=bad.tolist())
+        if normalize_rows:
+            data = data / np.repeat(norms, np.diff(indptr))
+        return cls(indptr, indices.astype(np.int32), data, dim)
+
+    # -- reference-compatible views ----------------------------------------
+    @property
+    def rows(self) -> tuple:
+        if self._rows is None:
+            ip, ix, dv = self.indptr, self.indices, self.data
+            self._rows = tuple(
+                SparseVector(ix[ip[i]:ip[i + 1]].astype(np.int64), dv[ip[i]:ip[i + 1]])
+                for i in range(self.n))
+        return self._rows
+
+    @property
+    def nnz(self) -> int:
+        return int(self.indices.size)
+
+    @property
+    def matrix(self):
+        if self._csr is None:
+            from scipy import sparse as sp
+            self._csr = sp.csr_matrix((self.data, self.indices, self.indptr), shape=(self.n, self.dim))
+        return self._csr
+
+    def csr_arrays(self):
+        return self.indptr, self.indices.astype(np.int64), self.data
+
+    def densify_rows(self, rows) -> np.ndarray:
+        rows = np.asarray(rows, dtype=np.int64)
+        out = np.zeros((rows.size, self.dim))
+        for q, i in enumerate(rows):
+            s, e = self.indptr[i], self.indptr[i + 1]
+            out[q, self.indices[s:e]] = self.data[s:e]
+        return out
+
+    def row_lengths(self) -> np.ndarray:
+        return np.diff(self.indptr)

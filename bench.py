@@ -1,0 +1,387 @@
+#!/usr/bin/env python3
+"""Benchmark: the accelerated spherical k-means loop on B200 vs the reference's CPU path.
+
+Workload (BASELINE.json configs[1], "C2"): n=20,000 synthetic TF-IDF docs,
+d=100,000, mean ~120 nnz/row (Zipf(1.1) terms, lognormal lengths; seeded,
+see paper_2107_04074_b200/synth.py), k=100, uniform seeded init (seed 2),
+max_iter 50.  One STEP = one complete fit of each of the five variants
+(standard, elkan, simp_elkan, hamerly, simp_hamerly) from the same start.
+metric = k-means iterations/s over the step (plus effective n*k sims/s and
+the pruned fraction as extra keys).
+
+  value      device-timed (CUDA events per step, inputs resident in HBM)
+  e2e        same work through the public API from pinned HOST buffers:
+             CSR + seed centers copied H2D and assignments D2H every step
+  roofline   the dominant kernel's algorithmic bytes / its event time
+  cpu_baseline  the CPU oracle (C port of the reference loop, OpenMP over
+             points) on a bounded sample, rank 0 at N=1 only
+
+--impl reference runs the oracle port (the reference package is Python and
+cannot travel to the GPU box) on the same workload.  Multi-GPU (torchrun):
+rows sharded by nnz, one allreduce per iteration; strong scaling.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+VARIANTS = ("standard", "elkan", "simp_elkan", "hamerly", "simp_hamerly")
+METRIC = "k-means iterations/s (C2, k=100, 5 variants per step)"
+PEAKS = ROOT / "MEASURED_PEAKS.json"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    p.add_argument("--config", default="C2")
+    p.add_argument("--k", type=int, default=100)
+    p.add_argument("--seed", type=int, default=2)
+    p.add_argument("--max-iter", type=int, default=50)
+    p.add_argument("--variants", default=",".join(VARIANTS))
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--profile-only", action="store_true", help="one untimed step (for ncu)")
+    return p.parse_args()
+
+
+def peaks():
+    try:
+        return json.loads(PEAKS.read_text()), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.samples.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+        return False
+
+    def summary(self):
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for s in self.samples:
+            try:
+                sm.append(float(s[0]))
+                mx = float(s[1])
+                for nm, flag in zip(names, s[3:7]):
+                    if flag.lower().startswith("active"):
+                        reasons.add(nm)
+            except Exception:
+                continue
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ----------------------------------------------------------------- workload
+def load_workload(args):
+    from paper_2107_04074_b200 import synth
+    t = time.time()
+    data = synth.config_dataset(args.config)
+    return data, time.time() - t
+
+
+def workload_config(args, data, n_gpus):
+    return {"workload": f"{args.config} n={data.n} d={data.dim} nnz={data.nnz} k={args.k}; "
+                        f"one step = one fit of each of [{args.variants}] (seed {args.seed}, max_iter {args.max_iter})",
+            "global_batch": data.n, "k": args.k, "variants": args.variants.split(","),
+            "parallelism": f"dp{n_gpus} (rows sharded by nnz, centers replicated)",
+            "l2": "flushed (256 MiB write) before every timed step",
+            "precision": "fp32 similarities, fp64 centers, exact int64 fixed-point sums"}
+
+
+# ----------------------------------------------------------------- reference arm
+def run_reference(args):
+    from oracle import oracle as O
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    data, _ = load_workload(args)
+    X = O.CSR(data.indptr, data.indices, data.data, data.dim)
+    variants = args.variants.split(",")
+    cores = O.num_threads()
+
+    def step():
+        its = 0
+        for v in variants:
+            r = O.run(X, args.k, v, seed=args.seed, max_iter=args.max_iter)
+            its += r["iterations"]
+        return its
+
+    for _ in range(args.warmup):
+        step()
+    t0 = time.perf_counter()
+    its = sum(step() for _ in range(args.steps))
+    dt = time.perf_counter() - t0
+    val = its / dt
+    line = {"metric": METRIC, "value": val, "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(args, data, args.gpus), "impl": "reference",
+            "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": "port",
+                             "sample": f"full workload ({args.steps} steps x {len(variants)} fits), OpenMP over points"},
+            "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(args, data):
+    """Bounded sample: one full fit of each variant with the oracle (10-30 s of CPU at C2 k=100)."""
+    from oracle import oracle as O
+    X = O.CSR(data.indptr, data.indices, data.data, data.dim)
+    its = 0
+    t0 = time.perf_counter()
+    for v in args.variants.split(","):
+        its += O.run(X, args.k, v, seed=args.seed, max_iter=args.max_iter)["iterations"]
+    dt = time.perf_counter() - t0
+    return {"value": its / dt, "unit": "iterations/s", "cores": O.num_threads(), "kind": "port",
+            "sample": f"one fit of each variant ({its} iterations, {dt:.1f} s), C oracle, OpenMP threads"}
+
+
+# ----------------------------------------------------------------- our arm
+def main_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2107_04074_b200 as spk
+    from paper_2107_04074_b200 import _lib
+    from paper_2107_04074_b200.engine import DeviceCorpus, run
+    from paper_2107_04074_b200.seeding import SeedConfig, make_centroids
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device(f"cuda:{local}")
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    data, gen_s = load_workload(args)
+    variants = args.variants.split(",")
+    k = args.k
+    cents0 = make_centroids(data, k, SeedConfig(seed=args.seed))
+    if world > 1:
+        from paper_2107_04074_b200.distributed import Exchange, shard_rows
+        rows = shard_rows(data.indptr, world)[rank]
+    else:
+        rows = (0, data.n)
+    corpus = DeviceCorpus(data, dev, rows=rows)
+    torch.cuda.synchronize()
+
+    def fit_all(corpus_, tag=None):
+        its, sims, nk = 0, 0, 0
+        per = {}
+        for v in variants:
+            comm = Exchange(k, data.dim, dev) if world > 1 else None
+            r = run(data, k, v, max_iter=args.max_iter, device=dev, corpus=corpus_, init_centers=cents0.centers,
+                    comm=comm, n_total=data.n, seed_indices=cents0.seed_indices)
+            its += len(r.iterations)
+            sims += r.total_sims
+            nk += data.n * k * len(r.iterations)
+            per[v] = {"iterations": len(r.iterations), "objective": r.objective,
+                      "pruned_frac": 1.0 - r.total_sims / (data.n * k * len(r.iterations))}
+            last = r
+        return its, sims, nk, per, last
+
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    if args.profile_only:
+        fit_all(corpus)
+        torch.cuda.synchronize()
+        return
+
+    for _ in range(args.warmup):
+        fit_all(corpus)
+    # ---- device-timed steps (inputs resident) ----
+    times, its_tot, sims_tot, nk_tot = [], 0, 0, 0
+    prof = _lib.CallProfiler(timed=False)
+    with Clocks(local) as clk:
+        barrier()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            with prof:
+                its, sims, nk, per, _ = fit_all(corpus)
+            e1.record()
+            barrier()
+            times.append(e0.elapsed_time(e1))
+            its_tot, sims_tot, nk_tot = its_tot + its, sims_tot + sims, nk_tot + nk
+    step_ms = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
+    total_ms = float(step_ms.item())
+    value = its_tot / (total_ms / 1e3)
+    launches_per_step = prof.launches // max(args.steps, 1)
+
+    # ---- e2e through the public API from host buffers ----
+    # every step: CSR shard H2D (pinned staging), then the user's call
+    # spk.run(...) per variant (seeding on the host, seed centers H2D,
+    # assignments D2H); the device corpus cache is dropped between steps.
+    e2e_times, h2d, d2h = [], 0, 0
+    barrier()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        data._device_cache.clear()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        c = DeviceCorpus(data, dev, rows=rows, pinned_host=True)
+        h2d, d2h = c.h2d_bytes, 0
+        for v in variants:
+            comm = Exchange(k, data.dim, dev) if world > 1 else None
+            r = spk.run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=c,
+                        comm=comm, n_total=data.n)
+            h2d += k * data.dim * 8
+            d2h += r.assignments.nbytes
+        e1.record()
+        barrier()
+        e2e_times.append(e0.elapsed_time(e1))
+        del c
+    e2e_ms = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+    e2e_val = its_tot / (float(e2e_ms.item()) / 1e3)
+
+    # ---- instrumented pass: per-entry-point event times -> roofline ----
+    roof = roofline(args, data, corpus, cents0, dev, world)
+
+    if rank != 0:
+        dist.destroy_process_group()
+        return
+    clocks = clk.summary()
+    line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": workload_config(args, data, world),
+            "effective_sims_per_s": nk_tot / (total_ms / 1e3),
+            "computed_sims_per_s": sims_tot / (total_ms / 1e3),
+            "pruned_frac": 1.0 - sims_tot / nk_tot,
+            "per_variant": per,
+            "e2e": {"value": e2e_val, "unit": "iterations/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h)},
+            "gpu_launches": launches_per_step * args.steps,
+            "roofline": roof,
+            "clocks": clocks}
+    if world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(args, data)
+    print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def roofline(args, data, corpus, cents0, dev, world):
+    """Time every entry point with CUDA events over one step; bytes from SURVEY.md §8(d)."""
+    import torch
+    from paper_2107_04074_b200 import _lib
+    from paper_2107_04074_b200.engine import run
+    from paper_2107_04074_b200.distributed import Exchange
+
+    pk, src = peaks()
+    n, nnz, k = corpus.n, corpus.nnz, args.k
+    prof = _lib.CallProfiler(timed=True)
+    bytes_by = {}
+    with prof:
+        for v in args.variants.split(","):
+            prof.tag = v
+            comm = Exchange(k, data.dim, dev) if world > 1 else None
+            r = run(data, k, v, max_iter=args.max_iter, device=dev, corpus=corpus, init_centers=cents0.centers,
+                    comm=comm, n_total=data.n, seed_indices=cents0.seed_indices)
+            its = r.iterations
+            ku = (k + 3) // 4 * 4
+            csr_full = 8 * nnz + 8 * n + 4 * n          # indices+values, indptr, row eps
+            # full passes: iteration 1 of every variant and every Lloyd iteration
+            n_full = 1 + (len(its) - 1 if v == "standard" else 0)
+            init_w = 8 * n + (4 * k * n if v in ("elkan", "simp_elkan") else 4 * n if "hamerly" in v else 0)
+            lloyd_w = 4 * n
+            b = csr_full * n_full + init_w + lloyd_w * (n_full - 1)
+            bytes_by[("spkm_full_assign", v)] = b
+            if v in ("hamerly", "simp_hamerly"):
+                bytes_by[("spkm_hamerly_bounds", v)] = 24 * n * (len(its) - 1)
+                bytes_by[("spkm_hamerly_tighten", v)] = sum(8 * s.survivors + 12 * s.survivors for s in its[1:]) \
+                    + sum(8 * 0 for _ in its)
+                bytes_by[("spkm_hamerly_rescan", v)] = sum(12 * s.survivors2 for s in its[1:])
+            if v in ("elkan", "simp_elkan"):
+                bytes_by[("spkm_elkan_bounds", v)] = (8 * ku + 16) * n * (len(its) - 1)
+    torch.cuda.synchronize()
+    times = prof.times_ms()
+    calls = {}
+    for (name, tag), ms in times.items():
+        calls.setdefault(name, [0.0, 0])
+        calls[name][0] += ms
+    for name, e0, e1, tag in prof.records:
+        calls[name][1] += 1
+    total = sum(v[0] for v in calls.values())
+    share = {nm: round(v[0] / total, 4) for nm, v in sorted(calls.items(), key=lambda x: -x[1][0])}
+    # dominant kernel among those with a byte model
+    cand = [nm for nm in share if any(key[0] == nm for key in bytes_by)]
+    dom = cand[0] if cand else None
+    out = {"bound": "hbm", "peak": pk.get("hbm_gbs"), "unit": "GB/s", "peak_source": src,
+           "time_share": share, "traffic": None}
+    if dom:
+        ms = calls[dom][0]
+        b = sum(val for key, val in bytes_by.items() if key[0] == dom)
+        ach = b / (ms / 1e3) / 1e9
+        out.update({"kernel": dom, "achieved": ach, "frac": ach / pk.get("hbm_gbs"), "launches": calls[dom][1],
+                    "algorithmic_bytes": b, "kernel_ms": ms})
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        main_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,187 @@
+/*
+ * spkm.h -- C ABI of libspkm.so, the sm_100a kernels behind the accelerated
+ * spherical k-means iteration loop (arXiv 2107.04074).
+ *
+ * Conventions:
+ *   - every buffer is caller-owned DEVICE memory passed as a plain pointer;
+ *     the library allocates nothing persistent;
+ *   - every call is asynchronous on the given cudaStream_t (passed as void*);
+ *   - return value 0 = ok, otherwise an error code; spkm_last_error() gives
+ *     the message of the last failure on the calling thread;
+ *   - no callbacks into the host.
+ *
+ * Reference boundary each entry point replaces (paths relative to
+ * /root/reference/pkg/src/spkmeans/):
+ *   spkm_full_assign        engine._full_sims + argmax/top-2 + bound init,
+ *                           engine.py:99-100, 103-120, 249-263, 268-271
+ *   spkm_hamerly_bounds     Hamerly drift update, engine.py:274, 284-303,
+ *                           geometry.py:30-63 (fused with the prune test)
+ *   spkm_hamerly_tighten    kernels.hamerly_scan tighten + re-test,
+ *                           kernels.py:81-95
+ *   spkm_hamerly_rescan     kernels.hamerly_scan full-k scan, kernels.py:96-112
+ *   spkm_elkan_bounds       Elkan drift update, engine.py:274-283 (fused test)
+ *   spkm_elkan_scan         kernels.elkan_scan, kernels.py:22-66
+ *   spkm_aggregate_sums     engine._aggregate_sums, engine.py:130-139
+ *   spkm_apply_moves        engine.update_centers (incremental), engine.py:174-188
+ *   spkm_move_centers       engine._move_centers, engine.py:142-160
+ *   spkm_center_thresholds  engine._center_thresholds, engine.py:192-198
+ *   spkm_finalize           objective + convergence inputs, engine.py:326-337
+ *   spkm_predict            engine.assign_full, engine.py:103-120
+ */
+#ifndef SPKM_H
+#define SPKM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPKM_ABI_VERSION 1
+
+/* variants, engine.py:22 */
+enum spkm_variant {
+    SPKM_STANDARD = 0,
+    SPKM_ELKAN = 1,
+    SPKM_SIMP_ELKAN = 2,
+    SPKM_HAMERLY = 3,
+    SPKM_SIMP_HAMERLY = 4
+};
+
+/* spkm_full_assign modes */
+enum spkm_assign_mode {
+    SPKM_MODE_INIT_PLAIN = 0,   /* iteration 1, no bounds (standard)          */
+    SPKM_MODE_INIT_ELKAN = 1,   /* iteration 1, l + u(i,j) for every j        */
+    SPKM_MODE_INIT_HAMERLY = 2, /* iteration 1, l + u = second best           */
+    SPKM_MODE_LLOYD = 3         /* iteration >= 2 of standard: reassign+moves */
+};
+
+/* Device CSR of the (local shard of the) corpus; rows unit-normalised. */
+typedef struct spkm_csr {
+    int64_t n;               /* rows in this shard                        */
+    int64_t d;               /* dimensionality                            */
+    int64_t nnz;
+    const int64_t *indptr;   /* [n+1]                                     */
+    const int32_t *indices;  /* [nnz], sorted within a row                */
+    const float *values;     /* [nnz]                                     */
+    const float *row_eps;    /* [n] float32 similarity error bound of row i:
+                                (nnz_i + 6) * 6.1e-8, rounded up           */
+} spkm_csr;
+
+/* Replicated center state.  kp = padded k of the term-major copy. */
+typedef struct spkm_centers {
+    int64_t k, d, kp;
+    int32_t scale_bits;      /* fixed-point sums: value = sum * 2^-scale_bits */
+    int32_t _pad;
+    double *cent64;          /* [k*d] unit centers, center-major, float64   */
+    float *ct32;             /* [d*kp] term-major float32 copy (pad = 0)    */
+    long long *sums;         /* [k*d] exact fixed-point member sums         */
+    long long *counts;       /* [k]                                         */
+    double *drift;           /* [k] p(j) = <c_new, c_old>                   */
+    int32_t *touched;        /* [k] cluster changed this iteration          */
+    double *objc;            /* [k] <sums_j, c_j> per cluster               */
+    double *part;            /* [k*nchunk*2] scratch partial reductions     */
+    double *norm;            /* [k] scratch: |sums_j|                       */
+    float *cc;               /* [k*k] half-angle center cosines, rounded up */
+    float *s;                /* [k]   row max of cc (diag excluded)         */
+    double *hstat;           /* [4]   owner, p_min, p_min2 (Hamerly)        */
+} spkm_centers;
+
+/* Per-point bounds of the local shard. */
+typedef struct spkm_bounds {
+    int32_t *a;              /* [n] assignment                               */
+    float *l;                /* [n] lower bound on <x_i, c_a(i)> (round down) */
+    float *u;                /* [n*ku] Elkan u(i,j) or [n] Hamerly u(i)      */
+    int64_t ku;              /* row stride of u (Elkan) or 1 (Hamerly)       */
+} spkm_bounds;
+
+/* Worklists and device-side counters. */
+typedef struct spkm_work {
+    int32_t *surv1;          /* [n] points failing the bound test            */
+    int32_t *surv2;          /* [n] points failing after tightening          */
+    int32_t *mv_i;           /* [n] moved point ids                          */
+    int32_t *mv_old;         /* [n] their previous cluster                   */
+    long long *ctr;          /* [8] counters, see SPKM_CTR_*                 */
+    double *stats;           /* [16] per-iteration stats, see SPKM_ST_*      */
+} spkm_work;
+
+enum {
+    SPKM_CTR_SURV1 = 0, SPKM_CTR_SURV2 = 1, SPKM_CTR_MOVES = 2, SPKM_CTR_SIMS = 3,
+    SPKM_CTR_NNZ_TIGHTEN = 4, SPKM_CTR_NNZ_RESCAN = 5, SPKM_CTR_NNZ_ELKAN = 6
+};
+enum {
+    SPKM_ST_SIMS = 0, SPKM_ST_REASSIGN = 1, SPKM_ST_OBJECTIVE = 2, SPKM_ST_ALLONE = 3,
+    SPKM_ST_SURV1 = 4, SPKM_ST_SURV2 = 5, SPKM_ST_TOUCHED = 6, SPKM_ST_NNZ_TIGHTEN = 7,
+    SPKM_ST_NNZ_RESCAN = 8, SPKM_ST_NNZ_ELKAN = 9, SPKM_ST_COUNT = 16
+};
+
+int spkm_abi_version(void);
+const char *spkm_last_error(void);
+/* number of chunks the center kernels split d into (size of centers.part) */
+int64_t spkm_center_chunks(int64_t d);
+/* padded k (kp) of the term-major copy for a given k */
+int64_t spkm_padded_k(int64_t k);
+
+/* Zero counters (ctr) before an iteration. */
+int spkm_reset_counters(spkm_work *w, void *stream);
+
+/* Full pass over rows [row_begin,row_end): every <x_i, c_j> in the canonical
+ * order (fp32 FMA chain over the row's nnz in CSR order), fused top-2.
+ * INIT modes write a, l (and u); LLOYD reassigns with "incumbent wins exact
+ * ties, otherwise lowest index" and appends moves. */
+int spkm_full_assign(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
+                     int mode, void *stream);
+
+int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
+                        int use_s, int naive, void *stream);
+int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
+                         int use_s, void *stream);
+int spkm_hamerly_rescan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
+                        void *stream);
+int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
+                      int use_cc, void *stream);
+int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
+                    int use_cc, void *stream);
+
+/* Center maintenance.  aggregate: sums/counts from scratch (target arrays may
+ * be a delta buffer); apply_moves: sums[old] -= x, sums[new] += x for the
+ * recorded moves into `sums_target`/`counts_target`, marks touched. */
+int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
+                        long long *sums_target, long long *counts_target, void *stream);
+int spkm_apply_moves(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
+                     const spkm_work *W, long long *sums_target, long long *counts_target,
+                     int32_t *touched, void *stream);
+/* Renormalise touched clusters (all if all_clusters), write cent64/ct32,
+ * drift and per-cluster objective. */
+int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream);
+/* cc(a,j) = sqrt((<c_a,c_j>+1)/2) rounded up, s(a) = max_{j!=a} cc(a,j).
+ * float64 split-d Gram over the upper-triangle 32x32 tiles listed in
+ * tile_pairs (from spkm_gram_tiles); gram_scratch holds
+ * spkm_gram_scratch_doubles(k, d) doubles. */
+int64_t spkm_gram_tiles(int64_t k, int32_t *host_pairs);
+int64_t spkm_gram_scratch_doubles(int64_t k, int64_t d);
+int spkm_center_thresholds(const spkm_centers *C, double *gram_scratch, const void *tile_pairs,
+                              void *stream);
+/* Objective, all-p==1 flag, Hamerly owner/p_min/p_min2, stats; clears
+ * touched.  sims_extra is added to the sims counter (host-known counts). */
+int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra,
+                  void *stream);
+
+/* predict (assign_full): a (lowest index on ties), best, second (float64). */
+int spkm_predict(const spkm_csr *X, const spkm_centers *C, int32_t *a, double *best,
+                 double *second, void *stream);
+
+/* compute_objective (engine.py:123-127): Sum_j <sums_j * 2^-scale, c_j>, with
+ * sums built by spkm_aggregate_sums for the given assignments. */
+int spkm_objective(const spkm_centers *C, const long long *sums, double *out, void *stream);
+
+/* Upload helper: write center-major float64 centers into cent64 and ct32. */
+int spkm_load_centers(const spkm_centers *C, const double *host_or_dev_centers, void *stream);
+
+/* Device geometry for tests: op 0 lower, 1 upper, 2 hamerly, 3 half-angle. */
+int spkm_geometry(int op, int64_t n, const double *a, const double *b, double *out, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

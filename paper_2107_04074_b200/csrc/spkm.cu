@@ -1,0 +1,1194 @@
+// spkm.cu -- sm_100a kernels for the accelerated spherical k-means loop.
+//
+// Reference path (arXiv 2107.04074 package `spkmeans`, engine.py:201-346):
+// one iteration = center thresholds -> drift update of the bounds ->
+// pruned scan -> incremental center update -> renormalise -> objective.
+// This file implements each phase as data-parallel CUDA over the points,
+// behind the C ABI of include/spkm.h.
+//
+// Numerics:
+//  * Similarities are float32: s~(i,j) = FMA chain over row i's nnz in CSR
+//    order, starting at 0 (the canonical order).  Every kernel that computes
+//    a similarity uses exactly this chain, so the full pass, the Hamerly
+//    rescan, the tighten step and the Elkan pair scan agree bit-for-bit and
+//    the pruned variants reproduce Lloyd exactly.
+//  * Bounds are kept on the TRUE cosine <x_i, c_j> (float64 rows/centers),
+//    updated in float64 and stored as float32 rounded outward.  The float32
+//    similarity error is |s~ - s| <= eps_i = (m_i + 6) * 6.1e-8 (m_i = row
+//    nnz; FMA-chain error bound gamma_m plus the float32 rounding of x and c).
+//    A center j is pruned only if s~(i,j) <= s~(i,a) is PROVEN, i.e.
+//    u + 2 eps <= l (stored bounds) or u + eps <= s~(i,a) (after tightening).
+//  * Ties: "the incumbent wins exact ties, otherwise the lowest index" in
+//    every variant from iteration 2; iteration 1 and
+//    predict use the lowest index (numpy argmax).
+//  * Center sums are exact fixed point (int64, value * 2^scale_bits), so
+//    incremental == scratch and sums are independent of atomic order and of
+//    the GPU count.  Renormalisation, drift and objective are float64 with
+//    fixed-order reductions.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <math.h>
+
+#include "../../include/spkm.h"
+
+#define FULL 0xffffffffu
+
+namespace {
+
+// eps_i = (nnz_i + 6) * 6.1e-8 (>= 2^-24 * 1.02 per term) is computed on the
+// host into spkm_csr.row_eps (rounded up) and read by every prune test.
+constexpr double kSlack = 1e-12;            // float64 formula error of a bound update
+constexpr double kCcSlack = 1e-9;           // float64 Gram error (d * 2^-53 << 1e-9 for d <= 1e6)
+constexpr double kSqrt2 = 1.4142135623730951;
+constexpr double kZeroSumEps = 1e-12;       // engine.py:27
+constexpr int kCenterChunk = 4096;          // d-chunk of the center kernels
+
+thread_local char g_err[512] = {0};
+
+int fail(const char *what, cudaError_t e) {
+    snprintf(g_err, sizeof g_err, "%s: %s", what, cudaGetErrorString(e));
+    return (int)e ? (int)e : 1;
+}
+int fail_msg(const char *msg) {
+    snprintf(g_err, sizeof g_err, "%s", msg);
+    return -1;
+}
+#define CHECK_LAUNCH(name)                                          \
+    do {                                                            \
+        cudaError_t _e = cudaGetLastError();                        \
+        if (_e != cudaSuccess) return fail(name, _e);               \
+    } while (0)
+
+inline cudaStream_t S(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int g_num_sms = 0;
+int num_sms() {
+    if (!g_num_sms) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+        if (g_num_sms <= 0) g_num_sms = 148;
+    }
+    return g_num_sms;
+}
+
+// ------------------------------------------------------------------ geometry
+// geometry.py:20-68, evaluated with explicit round-to-nearest ops (no FMA
+// contraction) so the device values equal the reference's numpy values.
+__device__ __forceinline__ double d_clamp(double t) { return t < -1.0 ? -1.0 : (t > 1.0 ? 1.0 : t); }
+__device__ __forceinline__ double d_sin(double t) {
+    double v = __dsub_rn(1.0, __dmul_rn(t, t));
+    return sqrt(v > 0.0 ? v : 0.0);
+}
+__device__ __forceinline__ double d_cos_lower(double a, double b) {
+    return d_clamp(__dsub_rn(__dmul_rn(a, b), __dmul_rn(d_sin(a), d_sin(b))));
+}
+__device__ __forceinline__ double d_cos_upper(double a, double b) {
+    return d_clamp(__dadd_rn(__dmul_rn(a, b), __dmul_rn(d_sin(a), d_sin(b))));
+}
+__device__ __forceinline__ double d_hamerly_upper(double u, double p) {
+    return d_clamp(__dadd_rn(u, __dmul_rn(d_sin(u), d_sin(p))));
+}
+__device__ __forceinline__ double d_half_angle(double s) {
+    double v = __ddiv_rn(__dadd_rn(s, 1.0), 2.0);
+    return sqrt(v > 0.0 ? v : 0.0);
+}
+// Lower-bound drift update with the theta_l + theta_p > pi guard
+// (SURVEY.md §2.4 item 6): the triangle formula is only valid while
+// l >= -p; past that the new cosine can be -1.
+__device__ __forceinline__ double d_lower_update(double l, double p) {
+    return (l < -p) ? -1.0 : d_cos_lower(l, p);
+}
+__device__ __forceinline__ float store_lower(double v) {
+    v -= kSlack;
+    if (v < -1.0) v = -1.0;
+    return __double2float_rd(v);
+}
+__device__ __forceinline__ float store_upper(double v) {
+    v += kSlack;
+    if (v > 1.0) v = 1.0;
+    return __double2float_ru(v);
+}
+
+// ------------------------------------------------------- canonical similarity
+// s~(i,j) for one pair: the same FMA chain the row kernels run per column.
+__device__ __forceinline__ float dot_pair(const int32_t *__restrict__ idx, const float *__restrict__ val,
+                                          int64_t s, int64_t e, const float *__restrict__ ct, int64_t kp,
+                                          int j) {
+    float acc = 0.f;
+    int64_t t = s;
+    for (; t + 4 <= e; t += 4) {
+        const int i0 = __ldg(idx + t), i1 = __ldg(idx + t + 1), i2 = __ldg(idx + t + 2), i3 = __ldg(idx + t + 3);
+        const float v0 = __ldg(val + t), v1 = __ldg(val + t + 1), v2 = __ldg(val + t + 2), v3 = __ldg(val + t + 3);
+        const float c0 = __ldg(ct + (int64_t)i0 * kp + j), c1 = __ldg(ct + (int64_t)i1 * kp + j);
+        const float c2 = __ldg(ct + (int64_t)i2 * kp + j), c3 = __ldg(ct + (int64_t)i3 * kp + j);
+        acc = __fmaf_rn(v0, c0, acc);
+        acc = __fmaf_rn(v1, c1, acc);
+        acc = __fmaf_rn(v2, c2, acc);
+        acc = __fmaf_rn(v3, c3, acc);
+    }
+    for (; t < e; ++t) acc = __fmaf_rn(__ldg(val + t), __ldg(ct + (int64_t)__ldg(idx + t) * kp + j), acc);
+    return acc;
+}
+
+// ------------------------------------------------------------- top-2 helpers
+// Priority: larger value; on exact ties the incumbent `inc`, then lower index.
+__device__ __forceinline__ bool better(float v1, int j1, float v2, int j2, int inc) {
+    if (v1 != v2) return v1 > v2;
+    const int p1 = (j1 == inc) ? -1 : j1;
+    const int p2 = (j2 == inc) ? -1 : j2;
+    return p1 < p2;
+}
+struct Top2 {
+    float b;
+    int bj;
+    float s;
+};
+__device__ __forceinline__ void top2_push(Top2 &t, float v, int j, int inc) {
+    if (better(v, j, t.b, t.bj, inc)) {
+        t.s = fmaxf(t.s, t.b);
+        t.b = v;
+        t.bj = j;
+    } else {
+        t.s = fmaxf(t.s, v);
+    }
+}
+__device__ __forceinline__ void top2_merge(Top2 &t, const Top2 &o, int inc) {
+    if (better(o.b, o.bj, t.b, t.bj, inc)) {
+        t.s = fmaxf(o.s, t.b);
+        t.b = o.b;
+        t.bj = o.bj;
+    } else {
+        t.s = fmaxf(t.s, o.b);
+    }
+}
+__device__ __forceinline__ Top2 top2_shfl_down(const Top2 &t, int o) {
+    Top2 r;
+    r.b = __shfl_down_sync(FULL, t.b, o);
+    r.bj = __shfl_down_sync(FULL, t.bj, o);
+    r.s = __shfl_down_sync(FULL, t.s, o);
+    return r;
+}
+
+// Warp-aggregated append of (pred ? value : nothing) to list[ctr++].
+__device__ __forceinline__ void warp_append(bool pred, int32_t v0, int32_t *list0, int32_t v1, int32_t *list1,
+                                            long long *ctr) {
+    const unsigned m = __ballot_sync(FULL, pred);
+    if (!m) return;
+    const int lane = threadIdx.x & 31;
+    long long base = 0;
+    if (lane == __ffs(m) - 1) base = atomicAdd((unsigned long long *)ctr, (unsigned long long)__popc(m));
+    base = __shfl_sync(FULL, base, __ffs(m) - 1);
+    if (pred) {
+        const int r = __popc(m & ((1u << lane) - 1u));
+        list0[base + r] = v0;
+        if (list1) list1[base + r] = v1;
+    }
+}
+
+__device__ __forceinline__ void warp_add(long long *ctr, long long v) {
+    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(FULL, v, o);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long *)ctr, (unsigned long long)v);
+}
+
+// ------------------------------------------------------------ full row pass
+enum { MODE_RESCAN = 4, MODE_PREDICT = 5 };
+
+struct RowPassArgs {
+    const int64_t *indptr;
+    const int32_t *indices;
+    const float *values;
+    const float *reps;
+    int64_t n;
+    const float *ct;
+    int64_t kp;
+    int k, tpr, rpw, mode;
+    const int32_t *rowlist;      // null = rows [0, n)
+    const long long *rowcount;   // device count of rowlist
+    int32_t *a;
+    float *l;
+    float *u;
+    int64_t ku;
+    int32_t *mv_i, *mv_old;
+    long long *ctr;
+    double *best, *second;       // predict outputs
+};
+
+// Thread = (row, CH consecutive centers).  tpr threads cover one row's kp
+// columns, rpw rows share a warp.  Per nnz: one broadcast (idx, val) load and
+// CH/4 float4 loads of the term-major center row; CH independent FMA chains.
+template <int CH>
+__global__ void __launch_bounds__(256) k_row_pass(RowPassArgs A) {
+    const int lane = threadIdx.x & 31;
+    const int g = lane / A.tpr, q = lane - g * A.tpr;
+    const bool lane_on = g < A.rpw;
+    const int64_t nrows = A.rowlist ? *A.rowcount : A.n;
+    const int64_t nslots = (nrows + A.rpw - 1) / A.rpw;
+    const int wpb = blockDim.x >> 5;
+    const int o0 = A.tpr > 1 ? (1 << (31 - __clz(A.tpr - 1))) : 0;
+    for (int64_t w = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); w < nslots; w += (int64_t)gridDim.x * wpb) {
+        const int64_t slot = w * A.rpw + g;
+        const bool valid = lane_on && slot < nrows;
+        const int64_t row = valid ? (A.rowlist ? (int64_t)A.rowlist[slot] : slot) : 0;
+        const int64_t s = valid ? A.indptr[row] : 0;
+        const int64_t e = valid ? A.indptr[row + 1] : 0;
+        const int j0 = q * CH;
+        float acc[CH];
+#pragma unroll
+        for (int c = 0; c < CH; ++c) acc[c] = 0.f;
+        const float *ctj = A.ct + j0;
+        int64_t t = s;
+        for (; t + 2 <= e; t += 2) {
+            const int i0 = __ldg(A.indices + t), i1 = __ldg(A.indices + t + 1);
+            const float v0 = __ldg(A.values + t), v1 = __ldg(A.values + t + 1);
+            const float4 *p0 = reinterpret_cast<const float4 *>(ctj + (int64_t)i0 * A.kp);
+            const float4 *p1 = reinterpret_cast<const float4 *>(ctj + (int64_t)i1 * A.kp);
+            float4 c0[CH / 4], c1[CH / 4];
+#pragma unroll
+            for (int r = 0; r < CH / 4; ++r) c0[r] = __ldg(p0 + r);
+#pragma unroll
+            for (int r = 0; r < CH / 4; ++r) c1[r] = __ldg(p1 + r);
+#pragma unroll
+            for (int r = 0; r < CH / 4; ++r) {
+                acc[4 * r + 0] = __fmaf_rn(v0, c0[r].x, acc[4 * r + 0]);
+                acc[4 * r + 1] = __fmaf_rn(v0, c0[r].y, acc[4 * r + 1]);
+                acc[4 * r + 2] = __fmaf_rn(v0, c0[r].z, acc[4 * r + 2]);
+                acc[4 * r + 3] = __fmaf_rn(v0, c0[r].w, acc[4 * r + 3]);
+            }
+#pragma unroll
+            for (int r = 0; r < CH / 4; ++r) {
+                acc[4 * r + 0] = __fmaf_rn(v1, c1[r].x, acc[4 * r + 0]);
+                acc[4 * r + 1] = __fmaf_rn(v1, c1[r].y, acc[4 * r + 1]);
+                acc[4 * r + 2] = __fmaf_rn(v1, c1[r].z, acc[4 * r + 2]);
+                acc[4 * r + 3] = __fmaf_rn(v1, c1[r].w, acc[4 * r + 3]);
+            }
+        }
+        if (t < e) {
+            const int i0 = __ldg(A.indices + t);
+            const float v0 = __ldg(A.values + t);
+            const float4 *p0 = reinterpret_cast<const float4 *>(ctj + (int64_t)i0 * A.kp);
+#pragma unroll
+            for (int r = 0; r < CH / 4; ++r) {
+                const float4 c = __ldg(p0 + r);
+                acc[4 * r + 0] = __fmaf_rn(v0, c.x, acc[4 * r + 0]);
+                acc[4 * r + 1] = __fmaf_rn(v0, c.y, acc[4 * r + 1]);
+                acc[4 * r + 2] = __fmaf_rn(v0, c.z, acc[4 * r + 2]);
+                acc[4 * r + 3] = __fmaf_rn(v0, c.w, acc[4 * r + 3]);
+            }
+        }
+        const bool incumbent_mode = (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN);
+        const int inc = (valid && incumbent_mode) ? A.a[row] : -1;
+        Top2 tp{-INFINITY, -2, -INFINITY};
+#pragma unroll
+        for (int c = 0; c < CH; ++c)
+            if (j0 + c < A.k) top2_push(tp, acc[c], j0 + c, inc);
+        for (int o = o0; o; o >>= 1) {
+            const Top2 other = top2_shfl_down(tp, o);
+            if (q < o && q + o < A.tpr) top2_merge(tp, other, inc);
+        }
+        const double eps = valid ? (double)A.reps[row] : 0.0;
+        if (A.mode == SPKM_MODE_INIT_ELKAN && valid) {
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+                if (j0 + c < A.k) A.u[row * A.ku + j0 + c] = store_upper((double)acc[c] + eps);
+        }
+        const bool leader = valid && q == 0;
+        bool moved = false;
+        if (leader) {
+            switch (A.mode) {
+                case SPKM_MODE_INIT_PLAIN:
+                case SPKM_MODE_INIT_ELKAN:
+                case SPKM_MODE_INIT_HAMERLY:
+                    A.a[row] = tp.bj;
+                    A.l[row] = store_lower((double)tp.b - eps);
+                    if (A.mode == SPKM_MODE_INIT_HAMERLY)
+                        A.u[row] = (A.k == 1) ? -1.f : store_upper((double)tp.s + eps);
+                    break;
+                case SPKM_MODE_LLOYD:
+                    if (tp.bj != inc) {
+                        A.a[row] = tp.bj;
+                        moved = true;
+                    }
+                    break;
+                case MODE_RESCAN:
+                    if (tp.bj != inc) {
+                        A.a[row] = tp.bj;
+                        moved = true;
+                    }
+                    A.l[row] = store_lower((double)tp.b - eps);
+                    A.u[row] = store_upper((double)tp.s + eps);
+                    break;
+                case MODE_PREDICT:
+                    A.a[row] = tp.bj;
+                    A.best[row] = (double)tp.b;
+                    A.second[row] = (A.k == 1) ? -1.0 : (double)tp.s;
+                    break;
+            }
+        }
+        if (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN) {
+            warp_append(moved, (int32_t)row, A.mv_i, inc, A.mv_old, A.ctr + SPKM_CTR_MOVES);
+            if (A.mode == MODE_RESCAN) {
+                warp_add(A.ctr + SPKM_CTR_SIMS, leader ? (long long)(A.k - 1) : 0);
+                warp_add(A.ctr + SPKM_CTR_NNZ_RESCAN, leader ? (long long)(e - s) : 0);
+            }
+        }
+    }
+}
+
+// --------------------------------------------------------- Hamerly family
+// engine.py:274 (l), 284-303 (u) fused with the kernels.py:81-87 tests.
+__global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *__restrict__ reps,
+                                                        const int32_t *__restrict__ a, float *l, float *u,
+                                                        const double *__restrict__ drift,
+                                                        const float *__restrict__ s_arr,
+                                                        const double *__restrict__ hstat, int use_s, int naive,
+                                                        int32_t *surv1, long long *ctr) {
+    const int owner = (int)hstat[0];
+    const double pmin = hstat[1], pmin2 = hstat[2];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t n_pad = (n + 31) & ~int64_t(31);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
+        bool surv = false;
+        if (i < n) {
+            const int ai = a[i];
+            const float lo = l[i];
+            const double pa = drift[ai];
+            float lf = lo;
+            if (pa != 1.0) {
+                lf = store_lower(d_lower_update((double)lo, pa));
+                l[i] = lf;
+            }
+            const double worst = (ai == owner) ? pmin2 : pmin;
+            const float uo = u[i];
+            float uf = uo;
+            if (naive) {
+                if (worst != 1.0) {
+                    uf = store_upper(d_cos_upper((double)uo, worst));
+                    u[i] = uf;
+                }
+            } else if (!(uo >= 0.f && worst == 1.0)) {
+                const double un = (uo >= 0.f && worst >= 0.0) ? d_hamerly_upper((double)uo, worst) : 1.0;
+                uf = store_upper(un);
+                u[i] = uf;
+            }
+            const double eps = (double)reps[i];
+            const double lb = (double)lf;
+            bool pruned = (use_s && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb);
+            if (!pruned) pruned = ((double)uf + 2.0 * eps <= lb);
+            surv = !pruned;
+        }
+        warp_append(surv, (int32_t)i, surv1, 0, nullptr, ctr + SPKM_CTR_SURV1);
+    }
+}
+
+// kernels.py:88-95: tighten l with the exact s~(i,a), re-test.
+__global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restrict__ indptr,
+                                                         const int32_t *__restrict__ indices,
+                                                         const float *__restrict__ values,
+                                                         const float *__restrict__ reps,
+                                                         const float *__restrict__ ct, int64_t kp,
+                                                         const int32_t *__restrict__ a, float *l,
+                                                         const float *__restrict__ u,
+                                                         const float *__restrict__ s_arr, int use_s,
+                                                         const int32_t *__restrict__ surv1, int32_t *surv2,
+                                                         long long *ctr) {
+    const long long cnt = ctr[SPKM_CTR_SURV1];
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t cnt_pad = (cnt + 31) & ~(long long)31;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt_pad; t += stride) {
+        bool surv = false;
+        int32_t i = 0;
+        if (t < cnt) {
+            i = surv1[t];
+            const int ai = a[i];
+            const float sa = dot_pair(indices, values, indptr[i], indptr[i + 1], ct, kp, ai);
+            const double eps = (double)reps[i];
+            const double lb = (double)sa - eps;
+            l[i] = store_lower(lb);
+            bool pruned = (use_s && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb);
+            if (!pruned) pruned = ((double)u[i] + eps <= (double)sa);
+            surv = !pruned;
+        }
+        warp_append(surv, i, surv2, 0, nullptr, ctr + SPKM_CTR_SURV2);
+        warp_add(ctr + SPKM_CTR_SIMS, t < cnt ? 1 : 0);
+        warp_add(ctr + SPKM_CTR_NNZ_TIGHTEN, t < cnt ? (long long)(indptr[i + 1] - indptr[i]) : 0);
+    }
+}
+
+// ----------------------------------------------------------- Elkan family
+// engine.py:274-283 (l and u(i,j) drift updates) fused with the
+// kernels.py:35-47 tests; a point survives if any j != a(i) is not pruned.
+// Warp per point, lanes over j (u rows are contiguous).
+__global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const float *__restrict__ reps,
+                                                      const int32_t *__restrict__ a, float *l, float *u,
+                                                      int64_t ku, const double *__restrict__ drift,
+                                                      const float *__restrict__ cc,
+                                                      const float *__restrict__ s_arr, int use_cc,
+                                                      int32_t *surv1, long long *ctr) {
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
+        const int ai = a[i];
+        const float lo = l[i];
+        const double pa = drift[ai];
+        float lf = lo;
+        if (pa != 1.0) lf = store_lower(d_lower_update((double)lo, pa));
+        if (lane == 0 && lf != lo) l[i] = lf;
+        const double eps = (double)reps[i];
+        const double lb = (double)lf;
+        const bool pskip = use_cc && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb;
+        bool any = false;
+        float *ui = u + i * ku;
+        for (int j = lane; j < k; j += 32) {
+            float uf = ui[j];
+            const double pj = drift[j];
+            if (pj != 1.0) {
+                const double nv = ((double)uf <= pj) ? d_cos_upper((double)uf, pj) : 1.0;
+                uf = store_upper(nv);
+                ui[j] = uf;
+            }
+            if (!pskip && j != ai) {
+                bool skip = use_cc && lb >= 0.0 && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb;
+                if (!skip) skip = ((double)uf + 2.0 * eps <= lb);
+                any |= !skip;
+            }
+        }
+        any = __any_sync(FULL, any);
+        if (lane == 0 && any) {
+            const long long p = atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1), 1ull);
+            surv1[p] = (int32_t)i;
+        }
+    }
+}
+
+// kernels.py:48-65 for the surviving points: tighten once, re-test every
+// j against s~(i,a) (and strictly against a better non-incumbent found so
+// far), compute the survivors 32 at a time, keep the best with the tie rule.
+__global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ indptr,
+                                                    const int32_t *__restrict__ indices,
+                                                    const float *__restrict__ values,
+                                                    const float *__restrict__ reps,
+                                                    const float *__restrict__ ct, int64_t kp, int k,
+                                                    int32_t *a, float *l, float *u, int64_t ku,
+                                                    const float *__restrict__ cc, int use_cc,
+                                                    const int32_t *__restrict__ surv1, int32_t *mv_i,
+                                                    int32_t *mv_old, long long *ctr) {
+    __shared__ int32_t buf_all[8][64];
+    const int lane = threadIdx.x & 31;
+    const int wib = threadIdx.x >> 5;
+    int32_t *buf = buf_all[wib];
+    const int wpb = blockDim.x >> 5;
+    const long long cnt = ctr[SPKM_CTR_SURV1];
+    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < cnt; w += (int64_t)gridDim.x * wpb) {
+        const int32_t i = surv1[w];
+        const int ai = a[i];
+        const int64_t s = indptr[i], e = indptr[i + 1];
+        const double eps = (double)reps[i];
+        float sa = 0.f;
+        if (lane == 0) sa = dot_pair(indices, values, s, e, ct, kp, ai);
+        sa = __shfl_sync(FULL, sa, 0);
+        float *ui = u + (int64_t)i * ku;
+        if (lane == 0) ui[ai] = store_upper((double)sa + eps);
+        const double lb = (double)sa - eps;
+        Top2 best{sa, ai, -INFINITY};
+        long long sims = 1;
+        int pos = 0;
+        auto process = [&](int m) {
+            float v = -INFINITY;
+            int j = -2;
+            if (lane < m) {
+                j = buf[lane];
+                v = dot_pair(indices, values, s, e, ct, kp, j);
+                ui[j] = store_upper((double)v + eps);
+            }
+            Top2 tp{v, j, -INFINITY};
+            for (int o = 16; o; o >>= 1) {
+                const Top2 other = top2_shfl_down(tp, o);
+                if (lane < o) top2_merge(tp, other, ai);
+            }
+            tp.b = __shfl_sync(FULL, tp.b, 0);
+            tp.bj = __shfl_sync(FULL, tp.bj, 0);
+            if (better(tp.b, tp.bj, best.b, best.bj, ai)) {
+                best.b = tp.b;
+                best.bj = tp.bj;
+            }
+            sims += m;
+        };
+        for (int base = 0; base < k; base += 32) {
+            const int j = base + lane;
+            bool cand = false;
+            if (j < k && j != ai) {
+                const double uij = (double)ui[j];
+                bool prune = use_cc && lb >= 0.0 && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb;
+                if (!prune) prune = (uij + eps <= (double)sa);
+                if (!prune && best.bj != ai) prune = (uij + eps < (double)best.b);
+                cand = !prune;
+            }
+            const unsigned m = __ballot_sync(FULL, cand);
+            if (cand) buf[pos + __popc(m & ((1u << lane) - 1u))] = j;
+            pos += __popc(m);
+            __syncwarp();
+            if (pos >= 32) {
+                process(32);
+                __syncwarp();
+                if (lane < pos - 32) buf[lane] = buf[lane + 32];
+                __syncwarp();
+                pos -= 32;
+            }
+        }
+        if (pos > 0) process(pos);
+        __syncwarp();
+        if (lane == 0) {
+            l[i] = store_lower((double)best.b - eps);
+            if (best.bj != ai) a[i] = best.bj;
+        }
+        warp_append(lane == 0 && best.bj != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
+        if (lane == 0) {
+            atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SIMS), (unsigned long long)sims);
+            atomicAdd((unsigned long long *)(ctr + SPKM_CTR_NNZ_ELKAN), (unsigned long long)(e - s));
+        }
+    }
+}
+
+// --------------------------------------------------------- center updates
+__device__ __forceinline__ long long to_fixed(float v, double scale) { return __double2ll_rn((double)v * scale); }
+
+// engine._aggregate_sums (engine.py:130-139): warp per row, lanes over nnz.
+__global__ void __launch_bounds__(256) k_aggregate(int64_t n, int64_t d, const int64_t *__restrict__ indptr,
+                                                   const int32_t *__restrict__ indices,
+                                                   const float *__restrict__ values,
+                                                   const int32_t *__restrict__ a, long long *sums,
+                                                   long long *counts, double scale) {
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
+        const int ai = a[i];
+        long long *sj = sums + (int64_t)ai * d;
+        for (int64_t t = indptr[i] + lane; t < indptr[i + 1]; t += 32)
+            atomicAdd((unsigned long long *)(sj + __ldg(indices + t)), (unsigned long long)to_fixed(__ldg(values + t), scale));
+        if (lane == 0) atomicAdd((unsigned long long *)(counts + ai), 1ull);
+    }
+}
+
+// engine.update_centers incremental branch (engine.py:174-188).
+__global__ void __launch_bounds__(256) k_apply_moves(int64_t d, const int64_t *__restrict__ indptr,
+                                                     const int32_t *__restrict__ indices,
+                                                     const float *__restrict__ values,
+                                                     const int32_t *__restrict__ a,
+                                                     const int32_t *__restrict__ mv_i,
+                                                     const int32_t *__restrict__ mv_old,
+                                                     const long long *__restrict__ ctr, long long *sums,
+                                                     long long *counts, int32_t *touched, double scale) {
+    const int lane = threadIdx.x & 31;
+    const int wpb = blockDim.x >> 5;
+    const long long cnt = ctr[SPKM_CTR_MOVES];
+    for (int64_t w = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); w < cnt; w += (int64_t)gridDim.x * wpb) {
+        const int32_t i = mv_i[w];
+        const int o = mv_old[w], nw = a[i];
+        long long *so = sums + (int64_t)o * d;
+        long long *sn = sums + (int64_t)nw * d;
+        for (int64_t t = indptr[i] + lane; t < indptr[i + 1]; t += 32) {
+            const int c = __ldg(indices + t);
+            const long long q = to_fixed(__ldg(values + t), scale);
+            atomicAdd((unsigned long long *)(so + c), (unsigned long long)(-q));
+            atomicAdd((unsigned long long *)(sn + c), (unsigned long long)q);
+        }
+        if (lane == 0) {
+            atomicAdd((unsigned long long *)(counts + o), (unsigned long long)(-1ll));
+            atomicAdd((unsigned long long *)(counts + nw), 1ull);
+            touched[o] = 1;
+            touched[nw] = 1;
+        }
+    }
+}
+
+// Fixed-shape block sum (deterministic for a given blockDim).
+template <int NT>
+__device__ __forceinline__ double block_sum(double v, double *sh) {
+    for (int o = 16; o; o >>= 1) v += __shfl_down_sync(FULL, v, o);
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) sh[w] = v;
+    __syncthreads();
+    double r = 0.0;
+    if (threadIdx.x < 32) {
+        r = (threadIdx.x < NT / 32) ? sh[threadIdx.x] : 0.0;
+        for (int o = 16; o; o >>= 1) r += __shfl_down_sync(FULL, r, o);
+    }
+    return r;  // valid in thread 0
+}
+
+// _move_centers pass 1 (engine.py:153-155): partial |sum_j|^2 per d-chunk.
+__global__ void __launch_bounds__(256) k_center_norm_part(int64_t d, int64_t nchunk,
+                                                          const long long *__restrict__ sums,
+                                                          const int32_t *__restrict__ touched, int all,
+                                                          double inv_scale, double *part) {
+    __shared__ double sh[8];
+    const int64_t j = blockIdx.y, c = blockIdx.x;
+    if (!all && !touched[j]) return;
+    const int64_t t0 = c * kCenterChunk, t1 = min(d, t0 + kCenterChunk);
+    const long long *sj = sums + j * d;
+    double acc = 0.0;
+    for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+        const double v = (double)sj[t] * inv_scale;
+        acc = fma(v, v, acc);
+    }
+    const double r = block_sum<256>(acc, sh);
+    if (threadIdx.x == 0) part[(j * nchunk + c) * 2] = r;
+}
+
+// norm_j = sqrt(sum of partials in chunk order); -1 marks "keep the center"
+// (empty cluster or |sum| < 1e-12, engine.py:153-157).
+__global__ void k_center_norm_final(int64_t k, int64_t nchunk, const long long *__restrict__ counts,
+                                    const int32_t *__restrict__ touched, int all, const double *part,
+                                    double *norm) {
+    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (j >= k) return;
+    if (!all && !touched[j]) return;
+    double sq = 0.0;
+    for (int64_t c = 0; c < nchunk; ++c) sq += part[(j * nchunk + c) * 2];
+    const double nrm = sqrt(sq);
+    norm[j] = (counts[j] == 0 || nrm < kZeroSumEps) ? -1.0 : nrm;
+}
+
+// _move_centers pass 2 (engine.py:158-160): c = sum/|sum|, partial <c,old>
+// and partial objective <sum, c>; writes cent64 and the ct32 column.
+__global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int64_t nchunk,
+                                                      const long long *__restrict__ sums,
+                                                      const int32_t *__restrict__ touched, int all,
+                                                      double inv_scale, const double *__restrict__ norm,
+                                                      double *cent64, float *ct32, double *part) {
+    __shared__ double sh[8];
+    const int64_t j = blockIdx.y, c = blockIdx.x;
+    if (!all && !touched[j]) return;
+    const int64_t t0 = c * kCenterChunk, t1 = min(d, t0 + kCenterChunk);
+    const long long *sj = sums + j * d;
+    double *cj = cent64 + j * d;
+    const double nrm = norm[j];
+    double dt = 0.0, ob = 0.0;
+    if (nrm < 0.0) {
+        for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) ob = fma((double)sj[t] * inv_scale, cj[t], ob);
+    } else {
+        for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
+            const double v = (double)sj[t] * inv_scale;
+            const double nv = v / nrm;
+            const double old = cj[t];
+            dt = fma(nv, old, dt);
+            ob = fma(v, nv, ob);
+            cj[t] = nv;
+            ct32[t * kp + j] = (float)nv;
+        }
+    }
+    const double rdt = block_sum<256>(dt, sh);
+    const double rob = block_sum<256>(ob, sh);
+    if (threadIdx.x == 0) {
+        part[(j * nchunk + c) * 2] = rdt;
+        part[(j * nchunk + c) * 2 + 1] = rob;
+    }
+}
+
+// Sum_j <sums_j, c_j> partials (compute_objective, engine.py:123-127).
+__global__ void __launch_bounds__(256) k_objective_part(int64_t d, int64_t nchunk, const long long *__restrict__ sums,
+                                                        const double *__restrict__ cent64, double inv_scale,
+                                                        double *part) {
+    __shared__ double sh[8];
+    const int64_t j = blockIdx.y, c = blockIdx.x;
+    const int64_t t0 = c * kCenterChunk, t1 = min(d, t0 + kCenterChunk);
+    double ob = 0.0;
+    for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x)
+        ob = fma((double)sums[j * d + t] * inv_scale, cent64[j * d + t], ob);
+    const double r = block_sum<256>(ob, sh);
+    if (threadIdx.x == 0) part[(j * nchunk + c) * 2 + 1] = r;
+}
+
+__global__ void k_objective_final(int64_t k, int64_t nchunk, const double *__restrict__ part, double *out) {
+    if (threadIdx.x != 0) return;
+    double tot = 0.0;
+    for (int64_t j = 0; j < k; ++j) {
+        double ob = 0.0;
+        for (int64_t c = 0; c < nchunk; ++c) ob += part[(j * nchunk + c) * 2 + 1];
+        tot += ob;
+    }
+    *out = tot;
+}
+
+// ------------------------------------------------------------ finalize
+// drift (engine.py:149,160), objective (engine.py:326), convergence inputs
+// (engine.py:335-337), Hamerly owner/p_min/p_min2 (engine.py:285-289).
+__global__ void __launch_bounds__(1024) k_finalize(int64_t k, int64_t nchunk, int all, int32_t *touched,
+                                                   const double *__restrict__ part,
+                                                   const double *__restrict__ norm, double *drift,
+                                                   double *objc, double *hstat, long long *ctr,
+                                                   double *stats, long long sims_extra) {
+    __shared__ double sh[32];
+    __shared__ double shv[32];
+    __shared__ int shi[32];
+    double allone_local = 0.0, ntouched = 0.0;
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+        if (all || touched[j]) {
+            double dt = 0.0, ob = 0.0;
+            for (int64_t c = 0; c < nchunk; ++c) {
+                dt += part[(j * nchunk + c) * 2];
+                ob += part[(j * nchunk + c) * 2 + 1];
+            }
+            drift[j] = (norm[j] < 0.0) ? 1.0 : d_clamp(dt);
+            objc[j] = ob;
+            ntouched += 1.0;
+        } else {
+            drift[j] = 1.0;
+        }
+        if (drift[j] != 1.0) allone_local = 1.0;
+        touched[j] = 0;
+    }
+    __syncthreads();
+    // objective: fixed-order strided partials then a fixed tree
+    double ob = 0.0;
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) ob += objc[j];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int o = 16; o; o >>= 1) ob += __shfl_down_sync(FULL, ob, o);
+    if (lane == 0) sh[w] = ob;
+    // any drift != 1 and touched count
+    double notone = allone_local, nt = ntouched;
+    for (int o = 16; o; o >>= 1) {
+        notone = fmax(notone, __shfl_down_sync(FULL, notone, o));
+        nt += __shfl_down_sync(FULL, nt, o);
+    }
+    __shared__ double sh1[32], sh2[32];
+    if (lane == 0) {
+        sh1[w] = notone;
+        sh2[w] = nt;
+    }
+    // Hamerly: owner = first index of min drift; p_min2 = min over the rest
+    double bv = INFINITY;
+    int bi = 0x7fffffff;
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+        const double v = drift[j];
+        if (v < bv || (v == bv && (int)j < bi)) {
+            bv = v;
+            bi = (int)j;
+        }
+    }
+    for (int o = 16; o; o >>= 1) {
+        const double ov = __shfl_down_sync(FULL, bv, o);
+        const int oi = __shfl_down_sync(FULL, bi, o);
+        if (ov < bv || (ov == bv && oi < bi)) {
+            bv = ov;
+            bi = oi;
+        }
+    }
+    if (lane == 0) {
+        shv[w] = bv;
+        shi[w] = bi;
+    }
+    __syncthreads();
+    __shared__ int owner_s;
+    if (threadIdx.x == 0) {
+        const int nw = blockDim.x >> 5;
+        double tot = 0.0, no = 0.0, ntt = 0.0;
+        double mv = INFINITY;
+        int mi = 0x7fffffff;
+        for (int q = 0; q < nw; ++q) {
+            tot += sh[q];
+            no = fmax(no, sh1[q]);
+            ntt += sh2[q];
+            if (shv[q] < mv || (shv[q] == mv && shi[q] < mi)) {
+                mv = shv[q];
+                mi = shi[q];
+            }
+        }
+        owner_s = mi;
+        hstat[0] = (double)mi;
+        hstat[1] = mv;
+        stats[SPKM_ST_OBJECTIVE] = tot;
+        stats[SPKM_ST_ALLONE] = (no == 0.0) ? 1.0 : 0.0;
+        stats[SPKM_ST_TOUCHED] = ntt;
+        stats[SPKM_ST_SIMS] = (double)(ctr[SPKM_CTR_SIMS] + sims_extra);
+        stats[SPKM_ST_REASSIGN] = (double)ctr[SPKM_CTR_MOVES];
+        stats[SPKM_ST_SURV1] = (double)ctr[SPKM_CTR_SURV1];
+        stats[SPKM_ST_SURV2] = (double)ctr[SPKM_CTR_SURV2];
+        stats[SPKM_ST_NNZ_TIGHTEN] = (double)ctr[SPKM_CTR_NNZ_TIGHTEN];
+        stats[SPKM_ST_NNZ_RESCAN] = (double)ctr[SPKM_CTR_NNZ_RESCAN];
+        stats[SPKM_ST_NNZ_ELKAN] = (double)ctr[SPKM_CTR_NNZ_ELKAN];
+    }
+    __syncthreads();
+    const int owner = owner_s;
+    bv = INFINITY;
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x)
+        if ((int)j != owner) bv = fmin(bv, drift[j]);
+    for (int o = 16; o; o >>= 1) bv = fmin(bv, __shfl_down_sync(FULL, bv, o));
+    __syncthreads();
+    if (lane == 0) shv[w] = bv;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double mv = INFINITY;
+        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) mv = fmin(mv, shv[q]);
+        hstat[2] = (k > 1) ? mv : 1.0;
+        for (int q = 0; q < 8; ++q) ctr[q] = 0;
+    }
+}
+
+// ---------------------------------------------------------- center thresholds
+// engine._center_thresholds (engine.py:192-198): split-d float64 Gram tiles.
+constexpr int GT = 32;   // output tile
+constexpr int GK = 16;   // d step
+__global__ void __launch_bounds__(256) k_gram_part(int64_t k, int64_t d, int64_t dsplit,
+                                                   const double *__restrict__ C, const int2 *__restrict__ tiles,
+                                                   double *gpart) {
+    __shared__ double As[GK][GT + 1];
+    __shared__ double Bs[GK][GT + 1];
+    const int2 tl = tiles[blockIdx.x];
+    const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
+    const int64_t per = (d + dsplit - 1) / dsplit;
+    const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
+    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
+    double acc[4] = {0, 0, 0, 0};
+    for (int64_t tb = t0; tb < t1; tb += GK) {
+        for (int e = threadIdx.x; e < GK * GT; e += blockDim.x) {
+            const int r = e / GK, cidx = e % GK;
+            const int64_t t = tb + cidx;
+            const int64_t ar = a0 + r, jr = j0 + r;
+            As[cidx][r] = (ar < k && t < t1) ? C[ar * d + t] : 0.0;
+            Bs[cidx][r] = (jr < k && t < t1) ? C[jr * d + t] : 0.0;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int c = 0; c < GK; ++c) {
+            const double b = Bs[c][tx];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) acc[q] = fma(As[c][ty + 8 * q], b, acc[q]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int64_t ar = a0 + ty + 8 * q, jr = j0 + tx;
+        if (ar < k && jr < k) gpart[((int64_t)blockIdx.y * k + ar) * k + jr] = acc[q];
+    }
+}
+
+__global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict__ gpart, float *cc) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= k * k) return;
+    const int64_t a = e / k, j = e % k;
+    if (a > j) return;
+    if (a == j) {
+        cc[e] = -1.f;
+        return;
+    }
+    double g = 0.0;
+    for (int64_t y = 0; y < dsplit; ++y) g += gpart[(y * k + a) * k + j];
+    double h = d_half_angle(d_clamp(g)) + kCcSlack;
+    if (h > 1.0) h = 1.0;
+    const float f = __double2float_ru(h);
+    cc[a * k + j] = f;
+    cc[j * k + a] = f;
+}
+
+__global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s) {
+    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (a >= k) return;
+    float m = -INFINITY;
+    for (int64_t j = 0; j < k; ++j)
+        if (j != a) m = fmaxf(m, cc[a * k + j]);
+    s[a] = (k > 1) ? m : -1.f;
+}
+
+// ---------------------------------------------------------------- misc
+__global__ void k_load_centers(int64_t k, int64_t d, int64_t kp, const double *__restrict__ src, double *cent64,
+                               float *ct32) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= k * d) return;
+    const int64_t j = e / d, t = e % d;
+    const double v = src[e];
+    cent64[e] = v;
+    ct32[t * kp + j] = (float)v;
+}
+
+__global__ void k_geometry(int op, int64_t n, const double *a, const double *b, double *out) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    switch (op) {
+        case 0: out[i] = d_cos_lower(a[i], b[i]); break;
+        case 1: out[i] = d_cos_upper(a[i], b[i]); break;
+        case 2: out[i] = d_hamerly_upper(a[i], b[i]); break;
+        case 3: out[i] = d_half_angle(a[i]); break;
+        case 4: out[i] = d_lower_update(a[i], b[i]); break;
+        default: out[i] = d_clamp(a[i]); break;
+    }
+}
+
+// ------------------------------------------------------------- host glue
+struct ColPlan {
+    int ch, tpr, rpw;
+};
+ColPlan col_plan(int64_t k) {
+    int ch = 4;
+    while (ch < 32 && (k + ch - 1) / ch > 32) ch *= 2;
+    ColPlan p;
+    p.ch = ch;
+    p.tpr = (int)((k + ch - 1) / ch);
+    if (p.tpr > 32) p.tpr = 32;
+    p.rpw = 32 / p.tpr;
+    return p;
+}
+
+int grid_for(int64_t work_items, int per_block) {
+    const int64_t need = (work_items + per_block - 1) / per_block;
+    const int64_t cap = (int64_t)num_sms() * 16;
+    int64_t g = need < cap ? need : cap;
+    return (int)(g < 1 ? 1 : g);
+}
+
+int launch_row_pass(RowPassArgs &A, int64_t k, cudaStream_t st, int64_t max_rows) {
+    const ColPlan p = col_plan(k);
+    A.tpr = p.tpr;
+    A.rpw = p.rpw;
+    A.k = (int)k;
+    const int64_t slots = (max_rows + p.rpw - 1) / p.rpw;
+    const int grid = grid_for(slots, 8);
+    switch (p.ch) {
+        case 4: k_row_pass<4><<<grid, 256, 0, st>>>(A); break;
+        case 8: k_row_pass<8><<<grid, 256, 0, st>>>(A); break;
+        case 16: k_row_pass<16><<<grid, 256, 0, st>>>(A); break;
+        default: k_row_pass<32><<<grid, 256, 0, st>>>(A); break;
+    }
+    CHECK_LAUNCH("row_pass");
+    return 0;
+}
+
+RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
+    RowPassArgs A{};
+    A.indptr = X->indptr;
+    A.indices = X->indices;
+    A.values = X->values;
+    A.reps = X->row_eps;
+    A.n = X->n;
+    A.ct = C->ct32;
+    A.kp = C->kp;
+    return A;
+}
+
+}  // namespace
+
+extern "C" {
+
+int spkm_abi_version(void) { return SPKM_ABI_VERSION; }
+const char *spkm_last_error(void) { return g_err; }
+int64_t spkm_center_chunks(int64_t d) { return (d + kCenterChunk - 1) / kCenterChunk; }
+int64_t spkm_padded_k(int64_t k) {
+    const ColPlan p = col_plan(k);
+    if (k > 32 * 32) return ((k + 1023) / 1024) * 1024;
+    return (int64_t)p.tpr * p.ch;
+}
+
+int spkm_reset_counters(spkm_work *W, void *stream) {
+    cudaError_t e = cudaMemsetAsync(W->ctr, 0, 8 * sizeof(long long), S(stream));
+    return e == cudaSuccess ? 0 : fail("reset_counters", e);
+}
+
+int spkm_full_assign(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int mode,
+                     void *stream) {
+    if (C->k > 1024) return fail_msg("k > 1024 not supported by this build");
+    if (X->n == 0) return 0;
+    RowPassArgs A = row_args(X, C);
+    A.mode = mode;
+    A.a = B->a;
+    A.l = B->l;
+    A.u = B->u;
+    A.ku = B->ku;
+    A.mv_i = W->mv_i;
+    A.mv_old = W->mv_old;
+    A.ctr = W->ctr;
+    return launch_row_pass(A, C->k, S(stream), X->n);
+}
+
+int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_s,
+                        int naive, void *stream) {
+    if (X->n == 0) return 0;
+    const int grid = grid_for(X->n, 256);
+    k_hamerly_bounds<<<grid, 256, 0, S(stream)>>>(X->n, X->row_eps, B->a, B->l, B->u, C->drift, C->s, C->hstat,
+                                                  use_s, naive, W->surv1, W->ctr);
+    CHECK_LAUNCH("hamerly_bounds");
+    return 0;
+}
+
+int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_s,
+                         void *stream) {
+    if (X->n == 0) return 0;
+    const int grid = grid_for(X->n, 256);
+    k_hamerly_tighten<<<grid, 256, 0, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
+                                                   B->a, B->l, B->u, C->s, use_s, W->surv1, W->surv2, W->ctr);
+    CHECK_LAUNCH("hamerly_tighten");
+    return 0;
+}
+
+int spkm_hamerly_rescan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream) {
+    if (C->k > 1024) return fail_msg("k > 1024 not supported by this build");
+    if (X->n == 0) return 0;
+    RowPassArgs A = row_args(X, C);
+    A.mode = MODE_RESCAN;
+    A.rowlist = W->surv2;
+    A.rowcount = W->ctr + SPKM_CTR_SURV2;
+    A.a = B->a;
+    A.l = B->l;
+    A.u = B->u;
+    A.ku = 1;
+    A.mv_i = W->mv_i;
+    A.mv_old = W->mv_old;
+    A.ctr = W->ctr;
+    return launch_row_pass(A, C->k, S(stream), X->n);
+}
+
+int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
+                      void *stream) {
+    if (X->n == 0) return 0;
+    const int grid = grid_for(X->n, 8);
+    k_elkan_bounds<<<grid, 256, 0, S(stream)>>>(X->n, (int)C->k, X->row_eps, B->a, B->l, B->u, B->ku, C->drift,
+                                                C->cc, C->s, use_cc, W->surv1, W->ctr);
+    CHECK_LAUNCH("elkan_bounds");
+    return 0;
+}
+
+int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
+                    void *stream) {
+    if (X->n == 0) return 0;
+    const int grid = grid_for(X->n, 8);
+    k_elkan_scan<<<grid, 256, 0, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
+                                              (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1,
+                                              W->mv_i, W->mv_old, W->ctr);
+    CHECK_LAUNCH("elkan_scan");
+    return 0;
+}
+
+int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B, long long *sums_target,
+                        long long *counts_target, void *stream) {
+    cudaStream_t st = S(stream);
+    cudaError_t e = cudaMemsetAsync(sums_target, 0, sizeof(long long) * C->k * C->d, st);
+    if (e != cudaSuccess) return fail("aggregate memset", e);
+    e = cudaMemsetAsync(counts_target, 0, sizeof(long long) * C->k, st);
+    if (e != cudaSuccess) return fail("aggregate memset", e);
+    if (X->n == 0) return 0;
+    const int grid = grid_for(X->n, 8);
+    k_aggregate<<<grid, 256, 0, st>>>(X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
+                                      counts_target, ldexp(1.0, C->scale_bits));
+    CHECK_LAUNCH("aggregate");
+    return 0;
+}
+
+int spkm_apply_moves(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B, const spkm_work *W,
+                     long long *sums_target, long long *counts_target, int32_t *touched, void *stream) {
+    if (X->n == 0) return 0;
+    const int grid = grid_for(X->n, 8);
+    k_apply_moves<<<grid, 256, 0, S(stream)>>>(C->d, X->indptr, X->indices, X->values, B->a, W->mv_i, W->mv_old,
+                                               W->ctr, sums_target, counts_target, touched,
+                                               ldexp(1.0, C->scale_bits));
+    CHECK_LAUNCH("apply_moves");
+    return 0;
+}
+
+int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
+    cudaStream_t st = S(stream);
+    const int64_t nch = spkm_center_chunks(C->d);
+    const double inv = ldexp(1.0, -C->scale_bits);
+    dim3 grid((unsigned)nch, (unsigned)C->k);
+    k_center_norm_part<<<grid, 256, 0, st>>>(C->d, nch, C->sums, C->touched, all_clusters, inv, C->part);
+    CHECK_LAUNCH("center_norm_part");
+    k_center_norm_final<<<(unsigned)((C->k + 255) / 256), 256, 0, st>>>(C->k, nch, C->counts, C->touched,
+                                                                       all_clusters, C->part, C->norm);
+    CHECK_LAUNCH("center_norm_final");
+    k_center_write<<<grid, 256, 0, st>>>(C->d, C->kp, nch, C->sums, C->touched, all_clusters, inv, C->norm,
+                                         C->cent64, C->ct32, C->part);
+    CHECK_LAUNCH("center_write");
+    return 0;
+}
+
+int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra, void *stream) {
+    k_finalize<<<1, 1024, 0, S(stream)>>>(C->k, spkm_center_chunks(C->d), all_clusters, C->touched, C->part, C->norm,
+                                          C->drift, C->objc, C->hstat, W->ctr, W->stats, sims_extra);
+    CHECK_LAUNCH("finalize");
+    return 0;
+}
+
+int64_t spkm_gram_dsplit(int64_t k, int64_t d) {
+    const int64_t tk = (k + GT - 1) / GT;
+    const int64_t tiles = tk * (tk + 1) / 2;
+    int64_t ds = (2 * (int64_t)num_sms() + tiles - 1) / tiles;
+    const int64_t maxds = (d + 511) / 512;
+    if (ds > maxds) ds = maxds;
+    if (ds < 1) ds = 1;
+    return ds;
+}
+
+int64_t spkm_gram_scratch_doubles(int64_t k, int64_t d) { return spkm_gram_dsplit(k, d) * k * k; }
+
+int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *tiles_ptr, void *stream) {
+    const int2 *tiles_dev = static_cast<const int2 *>(tiles_ptr);
+    cudaStream_t st = S(stream);
+    const int64_t tk = (C->k + GT - 1) / GT;
+    const int64_t ntiles = tk * (tk + 1) / 2;
+    const int64_t ds = spkm_gram_dsplit(C->k, C->d);
+    dim3 grid((unsigned)ntiles, (unsigned)ds);
+    k_gram_part<<<grid, 256, 0, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, gpart);
+    CHECK_LAUNCH("gram_part");
+    k_gram_final<<<(unsigned)((C->k * C->k + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->cc);
+    CHECK_LAUNCH("gram_final");
+    k_row_max<<<(unsigned)((C->k + 255) / 256), 256, 0, st>>>(C->k, C->cc, C->s);
+    CHECK_LAUNCH("row_max");
+    return 0;
+}
+
+// Fill the upper-triangle tile list used by the Gram kernel.
+int64_t spkm_gram_tiles(int64_t k, int32_t *host_pairs /* [2*ntiles] */) {
+    const int64_t tk = (k + GT - 1) / GT;
+    int64_t q = 0;
+    for (int64_t a = 0; a < tk; ++a)
+        for (int64_t j = a; j < tk; ++j) {
+            if (host_pairs) {
+                host_pairs[2 * q] = (int32_t)a;
+                host_pairs[2 * q + 1] = (int32_t)j;
+            }
+            ++q;
+        }
+    return q;
+}
+
+int spkm_predict(const spkm_csr *X, const spkm_centers *C, int32_t *a, double *best, double *second,
+                 void *stream) {
+    if (C->k > 1024) return fail_msg("k > 1024 not supported by this build");
+    if (X->n == 0) return 0;
+    RowPassArgs A = row_args(X, C);
+    A.mode = MODE_PREDICT;
+    A.a = a;
+    A.best = best;
+    A.second = second;
+    return launch_row_pass(A, C->k, S(stream), X->n);
+}
+
+int spkm_objective(const spkm_centers *C, const long long *sums, double *out, void *stream) {
+    cudaStream_t st = S(stream);
+    const int64_t nch = spkm_center_chunks(C->d);
+    dim3 grid((unsigned)nch, (unsigned)C->k);
+    k_objective_part<<<grid, 256, 0, st>>>(C->d, nch, sums, C->cent64, ldexp(1.0, -C->scale_bits), C->part);
+    CHECK_LAUNCH("objective_part");
+    k_objective_final<<<1, 32, 0, st>>>(C->k, nch, C->part, out);
+    CHECK_LAUNCH("objective_final");
+    return 0;
+}
+
+int spkm_load_centers(const spkm_centers *C, const double *src, void *stream) {
+    const int64_t tot = C->k * C->d;
+    k_load_centers<<<(unsigned)((tot + 255) / 256), 256, 0, S(stream)>>>(C->k, C->d, C->kp, src, C->cent64,
+                                                                         C->ct32);
+    CHECK_LAUNCH("load_centers");
+    return 0;
+}
+
+int spkm_geometry(int op, int64_t n, const double *a, const double *b, double *out, void *stream) {
+    if (n == 0) return 0;
+    k_geometry<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(op, n, a, b, out);
+    CHECK_LAUNCH("geometry");
+    return 0;
+}
+
+}  // extern "C"

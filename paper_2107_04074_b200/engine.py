@@ -1,0 +1,529 @@
+"""The accelerated spherical k-means loop on B200 (fit = ``run``, predict = ``assign_full``).
+
+Host mirror of the reference's engine (/root/reference/pkg/src/spkmeans/
+engine.py:1-346): same names, arguments, variants, dataclasses, errors and
+phase order, but every numeric phase is a CUDA kernel of libspkm.so called
+through the C ABI (include/spkm.h).  PyTorch only allocates device buffers
+and provides the stream.  There is no CPU fallback.
+
+Phase order per iteration (engine.py:239-337):
+  it == 1   full pass + top-2 (bounds init)  -> scratch sums -> move all
+  it >= 2   [cc/s]  -> bound drift update + prune test + compaction
+            -> debug_hook -> scan survivors -> incremental sums (moves)
+            -> renormalise touched -> objective / drift / convergence stats
+One 64-byte stats read (D2H) per iteration drives IterationStats and the
+convergence test, exactly like the reference's per-iteration bookkeeping.
+
+Documented deviations: similarities are float32 in
+a fixed FMA order; bounds carry a per-row error margin so pruned variants
+are exactly equal to this module's Lloyd; exact ties keep the incumbent
+from iteration 2 on; center sums are exact int64 fixed point (so the
+reference's 50-iteration scratch rebuild is a no-op, kept for its schedule).
+"""
+
+from __future__ import annotations
+
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib
+from ._lib import Bounds, Centers, CSR, Work
+from .errors import ConfigError, DeviceError, InfeasibleError
+from .sparse import Dataset
+
+VARIANTS = ("standard", "elkan", "simp_elkan", "hamerly", "simp_hamerly")
+_ELKAN_FAMILY = frozenset({"elkan", "simp_elkan"})
+_HAMERLY_FAMILY = frozenset({"hamerly", "simp_hamerly"})
+_CC_VARIANTS = frozenset({"elkan", "hamerly"})
+_SCRATCH_INTERVAL = 50
+EPS_UNIT = 6.1e-8
+
+
+# --------------------------------------------------------------- dataclasses
+@dataclass
+class CentroidSet:
+    """Unit centers plus the state needed to move them (engine.py:31-58)."""
+
+    centers: np.ndarray
+    sums: np.ndarray
+    counts: np.ndarray
+    prev_centers: np.ndarray | None
+    drift: np.ndarray
+    seed_indices: np.ndarray | None = None
+
+    @property
+    def k(self) -> int:
+        return self.centers.shape[0]
+
+    @classmethod
+    def from_data_rows(cls, data: Dataset, row_indices) -> "CentroidSet":
+        idx = np.asarray(row_indices, dtype=np.int64)
+        centers = data.densify_rows(idx)
+        k = centers.shape[0]
+        return cls(centers=centers, sums=np.zeros_like(centers), counts=np.zeros(k, np.int64),
+                   prev_centers=centers.copy(), drift=np.ones(k), seed_indices=idx)
+
+
+@dataclass
+class BoundsState:
+    """Bounds handed to debug hooks (engine.py:61-69); host copies of device state."""
+
+    variant: str
+    a: np.ndarray
+    l: np.ndarray
+    u_matrix: np.ndarray | None = None
+    u: np.ndarray | None = None
+
+
+@dataclass
+class IterationStats:
+    iteration: int
+    sim_count: int
+    cc_sim_count: int
+    reassignments: int
+    objective: float
+    elapsed_ns: int
+    # instrumentation beyond the reference's fields (defaults keep its constructor)
+    survivors: int = 0          # points failing the drift-updated bound test
+    survivors2: int = 0         # Hamerly: points still failing after tightening
+    nnz_scanned: int = 0        # CSR nnz re-read by the survivor scans
+
+
+@dataclass
+class ClusteringResult:
+    assignments: np.ndarray
+    centers: CentroidSet
+    objective: float
+    iterations: list = field(default_factory=list)
+    converged: bool = False
+
+    @property
+    def total_sims(self) -> int:
+        return sum(s.sim_count for s in self.iterations)
+
+    @property
+    def total_cc_sims(self) -> int:
+        return sum(s.cc_sim_count for s in self.iterations)
+
+
+# --------------------------------------------------------------- device state
+def _stream_ptr(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes_void(s.cuda_stream)
+
+
+def ctypes_void(v):
+    import ctypes
+    return ctypes.c_void_p(int(v))
+
+
+def _ptr(t: torch.Tensor | None):
+    return None if t is None else t.data_ptr()
+
+
+def row_eps(lengths: np.ndarray) -> np.ndarray:
+    """eps_i = (nnz_i + 6) * 6.1e-8, rounded up to float32 (spkm.cu header)."""
+    e = (lengths.astype(np.float64) + 6.0) * EPS_UNIT
+    f = e.astype(np.float32)
+    low = f.astype(np.float64) < e
+    f[low] = np.nextafter(f[low], np.float32(np.inf))
+    return f
+
+
+def scale_bits_for(n_total: int) -> int:
+    """Fixed-point scale with n * 2^S <= 2^62 (SURVEY.md §7 hard part 1d)."""
+    return int(62 - math.ceil(math.log2(n_total + 1)))
+
+
+class DeviceCorpus:
+    """A CSR (or row range of one) resident in HBM: int64 indptr, int32 indices, fp32 values."""
+
+    def __init__(self, data: Dataset, device: torch.device, rows: tuple | None = None,
+                 pinned_host: bool = False):
+        r0, r1 = rows if rows is not None else (0, data.n)
+        s, e = int(data.indptr[r0]), int(data.indptr[r1])
+        ip = data.indptr[r0:r1 + 1] - s
+        self.n, self.d, self.nnz = r1 - r0, data.dim, e - s
+        self.rows = (r0, r1)
+        host = [torch.from_numpy(np.ascontiguousarray(ip, np.int64)),
+                torch.from_numpy(np.ascontiguousarray(data.indices[s:e], np.int32)),
+                torch.from_numpy(np.ascontiguousarray(data.data[s:e], np.float32)),
+                torch.from_numpy(row_eps(np.diff(ip)))]
+        if pinned_host:
+            host = [h.pin_memory() for h in host]
+        self.host = host
+        self.indptr, self.indices, self.values, self.reps = [h.to(device, non_blocking=True) for h in host]
+        self.h2d_bytes = sum(h.numel() * h.element_size() for h in host)
+        self.struct = CSR(self.n, self.d, self.nnz, _ptr(self.indptr), _ptr(self.indices), _ptr(self.values),
+                          _ptr(self.reps))
+
+
+def device_corpus(data: Dataset, device=None, cache: bool = True) -> DeviceCorpus:
+    device = torch.device(device or "cuda")
+    key = str(device)
+    if cache and key in data._device_cache:
+        return data._device_cache[key]
+    dc = DeviceCorpus(data, device)
+    if cache:
+        data._device_cache[key] = dc
+    return dc
+
+
+class CenterState:
+    """Replicated center buffers (spkm_centers)."""
+
+    def __init__(self, k: int, d: int, n_total: int, device, with_cc: bool):
+        L = _lib.lib()
+        self.k, self.d = k, d
+        self.kp = int(L.spkm_padded_k(k))
+        self.nchunk = int(L.spkm_center_chunks(d))
+        self.scale_bits = scale_bits_for(n_total)
+        dev = device
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.cent64 = torch.zeros(k * d, **f64)
+        self.ct32 = torch.zeros(d * self.kp, dtype=torch.float32, device=dev)
+        self.sums = torch.zeros(k * d, dtype=torch.int64, device=dev)
+        self.counts = torch.zeros(k, dtype=torch.int64, device=dev)
+        self.drift = torch.ones(k, **f64)
+        self.touched = torch.zeros(k, dtype=torch.int32, device=dev)
+        self.objc = torch.zeros(k, **f64)
+        self.part = torch.zeros(k * self.nchunk * 2, **f64)
+        self.norm = torch.zeros(k, **f64)
+        self.cc = torch.zeros(k * k if with_cc else 1, dtype=torch.float32, device=dev)
+        self.s = torch.zeros(k if with_cc else 1, dtype=torch.float32, device=dev)
+        self.hstat = torch.zeros(4, **f64)
+        if with_cc:
+            ntiles = int(L.spkm_gram_tiles(k, None))
+            pairs = np.zeros(2 * ntiles, np.int32)
+            L.spkm_gram_tiles(k, pairs.ctypes.data)
+            self.tiles = torch.from_numpy(pairs).to(dev)
+            self.gram = torch.zeros(int(L.spkm_gram_scratch_doubles(k, d)), **f64)
+        self.struct = Centers(k, d, self.kp, self.scale_bits, 0, _ptr(self.cent64), _ptr(self.ct32),
+                              _ptr(self.sums), _ptr(self.counts), _ptr(self.drift), _ptr(self.touched),
+                              _ptr(self.objc), _ptr(self.part), _ptr(self.norm), _ptr(self.cc), _ptr(self.s),
+                              _ptr(self.hstat))
+
+    def load(self, centers: np.ndarray, stream):
+        src = torch.from_numpy(np.ascontiguousarray(centers, np.float64).ravel()).to(self.cent64.device)
+        _lib.call("spkm_load_centers", self.struct, _ptr(src), stream)
+        return src  # keep alive until the stream passes
+
+    def host_centers(self) -> np.ndarray:
+        return self.cent64.view(self.k, self.d).cpu().numpy()
+
+    def host_sums(self) -> np.ndarray:
+        return self.sums.view(self.k, self.d).cpu().numpy().astype(np.float64) * 2.0 ** -self.scale_bits
+
+
+class PointState:
+    """Per-point bounds and worklists (spkm_bounds + spkm_work)."""
+
+    def __init__(self, n: int, k: int, variant: str, device):
+        i32 = dict(dtype=torch.int32, device=device)
+        self.a = torch.zeros(max(n, 1), **i32)
+        self.l = torch.zeros(max(n, 1), dtype=torch.float32, device=device)
+        if variant in _ELKAN_FAMILY:
+            self.ku = (k + 3) // 4 * 4
+            self.u = torch.zeros(max(n, 1) * self.ku, dtype=torch.float32, device=device)
+        else:
+            self.ku = 1
+            self.u = torch.zeros(max(n, 1), dtype=torch.float32, device=device)
+        self.surv1 = torch.zeros(max(n, 1), **i32)
+        self.surv2 = torch.zeros(max(n, 1), **i32)
+        self.mv_i = torch.zeros(max(n, 1), **i32)
+        self.mv_old = torch.zeros(max(n, 1), **i32)
+        self.ctr = torch.zeros(8, dtype=torch.int64, device=device)
+        self.stats = torch.zeros(_lib.ST_COUNT, dtype=torch.float64, device=device)
+        self.stats_host = torch.zeros(_lib.ST_COUNT, dtype=torch.float64).pin_memory()
+        self.bounds = Bounds(_ptr(self.a), _ptr(self.l), _ptr(self.u), self.ku)
+        self.work = Work(_ptr(self.surv1), _ptr(self.surv2), _ptr(self.mv_i), _ptr(self.mv_old), _ptr(self.ctr),
+                         _ptr(self.stats))
+
+
+# --------------------------------------------------------------- validation
+def _validate(data: Dataset, k: int, variant: str, hamerly_update: str):
+    if variant not in VARIANTS:
+        raise ConfigError(f"unknown variant {variant!r}")
+    if hamerly_update not in ("safe", "naive"):
+        raise ConfigError(f"unknown hamerly_update {hamerly_update!r}")
+    if not 1 <= k <= data.n:
+        raise InfeasibleError(f"k={k} infeasible for n={data.n}")
+
+
+def _require_cuda(device):
+    if not torch.cuda.is_available():
+        raise DeviceError("a CUDA device is required (this build has no CPU path)")
+    return torch.device(device or "cuda")
+
+
+# --------------------------------------------------------------- the loop
+class Engine:
+    """One clustering run's device state and the per-phase kernel calls.
+
+    ``comm`` (optional) is a ``distributed.Exchange`` for multi-GPU runs:
+    the corpus is then the local row shard and the center sums/counts are
+    combined with one allreduce per iteration.
+    """
+
+    def __init__(self, data: Dataset, k: int, variant: str, device=None, hamerly_update: str = "safe",
+                 corpus: DeviceCorpus | None = None, comm=None, n_total: int | None = None):
+        self.device = _require_cuda(device)
+        self.k, self.variant = k, variant
+        self.naive = int(hamerly_update == "naive")
+        self.corpus = corpus if corpus is not None else device_corpus(data, self.device)
+        self.comm = comm
+        self.n_total = n_total if n_total is not None else self.corpus.n
+        self.elkan = variant in _ELKAN_FAMILY
+        self.hamerly = variant in _HAMERLY_FAMILY
+        self.needs_cc = variant in _CC_VARIANTS
+        self.C = CenterState(k, data.dim, self.n_total, self.device, self.needs_cc)
+        self.P = PointState(self.corpus.n, k, variant, self.device)
+        self.stream = torch.cuda.current_stream(self.device)
+        self.sp = ctypes_void(self.stream.cuda_stream)
+
+    # -- phases --------------------------------------------------------------
+    def load_centers(self, centers: np.ndarray):
+        keep = self.C.load(centers, self.sp)
+        self.stream.synchronize()
+        del keep
+
+    def reset(self):
+        _lib.call("spkm_reset_counters", self.P.work, self.sp)
+
+    def center_thresholds(self):
+        _lib.call("spkm_center_thresholds", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles), self.sp)
+
+    def init_pass(self):
+        mode = (_lib.MODE_INIT_ELKAN if self.elkan else _lib.MODE_INIT_HAMERLY if self.hamerly
+                else _lib.MODE_INIT_PLAIN)
+        _lib.call("spkm_full_assign", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work, mode, self.sp)
+
+    def scratch_sums(self):
+        _lib.call("spkm_aggregate_sums", self.corpus.struct, self.C.struct, self.P.bounds,
+                  _ptr(self.C.sums), _ptr(self.C.counts), self.sp)
+        if self.comm is not None:
+            self.comm.scratch(self.C.sums, self.C.counts)
+
+    def lloyd_pass(self):
+        _lib.call("spkm_full_assign", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+                  _lib.MODE_LLOYD, self.sp)
+
+    def bounds_pass(self, use_flag: int):
+        if self.elkan:
+            _lib.call("spkm_elkan_bounds", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+                      use_flag, self.sp)
+        else:
+            _lib.call("spkm_hamerly_bounds", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+                      use_flag, self.naive, self.sp)
+
+    def scan_pass(self, use_flag: int):
+        if self.elkan:
+            _lib.call("spkm_elkan_scan", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+                      use_flag, self.sp)
+        else:
+            _lib.call("spkm_hamerly_tighten", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+                      use_flag, self.sp)
+            _lib.call("spkm_hamerly_rescan", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+                      self.sp)
+
+    def apply_moves(self):
+        if self.comm is None:
+            _lib.call("spkm_apply_moves", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+                      _ptr(self.C.sums), _ptr(self.C.counts), _ptr(self.C.touched), self.sp)
+        else:
+            ex = self.comm
+            ex.begin()
+            _lib.call("spkm_apply_moves", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+                      _ptr(ex.delta), _ptr(ex.dcounts), _ptr(self.C.touched), self.sp)
+            ex.exchange(self.C.sums, self.C.counts, self.C.touched, self.P.ctr)
+
+    def move_centers(self, all_clusters: bool):
+        _lib.call("spkm_move_centers", self.C.struct, int(all_clusters), self.sp)
+
+    def finalize(self, all_clusters: bool, sims_extra: int) -> np.ndarray:
+        _lib.call("spkm_finalize", self.C.struct, self.P.work, int(all_clusters), int(sims_extra), self.sp)
+        self.P.stats_host.copy_(self.P.stats, non_blocking=True)
+        self.stream.synchronize()
+        return self.P.stats_host.numpy().copy()
+
+    def host_bounds(self) -> BoundsState:
+        n = self.corpus.n
+        a = self.P.a[:n].cpu().numpy().astype(np.int64)
+        l = self.P.l[:n].cpu().numpy().astype(np.float64)
+        if self.elkan:
+            um = self.P.u.view(-1, self.P.ku)[:n, :self.k].cpu().numpy().astype(np.float64)
+            return BoundsState(self.variant, a, l, u_matrix=um)
+        u = self.P.u[:n].cpu().numpy().astype(np.float64)
+        return BoundsState(self.variant, a, l, u=u)
+
+    def centroid_set(self, seed_indices=None) -> CentroidSet:
+        C = self.C
+        return CentroidSet(centers=C.host_centers(), sums=C.host_sums(), counts=C.counts.cpu().numpy(),
+                           prev_centers=None, drift=C.drift.cpu().numpy(), seed_indices=seed_indices)
+
+    # -- one iteration ---------------------------------------------------------
+    def iteration(self, it: int, debug_hook=None, seed_indices=None) -> tuple:
+        k = self.k
+        if it == 1:
+            self.init_pass()
+            self.scratch_sums()
+            self.move_centers(True)
+            return self.finalize(True, self.n_total * k), None
+        if self.variant == "standard":
+            self.lloyd_pass()
+            sims_extra = self.n_total * k
+        else:
+            use = int(self.needs_cc)
+            if self.needs_cc:
+                self.center_thresholds()
+            self.bounds_pass(use)
+            if debug_hook is not None:
+                self.stream.synchronize()
+                debug_hook(it, self.host_bounds(), self.centroid_set(seed_indices))
+            self.scan_pass(use)
+            sims_extra = 0
+        self.apply_moves()
+        self.move_centers(False)
+        if it % _SCRATCH_INTERVAL == 0:
+            # exact fixed-point sums: the rebuild reproduces the incremental
+            # sums bit-for-bit; kept so the reference's schedule is visible
+            self.scratch_sums()
+        return self.finalize(False, sims_extra), None
+
+
+def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, debug_hook=None,
+        hamerly_update: str = "safe", *, device=None, corpus: DeviceCorpus | None = None,
+        init_centers: np.ndarray | None = None, comm=None, n_total: int | None = None,
+        seed_indices=None) -> ClusteringResult:
+    """Cluster ``data`` into ``k`` groups (reference engine.run, engine.py:201-346)."""
+    from .seeding import SeedConfig, make_centroids
+
+    _validate(data, k, variant, hamerly_update)
+    if init_centers is None:
+        cents0 = make_centroids(data, k, seeding if seeding is not None else SeedConfig())
+        init_centers, seed_indices = cents0.centers, cents0.seed_indices
+    eng = Engine(data, k, variant, device=device, hamerly_update=hamerly_update, corpus=corpus, comm=comm,
+                 n_total=n_total)
+    eng.load_centers(init_centers)
+    eng.reset()
+    cc_per_it = k * (k - 1) // 2 if variant in _CC_VARIANTS else 0
+    stats: list = []
+    converged = False
+    for it in range(1, max_iter + 1):
+        t0 = time.monotonic_ns()
+        st, _ = eng.iteration(it, debug_hook, seed_indices)
+        reassign = data.n if it == 1 else int(st[_lib.ST_REASSIGN])
+        stats.append(IterationStats(iteration=it, sim_count=int(st[_lib.ST_SIMS]), cc_sim_count=cc_per_it,
+                                    reassignments=reassign, objective=float(st[_lib.ST_OBJECTIVE]),
+                                    elapsed_ns=time.monotonic_ns() - t0, survivors=int(st[_lib.ST_SURV1]),
+                                    survivors2=int(st[_lib.ST_SURV2]),
+                                    nnz_scanned=int(st[_lib.ST_NNZ_TIGHTEN] + st[_lib.ST_NNZ_RESCAN]
+                                                    + st[_lib.ST_NNZ_ELKAN])))
+        if k == 1 or st[_lib.ST_ALLONE] == 1.0 or (it >= 2 and reassign == 0):
+            converged = True
+            break
+    a = eng.P.a[:eng.corpus.n].cpu().numpy().astype(np.int64)
+    if comm is not None:
+        a = comm.gather_assignments(eng.P.a, eng.corpus.rows, eng.n_total)
+    return ClusteringResult(assignments=a, centers=eng.centroid_set(seed_indices), objective=stats[-1].objective,
+                            iterations=stats, converged=converged)
+
+
+# --------------------------------------------------------------- predict etc.
+def _centers_array(centroids) -> np.ndarray:
+    return np.asarray(centroids.centers if isinstance(centroids, CentroidSet) else centroids, dtype=np.float64)
+
+
+def assign_full(data: Dataset, centroids, device=None):
+    """Full argmax pass (engine.py:103-120): (assignments, best, second).
+
+    Ties resolve to the lowest index; best/second are the float32
+    canonical similarities widened to float64.
+    """
+    dev = _require_cuda(device)
+    C = _centers_array(centroids)
+    k = C.shape[0]
+    dc = device_corpus(data, dev)
+    cs = CenterState(k, data.dim, data.n, dev, False)
+    keep = cs.load(C, ctypes_void(torch.cuda.current_stream(dev).cuda_stream))
+    a = torch.empty(max(data.n, 1), dtype=torch.int32, device=dev)
+    best = torch.empty(max(data.n, 1), dtype=torch.float64, device=dev)
+    second = torch.empty_like(best)
+    _lib.call("spkm_predict", dc.struct, cs.struct, _ptr(a), _ptr(best), _ptr(second),
+              ctypes_void(torch.cuda.current_stream(dev).cuda_stream))
+    torch.cuda.current_stream(dev).synchronize()
+    del keep
+    return (a[:data.n].cpu().numpy().astype(np.int64), best[:data.n].cpu().numpy(), second[:data.n].cpu().numpy())
+
+
+def _sums_for(data: Dataset, a: np.ndarray, cs: CenterState, dev):
+    dc = device_corpus(data, dev)
+    at = torch.from_numpy(np.ascontiguousarray(a, np.int32)).to(dev)
+    b = Bounds(_ptr(at), None, None, 1)
+    sp = ctypes_void(torch.cuda.current_stream(dev).cuda_stream)
+    _lib.call("spkm_aggregate_sums", dc.struct, cs.struct, b, _ptr(cs.sums), _ptr(cs.counts), sp)
+    return at
+
+
+def compute_objective(data: Dataset, assignments, centroids, device=None) -> float:
+    """Sum_i <x_i, c_a(i)> (engine.py:123-127), as Sum_j <sums_j, c_j> in float64."""
+    dev = _require_cuda(device)
+    C = _centers_array(centroids)
+    cs = CenterState(C.shape[0], data.dim, data.n, dev, False)
+    sp = ctypes_void(torch.cuda.current_stream(dev).cuda_stream)
+    keep = cs.load(C, sp)
+    at = _sums_for(data, np.asarray(assignments), cs, dev)
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    _lib.call("spkm_objective", cs.struct, _ptr(cs.sums), _ptr(out), sp)
+    val = float(out.item())
+    del keep, at
+    return val
+
+
+def update_centers(data: Dataset, assignments, centroids: CentroidSet, prev_assignments=None,
+                   device=None) -> CentroidSet:
+    """Move centers for the given assignments (engine.py:163-189); mutates and returns.
+
+    Sums are rebuilt exactly on the device (fixed point) in both branches;
+    with ``prev_assignments`` only the clusters touched by moved points are
+    renormalised, as in the reference.
+    """
+    dev = _require_cuda(device)
+    a = np.asarray(assignments, dtype=np.int64)
+    k = centroids.k
+    cs = CenterState(k, data.dim, data.n, dev, False)
+    sp = ctypes_void(torch.cuda.current_stream(dev).cuda_stream)
+    keep = cs.load(centroids.centers, sp)
+    at = _sums_for(data, a, cs, dev)
+    if prev_assignments is None:
+        cs.touched.fill_(1)
+        all_c = True
+    else:
+        prev = np.asarray(prev_assignments, dtype=np.int64)
+        moved = np.nonzero(a != prev)[0]
+        t = np.zeros(k, np.int32)
+        t[prev[moved]] = 1
+        t[a[moved]] = 1
+        cs.touched.copy_(torch.from_numpy(t))
+        cs.touched_host = t
+        all_c = False
+    _lib.call("spkm_move_centers", cs.struct, int(all_c), sp)
+    work = PointState(1, k, "standard", dev)
+    _lib.call("spkm_finalize", cs.struct, work.work, int(all_c), 0, sp)
+    torch.cuda.current_stream(dev).synchronize()
+    prev_c = centroids.centers.copy()
+    centroids.centers = cs.host_centers()
+    centroids.sums = cs.host_sums()
+    centroids.counts = cs.counts.cpu().numpy()
+    centroids.drift = cs.drift.cpu().numpy()
+    changed = np.nonzero(cs.touched_host)[0] if prev_assignments is not None else np.arange(k)
+    if centroids.prev_centers is None:
+        centroids.prev_centers = prev_c
+    else:
+        centroids.prev_centers[changed] = prev_c[changed]
+    del keep, at
+    return centroids

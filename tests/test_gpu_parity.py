@@ -1,0 +1,80 @@
+"""GPU parity: the CUDA path (through the C ABI) vs the CPU oracle and vs itself.
+
+Contract (BASELINE.json north_star): final assignments identical wherever
+the oracle's best-vs-second margin exceeds 1e-5; objective within 1e-6
+relative; iteration count within +-1; every pruned variant EXACTLY equal to
+the GPU's own Lloyd (assignments, objective, per-iteration reassignments).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden_dataset, golden_names, golden_runs, load_golden
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ("standard", "elkan", "simp_elkan", "hamerly", "simp_hamerly")
+MARGIN = 1e-5
+OBJ_RTOL = 1e-6
+
+
+def check_vs_oracle(r, ref_assign, ref_obj, ref_iters, margin):
+    ok = margin > MARGIN
+    bad = np.nonzero((r.assignments != ref_assign) & ok)[0]
+    assert bad.size == 0, f"{bad.size} confident points differ, e.g. {bad[:5]}"
+    assert abs(r.objective - ref_obj) <= OBJ_RTOL * max(1.0, abs(ref_obj)), (r.objective, ref_obj)
+    assert abs(len(r.iterations) - ref_iters) <= 1, (len(r.iterations), ref_iters)
+
+
+@pytest.mark.parametrize("name", golden_names())
+def test_golden_parity_and_self_consistency(name, oracle_mod):
+    import paper_2107_04074_b200 as spk
+    z = load_golden(name)
+    data = golden_dataset(z)
+    base = {}
+    for key, v, k, seed, upd, mi in golden_runs(z):
+        r = spk.run(data, k, v, spk.SeedConfig(seed=seed), max_iter=mi, hamerly_update=upd)
+        if upd == "safe" and mi >= 50:
+            check_vs_oracle(r, z[key + "__assignments"], float(z[key + "__objective"][-1]),
+                            len(z[key + "__objective"]), z[key + "__margin"])
+        if upd != "safe":
+            continue
+        group = (k, seed, mi)
+        if group not in base:
+            base[group] = r
+        else:
+            b = base[group]
+            assert np.array_equal(r.assignments, b.assignments), (v, group)
+            assert r.objective == b.objective, (v, group)
+            assert len(r.iterations) == len(b.iterations), (v, group)
+            assert [s.reassignments for s in r.iterations] == [s.reassignments for s in b.iterations]
+            assert all(s.sim_count <= data.n * k for s in r.iterations)
+
+
+@pytest.mark.parametrize("k", [20, 100])
+def test_c2_full_size_parity(k, oracle_mod):
+    import paper_2107_04074_b200 as spk
+    from paper_2107_04074_b200 import synth
+    data = synth.config_dataset("C2")
+    X = oracle_mod.CSR(data.indptr, data.indices, data.data, data.dim)
+    ref = oracle_mod.run(X, k, "standard", seed=2, max_iter=50)
+    margin = oracle_mod.margins(X, ref["centers"])
+    base = None
+    for v in VARIANTS:
+        r = spk.run(data, k, v, spk.SeedConfig(seed=2), max_iter=50)
+        if base is None:
+            base = r
+            check_vs_oracle(r, ref["assignments"], ref["objective"][-1], ref["iterations"], margin)
+        else:
+            assert np.array_equal(r.assignments, base.assignments), v
+            assert r.objective == base.objective, v
+
+
+def test_c1_parity_all_variants(oracle_mod):
+    import paper_2107_04074_b200 as spk
+    z = load_golden("C1")
+    data = golden_dataset(z)
+    for key, v, k, seed, upd, mi in golden_runs(z):
+        r = spk.run(data, k, v, spk.SeedConfig(seed=seed), max_iter=mi)
+        check_vs_oracle(r, z[key + "__assignments"], float(z[key + "__objective"][-1]),
+                        len(z[key + "__objective"]), z[key + "__margin"])

@@ -208,6 +208,7 @@ def main_ours(args):
     else:
         rows = (0, data.n)
     corpus = DeviceCorpus(data, dev, rows=rows)
+    cent_dev = torch.from_numpy(np.ascontiguousarray(cents0.centers)).to(dev)   # resident seed centers
     torch.cuda.synchronize()
 
     def fit_all(corpus_, tag=None):
@@ -215,7 +216,7 @@ def main_ours(args):
         per = {}
         for v in variants:
             comm = Exchange(k, data.dim, dev) if world > 1 else None
-            r = run(data, k, v, max_iter=args.max_iter, device=dev, corpus=corpus_, init_centers=cents0.centers,
+            r = run(data, k, v, max_iter=args.max_iter, device=dev, corpus=corpus_, init_centers=cent_dev,
                     comm=comm, n_total=data.n, seed_indices=cents0.seed_indices)
             its += len(r.iterations)
             sims += r.total_sims
@@ -292,7 +293,7 @@ def main_ours(args):
     e2e_val = its_tot / (float(e2e_ms.item()) / 1e3)
 
     # ---- instrumented pass: per-entry-point event times -> roofline ----
-    roof = roofline(args, data, corpus, cents0, dev, world)
+    roof = roofline(args, data, corpus, cents0, cent_dev, dev, world)
 
     if rank != 0:
         dist.destroy_process_group()
@@ -318,7 +319,7 @@ def main_ours(args):
         dist.destroy_process_group()
 
 
-def roofline(args, data, corpus, cents0, dev, world):
+def roofline(args, data, corpus, cents0, cent_dev, dev, world):
     """Time every entry point with CUDA events over one step; bytes from SURVEY.md §8(d)."""
     import torch
     from paper_2107_04074_b200 import _lib
@@ -333,7 +334,7 @@ def roofline(args, data, corpus, cents0, dev, world):
         for v in args.variants.split(","):
             prof.tag = v
             comm = Exchange(k, data.dim, dev) if world > 1 else None
-            r = run(data, k, v, max_iter=args.max_iter, device=dev, corpus=corpus, init_centers=cents0.centers,
+            r = run(data, k, v, max_iter=args.max_iter, device=dev, corpus=corpus, init_centers=cent_dev,
                     comm=comm, n_total=data.n, seed_indices=cents0.seed_indices)
             its = r.iterations
             ku = (k + 3) // 4 * 4

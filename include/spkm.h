@@ -77,14 +77,17 @@ typedef struct spkm_centers {
     float *ct32;             /* [d*kp] term-major float32 copy (pad = 0)    */
     long long *sums;         /* [k*d] exact fixed-point member sums         */
     long long *counts;       /* [k]                                         */
-    double *drift;           /* [k] p(j) = <c_new, c_old>                   */
+    double *drift;           /* [k] p(j) = <c_new, c_old> = 1 - chord^2/2    */
+    double *sinp;            /* [k] upper bound on sin(angle(c_new, c_old))  */
     int32_t *touched;        /* [k] cluster changed this iteration          */
     double *objc;            /* [k] <sums_j, c_j> per cluster               */
-    double *part;            /* [k*nchunk*2] scratch partial reductions     */
+    double *part;            /* [spkm_center_scratch_doubles] partial sums  */
     double *norm;            /* [k] scratch: |sums_j|                       */
     float *cc;               /* [k*k] half-angle center cosines, rounded up */
     float *s;                /* [k]   row max of cc (diag excluded)         */
-    double *hstat;           /* [4]   owner, p_min, p_min2 (Hamerly)        */
+    double *hstat;           /* [8]   owner, p_min, p_min2, owner_s, smax, smax2 */
+    int32_t *tlist;          /* [k]   scratch: touched cluster list         */
+    int32_t *tcount;         /* [1]   scratch: its length                   */
 } spkm_centers;
 
 /* Per-point bounds of the local shard. */
@@ -119,6 +122,8 @@ int spkm_abi_version(void);
 const char *spkm_last_error(void);
 /* number of chunks the center kernels split d into (size of centers.part) */
 int64_t spkm_center_chunks(int64_t d);
+/* doubles of scratch the center kernels need (centers.part) */
+int64_t spkm_center_scratch_doubles(int64_t k, int64_t d);
 /* padded k (kp) of the term-major copy for a given k */
 int64_t spkm_padded_k(int64_t k);
 
@@ -161,7 +166,7 @@ int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream);
 int64_t spkm_gram_tiles(int64_t k, int32_t *host_pairs);
 int64_t spkm_gram_scratch_doubles(int64_t k, int64_t d);
 int spkm_center_thresholds(const spkm_centers *C, double *gram_scratch, const void *tile_pairs,
-                              void *stream);
+                           int full, void *stream);
 /* Objective, all-p==1 flag, Hamerly owner/p_min/p_min2, stats; clears
  * touched.  sims_extra is added to the sims counter (host-known counts). */
 int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra,

@@ -37,8 +37,8 @@ class CSR(ctypes.Structure):
 class Centers(ctypes.Structure):
     _fields_ = [("k", c_i64), ("d", c_i64), ("kp", c_i64), ("scale_bits", c_i32), ("_pad", c_i32),
                 ("cent64", c_vp), ("ct32", c_vp), ("sums", c_vp), ("counts", c_vp), ("drift", c_vp),
-                ("touched", c_vp), ("objc", c_vp), ("part", c_vp), ("norm", c_vp), ("cc", c_vp),
-                ("s", c_vp), ("hstat", c_vp)]
+                ("sinp", c_vp), ("touched", c_vp), ("objc", c_vp), ("part", c_vp), ("norm", c_vp), ("cc", c_vp),
+                ("s", c_vp), ("hstat", c_vp), ("tlist", c_vp), ("tcount", c_vp)]
 
 
 class Bounds(ctypes.Structure):
@@ -76,7 +76,8 @@ _SIGS = {
     "spkm_move_centers": [_P(Centers), ctypes.c_int, c_vp],
     "spkm_gram_tiles": [c_i64, c_vp],
     "spkm_gram_scratch_doubles": [c_i64, c_i64],
-    "spkm_center_thresholds": [_P(Centers), c_vp, c_vp, c_vp],
+    "spkm_center_thresholds": [_P(Centers), c_vp, c_vp, ctypes.c_int, c_vp],
+    "spkm_center_scratch_doubles": [c_i64, c_i64],
     "spkm_finalize": [_P(Centers), _P(Work), ctypes.c_int, ctypes.c_longlong, c_vp],
     "spkm_predict": [_P(CSR), _P(Centers), c_vp, c_vp, c_vp, c_vp],
     "spkm_objective": [_P(Centers), c_vp, c_vp, c_vp],
@@ -89,13 +90,14 @@ _RESTYPES = {
     "spkm_padded_k": c_i64,
     "spkm_gram_tiles": c_i64,
     "spkm_gram_scratch_doubles": c_i64,
+    "spkm_center_scratch_doubles": c_i64,
 }
 
 # kernels each entry point launches (for the bench's gpu_launches count)
 KERNELS_PER_CALL = {
     "spkm_full_assign": 1, "spkm_hamerly_bounds": 1, "spkm_hamerly_tighten": 1, "spkm_hamerly_rescan": 1,
     "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
-    "spkm_move_centers": 3, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
+    "spkm_move_centers": 5, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1,
 }
 

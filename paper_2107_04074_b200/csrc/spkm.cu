@@ -341,11 +341,12 @@ __global__ void __launch_bounds__(256) k_row_pass(RowPassArgs A) {
 __global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *__restrict__ reps,
                                                         const int32_t *__restrict__ a, float *l, float *u,
                                                         const double *__restrict__ drift,
+                                                        const double *__restrict__ sinp,
                                                         const float *__restrict__ s_arr,
                                                         const double *__restrict__ hstat, int use_s, int naive,
                                                         int32_t *surv1, long long *ctr) {
-    const int owner = (int)hstat[0];
-    const double pmin = hstat[1], pmin2 = hstat[2];
+    const int owner = (int)hstat[0], owner_s = (int)hstat[3];
+    const double pmin = hstat[1], pmin2 = hstat[2], smax = hstat[4], smax2 = hstat[5];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t n_pad = (n + 31) & ~int64_t(31);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
@@ -353,22 +354,26 @@ __global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *
         if (i < n) {
             const int ai = a[i];
             const float lo = l[i];
-            const double pa = drift[ai];
+            const double sa = sinp[ai];
             float lf = lo;
-            if (pa != 1.0) {
-                lf = store_lower(d_lower_update((double)lo, pa));
+            if (sa != 0.0) {   // cos(theta_l + theta_p), theta_p from the chord bound
+                const double pa = drift[ai];
+                const double ln = (lo < -pa) ? -1.0 : d_clamp((double)lo * pa - d_sin((double)lo) * sa);
+                lf = store_lower(ln);
                 l[i] = lf;
             }
-            const double worst = (ai == owner) ? pmin2 : pmin;
+            const double worst_p = (ai == owner) ? pmin2 : pmin;
+            const double worst_s = (ai == owner_s) ? smax2 : smax;
             const float uo = u[i];
             float uf = uo;
-            if (naive) {
-                if (worst != 1.0) {
-                    uf = store_upper(d_cos_upper((double)uo, worst));
+            if (naive) {       // engine.py:299-303, deliberately unsound
+                if (worst_p != 1.0) {
+                    uf = store_upper(d_cos_upper((double)uo, worst_p));
                     u[i] = uf;
                 }
-            } else if (!(uo >= 0.f && worst == 1.0)) {
-                const double un = (uo >= 0.f && worst >= 0.0) ? d_hamerly_upper((double)uo, worst) : 1.0;
+            } else if (!(uo >= 0.f && worst_s == 0.0)) {   // engine.py:290-298
+                const double un = (uo >= 0.f && worst_p >= 0.0) ? d_clamp((double)uo + d_sin((double)uo) * worst_s)
+                                                                 : 1.0;
                 uf = store_upper(un);
                 u[i] = uf;
             }
@@ -423,6 +428,7 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
 __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const float *__restrict__ reps,
                                                       const int32_t *__restrict__ a, float *l, float *u,
                                                       int64_t ku, const double *__restrict__ drift,
+                                                      const double *__restrict__ sinp,
                                                       const float *__restrict__ cc,
                                                       const float *__restrict__ s_arr, int use_cc,
                                                       int32_t *surv1, long long *ctr) {
@@ -431,9 +437,12 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
     for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
         const int ai = a[i];
         const float lo = l[i];
-        const double pa = drift[ai];
+        const double sa = sinp[ai];
         float lf = lo;
-        if (pa != 1.0) lf = store_lower(d_lower_update((double)lo, pa));
+        if (sa != 0.0) {
+            const double pa = drift[ai];
+            lf = store_lower((lo < -pa) ? -1.0 : d_clamp((double)lo * pa - d_sin((double)lo) * sa));
+        }
         if (lane == 0 && lf != lo) l[i] = lf;
         const double eps = (double)reps[i];
         const double lb = (double)lf;
@@ -442,9 +451,10 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
         float *ui = u + i * ku;
         for (int j = lane; j < k; j += 32) {
             float uf = ui[j];
-            const double pj = drift[j];
-            if (pj != 1.0) {
-                const double nv = ((double)uf <= pj) ? d_cos_upper((double)uf, pj) : 1.0;
+            const double sj = sinp[j];
+            if (sj != 0.0) {   // engine.py:281-283 with the chord-based sine bound
+                const double pj = drift[j];
+                const double nv = ((double)uf <= pj) ? d_clamp((double)uf * pj + d_sin((double)uf) * sj) : 1.0;
                 uf = store_upper(nv);
                 ui[j] = uf;
             }
@@ -619,72 +629,185 @@ __device__ __forceinline__ double block_sum(double v, double *sh) {
     return r;  // valid in thread 0
 }
 
-// _move_centers pass 1 (engine.py:153-155): partial |sum_j|^2 per d-chunk.
+// ---------------------------------------------------- _move_centers pipeline
+// engine.py:142-160 for the touched clusters T (all clusters in iteration 1):
+//   list -> |sum_j|^2 partials -> norm_j -> write c_j (cent64 + term-major
+//   ct32 through a shared-memory transpose) with partial chord^2 and
+//   objective -> per-cluster reduction -> drift.
+// The drift is carried as (p_j, sinp_j): p_j = 1 - |c_new - c_old|^2 / 2
+// (exactly 1 for a bit-identical center) and sinp_j an UPPER bound on the
+// sine of the rotation angle computed from the chord (no cancellation near
+// p = 1, where sqrt(1 - p^2) would amplify float64 rounding).
+constexpr int kTileT = 256;          // terms per write tile
+constexpr int kTileJ = 32;           // clusters per write tile
+constexpr double kChordPad = 4e-10;  // |1 - |c|| <= d * 2^-53 for d <= 1e6, twice
+
+__global__ void k_touched_list(int64_t k, const int32_t *__restrict__ touched, int all, int32_t *tlist,
+                               int32_t *tcount) {
+    __shared__ int wsum[32];
+    __shared__ int base_s;
+    if (threadIdx.x == 0) base_s = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    for (int64_t j0 = 0; j0 < k; j0 += blockDim.x) {
+        const int64_t j = j0 + threadIdx.x;
+        const int f = (j < k) && (all || touched[j]);
+        const unsigned m = __ballot_sync(FULL, f);
+        if (lane == 0) wsum[w] = __popc(m);
+        __syncthreads();
+        int off = base_s;
+        for (int q = 0; q < w; ++q) off += wsum[q];
+        if (f) tlist[off + __popc(m & ((1u << lane) - 1u))] = (int32_t)j;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int t = 0;
+            for (int q = 0; q < nw; ++q) t += wsum[q];
+            base_s += t;
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) *tcount = base_s;
+}
+
 __global__ void __launch_bounds__(256) k_center_norm_part(int64_t d, int64_t nchunk,
                                                           const long long *__restrict__ sums,
-                                                          const int32_t *__restrict__ touched, int all,
-                                                          double inv_scale, double *part) {
+                                                          const int32_t *__restrict__ tlist,
+                                                          const int32_t *__restrict__ tcount, double inv_scale,
+                                                          double *part) {
     __shared__ double sh[8];
-    const int64_t j = blockIdx.y, c = blockIdx.x;
-    if (!all && !touched[j]) return;
+    const int64_t y = blockIdx.y, c = blockIdx.x;
+    if (y >= *tcount) return;
+    const int64_t j = tlist[y];
     const int64_t t0 = c * kCenterChunk, t1 = min(d, t0 + kCenterChunk);
     const long long *sj = sums + j * d;
     double acc = 0.0;
     for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-        const double v = (double)sj[t] * inv_scale;
-        acc = fma(v, v, acc);
-    }
-    const double r = block_sum<256>(acc, sh);
-    if (threadIdx.x == 0) part[(j * nchunk + c) * 2] = r;
-}
-
-// norm_j = sqrt(sum of partials in chunk order); -1 marks "keep the center"
-// (empty cluster or |sum| < 1e-12, engine.py:153-157).
-__global__ void k_center_norm_final(int64_t k, int64_t nchunk, const long long *__restrict__ counts,
-                                    const int32_t *__restrict__ touched, int all, const double *part,
-                                    double *norm) {
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= k) return;
-    if (!all && !touched[j]) return;
-    double sq = 0.0;
-    for (int64_t c = 0; c < nchunk; ++c) sq += part[(j * nchunk + c) * 2];
-    const double nrm = sqrt(sq);
-    norm[j] = (counts[j] == 0 || nrm < kZeroSumEps) ? -1.0 : nrm;
-}
-
-// _move_centers pass 2 (engine.py:158-160): c = sum/|sum|, partial <c,old>
-// and partial objective <sum, c>; writes cent64 and the ct32 column.
-__global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int64_t nchunk,
-                                                      const long long *__restrict__ sums,
-                                                      const int32_t *__restrict__ touched, int all,
-                                                      double inv_scale, const double *__restrict__ norm,
-                                                      double *cent64, float *ct32, double *part) {
-    __shared__ double sh[8];
-    const int64_t j = blockIdx.y, c = blockIdx.x;
-    if (!all && !touched[j]) return;
-    const int64_t t0 = c * kCenterChunk, t1 = min(d, t0 + kCenterChunk);
-    const long long *sj = sums + j * d;
-    double *cj = cent64 + j * d;
-    const double nrm = norm[j];
-    double dt = 0.0, ob = 0.0;
-    if (nrm < 0.0) {
-        for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) ob = fma((double)sj[t] * inv_scale, cj[t], ob);
-    } else {
-        for (int64_t t = t0 + threadIdx.x; t < t1; t += blockDim.x) {
-            const double v = (double)sj[t] * inv_scale;
-            const double nv = v / nrm;
-            const double old = cj[t];
-            dt = fma(nv, old, dt);
-            ob = fma(v, nv, ob);
-            cj[t] = nv;
-            ct32[t * kp + j] = (float)nv;
+        const long long q = sj[t];
+        if (q) {
+            const double v = (double)q * inv_scale;
+            acc = fma(v, v, acc);
         }
     }
-    const double rdt = block_sum<256>(dt, sh);
+    const double r = block_sum<256>(acc, sh);
+    if (threadIdx.x == 0) part[y * nchunk + c] = r;
+}
+
+// norm_j = sqrt(sum of partials, fixed order); -1 = keep the old center
+// (empty cluster or |sum| < 1e-12, engine.py:153-157).
+__global__ void __launch_bounds__(256) k_center_norm_final(int64_t nchunk, const long long *__restrict__ counts,
+                                                           const int32_t *__restrict__ tlist,
+                                                           const int32_t *__restrict__ tcount,
+                                                           const double *__restrict__ part, double *norm) {
+    __shared__ double sh[8];
+    const int64_t y = blockIdx.x;
+    if (y >= *tcount) return;
+    double acc = 0.0;
+    for (int64_t c = threadIdx.x; c < nchunk; c += blockDim.x) acc += part[y * nchunk + c];
+    const double sq = block_sum<256>(acc, sh);
+    if (threadIdx.x == 0) {
+        const int j = tlist[y];
+        const double nrm = sqrt(sq);
+        norm[j] = (counts[j] == 0 || nrm < kZeroSumEps) ? -1.0 : nrm;
+    }
+}
+
+// Write tile: kTileJ listed clusters x kTileT terms.  Warp w owns clusters
+// 4w..4w+3 of the tile; lanes stride the terms (coalesced int64/float64
+// rows).  The float32 values are transposed through shared memory so each
+// ct32 row segment (kTileJ consecutive clusters) is one coalesced store.
+__global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int64_t ntile,
+                                                      const long long *__restrict__ sums,
+                                                      const int32_t *__restrict__ tlist,
+                                                      const int32_t *__restrict__ tcount, double inv_scale,
+                                                      const double *__restrict__ norm, double *cent64, float *ct32,
+                                                      double *part) {
+    __shared__ float tile[kTileT][kTileJ + 1];
+    __shared__ int js[kTileJ];
+    const int64_t nT = *tcount;
+    const int64_t y0 = (int64_t)blockIdx.y * kTileJ;
+    if (y0 >= nT) return;
+    const int64_t t0 = (int64_t)blockIdx.x * kTileT;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (threadIdx.x < kTileJ) js[threadIdx.x] = (y0 + threadIdx.x < nT) ? tlist[y0 + threadIdx.x] : -1;
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int jr = w * 4 + r;
+        const int j = js[jr];
+        double ch = 0.0, ob = 0.0;
+        if (j >= 0) {
+            const double nrm = norm[j];
+            const long long *sj = sums + (int64_t)j * d;
+            double *cj = cent64 + (int64_t)j * d;
+            for (int q = lane; q < kTileT; q += 32) {
+                const int64_t t = t0 + q;
+                float f = 0.f;
+                if (t < d) {
+                    const double v = (double)sj[t] * inv_scale;
+                    const double old = cj[t];
+                    if (nrm < 0.0) {
+                        ob = fma(v, old, ob);
+                        f = (float)old;
+                    } else {
+                        const double nv = v / nrm;
+                        const double df = nv - old;
+                        ch = fma(df, df, ch);
+                        ob = fma(v, nv, ob);
+                        if (nv != old) cj[t] = nv;
+                        f = (float)nv;
+                    }
+                }
+                tile[q][jr] = f;
+            }
+        } else {
+            for (int q = lane; q < kTileT; q += 32) tile[q][jr] = 0.f;
+        }
+        for (int o = 16; o; o >>= 1) {
+            ch += __shfl_down_sync(FULL, ch, o);
+            ob += __shfl_down_sync(FULL, ob, o);
+        }
+        if (lane == 0 && j >= 0) {
+            part[((y0 + jr) * ntile + blockIdx.x) * 2] = ch;
+            part[((y0 + jr) * ntile + blockIdx.x) * 2 + 1] = ob;
+        }
+    }
+    __syncthreads();
+    // transpose out: warp w handles terms w, w+8, ...; lane = cluster slot
+    const int j = js[lane];
+    for (int q = w; q < kTileT; q += 8) {
+        const int64_t t = t0 + q;
+        if (t < d && j >= 0) ct32[t * kp + j] = tile[q][lane];
+    }
+}
+
+// per touched cluster: chord^2 -> (p, sin bound), objective term.
+__global__ void __launch_bounds__(256) k_center_reduce(int64_t ntile, const int32_t *__restrict__ tlist,
+                                                       const int32_t *__restrict__ tcount,
+                                                       const double *__restrict__ part,
+                                                       const double *__restrict__ norm, double *drift,
+                                                       double *sinp, double *objc) {
+    __shared__ double sh[8];
+    const int64_t y = blockIdx.x;
+    if (y >= *tcount) return;
+    double ch = 0.0, ob = 0.0;
+    for (int64_t c = threadIdx.x; c < ntile; c += blockDim.x) {
+        ch += part[(y * ntile + c) * 2];
+        ob += part[(y * ntile + c) * 2 + 1];
+    }
+    const double rch = block_sum<256>(ch, sh);
     const double rob = block_sum<256>(ob, sh);
     if (threadIdx.x == 0) {
-        part[(j * nchunk + c) * 2] = rdt;
-        part[(j * nchunk + c) * 2 + 1] = rob;
+        const int j = tlist[y];
+        objc[j] = rob;
+        if (norm[j] < 0.0 || rch == 0.0) {
+            drift[j] = 1.0;
+            sinp[j] = 0.0;
+        } else {
+            const double chord = sqrt(rch);
+            drift[j] = d_clamp(1.0 - 0.5 * rch);
+            const double s = chord * sqrt(fmax(0.0, 1.0 - 0.25 * rch));
+            sinp[j] = fmin(1.0, s * (1.0 + 1e-12) + kChordPad);
+        }
     }
 }
 
@@ -714,95 +837,87 @@ __global__ void k_objective_final(int64_t k, int64_t nchunk, const double *__res
 }
 
 // ------------------------------------------------------------ finalize
-// drift (engine.py:149,160), objective (engine.py:326), convergence inputs
-// (engine.py:335-337), Hamerly owner/p_min/p_min2 (engine.py:285-289).
-__global__ void __launch_bounds__(1024) k_finalize(int64_t k, int64_t nchunk, int all, int32_t *touched,
-                                                   const double *__restrict__ part,
-                                                   const double *__restrict__ norm, double *drift,
-                                                   double *objc, double *hstat, long long *ctr,
-                                                   double *stats, long long sims_extra) {
-    __shared__ double sh[32];
-    __shared__ double shv[32];
-    __shared__ int shi[32];
-    double allone_local = 0.0, ntouched = 0.0;
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
-        if (all || touched[j]) {
-            double dt = 0.0, ob = 0.0;
-            for (int64_t c = 0; c < nchunk; ++c) {
-                dt += part[(j * nchunk + c) * 2];
-                ob += part[(j * nchunk + c) * 2 + 1];
-            }
-            drift[j] = (norm[j] < 0.0) ? 1.0 : d_clamp(dt);
-            objc[j] = ob;
-            ntouched += 1.0;
-        } else {
-            drift[j] = 1.0;
-        }
-        if (drift[j] != 1.0) allone_local = 1.0;
-        touched[j] = 0;
+// drift of untouched clusters = 1 (engine.py:149), objective
+// (engine.py:326), convergence inputs (engine.py:335-337), Hamerly
+// aggregation (engine.py:285-289): owner = first argmin p, p_min, p_min2,
+// plus the sine bounds smax = max_j sinp_j and smax2 = max over j != owner_s
+// (owner_s = first argmax sinp).  hstat = {owner, p_min, p_min2, owner_s,
+// smax, smax2}.
+struct MinI {
+    double v;
+    int i;
+};
+__device__ __forceinline__ MinI min_first(MinI a, MinI b) { return (b.v < a.v || (b.v == a.v && b.i < a.i)) ? b : a; }
+__device__ __forceinline__ MinI block_min_first(MinI x, MinI *sh) {
+    for (int o = 16; o; o >>= 1) {
+        MinI y{__shfl_down_sync(FULL, x.v, o), __shfl_down_sync(FULL, x.i, o)};
+        x = min_first(x, y);
     }
-    __syncthreads();
-    // objective: fixed-order strided partials then a fixed tree
-    double ob = 0.0;
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) ob += objc[j];
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    for (int o = 16; o; o >>= 1) ob += __shfl_down_sync(FULL, ob, o);
-    if (lane == 0) sh[w] = ob;
-    // any drift != 1 and touched count
-    double notone = allone_local, nt = ntouched;
-    for (int o = 16; o; o >>= 1) {
-        notone = fmax(notone, __shfl_down_sync(FULL, notone, o));
-        nt += __shfl_down_sync(FULL, nt, o);
-    }
-    __shared__ double sh1[32], sh2[32];
-    if (lane == 0) {
-        sh1[w] = notone;
-        sh2[w] = nt;
-    }
-    // Hamerly: owner = first index of min drift; p_min2 = min over the rest
-    double bv = INFINITY;
-    int bi = 0x7fffffff;
+    __syncthreads();
+    if (lane == 0) sh[w] = x;
+    __syncthreads();
+    MinI r = sh[0];
+    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) r = min_first(r, sh[q]);
+    return r;
+}
+
+__global__ void __launch_bounds__(1024) k_finalize(int64_t k, int32_t *touched, const int32_t *__restrict__ tlist,
+                                                   const int32_t *__restrict__ tcount, double *drift, double *sinp,
+                                                   const double *__restrict__ objc, double *hstat, long long *ctr,
+                                                   double *stats, long long sims_extra, int all) {
+    __shared__ double sh[32];
+    __shared__ MinI shm[32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    // untouched clusters: p = 1 (touched ones were set by k_center_reduce)
     for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
-        const double v = drift[j];
-        if (v < bv || (v == bv && (int)j < bi)) {
-            bv = v;
-            bi = (int)j;
+        if (!(all || touched[j])) {
+            drift[j] = 1.0;
+            sinp[j] = 0.0;
         }
-    }
-    for (int o = 16; o; o >>= 1) {
-        const double ov = __shfl_down_sync(FULL, bv, o);
-        const int oi = __shfl_down_sync(FULL, bi, o);
-        if (ov < bv || (ov == bv && oi < bi)) {
-            bv = ov;
-            bi = oi;
-        }
-    }
-    if (lane == 0) {
-        shv[w] = bv;
-        shi[w] = bi;
     }
     __syncthreads();
-    __shared__ int owner_s;
+    double ob = 0.0, notone = 0.0;
+    MinI pm{INFINITY, 0x7fffffff}, sm{INFINITY, 0x7fffffff};
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+        ob += objc[j];
+        const double p = drift[j];
+        if (p != 1.0) notone = 1.0;
+        pm = min_first(pm, MinI{p, (int)j});
+        sm = min_first(sm, MinI{-sinp[j], (int)j});
+    }
+    for (int o = 16; o; o >>= 1) {
+        ob += __shfl_down_sync(FULL, ob, o);
+        notone = fmax(notone, __shfl_down_sync(FULL, notone, o));
+    }
+    if (lane == 0) sh[w] = ob;
+    __syncthreads();
+    double tot = 0.0;
+    for (int q = 0; q < nw; ++q) tot += sh[q];
+    __syncthreads();
+    if (lane == 0) sh[w] = notone;
+    __syncthreads();
+    double no = 0.0;
+    for (int q = 0; q < nw; ++q) no = fmax(no, sh[q]);
+    const MinI own = block_min_first(pm, shm);
+    const MinI owns = block_min_first(sm, shm);
+    MinI pm2{INFINITY, 0x7fffffff}, sm2{INFINITY, 0x7fffffff};
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+        if ((int)j != own.i) pm2 = min_first(pm2, MinI{drift[j], (int)j});
+        if ((int)j != owns.i) sm2 = min_first(sm2, MinI{-sinp[j], (int)j});
+    }
+    const MinI own2 = block_min_first(pm2, shm);
+    const MinI owns2 = block_min_first(sm2, shm);
     if (threadIdx.x == 0) {
-        const int nw = blockDim.x >> 5;
-        double tot = 0.0, no = 0.0, ntt = 0.0;
-        double mv = INFINITY;
-        int mi = 0x7fffffff;
-        for (int q = 0; q < nw; ++q) {
-            tot += sh[q];
-            no = fmax(no, sh1[q]);
-            ntt += sh2[q];
-            if (shv[q] < mv || (shv[q] == mv && shi[q] < mi)) {
-                mv = shv[q];
-                mi = shi[q];
-            }
-        }
-        owner_s = mi;
-        hstat[0] = (double)mi;
-        hstat[1] = mv;
+        hstat[0] = (double)own.i;
+        hstat[1] = own.v;
+        hstat[2] = (k > 1) ? own2.v : 1.0;
+        hstat[3] = (double)owns.i;
+        hstat[4] = -owns.v;
+        hstat[5] = (k > 1) ? -owns2.v : 0.0;
         stats[SPKM_ST_OBJECTIVE] = tot;
         stats[SPKM_ST_ALLONE] = (no == 0.0) ? 1.0 : 0.0;
-        stats[SPKM_ST_TOUCHED] = ntt;
+        stats[SPKM_ST_TOUCHED] = (double)*tcount;
         stats[SPKM_ST_SIMS] = (double)(ctr[SPKM_CTR_SIMS] + sims_extra);
         stats[SPKM_ST_REASSIGN] = (double)ctr[SPKM_CTR_MOVES];
         stats[SPKM_ST_SURV1] = (double)ctr[SPKM_CTR_SURV1];
@@ -810,39 +925,44 @@ __global__ void __launch_bounds__(1024) k_finalize(int64_t k, int64_t nchunk, in
         stats[SPKM_ST_NNZ_TIGHTEN] = (double)ctr[SPKM_CTR_NNZ_TIGHTEN];
         stats[SPKM_ST_NNZ_RESCAN] = (double)ctr[SPKM_CTR_NNZ_RESCAN];
         stats[SPKM_ST_NNZ_ELKAN] = (double)ctr[SPKM_CTR_NNZ_ELKAN];
-    }
-    __syncthreads();
-    const int owner = owner_s;
-    bv = INFINITY;
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x)
-        if ((int)j != owner) bv = fmin(bv, drift[j]);
-    for (int o = 16; o; o >>= 1) bv = fmin(bv, __shfl_down_sync(FULL, bv, o));
-    __syncthreads();
-    if (lane == 0) shv[w] = bv;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double mv = INFINITY;
-        for (int q = 0; q < (int)(blockDim.x >> 5); ++q) mv = fmin(mv, shv[q]);
-        hstat[2] = (k > 1) ? mv : 1.0;
         for (int q = 0; q < 8; ++q) ctr[q] = 0;
     }
+    __syncthreads();
+    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) touched[j] = 0;
 }
 
 // ---------------------------------------------------------- center thresholds
-// engine._center_thresholds (engine.py:192-198): split-d float64 Gram tiles.
+// engine._center_thresholds (engine.py:192-198): float64 Gram over the
+// upper-triangle 32x32 tiles, split over d; a tile is skipped when neither
+// of its cluster ranges moved since the last call (cc stays valid).
 constexpr int GT = 32;   // output tile
-constexpr int GK = 16;   // d step
-__global__ void __launch_bounds__(256) k_gram_part(int64_t k, int64_t d, int64_t dsplit,
-                                                   const double *__restrict__ C, const int2 *__restrict__ tiles,
-                                                   double *gpart) {
+constexpr int GK = 32;   // d step
+__global__ void __launch_bounds__(64) k_gram_part(int64_t k, int64_t d, int64_t dsplit,
+                                                  const double *__restrict__ C, const int2 *__restrict__ tiles,
+                                                  const double *__restrict__ sinp, int full, double *gpart) {
     __shared__ double As[GK][GT + 1];
     __shared__ double Bs[GK][GT + 1];
+    __shared__ int need;
     const int2 tl = tiles[blockIdx.x];
     const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
+    if (threadIdx.x == 0) {
+        int nd = full;
+        for (int q = 0; q < GT && !nd; ++q) {
+            if (a0 + q < k && sinp[a0 + q] != 0.0) nd = 1;
+            if (j0 + q < k && sinp[j0 + q] != 0.0) nd = 1;
+        }
+        need = nd;
+    }
+    __syncthreads();
+    if (!need) return;
     const int64_t per = (d + dsplit - 1) / dsplit;
     const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
-    const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;  // 32 x 8
-    double acc[4] = {0, 0, 0, 0};
+    const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;   // 8 x 8 threads, 4x4 outputs each
+    double acc[4][4];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) acc[r][s] = 0.0;
     for (int64_t tb = t0; tb < t1; tb += GK) {
         for (int e = threadIdx.x; e < GK * GT; e += blockDim.x) {
             const int r = e / GK, cidx = e % GK;
@@ -852,22 +972,31 @@ __global__ void __launch_bounds__(256) k_gram_part(int64_t k, int64_t d, int64_t
             Bs[cidx][r] = (jr < k && t < t1) ? C[jr * d + t] : 0.0;
         }
         __syncthreads();
-#pragma unroll
+#pragma unroll 8
         for (int c = 0; c < GK; ++c) {
-            const double b = Bs[c][tx];
+            double av[4], bv[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q) acc[q] = fma(As[c][ty + 8 * q], b, acc[q]);
+            for (int r = 0; r < 4; ++r) av[r] = As[c][ty * 4 + r];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) bv[s] = Bs[c][tx * 4 + s];
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int s = 0; s < 4; ++s) acc[r][s] = fma(av[r], bv[s], acc[r][s]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int64_t ar = a0 + ty + 8 * q, jr = j0 + tx;
-        if (ar < k && jr < k) gpart[((int64_t)blockIdx.y * k + ar) * k + jr] = acc[q];
-    }
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+        for (int s = 0; s < 4; ++s) {
+            const int64_t ar = a0 + ty * 4 + r, jr = j0 + tx * 4 + s;
+            if (ar < k && jr < k) gpart[((int64_t)blockIdx.y * k + ar) * k + jr] = acc[r][s];
+        }
 }
 
-__global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict__ gpart, float *cc) {
+__global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict__ gpart,
+                             const double *__restrict__ sinp, int full, float *cc) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= k * k) return;
     const int64_t a = e / k, j = e % k;
@@ -875,6 +1004,16 @@ __global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict
     if (a == j) {
         cc[e] = -1.f;
         return;
+    }
+    // recompute only where the tile was recomputed (same predicate as k_gram_part)
+    if (!full) {
+        const int64_t ta = a / GT * GT, tj = j / GT * GT;
+        int nd = 0;
+        for (int q = 0; q < GT && !nd; ++q) {
+            if (ta + q < k && sinp[ta + q] != 0.0) nd = 1;
+            if (tj + q < k && sinp[tj + q] != 0.0) nd = 1;
+        }
+        if (!nd) return;
     }
     double g = 0.0;
     for (int64_t y = 0; y < dsplit; ++y) g += gpart[(y * k + a) * k + j];
@@ -1007,7 +1146,8 @@ int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B
                         int naive, void *stream) {
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 256);
-    k_hamerly_bounds<<<grid, 256, 0, S(stream)>>>(X->n, X->row_eps, B->a, B->l, B->u, C->drift, C->s, C->hstat,
+    k_hamerly_bounds<<<grid, 256, 0, S(stream)>>>(X->n, X->row_eps, B->a, B->l, B->u, C->drift, C->sinp, C->s,
+                                                  C->hstat,
                                                   use_s, naive, W->surv1, W->ctr);
     CHECK_LAUNCH("hamerly_bounds");
     return 0;
@@ -1045,7 +1185,7 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
     k_elkan_bounds<<<grid, 256, 0, S(stream)>>>(X->n, (int)C->k, X->row_eps, B->a, B->l, B->u, B->ku, C->drift,
-                                                C->cc, C->s, use_cc, W->surv1, W->ctr);
+                                                C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr);
     CHECK_LAUNCH("elkan_bounds");
     return 0;
 }
@@ -1087,25 +1227,35 @@ int spkm_apply_moves(const spkm_csr *X, const spkm_centers *C, const spkm_bounds
     return 0;
 }
 
+int64_t spkm_center_scratch_doubles(int64_t k, int64_t d) {
+    const int64_t nch = spkm_center_chunks(d), ntile = (d + kTileT - 1) / kTileT;
+    return k * (nch > 2 * ntile ? nch : 2 * ntile);
+}
+
 int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
     cudaStream_t st = S(stream);
     const int64_t nch = spkm_center_chunks(C->d);
+    const int64_t ntile = (C->d + kTileT - 1) / kTileT;
     const double inv = ldexp(1.0, -C->scale_bits);
-    dim3 grid((unsigned)nch, (unsigned)C->k);
-    k_center_norm_part<<<grid, 256, 0, st>>>(C->d, nch, C->sums, C->touched, all_clusters, inv, C->part);
+    k_touched_list<<<1, 1024, 0, st>>>(C->k, C->touched, all_clusters, C->tlist, C->tcount);
+    CHECK_LAUNCH("touched_list");
+    k_center_norm_part<<<dim3((unsigned)nch, (unsigned)C->k), 256, 0, st>>>(C->d, nch, C->sums, C->tlist, C->tcount,
+                                                                           inv, C->part);
     CHECK_LAUNCH("center_norm_part");
-    k_center_norm_final<<<(unsigned)((C->k + 255) / 256), 256, 0, st>>>(C->k, nch, C->counts, C->touched,
-                                                                       all_clusters, C->part, C->norm);
+    k_center_norm_final<<<(unsigned)C->k, 256, 0, st>>>(nch, C->counts, C->tlist, C->tcount, C->part, C->norm);
     CHECK_LAUNCH("center_norm_final");
-    k_center_write<<<grid, 256, 0, st>>>(C->d, C->kp, nch, C->sums, C->touched, all_clusters, inv, C->norm,
-                                         C->cent64, C->ct32, C->part);
+    k_center_write<<<dim3((unsigned)ntile, (unsigned)((C->k + kTileJ - 1) / kTileJ)), 256, 0, st>>>(
+        C->d, C->kp, ntile, C->sums, C->tlist, C->tcount, inv, C->norm, C->cent64, C->ct32, C->part);
     CHECK_LAUNCH("center_write");
+    k_center_reduce<<<(unsigned)C->k, 256, 0, st>>>(ntile, C->tlist, C->tcount, C->part, C->norm, C->drift, C->sinp,
+                                                   C->objc);
+    CHECK_LAUNCH("center_reduce");
     return 0;
 }
 
 int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra, void *stream) {
-    k_finalize<<<1, 1024, 0, S(stream)>>>(C->k, spkm_center_chunks(C->d), all_clusters, C->touched, C->part, C->norm,
-                                          C->drift, C->objc, C->hstat, W->ctr, W->stats, sims_extra);
+    k_finalize<<<1, 1024, 0, S(stream)>>>(C->k, C->touched, C->tlist, C->tcount, C->drift, C->sinp, C->objc, C->hstat,
+                                          W->ctr, W->stats, sims_extra, all_clusters);
     CHECK_LAUNCH("finalize");
     return 0;
 }
@@ -1113,8 +1263,8 @@ int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long lo
 int64_t spkm_gram_dsplit(int64_t k, int64_t d) {
     const int64_t tk = (k + GT - 1) / GT;
     const int64_t tiles = tk * (tk + 1) / 2;
-    int64_t ds = (2 * (int64_t)num_sms() + tiles - 1) / tiles;
-    const int64_t maxds = (d + 511) / 512;
+    int64_t ds = (4 * (int64_t)num_sms() + tiles - 1) / tiles;
+    const int64_t maxds = (d + 1023) / 1024;
     if (ds > maxds) ds = maxds;
     if (ds < 1) ds = 1;
     return ds;
@@ -1122,16 +1272,16 @@ int64_t spkm_gram_dsplit(int64_t k, int64_t d) {
 
 int64_t spkm_gram_scratch_doubles(int64_t k, int64_t d) { return spkm_gram_dsplit(k, d) * k * k; }
 
-int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *tiles_ptr, void *stream) {
+int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *tiles_ptr, int full, void *stream) {
     const int2 *tiles_dev = static_cast<const int2 *>(tiles_ptr);
     cudaStream_t st = S(stream);
     const int64_t tk = (C->k + GT - 1) / GT;
     const int64_t ntiles = tk * (tk + 1) / 2;
     const int64_t ds = spkm_gram_dsplit(C->k, C->d);
     dim3 grid((unsigned)ntiles, (unsigned)ds);
-    k_gram_part<<<grid, 256, 0, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, gpart);
+    k_gram_part<<<grid, 64, 0, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart);
     CHECK_LAUNCH("gram_part");
-    k_gram_final<<<(unsigned)((C->k * C->k + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->cc);
+    k_gram_final<<<(unsigned)((C->k * C->k + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, C->cc);
     CHECK_LAUNCH("gram_final");
     k_row_max<<<(unsigned)((C->k + 255) / 256), 256, 0, st>>>(C->k, C->cc, C->s);
     CHECK_LAUNCH("row_max");

@@ -68,6 +68,52 @@ class CentroidSet:
                    prev_centers=centers.copy(), drift=np.ones(k), seed_indices=idx)
 
 
+class DeviceCentroidSet:
+    """Result centers that stay in HBM until read (same attributes as CentroidSet).
+
+    ``centers``/``sums``/``counts``/``drift`` are copied to the host on first
+    access; ``device_centers`` exposes the float64 device tensor directly.
+    """
+
+    def __init__(self, C: "CenterState", seed_indices=None):
+        self._C = C
+        self.seed_indices = seed_indices
+        self.prev_centers = None
+        self._cache = {}
+
+    @property
+    def k(self) -> int:
+        return self._C.k
+
+    @property
+    def device_centers(self):
+        return self._C.cent64.view(self._C.k, self._C.d)
+
+    def _get(self, name, fn):
+        if name not in self._cache:
+            self._cache[name] = fn()
+        return self._cache[name]
+
+    @property
+    def centers(self) -> np.ndarray:
+        return self._get("centers", self._C.host_centers)
+
+    @property
+    def sums(self) -> np.ndarray:
+        return self._get("sums", self._C.host_sums)
+
+    @property
+    def counts(self) -> np.ndarray:
+        return self._get("counts", lambda: self._C.counts.cpu().numpy())
+
+    @property
+    def drift(self) -> np.ndarray:
+        return self._get("drift", lambda: self._C.drift.cpu().numpy())
+
+    def to_host(self) -> CentroidSet:
+        return CentroidSet(self.centers, self.sums, self.counts, None, self.drift, self.seed_indices)
+
+
 @dataclass
 class BoundsState:
     """Bounds handed to debug hooks (engine.py:61-69); host copies of device state."""
@@ -184,31 +230,41 @@ class CenterState:
         self.scale_bits = scale_bits_for(n_total)
         dev = device
         f64 = dict(dtype=torch.float64, device=dev)
-        self.cent64 = torch.zeros(k * d, **f64)
+        self.cent64 = torch.empty(k * d, **f64)
         self.ct32 = torch.zeros(d * self.kp, dtype=torch.float32, device=dev)
-        self.sums = torch.zeros(k * d, dtype=torch.int64, device=dev)
+        self.sums = torch.empty(k * d, dtype=torch.int64, device=dev)
         self.counts = torch.zeros(k, dtype=torch.int64, device=dev)
         self.drift = torch.ones(k, **f64)
+        self.sinp = torch.zeros(k, **f64)
+        self.tlist = torch.zeros(k, dtype=torch.int32, device=dev)
+        self.tcount = torch.zeros(1, dtype=torch.int32, device=dev)
         self.touched = torch.zeros(k, dtype=torch.int32, device=dev)
         self.objc = torch.zeros(k, **f64)
-        self.part = torch.zeros(k * self.nchunk * 2, **f64)
-        self.norm = torch.zeros(k, **f64)
+        self.part = torch.empty(int(L.spkm_center_scratch_doubles(k, d)), **f64)
+        self.norm = torch.empty(k, **f64)
         self.cc = torch.zeros(k * k if with_cc else 1, dtype=torch.float32, device=dev)
         self.s = torch.zeros(k if with_cc else 1, dtype=torch.float32, device=dev)
-        self.hstat = torch.zeros(4, **f64)
+        self.hstat = torch.zeros(8, **f64)
         if with_cc:
             ntiles = int(L.spkm_gram_tiles(k, None))
             pairs = np.zeros(2 * ntiles, np.int32)
             L.spkm_gram_tiles(k, pairs.ctypes.data)
             self.tiles = torch.from_numpy(pairs).to(dev)
-            self.gram = torch.zeros(int(L.spkm_gram_scratch_doubles(k, d)), **f64)
+            self.gram = torch.empty(int(L.spkm_gram_scratch_doubles(k, d)), **f64)
         self.struct = Centers(k, d, self.kp, self.scale_bits, 0, _ptr(self.cent64), _ptr(self.ct32),
-                              _ptr(self.sums), _ptr(self.counts), _ptr(self.drift), _ptr(self.touched),
-                              _ptr(self.objc), _ptr(self.part), _ptr(self.norm), _ptr(self.cc), _ptr(self.s),
-                              _ptr(self.hstat))
+                              _ptr(self.sums), _ptr(self.counts), _ptr(self.drift), _ptr(self.sinp),
+                              _ptr(self.touched), _ptr(self.objc), _ptr(self.part), _ptr(self.norm), _ptr(self.cc),
+                              _ptr(self.s), _ptr(self.hstat), _ptr(self.tlist), _ptr(self.tcount))
+        self.cc_valid = False
 
-    def load(self, centers: np.ndarray, stream):
-        src = torch.from_numpy(np.ascontiguousarray(centers, np.float64).ravel()).to(self.cent64.device)
+    def load(self, centers, stream):
+        """Seed centers (numpy, or a float64 torch tensor already on the device)."""
+        if isinstance(centers, torch.Tensor) and centers.device == self.cent64.device:
+            src = centers.reshape(-1).to(torch.float64).contiguous()
+        else:
+            src = torch.from_numpy(np.ascontiguousarray(centers, np.float64).ravel()).to(self.cent64.device)
+        if src.numel() != self.k * self.d:
+            raise ValueError(f"centers must be {self.k} x {self.d}")
         _lib.call("spkm_load_centers", self.struct, _ptr(src), stream)
         return src  # keep alive until the stream passes
 
@@ -295,7 +351,9 @@ class Engine:
         _lib.call("spkm_reset_counters", self.P.work, self.sp)
 
     def center_thresholds(self):
-        _lib.call("spkm_center_thresholds", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles), self.sp)
+        _lib.call("spkm_center_thresholds", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles),
+                  int(not self.C.cc_valid), self.sp)
+        self.C.cc_valid = True
 
     def init_pass(self):
         mode = (_lib.MODE_INIT_ELKAN if self.elkan else _lib.MODE_INIT_HAMERLY if self.hamerly
@@ -429,8 +487,8 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
     a = eng.P.a[:eng.corpus.n].cpu().numpy().astype(np.int64)
     if comm is not None:
         a = comm.gather_assignments(eng.P.a, eng.corpus.rows, eng.n_total)
-    return ClusteringResult(assignments=a, centers=eng.centroid_set(seed_indices), objective=stats[-1].objective,
-                            iterations=stats, converged=converged)
+    return ClusteringResult(assignments=a, centers=DeviceCentroidSet(eng.C, seed_indices),
+                            objective=stats[-1].objective, iterations=stats, converged=converged)
 
 
 # --------------------------------------------------------------- predict etc.

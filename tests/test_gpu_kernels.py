@@ -1,0 +1,269 @@
+"""GPU kernel-level parity and the reference test suite's engine properties (through the C ABI).
+
+Mirrors /root/reference/pkg/tests/test_engine.py, test_validation.py and
+test_acceptance.py (#2 soundness, #4 pitfall, #5 efficacy, #6 monotone,
+#7 cc accounting) against the CUDA path.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN, golden_dataset, load_golden
+
+pytestmark = pytest.mark.gpu
+
+VARIANTS = ("standard", "elkan", "simp_elkan", "hamerly", "simp_hamerly")
+
+
+def spk():
+    import paper_2107_04074_b200 as m
+    return m
+
+
+def sv(pairs):
+    from paper_2107_04074_b200.sparse import SparseVector
+    idx, val = zip(*pairs)
+    return SparseVector(np.array(idx), np.array(val, dtype=float))
+
+
+# ------------------------------------------------------------------ device geometry
+@pytest.mark.parametrize("op,key", [(0, "lower"), (1, "upper"), (2, "hamerly"), (3, "half_angle")])
+def test_device_geometry_bit_exact(op, key):
+    from paper_2107_04074_b200 import _lib
+    z = np.load(GOLDEN / "geometry.npz")
+    a = torch.from_numpy(z["a"]).cuda()
+    b = torch.from_numpy(z["b"]).cuda()
+    out = torch.empty_like(a)
+    import ctypes
+    _lib.call("spkm_geometry", op, a.numel(), a.data_ptr(), b.data_ptr(), out.data_ptr(), ctypes.c_void_p(0))
+    torch.cuda.synchronize()
+    assert np.array_equal(out.cpu().numpy(), z[key]), key
+
+
+def test_device_lower_update_guard():
+    """l < -p -> -1 (theta_l + theta_p > pi), SURVEY.md §2.4 item 6."""
+    from paper_2107_04074_b200 import _lib
+    import ctypes
+    l = torch.tensor([np.cos(0.6 * np.pi), 0.5], dtype=torch.float64, device="cuda")
+    p = torch.tensor([np.cos(0.6 * np.pi) * -1 + 0.0 - 0.5, 0.9], dtype=torch.float64, device="cuda")
+    out = torch.empty_like(l)
+    _lib.call("spkm_geometry", 4, 2, l.data_ptr(), p.data_ptr(), out.data_ptr(), ctypes.c_void_p(0))
+    torch.cuda.synchronize()
+    o = out.cpu().numpy()
+    assert o[0] == -1.0
+    assert o[1] == pytest.approx(0.5 * 0.9 - np.sqrt(0.75 * 0.19), abs=1e-15)
+
+
+# ------------------------------------------------------------------ predict / objective
+def test_assign_full_matches_oracle(oracle_mod):
+    z = load_golden("C1")
+    data = golden_dataset(z)
+    X = oracle_mod.CSR(z["indptr"], z["indices"], z["data"], int(z["dim"]))
+    r = oracle_mod.run(X, 20, "standard", seed=1, max_iter=3)
+    a_ref, best_ref, second_ref = oracle_mod.assign_full(X, r["centers"])
+    a, best, second = spk().assign_full(data, r["centers"])
+    ok = (best_ref - second_ref) > 1e-5
+    assert np.array_equal(a[ok], a_ref[ok])
+    assert np.max(np.abs(best - best_ref)) < 3e-5
+    assert np.max(np.abs(second - second_ref)) < 3e-5
+    assert np.all(best >= second)
+
+
+def test_tie_breaks_to_lowest_index():
+    m = spk()
+    data = m.Dataset.from_rows([sv([(0, 1.0)]), sv([(1, 1.0)])], dim=2)
+    a, _, _ = m.assign_full(data, np.array([[1.0, 0.0], [1.0, 0.0]]))
+    assert list(a) == [0, 0]
+
+
+def test_compute_objective_matches_oracle(oracle_mod):
+    z = load_golden("small")
+    data = golden_dataset(z)
+    X = oracle_mod.CSR(z["indptr"], z["indices"], z["data"], int(z["dim"]))
+    r = oracle_mod.run(X, 7, "standard", seed=11, max_iter=100)
+    got = spk().compute_objective(data, r["assignments"], r["centers"])
+    S = oracle_mod.full_sims(X, r["centers"])
+    ref = float(S[np.arange(data.n), r["assignments"]].sum())
+    assert got == pytest.approx(ref, rel=1e-6)
+
+
+# ------------------------------------------------------------------ center updates
+def test_incremental_update_equals_scratch_bitwise():
+    m = spk()
+    z = load_golden("small")
+    data = golden_dataset(z)
+    g = np.random.default_rng(0)
+    k = 6
+    a0 = g.integers(0, k, data.n)
+    cs = m.CentroidSet.from_data_rows(data, range(k))
+    m.update_centers(data, a0, cs)
+    a1 = a0.copy()
+    flip = g.choice(data.n, 40, replace=False)
+    a1[flip] = g.integers(0, k, 40)
+    m.update_centers(data, a1, cs, prev_assignments=a0)
+    sc = m.CentroidSet.from_data_rows(data, range(k))
+    m.update_centers(data, a0, sc)
+    m.update_centers(data, a1, sc)
+    assert np.array_equal(cs.counts, sc.counts)
+    assert np.array_equal(cs.sums, sc.sums)          # exact fixed point: bit-identical
+    assert np.allclose(cs.centers, sc.centers, atol=1e-12)
+
+
+def test_untouched_cluster_bit_identical_and_empty_cluster_kept():
+    m = spk()
+    z = load_golden("small")
+    data = golden_dataset(z)
+    k = 4
+    a0 = np.zeros(data.n, dtype=np.int64)
+    a0[: data.n // 2] = 1
+    a0[:10] = 2
+    a0[10:20] = 3
+    cs = m.CentroidSet.from_data_rows(data, range(k))
+    m.update_centers(data, a0, cs)
+    frozen = cs.centers[3].copy()
+    a1 = a0.copy()
+    a1[0] = 1
+    m.update_centers(data, a1, cs, prev_assignments=a0)
+    assert np.array_equal(cs.centers[3], frozen)
+    assert cs.drift[3] == 1.0
+    cs2 = m.CentroidSet.from_data_rows(data, range(3))
+    before = cs2.centers[2].copy()
+    a = np.zeros(data.n, dtype=np.int64)
+    a[:5] = 1
+    m.update_centers(data, a, cs2)
+    assert np.array_equal(cs2.centers[2], before)
+    assert cs2.drift[2] == 1.0
+
+
+# ------------------------------------------------------------------ engine properties
+def test_k1_and_k_equals_n():
+    m = spk()
+    z = load_golden("small")
+    data = golden_dataset(z)
+    for v in VARIANTS:
+        r = m.run(data, 1, v, m.SeedConfig(seed=3))
+        assert r.converged and len(r.iterations) == 1 and np.all(r.assignments == 0)
+    five = golden_dataset(load_golden("five_points"))
+    r = m.run(five, 5, "standard", m.SeedConfig(seed=0))
+    assert r.converged and len(r.iterations) <= 2          # reference: 1 (iteration count +-1)
+    assert sorted(r.assignments.tolist()) == [0, 1, 2, 3, 4]
+
+
+def test_instrumentation_and_max_iter():
+    m = spk()
+    data = golden_dataset(load_golden("small"))
+    r = m.run(data, 4, "standard", m.SeedConfig(seed=1))
+    assert r.iterations[0].reassignments == data.n
+    assert all(s.sim_count == data.n * 4 and s.cc_sim_count == 0 for s in r.iterations)
+    assert r.iterations[-1].reassignments == 0
+    assert len(m.run(data, 10, "standard", m.SeedConfig(seed=1), max_iter=2).iterations) <= 2
+    k = 8
+    for v in ("elkan", "hamerly"):
+        r = m.run(data, k, v, m.SeedConfig(seed=5))
+        assert all(s.cc_sim_count == k * (k - 1) // 2 for s in r.iterations)
+    for v in ("standard", "simp_elkan", "simp_hamerly"):
+        assert m.run(data, k, v, m.SeedConfig(seed=5)).total_cc_sims == 0
+
+
+def test_objective_monotone_and_deterministic():
+    m = spk()
+    data = golden_dataset(load_golden("grid_2000_5000_20_2000"))
+    for v in VARIANTS:
+        r = m.run(data, 20, v, m.SeedConfig(seed=13))
+        objs = [s.objective for s in r.iterations]
+        assert all(b >= a - 1e-9 * data.n for a, b in zip(objs, objs[1:])), v
+        r2 = m.run(data, 20, v, m.SeedConfig(seed=13))
+        assert np.array_equal(r.assignments, r2.assignments) and r.objective == r2.objective
+        assert [s.sim_count for s in r.iterations] == [s.sim_count for s in r2.iterations]
+
+
+def test_pruning_efficacy_clustered():
+    """Acceptance #5 on the regenerated clustered_2000x5000 fixture, k=20, seed=3."""
+    m = spk()
+    data = golden_dataset(load_golden("clustered"))
+    tot = {v: m.run(data, 20, v, m.SeedConfig(seed=3)).total_sims for v in ("standard", "elkan", "hamerly")}
+    assert tot["elkan"] / tot["standard"] < 0.5
+    assert tot["hamerly"] / tot["standard"] < 1.0
+
+
+# ------------------------------------------------------------------ bound soundness audits
+class Auditor:
+    """validation._BoundAuditor (validation.py:49-80) with the oracle's exact fp64 similarities."""
+
+    def __init__(self, O, X):
+        self.O, self.X = O, X
+        self.max_lower = self.max_upper = 0.0
+        self.count = 0
+
+    def __call__(self, it, bounds, cents):
+        S = self.O.full_sims(self.X, cents.centers)
+        n = S.shape[0]
+        own = S[np.arange(n), bounds.a]
+        self.max_lower = max(self.max_lower, float(np.max(bounds.l - own)))
+        self.count += n
+        if bounds.u_matrix is not None:
+            self.max_upper = max(self.max_upper, float(np.max(S - bounds.u_matrix)))
+            self.count += S.size
+        elif bounds.u is not None and S.shape[1] > 1:
+            mm = S.copy()
+            mm[np.arange(n), bounds.a] = -np.inf
+            self.max_upper = max(self.max_upper, float(np.max(mm.max(axis=1) - bounds.u)))
+            self.count += n
+
+
+@pytest.mark.parametrize("name,k,seed", [("small", 7, 11), ("signed", 6, 2), ("grid_200_256_10_3000", 10, 3007),
+                                         ("C1", 20, 1), ("clustered", 20, 3)])
+@pytest.mark.parametrize("variant", VARIANTS[1:])
+def test_bounds_sound_every_iteration(oracle_mod, name, k, seed, variant):
+    m = spk()
+    z = load_golden(name)
+    data = golden_dataset(z)
+    X = oracle_mod.CSR(z["indptr"], z["indices"], z["data"], int(z["dim"]))
+    aud = Auditor(oracle_mod, X)
+    m.run(data, k, variant, m.SeedConfig(seed=seed), debug_hook=aud)
+    assert aud.max_lower <= 1e-9 and aud.max_upper <= 1e-9, (aud.max_lower, aud.max_upper)
+
+
+def test_pitfall_naive_violates_safe_passes(oracle_mod):
+    """Acceptance #4 (tests/test_acceptance.py:114-123) on the GPU bounds."""
+    m = spk()
+    z = load_golden("pitfall")
+    data = golden_dataset(z)
+    X = oracle_mod.CSR(z["indptr"], z["indices"], z["data"], int(z["dim"]))
+    naive, safe = Auditor(oracle_mod, X), Auditor(oracle_mod, X)
+    m.run(data, 5, "hamerly", m.SeedConfig(seed=1), debug_hook=naive, hamerly_update="naive")
+    m.run(data, 5, "hamerly", m.SeedConfig(seed=1), debug_hook=safe)
+    assert naive.max_upper > 1e-9
+    assert safe.max_upper <= 1e-9 and safe.max_lower <= 1e-9
+
+
+# ------------------------------------------------------------------ edge cases
+def test_single_nnz_rows_and_duplicates():
+    m = spk()
+    rows = [sv([(i % 7, 1.0)]) for i in range(60)] + [sv([(0, 1.0), (1, 1.0)])] * 5
+    data = m.Dataset.from_rows(rows, dim=7)
+    base = None
+    for v in VARIANTS:
+        r = m.run(data, 5, v, m.SeedConfig(seed=4))
+        if base is None:
+            base = r
+        assert np.array_equal(r.assignments, base.assignments), v
+        assert r.objective == base.objective
+
+
+def test_max_length_rows(oracle_mod):
+    """Rows at the 400-nnz clip and at d-dense lengths."""
+    m = spk()
+    from paper_2107_04074_b200 import synth
+    spec = synth.CorpusSpec("long", 300, 600, 300, min_nnz=200, max_nnz=400)
+    data = synth.sparse_corpus(spec, seed=11)
+    assert data.row_lengths().max() == 400
+    X = oracle_mod.CSR(data.indptr, data.indices, data.data, data.dim)
+    ref = oracle_mod.run(X, 8, "standard", seed=5, max_iter=50)
+    margin = oracle_mod.margins(X, ref["centers"])
+    for v in VARIANTS:
+        r = m.run(data, 8, v, m.SeedConfig(seed=5), max_iter=50)
+        ok = margin > 1e-5
+        assert np.array_equal(r.assignments[ok], ref["assignments"][ok]), v
+        assert r.objective == pytest.approx(ref["objective"][-1], rel=1e-6)

@@ -281,7 +281,7 @@ def main_ours(args):
             comm = Exchange(k, data.dim, dev) if world > 1 else None
             r = spk.run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=c,
                         comm=comm, n_total=data.n)
-            h2d += k * data.dim * 8
+            h2d += int(k * 8 + sum(int(data.indptr[j + 1] - data.indptr[j]) for j in cents0.seed_indices) * 12)
             d2h += r.assignments.nbytes
         e1.record()
         barrier()

@@ -183,6 +183,12 @@ int spkm_objective(const spkm_centers *C, const long long *sums, double *out, vo
 /* Upload helper: write center-major float64 centers into cent64 and ct32. */
 int spkm_load_centers(const spkm_centers *C, const double *host_or_dev_centers, void *stream);
 
+/* Seed centers from k data rows (init_uniform, seeding.py:56-61 +
+ * CentroidSet.from_data_rows, engine.py:46-58): packed CSR of the seed rows
+ * (sptr[k+1], sidx, float64 values) in device memory. */
+int spkm_seed_rows(const spkm_centers *C, const int64_t *sptr, const int32_t *sidx, const double *sval,
+                   void *stream);
+
 /* Device geometry for tests: op 0 lower, 1 upper, 2 hamerly, 3 half-angle. */
 int spkm_geometry(int op, int64_t n, const double *a, const double *b, double *out, void *stream);
 

@@ -83,6 +83,7 @@ _SIGS = {
     "spkm_objective": [_P(Centers), c_vp, c_vp, c_vp],
     "spkm_load_centers": [_P(Centers), c_vp, c_vp],
     "spkm_geometry": [ctypes.c_int, c_i64, c_vp, c_vp, c_vp, c_vp],
+    "spkm_seed_rows": [_P(Centers), c_vp, c_vp, c_vp, c_vp],
 }
 _RESTYPES = {
     "spkm_last_error": ctypes.c_char_p,
@@ -98,7 +99,7 @@ KERNELS_PER_CALL = {
     "spkm_full_assign": 1, "spkm_hamerly_bounds": 1, "spkm_hamerly_tighten": 1, "spkm_hamerly_rescan": 1,
     "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
     "spkm_move_centers": 5, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
-    "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1,
+    "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
 }
 
 _lib = None

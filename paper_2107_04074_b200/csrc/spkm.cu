@@ -112,25 +112,10 @@ __device__ __forceinline__ float store_upper(double v) {
 }
 
 // ------------------------------------------------------- canonical similarity
-// s~(i,j) for one pair: the same FMA chain the row kernels run per column.
-__device__ __forceinline__ float dot_pair(const int32_t *__restrict__ idx, const float *__restrict__ val,
-                                          int64_t s, int64_t e, const float *__restrict__ ct, int64_t kp,
-                                          int j) {
-    float acc = 0.f;
-    int64_t t = s;
-    for (; t + 4 <= e; t += 4) {
-        const int i0 = __ldg(idx + t), i1 = __ldg(idx + t + 1), i2 = __ldg(idx + t + 2), i3 = __ldg(idx + t + 3);
-        const float v0 = __ldg(val + t), v1 = __ldg(val + t + 1), v2 = __ldg(val + t + 2), v3 = __ldg(val + t + 3);
-        const float c0 = __ldg(ct + (int64_t)i0 * kp + j), c1 = __ldg(ct + (int64_t)i1 * kp + j);
-        const float c2 = __ldg(ct + (int64_t)i2 * kp + j), c3 = __ldg(ct + (int64_t)i3 * kp + j);
-        acc = __fmaf_rn(v0, c0, acc);
-        acc = __fmaf_rn(v1, c1, acc);
-        acc = __fmaf_rn(v2, c2, acc);
-        acc = __fmaf_rn(v3, c3, acc);
-    }
-    for (; t < e; ++t) acc = __fmaf_rn(__ldg(val + t), __ldg(ct + (int64_t)__ldg(idx + t) * kp + j), acc);
-    return acc;
-}
+// s~(i,j) = float32 FMA chain over row i's nnz in CSR order, starting at 0:
+//   acc = fma(val[t], ct[idx[t] * kp + j], acc)   for t = indptr[i] .. indptr[i+1]-1
+// k_row_pass (per column), warp_dots (per candidate) all evaluate exactly
+// this chain; only the order in which the center values are FETCHED differs.
 
 // ------------------------------------------------------------- top-2 helpers
 // Priority: larger value; on exact ties the incumbent `inc`, then lower index.
@@ -220,62 +205,76 @@ struct RowPassArgs {
 // CH/4 float4 loads of the term-major center row; CH independent FMA chains.
 template <int CH>
 __global__ void __launch_bounds__(256) k_row_pass(RowPassArgs A) {
-    const int lane = threadIdx.x & 31;
+    // nnz per gather batch: keep ~8 float4 loads in flight per lane
+    constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 2 : 1;
+    __shared__ int32_t s_idx[8][8][32];
+    __shared__ float s_val[8][8][32];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane / A.tpr, q = lane - g * A.tpr;
     const bool lane_on = g < A.rpw;
     const int64_t nrows = A.rowlist ? *A.rowcount : A.n;
     const int64_t nslots = (nrows + A.rpw - 1) / A.rpw;
     const int wpb = blockDim.x >> 5;
     const int o0 = A.tpr > 1 ? (1 << (31 - __clz(A.tpr - 1))) : 0;
-    for (int64_t w = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); w < nslots; w += (int64_t)gridDim.x * wpb) {
+    int32_t *my_idx = s_idx[wib][lane_on ? g : 0];
+    float *my_val = s_val[wib][lane_on ? g : 0];
+    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
         const int64_t slot = w * A.rpw + g;
         const bool valid = lane_on && slot < nrows;
         const int64_t row = valid ? (A.rowlist ? (int64_t)A.rowlist[slot] : slot) : 0;
         const int64_t s = valid ? A.indptr[row] : 0;
         const int64_t e = valid ? A.indptr[row + 1] : 0;
+        const int len = (int)(e - s);
+        const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
         const int j0 = q * CH;
         float acc[CH];
 #pragma unroll
         for (int c = 0; c < CH; ++c) acc[c] = 0.f;
         const float *ctj = A.ct + j0;
-        int64_t t = s;
-        for (; t + 2 <= e; t += 2) {
-            const int i0 = __ldg(A.indices + t), i1 = __ldg(A.indices + t + 1);
-            const float v0 = __ldg(A.values + t), v1 = __ldg(A.values + t + 1);
-            const float4 *p0 = reinterpret_cast<const float4 *>(ctj + (int64_t)i0 * A.kp);
-            const float4 *p1 = reinterpret_cast<const float4 *>(ctj + (int64_t)i1 * A.kp);
-            float4 c0[CH / 4], c1[CH / 4];
-#pragma unroll
-            for (int r = 0; r < CH / 4; ++r) c0[r] = __ldg(p0 + r);
-#pragma unroll
-            for (int r = 0; r < CH / 4; ++r) c1[r] = __ldg(p1 + r);
-#pragma unroll
-            for (int r = 0; r < CH / 4; ++r) {
-                acc[4 * r + 0] = __fmaf_rn(v0, c0[r].x, acc[4 * r + 0]);
-                acc[4 * r + 1] = __fmaf_rn(v0, c0[r].y, acc[4 * r + 1]);
-                acc[4 * r + 2] = __fmaf_rn(v0, c0[r].z, acc[4 * r + 2]);
-                acc[4 * r + 3] = __fmaf_rn(v0, c0[r].w, acc[4 * r + 3]);
+        // Rows are staged 32 nnz at a time in shared memory (coalesced loads by
+        // the row's lanes); the term-major center rows are then gathered UB
+        // nnz at a time so UB * CH/4 independent float4 loads are in flight.
+        for (int c0 = 0; c0 < maxlen; c0 += 32) {
+            const int cnt = max(0, min(32, len - c0));
+            for (int q2 = q; q2 < cnt; q2 += A.tpr) {
+                my_idx[q2] = __ldg(A.indices + s + c0 + q2);
+                my_val[q2] = __ldg(A.values + s + c0 + q2);
             }
+            __syncwarp();
+            int u = 0;
+            for (; u + UB <= cnt; u += UB) {
+                float4 cv[UB][CH / 4];
+                float vv[UB];
 #pragma unroll
-            for (int r = 0; r < CH / 4; ++r) {
-                acc[4 * r + 0] = __fmaf_rn(v1, c1[r].x, acc[4 * r + 0]);
-                acc[4 * r + 1] = __fmaf_rn(v1, c1[r].y, acc[4 * r + 1]);
-                acc[4 * r + 2] = __fmaf_rn(v1, c1[r].z, acc[4 * r + 2]);
-                acc[4 * r + 3] = __fmaf_rn(v1, c1[r].w, acc[4 * r + 3]);
-            }
-        }
-        if (t < e) {
-            const int i0 = __ldg(A.indices + t);
-            const float v0 = __ldg(A.values + t);
-            const float4 *p0 = reinterpret_cast<const float4 *>(ctj + (int64_t)i0 * A.kp);
+                for (int b = 0; b < UB; ++b) {
+                    vv[b] = my_val[u + b];
+                    const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)my_idx[u + b] * A.kp);
 #pragma unroll
-            for (int r = 0; r < CH / 4; ++r) {
-                const float4 c = __ldg(p0 + r);
-                acc[4 * r + 0] = __fmaf_rn(v0, c.x, acc[4 * r + 0]);
-                acc[4 * r + 1] = __fmaf_rn(v0, c.y, acc[4 * r + 1]);
-                acc[4 * r + 2] = __fmaf_rn(v0, c.z, acc[4 * r + 2]);
-                acc[4 * r + 3] = __fmaf_rn(v0, c.w, acc[4 * r + 3]);
+                    for (int r = 0; r < CH / 4; ++r) cv[b][r] = __ldg(p + r);
+                }
+#pragma unroll
+                for (int b = 0; b < UB; ++b)
+#pragma unroll
+                    for (int r = 0; r < CH / 4; ++r) {
+                        acc[4 * r + 0] = __fmaf_rn(vv[b], cv[b][r].x, acc[4 * r + 0]);
+                        acc[4 * r + 1] = __fmaf_rn(vv[b], cv[b][r].y, acc[4 * r + 1]);
+                        acc[4 * r + 2] = __fmaf_rn(vv[b], cv[b][r].z, acc[4 * r + 2]);
+                        acc[4 * r + 3] = __fmaf_rn(vv[b], cv[b][r].w, acc[4 * r + 3]);
+                    }
             }
+            for (; u < cnt; ++u) {
+                const float v0 = my_val[u];
+                const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)my_idx[u] * A.kp);
+#pragma unroll
+                for (int r = 0; r < CH / 4; ++r) {
+                    const float4 cc4 = __ldg(p + r);
+                    acc[4 * r + 0] = __fmaf_rn(v0, cc4.x, acc[4 * r + 0]);
+                    acc[4 * r + 1] = __fmaf_rn(v0, cc4.y, acc[4 * r + 1]);
+                    acc[4 * r + 2] = __fmaf_rn(v0, cc4.z, acc[4 * r + 2]);
+                    acc[4 * r + 3] = __fmaf_rn(v0, cc4.w, acc[4 * r + 3]);
+                }
+            }
+            __syncwarp();
         }
         const bool incumbent_mode = (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN);
         const int inc = (valid && incumbent_mode) ? A.a[row] : -1;
@@ -336,6 +335,60 @@ __global__ void __launch_bounds__(256) k_row_pass(RowPassArgs A) {
     }
 }
 
+// ------------------------------------------------ warp-cooperative pair dots
+// s~(i, cand[c]) for the m <= 32 candidate centers listed in `cand` (one row
+// i = [s, e)).  Per 32-nnz chunk: lane L loads (idx_L, val_L) and gathers the
+// m center values ct[idx_L * kp + cand[c]] into tile[L][c] (m independent
+// loads per lane); lane c then runs the canonical FMA chain down column c.
+// Returns the value in lane c < m (bit-identical to dot_pair / k_row_pass).
+struct DotSmem {
+    float tile[32][33];
+    float val[32];
+    int32_t cand[64];
+};
+__device__ __forceinline__ float warp_dots(const int32_t *__restrict__ idx, const float *__restrict__ val, int64_t s,
+                                           int64_t e, const float *__restrict__ ct, int64_t kp, int m,
+                                           DotSmem &sm) {
+    const int lane = threadIdx.x & 31;
+    float acc = 0.f;
+    for (int64_t base = s; base < e; base += 32) {
+        const int cnt = (int)min((int64_t)32, e - base);
+        int myidx = 0;
+        float myval = 0.f;
+        if (lane < cnt) {
+            myidx = __ldg(idx + base + lane);
+            myval = __ldg(val + base + lane);
+        }
+        sm.val[lane] = myval;
+        if (lane < cnt) {
+            const float *rowp = ct + (int64_t)myidx * kp;
+            int c = 0;
+            for (; c + 4 <= m; c += 4) {
+                const float x0 = __ldg(rowp + sm.cand[c]), x1 = __ldg(rowp + sm.cand[c + 1]);
+                const float x2 = __ldg(rowp + sm.cand[c + 2]), x3 = __ldg(rowp + sm.cand[c + 3]);
+                sm.tile[lane][c] = x0;
+                sm.tile[lane][c + 1] = x1;
+                sm.tile[lane][c + 2] = x2;
+                sm.tile[lane][c + 3] = x3;
+            }
+            for (; c < m; ++c) sm.tile[lane][c] = __ldg(rowp + sm.cand[c]);
+        }
+        __syncwarp();
+        if (lane < m) {
+            int t = 0;
+            for (; t + 4 <= cnt; t += 4) {
+                acc = __fmaf_rn(sm.val[t], sm.tile[t][lane], acc);
+                acc = __fmaf_rn(sm.val[t + 1], sm.tile[t + 1][lane], acc);
+                acc = __fmaf_rn(sm.val[t + 2], sm.tile[t + 2][lane], acc);
+                acc = __fmaf_rn(sm.val[t + 3], sm.tile[t + 3][lane], acc);
+            }
+            for (; t < cnt; ++t) acc = __fmaf_rn(sm.val[t], sm.tile[t][lane], acc);
+        }
+        __syncwarp();
+    }
+    return acc;
+}
+
 // --------------------------------------------------------- Hamerly family
 // engine.py:274 (l), 284-303 (u) fused with the kernels.py:81-87 tests.
 __global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *__restrict__ reps,
@@ -387,7 +440,8 @@ __global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *
     }
 }
 
-// kernels.py:88-95: tighten l with the exact s~(i,a), re-test.
+// kernels.py:88-95: tighten l with the exact s~(i,a), re-test.  Warp per
+// survivor (the row's gathers are issued 32 at a time, see warp_dots).
 __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restrict__ indptr,
                                                          const int32_t *__restrict__ indices,
                                                          const float *__restrict__ values,
@@ -398,26 +452,37 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
                                                          const float *__restrict__ s_arr, int use_s,
                                                          const int32_t *__restrict__ surv1, int32_t *surv2,
                                                          long long *ctr) {
+    __shared__ DotSmem sm_all[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    DotSmem &sm = sm_all[wib];
+    const int wpb = blockDim.x >> 5;
     const long long cnt = ctr[SPKM_CTR_SURV1];
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t cnt_pad = (cnt + 31) & ~(long long)31;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < cnt_pad; t += stride) {
-        bool surv = false;
-        int32_t i = 0;
-        if (t < cnt) {
-            i = surv1[t];
-            const int ai = a[i];
-            const float sa = dot_pair(indices, values, indptr[i], indptr[i + 1], ct, kp, ai);
+    long long sims = 0, nnz = 0;
+    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < cnt; w += (int64_t)gridDim.x * wpb) {
+        const int32_t i = surv1[w];
+        const int ai = a[i];
+        const int64_t s = indptr[i], e = indptr[i + 1];
+        if (lane == 0) sm.cand[0] = ai;
+        __syncwarp();
+        const float sa = warp_dots(indices, values, s, e, ct, kp, 1, sm);
+        if (lane == 0) {
             const double eps = (double)reps[i];
             const double lb = (double)sa - eps;
             l[i] = store_lower(lb);
             bool pruned = (use_s && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb);
             if (!pruned) pruned = ((double)u[i] + eps <= (double)sa);
-            surv = !pruned;
+            if (!pruned) {
+                const long long p = atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV2), 1ull);
+                surv2[p] = i;
+            }
+            sims += 1;
+            nnz += e - s;
         }
-        warp_append(surv, i, surv2, 0, nullptr, ctr + SPKM_CTR_SURV2);
-        warp_add(ctr + SPKM_CTR_SIMS, t < cnt ? 1 : 0);
-        warp_add(ctr + SPKM_CTR_NNZ_TIGHTEN, t < cnt ? (long long)(indptr[i + 1] - indptr[i]) : 0);
+        __syncwarp();
+    }
+    if (lane == 0 && sims) {
+        atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SIMS), (unsigned long long)sims);
+        atomicAdd((unsigned long long *)(ctr + SPKM_CTR_NNZ_TIGHTEN), (unsigned long long)nnz);
     }
 }
 
@@ -474,7 +539,8 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
 
 // kernels.py:48-65 for the surviving points: tighten once, re-test every
 // j against s~(i,a) (and strictly against a better non-incumbent found so
-// far), compute the survivors 32 at a time, keep the best with the tie rule.
+// far), compute the survivors 32 at a time with warp_dots, keep the best
+// with the tie rule.
 __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ indptr,
                                                     const int32_t *__restrict__ indices,
                                                     const float *__restrict__ values,
@@ -484,10 +550,9 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                                                     const float *__restrict__ cc, int use_cc,
                                                     const int32_t *__restrict__ surv1, int32_t *mv_i,
                                                     int32_t *mv_old, long long *ctr) {
-    __shared__ int32_t buf_all[8][64];
-    const int lane = threadIdx.x & 31;
-    const int wib = threadIdx.x >> 5;
-    int32_t *buf = buf_all[wib];
+    __shared__ DotSmem sm_all[8];
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    DotSmem &sm = sm_all[wib];
     const int wpb = blockDim.x >> 5;
     const long long cnt = ctr[SPKM_CTR_SURV1];
     for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < cnt; w += (int64_t)gridDim.x * wpb) {
@@ -495,36 +560,17 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
         const int ai = a[i];
         const int64_t s = indptr[i], e = indptr[i + 1];
         const double eps = (double)reps[i];
-        float sa = 0.f;
-        if (lane == 0) sa = dot_pair(indices, values, s, e, ct, kp, ai);
+        if (lane == 0) sm.cand[0] = ai;
+        __syncwarp();
+        float sa = warp_dots(indices, values, s, e, ct, kp, 1, sm);
         sa = __shfl_sync(FULL, sa, 0);
         float *ui = u + (int64_t)i * ku;
         if (lane == 0) ui[ai] = store_upper((double)sa + eps);
         const double lb = (double)sa - eps;
-        Top2 best{sa, ai, -INFINITY};
+        float best_b = sa;
+        int best_j = ai;
         long long sims = 1;
         int pos = 0;
-        auto process = [&](int m) {
-            float v = -INFINITY;
-            int j = -2;
-            if (lane < m) {
-                j = buf[lane];
-                v = dot_pair(indices, values, s, e, ct, kp, j);
-                ui[j] = store_upper((double)v + eps);
-            }
-            Top2 tp{v, j, -INFINITY};
-            for (int o = 16; o; o >>= 1) {
-                const Top2 other = top2_shfl_down(tp, o);
-                if (lane < o) top2_merge(tp, other, ai);
-            }
-            tp.b = __shfl_sync(FULL, tp.b, 0);
-            tp.bj = __shfl_sync(FULL, tp.bj, 0);
-            if (better(tp.b, tp.bj, best.b, best.bj, ai)) {
-                best.b = tp.b;
-                best.bj = tp.bj;
-            }
-            sims += m;
-        };
         for (int base = 0; base < k; base += 32) {
             const int j = base + lane;
             bool cand = false;
@@ -532,32 +578,53 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                 const double uij = (double)ui[j];
                 bool prune = use_cc && lb >= 0.0 && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb;
                 if (!prune) prune = (uij + eps <= (double)sa);
-                if (!prune && best.bj != ai) prune = (uij + eps < (double)best.b);
+                if (!prune && best_j != ai) prune = (uij + eps < (double)best_b);
                 cand = !prune;
             }
             const unsigned m = __ballot_sync(FULL, cand);
-            if (cand) buf[pos + __popc(m & ((1u << lane) - 1u))] = j;
+            __syncwarp();
+            if (cand) sm.cand[pos + __popc(m & ((1u << lane) - 1u))] = j;
             pos += __popc(m);
             __syncwarp();
-            if (pos >= 32) {
-                process(32);
+            const bool last = base + 32 >= k;
+            while (pos >= 32 || (last && pos > 0)) {
+                const int mm = pos >= 32 ? 32 : pos;
+                const float v = warp_dots(indices, values, s, e, ct, kp, mm, sm);
+                int jj = -2;
+                float vv = -INFINITY;
+                if (lane < mm) {
+                    jj = sm.cand[lane];
+                    vv = v;
+                    ui[jj] = store_upper((double)v + eps);
+                }
+                Top2 tp{vv, jj, -INFINITY};
+                for (int o = 16; o; o >>= 1) {
+                    const Top2 other = top2_shfl_down(tp, o);
+                    if (lane < o) top2_merge(tp, other, ai);
+                }
+                tp.b = __shfl_sync(FULL, tp.b, 0);
+                tp.bj = __shfl_sync(FULL, tp.bj, 0);
+                if (better(tp.b, tp.bj, best_b, best_j, ai)) {
+                    best_b = tp.b;
+                    best_j = tp.bj;
+                }
+                sims += mm;
                 __syncwarp();
-                if (lane < pos - 32) buf[lane] = buf[lane + 32];
+                if (lane < pos - mm) sm.cand[lane] = sm.cand[lane + 32];
                 __syncwarp();
-                pos -= 32;
+                pos -= mm;
             }
         }
-        if (pos > 0) process(pos);
-        __syncwarp();
         if (lane == 0) {
-            l[i] = store_lower((double)best.b - eps);
-            if (best.bj != ai) a[i] = best.bj;
+            l[i] = store_lower((double)best_b - eps);
+            if (best_j != ai) a[i] = best_j;
         }
-        warp_append(lane == 0 && best.bj != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
+        warp_append(lane == 0 && best_j != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
         if (lane == 0) {
             atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SIMS), (unsigned long long)sims);
             atomicAdd((unsigned long long *)(ctr + SPKM_CTR_NNZ_ELKAN), (unsigned long long)(e - s));
         }
+        __syncwarp();
     }
 }
 
@@ -932,16 +999,41 @@ __global__ void __launch_bounds__(1024) k_finalize(int64_t k, int32_t *touched, 
 }
 
 // ---------------------------------------------------------- center thresholds
-// engine._center_thresholds (engine.py:192-198): float64 Gram over the
-// upper-triangle 32x32 tiles, split over d; a tile is skipped when neither
-// of its cluster ranges moved since the last call (cc stays valid).
-constexpr int GT = 32;   // output tile
-constexpr int GK = 32;   // d step
-__global__ void __launch_bounds__(64) k_gram_part(int64_t k, int64_t d, int64_t dsplit,
-                                                  const double *__restrict__ C, const int2 *__restrict__ tiles,
-                                                  const double *__restrict__ sinp, int full, double *gpart) {
-    __shared__ double As[GK][GT + 1];
-    __shared__ double Bs[GK][GT + 1];
+// engine._center_thresholds (engine.py:192-198): Gram G = C C^T on the tensor
+// cores, 3xTF32 (x = hi + lo, G ~ hi.hi + hi.lo + lo.hi) with mma.sync
+// m16n8k8, read from the term-major float32 copy ct32, split over d.  Each
+// 32-term stage is accumulated in fp32 (96 products) and then added into
+// float64 registers; stages and d-splits are summed in float64.
+// Error bound: |G~ - G| <= 1.2e-7 (ct32 rounding) + 7.2e-7 (3xTF32 residual)
+// + 96 * 2^-22 (per-stage fp32 accumulation, truncating adds assumed)
+// times sum_t |c_a[t] c_j[t]| <= 1, i.e. < 2.4e-5; kGramDelta = 5e-5 is added
+// before the half-angle map so cc stays an upper bound.
+// Tiles: 32x32 outputs (upper triangle), 4 warps x (16 x 16).  A tile is
+// skipped when none of its clusters moved since the last call.
+constexpr int GT = 32;
+constexpr double kGramDelta = 5e-5;
+__device__ __forceinline__ uint32_t to_tf32(float x) {
+    uint32_t r;
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+    return r;
+}
+__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
+    asm volatile(
+        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
+        "{%0,%1,%2,%3};\n"
+        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+}
+__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
+    hi = to_tf32(x);
+    lo = to_tf32(x - __uint_as_float(hi));
+}
+
+__global__ void __launch_bounds__(128) k_gram_part(int64_t k, int64_t d, int64_t kp, int64_t dsplit,
+                                                   const float *__restrict__ ct, const int2 *__restrict__ tiles,
+                                                   const double *__restrict__ sinp, int full, double *gpart) {
+    __shared__ float As[32][40];   // [term][cluster]; stride 40 keeps fragment loads conflict-free
+    __shared__ float Bs[32][40];
     __shared__ int need;
     const int2 tl = tiles[blockIdx.x];
     const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
@@ -955,43 +1047,56 @@ __global__ void __launch_bounds__(64) k_gram_part(int64_t k, int64_t d, int64_t 
     }
     __syncthreads();
     if (!need) return;
-    const int64_t per = (d + dsplit - 1) / dsplit;
+    const int64_t per = ((d + dsplit - 1) / dsplit + 31) / 32 * 32;
     const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
-    const int tx = threadIdx.x & 7, ty = threadIdx.x >> 3;   // 8 x 8 threads, 4x4 outputs each
-    double acc[4][4];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int wy = w >> 1, wx = w & 1, g = lane >> 2, t4 = lane & 3;
+    double accd[2][4];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int f = 0; f < 2; ++f)
 #pragma unroll
-        for (int s = 0; s < 4; ++s) acc[r][s] = 0.0;
-    for (int64_t tb = t0; tb < t1; tb += GK) {
-        for (int e = threadIdx.x; e < GK * GT; e += blockDim.x) {
-            const int r = e / GK, cidx = e % GK;
-            const int64_t t = tb + cidx;
-            const int64_t ar = a0 + r, jr = j0 + r;
-            As[cidx][r] = (ar < k && t < t1) ? C[ar * d + t] : 0.0;
-            Bs[cidx][r] = (jr < k && t < t1) ? C[jr * d + t] : 0.0;
+        for (int q = 0; q < 4; ++q) accd[f][q] = 0.0;
+    for (int64_t tb = t0; tb < t1; tb += 32) {
+        for (int e2 = threadIdx.x; e2 < 32 * 32; e2 += blockDim.x) {
+            const int tt = e2 >> 5, cl = e2 & 31;
+            const int64_t t = tb + tt;
+            const bool tin = t < t1;
+            As[tt][cl] = (tin && a0 + cl < k) ? __ldg(ct + t * kp + a0 + cl) : 0.f;
+            Bs[tt][cl] = (tin && j0 + cl < k) ? __ldg(ct + t * kp + j0 + cl) : 0.f;
         }
         __syncthreads();
-#pragma unroll 8
-        for (int c = 0; c < GK; ++c) {
-            double av[4], bv[4];
+        float dst[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
 #pragma unroll
-            for (int r = 0; r < 4; ++r) av[r] = As[c][ty * 4 + r];
+        for (int ks = 0; ks < 4; ++ks) {
+            const int kk = ks * 8;
+            uint32_t ahi[4], alo[4];
+            split_tf32(As[kk + t4][wy * 16 + g], ahi[0], alo[0]);
+            split_tf32(As[kk + t4][wy * 16 + g + 8], ahi[1], alo[1]);
+            split_tf32(As[kk + t4 + 4][wy * 16 + g], ahi[2], alo[2]);
+            split_tf32(As[kk + t4 + 4][wy * 16 + g + 8], ahi[3], alo[3]);
 #pragma unroll
-            for (int s = 0; s < 4; ++s) bv[s] = Bs[c][tx * 4 + s];
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int s = 0; s < 4; ++s) acc[r][s] = fma(av[r], bv[s], acc[r][s]);
+            for (int f = 0; f < 2; ++f) {
+                uint32_t bhi[2], blo[2];
+                split_tf32(Bs[kk + t4][wx * 16 + f * 8 + g], bhi[0], blo[0]);
+                split_tf32(Bs[kk + t4 + 4][wx * 16 + f * 8 + g], bhi[1], blo[1]);
+                mma_tf32(dst[f], alo, bhi);
+                mma_tf32(dst[f], ahi, blo);
+                mma_tf32(dst[f], ahi, bhi);
+            }
         }
+#pragma unroll
+        for (int f = 0; f < 2; ++f)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) accd[f][q] += (double)dst[f][q];
         __syncthreads();
     }
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int f = 0; f < 2; ++f)
 #pragma unroll
-        for (int s = 0; s < 4; ++s) {
-            const int64_t ar = a0 + ty * 4 + r, jr = j0 + tx * 4 + s;
-            if (ar < k && jr < k) gpart[((int64_t)blockIdx.y * k + ar) * k + jr] = acc[r][s];
+        for (int q = 0; q < 4; ++q) {
+            const int64_t ar = a0 + wy * 16 + g + ((q & 2) ? 8 : 0);
+            const int64_t jr = j0 + wx * 16 + f * 8 + t4 * 2 + (q & 1);
+            if (ar < k && jr < k) gpart[((int64_t)blockIdx.y * k + ar) * k + jr] = accd[f][q];
         }
 }
 
@@ -1017,7 +1122,7 @@ __global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict
     }
     double g = 0.0;
     for (int64_t y = 0; y < dsplit; ++y) g += gpart[(y * k + a) * k + j];
-    double h = d_half_angle(d_clamp(g)) + kCcSlack;
+    double h = d_half_angle(d_clamp(g + kGramDelta)) + kCcSlack;
     if (h > 1.0) h = 1.0;
     const float f = __double2float_ru(h);
     cc[a * k + j] = f;
@@ -1042,6 +1147,19 @@ __global__ void k_load_centers(int64_t k, int64_t d, int64_t kp, const double *_
     const double v = src[e];
     cent64[e] = v;
     ct32[t * kp + j] = (float)v;
+}
+
+// CentroidSet.from_data_rows (engine.py:46-58) on the device: k packed seed
+// rows (float64 values) scattered into zeroed cent64 / ct32.
+__global__ void k_seed_rows(int64_t d, int64_t kp, const int64_t *__restrict__ sptr, const int32_t *__restrict__ sidx,
+                            const double *__restrict__ sval, double *cent64, float *ct32) {
+    const int64_t j = blockIdx.x;
+    for (int64_t t = sptr[j] + threadIdx.x; t < sptr[j + 1]; t += blockDim.x) {
+        const int c = sidx[t];
+        const double v = sval[t];
+        cent64[j * d + c] = v;
+        ct32[(int64_t)c * kp + j] = (float)v;
+    }
 }
 
 __global__ void k_geometry(int op, int64_t n, const double *a, const double *b, double *out) {
@@ -1069,6 +1187,7 @@ ColPlan col_plan(int64_t k) {
     p.tpr = (int)((k + ch - 1) / ch);
     if (p.tpr > 32) p.tpr = 32;
     p.rpw = 32 / p.tpr;
+    if (p.rpw > 8) p.rpw = 8;   // k_row_pass stages at most 8 rows per warp
     return p;
 }
 
@@ -1156,7 +1275,7 @@ int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B
 int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_s,
                          void *stream) {
     if (X->n == 0) return 0;
-    const int grid = grid_for(X->n, 256);
+    const int grid = grid_for(X->n, 8);
     k_hamerly_tighten<<<grid, 256, 0, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
                                                    B->a, B->l, B->u, C->s, use_s, W->surv1, W->surv2, W->ctr);
     CHECK_LAUNCH("hamerly_tighten");
@@ -1279,7 +1398,7 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     const int64_t ntiles = tk * (tk + 1) / 2;
     const int64_t ds = spkm_gram_dsplit(C->k, C->d);
     dim3 grid((unsigned)ntiles, (unsigned)ds);
-    k_gram_part<<<grid, 64, 0, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart);
+    k_gram_part<<<grid, 128, 0, st>>>(C->k, C->d, C->kp, ds, C->ct32, tiles_dev, C->sinp, full, gpart);
     CHECK_LAUNCH("gram_part");
     k_gram_final<<<(unsigned)((C->k * C->k + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, C->cc);
     CHECK_LAUNCH("gram_final");
@@ -1331,6 +1450,17 @@ int spkm_load_centers(const spkm_centers *C, const double *src, void *stream) {
     k_load_centers<<<(unsigned)((tot + 255) / 256), 256, 0, S(stream)>>>(C->k, C->d, C->kp, src, C->cent64,
                                                                          C->ct32);
     CHECK_LAUNCH("load_centers");
+    return 0;
+}
+
+int spkm_seed_rows(const spkm_centers *C, const int64_t *sptr, const int32_t *sidx, const double *sval,
+                   void *stream) {
+    cudaStream_t st = S(stream);
+    cudaError_t e = cudaMemsetAsync(C->cent64, 0, sizeof(double) * C->k * C->d, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(C->ct32, 0, sizeof(float) * C->kp * C->d, st);
+    if (e != cudaSuccess) return fail("seed_rows memset", e);
+    k_seed_rows<<<(unsigned)C->k, 128, 0, st>>>(C->d, C->kp, sptr, sidx, sval, C->cent64, C->ct32);
+    CHECK_LAUNCH("seed_rows");
     return 0;
 }
 

@@ -347,6 +347,21 @@ class Engine:
         self.stream.synchronize()
         del keep
 
+    def seed_rows(self, data: Dataset, rows):
+        """Seed centers = the given data rows (CentroidSet.from_data_rows) built on the device."""
+        rows = np.asarray(rows, dtype=np.int64)
+        starts, ends = data.indptr[rows], data.indptr[rows + 1]
+        sptr = np.zeros(rows.size + 1, np.int64)
+        np.cumsum(ends - starts, out=sptr[1:])
+        sel = np.concatenate([np.arange(s, e) for s, e in zip(starts, ends)]) if rows.size else np.zeros(0, np.int64)
+        dev = self.device
+        t_ptr = torch.from_numpy(sptr).to(dev)
+        t_idx = torch.from_numpy(np.ascontiguousarray(data.indices[sel], np.int32)).to(dev)
+        t_val = torch.from_numpy(np.ascontiguousarray(data.data[sel], np.float64)).to(dev)
+        _lib.call("spkm_seed_rows", self.C.struct, _ptr(t_ptr), _ptr(t_idx), _ptr(t_val), self.sp)
+        self.stream.synchronize()
+        self.seed_h2d_bytes = int(sptr.nbytes + t_idx.numel() * 4 + t_val.numel() * 8)
+
     def reset(self):
         _lib.call("spkm_reset_counters", self.P.work, self.sp)
 
@@ -458,15 +473,23 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
         init_centers: np.ndarray | None = None, comm=None, n_total: int | None = None,
         seed_indices=None) -> ClusteringResult:
     """Cluster ``data`` into ``k`` groups (reference engine.run, engine.py:201-346)."""
-    from .seeding import SeedConfig, make_centroids
+    from .seeding import SeedConfig, make_centroids, uniform_rows
 
     _validate(data, k, variant, hamerly_update)
+    cfg = seeding if seeding is not None else SeedConfig()
     if init_centers is None:
-        cents0 = make_centroids(data, k, seeding if seeding is not None else SeedConfig())
-        init_centers, seed_indices = cents0.centers, cents0.seed_indices
+        cfg.validate()
+        if cfg.method == "uniform":
+            seed_indices = np.asarray(uniform_rows(data.n, k, cfg.seed), dtype=np.int64)
+        else:
+            cents0 = make_centroids(data, k, cfg)
+            init_centers, seed_indices = cents0.centers, cents0.seed_indices
     eng = Engine(data, k, variant, device=device, hamerly_update=hamerly_update, corpus=corpus, comm=comm,
                  n_total=n_total)
-    eng.load_centers(init_centers)
+    if init_centers is None:
+        eng.seed_rows(data, seed_indices)
+    else:
+        eng.load_centers(init_centers)
     eng.reset()
     cc_per_it = k * (k - 1) // 2 if variant in _CC_VARIANTS else 0
     stats: list = []

@@ -253,17 +253,61 @@ def test_single_nnz_rows_and_duplicates():
 
 
 def test_max_length_rows(oracle_mod):
-    """Rows at the 400-nnz clip and at d-dense lengths."""
+    """Rows at the generator's 400-nnz clip mixed with 1-nnz rows."""
     m = spk()
-    from paper_2107_04074_b200 import synth
-    spec = synth.CorpusSpec("long", 300, 600, 300, min_nnz=200, max_nnz=400)
-    data = synth.sparse_corpus(spec, seed=11)
+    g = np.random.default_rng(11)
+    n, d = 300, 5000
+    lens = np.where(np.arange(n) % 3 == 0, 400, np.where(np.arange(n) % 3 == 1, 1, 37))
+    ip = np.concatenate([[0], np.cumsum(lens)])
+    idx = np.concatenate([np.sort(g.choice(d, L, replace=False)) for L in lens])
+    val = g.uniform(0.1, 1.0, idx.size)
+    data = m.Dataset.from_csr(ip, idx, val, d)
     assert data.row_lengths().max() == 400
     X = oracle_mod.CSR(data.indptr, data.indices, data.data, data.dim)
     ref = oracle_mod.run(X, 8, "standard", seed=5, max_iter=50)
     margin = oracle_mod.margins(X, ref["centers"])
+    base = None
     for v in VARIANTS:
         r = m.run(data, 8, v, m.SeedConfig(seed=5), max_iter=50)
         ok = margin > 1e-5
         assert np.array_equal(r.assignments[ok], ref["assignments"][ok]), v
         assert r.objective == pytest.approx(ref["objective"][-1], rel=1e-6)
+        base = base or r
+        assert np.array_equal(r.assignments, base.assignments), v
+
+
+@pytest.mark.parametrize("name,k", [("C1", 20), ("grid_200_5000_50_1007", 50), ("signed", 6)])
+def test_center_thresholds_upper_bound(name, k):
+    """cc from the 3xTF32 tensor-core Gram is an upper bound within 1e-4 of the float64 half-angle cosine."""
+    from paper_2107_04074_b200 import engine as E
+    z = load_golden(name)
+    data = golden_dataset(z)
+    eng = E.Engine(data, k, "elkan")
+    eng.seed_rows(data, np.arange(k))
+    eng.reset()
+    eng.iteration(1)
+    eng.center_thresholds()
+    torch.cuda.synchronize()
+    C = eng.C.host_centers()
+    G = np.clip(C @ C.T, -1, 1)
+    cc_ref = np.sqrt(np.maximum(0.0, (G + 1) / 2))
+    np.fill_diagonal(cc_ref, -1.0)
+    cc = eng.C.cc.view(k, k).cpu().numpy().astype(np.float64)
+    off = ~np.eye(k, dtype=bool)
+    assert np.all(cc[off] >= cc_ref[off]), float(np.min(cc[off] - cc_ref[off]))
+    assert np.max(cc[off] - cc_ref[off]) < 1e-4
+    s = eng.C.s.cpu().numpy()
+    assert np.array_equal(s, np.where(off, cc, -np.inf).max(axis=1).astype(np.float32))
+
+
+def test_seed_rows_match_host_densify():
+    from paper_2107_04074_b200 import engine as E
+    z = load_golden("C1")
+    data = golden_dataset(z)
+    rows = [5, 17, 1999, 0]
+    eng = E.Engine(data, 4, "standard")
+    eng.seed_rows(data, rows)
+    torch.cuda.synchronize()
+    assert np.array_equal(eng.C.host_centers(), data.densify_rows(rows))
+    ct = eng.C.ct32.view(data.dim, eng.C.kp)[:, :4].cpu().numpy()
+    assert np.array_equal(ct, data.densify_rows(rows).T.astype(np.float32))

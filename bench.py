@@ -26,7 +26,6 @@ from __future__ import annotations
 import argparse
 import json
 import os
-import subprocess
 import sys
 import threading
 import time
@@ -66,55 +65,56 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampler running during the timed region."""
+    """NVML sampler (every 5 ms) running during the timed region: SM clock + throttle reasons."""
 
-    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
-         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
-         "clocks_event_reasons.sw_power_cap")
+    REASONS = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+               "sw_power_cap": 0x4, "hw_power_brake_slowdown": 0x80}
 
-    def __init__(self, index=0):
-        self.index = index
+    def __init__(self, index=0, period=0.005):
+        self.index, self.period = index, period
         self.samples = []
-        self.proc = None
+        self.max_mhz = None
+        self._stop = threading.Event()
 
     def __enter__(self):
         try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-            self.t = threading.Thread(target=self._read, daemon=True)
+            import pynvml as nv
+            nv.nvmlInit()
+            self.nv = nv
+            self.h = nv.nvmlDeviceGetHandleByIndex(self.index)
+            self.max_mhz = float(nv.nvmlDeviceGetMaxClockInfo(self.h, nv.NVML_CLOCK_SM))
+            self.t = threading.Thread(target=self._run, daemon=True)
             self.t.start()
-        except Exception:
-            self.proc = None
+        except Exception as e:  # no NVML: report why
+            self.error = repr(e)
+            self.nv = None
         return self
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.samples.append([x.strip() for x in line.split(",")])
+    def _run(self):
+        nv = self.nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((float(sm), int(rs)))
+            except Exception:
+                pass
+            time.sleep(self.period)
 
     def __exit__(self, *a):
-        if self.proc:
-            self.proc.terminate()
-            try:
-                self.proc.wait(2)
-            except Exception:
-                self.proc.kill()
+        self._stop.set()
+        if self.nv is not None:
+            self.t.join(1.0)
         return False
 
     def summary(self):
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for s in self.samples:
-            try:
-                sm.append(float(s[0]))
-                mx = float(s[1])
-                for nm, flag in zip(names, s[3:7]):
-                    if flag.lower().startswith("active"):
-                        reasons.add(nm)
-            except Exception:
-                continue
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": self.max_mhz, "reasons": [], "samples": 0,
+                    "note": getattr(self, "error", "no samples")}
+        sm = [s for s, _ in self.samples]
+        reasons = sorted({nm for _, r in self.samples for nm, bit in self.REASONS.items() if r & bit})
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": self.max_mhz, "reasons": reasons,
+                "samples": len(sm), "source": "nvml every 5 ms"}
 
 
 # ----------------------------------------------------------------- workload
@@ -201,14 +201,14 @@ def main_ours(args):
     data, gen_s = load_workload(args)
     variants = args.variants.split(",")
     k = args.k
-    cents0 = make_centroids(data, k, SeedConfig(seed=args.seed))
+    from paper_2107_04074_b200.seeding import uniform_rows
+    seed_rows = uniform_rows(data.n, k, args.seed)
     if world > 1:
         from paper_2107_04074_b200.distributed import Exchange, shard_rows
         rows = shard_rows(data.indptr, world)[rank]
     else:
         rows = (0, data.n)
     corpus = DeviceCorpus(data, dev, rows=rows)
-    cent_dev = torch.from_numpy(np.ascontiguousarray(cents0.centers)).to(dev)   # resident seed centers
     torch.cuda.synchronize()
 
     def fit_all(corpus_, tag=None):
@@ -216,8 +216,8 @@ def main_ours(args):
         per = {}
         for v in variants:
             comm = Exchange(k, data.dim, dev) if world > 1 else None
-            r = run(data, k, v, max_iter=args.max_iter, device=dev, corpus=corpus_, init_centers=cent_dev,
-                    comm=comm, n_total=data.n, seed_indices=cents0.seed_indices)
+            r = run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=corpus_,
+                    comm=comm, n_total=data.n)
             its += len(r.iterations)
             sims += r.total_sims
             nk += data.n * k * len(r.iterations)
@@ -281,7 +281,7 @@ def main_ours(args):
             comm = Exchange(k, data.dim, dev) if world > 1 else None
             r = spk.run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=c,
                         comm=comm, n_total=data.n)
-            h2d += int(k * 8 + sum(int(data.indptr[j + 1] - data.indptr[j]) for j in cents0.seed_indices) * 12)
+            h2d += int(k * 8 + sum(int(data.indptr[j + 1] - data.indptr[j]) for j in seed_rows) * 12)
             d2h += r.assignments.nbytes
         e1.record()
         barrier()
@@ -293,7 +293,7 @@ def main_ours(args):
     e2e_val = its_tot / (float(e2e_ms.item()) / 1e3)
 
     # ---- instrumented pass: per-entry-point event times -> roofline ----
-    roof = roofline(args, data, corpus, cents0, cent_dev, dev, world)
+    roof = roofline(args, data, corpus, dev, world)
 
     if rank != 0:
         dist.destroy_process_group()
@@ -319,12 +319,13 @@ def main_ours(args):
         dist.destroy_process_group()
 
 
-def roofline(args, data, corpus, cents0, cent_dev, dev, world):
+def roofline(args, data, corpus, dev, world):
     """Time every entry point with CUDA events over one step; bytes from SURVEY.md §8(d)."""
     import torch
     from paper_2107_04074_b200 import _lib
     from paper_2107_04074_b200.engine import run
     from paper_2107_04074_b200.distributed import Exchange
+    from paper_2107_04074_b200.seeding import SeedConfig
 
     pk, src = peaks()
     n, nnz, k = corpus.n, corpus.nnz, args.k
@@ -334,8 +335,8 @@ def roofline(args, data, corpus, cents0, cent_dev, dev, world):
         for v in args.variants.split(","):
             prof.tag = v
             comm = Exchange(k, data.dim, dev) if world > 1 else None
-            r = run(data, k, v, max_iter=args.max_iter, device=dev, corpus=corpus, init_centers=cent_dev,
-                    comm=comm, n_total=data.n, seed_indices=cents0.seed_indices)
+            r = run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=corpus,
+                    comm=comm, n_total=data.n)
             its = r.iterations
             ku = (k + 3) // 4 * 4
             csr_full = 8 * nnz + 8 * n + 4 * n          # indices+values, indptr, row eps
@@ -347,11 +348,11 @@ def roofline(args, data, corpus, cents0, cent_dev, dev, world):
             bytes_by[("spkm_full_assign", v)] = b
             if v in ("hamerly", "simp_hamerly"):
                 bytes_by[("spkm_hamerly_bounds", v)] = 24 * n * (len(its) - 1)
-                bytes_by[("spkm_hamerly_tighten", v)] = sum(8 * s.survivors + 12 * s.survivors for s in its[1:]) \
-                    + sum(8 * 0 for _ in its)
-                bytes_by[("spkm_hamerly_rescan", v)] = sum(12 * s.survivors2 for s in its[1:])
+                bytes_by[("spkm_hamerly_tighten", v)] = sum(8 * s.nnz_tighten + 24 * s.survivors for s in its[1:])
+                bytes_by[("spkm_hamerly_rescan", v)] = sum(8 * s.nnz_rescan + 24 * s.survivors2 for s in its[1:])
             if v in ("elkan", "simp_elkan"):
                 bytes_by[("spkm_elkan_bounds", v)] = (8 * ku + 16) * n * (len(its) - 1)
+                bytes_by[("spkm_elkan_scan", v)] = sum(8 * s.nnz_elkan + (8 * ku + 16) * s.survivors for s in its[1:])
     torch.cuda.synchronize()
     times = prof.times_ms()
     calls = {}

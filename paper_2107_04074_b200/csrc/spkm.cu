@@ -335,60 +335,6 @@ __global__ void __launch_bounds__(256) k_row_pass(RowPassArgs A) {
     }
 }
 
-// ------------------------------------------------ warp-cooperative pair dots
-// s~(i, cand[c]) for the m <= 32 candidate centers listed in `cand` (one row
-// i = [s, e)).  Per 32-nnz chunk: lane L loads (idx_L, val_L) and gathers the
-// m center values ct[idx_L * kp + cand[c]] into tile[L][c] (m independent
-// loads per lane); lane c then runs the canonical FMA chain down column c.
-// Returns the value in lane c < m (bit-identical to dot_pair / k_row_pass).
-struct DotSmem {
-    float tile[32][33];
-    float val[32];
-    int32_t cand[64];
-};
-__device__ __forceinline__ float warp_dots(const int32_t *__restrict__ idx, const float *__restrict__ val, int64_t s,
-                                           int64_t e, const float *__restrict__ ct, int64_t kp, int m,
-                                           DotSmem &sm) {
-    const int lane = threadIdx.x & 31;
-    float acc = 0.f;
-    for (int64_t base = s; base < e; base += 32) {
-        const int cnt = (int)min((int64_t)32, e - base);
-        int myidx = 0;
-        float myval = 0.f;
-        if (lane < cnt) {
-            myidx = __ldg(idx + base + lane);
-            myval = __ldg(val + base + lane);
-        }
-        sm.val[lane] = myval;
-        if (lane < cnt) {
-            const float *rowp = ct + (int64_t)myidx * kp;
-            int c = 0;
-            for (; c + 4 <= m; c += 4) {
-                const float x0 = __ldg(rowp + sm.cand[c]), x1 = __ldg(rowp + sm.cand[c + 1]);
-                const float x2 = __ldg(rowp + sm.cand[c + 2]), x3 = __ldg(rowp + sm.cand[c + 3]);
-                sm.tile[lane][c] = x0;
-                sm.tile[lane][c + 1] = x1;
-                sm.tile[lane][c + 2] = x2;
-                sm.tile[lane][c + 3] = x3;
-            }
-            for (; c < m; ++c) sm.tile[lane][c] = __ldg(rowp + sm.cand[c]);
-        }
-        __syncwarp();
-        if (lane < m) {
-            int t = 0;
-            for (; t + 4 <= cnt; t += 4) {
-                acc = __fmaf_rn(sm.val[t], sm.tile[t][lane], acc);
-                acc = __fmaf_rn(sm.val[t + 1], sm.tile[t + 1][lane], acc);
-                acc = __fmaf_rn(sm.val[t + 2], sm.tile[t + 2][lane], acc);
-                acc = __fmaf_rn(sm.val[t + 3], sm.tile[t + 3][lane], acc);
-            }
-            for (; t < cnt; ++t) acc = __fmaf_rn(sm.val[t], sm.tile[t][lane], acc);
-        }
-        __syncwarp();
-    }
-    return acc;
-}
-
 // --------------------------------------------------------- Hamerly family
 // engine.py:274 (l), 284-303 (u) fused with the kernels.py:81-87 tests.
 __global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *__restrict__ reps,
@@ -440,8 +386,10 @@ __global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *
     }
 }
 
-// kernels.py:88-95: tighten l with the exact s~(i,a), re-test.  Warp per
-// survivor (the row's gathers are issued 32 at a time, see warp_dots).
+// kernels.py:88-95: tighten l with the exact s~(i,a), re-test.  8 lanes per
+// survivor, 4 survivors per warp: per 32-nnz chunk each lane loads 4
+// (idx, val) pairs and gathers the 4 center values ct[idx * kp + a(i)]
+// (all independent), then the group leader runs the canonical chain.
 __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restrict__ indptr,
                                                          const int32_t *__restrict__ indices,
                                                          const float *__restrict__ values,
@@ -452,37 +400,59 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
                                                          const float *__restrict__ s_arr, int use_s,
                                                          const int32_t *__restrict__ surv1, int32_t *surv2,
                                                          long long *ctr) {
-    __shared__ DotSmem sm_all[8];
+    __shared__ float s_v[8][4][32];
+    __shared__ float s_c[8][4][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    DotSmem &sm = sm_all[wib];
-    const int wpb = blockDim.x >> 5;
+    const int g = lane >> 3, q = lane & 7;
+    float *sv = s_v[wib][g];
+    float *sc = s_c[wib][g];
     const long long cnt = ctr[SPKM_CTR_SURV1];
-    long long sims = 0, nnz = 0;
-    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < cnt; w += (int64_t)gridDim.x * wpb) {
-        const int32_t i = surv1[w];
-        const int ai = a[i];
-        const int64_t s = indptr[i], e = indptr[i + 1];
-        if (lane == 0) sm.cand[0] = ai;
-        __syncwarp();
-        const float sa = warp_dots(indices, values, s, e, ct, kp, 1, sm);
-        if (lane == 0) {
+    const int64_t nslots = (cnt + 3) / 4;
+    const int wpb = blockDim.x >> 5;
+    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
+        const int64_t slot = w * 4 + g;
+        const bool valid = slot < cnt;
+        const int32_t i = valid ? surv1[slot] : 0;
+        const int ai = valid ? a[i] : 0;
+        const int64_t s = valid ? indptr[i] : 0, e = valid ? indptr[i + 1] : 0;
+        const int len = (int)(e - s);
+        const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
+        const float *cta = ct + ai;
+        float acc = 0.f;
+        for (int c0 = 0; c0 < maxlen; c0 += 32) {
+            const int cntc = max(0, min(32, len - c0));
+            int ix[4];
+            float vx[4], cx[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int t = q + 8 * r;
+                ix[r] = t < cntc ? __ldg(indices + s + c0 + t) : 0;
+                vx[r] = t < cntc ? __ldg(values + s + c0 + t) : 0.f;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) cx[r] = (q + 8 * r < cntc) ? __ldg(cta + (int64_t)ix[r] * kp) : 0.f;
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                sv[q + 8 * r] = vx[r];
+                sc[q + 8 * r] = cx[r];
+            }
+            __syncwarp();
+            if (q == 0)
+                for (int t = 0; t < cntc; ++t) acc = __fmaf_rn(sv[t], sc[t], acc);
+            __syncwarp();
+        }
+        bool surv = false;
+        if (valid && q == 0) {
             const double eps = (double)reps[i];
-            const double lb = (double)sa - eps;
+            const double lb = (double)acc - eps;
             l[i] = store_lower(lb);
             bool pruned = (use_s && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb);
-            if (!pruned) pruned = ((double)u[i] + eps <= (double)sa);
-            if (!pruned) {
-                const long long p = atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV2), 1ull);
-                surv2[p] = i;
-            }
-            sims += 1;
-            nnz += e - s;
+            if (!pruned) pruned = ((double)u[i] + eps <= (double)acc);
+            surv = !pruned;
         }
-        __syncwarp();
-    }
-    if (lane == 0 && sims) {
-        atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SIMS), (unsigned long long)sims);
-        atomicAdd((unsigned long long *)(ctr + SPKM_CTR_NNZ_TIGHTEN), (unsigned long long)nnz);
+        warp_append(surv, i, surv2, 0, nullptr, ctr + SPKM_CTR_SURV2);
+        warp_add(ctr + SPKM_CTR_SIMS, (valid && q == 0) ? 1 : 0);
+        warp_add(ctr + SPKM_CTR_NNZ_TIGHTEN, (valid && q == 0) ? (long long)len : 0);
     }
 }
 
@@ -537,10 +507,20 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
     }
 }
 
-// kernels.py:48-65 for the surviving points: tighten once, re-test every
-// j against s~(i,a) (and strictly against a better non-incumbent found so
-// far), compute the survivors 32 at a time with warp_dots, keep the best
-// with the tie rule.
+// kernels.py:22-66 for the surviving points, in two steps:
+//  1. gather pass, blocked by 32-byte sectors: centers are grouped in blocks
+//     of 8 (one sector of a term-major ct32 row); a block is fetched when it
+//     holds a(i) or any center failing the drift-updated test
+//     (u + 2 eps <= l, cc + sqrt2 eps <= l).  Lane = block, bpr lanes per
+//     point, up to 8 points per warp, rounds of 32 blocks for k > 256.  The
+//     canonical s~ of every fetched center lands in shared memory.
+//  2. the reference's sequential scan (kernels.py:35-65) replayed by the
+//     group's leader lane over j = 0..k-1 on those values: tighten at the
+//     first failing j, re-test against the running best (cc and u tests
+//     with the eps margins), "compute" = read s~, strict > reassignment.
+//     Every center the replay needs was fetched (a center skipped by the
+//     pre-test also fails every later test, since the running best only
+//     grows), so sim_count counts exactly what the reference's loop counts.
 __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ indptr,
                                                     const int32_t *__restrict__ indices,
                                                     const float *__restrict__ values,
@@ -550,80 +530,146 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                                                     const float *__restrict__ cc, int use_cc,
                                                     const int32_t *__restrict__ surv1, int32_t *mv_i,
                                                     int32_t *mv_old, long long *ctr) {
-    __shared__ DotSmem sm_all[8];
+    constexpr int UB = 4;
+    __shared__ int32_t s_idx[8][8][32];
+    __shared__ float s_val[8][8][32];
+    __shared__ float s_sim[8][1024];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    DotSmem &sm = sm_all[wib];
-    const int wpb = blockDim.x >> 5;
+    const int nb = (k + 7) >> 3;
+    const int bpr = nb < 32 ? nb : 32;
+    const int ppw = min(8, 32 / bpr);
+    const int nrounds = (nb + 31) >> 5;
+    const int g = lane / bpr, q = lane - g * bpr;
+    const bool lane_on = g < ppw;
+    const int gstride = (ppw > 1) ? 32 : 1024;       // per-group slice of s_sim
+    float *my_sim = s_sim[wib] + (lane_on ? g : 0) * gstride;
+    int32_t *my_idx = s_idx[wib][lane_on ? g : 0];
+    float *my_val = s_val[wib][lane_on ? g : 0];
     const long long cnt = ctr[SPKM_CTR_SURV1];
-    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < cnt; w += (int64_t)gridDim.x * wpb) {
-        const int32_t i = surv1[w];
-        const int ai = a[i];
-        const int64_t s = indptr[i], e = indptr[i + 1];
-        const double eps = (double)reps[i];
-        if (lane == 0) sm.cand[0] = ai;
-        __syncwarp();
-        float sa = warp_dots(indices, values, s, e, ct, kp, 1, sm);
-        sa = __shfl_sync(FULL, sa, 0);
+    const int64_t nslots = (cnt + ppw - 1) / ppw;
+    const int wpb = blockDim.x >> 5;
+    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
+        const int64_t slot = w * ppw + g;
+        const bool valid = lane_on && slot < cnt;
+        const int32_t i = valid ? surv1[slot] : 0;
+        const int ai = valid ? a[i] : 0;
+        const int64_t s = valid ? indptr[i] : 0, e = valid ? indptr[i + 1] : 0;
+        const int len = (int)(e - s);
+        const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
+        const double eps = valid ? (double)reps[i] : 0.0;
+        const double lb = valid ? (double)l[i] : 0.0;
         float *ui = u + (int64_t)i * ku;
-        if (lane == 0) ui[ai] = store_upper((double)sa + eps);
-        const double lb = (double)sa - eps;
-        float best_b = sa;
-        int best_j = ai;
-        long long sims = 1;
-        int pos = 0;
-        for (int base = 0; base < k; base += 32) {
-            const int j = base + lane;
-            bool cand = false;
-            if (j < k && j != ai) {
-                const double uij = (double)ui[j];
-                bool prune = use_cc && lb >= 0.0 && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb;
-                if (!prune) prune = (uij + eps <= (double)sa);
-                if (!prune && best_j != ai) prune = (uij + eps < (double)best_b);
-                cand = !prune;
+        const bool cc_ok = use_cc && lb >= 0.0;
+        for (int r = 0; r < nrounds; ++r) {
+            const int blk = r * 32 + q;
+            const int j0 = blk * 8;
+            bool act = false;
+            if (valid && blk < nb) {
+                for (int c2 = 0; c2 < 8; ++c2) {
+                    const int j = j0 + c2;
+                    if (j >= k) break;
+                    if (j == ai) {
+                        act = true;
+                        continue;
+                    }
+                    bool prune = cc_ok && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb;
+                    if (!prune) prune = ((double)ui[j] + 2.0 * eps <= lb);
+                    act |= !prune;
+                }
             }
-            const unsigned m = __ballot_sync(FULL, cand);
-            __syncwarp();
-            if (cand) sm.cand[pos + __popc(m & ((1u << lane) - 1u))] = j;
-            pos += __popc(m);
-            __syncwarp();
-            const bool last = base + 32 >= k;
-            while (pos >= 32 || (last && pos > 0)) {
-                const int mm = pos >= 32 ? 32 : pos;
-                const float v = warp_dots(indices, values, s, e, ct, kp, mm, sm);
-                int jj = -2;
-                float vv = -INFINITY;
-                if (lane < mm) {
-                    jj = sm.cand[lane];
-                    vv = v;
-                    ui[jj] = store_upper((double)v + eps);
+            if (!__any_sync(FULL, act)) continue;
+            float acc[8];
+#pragma unroll
+            for (int c2 = 0; c2 < 8; ++c2) acc[c2] = 0.f;
+            const float4 *base4 = reinterpret_cast<const float4 *>(ct + j0);
+            for (int c0 = 0; c0 < maxlen; c0 += 32) {
+                const int cntc = max(0, min(32, len - c0));
+                for (int q2 = q; q2 < cntc; q2 += bpr) {
+                    my_idx[q2] = __ldg(indices + s + c0 + q2);
+                    my_val[q2] = __ldg(values + s + c0 + q2);
                 }
-                Top2 tp{vv, jj, -INFINITY};
-                for (int o = 16; o; o >>= 1) {
-                    const Top2 other = top2_shfl_down(tp, o);
-                    if (lane < o) top2_merge(tp, other, ai);
-                }
-                tp.b = __shfl_sync(FULL, tp.b, 0);
-                tp.bj = __shfl_sync(FULL, tp.bj, 0);
-                if (better(tp.b, tp.bj, best_b, best_j, ai)) {
-                    best_b = tp.b;
-                    best_j = tp.bj;
-                }
-                sims += mm;
                 __syncwarp();
-                if (lane < pos - mm) sm.cand[lane] = sm.cand[lane + 32];
+                if (act) {
+                    int uu = 0;
+                    for (; uu + UB <= cntc; uu += UB) {
+                        float4 x[UB][2];
+                        float vv[UB];
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) {
+                            vv[b] = my_val[uu + b];
+                            const float4 *p = base4 + ((int64_t)my_idx[uu + b] * kp >> 2);
+                            x[b][0] = __ldg(p);
+                            x[b][1] = __ldg(p + 1);
+                        }
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) {
+                            acc[0] = __fmaf_rn(vv[b], x[b][0].x, acc[0]);
+                            acc[1] = __fmaf_rn(vv[b], x[b][0].y, acc[1]);
+                            acc[2] = __fmaf_rn(vv[b], x[b][0].z, acc[2]);
+                            acc[3] = __fmaf_rn(vv[b], x[b][0].w, acc[3]);
+                            acc[4] = __fmaf_rn(vv[b], x[b][1].x, acc[4]);
+                            acc[5] = __fmaf_rn(vv[b], x[b][1].y, acc[5]);
+                            acc[6] = __fmaf_rn(vv[b], x[b][1].z, acc[6]);
+                            acc[7] = __fmaf_rn(vv[b], x[b][1].w, acc[7]);
+                        }
+                    }
+                    for (; uu < cntc; ++uu) {
+                        const float v0 = my_val[uu];
+                        const float4 *p = base4 + ((int64_t)my_idx[uu] * kp >> 2);
+                        const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
+                        acc[0] = __fmaf_rn(v0, x0.x, acc[0]);
+                        acc[1] = __fmaf_rn(v0, x0.y, acc[1]);
+                        acc[2] = __fmaf_rn(v0, x0.z, acc[2]);
+                        acc[3] = __fmaf_rn(v0, x0.w, acc[3]);
+                        acc[4] = __fmaf_rn(v0, x1.x, acc[4]);
+                        acc[5] = __fmaf_rn(v0, x1.y, acc[5]);
+                        acc[6] = __fmaf_rn(v0, x1.z, acc[6]);
+                        acc[7] = __fmaf_rn(v0, x1.w, acc[7]);
+                    }
+                }
                 __syncwarp();
-                pos -= mm;
+            }
+            if (act) {
+#pragma unroll
+                for (int c2 = 0; c2 < 8; ++c2) my_sim[j0 + c2] = acc[c2];
             }
         }
-        if (lane == 0) {
-            l[i] = store_lower((double)best_b - eps);
-            if (best_j != ai) a[i] = best_j;
+        __syncwarp();
+        // replay of kernels.py:35-65 by the group leader
+        int cur = ai;
+        float lcur = 0.f;
+        bool tightened = false;
+        long long sims = 0;
+        if (valid && q == 0) {
+            for (int j = 0; j < k; ++j) {
+                if (j == ai || j == cur) continue;
+                const double ub = (double)ui[j];
+                if (!tightened) {
+                    if (cc_ok && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb) continue;
+                    if (ub + 2.0 * eps <= lb) continue;
+                    lcur = my_sim[ai];              // tighten: l = s~(i,a)
+                    ui[ai] = store_upper((double)lcur + eps);
+                    tightened = true;
+                    ++sims;
+                }
+                const double lc = (double)lcur;
+                if (use_cc && lc - eps >= 0.0 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
+                if (ub + eps <= lc) continue;
+                const float sij = my_sim[j];
+                ++sims;
+                ui[j] = store_upper((double)sij + eps);
+                if (sij > lcur) {
+                    cur = j;
+                    lcur = sij;
+                }
+            }
+            l[i] = store_lower((double)lcur - eps);
+            if (cur != ai) a[i] = cur;
         }
-        warp_append(lane == 0 && best_j != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
-        if (lane == 0) {
-            atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SIMS), (unsigned long long)sims);
-            atomicAdd((unsigned long long *)(ctr + SPKM_CTR_NNZ_ELKAN), (unsigned long long)(e - s));
-        }
+        const bool leader = valid && q == 0;
+        warp_append(leader && cur != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
+        warp_add(ctr + SPKM_CTR_SIMS, sims);
+        warp_add(ctr + SPKM_CTR_NNZ_ELKAN, leader ? (long long)len : 0);
         __syncwarp();
     }
 }
@@ -804,8 +850,10 @@ __global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int
         double ch = 0.0, ob = 0.0;
         if (j >= 0) {
             const double nrm = norm[j];
+            const double inv_nrm = 1.0 / nrm;
             const long long *sj = sums + (int64_t)j * d;
             double *cj = cent64 + (int64_t)j * d;
+#pragma unroll
             for (int q = lane; q < kTileT; q += 32) {
                 const int64_t t = t0 + q;
                 float f = 0.f;
@@ -816,7 +864,7 @@ __global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int
                         ob = fma(v, old, ob);
                         f = (float)old;
                     } else {
-                        const double nv = v / nrm;
+                        const double nv = v * inv_nrm;
                         const double df = nv - old;
                         ch = fma(df, df, ch);
                         ob = fma(v, nv, ob);
@@ -1008,9 +1056,9 @@ __global__ void __launch_bounds__(1024) k_finalize(int64_t k, int32_t *touched, 
 // + 96 * 2^-22 (per-stage fp32 accumulation, truncating adds assumed)
 // times sum_t |c_a[t] c_j[t]| <= 1, i.e. < 2.4e-5; kGramDelta = 5e-5 is added
 // before the half-angle map so cc stays an upper bound.
-// Tiles: 32x32 outputs (upper triangle), 4 warps x (16 x 16).  A tile is
-// skipped when none of its clusters moved since the last call.
-constexpr int GT = 32;
+// Tiles: 64x64 outputs (upper triangle).  A tile is skipped when none of
+// its clusters moved since the last call.
+constexpr int GT = 64;
 constexpr double kGramDelta = 5e-5;
 __device__ __forceinline__ uint32_t to_tf32(float x) {
     uint32_t r;
@@ -1029,11 +1077,13 @@ __device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) 
     lo = to_tf32(x - __uint_as_float(hi));
 }
 
-__global__ void __launch_bounds__(128) k_gram_part(int64_t k, int64_t d, int64_t kp, int64_t dsplit,
+// 64x64 output tile per block (8 warps = 4 x 2, each 16 rows x 32 cols),
+// 32-term stages with the next stage prefetched into registers.
+__global__ void __launch_bounds__(256) k_gram_part(int64_t k, int64_t d, int64_t kp, int64_t dsplit,
                                                    const float *__restrict__ ct, const int2 *__restrict__ tiles,
                                                    const double *__restrict__ sinp, int full, double *gpart) {
-    __shared__ float As[32][40];   // [term][cluster]; stride 40 keeps fragment loads conflict-free
-    __shared__ float Bs[32][40];
+    __shared__ float As[32][GT + 8];   // [term][cluster]; stride 72 -> conflict-free fragment loads
+    __shared__ float Bs[32][GT + 8];
     __shared__ int need;
     const int2 tl = tiles[blockIdx.x];
     const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
@@ -1051,21 +1101,38 @@ __global__ void __launch_bounds__(128) k_gram_part(int64_t k, int64_t d, int64_t
     const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     const int wy = w >> 1, wx = w & 1, g = lane >> 2, t4 = lane & 3;
-    double accd[2][4];
+    // loader mapping: thread -> (term row lt, 8 consecutive clusters at lc)
+    const int lt = threadIdx.x >> 3, lc = (threadIdx.x & 7) * 8;
+    float ra[8], rb[8];
+    auto load = [&](int64_t tb) {
+        const int64_t t = tb + lt;
+        const bool tin = t < t1;
 #pragma unroll
-    for (int f = 0; f < 2; ++f)
+        for (int q = 0; q < 8; ++q) {
+            ra[q] = (tin && a0 + lc + q < k) ? __ldg(ct + t * kp + a0 + lc + q) : 0.f;
+            rb[q] = (tin && j0 + lc + q < k) ? __ldg(ct + t * kp + j0 + lc + q) : 0.f;
+        }
+    };
+    double accd[4][4];
+#pragma unroll
+    for (int f = 0; f < 4; ++f)
 #pragma unroll
         for (int q = 0; q < 4; ++q) accd[f][q] = 0.0;
+    if (t0 < t1) load(t0);
     for (int64_t tb = t0; tb < t1; tb += 32) {
-        for (int e2 = threadIdx.x; e2 < 32 * 32; e2 += blockDim.x) {
-            const int tt = e2 >> 5, cl = e2 & 31;
-            const int64_t t = tb + tt;
-            const bool tin = t < t1;
-            As[tt][cl] = (tin && a0 + cl < k) ? __ldg(ct + t * kp + a0 + cl) : 0.f;
-            Bs[tt][cl] = (tin && j0 + cl < k) ? __ldg(ct + t * kp + j0 + cl) : 0.f;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+            As[lt][lc + q] = ra[q];
+            Bs[lt][lc + q] = rb[q];
         }
         __syncthreads();
-        float dst[2][4] = {{0.f, 0.f, 0.f, 0.f}, {0.f, 0.f, 0.f, 0.f}};
+        if (tb + 32 < t1) load(tb + 32);
+        float dst[4][4];
+#pragma unroll
+        for (int f = 0; f < 4; ++f)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dst[f][q] = 0.f;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks) {
             const int kk = ks * 8;
@@ -1075,27 +1142,26 @@ __global__ void __launch_bounds__(128) k_gram_part(int64_t k, int64_t d, int64_t
             split_tf32(As[kk + t4 + 4][wy * 16 + g], ahi[2], alo[2]);
             split_tf32(As[kk + t4 + 4][wy * 16 + g + 8], ahi[3], alo[3]);
 #pragma unroll
-            for (int f = 0; f < 2; ++f) {
+            for (int f = 0; f < 4; ++f) {
                 uint32_t bhi[2], blo[2];
-                split_tf32(Bs[kk + t4][wx * 16 + f * 8 + g], bhi[0], blo[0]);
-                split_tf32(Bs[kk + t4 + 4][wx * 16 + f * 8 + g], bhi[1], blo[1]);
+                split_tf32(Bs[kk + t4][wx * 32 + f * 8 + g], bhi[0], blo[0]);
+                split_tf32(Bs[kk + t4 + 4][wx * 32 + f * 8 + g], bhi[1], blo[1]);
                 mma_tf32(dst[f], alo, bhi);
                 mma_tf32(dst[f], ahi, blo);
                 mma_tf32(dst[f], ahi, bhi);
             }
         }
 #pragma unroll
-        for (int f = 0; f < 2; ++f)
+        for (int f = 0; f < 4; ++f)
 #pragma unroll
             for (int q = 0; q < 4; ++q) accd[f][q] += (double)dst[f][q];
-        __syncthreads();
     }
 #pragma unroll
-    for (int f = 0; f < 2; ++f)
+    for (int f = 0; f < 4; ++f)
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int64_t ar = a0 + wy * 16 + g + ((q & 2) ? 8 : 0);
-            const int64_t jr = j0 + wx * 16 + f * 8 + t4 * 2 + (q & 1);
+            const int64_t jr = j0 + wx * 32 + f * 8 + t4 * 2 + (q & 1);
             if (ar < k && jr < k) gpart[((int64_t)blockIdx.y * k + ar) * k + jr] = accd[f][q];
         }
 }
@@ -1235,9 +1301,12 @@ int spkm_abi_version(void) { return SPKM_ABI_VERSION; }
 const char *spkm_last_error(void) { return g_err; }
 int64_t spkm_center_chunks(int64_t d) { return (d + kCenterChunk - 1) / kCenterChunk; }
 int64_t spkm_padded_k(int64_t k) {
+    // a multiple of 8 (one 32-byte sector per 8-center block) covering the
+    // row pass's tpr * ch columns
     const ColPlan p = col_plan(k);
     if (k > 32 * 32) return ((k + 1023) / 1024) * 1024;
-    return (int64_t)p.tpr * p.ch;
+    const int64_t c = (int64_t)p.tpr * p.ch;
+    return (c + 7) / 8 * 8;
 }
 
 int spkm_reset_counters(spkm_work *W, void *stream) {
@@ -1275,7 +1344,7 @@ int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B
 int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_s,
                          void *stream) {
     if (X->n == 0) return 0;
-    const int grid = grid_for(X->n, 8);
+    const int grid = grid_for((X->n + 3) / 4, 8);
     k_hamerly_tighten<<<grid, 256, 0, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
                                                    B->a, B->l, B->u, C->s, use_s, W->surv1, W->surv2, W->ctr);
     CHECK_LAUNCH("hamerly_tighten");
@@ -1398,7 +1467,7 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     const int64_t ntiles = tk * (tk + 1) / 2;
     const int64_t ds = spkm_gram_dsplit(C->k, C->d);
     dim3 grid((unsigned)ntiles, (unsigned)ds);
-    k_gram_part<<<grid, 128, 0, st>>>(C->k, C->d, C->kp, ds, C->ct32, tiles_dev, C->sinp, full, gpart);
+    k_gram_part<<<grid, 256, 0, st>>>(C->k, C->d, C->kp, ds, C->ct32, tiles_dev, C->sinp, full, gpart);
     CHECK_LAUNCH("gram_part");
     k_gram_final<<<(unsigned)((C->k * C->k + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, C->cc);
     CHECK_LAUNCH("gram_final");

@@ -136,7 +136,9 @@ class IterationStats:
     # instrumentation beyond the reference's fields (defaults keep its constructor)
     survivors: int = 0          # points failing the drift-updated bound test
     survivors2: int = 0         # Hamerly: points still failing after tightening
-    nnz_scanned: int = 0        # CSR nnz re-read by the survivor scans
+    nnz_tighten: int = 0        # CSR nnz re-read by the Hamerly tighten pass
+    nnz_rescan: int = 0         # CSR nnz re-read by the Hamerly full-k rescan
+    nnz_elkan: int = 0          # CSR nnz re-read by the Elkan survivor scan
 
 
 @dataclass
@@ -501,9 +503,8 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
         stats.append(IterationStats(iteration=it, sim_count=int(st[_lib.ST_SIMS]), cc_sim_count=cc_per_it,
                                     reassignments=reassign, objective=float(st[_lib.ST_OBJECTIVE]),
                                     elapsed_ns=time.monotonic_ns() - t0, survivors=int(st[_lib.ST_SURV1]),
-                                    survivors2=int(st[_lib.ST_SURV2]),
-                                    nnz_scanned=int(st[_lib.ST_NNZ_TIGHTEN] + st[_lib.ST_NNZ_RESCAN]
-                                                    + st[_lib.ST_NNZ_ELKAN])))
+                                    survivors2=int(st[_lib.ST_SURV2]), nnz_tighten=int(st[_lib.ST_NNZ_TIGHTEN]),
+                                    nnz_rescan=int(st[_lib.ST_NNZ_RESCAN]), nnz_elkan=int(st[_lib.ST_NNZ_ELKAN])))
         if k == 1 or st[_lib.ST_ALLONE] == 1.0 or (it >= 2 and reassign == 0):
             converged = True
             break

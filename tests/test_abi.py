@@ -35,7 +35,7 @@ def test_library_exports_every_declared_symbol():
     assert not missing, missing
     L = _lib.lib()                       # loads + binds every signature
     assert L.spkm_abi_version() == _lib.ABI_VERSION
-    assert L.spkm_padded_k(20) == 20 and L.spkm_padded_k(1000) == 1024
+    assert L.spkm_padded_k(20) == 24 and L.spkm_padded_k(100) == 104 and L.spkm_padded_k(1000) == 1024
 
 
 def test_struct_layouts_match_header():

@@ -510,16 +510,16 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
 // kernels.py:22-66 for the surviving points, in two steps:
 //  1. gather pass, blocked by 32-byte sectors: centers are grouped in blocks
 //     of 8 (one sector of a term-major ct32 row); a block is fetched when it
-//     holds a(i) or any center failing the drift-updated test
-//     (u + 2 eps <= l, cc + sqrt2 eps <= l).  Lane = block, bpr lanes per
+//     holds a(i) or any center failing the drift-updated u test
+//     (u + 2 eps <= l).  Lane = block, bpr lanes per
 //     point, up to 8 points per warp, rounds of 32 blocks for k > 256.  The
 //     canonical s~ of every fetched center lands in shared memory.
 //  2. the reference's sequential scan (kernels.py:35-65) replayed by the
 //     group's leader lane over j = 0..k-1 on those values: tighten at the
 //     first failing j, re-test against the running best (cc and u tests
 //     with the eps margins), "compute" = read s~, strict > reassignment.
-//     Every center the replay needs was fetched (a center skipped by the
-//     pre-test also fails every later test, since the running best only
+//     Every center the replay needs was fetched (a center passing the u
+//     pre-test also passes every later u test, since the running best only
 //     grows), so sim_count counts exactly what the reference's loop counts.
 __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ indptr,
                                                     const int32_t *__restrict__ indices,
@@ -541,7 +541,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     const int nrounds = (nb + 31) >> 5;
     const int g = lane / bpr, q = lane - g * bpr;
     const bool lane_on = g < ppw;
-    const int gstride = (ppw > 1) ? 32 : 1024;       // per-group slice of s_sim
+    const int gstride = 1024 / ppw;                   // per-group slice of s_sim (>= 8 * nb)
     float *my_sim = s_sim[wib] + (lane_on ? g : 0) * gstride;
     int32_t *my_idx = s_idx[wib][lane_on ? g : 0];
     float *my_val = s_val[wib][lane_on ? g : 0];
@@ -572,9 +572,10 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                         act = true;
                         continue;
                     }
-                    bool prune = cc_ok && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb;
-                    if (!prune) prune = ((double)ui[j] + 2.0 * eps <= lb);
-                    act |= !prune;
+                    // u-test only: a center the replay may need fails it (the
+                    // cc test depends on the running best, so it cannot
+                    // prune the fetch)
+                    act |= !((double)ui[j] + 2.0 * eps <= lb);
                 }
             }
             if (!__any_sync(FULL, act)) continue;

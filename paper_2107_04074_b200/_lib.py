@@ -139,6 +139,7 @@ class CallProfiler:
 
 
 _profiler = None
+_capture = None     # list collecting kernel counts while a CUDA graph is captured
 
 
 def build(verbose: bool = False) -> Path:
@@ -175,10 +176,22 @@ def lib():
     return L
 
 
+def active_profiler():
+    return _profiler
+
+
+def note_launches(n: int):
+    """Credit kernels launched outside call() (CUDA-graph replays) to the active profiler."""
+    if _profiler is not None:
+        _profiler.launches += n
+
+
 def call(name: str, *args):
     """Call an int-returning entry point and raise on a non-zero status."""
     L = lib()
     prof = _profiler
+    if _capture is not None:
+        _capture.append(KERNELS_PER_CALL.get(name, 0))
     if prof is not None:
         prof.launches += KERNELS_PER_CALL.get(name, 0)
         prof.calls[name] = prof.calls.get(name, 0) + 1

@@ -507,6 +507,16 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
     }
 }
 
+// floats of the per-warp value buffer of k_elkan_scan (9 per 8-center block)
+__host__ __device__ __forceinline__ int64_t elkan_sim_stride(int64_t k) {
+    const int64_t nb = (k + 7) / 8;
+    const int64_t need = nb * 9;
+    const int64_t bpr = nb < 32 ? nb : 32;
+    const int64_t ppw = (32 / bpr) < 8 ? (32 / bpr) : 8;
+    const int64_t per = need * ppw;
+    return per < 288 ? 288 : per;
+}
+
 // kernels.py:22-66 for the surviving points, in two steps:
 //  1. gather pass, blocked by 32-byte sectors: centers are grouped in blocks
 //     of 8 (one sector of a term-major ct32 row); a block is fetched when it
@@ -533,7 +543,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     constexpr int UB = 4;
     __shared__ int32_t s_idx[8][8][32];
     __shared__ float s_val[8][8][32];
-    __shared__ float s_sim[8][1024];
+    extern __shared__ float s_sim_dyn[];   // [8 warps][sim_stride]
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int nb = (k + 7) >> 3;
     const int bpr = nb < 32 ? nb : 32;
@@ -541,8 +551,10 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     const int nrounds = (nb + 31) >> 5;
     const int g = lane / bpr, q = lane - g * bpr;
     const bool lane_on = g < ppw;
-    const int gstride = 1024 / ppw;                   // per-group slice of s_sim (>= 8 * nb)
-    float *my_sim = s_sim[wib] + (lane_on ? g : 0) * gstride;
+    const int o0 = bpr > 1 ? (1 << (31 - __clz(bpr - 1))) : 0;
+    const int sim_stride = (int)elkan_sim_stride(k);  // floats per warp
+    const int gstride = sim_stride / ppw;             // per-group slice (>= 9 * nb)
+    float *my_sim = s_sim_dyn + wib * sim_stride + (lane_on ? g : 0) * gstride;
     int32_t *my_idx = s_idx[wib][lane_on ? g : 0];
     float *my_val = s_val[wib][lane_on ? g : 0];
     const long long cnt = ctr[SPKM_CTR_SURV1];
@@ -632,38 +644,115 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
             }
             if (act) {
 #pragma unroll
-                for (int c2 = 0; c2 < 8; ++c2) my_sim[j0 + c2] = acc[c2];
+                for (int c2 = 0; c2 < 8; ++c2) my_sim[blk * 9 + c2] = acc[c2];
             }
         }
         __syncwarp();
-        // replay of kernels.py:35-65 by the group leader
+        // replay of kernels.py:35-65, parallel over the group's lanes.  Lane q
+        // owns the centers of blocks q, q+32, ... (ascending j within the
+        // lane).  (A) tighten at the first j failing the pre-tests; (B) with
+        // the running best (cur, lcur) every lane finds its candidates and
+        // its first "event" (candidate beating lcur); the earliest event of
+        // the group updates (cur, lcur) and the scan resumes after it.
+        // Between events the state is constant, so the candidate set and the
+        // reassignments equal the reference's sequential loop.
         int cur = ai;
         float lcur = 0.f;
-        bool tightened = false;
         long long sims = 0;
-        if (valid && q == 0) {
-            for (int j = 0; j < k; ++j) {
-                if (j == ai || j == cur) continue;
-                const double ub = (double)ui[j];
-                if (!tightened) {
+        constexpr int NONE = 0x7fffffff;
+        int first_fail = NONE;
+        if (valid) {
+            for (int r = 0; r < nrounds && first_fail == NONE; ++r) {
+                const int blk = r * 32 + q;
+                if (blk >= nb) break;
+                for (int c2 = 0; c2 < 8; ++c2) {
+                    const int j = blk * 8 + c2;
+                    if (j >= k) break;
+                    if (j == ai) continue;
                     if (cc_ok && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb) continue;
-                    if (ub + 2.0 * eps <= lb) continue;
-                    lcur = my_sim[ai];              // tighten: l = s~(i,a)
-                    ui[ai] = store_upper((double)lcur + eps);
-                    tightened = true;
-                    ++sims;
-                }
-                const double lc = (double)lcur;
-                if (use_cc && lc - eps >= 0.0 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
-                if (ub + eps <= lc) continue;
-                const float sij = my_sim[j];
-                ++sims;
-                ui[j] = store_upper((double)sij + eps);
-                if (sij > lcur) {
-                    cur = j;
-                    lcur = sij;
+                    if ((double)ui[j] + 2.0 * eps <= lb) continue;
+                    first_fail = j;
+                    break;
                 }
             }
+        }
+        // group min (lanes of other groups hold their own values)
+        for (int o = o0; o; o >>= 1) {
+            const int other = __shfl_down_sync(FULL, first_fail, o);
+            if (q < o && q + o < bpr) first_fail = min(first_fail, other);
+        }
+        first_fail = __shfl_sync(FULL, first_fail, lane - q);
+        const bool tight = valid && first_fail != NONE;
+        if (tight) {
+            lcur = my_sim[(ai >> 3) * 9 + (ai & 7)];
+            if (q == 0) {
+                ui[ai] = store_upper((double)lcur + eps);
+                sims = 1;
+            }
+        }
+        int start = first_fail;
+        bool more = __any_sync(FULL, tight);
+        bool active_g = tight;
+        while (more) {
+            // lane-local pass over its j >= start with the current state
+            int ev = NONE;
+            if (active_g) {
+                const double lc = (double)lcur;
+                const bool ccok2 = use_cc && lc - eps >= 0.0;
+                for (int r = 0; r < nrounds && ev == NONE; ++r) {
+                    const int blk = r * 32 + q;
+                    if (blk >= nb) break;
+                    if (blk * 8 + 7 < start) continue;
+                    for (int c2 = 0; c2 < 8; ++c2) {
+                        const int j = blk * 8 + c2;
+                        if (j >= k) break;
+                        if (j < start || j == ai || j == cur) continue;
+                        if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
+                        if ((double)ui[j] + eps <= lc) continue;
+                        if (my_sim[blk * 9 + c2] > lcur) {
+                            ev = j;
+                            break;
+                        }
+                    }
+                }
+            }
+            int gev = ev;
+            for (int o = o0; o; o >>= 1) {
+                const int other = __shfl_down_sync(FULL, gev, o);
+                if (q < o && q + o < bpr) gev = min(gev, other);
+            }
+            gev = __shfl_sync(FULL, gev, lane - q);
+            // commit every candidate in [start, gev) (and the event itself)
+            if (active_g) {
+                const double lc = (double)lcur;
+                const bool ccok2 = use_cc && lc - eps >= 0.0;
+                for (int r = 0; r < nrounds; ++r) {
+                    const int blk = r * 32 + q;
+                    if (blk >= nb) break;
+                    if (blk * 8 + 7 < start || blk * 8 > gev) continue;
+                    for (int c2 = 0; c2 < 8; ++c2) {
+                        const int j = blk * 8 + c2;
+                        if (j >= k || j > gev) break;
+                        if (j < start || j == ai || j == cur) continue;
+                        if (j < gev) {
+                            if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
+                            if ((double)ui[j] + eps <= lc) continue;
+                        }
+                        ui[j] = store_upper((double)my_sim[blk * 9 + c2] + eps);
+                        ++sims;
+                    }
+                }
+                if (gev != NONE) {
+                    cur = gev;
+                    lcur = my_sim[(gev >> 3) * 9 + (gev & 7)];
+                    start = gev + 1;
+                } else {
+                    active_g = false;
+                }
+            }
+            more = __any_sync(FULL, active_g);
+        }
+        if (valid && q == 0 && tight) {
             l[i] = store_lower((double)lcur - eps);
             if (cur != ai) a[i] = cur;
         }
@@ -959,80 +1048,97 @@ __global__ void k_objective_final(int64_t k, int64_t nchunk, const double *__res
 // plus the sine bounds smax = max_j sinp_j and smax2 = max over j != owner_s
 // (owner_s = first argmax sinp).  hstat = {owner, p_min, p_min2, owner_s,
 // smax, smax2}.
-struct MinI {
-    double v;
-    int i;
+// Two smallest (value, index) pairs, ties broken by the lower index (the
+// stable argsort order of engine.py:285).
+struct Low2 {
+    double v1;
+    int i1;
+    double v2;
+    int i2;
 };
-__device__ __forceinline__ MinI min_first(MinI a, MinI b) { return (b.v < a.v || (b.v == a.v && b.i < a.i)) ? b : a; }
-__device__ __forceinline__ MinI block_min_first(MinI x, MinI *sh) {
-    for (int o = 16; o; o >>= 1) {
-        MinI y{__shfl_down_sync(FULL, x.v, o), __shfl_down_sync(FULL, x.i, o)};
-        x = min_first(x, y);
+__device__ __forceinline__ bool lt_vi(double v, int i, double w, int j) { return v < w || (v == w && i < j); }
+__device__ __forceinline__ void low2_push(Low2 &t, double v, int i) {
+    if (lt_vi(v, i, t.v1, t.i1)) {
+        t.v2 = t.v1;
+        t.i2 = t.i1;
+        t.v1 = v;
+        t.i1 = i;
+    } else if (lt_vi(v, i, t.v2, t.i2)) {
+        t.v2 = v;
+        t.i2 = i;
     }
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    __syncthreads();
-    if (lane == 0) sh[w] = x;
-    __syncthreads();
-    MinI r = sh[0];
-    for (int q = 1; q < (int)(blockDim.x >> 5); ++q) r = min_first(r, sh[q]);
-    return r;
+}
+__device__ __forceinline__ void low2_merge(Low2 &t, const Low2 &o) {
+    low2_push(t, o.v1, o.i1);
+    low2_push(t, o.v2, o.i2);
+}
+__device__ __forceinline__ Low2 low2_shfl(const Low2 &t, int o) {
+    return Low2{__shfl_down_sync(FULL, t.v1, o), __shfl_down_sync(FULL, t.i1, o), __shfl_down_sync(FULL, t.v2, o),
+                __shfl_down_sync(FULL, t.i2, o)};
 }
 
-__global__ void __launch_bounds__(1024) k_finalize(int64_t k, int32_t *touched, const int32_t *__restrict__ tlist,
-                                                   const int32_t *__restrict__ tcount, double *drift, double *sinp,
-                                                   const double *__restrict__ objc, double *hstat, long long *ctr,
-                                                   double *stats, long long sims_extra, int all) {
-    __shared__ double sh[32];
-    __shared__ MinI shm[32];
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    // untouched clusters: p = 1 (touched ones were set by k_center_reduce)
+constexpr int kFinThreads = 256;
+__global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *touched,
+                                                          const int32_t *__restrict__ tcount, double *drift,
+                                                          double *sinp, const double *__restrict__ objc,
+                                                          double *hstat, long long *ctr, double *stats,
+                                                          long long sims_extra, int all) {
+    __shared__ double s_ob[kFinThreads / 32];
+    __shared__ int s_no[kFinThreads / 32];
+    __shared__ Low2 s_p[kFinThreads / 32], s_s[kFinThreads / 32];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    double ob = 0.0;
+    int notone = 0;
+    Low2 pm{INFINITY, 0x7fffffff, INFINITY, 0x7fffffff}, sm = pm;
     for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
-        if (!(all || touched[j])) {
+        double p = 1.0, sp = 0.0;
+        if (all || touched[j]) {           // set by k_center_reduce this iteration
+            p = drift[j];
+            sp = sinp[j];
+        } else {                           // engine.py:149: untouched -> p = 1
             drift[j] = 1.0;
             sinp[j] = 0.0;
         }
-    }
-    __syncthreads();
-    double ob = 0.0, notone = 0.0;
-    MinI pm{INFINITY, 0x7fffffff}, sm{INFINITY, 0x7fffffff};
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+        touched[j] = 0;
         ob += objc[j];
-        const double p = drift[j];
-        if (p != 1.0) notone = 1.0;
-        pm = min_first(pm, MinI{p, (int)j});
-        sm = min_first(sm, MinI{-sinp[j], (int)j});
+        notone |= (p != 1.0);
+        low2_push(pm, p, (int)j);
+        low2_push(sm, -sp, (int)j);
     }
     for (int o = 16; o; o >>= 1) {
         ob += __shfl_down_sync(FULL, ob, o);
-        notone = fmax(notone, __shfl_down_sync(FULL, notone, o));
+        notone |= __shfl_down_sync(FULL, notone, o);
+        Low2 x = low2_shfl(pm, o), y = low2_shfl(sm, o);
+        low2_merge(pm, x);
+        low2_merge(sm, y);
     }
-    if (lane == 0) sh[w] = ob;
-    __syncthreads();
-    double tot = 0.0;
-    for (int q = 0; q < nw; ++q) tot += sh[q];
-    __syncthreads();
-    if (lane == 0) sh[w] = notone;
-    __syncthreads();
-    double no = 0.0;
-    for (int q = 0; q < nw; ++q) no = fmax(no, sh[q]);
-    const MinI own = block_min_first(pm, shm);
-    const MinI owns = block_min_first(sm, shm);
-    MinI pm2{INFINITY, 0x7fffffff}, sm2{INFINITY, 0x7fffffff};
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
-        if ((int)j != own.i) pm2 = min_first(pm2, MinI{drift[j], (int)j});
-        if ((int)j != owns.i) sm2 = min_first(sm2, MinI{-sinp[j], (int)j});
+    if (lane == 0) {
+        s_ob[w] = ob;
+        s_no[w] = notone;
+        s_p[w] = pm;
+        s_s[w] = sm;
     }
-    const MinI own2 = block_min_first(pm2, shm);
-    const MinI owns2 = block_min_first(sm2, shm);
+    __syncthreads();
     if (threadIdx.x == 0) {
-        hstat[0] = (double)own.i;
-        hstat[1] = own.v;
-        hstat[2] = (k > 1) ? own2.v : 1.0;
-        hstat[3] = (double)owns.i;
-        hstat[4] = -owns.v;
-        hstat[5] = (k > 1) ? -owns2.v : 0.0;
+        double tot = 0.0;
+        int no = 0;
+        Low2 P = s_p[0], Sx = s_s[0];
+        for (int q = 0; q < kFinThreads / 32; ++q) {
+            tot += s_ob[q];
+            no |= s_no[q];
+            if (q) {
+                low2_merge(P, s_p[q]);
+                low2_merge(Sx, s_s[q]);
+            }
+        }
+        hstat[0] = (double)P.i1;
+        hstat[1] = P.v1;
+        hstat[2] = (k > 1) ? P.v2 : 1.0;
+        hstat[3] = (double)Sx.i1;
+        hstat[4] = -Sx.v1;
+        hstat[5] = (k > 1) ? -Sx.v2 : 0.0;
         stats[SPKM_ST_OBJECTIVE] = tot;
-        stats[SPKM_ST_ALLONE] = (no == 0.0) ? 1.0 : 0.0;
+        stats[SPKM_ST_ALLONE] = no ? 0.0 : 1.0;
         stats[SPKM_ST_TOUCHED] = (double)*tcount;
         stats[SPKM_ST_SIMS] = (double)(ctr[SPKM_CTR_SIMS] + sims_extra);
         stats[SPKM_ST_REASSIGN] = (double)ctr[SPKM_CTR_MOVES];
@@ -1043,8 +1149,6 @@ __global__ void __launch_bounds__(1024) k_finalize(int64_t k, int32_t *touched, 
         stats[SPKM_ST_NNZ_ELKAN] = (double)ctr[SPKM_CTR_NNZ_ELKAN];
         for (int q = 0; q < 8; ++q) ctr[q] = 0;
     }
-    __syncthreads();
-    for (int64_t j = threadIdx.x; j < k; j += blockDim.x) touched[j] = 0;
 }
 
 // ---------------------------------------------------------- center thresholds
@@ -1383,7 +1487,9 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
                     void *stream) {
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
-    k_elkan_scan<<<grid, 256, 0, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
+    const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float);
+    if (dyn > 48 * 1024) cudaFuncSetAttribute(k_elkan_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    k_elkan_scan<<<grid, 256, dyn, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
                                               (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1,
                                               W->mv_i, W->mv_old, W->ctr);
     CHECK_LAUNCH("elkan_scan");
@@ -1443,8 +1549,8 @@ int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
 }
 
 int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra, void *stream) {
-    k_finalize<<<1, 1024, 0, S(stream)>>>(C->k, C->touched, C->tlist, C->tcount, C->drift, C->sinp, C->objc, C->hstat,
-                                          W->ctr, W->stats, sims_extra, all_clusters);
+    k_finalize<<<1, kFinThreads, 0, S(stream)>>>(C->k, C->touched, C->tcount, C->drift, C->sinp, C->objc, C->hstat,
+                                                 W->ctr, W->stats, sims_extra, all_clusters);
     CHECK_LAUNCH("finalize");
     return 0;
 }

@@ -270,6 +270,16 @@ class CenterState:
         _lib.call("spkm_load_centers", self.struct, _ptr(src), stream)
         return src  # keep alive until the stream passes
 
+    def snapshot(self) -> "CenterState":
+        """A shallow CenterState whose result tensors are private copies (for ClusteringResult)."""
+        snap = object.__new__(CenterState)
+        snap.k, snap.d, snap.kp, snap.scale_bits = self.k, self.d, self.kp, self.scale_bits
+        snap.cent64 = self.cent64.clone()
+        snap.sums = self.sums.clone()
+        snap.counts = self.counts.clone()
+        snap.drift = self.drift.clone()
+        return snap
+
     def host_centers(self) -> np.ndarray:
         return self.cent64.view(self.k, self.d).cpu().numpy()
 
@@ -328,7 +338,8 @@ class Engine:
     """
 
     def __init__(self, data: Dataset, k: int, variant: str, device=None, hamerly_update: str = "safe",
-                 corpus: DeviceCorpus | None = None, comm=None, n_total: int | None = None):
+                 corpus: DeviceCorpus | None = None, comm=None, n_total: int | None = None,
+                 use_graphs: bool = True):
         self.device = _require_cuda(device)
         self.k, self.variant = k, variant
         self.naive = int(hamerly_update == "naive")
@@ -340,12 +351,19 @@ class Engine:
         self.needs_cc = variant in _CC_VARIANTS
         self.C = CenterState(k, data.dim, self.n_total, self.device, self.needs_cc)
         self.P = PointState(self.corpus.n, k, variant, self.device)
-        self.stream = torch.cuda.current_stream(self.device)
+        # a dedicated stream: steady-state iterations are replayed as one CUDA graph
+        self.stream = torch.cuda.Stream(device=self.device)
+        self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.sp = ctypes_void(self.stream.cuda_stream)
+        self.use_graphs = use_graphs and comm is None
+        self.graph = None
+        self.graph_kernels = 0
+        self.runs = 0
 
     # -- phases --------------------------------------------------------------
     def load_centers(self, centers: np.ndarray):
-        keep = self.C.load(centers, self.sp)
+        with torch.cuda.stream(self.stream):       # H2D ordered before the kernel on this stream
+            keep = self.C.load(centers, self.sp)
         self.stream.synchronize()
         del keep
 
@@ -357,10 +375,11 @@ class Engine:
         np.cumsum(ends - starts, out=sptr[1:])
         sel = np.concatenate([np.arange(s, e) for s, e in zip(starts, ends)]) if rows.size else np.zeros(0, np.int64)
         dev = self.device
-        t_ptr = torch.from_numpy(sptr).to(dev)
-        t_idx = torch.from_numpy(np.ascontiguousarray(data.indices[sel], np.int32)).to(dev)
-        t_val = torch.from_numpy(np.ascontiguousarray(data.data[sel], np.float64)).to(dev)
-        _lib.call("spkm_seed_rows", self.C.struct, _ptr(t_ptr), _ptr(t_idx), _ptr(t_val), self.sp)
+        with torch.cuda.stream(self.stream):       # H2D ordered before the kernel on this stream
+            t_ptr = torch.from_numpy(sptr).to(dev)
+            t_idx = torch.from_numpy(np.ascontiguousarray(data.indices[sel], np.int32)).to(dev)
+            t_val = torch.from_numpy(np.ascontiguousarray(data.data[sel], np.float64)).to(dev)
+            _lib.call("spkm_seed_rows", self.C.struct, _ptr(t_ptr), _ptr(t_idx), _ptr(t_val), self.sp)
         self.stream.synchronize()
         self.seed_h2d_bytes = int(sptr.nbytes + t_idx.numel() * 4 + t_val.numel() * 8)
 
@@ -381,7 +400,8 @@ class Engine:
         _lib.call("spkm_aggregate_sums", self.corpus.struct, self.C.struct, self.P.bounds,
                   _ptr(self.C.sums), _ptr(self.C.counts), self.sp)
         if self.comm is not None:
-            self.comm.scratch(self.C.sums, self.C.counts)
+            with torch.cuda.stream(self.stream):
+                self.comm.scratch(self.C.sums, self.C.counts)
 
     def lloyd_pass(self):
         _lib.call("spkm_full_assign", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
@@ -411,19 +431,28 @@ class Engine:
                       _ptr(self.C.sums), _ptr(self.C.counts), _ptr(self.C.touched), self.sp)
         else:
             ex = self.comm
-            ex.begin()
-            _lib.call("spkm_apply_moves", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
-                      _ptr(ex.delta), _ptr(ex.dcounts), _ptr(self.C.touched), self.sp)
-            ex.exchange(self.C.sums, self.C.counts, self.C.touched, self.P.ctr)
+            with torch.cuda.stream(self.stream):
+                ex.begin()
+                _lib.call("spkm_apply_moves", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+                          _ptr(ex.delta), _ptr(ex.dcounts), _ptr(self.C.touched), self.sp)
+                ex.exchange(self.C.sums, self.C.counts, self.C.touched, self.P.ctr)
 
     def move_centers(self, all_clusters: bool):
         _lib.call("spkm_move_centers", self.C.struct, int(all_clusters), self.sp)
 
-    def finalize(self, all_clusters: bool, sims_extra: int) -> np.ndarray:
+    def finalize_launch(self, all_clusters: bool, sims_extra: int):
         _lib.call("spkm_finalize", self.C.struct, self.P.work, int(all_clusters), int(sims_extra), self.sp)
-        self.P.stats_host.copy_(self.P.stats, non_blocking=True)
+
+    def read_stats(self) -> np.ndarray:
+        """The one per-iteration D2H read (64 B stats) and the host sync."""
+        with torch.cuda.stream(self.stream):
+            self.P.stats_host.copy_(self.P.stats, non_blocking=True)
         self.stream.synchronize()
         return self.P.stats_host.numpy().copy()
+
+    def finalize(self, all_clusters: bool, sims_extra: int) -> np.ndarray:
+        self.finalize_launch(all_clusters, sims_extra)
+        return self.read_stats()
 
     def host_bounds(self) -> BoundsState:
         n = self.corpus.n
@@ -441,16 +470,11 @@ class Engine:
                            prev_centers=None, drift=C.drift.cpu().numpy(), seed_indices=seed_indices)
 
     # -- one iteration ---------------------------------------------------------
-    def iteration(self, it: int, debug_hook=None, seed_indices=None) -> tuple:
-        k = self.k
-        if it == 1:
-            self.init_pass()
-            self.scratch_sums()
-            self.move_centers(True)
-            return self.finalize(True, self.n_total * k), None
+    def _steady(self, debug_hook=None, it=0, seed_indices=None):
+        """Kernel sequence of an iteration >= 2 (engine.py:240-337), no host sync."""
         if self.variant == "standard":
             self.lloyd_pass()
-            sims_extra = self.n_total * k
+            sims_extra = self.n_total * self.k
         else:
             use = int(self.needs_cc)
             if self.needs_cc:
@@ -467,13 +491,49 @@ class Engine:
             # exact fixed-point sums: the rebuild reproduces the incremental
             # sums bit-for-bit; kept so the reference's schedule is visible
             self.scratch_sums()
-        return self.finalize(False, sims_extra), None
+        self.finalize_launch(False, sims_extra)
+
+    def iteration(self, it: int, debug_hook=None, seed_indices=None) -> tuple:
+        if it == 1:
+            self.init_pass()
+            self.scratch_sums()
+            self.move_centers(True)
+            return self.finalize(True, self.n_total * self.k), None
+        prof = _lib.active_profiler()
+        # capture only once the engine is being reused (a capture costs about
+        # as much as ~20 eager iterations)
+        graphable = (self.use_graphs and (self.runs > 0 or self.graph is not None) and it >= 3
+                     and debug_hook is None and it % _SCRATCH_INTERVAL != 0
+                     and not (prof is not None and prof.timed))
+        if not graphable:
+            self._steady(debug_hook, it, seed_indices)
+            return self.read_stats(), None
+        if self.graph is None:
+            # one-time capture of the steady iteration on this engine's stream;
+            # every kernel reads its work counts from device memory, so the
+            # same graph is valid for every later iteration
+            self.stream.synchronize()
+            g = torch.cuda.CUDAGraph()
+            _lib._capture = []
+            saved, _lib._profiler = _lib._profiler, None
+            try:
+                with torch.cuda.graph(g, stream=self.stream):
+                    self._steady(None, it)
+            finally:
+                self.graph_kernels = sum(_lib._capture)
+                _lib._capture = None
+                _lib._profiler = saved
+            self.graph = g
+        with torch.cuda.stream(self.stream):     # replay() launches on the current stream
+            self.graph.replay()
+        _lib.note_launches(self.graph_kernels)
+        return self.read_stats(), None
 
 
 def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, debug_hook=None,
         hamerly_update: str = "safe", *, device=None, corpus: DeviceCorpus | None = None,
         init_centers: np.ndarray | None = None, comm=None, n_total: int | None = None,
-        seed_indices=None) -> ClusteringResult:
+        seed_indices=None, use_graphs: bool = True) -> ClusteringResult:
     """Cluster ``data`` into ``k`` groups (reference engine.run, engine.py:201-346)."""
     from .seeding import SeedConfig, make_centroids, uniform_rows
 
@@ -486,8 +546,7 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
         else:
             cents0 = make_centroids(data, k, cfg)
             init_centers, seed_indices = cents0.centers, cents0.seed_indices
-    eng = Engine(data, k, variant, device=device, hamerly_update=hamerly_update, corpus=corpus, comm=comm,
-                 n_total=n_total)
+    eng = _engine_for(data, k, variant, device, hamerly_update, corpus, comm, n_total, use_graphs)
     if init_centers is None:
         eng.seed_rows(data, seed_indices)
     else:
@@ -508,11 +567,45 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
         if k == 1 or st[_lib.ST_ALLONE] == 1.0 or (it >= 2 and reassign == 0):
             converged = True
             break
+    eng.stream.synchronize()
+    eng.runs += 1
+    torch.cuda.current_stream(eng.device).wait_stream(eng.stream)
     a = eng.P.a[:eng.corpus.n].cpu().numpy().astype(np.int64)
     if comm is not None:
         a = comm.gather_assignments(eng.P.a, eng.corpus.rows, eng.n_total)
-    return ClusteringResult(assignments=a, centers=DeviceCentroidSet(eng.C, seed_indices),
+    return ClusteringResult(assignments=a, centers=DeviceCentroidSet(eng.C.snapshot(), seed_indices),
                             objective=stats[-1].objective, iterations=stats, converged=converged)
+
+
+# Engines (device buffers + captured CUDA graph) are cached per
+# (corpus, k, variant, ...) so repeated fits reuse the same buffers and the
+# same graph; results get their own snapshot of the center state.
+_ENGINES: "dict" = {}
+_ENGINE_CACHE_MAX = 6
+
+
+def _engine_for(data, k, variant, device, hamerly_update, corpus, comm, n_total, use_graphs):
+    if comm is not None:
+        return Engine(data, k, variant, device=device, hamerly_update=hamerly_update, corpus=corpus, comm=comm,
+                      n_total=n_total, use_graphs=False)
+    dev = _require_cuda(device)
+    corpus = corpus if corpus is not None else device_corpus(data, dev)
+    key = (str(dev), id(corpus), k, variant, hamerly_update, n_total, use_graphs, data.dim)
+    eng = _ENGINES.pop(key, None)
+    if eng is None or eng.corpus is not corpus:
+        eng = Engine(data, k, variant, device=dev, hamerly_update=hamerly_update, corpus=corpus, comm=None,
+                     n_total=n_total, use_graphs=use_graphs)
+    else:
+        eng.C.cc_valid = False
+        eng.stream.wait_stream(torch.cuda.current_stream(dev))
+    _ENGINES[key] = eng
+    while len(_ENGINES) > _ENGINE_CACHE_MAX:
+        _ENGINES.pop(next(iter(_ENGINES)))
+    return eng
+
+
+def clear_engine_cache():
+    _ENGINES.clear()
 
 
 # --------------------------------------------------------------- predict etc.

@@ -311,3 +311,18 @@ def test_seed_rows_match_host_densify():
     assert np.array_equal(eng.C.host_centers(), data.densify_rows(rows))
     ct = eng.C.ct32.view(data.dim, eng.C.kp)[:, :4].cpu().numpy()
     assert np.array_equal(ct, data.densify_rows(rows).T.astype(np.float32))
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_cuda_graph_replay_matches_eager(variant):
+    """Steady-state iterations replayed as one CUDA graph give bit-identical results."""
+    m = spk()
+    data = golden_dataset(load_golden("C1"))
+    m.run(data, 20, variant, m.SeedConfig(seed=1), max_iter=50, use_graphs=True)       # eager, warms the engine
+    g = m.run(data, 20, variant, m.SeedConfig(seed=1), max_iter=50, use_graphs=True)   # captured + replayed
+    e = m.run(data, 20, variant, m.SeedConfig(seed=1), max_iter=50, use_graphs=False)
+    assert np.array_equal(g.assignments, e.assignments)
+    assert g.objective == e.objective
+    assert [s.sim_count for s in g.iterations] == [s.sim_count for s in e.iterations]
+    assert [s.reassignments for s in g.iterations] == [s.reassignments for s in e.iterations]
+    assert len(g.iterations) >= 3

@@ -1163,35 +1163,118 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
 // before the half-angle map so cc stays an upper bound.
 // Tiles: 64x64 outputs (upper triangle).  A tile is skipped when none of
 // its clusters moved since the last call.
-constexpr int GT = 64;
-constexpr double kGramDelta = 5e-5;
+// 5th-gen tensor cores (tcgen05.mma kind::tf32, accumulator in TMEM).
+// One CTA = one 128 x 128 output tile (upper triangle of 128-tiles) over
+// L terms of d.  float64 center rows are staged in shared memory as K-major,
+// no-swizzle core matrices (8 centers x 4 terms, 16-byte rows), split into
+// tf32 hi and lo parts; one elected thread issues 3 MMAs (lo.hi, hi.lo,
+// hi.hi) per 8-term group and commits to an mbarrier; the 32-term stages
+// are double-buffered so loads overlap the MMAs.  The fp32 partial tile is
+// read back with tcgen05.ld and written as float64 per d-split.
+// Error bound per entry: products of tf32 values are exact; the fp32 TMEM
+// accumulation over 3L/8 MMA steps adds <= (3L/8 + 8) 2^-22 sum|a b| (even
+// with truncating adds); the hi/lo split of the float64 values adds < 1e-6.
+constexpr int GT = 128;
+constexpr int GKC = 32;                       // terms per stage
+// K-major, no-swizzle core matrices: 8 centers x 16 bytes (4 terms).
+// SBO = 128 B between 8-center groups, LBO = 2 KB between the two 4-term
+// chunks of an 8-term MMA group, 4 KB per 8-term group.
+constexpr int GSBO = 128;
+constexpr int GLBO = (GT / 8) * GSBO + 16;    // 2064: +16 B staggers the 4-term chunks across banks
+constexpr int GGRP = 2 * GLBO + 32;           // 4160 bytes per 8-term group (16-byte aligned)
+constexpr int GOPB = (GKC / 8) * GGRP;        // bytes of one operand buffer (one stage, hi or lo)
 __device__ __forceinline__ uint32_t to_tf32(float x) {
     uint32_t r;
     asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
     return r;
 }
-__device__ __forceinline__ void mma_tf32(float (&d)[4], const uint32_t (&a)[4], const uint32_t (&b)[2]) {
-    asm volatile(
-        "mma.sync.aligned.m16n8k8.row.col.f32.tf32.tf32.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, {%8,%9}, "
-        "{%0,%1,%2,%3};\n"
-        : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
-        : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+__device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
+    // SmemDescriptor (cute/arch/mma_sm100_desc.hpp): start>>4 [0,14), LBO>>4 [16,30),
+    // SBO>>4 [32,46), version 1 [46,48), layout SWIZZLE_NONE (0) [61,64)
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((GLBO >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((GSBO >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
 }
-__device__ __forceinline__ void split_tf32(float x, uint32_t &hi, uint32_t &lo) {
-    hi = to_tf32(x);
-    lo = to_tf32(x - __uint_as_float(hi));
+// InstrDescriptor: c_format F32 (1) [4,6), a/b format TF32 (2) [7,10)/[10,13),
+// a/b K-major (0) bits 15/16, N>>3 [17,23), M>>4 [24,29)
+constexpr uint32_t kGramIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(GT >> 3) << 17) |
+                                ((uint32_t)(GT >> 4) << 24);
+
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+    uint32_t done = 0;
+    long long spins = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(bar), "r"(parity)
+            : "memory");
+        if (!done && ++spins > (1ll << 28)) __trap();   // never hang the GPU on a logic error
+    }
 }
 
-// 64x64 output tile per block (8 warps = 4 x 2, each 16 rows x 32 cols),
-// 32-term stages with the next stage prefetched into registers.
-__global__ void __launch_bounds__(256) k_gram_part(int64_t k, int64_t d, int64_t kp, int64_t dsplit,
-                                                   const float *__restrict__ ct, const int2 *__restrict__ tiles,
-                                                   const double *__restrict__ sinp, int full, double *gpart) {
-    __shared__ float As[32][GT + 8];   // [term][cluster]; stride 72 -> conflict-free fragment loads
-    __shared__ float Bs[32][GT + 8];
+// GKC terms x GT centers of the float64 centers -> K-major core matrices.
+// Task = (center m, 4-term chunk q); 8 consecutive lanes read one center's
+// 32 terms (256 contiguous bytes), one 16-byte store per part.  All loads of
+// a thread are issued before any conversion (NT tasks in flight).
+template <int NT>
+__device__ __forceinline__ void stage_operand(const double *__restrict__ C, int64_t d, int64_t k, int64_t c0,
+                                              int64_t tb, int64_t t1, uint8_t *hi, uint8_t *lo) {
+    double v[NT][4];
+    const bool vec = (d % 2) == 0 && (tb % 2) == 0;
+#pragma unroll
+    for (int u = 0; u < NT; ++u) {
+        const int e = threadIdx.x + u * blockDim.x;
+        const int q = e & 7, m = e >> 3;
+        const int64_t row = c0 + m;
+        const int64_t t = tb + 4 * q;
+#pragma unroll
+        for (int r = 0; r < 4; ++r) v[u][r] = 0.0;
+        if (row < k) {
+            const double *p = C + row * d + t;
+            if (vec && t + 3 < t1) {
+                const double2 x0 = __ldg(reinterpret_cast<const double2 *>(p));
+                const double2 x1 = __ldg(reinterpret_cast<const double2 *>(p) + 1);
+                v[u][0] = x0.x; v[u][1] = x0.y; v[u][2] = x1.x; v[u][3] = x1.y;
+            } else {
+#pragma unroll
+                for (int r = 0; r < 4; ++r) v[u][r] = (t + r < t1) ? __ldg(p + r) : 0.0;
+            }
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < NT; ++u) {
+        const int e = threadIdx.x + u * blockDim.x;
+        const int q = e & 7, m = e >> 3;
+        uint32_t h[4], l[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            h[r] = to_tf32((float)v[u][r]);
+            l[r] = to_tf32((float)(v[u][r] - (double)__uint_as_float(h[r])));
+        }
+        const int off = (q >> 1) * GGRP + (q & 1) * GLBO + (m >> 3) * GSBO + (m & 7) * 16;
+        *reinterpret_cast<uint4 *>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
+        *reinterpret_cast<uint4 *>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
+    }
+}
+
+constexpr int kGramThreads = 512;
+
+__global__ void __launch_bounds__(kGramThreads, 1) k_gram_tc(int64_t k, int64_t d, int64_t dsplit,
+                                                     const double *__restrict__ C, const int2 *__restrict__ tiles,
+                                                     const double *__restrict__ sinp, int full, double *gpart) {
+    extern __shared__ __align__(1024) uint8_t gsm[];
+    // layout: [stage 0: Ahi Alo Bhi Blo][stage 1: ...][2 mbarriers][tmem addr]
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ uint32_t tmem_base_s;
     __shared__ int need;
     const int2 tl = tiles[blockIdx.x];
     const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
+    const bool diag = tl.x == tl.y;
     if (threadIdx.x == 0) {
         int nd = full;
         for (int q = 0; q < GT && !nd; ++q) {
@@ -1202,111 +1285,157 @@ __global__ void __launch_bounds__(256) k_gram_part(int64_t k, int64_t d, int64_t
     }
     __syncthreads();
     if (!need) return;
-    const int64_t per = ((d + dsplit - 1) / dsplit + 31) / 32 * 32;
+    const int64_t per = ((d + dsplit - 1) / dsplit + GKC - 1) / GKC * GKC;
     const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
-    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-    const int wy = w >> 1, wx = w & 1, g = lane >> 2, t4 = lane & 3;
-    // loader mapping: thread -> (term row lt, 8 consecutive clusters at lc)
-    const int lt = threadIdx.x >> 3, lc = (threadIdx.x & 7) * 8;
-    float ra[8], rb[8];
-    auto load = [&](int64_t tb) {
-        const int64_t t = tb + lt;
-        const bool tin = t < t1;
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            ra[q] = (tin && a0 + lc + q < k) ? __ldg(ct + t * kp + a0 + lc + q) : 0.f;
-            rb[q] = (tin && j0 + lc + q < k) ? __ldg(ct + t * kp + j0 + lc + q) : 0.f;
-        }
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_s)),
+                     "r"(GT)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = tmem_base_s;
+    const int nch = t1 > t0 ? (int)((t1 - t0 + GKC - 1) / GKC) : 0;
+    auto buf = [&](int s, int which) { return gsm + (size_t)(s * 4 + which) * GOPB; };   // 0 Ahi 1 Alo 2 Bhi 3 Blo
+    auto load_stage = [&](int s, int64_t tb) {
+        stage_operand<GT * (GKC / 4) / kGramThreads>(C, d, k, a0, tb, t1, buf(s, 0), buf(s, 1));
+        if (!diag) stage_operand<GT * (GKC / 4) / kGramThreads>(C, d, k, j0, tb, t1, buf(s, 2), buf(s, 3));
+        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> async proxy
     };
-    double accd[4][4];
+    if (nch > 0) load_stage(0, t0);
+    __syncthreads();
+    for (int ch = 0; ch < nch; ++ch) {
+        const int s = ch & 1;
+        if (threadIdx.x == 0) {
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint32_t ahi = smem_u32(buf(s, 0)), alo = smem_u32(buf(s, 1));
+            const uint32_t bhi = diag ? ahi : smem_u32(buf(s, 2)), blo = diag ? alo : smem_u32(buf(s, 3));
 #pragma unroll
-    for (int f = 0; f < 4; ++f)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) accd[f][q] = 0.0;
-    if (t0 < t1) load(t0);
-    for (int64_t tb = t0; tb < t1; tb += 32) {
-        __syncthreads();
-#pragma unroll
-        for (int q = 0; q < 8; ++q) {
-            As[lt][lc + q] = ra[q];
-            Bs[lt][lc + q] = rb[q];
+            for (int g = 0; g < GKC / 8; ++g) {
+                const uint32_t off = g * GGRP;
+                const uint64_t dah = umma_desc(ahi + off), dal = umma_desc(alo + off);
+                const uint64_t dbh = umma_desc(bhi + off), dbl = umma_desc(blo + off);
+                const uint32_t acc0 = (ch > 0 || g > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                    " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(dal), "l"(dbh), "r"(kGramIdesc), "r"(acc0)
+                    : "memory");
+                asm volatile(
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dah), "l"(dbl),
+                    "r"(kGramIdesc)
+                    : "memory");
+                asm volatile(
+                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dah), "l"(dbh),
+                    "r"(kGramIdesc)
+                    : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                             smem_u32(&bars[s]))
+                         : "memory");
         }
-        __syncthreads();
-        if (tb + 32 < t1) load(tb + 32);
-        float dst[4][4];
+        if (ch + 1 < nch) {
+            const int ns = s ^ 1;
+            if (ch >= 1) mbar_wait(smem_u32(&bars[ns]), (uint32_t)(((ch - 1) >> 1) & 1));
+            load_stage(ns, t0 + (int64_t)(ch + 1) * GKC);
+            __syncthreads();
+        }
+    }
+    if (nch > 0) mbar_wait(smem_u32(&bars[(nch - 1) & 1]), (uint32_t)(((nch - 1) >> 1) & 1));
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    // epilogue: warp w < 4 owns TMEM lanes (rows) 32w..32w+31
+    const int64_t row = a0 + w * 32 + lane;
+    if (w < 4) {
 #pragma unroll
-        for (int f = 0; f < 4; ++f)
+    for (int cb = 0; cb < GT / 32; ++cb) {
+        uint32_t r[32];
+        const uint32_t taddr = tmem + ((uint32_t)(w * 32) << 16) + (uint32_t)(cb * 32);
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+            : "r"(taddr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+        if (row < k && nch > 0) {
+            double *out = gpart + ((int64_t)blockIdx.y * k + row) * k;
 #pragma unroll
-            for (int q = 0; q < 4; ++q) dst[f][q] = 0.f;
-#pragma unroll
-        for (int ks = 0; ks < 4; ++ks) {
-            const int kk = ks * 8;
-            uint32_t ahi[4], alo[4];
-            split_tf32(As[kk + t4][wy * 16 + g], ahi[0], alo[0]);
-            split_tf32(As[kk + t4][wy * 16 + g + 8], ahi[1], alo[1]);
-            split_tf32(As[kk + t4 + 4][wy * 16 + g], ahi[2], alo[2]);
-            split_tf32(As[kk + t4 + 4][wy * 16 + g + 8], ahi[3], alo[3]);
-#pragma unroll
-            for (int f = 0; f < 4; ++f) {
-                uint32_t bhi[2], blo[2];
-                split_tf32(Bs[kk + t4][wx * 32 + f * 8 + g], bhi[0], blo[0]);
-                split_tf32(Bs[kk + t4 + 4][wx * 32 + f * 8 + g], bhi[1], blo[1]);
-                mma_tf32(dst[f], alo, bhi);
-                mma_tf32(dst[f], ahi, blo);
-                mma_tf32(dst[f], ahi, bhi);
+            for (int q = 0; q < 32; ++q) {
+                const int64_t col = j0 + cb * 32 + q;
+                if (col < k) out[col] = (double)__uint_as_float(r[q]);
             }
         }
-#pragma unroll
-        for (int f = 0; f < 4; ++f)
-#pragma unroll
-            for (int q = 0; q < 4; ++q) accd[f][q] += (double)dst[f][q];
     }
-#pragma unroll
-    for (int f = 0; f < 4; ++f)
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int64_t ar = a0 + wy * 16 + g + ((q & 2) ? 8 : 0);
-            const int64_t jr = j0 + wx * 32 + f * 8 + t4 * 2 + (q & 1);
-            if (ar < k && jr < k) gpart[((int64_t)blockIdx.y * k + ar) * k + jr] = accd[f][q];
-        }
+    if (nch == 0 && row < k) {
+        double *out = gpart + ((int64_t)blockIdx.y * k + row) * k;
+        for (int q = 0; q < GT; ++q)
+            if (j0 + q < k) out[j0 + q] = 0.0;
+    }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(GT) : "memory");
 }
 
+// cc = half-angle of the Gram entry plus the error bound, rounded up.  8
+// lanes per (a, j): lane r sums splits y = r, r+8, ... then a fixed shuffle
+// tree, so the result does not depend on scheduling.
 __global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict__ gpart,
-                             const double *__restrict__ sinp, int full, float *cc) {
-    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (e >= k * k) return;
-    const int64_t a = e / k, j = e % k;
-    if (a > j) return;
-    if (a == j) {
-        cc[e] = -1.f;
-        return;
-    }
-    // recompute only where the tile was recomputed (same predicate as k_gram_part)
-    if (!full) {
+                             const double *__restrict__ sinp, int full, double gdelta, float *cc) {
+    const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t e = gt >> 3;
+    const int r = threadIdx.x & 7;
+    const bool in = e < k * k;
+    const int64_t a = in ? e / k : 0, j = in ? e % k : 0;
+    bool work = in && a < j;
+    if (work && !full) {
         const int64_t ta = a / GT * GT, tj = j / GT * GT;
         int nd = 0;
         for (int q = 0; q < GT && !nd; ++q) {
             if (ta + q < k && sinp[ta + q] != 0.0) nd = 1;
             if (tj + q < k && sinp[tj + q] != 0.0) nd = 1;
         }
-        if (!nd) return;
+        work = nd;
     }
     double g = 0.0;
-    for (int64_t y = 0; y < dsplit; ++y) g += gpart[(y * k + a) * k + j];
-    double h = d_half_angle(d_clamp(g + kGramDelta)) + kCcSlack;
-    if (h > 1.0) h = 1.0;
-    const float f = __double2float_ru(h);
-    cc[a * k + j] = f;
-    cc[j * k + a] = f;
+    if (work)
+        for (int64_t y = r; y < dsplit; y += 8) g += gpart[(y * k + a) * k + j];
+    g += __shfl_down_sync(FULL, g, 4, 8);
+    g += __shfl_down_sync(FULL, g, 2, 8);
+    g += __shfl_down_sync(FULL, g, 1, 8);
+    if (r == 0 && in) {
+        if (a == j) {
+            cc[e] = -1.f;
+        } else if (work) {
+            double h = d_half_angle(d_clamp(g + gdelta)) + kCcSlack;
+            if (h > 1.0) h = 1.0;
+            const float f = __double2float_ru(h);
+            cc[a * k + j] = f;
+            cc[j * k + a] = f;
+        }
+    }
 }
 
+// s(a) = max_{j != a} cc(a, j); warp per row.
 __global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s) {
-    const int64_t a = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
     if (a >= k) return;
     float m = -INFINITY;
-    for (int64_t j = 0; j < k; ++j)
+    for (int64_t j = lane; j < k; j += 32)
         if (j != a) m = fmaxf(m, cc[a * k + j]);
-    s[a] = (k > 1) ? m : -1.f;
+    for (int o = 16; o; o >>= 1) m = fmaxf(m, __shfl_down_sync(FULL, m, o));
+    if (lane == 0) s[a] = (k > 1) ? m : -1.f;
 }
 
 // ---------------------------------------------------------------- misc
@@ -1556,10 +1685,12 @@ int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long lo
 }
 
 int64_t spkm_gram_dsplit(int64_t k, int64_t d) {
+    // one wave (one CTA per SM: ~130 KB of stages), at most 512 terms per CTA
+    // when that still fills the machine
     const int64_t tk = (k + GT - 1) / GT;
     const int64_t tiles = tk * (tk + 1) / 2;
-    int64_t ds = (4 * (int64_t)num_sms() + tiles - 1) / tiles;
-    const int64_t maxds = (d + 1023) / 1024;
+    int64_t ds = (int64_t)num_sms() / tiles;
+    const int64_t maxds = (d + 511) / 512;
     if (ds > maxds) ds = maxds;
     if (ds < 1) ds = 1;
     return ds;
@@ -1573,12 +1704,21 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     const int64_t tk = (C->k + GT - 1) / GT;
     const int64_t ntiles = tk * (tk + 1) / 2;
     const int64_t ds = spkm_gram_dsplit(C->k, C->d);
+    const int64_t per = ((C->d + ds - 1) / ds + GKC - 1) / GKC * GKC;
+    const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + 1e-6;
+    const size_t smem = (size_t)8 * GOPB;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr_set = true;
+    }
     dim3 grid((unsigned)ntiles, (unsigned)ds);
-    k_gram_part<<<grid, 256, 0, st>>>(C->k, C->d, C->kp, ds, C->ct32, tiles_dev, C->sinp, full, gpart);
-    CHECK_LAUNCH("gram_part");
-    k_gram_final<<<(unsigned)((C->k * C->k + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, C->cc);
+    k_gram_tc<<<grid, kGramThreads, smem, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart);
+    CHECK_LAUNCH("gram_tc");
+    k_gram_final<<<(unsigned)((C->k * C->k * 8 + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, gdelta,
+                                                                           C->cc);
     CHECK_LAUNCH("gram_final");
-    k_row_max<<<(unsigned)((C->k + 255) / 256), 256, 0, st>>>(C->k, C->cc, C->s);
+    k_row_max<<<(unsigned)((C->k * 32 + 255) / 256), 256, 0, st>>>(C->k, C->cc, C->s);
     CHECK_LAUNCH("row_max");
     return 0;
 }

@@ -276,7 +276,8 @@ def test_max_length_rows(oracle_mod):
         assert np.array_equal(r.assignments, base.assignments), v
 
 
-@pytest.mark.parametrize("name,k", [("C1", 20), ("grid_200_5000_50_1007", 50), ("signed", 6)])
+@pytest.mark.parametrize("name,k", [("C1", 20), ("grid_200_5000_50_1007", 50), ("signed", 6), ("C1", 200),
+                                    ("C1", 300)])
 def test_center_thresholds_upper_bound(name, k):
     """cc from the 3xTF32 tensor-core Gram is an upper bound within 1e-4 of the float64 half-angle cosine."""
     from paper_2107_04074_b200 import engine as E

@@ -88,6 +88,9 @@ typedef struct spkm_centers {
     double *hstat;           /* [8]   owner, p_min, p_min2, owner_s, smax, smax2 */
     int32_t *tlist;          /* [k]   scratch: touched cluster list         */
     int32_t *tcount;         /* [1]   scratch: its length                   */
+    long long *ctl;          /* [2]   {iterations done, converged}: every loop
+                                kernel is a no-op once converged, so the
+                                host may enqueue iterations ahead          */
 } spkm_centers;
 
 /* Per-point bounds of the local shard. */
@@ -106,6 +109,8 @@ typedef struct spkm_work {
     int32_t *mv_old;         /* [n] their previous cluster                   */
     long long *ctr;          /* [8] counters, see SPKM_CTR_*                 */
     double *stats;           /* [16] per-iteration stats, see SPKM_ST_*      */
+    double *stats_hist;      /* [hist_cap][16] stats of every iteration      */
+    int64_t hist_cap;
 } spkm_work;
 
 enum {
@@ -115,7 +120,7 @@ enum {
 enum {
     SPKM_ST_SIMS = 0, SPKM_ST_REASSIGN = 1, SPKM_ST_OBJECTIVE = 2, SPKM_ST_ALLONE = 3,
     SPKM_ST_SURV1 = 4, SPKM_ST_SURV2 = 5, SPKM_ST_TOUCHED = 6, SPKM_ST_NNZ_TIGHTEN = 7,
-    SPKM_ST_NNZ_RESCAN = 8, SPKM_ST_NNZ_ELKAN = 9, SPKM_ST_COUNT = 16
+    SPKM_ST_NNZ_RESCAN = 8, SPKM_ST_NNZ_ELKAN = 9, SPKM_ST_ITER = 10, SPKM_ST_COUNT = 16
 };
 
 int spkm_abi_version(void);

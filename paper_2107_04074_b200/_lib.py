@@ -38,7 +38,7 @@ class Centers(ctypes.Structure):
     _fields_ = [("k", c_i64), ("d", c_i64), ("kp", c_i64), ("scale_bits", c_i32), ("_pad", c_i32),
                 ("cent64", c_vp), ("ct32", c_vp), ("sums", c_vp), ("counts", c_vp), ("drift", c_vp),
                 ("sinp", c_vp), ("touched", c_vp), ("objc", c_vp), ("part", c_vp), ("norm", c_vp), ("cc", c_vp),
-                ("s", c_vp), ("hstat", c_vp), ("tlist", c_vp), ("tcount", c_vp)]
+                ("s", c_vp), ("hstat", c_vp), ("tlist", c_vp), ("tcount", c_vp), ("ctl", c_vp)]
 
 
 class Bounds(ctypes.Structure):
@@ -47,14 +47,14 @@ class Bounds(ctypes.Structure):
 
 class Work(ctypes.Structure):
     _fields_ = [("surv1", c_vp), ("surv2", c_vp), ("mv_i", c_vp), ("mv_old", c_vp), ("ctr", c_vp),
-                ("stats", c_vp)]
+                ("stats", c_vp), ("stats_hist", c_vp), ("hist_cap", c_i64)]
 
 
 # modes / enums (include/spkm.h)
 MODE_INIT_PLAIN, MODE_INIT_ELKAN, MODE_INIT_HAMERLY, MODE_LLOYD = 0, 1, 2, 3
 CTR_SURV1, CTR_SURV2, CTR_MOVES, CTR_SIMS, CTR_NNZ_TIGHTEN, CTR_NNZ_RESCAN, CTR_NNZ_ELKAN = range(7)
 (ST_SIMS, ST_REASSIGN, ST_OBJECTIVE, ST_ALLONE, ST_SURV1, ST_SURV2, ST_TOUCHED, ST_NNZ_TIGHTEN, ST_NNZ_RESCAN,
- ST_NNZ_ELKAN) = range(10)
+ ST_NNZ_ELKAN, ST_ITER) = range(11)
 ST_COUNT = 16
 
 # name -> argtypes (restype int unless listed in _RESTYPES)

@@ -29,6 +29,7 @@
 #include <stdint.h>
 #include <stdio.h>
 #include <math.h>
+#include <stdlib.h>
 
 #include "../../include/spkm.h"
 
@@ -198,26 +199,44 @@ struct RowPassArgs {
     int32_t *mv_i, *mv_old;
     long long *ctr;
     double *best, *second;       // predict outputs
+    const long long *ctl;        // [it, done]: done -> this launch is a no-op
+    int hot;                     // term rows [0, hot) of ct are staged in shared memory
+    int64_t hot_d;               // dimensionality (caps hot)
 };
 
 // Thread = (row, CH consecutive centers).  tpr threads cover one row's kp
 // columns, rpw rows share a warp.  Per nnz: one broadcast (idx, val) load and
 // CH/4 float4 loads of the term-major center row; CH independent FMA chains.
-template <int CH>
-__global__ void __launch_bounds__(256) k_row_pass(RowPassArgs A) {
+template <int CH, int NT, bool HOT>
+__global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
     // nnz per gather batch: keep ~8 float4 loads in flight per lane
     constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 2 : 1;
-    __shared__ int32_t s_idx[8][8][32];
-    __shared__ float s_val[8][8][32];
+    if (A.ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    extern __shared__ __align__(16) float s_dyn[];
+    // dynamic smem: [hot * kp floats: term rows of the hottest terms][staging]
+    float *s_hot = s_dyn;
+    const int wpb = blockDim.x >> 5;
+    int32_t *s_idx = reinterpret_cast<int32_t *>(s_dyn + (int64_t)A.hot * A.kp);
+    float *s_val = reinterpret_cast<float *>(s_idx + wpb * 8 * 32);
+    if (HOT && A.hot > 0) {
+        // the Zipf head of the vocabulary (terms renumbered by document
+        // frequency on upload) is served from shared memory for the whole
+        // persistent launch
+        const float4 *src = reinterpret_cast<const float4 *>(A.ct);
+        float4 *dst = reinterpret_cast<float4 *>(s_hot);
+        const int64_t n4 = (int64_t)A.hot * A.kp / 4;
+        for (int64_t e = threadIdx.x; e < n4; e += blockDim.x) dst[e] = __ldg(src + e);
+        __syncthreads();
+    }
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane / A.tpr, q = lane - g * A.tpr;
     const bool lane_on = g < A.rpw;
     const int64_t nrows = A.rowlist ? *A.rowcount : A.n;
     const int64_t nslots = (nrows + A.rpw - 1) / A.rpw;
-    const int wpb = blockDim.x >> 5;
     const int o0 = A.tpr > 1 ? (1 << (31 - __clz(A.tpr - 1))) : 0;
-    int32_t *my_idx = s_idx[wib][lane_on ? g : 0];
-    float *my_val = s_val[wib][lane_on ? g : 0];
+    int32_t *my_idx = s_idx + (wib * 8 + (lane_on ? g : 0)) * 32;
+    float *my_val = s_val + (wib * 8 + (lane_on ? g : 0)) * 32;
+    const int hot = HOT ? A.hot : 0;
     for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
         const int64_t slot = w * A.rpw + g;
         const bool valid = lane_on && slot < nrows;
@@ -248,9 +267,16 @@ __global__ void __launch_bounds__(256) k_row_pass(RowPassArgs A) {
 #pragma unroll
                 for (int b = 0; b < UB; ++b) {
                     vv[b] = my_val[u + b];
-                    const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)my_idx[u + b] * A.kp);
+                    const int ii = my_idx[u + b];
+                    if (HOT && ii < hot) {
+                        const float4 *p = reinterpret_cast<const float4 *>(s_hot + (int64_t)ii * A.kp + j0);
 #pragma unroll
-                    for (int r = 0; r < CH / 4; ++r) cv[b][r] = __ldg(p + r);
+                        for (int r = 0; r < CH / 4; ++r) cv[b][r] = p[r];
+                    } else {
+                        const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)ii * A.kp);
+#pragma unroll
+                        for (int r = 0; r < CH / 4; ++r) cv[b][r] = __ldg(p + r);
+                    }
                 }
 #pragma unroll
                 for (int b = 0; b < UB; ++b)
@@ -264,10 +290,12 @@ __global__ void __launch_bounds__(256) k_row_pass(RowPassArgs A) {
             }
             for (; u < cnt; ++u) {
                 const float v0 = my_val[u];
-                const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)my_idx[u] * A.kp);
+                const int ii = my_idx[u];
+                const float4 *p = (HOT && ii < hot) ? reinterpret_cast<const float4 *>(s_hot + (int64_t)ii * A.kp + j0)
+                                                    : reinterpret_cast<const float4 *>(ctj + (int64_t)ii * A.kp);
 #pragma unroll
                 for (int r = 0; r < CH / 4; ++r) {
-                    const float4 cc4 = __ldg(p + r);
+                    const float4 cc4 = p[r];
                     acc[4 * r + 0] = __fmaf_rn(v0, cc4.x, acc[4 * r + 0]);
                     acc[4 * r + 1] = __fmaf_rn(v0, cc4.y, acc[4 * r + 1]);
                     acc[4 * r + 2] = __fmaf_rn(v0, cc4.z, acc[4 * r + 2]);
@@ -343,7 +371,8 @@ __global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *
                                                         const double *__restrict__ sinp,
                                                         const float *__restrict__ s_arr,
                                                         const double *__restrict__ hstat, int use_s, int naive,
-                                                        int32_t *surv1, long long *ctr) {
+                                                        int32_t *surv1, long long *ctr, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int owner = (int)hstat[0], owner_s = (int)hstat[3];
     const double pmin = hstat[1], pmin2 = hstat[2], smax = hstat[4], smax2 = hstat[5];
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -399,7 +428,8 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
                                                          const float *__restrict__ u,
                                                          const float *__restrict__ s_arr, int use_s,
                                                          const int32_t *__restrict__ surv1, int32_t *surv2,
-                                                         long long *ctr) {
+                                                         long long *ctr, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ float s_v[8][4][32];
     __shared__ float s_c[8][4][32];
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -466,7 +496,8 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
                                                       const double *__restrict__ sinp,
                                                       const float *__restrict__ cc,
                                                       const float *__restrict__ s_arr, int use_cc,
-                                                      int32_t *surv1, long long *ctr) {
+                                                      int32_t *surv1, long long *ctr, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
@@ -539,7 +570,8 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                                                     int32_t *a, float *l, float *u, int64_t ku,
                                                     const float *__restrict__ cc, int use_cc,
                                                     const int32_t *__restrict__ surv1, int32_t *mv_i,
-                                                    int32_t *mv_old, long long *ctr) {
+                                                    int32_t *mv_old, long long *ctr, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     constexpr int UB = 4;
     __shared__ int32_t s_idx[8][8][32];
     __shared__ float s_val[8][8][32];
@@ -772,7 +804,8 @@ __global__ void __launch_bounds__(256) k_aggregate(int64_t n, int64_t d, const i
                                                    const int32_t *__restrict__ indices,
                                                    const float *__restrict__ values,
                                                    const int32_t *__restrict__ a, long long *sums,
-                                                   long long *counts, double scale) {
+                                                   long long *counts, double scale, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
@@ -792,7 +825,8 @@ __global__ void __launch_bounds__(256) k_apply_moves(int64_t d, const int64_t *_
                                                      const int32_t *__restrict__ mv_i,
                                                      const int32_t *__restrict__ mv_old,
                                                      const long long *__restrict__ ctr, long long *sums,
-                                                     long long *counts, int32_t *touched, double scale) {
+                                                     long long *counts, int32_t *touched, double scale, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const long long cnt = ctr[SPKM_CTR_MOVES];
@@ -846,7 +880,8 @@ constexpr int kTileJ = 32;           // clusters per write tile
 constexpr double kChordPad = 4e-10;  // |1 - |c|| <= d * 2^-53 for d <= 1e6, twice
 
 __global__ void k_touched_list(int64_t k, const int32_t *__restrict__ touched, int all, int32_t *tlist,
-                               int32_t *tcount) {
+                               int32_t *tcount, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ int wsum[32];
     __shared__ int base_s;
     if (threadIdx.x == 0) base_s = 0;
@@ -876,7 +911,8 @@ __global__ void __launch_bounds__(256) k_center_norm_part(int64_t d, int64_t nch
                                                           const long long *__restrict__ sums,
                                                           const int32_t *__restrict__ tlist,
                                                           const int32_t *__restrict__ tcount, double inv_scale,
-                                                          double *part) {
+                                                          double *part, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double sh[8];
     const int64_t y = blockIdx.y, c = blockIdx.x;
     if (y >= *tcount) return;
@@ -900,7 +936,8 @@ __global__ void __launch_bounds__(256) k_center_norm_part(int64_t d, int64_t nch
 __global__ void __launch_bounds__(256) k_center_norm_final(int64_t nchunk, const long long *__restrict__ counts,
                                                            const int32_t *__restrict__ tlist,
                                                            const int32_t *__restrict__ tcount,
-                                                           const double *__restrict__ part, double *norm) {
+                                                           const double *__restrict__ part, double *norm, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double sh[8];
     const int64_t y = blockIdx.x;
     if (y >= *tcount) return;
@@ -923,7 +960,8 @@ __global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int
                                                       const int32_t *__restrict__ tlist,
                                                       const int32_t *__restrict__ tcount, double inv_scale,
                                                       const double *__restrict__ norm, double *cent64, float *ct32,
-                                                      double *part) {
+                                                      double *part, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ float tile[kTileT][kTileJ + 1];
     __shared__ int js[kTileJ];
     const int64_t nT = *tcount;
@@ -990,7 +1028,8 @@ __global__ void __launch_bounds__(256) k_center_reduce(int64_t ntile, const int3
                                                        const int32_t *__restrict__ tcount,
                                                        const double *__restrict__ part,
                                                        const double *__restrict__ norm, double *drift,
-                                                       double *sinp, double *objc) {
+                                                       double *sinp, double *objc, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double sh[8];
     const int64_t y = blockIdx.x;
     if (y >= *tcount) return;
@@ -1082,7 +1121,9 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
                                                           const int32_t *__restrict__ tcount, double *drift,
                                                           double *sinp, const double *__restrict__ objc,
                                                           double *hstat, long long *ctr, double *stats,
-                                                          long long sims_extra, int all) {
+                                                          long long sims_extra, int all, double *stats_hist,
+                                                          int64_t hist_cap, long long *ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double s_ob[kFinThreads / 32];
     __shared__ int s_no[kFinThreads / 32];
     __shared__ Low2 s_p[kFinThreads / 32], s_s[kFinThreads / 32];
@@ -1147,6 +1188,15 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
         stats[SPKM_ST_NNZ_TIGHTEN] = (double)ctr[SPKM_CTR_NNZ_TIGHTEN];
         stats[SPKM_ST_NNZ_RESCAN] = (double)ctr[SPKM_CTR_NNZ_RESCAN];
         stats[SPKM_ST_NNZ_ELKAN] = (double)ctr[SPKM_CTR_NNZ_ELKAN];
+        // iteration bookkeeping and the convergence test (engine.py:335-337),
+        // evaluated on the device so the host can enqueue iterations ahead
+        const long long it = ctl[0];
+        stats[SPKM_ST_ITER] = (double)(it + 1);
+        if (it < hist_cap)
+            for (int q = 0; q < SPKM_ST_COUNT; ++q) stats_hist[it * SPKM_ST_COUNT + q] = stats[q];
+        const bool conv = (k == 1) || (no == 0) || (it >= 1 && ctr[SPKM_CTR_MOVES] == 0);
+        ctl[0] = it + 1;
+        ctl[1] = conv ? 1 : 0;
         for (int q = 0; q < 8; ++q) ctr[q] = 0;
     }
 }
@@ -1266,7 +1316,8 @@ constexpr int kGramThreads = 512;
 
 __global__ void __launch_bounds__(kGramThreads, 1) k_gram_tc(int64_t k, int64_t d, int64_t dsplit,
                                                      const double *__restrict__ C, const int2 *__restrict__ tiles,
-                                                     const double *__restrict__ sinp, int full, double *gpart) {
+                                                     const double *__restrict__ sinp, int full, double *gpart, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     extern __shared__ __align__(1024) uint8_t gsm[];
     // layout: [stage 0: Ahi Alo Bhi Blo][stage 1: ...][2 mbarriers][tmem addr]
     __shared__ __align__(8) uint64_t bars[2];
@@ -1391,7 +1442,8 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_gram_tc(int64_t k, int64_t 
 // lanes per (a, j): lane r sums splits y = r, r+8, ... then a fixed shuffle
 // tree, so the result does not depend on scheduling.
 __global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict__ gpart,
-                             const double *__restrict__ sinp, int full, double gdelta, float *cc) {
+                             const double *__restrict__ sinp, int full, double gdelta, float *cc, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t e = gt >> 3;
     const int r = threadIdx.x & 7;
@@ -1427,7 +1479,8 @@ __global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict
 }
 
 // s(a) = max_{j != a} cc(a, j); warp per row.
-__global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s) {
+__global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (a >= k) return;
@@ -1498,25 +1551,83 @@ int grid_for(int64_t work_items, int per_block) {
     return (int)(g < 1 ? 1 : g);
 }
 
+template <int CH, int NT, bool HOT>
+int launch_rp(RowPassArgs &A, int grid, size_t smem, cudaStream_t st) {
+    static int attr = -1;
+    if ((int)smem > 48 * 1024 && attr < (int)smem) {
+        cudaFuncSetAttribute(k_row_pass<CH, NT, HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = (int)smem;
+    }
+    k_row_pass<CH, NT, HOT><<<grid, NT, smem, st>>>(A);
+    CHECK_LAUNCH("row_pass");
+    return 0;
+}
+
+// Shared-memory budget of the hot-term table: one persistent 1024-thread CTA
+// per SM for k <= 256 (<= 64 registers/thread), 256-thread CTAs otherwise.
+constexpr int64_t kSmemBudget = 200 * 1024;
+
+int64_t hot_terms_for(int64_t k, int64_t kp, int64_t d) {
+    const ColPlan p = col_plan(k);
+    if (p.ch > 8) return 0;
+    const int64_t staging = (int64_t)(1024 / 32) * 8 * 32 * 8;   // see k_row_pass staging layout
+    int64_t h = (kSmemBudget - staging) / (kp * 4);
+    if (h > d) h = d;
+    return h < 0 ? 0 : h;
+}
+
+int row_pass_mode() {
+    // SPKM_ROWPASS=1 selects the experimental shared-memory hot-term table
+    // (persistent 1024-thread CTAs); measured slower than the L1-cached
+    // 256-thread CTAs on C2 (profiles/r01_rowpass_hot_vs_plain.txt), so off.
+    static int mode = -1;
+    if (mode < 0) {
+        const char *s = getenv("SPKM_ROWPASS");
+        mode = s ? atoi(s) : 0;
+    }
+    return mode;
+}
+
 int launch_row_pass(RowPassArgs &A, int64_t k, cudaStream_t st, int64_t max_rows) {
     const ColPlan p = col_plan(k);
     A.tpr = p.tpr;
     A.rpw = p.rpw;
     A.k = (int)k;
     const int64_t slots = (max_rows + p.rpw - 1) / p.rpw;
-    const int grid = grid_for(slots, 8);
-    switch (p.ch) {
-        case 4: k_row_pass<4><<<grid, 256, 0, st>>>(A); break;
-        case 8: k_row_pass<8><<<grid, 256, 0, st>>>(A); break;
-        case 16: k_row_pass<16><<<grid, 256, 0, st>>>(A); break;
-        default: k_row_pass<32><<<grid, 256, 0, st>>>(A); break;
+    if (p.ch <= 8 && row_pass_mode() == 1) {
+        const int64_t d = A.hot_d;
+        A.hot = (int)hot_terms_for(k, A.kp, d);
+        const size_t smem = (size_t)A.hot * A.kp * 4 + (size_t)(1024 / 32) * 8 * 32 * 8;
+        int64_t grid = (slots + 31) / 32;
+        if (grid > num_sms()) grid = num_sms();
+        if (grid < 1) grid = 1;
+        if (p.ch == 4) return launch_rp<4, 1024, true>(A, (int)grid, smem, st);
+        return launch_rp<8, 1024, true>(A, (int)grid, smem, st);
     }
-    CHECK_LAUNCH("row_pass");
-    return 0;
+    A.hot = 0;
+    int grid = grid_for(slots, 8);
+    {
+        static int gmode = -1;   // experiment: SPKM_RPGRID=n -> n CTAs per SM (persistent)
+        if (gmode < 0) {
+            const char *s = getenv("SPKM_RPGRID");
+            gmode = s ? atoi(s) : 0;
+        }
+        if (gmode > 0) {
+            const int64_t g2 = (int64_t)num_sms() * gmode;
+            if (g2 < grid) grid = (int)g2;
+        }
+    }
+    const size_t smem = (size_t)(256 / 32) * 8 * 32 * 8;
+    if (p.ch == 4) return launch_rp<4, 256, false>(A, grid, smem, st);
+    if (p.ch == 8) return launch_rp<8, 256, false>(A, grid, smem, st);
+    if (p.ch == 16) return launch_rp<16, 256, false>(A, grid, smem, st);
+    return launch_rp<32, 256, false>(A, grid, smem, st);
 }
 
 RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     RowPassArgs A{};
+    A.hot_d = C->d;
+    A.ctl = C->ctl;
     A.indptr = X->indptr;
     A.indices = X->indices;
     A.values = X->values;
@@ -1570,7 +1681,7 @@ int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B
     const int grid = grid_for(X->n, 256);
     k_hamerly_bounds<<<grid, 256, 0, S(stream)>>>(X->n, X->row_eps, B->a, B->l, B->u, C->drift, C->sinp, C->s,
                                                   C->hstat,
-                                                  use_s, naive, W->surv1, W->ctr);
+                                                  use_s, naive, W->surv1, W->ctr, C->ctl);
     CHECK_LAUNCH("hamerly_bounds");
     return 0;
 }
@@ -1580,7 +1691,7 @@ int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *
     if (X->n == 0) return 0;
     const int grid = grid_for((X->n + 3) / 4, 8);
     k_hamerly_tighten<<<grid, 256, 0, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
-                                                   B->a, B->l, B->u, C->s, use_s, W->surv1, W->surv2, W->ctr);
+                                                   B->a, B->l, B->u, C->s, use_s, W->surv1, W->surv2, W->ctr, C->ctl);
     CHECK_LAUNCH("hamerly_tighten");
     return 0;
 }
@@ -1607,7 +1718,7 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
     k_elkan_bounds<<<grid, 256, 0, S(stream)>>>(X->n, (int)C->k, X->row_eps, B->a, B->l, B->u, B->ku, C->drift,
-                                                C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr);
+                                                C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl);
     CHECK_LAUNCH("elkan_bounds");
     return 0;
 }
@@ -1620,7 +1731,7 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
     if (dyn > 48 * 1024) cudaFuncSetAttribute(k_elkan_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
     k_elkan_scan<<<grid, 256, dyn, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
                                               (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1,
-                                              W->mv_i, W->mv_old, W->ctr);
+                                              W->mv_i, W->mv_old, W->ctr, C->ctl);
     CHECK_LAUNCH("elkan_scan");
     return 0;
 }
@@ -1635,7 +1746,7 @@ int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bou
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
     k_aggregate<<<grid, 256, 0, st>>>(X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
-                                      counts_target, ldexp(1.0, C->scale_bits));
+                                      counts_target, ldexp(1.0, C->scale_bits), C->ctl);
     CHECK_LAUNCH("aggregate");
     return 0;
 }
@@ -1646,7 +1757,7 @@ int spkm_apply_moves(const spkm_csr *X, const spkm_centers *C, const spkm_bounds
     const int grid = grid_for(X->n, 8);
     k_apply_moves<<<grid, 256, 0, S(stream)>>>(C->d, X->indptr, X->indices, X->values, B->a, W->mv_i, W->mv_old,
                                                W->ctr, sums_target, counts_target, touched,
-                                               ldexp(1.0, C->scale_bits));
+                                               ldexp(1.0, C->scale_bits), C->ctl);
     CHECK_LAUNCH("apply_moves");
     return 0;
 }
@@ -1661,25 +1772,26 @@ int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
     const int64_t nch = spkm_center_chunks(C->d);
     const int64_t ntile = (C->d + kTileT - 1) / kTileT;
     const double inv = ldexp(1.0, -C->scale_bits);
-    k_touched_list<<<1, 1024, 0, st>>>(C->k, C->touched, all_clusters, C->tlist, C->tcount);
+    k_touched_list<<<1, 1024, 0, st>>>(C->k, C->touched, all_clusters, C->tlist, C->tcount, C->ctl);
     CHECK_LAUNCH("touched_list");
     k_center_norm_part<<<dim3((unsigned)nch, (unsigned)C->k), 256, 0, st>>>(C->d, nch, C->sums, C->tlist, C->tcount,
-                                                                           inv, C->part);
+                                                                           inv, C->part, C->ctl);
     CHECK_LAUNCH("center_norm_part");
-    k_center_norm_final<<<(unsigned)C->k, 256, 0, st>>>(nch, C->counts, C->tlist, C->tcount, C->part, C->norm);
+    k_center_norm_final<<<(unsigned)C->k, 256, 0, st>>>(nch, C->counts, C->tlist, C->tcount, C->part, C->norm, C->ctl);
     CHECK_LAUNCH("center_norm_final");
     k_center_write<<<dim3((unsigned)ntile, (unsigned)((C->k + kTileJ - 1) / kTileJ)), 256, 0, st>>>(
-        C->d, C->kp, ntile, C->sums, C->tlist, C->tcount, inv, C->norm, C->cent64, C->ct32, C->part);
+        C->d, C->kp, ntile, C->sums, C->tlist, C->tcount, inv, C->norm, C->cent64, C->ct32, C->part, C->ctl);
     CHECK_LAUNCH("center_write");
     k_center_reduce<<<(unsigned)C->k, 256, 0, st>>>(ntile, C->tlist, C->tcount, C->part, C->norm, C->drift, C->sinp,
-                                                   C->objc);
+                                                   C->objc, C->ctl);
     CHECK_LAUNCH("center_reduce");
     return 0;
 }
 
 int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra, void *stream) {
     k_finalize<<<1, kFinThreads, 0, S(stream)>>>(C->k, C->touched, C->tcount, C->drift, C->sinp, C->objc, C->hstat,
-                                                 W->ctr, W->stats, sims_extra, all_clusters);
+                                                 W->ctr, W->stats, sims_extra, all_clusters, W->stats_hist,
+                                                 W->hist_cap, C->ctl);
     CHECK_LAUNCH("finalize");
     return 0;
 }
@@ -1713,12 +1825,12 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
         attr_set = true;
     }
     dim3 grid((unsigned)ntiles, (unsigned)ds);
-    k_gram_tc<<<grid, kGramThreads, smem, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart);
+    k_gram_tc<<<grid, kGramThreads, smem, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart, C->ctl);
     CHECK_LAUNCH("gram_tc");
     k_gram_final<<<(unsigned)((C->k * C->k * 8 + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, gdelta,
-                                                                           C->cc);
+                                                                           C->cc, C->ctl);
     CHECK_LAUNCH("gram_final");
-    k_row_max<<<(unsigned)((C->k * 32 + 255) / 256), 256, 0, st>>>(C->k, C->cc, C->s);
+    k_row_max<<<(unsigned)((C->k * 32 + 255) / 256), 256, 0, st>>>(C->k, C->cc, C->s, C->ctl);
     CHECK_LAUNCH("row_max");
     return 0;
 }

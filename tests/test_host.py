@@ -197,3 +197,25 @@ def test_dense_corpus_unit_rows():
     assert X.shape == (2000, 16) and X.dtype == np.float32
     assert np.allclose(np.linalg.norm(X, axis=1), 1.0, atol=1e-6)
     assert lab.min() >= 0 and lab.max() < 5
+
+
+def test_device_corpus_permutations_roundtrip():
+    """Rows longest-first and terms by document frequency: the device CSR holds the same rows."""
+    import torch
+    from paper_2107_04074_b200.engine import DeviceCorpus
+    spec = synth.CorpusSpec("t", 500, 2000, 30)
+    data = synth.sparse_corpus(spec, seed=3)
+    for rows in [(0, data.n), (100, 357)]:
+        dc = DeviceCorpus(data, torch.device("cpu"), rows=rows)
+        ip, ix, dv = (t.numpy() for t in (dc.indptr, dc.indices, dc.values))
+        lens = np.diff(ip)
+        assert np.all(lens[:-1] >= lens[1:])                  # longest first
+        for j in range(0, dc.n, 7):
+            h = rows[0] + dc.row_perm[j]
+            s, e = data.indptr[h], data.indptr[h + 1]
+            assert np.array_equal(dc.order[ix[ip[j]:ip[j + 1]]], data.indices[s:e])   # same terms, CSR order kept
+            assert np.array_equal(dv[ip[j]:ip[j + 1]], data.data[s:e].astype(np.float32))
+        x = np.arange(dc.n)
+        assert np.array_equal(dc.to_host_rows(dc.to_device_rows(x)), x)
+    df = np.bincount(data.indices, minlength=data.dim)
+    assert np.all(np.diff(df[dc.order]) <= 0)                  # hottest terms first

@@ -24,6 +24,7 @@ def timeit(fn, reps=20):
 def lloyd_plain():
     _lib.call("spkm_full_assign", eng.corpus.struct, eng.C.struct, eng.P.bounds, eng.P.work, _lib.MODE_INIT_PLAIN, A)
 print("plain rows (init mode) us:", timeit(lloyd_plain))
+if len(sys.argv) > 3: sys.exit(0)
 a = eng.P.a[:data.n].clone()
 with torch.cuda.stream(eng.stream):
     order = torch.argsort(a.long(), stable=True).to(torch.int32)
@@ -54,3 +55,12 @@ c3 = E.DeviceCorpus(d3, torch.device("cuda")); torch.cuda.synchronize()
 def lloyd_rand():
     _lib.call("spkm_full_assign", c3.struct, eng.C.struct, eng.P.bounds, eng.P.work, _lib.MODE_INIT_PLAIN, A)
 print("random-order rows us:", timeit(lloyd_rand))
+
+lp = np.argsort(-np.diff(ip), kind="stable")
+rows = [np.arange(ip[i], ip[i+1]) for i in lp]
+sel = np.concatenate(rows); lens = np.diff(ip)[lp]
+d4 = E.Dataset(np.concatenate([[0], np.cumsum(lens)]), data.indices[sel], data.data[sel], data.dim)
+c4 = E.DeviceCorpus(d4, torch.device("cuda")); torch.cuda.synchronize()
+def lloyd_len():
+    _lib.call("spkm_full_assign", c4.struct, eng.C.struct, eng.P.bounds, eng.P.work, _lib.MODE_INIT_PLAIN, A)
+print("length-desc rows us:", timeit(lloyd_len))

@@ -49,6 +49,7 @@ def parse():
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C2")
     p.add_argument("--k", type=int, default=100)
+    p.add_argument("--n", type=int, default=None, help="row count override (subsample of the config)")
     p.add_argument("--seed", type=int, default=2)
     p.add_argument("--max-iter", type=int, default=50)
     p.add_argument("--variants", default=",".join(VARIANTS))
@@ -121,7 +122,7 @@ class Clocks:
 def load_workload(args):
     from paper_2107_04074_b200 import synth
     t = time.time()
-    data = synth.config_dataset(args.config)
+    data = synth.config_dataset(args.config, n_override=args.n)
     return data, time.time() - t
 
 

@@ -101,6 +101,18 @@ typedef struct spkm_bounds {
     int64_t ku;              /* row stride of u (Elkan) or 1 (Hamerly)       */
 } spkm_bounds;
 
+/* Dense corpus (config C5): rows and centers split into tf32 hi/lo parts for
+ * the tcgen05 3xTF32 pass; centers padded with zero rows to kpad (a multiple
+ * of 256). */
+typedef struct spkm_dense {
+    int64_t D;               /* dimensionality (multiple of 32)              */
+    int64_t kpad;
+    const float *xhi;        /* [n][D]                                       */
+    const float *xlo;        /* [n][D]                                       */
+    float *bhi;              /* [kpad][D]                                    */
+    float *blo;              /* [kpad][D]                                    */
+} spkm_dense;
+
 /* Worklists and device-side counters. */
 typedef struct spkm_work {
     int32_t *surv1;          /* [n] points failing the bound test            */
@@ -193,6 +205,15 @@ int spkm_load_centers(const spkm_centers *C, const double *host_or_dev_centers, 
  * (sptr[k+1], sidx, float64 values) in device memory. */
 int spkm_seed_rows(const spkm_centers *C, const int64_t *sptr, const int32_t *sidx, const double *sval,
                    void *stream);
+
+/* Dense path (config C5).  split: x -> tf32 hi + lo; centers: cent64 -> bhi/blo;
+ * assign: the tensor-core similarity pass with fused top-2.  mode is an
+ * spkm_assign_mode, 5 (predict: writes a, best, second) or 6 (Hamerly
+ * tighten + full scan over work->surv1, kernels.py:81-112). */
+int spkm_dense_split(const float *x, int64_t count, float *hi, float *lo, void *stream);
+int spkm_dense_centers(const spkm_centers *C, const spkm_dense *Dn, void *stream);
+int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense *Dn, spkm_bounds *B,
+                      spkm_work *W, int mode, int use_s, double *best, double *second, void *stream);
 
 /* Device geometry for tests: op 0 lower, 1 upper, 2 hamerly, 3 half-angle. */
 int spkm_geometry(int op, int64_t n, const double *a, const double *b, double *out, void *stream);

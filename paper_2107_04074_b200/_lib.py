@@ -45,6 +45,10 @@ class Bounds(ctypes.Structure):
     _fields_ = [("a", c_vp), ("l", c_vp), ("u", c_vp), ("ku", c_i64)]
 
 
+class Dense(ctypes.Structure):
+    _fields_ = [("D", c_i64), ("kpad", c_i64), ("xhi", c_vp), ("xlo", c_vp), ("bhi", c_vp), ("blo", c_vp)]
+
+
 class Work(ctypes.Structure):
     _fields_ = [("surv1", c_vp), ("surv2", c_vp), ("mv_i", c_vp), ("mv_old", c_vp), ("ctr", c_vp),
                 ("stats", c_vp), ("stats_hist", c_vp), ("hist_cap", c_i64)]
@@ -52,6 +56,7 @@ class Work(ctypes.Structure):
 
 # modes / enums (include/spkm.h)
 MODE_INIT_PLAIN, MODE_INIT_ELKAN, MODE_INIT_HAMERLY, MODE_LLOYD = 0, 1, 2, 3
+MODE_PREDICT, DMODE_RESCAN_H = 5, 6
 CTR_SURV1, CTR_SURV2, CTR_MOVES, CTR_SIMS, CTR_NNZ_TIGHTEN, CTR_NNZ_RESCAN, CTR_NNZ_ELKAN = range(7)
 (ST_SIMS, ST_REASSIGN, ST_OBJECTIVE, ST_ALLONE, ST_SURV1, ST_SURV2, ST_TOUCHED, ST_NNZ_TIGHTEN, ST_NNZ_RESCAN,
  ST_NNZ_ELKAN, ST_ITER) = range(11)
@@ -84,6 +89,10 @@ _SIGS = {
     "spkm_load_centers": [_P(Centers), c_vp, c_vp],
     "spkm_geometry": [ctypes.c_int, c_i64, c_vp, c_vp, c_vp, c_vp],
     "spkm_seed_rows": [_P(Centers), c_vp, c_vp, c_vp, c_vp],
+    "spkm_dense_split": [c_vp, c_i64, c_vp, c_vp, c_vp],
+    "spkm_dense_centers": [_P(Centers), _P(Dense), c_vp],
+    "spkm_dense_assign": [_P(CSR), _P(Centers), _P(Dense), _P(Bounds), _P(Work), ctypes.c_int, ctypes.c_int,
+                          c_vp, c_vp, c_vp],
 }
 _RESTYPES = {
     "spkm_last_error": ctypes.c_char_p,
@@ -100,6 +109,7 @@ KERNELS_PER_CALL = {
     "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
     "spkm_move_centers": 5, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
+    "spkm_dense_split": 1, "spkm_dense_centers": 1, "spkm_dense_assign": 1,
 }
 
 _lib = None

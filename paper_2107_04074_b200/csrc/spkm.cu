@@ -1491,6 +1491,301 @@ __global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s, con
     if (lane == 0) s[a] = (k > 1) ? m : -1.f;
 }
 
+
+// ============================================================== dense rows
+// Config C5 (dense unit vectors): every similarity of the dense corpus is
+// computed by this tensor-core pass, so all variants share one canonical
+// value (the 3xTF32 tcgen05 result) and pruned == Lloyd holds exactly.
+//   * x = hi + lo, c = hi + lo (tf32 parts) prepared once (rows at upload,
+//     centers after every move), so staging is pure 16-byte cp.async copies
+//     into K-major no-swizzle core matrices;
+//   * CTA = 128 rows (TMEM lanes) x 256 centers (TMEM columns) per pass,
+//     ceil(k/256) passes, D/32 double-buffered stages of 32 dims, 3 MMAs per
+//     8-dim group (lo.hi, hi.lo, hi.hi); thread = row in the epilogue, which
+//     keeps a running top-2 (tie rule) and the incumbent's value;
+//   * error: (3D/8 + 8) 2^-22 (fp32 TMEM accumulation, truncation assumed)
+//     + 3e-7 (fp32 rows/centers, split residuals) -> row eps (host).
+constexpr int DN_M = 128;
+constexpr int DN_N = 256;
+constexpr int DN_KC = 32;
+constexpr int DN_THREADS = 256;
+constexpr int DN_LBO_A = (DN_M / 8) * 128 + 16;
+constexpr int DN_GRP_A = 2 * DN_LBO_A + 32;
+constexpr int DN_LBO_B = (DN_N / 8) * 128 + 16;
+constexpr int DN_GRP_B = 2 * DN_LBO_B + 32;
+constexpr int DN_OPA = (DN_KC / 8) * DN_GRP_A;     // one stage, one part (hi or lo) of A
+constexpr int DN_OPB = (DN_KC / 8) * DN_GRP_B;
+constexpr int DN_STAGE = 2 * DN_OPA + 2 * DN_OPB;
+constexpr uint32_t kDenseIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(DN_N >> 3) << 17) |
+                                 ((uint32_t)(DN_M >> 4) << 24);
+enum { DMODE_RESCAN_H = 6 };
+
+__device__ __forceinline__ uint64_t umma_desc2(uint32_t saddr, uint32_t lbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((128 >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    return d;
+}
+__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool pred) {
+    const int sz = pred ? 16 : 0;   // src-size 0 -> zero fill
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+}
+
+struct DenseArgs {
+    int64_t n, D, k, kpad, ku;
+    const float *xhi, *xlo;          // [n][D]
+    const float *bhi, *blo;          // [kpad][D]
+    const float *reps;
+    const int32_t *rowlist;          // null: rows [0, n)
+    const long long *rowcount;
+    int mode, use_s;
+    int32_t *a;
+    float *l, *u;
+    const float *s_arr;
+    int32_t *mv_i, *mv_old, *surv2;
+    long long *ctr;
+    double *best, *second;
+    const long long *ctl;
+};
+
+__global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
+    if (P.ctl[1]) return;
+    extern __shared__ __align__(1024) uint8_t dsm[];
+    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ uint32_t tmem_base_s;
+    __shared__ int32_t rows_s[DN_M];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nrows = P.rowlist ? *P.rowcount : P.n;
+    const int64_t ntiles = (nrows + DN_M - 1) / DN_M;
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_s)),
+                     "r"(DN_N)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (threadIdx.x == 0) {
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[0])) : "memory");
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[1])) : "memory");
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = tmem_base_s;
+    const int nstage = (int)(P.D / DN_KC);
+    const int npass = (int)((P.k + DN_N - 1) / DN_N);
+    uint32_t bar_uses[2] = {0, 0};   // completions consumed per barrier (uniform across threads)
+    auto buf = [&](int s) { return dsm + (size_t)s * DN_STAGE; };
+    auto stage = [&](int s, int pass, int st) {
+        uint8_t *b = buf(s);
+        const uint32_t ahi = smem_u32(b), alo = ahi + DN_OPA, bhi = alo + DN_OPA, blo = bhi + DN_OPB;
+        const int64_t k0 = (int64_t)st * DN_KC;
+        for (int e = threadIdx.x; e < DN_M * (DN_KC / 4); e += DN_THREADS) {
+            const int m = e >> 3, q = e & 7;
+            const int32_t r = rows_s[m];
+            const int off = (q >> 1) * DN_GRP_A + (q & 1) * DN_LBO_A + (m >> 3) * 128 + (m & 7) * 16;
+            const int64_t src = (int64_t)(r < 0 ? 0 : r) * P.D + k0 + 4 * q;
+            cp_async16(ahi + off, P.xhi + src, r >= 0);
+            cp_async16(alo + off, P.xlo + src, r >= 0);
+        }
+        const int64_t c0 = (int64_t)pass * DN_N;
+        for (int e = threadIdx.x; e < DN_N * (DN_KC / 4); e += DN_THREADS) {
+            const int m = e >> 3, q = e & 7;
+            const int off = (q >> 1) * DN_GRP_B + (q & 1) * DN_LBO_B + (m >> 3) * 128 + (m & 7) * 16;
+            const int64_t src = (c0 + m) * P.D + k0 + 4 * q;
+            cp_async16(bhi + off, P.bhi + src, true);
+            cp_async16(blo + off, P.blo + src, true);
+        }
+        asm volatile("cp.async.commit_group;\n" ::: "memory");
+    };
+    const int64_t row_tile_base = 0;
+    (void)row_tile_base;
+    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        if (threadIdx.x < DN_M) {
+            const int64_t slot = tile * DN_M + threadIdx.x;
+            rows_s[threadIdx.x] = slot < nrows ? (P.rowlist ? P.rowlist[slot] : (int32_t)slot) : -1;
+        }
+        __syncthreads();
+        const int32_t my_row = (threadIdx.x < DN_M) ? rows_s[threadIdx.x] : -1;
+        const int inc = (my_row >= 0 && (P.mode == SPKM_MODE_LLOYD || P.mode == DMODE_RESCAN_H)) ? P.a[my_row] : -1;
+        Top2 tp{-INFINITY, -2, -INFINITY};
+        float s_inc = 0.f;
+        const double eps = my_row >= 0 ? (double)P.reps[my_row] : 0.0;
+        for (int pass = 0; pass < npass; ++pass) {
+            const int tot = nstage;
+            stage(0, pass, 0);
+            for (int st = 0; st < tot; ++st) {
+                const int s = st & 1;
+                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                __syncthreads();
+                if (threadIdx.x == 0) {
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    const uint32_t ahi = smem_u32(buf(s)), alo = ahi + DN_OPA, bhi = alo + DN_OPA, blo = bhi + DN_OPB;
+#pragma unroll
+                    for (int g = 0; g < DN_KC / 8; ++g) {
+                        const uint64_t dah = umma_desc2(ahi + g * DN_GRP_A, DN_LBO_A);
+                        const uint64_t dal = umma_desc2(alo + g * DN_GRP_A, DN_LBO_A);
+                        const uint64_t dbh = umma_desc2(bhi + g * DN_GRP_B, DN_LBO_B);
+                        const uint64_t dbl = umma_desc2(blo + g * DN_GRP_B, DN_LBO_B);
+                        const uint32_t acc0 = (st > 0 || g > 0) ? 1u : 0u;
+                        asm volatile(
+                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                            " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                            "l"(dal), "l"(dbh), "r"(kDenseIdesc), "r"(acc0)
+                            : "memory");
+                        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem),
+                                     "l"(dah), "l"(dbl), "r"(kDenseIdesc)
+                                     : "memory");
+                        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem),
+                                     "l"(dah), "l"(dbh), "r"(kDenseIdesc)
+                                     : "memory");
+                    }
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                     smem_u32(&bars[s]))
+                                 : "memory");
+                }
+                if (st + 1 < tot) {
+                    const int ns = s ^ 1;
+                    // the MMAs that last read buffer ns must be done before it is refilled
+                    if (st >= 1) {
+                        mbar_wait(smem_u32(&bars[ns]), bar_uses[ns] & 1);
+                        ++bar_uses[ns];
+                    }
+                    stage(ns, pass, st + 1);
+                }
+            }
+            // drain: wait for the last commit (and the one before, if not yet consumed)
+            {
+                const int sl = (tot - 1) & 1;
+                if (tot >= 2) {
+                    mbar_wait(smem_u32(&bars[sl ^ 1]), bar_uses[sl ^ 1] & 1);
+                    ++bar_uses[sl ^ 1];
+                }
+                mbar_wait(smem_u32(&bars[sl]), bar_uses[sl] & 1);
+                ++bar_uses[sl];
+            }
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            if (w < 4) {
+#pragma unroll 1
+                for (int cb = 0; cb < DN_N / 32; ++cb) {
+                    uint32_t r[32];
+                    const uint32_t taddr = tmem + ((uint32_t)(w * 32) << 16) + (uint32_t)(cb * 32);
+                    asm volatile(
+                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
+                          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
+                          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                        : "r"(taddr));
+                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                    if (my_row >= 0) {
+#pragma unroll
+                        for (int q = 0; q < 32; ++q) {
+                            const int j = pass * DN_N + cb * 32 + q;
+                            if (j < P.k) {
+                                const float v = __uint_as_float(r[q]);
+                                top2_push(tp, v, j, inc);
+                                if (j == inc) s_inc = v;
+                                if (P.mode == SPKM_MODE_INIT_ELKAN)
+                                    P.u[(int64_t)my_row * P.ku + j] = store_upper((double)v + eps);
+                            }
+                        }
+                    }
+                }
+            }
+            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+            __syncthreads();
+        }
+        // per-row results (thread = row)
+        bool moved = false, surv = false;
+        long long sims = 0;
+        if (my_row >= 0) {
+            switch (P.mode) {
+                case SPKM_MODE_INIT_PLAIN:
+                case SPKM_MODE_INIT_ELKAN:
+                case SPKM_MODE_INIT_HAMERLY:
+                    P.a[my_row] = tp.bj;
+                    P.l[my_row] = store_lower((double)tp.b - eps);
+                    if (P.mode == SPKM_MODE_INIT_HAMERLY)
+                        P.u[my_row] = (P.k == 1) ? -1.f : store_upper((double)tp.s + eps);
+                    break;
+                case SPKM_MODE_LLOYD:
+                    if (tp.bj != inc) {
+                        P.a[my_row] = tp.bj;
+                        moved = true;
+                    }
+                    break;
+                case DMODE_RESCAN_H: {
+                    // kernels.py:88-112 on the canonical values: tighten, re-test, full scan
+                    const double lb = (double)s_inc - eps;
+                    sims = 1;
+                    bool pruned = (P.use_s && lb >= 0.0 && (double)P.s_arr[inc] + kSqrt2 * eps <= lb);
+                    if (!pruned) pruned = ((double)P.u[my_row] + eps <= (double)s_inc);
+                    if (pruned) {
+                        P.l[my_row] = store_lower(lb);
+                    } else {
+                        surv = true;
+                        sims += P.k - 1;
+                        if (tp.bj != inc) {
+                            P.a[my_row] = tp.bj;
+                            moved = true;
+                        }
+                        P.l[my_row] = store_lower((double)tp.b - eps);
+                        P.u[my_row] = store_upper((double)tp.s + eps);
+                    }
+                    break;
+                }
+                case MODE_PREDICT:
+                    P.a[my_row] = tp.bj;
+                    P.best[my_row] = (double)tp.b;
+                    P.second[my_row] = (P.k == 1) ? -1.0 : (double)tp.s;
+                    break;
+            }
+        }
+        if (w < 4) {
+            if (P.mode == SPKM_MODE_LLOYD || P.mode == DMODE_RESCAN_H)
+                warp_append(moved, my_row, P.mv_i, inc, P.mv_old, P.ctr + SPKM_CTR_MOVES);
+            if (P.mode == DMODE_RESCAN_H) {
+                warp_append(surv, my_row, P.surv2, 0, nullptr, P.ctr + SPKM_CTR_SURV2);
+                warp_add(P.ctr + SPKM_CTR_SIMS, sims);
+                warp_add(P.ctr + SPKM_CTR_NNZ_RESCAN, my_row >= 0 ? P.D : 0);
+            }
+        }
+        __syncthreads();
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(DN_N) : "memory");
+}
+
+__global__ void k_split_tf32(const float *__restrict__ x, int64_t count, float *hi, float *lo) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
+        const float v = x[e];
+        const uint32_t h = to_tf32(v);
+        hi[e] = __uint_as_float(h);
+        lo[e] = __uint_as_float(to_tf32(v - __uint_as_float(h)));
+    }
+}
+
+// centers (float64, [k][D]) -> tf32 hi/lo rows padded with zeros to kpad
+__global__ void k_dense_centers(int64_t k, int64_t kpad, int64_t D, const double *__restrict__ C, float *hi,
+                                float *lo, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < kpad * D;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t j = e / D;
+        const double v = j < k ? C[e] : 0.0;
+        const uint32_t h = to_tf32((float)v);
+        hi[e] = __uint_as_float(h);
+        lo[e] = __uint_as_float(to_tf32((float)(v - (double)__uint_as_float(h))));
+    }
+}
+
 // ---------------------------------------------------------------- misc
 __global__ void k_load_centers(int64_t k, int64_t d, int64_t kp, const double *__restrict__ src, double *cent64,
                                float *ct32) {
@@ -1728,7 +2023,11 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
     const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float);
-    if (dyn > 48 * 1024) cudaFuncSetAttribute(k_elkan_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    static size_t dyn_set = 0;   // static smem (16 KB staging) + dyn must fit the opt-in limit
+    if (dyn > dyn_set) {
+        cudaFuncSetAttribute(k_elkan_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        dyn_set = dyn;
+    }
     k_elkan_scan<<<grid, 256, dyn, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
                                               (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1,
                                               W->mv_i, W->mv_old, W->ctr, C->ctl);
@@ -1860,6 +2159,70 @@ int spkm_predict(const spkm_csr *X, const spkm_centers *C, int32_t *a, double *b
     A.best = best;
     A.second = second;
     return launch_row_pass(A, C->k, S(stream), X->n);
+}
+
+
+int spkm_dense_split(const float *x, int64_t count, float *hi, float *lo, void *stream) {
+    if (count == 0) return 0;
+    k_split_tf32<<<grid_for(count, 256), 256, 0, S(stream)>>>(x, count, hi, lo);
+    CHECK_LAUNCH("dense_split");
+    return 0;
+}
+
+int spkm_dense_centers(const spkm_centers *C, const spkm_dense *Dn, void *stream) {
+    k_dense_centers<<<grid_for(Dn->kpad * Dn->D, 256), 256, 0, S(stream)>>>(C->k, Dn->kpad, Dn->D, C->cent64,
+                                                                           Dn->bhi, Dn->blo, C->ctl);
+    CHECK_LAUNCH("dense_centers");
+    return 0;
+}
+
+int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense *Dn, spkm_bounds *B,
+                      spkm_work *W, int mode, int use_s, double *best, double *second, void *stream) {
+    if (X->n == 0) return 0;
+    if (Dn->D % DN_KC != 0) return fail_msg("dense dimension must be a multiple of 32");
+    if (Dn->kpad % DN_N != 0 || Dn->kpad < C->k) return fail_msg("dense kpad must cover k in multiples of 256");
+    DenseArgs P{};
+    P.n = X->n;
+    P.D = Dn->D;
+    P.k = C->k;
+    P.kpad = Dn->kpad;
+    P.ku = B ? B->ku : 1;
+    P.xhi = Dn->xhi;
+    P.xlo = Dn->xlo;
+    P.bhi = Dn->bhi;
+    P.blo = Dn->blo;
+    P.reps = X->row_eps;
+    P.mode = mode;
+    P.use_s = use_s;
+    P.a = B->a;
+    P.l = B->l;
+    P.u = B->u;
+    P.s_arr = C->s;
+    P.ctl = C->ctl;
+    if (W) {
+        P.mv_i = W->mv_i;
+        P.mv_old = W->mv_old;
+        P.surv2 = W->surv2;
+        P.ctr = W->ctr;
+    }
+    P.best = best;
+    P.second = second;
+    if (mode == DMODE_RESCAN_H) {
+        P.rowlist = W->surv1;
+        P.rowcount = W->ctr + SPKM_CTR_SURV1;
+    }
+    const size_t smem = (size_t)2 * DN_STAGE;
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_dense_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        attr = true;
+    }
+    int64_t tiles = (X->n + DN_M - 1) / DN_M;
+    int grid = (int)(tiles < num_sms() ? tiles : num_sms());
+    if (grid < 1) grid = 1;
+    k_dense_pass<<<grid, DN_THREADS, smem, S(stream)>>>(P);
+    CHECK_LAUNCH("dense_pass");
+    return 0;
 }
 
 int spkm_objective(const spkm_centers *C, const long long *sums, double *out, void *stream) {

@@ -182,6 +182,14 @@ def row_eps(lengths: np.ndarray) -> np.ndarray:
     return f
 
 
+def row_eps_dense(D: int, n: int) -> np.ndarray:
+    e = (3.0 * D / 8.0 + 8.0) * 2.0 ** -22 + 3e-7
+    f = np.float32(e)
+    if float(f) < e:
+        f = np.nextafter(f, np.float32(np.inf))
+    return np.full(n, f, dtype=np.float32)
+
+
 def scale_bits_for(n_total: int) -> int:
     """Fixed-point scale with n * 2^S <= 2^62 (SURVEY.md §7 hard part 1d)."""
     return int(62 - math.ceil(math.log2(n_total + 1)))
@@ -253,8 +261,20 @@ class DeviceCorpus:
         if pinned_host:
             host = [h.pin_memory() for h in host]
         self.host = host
+        self.dense_dim = getattr(data, "dense_dim", None) if device.type == "cuda" else None
+        if self.dense_dim is not None and self.dense_dim % 32 != 0:
+            self.dense_dim = None
+        if self.dense_dim is not None:
+            # tensor-core path: every similarity is the 3xTF32 tcgen05 value
+            # with error <= (3D/8 + 8) 2^-22 + 3e-7 (spkm.cu, dense rows)
+            host[3] = torch.from_numpy(row_eps_dense(self.dense_dim, self.n))
         self.indptr, self.indices, self.values, self.reps = [h.to(device, non_blocking=True) for h in host]
         self.h2d_bytes = sum(h.numel() * h.element_size() for h in host)
+        if self.dense_dim is not None:
+            self.xhi = torch.empty(self.nnz, dtype=torch.float32, device=device)
+            self.xlo = torch.empty_like(self.xhi)
+            _lib.call("spkm_dense_split", _ptr(self.values), self.nnz, _ptr(self.xhi), _ptr(self.xlo),
+                      ctypes_void(torch.cuda.current_stream(device).cuda_stream))
         self.struct = CSR(self.n, self.d, self.nnz, _ptr(self.indptr), _ptr(self.indices), _ptr(self.values),
                           _ptr(self.reps))
 
@@ -304,6 +324,7 @@ class CenterState:
             L.spkm_gram_tiles(k, pairs.ctypes.data)
             self.tiles = torch.from_numpy(pairs).to(dev)
             self.gram = torch.empty(int(L.spkm_gram_scratch_doubles(k, d)), **f64)
+        self.dense = None
         self.struct = Centers(k, d, self.kp, self.scale_bits, 0, _ptr(self.cent64), _ptr(self.ct32),
                               _ptr(self.sums), _ptr(self.counts), _ptr(self.drift), _ptr(self.sinp),
                               _ptr(self.touched), _ptr(self.objc), _ptr(self.part), _ptr(self.norm), _ptr(self.cc),
@@ -327,6 +348,18 @@ class CenterState:
             raise ValueError(f"centers must be {self.k} x {self.d}")
         _lib.call("spkm_load_centers", self.struct, _ptr(src), stream)
         return src  # keep alive until the stream passes
+
+    def attach_dense(self, corpus: "DeviceCorpus"):
+        """tf32 hi/lo center rows (padded to 256) for the dense tensor-core pass."""
+        D = corpus.dense_dim
+        kpad = (self.k + 255) // 256 * 256
+        self.bhi = torch.zeros(kpad * D, dtype=torch.float32, device=self.cent64.device)
+        self.blo = torch.zeros_like(self.bhi)
+        self.dense = _lib.Dense(D, kpad, _ptr(corpus.xhi), _ptr(corpus.xlo), _ptr(self.bhi), _ptr(self.blo))
+
+    def refresh_dense(self, stream):
+        if self.dense is not None:
+            _lib.call("spkm_dense_centers", self.struct, self.dense, stream)
 
     def snapshot(self) -> "CenterState":
         """A shallow CenterState whose result tensors are private copies (for ClusteringResult)."""
@@ -424,6 +457,12 @@ class Engine:
         self.hamerly = variant in _HAMERLY_FAMILY
         self.needs_cc = variant in _CC_VARIANTS
         self.C = CenterState(k, data.dim, self.n_total, self.device, self.needs_cc, order=self.corpus.order)
+        self.dense = self.corpus.dense_dim is not None
+        if self.dense:
+            if self.elkan:
+                raise ConfigError("the Elkan family is not available for dense corpora in this build "
+                                  "(standard, hamerly and simp_hamerly are)")
+            self.C.attach_dense(self.corpus)
         self.P = PointState(self.corpus.n, k, variant, self.device)
         # a dedicated stream: steady-state iterations are replayed as one CUDA graph
         self.stream = torch.cuda.Stream(device=self.device)
@@ -438,6 +477,7 @@ class Engine:
     def load_centers(self, centers: np.ndarray):
         with torch.cuda.stream(self.stream):       # H2D ordered before the kernel on this stream
             keep = self.C.load(centers, self.sp)
+        self.C.refresh_dense(self.sp)
         self.stream.synchronize()
         del keep
 
@@ -454,6 +494,7 @@ class Engine:
             t_idx = torch.from_numpy(self.corpus.new_id[data.indices[sel]].astype(np.int32)).to(dev)
             t_val = torch.from_numpy(np.ascontiguousarray(data.data[sel], np.float64)).to(dev)
             _lib.call("spkm_seed_rows", self.C.struct, _ptr(t_ptr), _ptr(t_idx), _ptr(t_val), self.sp)
+        self.C.refresh_dense(self.sp)
         self.stream.synchronize()
         self.seed_h2d_bytes = int(sptr.nbytes + t_idx.numel() * 4 + t_val.numel() * 8)
 
@@ -467,9 +508,15 @@ class Engine:
                   int(not self.C.cc_valid), self.sp)
         self.C.cc_valid = True
 
+    def _dense(self, mode: int, use_s: int = 0):
+        _lib.call("spkm_dense_assign", self.corpus.struct, self.C.struct, self.C.dense, self.P.bounds, self.P.work,
+                  mode, use_s, None, None, self.sp)
+
     def init_pass(self):
         mode = (_lib.MODE_INIT_ELKAN if self.elkan else _lib.MODE_INIT_HAMERLY if self.hamerly
                 else _lib.MODE_INIT_PLAIN)
+        if self.dense:
+            return self._dense(mode)
         _lib.call("spkm_full_assign", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work, mode, self.sp)
 
     def scratch_sums(self):
@@ -480,6 +527,8 @@ class Engine:
                 self.comm.scratch(self.C.sums, self.C.counts)
 
     def lloyd_pass(self):
+        if self.dense:
+            return self._dense(_lib.MODE_LLOYD)
         _lib.call("spkm_full_assign", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
                   _lib.MODE_LLOYD, self.sp)
 
@@ -495,6 +544,8 @@ class Engine:
         if self.elkan:
             _lib.call("spkm_elkan_scan", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
                       use_flag, self.sp)
+        elif self.dense:
+            self._dense(_lib.DMODE_RESCAN_H, use_flag)   # tighten + full scan on the canonical TC values
         else:
             _lib.call("spkm_hamerly_tighten", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
                       use_flag, self.sp)
@@ -515,6 +566,7 @@ class Engine:
 
     def move_centers(self, all_clusters: bool):
         _lib.call("spkm_move_centers", self.C.struct, int(all_clusters), self.sp)
+        self.C.refresh_dense(self.sp)
 
     def finalize_launch(self, all_clusters: bool, sims_extra: int):
         _lib.call("spkm_finalize", self.C.struct, self.P.work, int(all_clusters), int(sims_extra), self.sp)
@@ -730,7 +782,7 @@ def clear_engine_cache():
 
 # --------------------------------------------------------------- predict etc.
 def _centers_array(centroids) -> np.ndarray:
-    return np.asarray(centroids.centers if isinstance(centroids, CentroidSet) else centroids, dtype=np.float64)
+    return np.asarray(centroids.centers if hasattr(centroids, "centers") else centroids, dtype=np.float64)
 
 
 def assign_full(data: Dataset, centroids, device=None):
@@ -748,8 +800,17 @@ def assign_full(data: Dataset, centroids, device=None):
     a = torch.empty(max(data.n, 1), dtype=torch.int32, device=dev)
     best = torch.empty(max(data.n, 1), dtype=torch.float64, device=dev)
     second = torch.empty_like(best)
-    _lib.call("spkm_predict", dc.struct, cs.struct, _ptr(a), _ptr(best), _ptr(second),
-              ctypes_void(torch.cuda.current_stream(dev).cuda_stream))
+    sp = ctypes_void(torch.cuda.current_stream(dev).cuda_stream)
+    if dc.dense_dim is not None:
+        # dense corpora: the same tensor-core similarity the fit uses
+        cs.attach_dense(dc)
+        cs.refresh_dense(sp)
+        b = Bounds(_ptr(a), None, None, 1)
+        work = PointState(1, k, "standard", dev)
+        _lib.call("spkm_dense_assign", dc.struct, cs.struct, cs.dense, b, work.work, 5, 0, _ptr(best),
+                  _ptr(second), sp)
+    else:
+        _lib.call("spkm_predict", dc.struct, cs.struct, _ptr(a), _ptr(best), _ptr(second), sp)
     torch.cuda.current_stream(dev).synchronize()
     del keep
     h = dc.to_host_rows

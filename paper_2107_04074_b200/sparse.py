@@ -172,6 +172,28 @@ class Dataset:
             data = data / np.repeat(norms, np.diff(indptr))
         return cls(indptr, indices.astype(np.int32), data, dim)
 
+    @classmethod
+    def dense(cls, X, normalize_rows=True) -> "Dataset":
+        """Dense vectors (config C5) as a CSR whose rows hold every column.
+
+        Rows are L2-normalised in float64 (values / sqrt(<v, v>)); a zero row
+        raises ZeroNormError like the sparse constructors.
+        """
+        X = np.asarray(X)
+        n, d = X.shape
+        data = np.ascontiguousarray(X, dtype=np.float64)
+        if normalize_rows:
+            nrm = np.sqrt(np.einsum("ij,ij->i", data, data))
+            bad = np.nonzero(nrm == 0.0)[0]
+            if bad.size:
+                raise ZeroNormError(rows=bad.tolist())
+            data /= nrm[:, None]
+        indptr = np.arange(n + 1, dtype=np.int64) * d
+        indices = np.tile(np.arange(d, dtype=np.int32), n)
+        ds = cls(indptr, indices, data.reshape(-1), d)
+        ds.dense_dim = d
+        return ds
+
     # -- reference-compatible views ----------------------------------------
     @property
     def rows(self) -> tuple:

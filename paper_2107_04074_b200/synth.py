@@ -207,7 +207,17 @@ def dense_corpus(n: int, d: int = 256, centers: int = 1000, sigma_total: float =
     return X, lab
 
 
+# C5: n=10M dense unit vectors, d=256, 1,000 generating centers, noise of
+# total norm 0.3 (sigma = 0.3 / sqrt(256) per coordinate; see dense_corpus)
+C5 = dict(n=10_000_000, d=256, centers=1000, sigma_total=0.3)
+
+
 def config_dataset(name: str, seed: int | None = None, n_override: int | None = None) -> Dataset:
+    if name == "C5":
+        n = n_override if n_override is not None else C5["n"]
+        X, _ = dense_corpus(n, C5["d"], C5["centers"], C5["sigma_total"],
+                            seed=DATA_SEED_BASE + 5 if seed is None else seed)
+        return Dataset.dense(X)
     spec = CONFIGS[name]
     if n_override is not None:
         spec = CorpusSpec(spec.name + f"[n={n_override}]", n_override, spec.d, spec.mean_nnz,

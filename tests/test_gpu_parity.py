@@ -78,3 +78,28 @@ def test_c1_parity_all_variants(oracle_mod):
         r = spk.run(data, k, v, spk.SeedConfig(seed=seed), max_iter=mi)
         check_vs_oracle(r, z[key + "__assignments"], float(z[key + "__objective"][-1]),
                         len(z[key + "__objective"]), z[key + "__margin"])
+
+
+def test_c5_dense_subsample_parity(oracle_mod):
+    """Config C5 (dense unit vectors, d=256, k=1000) on a 20k-row subsample of the generator."""
+    import paper_2107_04074_b200 as spk
+    from paper_2107_04074_b200 import synth
+    data = synth.config_dataset("C5", n_override=20_000)
+    X = oracle_mod.CSR(data.indptr, data.indices, data.data, data.dim)
+    ref = oracle_mod.run(X, 1000, "standard", seed=5, max_iter=50)
+    margin = oracle_mod.margins(X, ref["centers"])
+    base = None
+    for v in ("standard", "hamerly", "simp_hamerly"):       # tensor-core dense path (Elkan family: sparse only)
+        r = spk.run(data, 1000, v, spk.SeedConfig(seed=5), max_iter=50)
+        if base is None:
+            base = r
+            check_vs_oracle(r, ref["assignments"], ref["objective"][-1], ref["iterations"], margin)
+        else:
+            assert np.array_equal(r.assignments, base.assignments), v
+            assert r.objective == base.objective, v
+            assert [s.reassignments for s in r.iterations] == [s.reassignments for s in base.iterations]
+    a, best, second = spk.assign_full(data, base.centers)
+    _, rb, rs = oracle_mod.assign_full(X, base.centers.centers)
+    assert np.max(np.abs(best - rb)) < 3e-5 and np.max(np.abs(second - rs)) < 3e-5
+    with pytest.raises(spk.ConfigError):
+        spk.run(data, 10, "elkan", spk.SeedConfig(seed=5), max_iter=3)

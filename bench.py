@@ -330,8 +330,9 @@ def roofline(args, data, corpus, dev, world):
 
     pk, src = peaks()
     n, nnz, k = corpus.n, corpus.nnz, args.k
+    dense = getattr(corpus, "dense_dim", None) is not None
     prof = _lib.CallProfiler(timed=True)
-    bytes_by = {}
+    bytes_by, flops_by = {}, {}
     with prof:
         for v in args.variants.split(","):
             prof.tag = v
@@ -354,6 +355,12 @@ def roofline(args, data, corpus, dev, world):
             if v in ("elkan", "simp_elkan"):
                 bytes_by[("spkm_elkan_bounds", v)] = (8 * ku + 16) * n * (len(its) - 1)
                 bytes_by[("spkm_elkan_scan", v)] = sum(8 * s.nnz_elkan + (8 * ku + 16) * s.survivors for s in its[1:])
+            if dense:
+                # tensor-core pass: 3 tf32 MMAs per (row, padded center, dim)
+                kpad = (k + 255) // 256 * 256
+                D = corpus.dense_dim
+                rows = n * n_full + (sum(s.survivors for s in its[1:]) if "hamerly" in v else 0)
+                flops_by[("spkm_dense_assign", v)] = 6 * rows * kpad * D
     torch.cuda.synchronize()
     times = prof.times_ms()
     calls = {}
@@ -364,18 +371,64 @@ def roofline(args, data, corpus, dev, world):
         calls[name][1] += 1
     total = sum(v[0] for v in calls.values())
     share = {nm: round(v[0] / total, 4) for nm, v in sorted(calls.items(), key=lambda x: -x[1][0])}
-    # dominant kernel among those with a byte model
-    cand = [nm for nm in share if any(key[0] == nm for key in bytes_by)]
+    # dominant kernel among those with a byte (HBM) or flop (tensor) model
+    cand = [nm for nm in share if any(key[0] == nm for key in list(bytes_by) + list(flops_by))]
     dom = cand[0] if cand else None
     out = {"bound": "hbm", "peak": pk.get("hbm_gbs"), "unit": "GB/s", "peak_source": src,
            "time_share": share, "traffic": None}
-    if dom:
+    if dom and any(key[0] == dom for key in flops_by):
+        ms = calls[dom][0]
+        f = sum(val for key, val in flops_by.items() if key[0] == dom)
+        peak_tf32, how = tf32_peak(dev)
+        ach = f / (ms / 1e3) / 1e12
+        out.update({"bound": "tensor", "unit": "TFLOP/s", "kernel": dom, "achieved": ach, "peak": peak_tf32,
+                    "peak_source": how, "frac": ach / peak_tf32, "launches": calls[dom][1],
+                    "algorithmic_flops": f, "kernel_ms": ms,
+                    "note": "3xTF32 flops (3 MMAs per product) over the kernel's CUDA-event time"})
+    elif dom:
         ms = calls[dom][0]
         b = sum(val for key, val in bytes_by.items() if key[0] == dom)
         ach = b / (ms / 1e3) / 1e9
         out.update({"kernel": dom, "achieved": ach, "frac": ach / pk.get("hbm_gbs"), "launches": calls[dom][1],
                     "algorithmic_bytes": b, "kernel_ms": ms})
+    tr = ncu_traffic(dom)
+    if tr is not None:
+        out["traffic"] = tr["dram_bytes_per_launch"]
+        out["traffic_source"] = tr["source"]
     return out
+
+
+def tf32_peak(dev):
+    """Measured dense TF32 tensor throughput (cuBLAS via torch, 8192^3, best of 5)."""
+    import torch
+    try:
+        old = torch.backends.cuda.matmul.allow_tf32
+        torch.backends.cuda.matmul.allow_tf32 = True
+        a = torch.randn(8192, 8192, device=dev)
+        b = torch.randn(8192, 8192, device=dev)
+        best = 0.0
+        for _ in range(6):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            torch.matmul(a, b)
+            e1.record()
+            torch.cuda.synchronize()
+            best = max(best, 2 * 8192 ** 3 / (e0.elapsed_time(e1) / 1e3) / 1e12)
+        torch.backends.cuda.matmul.allow_tf32 = old
+        return best, "measured: cuBLAS TF32 GEMM 8192^3 in bench.py"
+    except Exception as e:  # pragma: no cover
+        return 1100.0, f"nominal dense TF32 ({e!r})"
+
+
+def ncu_traffic(kernel_entry):
+    """dram bytes per launch of the entry point's main kernel from a committed ncu --set full capture."""
+    p = ROOT / "profiles" / "ncu_traffic.json"
+    if kernel_entry is None or not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(kernel_entry)
+    except Exception:
+        return None
 
 
 def main():

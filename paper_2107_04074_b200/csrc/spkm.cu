@@ -1505,15 +1505,17 @@ __global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s, con
 //     keeps a running top-2 (tie rule) and the incumbent's value;
 //   * error: (3D/8 + 8) 2^-22 (fp32 TMEM accumulation, truncation assumed)
 //     + 3e-7 (fp32 rows/centers, split residuals) -> row eps (host).
-constexpr int DN_M = 128;
-constexpr int DN_N = 256;
-constexpr int DN_KC = 32;
-constexpr int DN_THREADS = 256;
+constexpr int DN_M = 128;                         // rows per tile (TMEM lanes)
+constexpr int DN_N = 256;                         // centers per pass (TMEM columns per accumulator)
+constexpr int DN_KC = 16;                         // dims per pipeline stage
+constexpr int DN_STAGES = 4;
+constexpr int DN_THREADS = 256;                   // w0: MMA issuer, w1-3: producers, w4-7: epilogue
+constexpr int DN_PRODUCERS = 96;
 constexpr int DN_LBO_A = (DN_M / 8) * 128 + 16;
 constexpr int DN_GRP_A = 2 * DN_LBO_A + 32;
 constexpr int DN_LBO_B = (DN_N / 8) * 128 + 16;
 constexpr int DN_GRP_B = 2 * DN_LBO_B + 32;
-constexpr int DN_OPA = (DN_KC / 8) * DN_GRP_A;     // one stage, one part (hi or lo) of A
+constexpr int DN_OPA = (DN_KC / 8) * DN_GRP_A;    // one stage, one part (hi or lo) of A
 constexpr int DN_OPB = (DN_KC / 8) * DN_GRP_B;
 constexpr int DN_STAGE = 2 * DN_OPA + 2 * DN_OPB;
 constexpr uint32_t kDenseIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(DN_N >> 3) << 17) |
@@ -1531,6 +1533,12 @@ __device__ __forceinline__ uint64_t umma_desc2(uint32_t saddr, uint32_t lbo) {
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool pred) {
     const int sz = pred ? 16 : 0;   // src-size 0 -> zero fill
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(sz) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+    asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
 struct DenseArgs {
@@ -1550,129 +1558,153 @@ struct DenseArgs {
     const long long *ctl;
 };
 
+// Warp-specialised tcgen05 pipeline.  Work items are (tile, pass, stage) in
+// a fixed order; producers fill stage buffers with 16-byte cp.async copies
+// (tf32 hi/lo parts prepared on upload / per move) and signal `full`; the
+// MMA thread waits, issues 6 MMAs (2 8-dim groups x 3xTF32) into the
+// accumulator of the pass (two TMEM buffers of 256 columns, so the epilogue
+// of pass p overlaps the MMAs of pass p+1) and commits to `empty`; after
+// the last stage of a pass it commits to `accf`; the epilogue warps (one
+// thread per row) read the 256 columns, fold them into a running top-2 and
+// release the buffer through `acce`.
 __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
     if (P.ctl[1]) return;
     extern __shared__ __align__(1024) uint8_t dsm[];
-    __shared__ __align__(8) uint64_t bars[2];
+    __shared__ __align__(8) uint64_t full_b[DN_STAGES], empty_b[DN_STAGES], accf[2], acce[2];
     __shared__ uint32_t tmem_base_s;
-    __shared__ int32_t rows_s[DN_M];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nrows = P.rowlist ? *P.rowcount : P.n;
     const int64_t ntiles = (nrows + DN_M - 1) / DN_M;
+    const int nks = (int)(P.D / DN_KC);
+    const int npass = (int)(P.kpad / DN_N);
     if (w == 0) {
         asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_s)),
-                     "r"(DN_N)
+                     "r"(2 * DN_N)
                      : "memory");
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[0])) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[1])) : "memory");
+        for (int s = 0; s < DN_STAGES; ++s) {
+            mbar_init(&full_b[s], DN_PRODUCERS);
+            mbar_init(&empty_b[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&accf[b], 1);
+            mbar_init(&acce[b], 128);
+        }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_base_s;
-    const int nstage = (int)(P.D / DN_KC);
-    const int npass = (int)((P.k + DN_N - 1) / DN_N);
-    uint32_t bar_uses[2] = {0, 0};   // completions consumed per barrier (uniform across threads)
-    auto buf = [&](int s) { return dsm + (size_t)s * DN_STAGE; };
-    auto stage = [&](int s, int pass, int st) {
-        uint8_t *b = buf(s);
-        const uint32_t ahi = smem_u32(b), alo = ahi + DN_OPA, bhi = alo + DN_OPA, blo = bhi + DN_OPB;
-        const int64_t k0 = (int64_t)st * DN_KC;
-        for (int e = threadIdx.x; e < DN_M * (DN_KC / 4); e += DN_THREADS) {
-            const int m = e >> 3, q = e & 7;
-            const int32_t r = rows_s[m];
-            const int off = (q >> 1) * DN_GRP_A + (q & 1) * DN_LBO_A + (m >> 3) * 128 + (m & 7) * 16;
-            const int64_t src = (int64_t)(r < 0 ? 0 : r) * P.D + k0 + 4 * q;
-            cp_async16(ahi + off, P.xhi + src, r >= 0);
-            cp_async16(alo + off, P.xlo + src, r >= 0);
-        }
-        const int64_t c0 = (int64_t)pass * DN_N;
-        for (int e = threadIdx.x; e < DN_N * (DN_KC / 4); e += DN_THREADS) {
-            const int m = e >> 3, q = e & 7;
-            const int off = (q >> 1) * DN_GRP_B + (q & 1) * DN_LBO_B + (m >> 3) * 128 + (m & 7) * 16;
-            const int64_t src = (c0 + m) * P.D + k0 + 4 * q;
-            cp_async16(bhi + off, P.bhi + src, true);
-            cp_async16(blo + off, P.blo + src, true);
-        }
-        asm volatile("cp.async.commit_group;\n" ::: "memory");
-    };
-    const int64_t row_tile_base = 0;
-    (void)row_tile_base;
-    for (int64_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        if (threadIdx.x < DN_M) {
-            const int64_t slot = tile * DN_M + threadIdx.x;
-            rows_s[threadIdx.x] = slot < nrows ? (P.rowlist ? P.rowlist[slot] : (int32_t)slot) : -1;
-        }
-        __syncthreads();
-        const int32_t my_row = (threadIdx.x < DN_M) ? rows_s[threadIdx.x] : -1;
-        const int inc = (my_row >= 0 && (P.mode == SPKM_MODE_LLOYD || P.mode == DMODE_RESCAN_H)) ? P.a[my_row] : -1;
-        Top2 tp{-INFINITY, -2, -INFINITY};
-        float s_inc = 0.f;
-        const double eps = my_row >= 0 ? (double)P.reps[my_row] : 0.0;
-        for (int pass = 0; pass < npass; ++pass) {
-            const int tot = nstage;
-            stage(0, pass, 0);
-            for (int st = 0; st < tot; ++st) {
-                const int s = st & 1;
-                asm volatile("cp.async.wait_group 0;\n" ::: "memory");
-                asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-                __syncthreads();
-                if (threadIdx.x == 0) {
-                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                    const uint32_t ahi = smem_u32(buf(s)), alo = ahi + DN_OPA, bhi = alo + DN_OPA, blo = bhi + DN_OPB;
-#pragma unroll
-                    for (int g = 0; g < DN_KC / 8; ++g) {
-                        const uint64_t dah = umma_desc2(ahi + g * DN_GRP_A, DN_LBO_A);
-                        const uint64_t dal = umma_desc2(alo + g * DN_GRP_A, DN_LBO_A);
-                        const uint64_t dbh = umma_desc2(bhi + g * DN_GRP_B, DN_LBO_B);
-                        const uint64_t dbl = umma_desc2(blo + g * DN_GRP_B, DN_LBO_B);
-                        const uint32_t acc0 = (st > 0 || g > 0) ? 1u : 0u;
-                        asm volatile(
-                            "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                            " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                            "l"(dal), "l"(dbh), "r"(kDenseIdesc), "r"(acc0)
-                            : "memory");
-                        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem),
-                                     "l"(dah), "l"(dbl), "r"(kDenseIdesc)
-                                     : "memory");
-                        asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem),
-                                     "l"(dah), "l"(dbh), "r"(kDenseIdesc)
-                                     : "memory");
+    auto stage_ptr = [&](int s) { return dsm + (size_t)s * DN_STAGE; };
+    const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+
+    if (w >= 1 && w <= 3) {
+        // ---------------- producers
+        const int pt = threadIdx.x - 32;
+        uint32_t it = 0;
+        for (int64_t ti = 0; ti < my_tiles; ++ti) {
+            const int64_t tile = blockIdx.x + ti * gridDim.x;
+            for (int pass = 0; pass < npass; ++pass) {
+                for (int ks = 0; ks < nks; ++ks, ++it) {
+                    const int s = it % DN_STAGES;
+                    if (it >= DN_STAGES) mbar_wait(smem_u32(&empty_b[s]), ((it / DN_STAGES) - 1) & 1);
+                    const uint32_t ahi = smem_u32(stage_ptr(s)), alo = ahi + DN_OPA, bhi = alo + DN_OPA,
+                                   blo = bhi + DN_OPB;
+                    const int64_t k0 = (int64_t)ks * DN_KC;
+                    for (int e = pt; e < DN_M * (DN_KC / 4); e += DN_PRODUCERS) {
+                        const int m = e >> 2, q = e & 3;
+                        const int64_t slot = tile * DN_M + m;
+                        const int32_t r = slot < nrows ? (P.rowlist ? P.rowlist[slot] : (int32_t)slot) : -1;
+                        const int off = (q >> 1) * DN_GRP_A + (q & 1) * DN_LBO_A + (m >> 3) * 128 + (m & 7) * 16;
+                        const int64_t src = (int64_t)(r < 0 ? 0 : r) * P.D + k0 + 4 * q;
+                        cp_async16(ahi + off, P.xhi + src, r >= 0);
+                        cp_async16(alo + off, P.xlo + src, r >= 0);
                     }
-                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                                     smem_u32(&bars[s]))
+                    const int64_t c0 = (int64_t)pass * DN_N;
+                    for (int e = pt; e < DN_N * (DN_KC / 4); e += DN_PRODUCERS) {
+                        const int m = e >> 2, q = e & 3;
+                        const int off = (q >> 1) * DN_GRP_B + (q & 1) * DN_LBO_B + (m >> 3) * 128 + (m & 7) * 16;
+                        const int64_t src = (c0 + m) * P.D + k0 + 4 * q;
+                        cp_async16(bhi + off, P.bhi + src, true);
+                        cp_async16(blo + off, P.blo + src, true);
+                    }
+                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full_b[s]))
                                  : "memory");
                 }
-                if (st + 1 < tot) {
-                    const int ns = s ^ 1;
-                    // the MMAs that last read buffer ns must be done before it is refilled
-                    if (st >= 1) {
-                        mbar_wait(smem_u32(&bars[ns]), bar_uses[ns] & 1);
-                        ++bar_uses[ns];
+            }
+        }
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+    } else if (w == 0) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            uint32_t it = 0, pcount = 0;
+            for (int64_t ti = 0; ti < my_tiles; ++ti) {
+                for (int pass = 0; pass < npass; ++pass, ++pcount) {
+                    const int b = pcount & 1;
+                    if (pcount >= 2) mbar_wait(smem_u32(&acce[b]), ((pcount >> 1) - 1) & 1);
+                    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                    const uint32_t dt = tmem + (uint32_t)(b * DN_N);
+                    for (int ks = 0; ks < nks; ++ks, ++it) {
+                        const int s = it % DN_STAGES;
+                        mbar_wait(smem_u32(&full_b[s]), (it / DN_STAGES) & 1);
+                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+                        const uint32_t ahi = smem_u32(stage_ptr(s)), alo = ahi + DN_OPA, bhi = alo + DN_OPA,
+                                       blo = bhi + DN_OPB;
+#pragma unroll
+                        for (int g = 0; g < DN_KC / 8; ++g) {
+                            const uint64_t dah = umma_desc2(ahi + g * DN_GRP_A, DN_LBO_A);
+                            const uint64_t dal = umma_desc2(alo + g * DN_GRP_A, DN_LBO_A);
+                            const uint64_t dbh = umma_desc2(bhi + g * DN_GRP_B, DN_LBO_B);
+                            const uint64_t dbl = umma_desc2(blo + g * DN_GRP_B, DN_LBO_B);
+                            const uint32_t acc0 = (ks > 0 || g > 0) ? 1u : 0u;
+                            asm volatile(
+                                "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                                " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                                "l"(dal), "l"(dbh), "r"(kDenseIdesc), "r"(acc0)
+                                : "memory");
+                            asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(dt),
+                                         "l"(dah), "l"(dbl), "r"(kDenseIdesc)
+                                         : "memory");
+                            asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(dt),
+                                         "l"(dah), "l"(dbh), "r"(kDenseIdesc)
+                                         : "memory");
+                        }
+                        asm volatile(
+                            "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                smem_u32(&empty_b[s]))
+                            : "memory");
                     }
-                    stage(ns, pass, st + 1);
+                    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                                     smem_u32(&accf[b]))
+                                 : "memory");
                 }
             }
-            // drain: wait for the last commit (and the one before, if not yet consumed)
-            {
-                const int sl = (tot - 1) & 1;
-                if (tot >= 2) {
-                    mbar_wait(smem_u32(&bars[sl ^ 1]), bar_uses[sl ^ 1] & 1);
-                    ++bar_uses[sl ^ 1];
-                }
-                mbar_wait(smem_u32(&bars[sl]), bar_uses[sl] & 1);
-                ++bar_uses[sl];
-            }
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            if (w < 4) {
+        }
+        __syncwarp();
+    } else {
+        // ---------------- epilogue: thread = row (TMEM lane quarter w % 4)
+        const int m = (w - 4) * 32 + lane;
+        uint32_t pcount = 0;
+        for (int64_t ti = 0; ti < my_tiles; ++ti) {
+            const int64_t tile = blockIdx.x + ti * gridDim.x;
+            const int64_t slot = tile * DN_M + m;
+            const int32_t my_row = slot < nrows ? (P.rowlist ? P.rowlist[slot] : (int32_t)slot) : -1;
+            const int inc = (my_row >= 0 && (P.mode == SPKM_MODE_LLOYD || P.mode == DMODE_RESCAN_H)) ? P.a[my_row] : -1;
+            const double eps = my_row >= 0 ? (double)P.reps[my_row] : 0.0;
+            Top2 tp{-INFINITY, -2, -INFINITY};
+            float s_inc = 0.f;
+            for (int pass = 0; pass < npass; ++pass, ++pcount) {
+                const int b = pcount & 1;
+                mbar_wait(smem_u32(&accf[b]), (pcount >> 1) & 1);
+                asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll 1
                 for (int cb = 0; cb < DN_N / 32; ++cb) {
                     uint32_t r[32];
-                    const uint32_t taddr = tmem + ((uint32_t)(w * 32) << 16) + (uint32_t)(cb * 32);
+                    const uint32_t taddr = tmem + ((uint32_t)((w - 4) * 32) << 16) + (uint32_t)(b * DN_N + cb * 32);
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
                         "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
@@ -1697,57 +1729,54 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
                         }
                     }
                 }
+                asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+                mbar_arrive(&acce[b]);
             }
-            asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-            __syncthreads();
-        }
-        // per-row results (thread = row)
-        bool moved = false, surv = false;
-        long long sims = 0;
-        if (my_row >= 0) {
-            switch (P.mode) {
-                case SPKM_MODE_INIT_PLAIN:
-                case SPKM_MODE_INIT_ELKAN:
-                case SPKM_MODE_INIT_HAMERLY:
-                    P.a[my_row] = tp.bj;
-                    P.l[my_row] = store_lower((double)tp.b - eps);
-                    if (P.mode == SPKM_MODE_INIT_HAMERLY)
-                        P.u[my_row] = (P.k == 1) ? -1.f : store_upper((double)tp.s + eps);
-                    break;
-                case SPKM_MODE_LLOYD:
-                    if (tp.bj != inc) {
+            bool moved = false, surv = false;
+            long long sims = 0;
+            if (my_row >= 0) {
+                switch (P.mode) {
+                    case SPKM_MODE_INIT_PLAIN:
+                    case SPKM_MODE_INIT_ELKAN:
+                    case SPKM_MODE_INIT_HAMERLY:
                         P.a[my_row] = tp.bj;
-                        moved = true;
-                    }
-                    break;
-                case DMODE_RESCAN_H: {
-                    // kernels.py:88-112 on the canonical values: tighten, re-test, full scan
-                    const double lb = (double)s_inc - eps;
-                    sims = 1;
-                    bool pruned = (P.use_s && lb >= 0.0 && (double)P.s_arr[inc] + kSqrt2 * eps <= lb);
-                    if (!pruned) pruned = ((double)P.u[my_row] + eps <= (double)s_inc);
-                    if (pruned) {
-                        P.l[my_row] = store_lower(lb);
-                    } else {
-                        surv = true;
-                        sims += P.k - 1;
+                        P.l[my_row] = store_lower((double)tp.b - eps);
+                        if (P.mode == SPKM_MODE_INIT_HAMERLY)
+                            P.u[my_row] = (P.k == 1) ? -1.f : store_upper((double)tp.s + eps);
+                        break;
+                    case SPKM_MODE_LLOYD:
                         if (tp.bj != inc) {
                             P.a[my_row] = tp.bj;
                             moved = true;
                         }
-                        P.l[my_row] = store_lower((double)tp.b - eps);
-                        P.u[my_row] = store_upper((double)tp.s + eps);
+                        break;
+                    case DMODE_RESCAN_H: {
+                        // kernels.py:88-112 on the canonical values: tighten, re-test, full scan
+                        const double lb = (double)s_inc - eps;
+                        sims = 1;
+                        bool pruned = (P.use_s && lb >= 0.0 && (double)P.s_arr[inc] + kSqrt2 * eps <= lb);
+                        if (!pruned) pruned = ((double)P.u[my_row] + eps <= (double)s_inc);
+                        if (pruned) {
+                            P.l[my_row] = store_lower(lb);
+                        } else {
+                            surv = true;
+                            sims += P.k - 1;
+                            if (tp.bj != inc) {
+                                P.a[my_row] = tp.bj;
+                                moved = true;
+                            }
+                            P.l[my_row] = store_lower((double)tp.b - eps);
+                            P.u[my_row] = store_upper((double)tp.s + eps);
+                        }
+                        break;
                     }
-                    break;
+                    case MODE_PREDICT:
+                        P.a[my_row] = tp.bj;
+                        P.best[my_row] = (double)tp.b;
+                        P.second[my_row] = (P.k == 1) ? -1.0 : (double)tp.s;
+                        break;
                 }
-                case MODE_PREDICT:
-                    P.a[my_row] = tp.bj;
-                    P.best[my_row] = (double)tp.b;
-                    P.second[my_row] = (P.k == 1) ? -1.0 : (double)tp.s;
-                    break;
             }
-        }
-        if (w < 4) {
             if (P.mode == SPKM_MODE_LLOYD || P.mode == DMODE_RESCAN_H)
                 warp_append(moved, my_row, P.mv_i, inc, P.mv_old, P.ctr + SPKM_CTR_MOVES);
             if (P.mode == DMODE_RESCAN_H) {
@@ -1756,11 +1785,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
                 warp_add(P.ctr + SPKM_CTR_NNZ_RESCAN, my_row >= 0 ? P.D : 0);
             }
         }
-        __syncthreads();
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
-    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(DN_N) : "memory");
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * DN_N) : "memory");
 }
 
 __global__ void k_split_tf32(const float *__restrict__ x, int64_t count, float *hi, float *lo) {
@@ -2179,7 +2207,7 @@ int spkm_dense_centers(const spkm_centers *C, const spkm_dense *Dn, void *stream
 int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense *Dn, spkm_bounds *B,
                       spkm_work *W, int mode, int use_s, double *best, double *second, void *stream) {
     if (X->n == 0) return 0;
-    if (Dn->D % DN_KC != 0) return fail_msg("dense dimension must be a multiple of 32");
+    if (Dn->D % 32 != 0) return fail_msg("dense dimension must be a multiple of 32");
     if (Dn->kpad % DN_N != 0 || Dn->kpad < C->k) return fail_msg("dense kpad must cover k in multiples of 256");
     DenseArgs P{};
     P.n = X->n;
@@ -2211,7 +2239,7 @@ int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense
         P.rowlist = W->surv1;
         P.rowcount = W->ctr + SPKM_CTR_SURV1;
     }
-    const size_t smem = (size_t)2 * DN_STAGE;
+    const size_t smem = (size_t)DN_STAGES * DN_STAGE;
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_dense_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

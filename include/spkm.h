@@ -27,6 +27,8 @@
  *   spkm_center_thresholds  engine._center_thresholds, engine.py:192-198
  *   spkm_finalize           objective + convergence inputs, engine.py:326-337
  *   spkm_predict            engine.assign_full, engine.py:103-120
+ *   spkm_seed_kmpp          seeding.init_kmpp, seeding.py:64-89
+ *   spkm_seed_afkmc2        seeding.init_afkmc2, seeding.py:92-146
  */
 #ifndef SPKM_H
 #define SPKM_H
@@ -214,6 +216,31 @@ int spkm_dense_split(const float *x, int64_t count, float *hi, float *lo, void *
 int spkm_dense_centers(const spkm_centers *C, const spkm_dense *Dn, void *stream);
 int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense *Dn, spkm_bounds *B,
                       spkm_work *W, int mode, int use_s, double *best, double *second, void *stream);
+
+/* Seeding (seeding.py:64-146): spherical k-means++ and AFK-MC2 on the
+ * device, with the reference's splitmix64 stream (rng.py) and its float64
+ * similarity order, so the picks equal the reference's.  The CSR is the
+ * device-order corpus with float64 values; row_host maps a device row to the
+ * reference's row id (row_dev is the inverse).  picks: device int64[k] of
+ * reference row ids in pick order.  trace (optional, device [(k-1) * n]):
+ * the kmpp weight vector of every pick (seeding.py:80-81). */
+typedef struct spkm_seed {
+    int64_t n, d;
+    const int64_t *indptr;
+    const int32_t *indices;
+    const double *values;
+    const int64_t *row_host;
+    const int64_t *row_dev;
+    double *scratch;         /* spkm_seed_scratch_doubles(n, d) doubles        */
+} spkm_seed;
+int64_t spkm_seed_scratch_doubles(int64_t n, int64_t d);
+int spkm_seed_kmpp(const spkm_seed *S, int64_t k, double alpha, uint64_t seed, int64_t *picks,
+                   double *trace, void *stream);
+int spkm_seed_afkmc2(const spkm_seed *S, int64_t k, double alpha, int64_t chain_length, uint64_t seed,
+                     int64_t *picks, void *stream);
+/* Host helper (no GPU): |row| of every CSR row in the reference's np.dot
+ * order (sparse.py:52), for Dataset.from_csr. */
+int spkm_host_row_norms(int64_t n, const int64_t *indptr, const double *values, double *out);
 
 /* Device geometry for tests: op 0 lower, 1 upper, 2 hamerly, 3 half-angle. */
 int spkm_geometry(int op, int64_t n, const double *a, const double *b, double *out, void *stream);

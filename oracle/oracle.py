@@ -10,6 +10,7 @@ Reference anchors:
   run            /root/reference/pkg/src/spkmeans/engine.py:201-346
   assign_full    engine.py:103-120
   init_uniform   seeding.py:56-61 + rng.py:31-73 (splitmix64)
+  seed_kmpp      seeding.py:64-89;  seed_afkmc2  seeding.py:92-146
   geometry       geometry.py:20-68
 Parity pin: tests/test_oracle.py against tests/golden/*.npz made by running
 the reference itself (tests/golden/make_golden.py).
@@ -63,6 +64,16 @@ def lib():
                ctypes.POINTER(ctypes.c_int), HOOK_T]
         )
         L.oracle_run.restype = ctypes.c_int64
+        L.oracle_seed_kmpp.argtypes = ([ctypes.c_int64] * 2 + [_i64p, _i32p, _f64p, ctypes.c_int64, ctypes.c_double,
+                                       ctypes.c_uint64, _i64p, _f64p])
+        L.oracle_seed_kmpp.restype = ctypes.c_int
+        L.oracle_seed_afkmc2.argtypes = ([ctypes.c_int64] * 2 + [_i64p, _i32p, _f64p, ctypes.c_int64,
+                                         ctypes.c_double, ctypes.c_int64, ctypes.c_uint64, _i64p])
+        L.oracle_seed_afkmc2.restype = ctypes.c_int
+        L.oracle_np_ddot.argtypes = [ctypes.c_int64, _f64p, _f64p]
+        L.oracle_np_ddot.restype = ctypes.c_double
+        L.oracle_np_sum.argtypes = [_f64p, ctypes.c_int64]
+        L.oracle_np_sum.restype = ctypes.c_double
         L.oracle_num_threads.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -102,6 +113,19 @@ def geometry(op: str, a, b=None) -> np.ndarray:
     out = np.empty_like(a)
     lib().oracle_geometry(ops[op], a.size, _p(a, _f64p), _p(b, _f64p), _p(out, _f64p))
     return out
+
+
+def np_ddot(x, y) -> float:
+    """np.dot of two float64 vectors in numpy's OpenBLAS order (spkm_oracle.c)."""
+    x = np.ascontiguousarray(x, np.float64)
+    y = np.ascontiguousarray(y, np.float64)
+    return float(lib().oracle_np_ddot(x.size, _p(x, _f64p), _p(y, _f64p)))
+
+
+def np_sum(a) -> float:
+    """np.sum of a float64 vector (numpy's pairwise summation)."""
+    a = np.ascontiguousarray(a, np.float64)
+    return float(lib().oracle_np_sum(_p(a, _f64p), a.size))
 
 
 class CSR:
@@ -219,3 +243,24 @@ def margins(X: CSR, centers) -> np.ndarray:
 
 if os.environ.get("SPKM_ORACLE_THREADS"):
     set_threads(int(os.environ["SPKM_ORACLE_THREADS"]))
+
+
+def seed_kmpp(X: CSR, k: int, alpha: float, seed: int, trace: bool = False):
+    """init_kmpp (seeding.py:64-89): picks, and the (k-1) x n weight trace."""
+    picks = np.empty(k, np.int64)
+    tr = np.empty((max(k - 1, 1), X.n)) if trace else None
+    rc = lib().oracle_seed_kmpp(X.n, X.d, *X.args(), k, float(alpha), seed & ((1 << 64) - 1), _p(picks, _i64p),
+                                _p(tr, _f64p) if trace else None)
+    if rc != 0:
+        raise ValueError(f"k={k} infeasible for n={X.n}")
+    return (picks, tr[:k - 1]) if trace else picks
+
+
+def seed_afkmc2(X: CSR, k: int, alpha: float, chain_length: int, seed: int):
+    """init_afkmc2 (seeding.py:92-146): picks."""
+    picks = np.empty(k, np.int64)
+    rc = lib().oracle_seed_afkmc2(X.n, X.d, *X.args(), k, float(alpha), int(chain_length), seed & ((1 << 64) - 1),
+                                  _p(picks, _i64p))
+    if rc != 0:
+        raise ValueError("infeasible seeding arguments")
+    return picks

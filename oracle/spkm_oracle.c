@@ -486,3 +486,205 @@ void oracle_set_threads(int t) {
     (void)t;
 #endif
 }
+
+/* ------------------------------------------------------------ seeding.py */
+/* np.dot(x, y) of two contiguous float64 vectors as numpy computes it: its
+ * bundled OpenBLAS (scipy-openblas 0.3.30, a third-party dependency the
+ * reference does not vendor; pyproject.toml:10-14 pins no version), ddot
+ * kernel for the SkylakeX core this container reports: 32-element blocks on
+ * 4 x 8 FMA accumulators, folded to 4 x 4, then one optional 16-element block
+ * on the 4 x 4 accumulators, the fixed sum ((a0+a1)+a2)+a3, 256->128-bit halves
+ * and hadd, then an FMA tail.  Pinned against np.dot in tests/test_oracle.py.
+ * y is gathered: y[i] = c[idx[i]] (sparse.py:80-87 dot_sparse_dense). */
+static double np_ddot_gather(int64_t m, const double *x, const int32_t *idx, const double *c) {
+    const int64_t n32 = m & ~(int64_t)31, n1 = m & ~(int64_t)15;
+    double z[32] = {0};
+    for (int64_t b = 0; b < n32; b += 32)
+        for (int L = 0; L < 32; ++L) z[L] = fma(x[b + L], c[idx[b + L]], z[L]);
+    double a[16];
+    for (int bb = 0; bb < 4; ++bb)
+        for (int l = 0; l < 4; ++l) a[4 * bb + l] = z[8 * bb + l] + z[8 * bb + l + 4];
+    if (n1 > n32)
+        for (int q = 0; q < 16; ++q) a[q] = fma(x[n32 + q], c[idx[n32 + q]], a[q]);
+    double t[4];
+    for (int l = 0; l < 4; ++l) t[l] = ((a[l] + a[4 + l]) + a[8 + l]) + a[12 + l];
+    double dot = (t[0] + t[2]) + (t[1] + t[3]);
+    for (int64_t i = n1; i < m; ++i) dot = fma(c[idx[i]], x[i], dot);
+    return dot;
+}
+
+/* np.dot(x, y), contiguous (for the order test) */
+double oracle_np_ddot(int64_t m, const double *x, const double *y) {
+    int32_t *idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(m > 0 ? m : 1));
+    for (int64_t i = 0; i < m; ++i) idx[i] = (int32_t)i;
+    double r = np_ddot_gather(m, x, idx, y);
+    free(idx);
+    return r;
+}
+
+/* numpy's pairwise_sum (np.add.reduce of a contiguous float64 array) */
+static double np_pairwise(const double *a, int64_t n) {
+    if (n < 8) {
+        double r = 0.0;
+        for (int64_t i = 0; i < n; ++i) r += a[i];
+        return r;
+    }
+    if (n <= 128) {
+        double r[8];
+        for (int j = 0; j < 8; ++j) r[j] = a[j];
+        int64_t i;
+        for (i = 8; i < n - (n % 8); i += 8)
+            for (int j = 0; j < 8; ++j) r[j] += a[i + j];
+        double res = ((r[0] + r[1]) + (r[2] + r[3])) + ((r[4] + r[5]) + (r[6] + r[7]));
+        for (; i < n; ++i) res += a[i];
+        return res;
+    }
+    int64_t n2 = n / 2;
+    n2 -= n2 % 8;
+    return np_pairwise(a, n2) + np_pairwise(a + n2, n - n2);
+}
+
+double oracle_np_sum(const double *a, int64_t n) { return np_pairwise(a, n); }
+
+static inline double rng_random(uint64_t *s) { return (double)(sm64_next(s) >> 11) * 0x1.0p-53; } /* rng.py:46-47 */
+
+/* rng.weighted_index, rng.py:75-92 */
+static int64_t weighted_index(uint64_t *s, const double *w, int64_t n, double *cum) {
+    double c = 0.0;
+    for (int64_t i = 0; i < n; ++i) { c += w[i]; cum[i] = c; }
+    const double total = cum[n - 1];
+    const double r = rng_random(s) * total;
+    int64_t lo = 0, hi = n;          /* searchsorted(cum, r, side="right") */
+    while (lo < hi) { int64_t m = (lo + hi) / 2; if (r < cum[m]) hi = m; else lo = m + 1; }
+    int64_t idx = lo < n - 1 ? lo : n - 1;
+    while (w[idx] == 0.0 && idx + 1 < n) ++idx;
+    return idx;
+}
+
+/* _uniform_among_unchosen, seeding.py:50-52 */
+static int64_t uniform_unchosen(uint64_t *s, int64_t n, const unsigned char *chosen, int64_t nchosen) {
+    int64_t m = (int64_t)(sm64_next(s) % (uint64_t)(n - nchosen));
+    for (int64_t i = 0; i < n; ++i)
+        if (!chosen[i] && m-- == 0) return i;
+    return -1;
+}
+
+/* _sims_to_center, seeding.py:45-47, c = the picked row densified */
+static void sims_to_row(int64_t n, const int64_t *indptr, const int32_t *indices, const double *data,
+                        const double *c, double *out) {
+    #pragma omp parallel for schedule(static)
+    for (int64_t i = 0; i < n; ++i)
+        out[i] = np_ddot_gather(indptr[i + 1] - indptr[i], data + indptr[i], indices + indptr[i], c);
+}
+
+static void densify(double *c, const int64_t *indptr, const int32_t *indices, const double *data, int64_t r,
+                    int set) {
+    for (int64_t e = indptr[r]; e < indptr[r + 1]; ++e) c[indices[e]] = set ? data[e] : 0.0;
+}
+
+/* init_kmpp, seeding.py:64-89.  trace (optional): (k-1) x n weight vectors. */
+int oracle_seed_kmpp(int64_t n, int64_t d, const int64_t *indptr, const int32_t *indices, const double *data,
+                     int64_t k, double alpha, uint64_t seed, int64_t *picks, double *trace) {
+    if (k < 1 || k > n) return -1;
+    uint64_t s = seed;
+    double *maxsim = (double *)malloc(sizeof(double) * (size_t)n);
+    double *sims = (double *)malloc(sizeof(double) * (size_t)n);
+    double *w = (double *)malloc(sizeof(double) * (size_t)n);
+    double *cum = (double *)malloc(sizeof(double) * (size_t)n);
+    double *c = (double *)calloc((size_t)d, sizeof(double));
+    unsigned char *chosen = (unsigned char *)calloc((size_t)n, 1);
+    picks[0] = (int64_t)(sm64_next(&s) % (uint64_t)n);
+    chosen[picks[0]] = 1;
+    densify(c, indptr, indices, data, picks[0], 1);
+    sims_to_row(n, indptr, indices, data, c, maxsim);
+    for (int64_t t = 1; t < k; ++t) {
+        int any = 0;
+        for (int64_t i = 0; i < n; ++i) {
+            double v = alpha - maxsim[i];
+            w[i] = chosen[i] ? 0.0 : (v >= 0.0 ? v : 0.0);   /* np.maximum(alpha - maxsim, 0) */
+            any |= w[i] > 0.0;
+        }
+        if (trace) memcpy(trace + (t - 1) * n, w, sizeof(double) * (size_t)n);
+        int64_t pick = any ? weighted_index(&s, w, n, cum) : uniform_unchosen(&s, n, chosen, t);
+        picks[t] = pick;
+        chosen[pick] = 1;
+        densify(c, indptr, indices, data, picks[t - 1], 0);
+        densify(c, indptr, indices, data, pick, 1);
+        sims_to_row(n, indptr, indices, data, c, sims);
+        for (int64_t i = 0; i < n; ++i) maxsim[i] = maxsim[i] >= sims[i] ? maxsim[i] : sims[i];
+    }
+    free(maxsim); free(sims); free(w); free(cum); free(c); free(chosen);
+    return 0;
+}
+
+/* bisect.bisect_right */
+static int64_t bisect_right(const double *a, int64_t n, double x) {
+    int64_t lo = 0, hi = n;
+    while (lo < hi) { int64_t m = (lo + hi) / 2; if (x < a[m]) hi = m; else lo = m + 1; }
+    return lo;
+}
+
+/* init_afkmc2, seeding.py:92-146 */
+int oracle_seed_afkmc2(int64_t n, int64_t d, const int64_t *indptr, const int32_t *indices, const double *data,
+                       int64_t k, double alpha, int64_t chain_length, uint64_t seed, int64_t *picks) {
+    if (k < 1 || k > n || chain_length < 1) return -1;
+    uint64_t s = seed;
+    double *sims = (double *)malloc(sizeof(double) * (size_t)n);
+    double *dd = (double *)malloc(sizeof(double) * (size_t)n);
+    double *q = (double *)malloc(sizeof(double) * (size_t)n);
+    double *cumq = (double *)malloc(sizeof(double) * (size_t)n);
+    double *dcur = (double *)malloc(sizeof(double) * (size_t)n);
+    double *cum = (double *)malloc(sizeof(double) * (size_t)n);
+    double *c = (double *)calloc((size_t)d, sizeof(double));
+    unsigned char *chosen = (unsigned char *)calloc((size_t)n, 1);
+    const int64_t first = (int64_t)(sm64_next(&s) % (uint64_t)n);
+    picks[0] = first;
+    chosen[first] = 1;
+    densify(c, indptr, indices, data, first, 1);
+    sims_to_row(n, indptr, indices, data, c, sims);
+    for (int64_t i = 0; i < n; ++i) { double v = alpha - sims[i]; dd[i] = v >= 0.0 ? v : 0.0; }
+    dd[first] = 0.0;
+    const double total_d = np_pairwise(dd, n);
+    for (int64_t i = 0; i < n; ++i) q[i] = total_d > 0.0 ? dd[i] / (2.0 * total_d) + 0.5 / (double)n : 1.0 / (double)n;
+    double acc = 0.0;
+    for (int64_t i = 0; i < n; ++i) { acc += q[i]; cumq[i] = acc; }
+    const double qtotal = cumq[n - 1];
+    memcpy(dcur, dd, sizeof(double) * (size_t)n);
+    int64_t prev = first;
+    for (int64_t t = 1; t < k; ++t) {
+        int any = 0;
+        for (int64_t i = 0; i < n; ++i) any |= dcur[i] > 0.0;
+        int64_t cur;
+        if (!any) {
+            cur = uniform_unchosen(&s, n, chosen, t);
+        } else {
+            double r = rng_random(&s) * qtotal;
+            cur = bisect_right(cumq, n, r);
+            if (cur > n - 1) cur = n - 1;
+            for (int64_t step = 1; step < chain_length; ++step) {
+                r = rng_random(&s) * qtotal;
+                int64_t cand = bisect_right(cumq, n, r);
+                if (cand > n - 1) cand = n - 1;
+                const double num = dcur[cand] * q[cur];
+                const double den = dcur[cur] * q[cand];
+                if (den <= 0.0) cur = cand;
+                else if (rng_random(&s) * den < num) cur = cand;
+            }
+            if (dcur[cur] <= 0.0) cur = weighted_index(&s, dcur, n, cum);
+        }
+        picks[t] = cur;
+        chosen[cur] = 1;
+        densify(c, indptr, indices, data, prev, 0);
+        densify(c, indptr, indices, data, cur, 1);
+        prev = cur;
+        sims_to_row(n, indptr, indices, data, c, sims);
+        for (int64_t i = 0; i < n; ++i) {
+            double v = alpha - sims[i];
+            v = v >= 0.0 ? v : 0.0;
+            dcur[i] = dcur[i] <= v ? dcur[i] : v;   /* np.minimum */
+        }
+        dcur[cur] = 0.0;
+    }
+    free(sims); free(dd); free(q); free(cumq); free(dcur); free(cum); free(c); free(chosen);
+    return 0;
+}

@@ -49,6 +49,11 @@ class Dense(ctypes.Structure):
     _fields_ = [("D", c_i64), ("kpad", c_i64), ("xhi", c_vp), ("xlo", c_vp), ("bhi", c_vp), ("blo", c_vp)]
 
 
+class Seed(ctypes.Structure):
+    _fields_ = [("n", c_i64), ("d", c_i64), ("indptr", c_vp), ("indices", c_vp), ("values", c_vp),
+                ("row_host", c_vp), ("row_dev", c_vp), ("scratch", c_vp)]
+
+
 class Work(ctypes.Structure):
     _fields_ = [("surv1", c_vp), ("surv2", c_vp), ("mv_i", c_vp), ("mv_old", c_vp), ("ctr", c_vp),
                 ("stats", c_vp), ("stats_hist", c_vp), ("hist_cap", c_i64)]
@@ -88,6 +93,10 @@ _SIGS = {
     "spkm_objective": [_P(Centers), c_vp, c_vp, c_vp],
     "spkm_load_centers": [_P(Centers), c_vp, c_vp],
     "spkm_geometry": [ctypes.c_int, c_i64, c_vp, c_vp, c_vp, c_vp],
+    "spkm_seed_scratch_doubles": [c_i64, c_i64],
+    "spkm_seed_kmpp": [_P(Seed), c_i64, ctypes.c_double, ctypes.c_uint64, c_vp, c_vp, c_vp],
+    "spkm_seed_afkmc2": [_P(Seed), c_i64, ctypes.c_double, c_i64, ctypes.c_uint64, c_vp, c_vp],
+    "spkm_host_row_norms": [c_i64, c_vp, c_vp, c_vp],
     "spkm_seed_rows": [_P(Centers), c_vp, c_vp, c_vp, c_vp],
     "spkm_dense_split": [c_vp, c_i64, c_vp, c_vp, c_vp],
     "spkm_dense_centers": [_P(Centers), _P(Dense), c_vp],
@@ -101,6 +110,7 @@ _RESTYPES = {
     "spkm_gram_tiles": c_i64,
     "spkm_gram_scratch_doubles": c_i64,
     "spkm_center_scratch_doubles": c_i64,
+    "spkm_seed_scratch_doubles": c_i64,
 }
 
 # kernels each entry point launches (for the bench's gpu_launches count)

@@ -30,6 +30,10 @@
 #include <stdio.h>
 #include <math.h>
 #include <stdlib.h>
+#include <limits.h>
+
+#include <functional>
+#include <vector>
 
 #include "../../include/spkm.h"
 
@@ -1961,6 +1965,8 @@ RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     return A;
 }
 
+#include "seed.cuh"
+
 }  // namespace
 
 extern "C" {
@@ -2287,6 +2293,109 @@ int spkm_geometry(int op, int64_t n, const double *a, const double *b, double *o
     if (n == 0) return 0;
     k_geometry<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(op, n, a, b, out);
     CHECK_LAUNCH("geometry");
+    return 0;
+}
+
+// ------------------------------------------------------------------ seeding
+int64_t spkm_seed_scratch_doubles(int64_t n, int64_t d) { return seed::scratch_doubles(n, d); }
+
+static int seed_init(const seed::Args &A, uint64_t seed_value, cudaStream_t st) {
+    seed::Ctl c{};
+    c.rng = seed_value;
+    const char *fs = getenv("SPKM_SEED_EXACT");   // test hook (see seed.cuh)
+    c.force_seq = (fs && atoi(fs)) ? 1 : 0;
+    cudaError_t e = cudaMemsetAsync(A.chosen, 0, (size_t)A.n, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(A.cden, 0, sizeof(double) * (size_t)A.d, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(A.ctl, &c, sizeof c, cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);   // c lives on this stack frame
+    return e == cudaSuccess ? 0 : fail("seed init", e);
+}
+
+int spkm_seed_kmpp(const spkm_seed *Sd, int64_t k, double alpha, uint64_t seed_value, int64_t *picks,
+                   double *trace, void *stream) {
+    if (k < 1 || k > Sd->n) return fail_msg("seed_kmpp: k must be in [1, n]");
+    cudaStream_t st = S(stream);
+    const seed::Args A = seed::carve(Sd, picks);
+    if (int rc = seed_init(A, seed_value, st)) return rc;
+    const int gs = grid_for(A.n, 8);
+    seed::k_select<<<1, seed::kSelThreads, 0, st>>>(A, seed::SEL_FIRST, 0, 0);
+    for (int64_t t = 0; t + 1 < k; ++t) {
+        seed::k_scatter<<<1, 256, 0, st>>>(A, t);
+        seed::k_sims<<<gs, 256, 0, st>>>(A, seed::SIM_KMPP, t, alpha);
+        seed::k_partials<<<(unsigned)A.nb, 256, 0, st>>>(A.w, A.n, A.part);
+        if (trace) {
+            cudaError_t e = cudaMemcpyAsync(trace + t * A.n, A.w, sizeof(double) * A.n, cudaMemcpyDeviceToDevice, st);
+            if (e != cudaSuccess) return fail("seed_kmpp trace", e);
+        }
+        seed::k_select<<<1, seed::kSelThreads, 0, st>>>(A, seed::SEL_KMPP, t + 1, 0);
+    }
+    CHECK_LAUNCH("seed_kmpp");
+    return 0;
+}
+
+int spkm_seed_afkmc2(const spkm_seed *Sd, int64_t k, double alpha, int64_t chain_length, uint64_t seed_value,
+                     int64_t *picks, void *stream) {
+    if (k < 1 || k > Sd->n) return fail_msg("seed_afkmc2: k must be in [1, n]");
+    if (chain_length < 1) return fail_msg("seed_afkmc2: chain_length must be >= 1");
+    cudaStream_t st = S(stream);
+    const seed::Args A = seed::carve(Sd, picks);
+    if (int rc = seed_init(A, seed_value, st)) return rc;
+    const int gs = grid_for(A.n, 8);
+    seed::k_select<<<1, seed::kSelThreads, 0, st>>>(A, seed::SEL_FIRST, 0, 0);
+    seed::k_scatter<<<1, 256, 0, st>>>(A, 0);
+    seed::k_sims<<<gs, 256, 0, st>>>(A, seed::SIM_AFK_INIT, 0, alpha);
+    // sum(d) in numpy's pairwise order: plan (integers) on the host, sums on the device
+    seed::PwPlan P;
+    seed::pw_plan(A.n, P);
+    const int64_t L = (int64_t)P.leaf_off.size() - 1;
+    const int H = (int)P.lvl.size() - 1;
+    if (L > seed::max_leaves(A.n) || H > 62) return fail_msg("seed_afkmc2: pairwise plan exceeds scratch");
+    cudaError_t e = cudaMemcpyAsync(A.leaf_off, P.leaf_off.data(), sizeof(int64_t) * (L + 1), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && !P.node_lr.empty())
+        e = cudaMemcpyAsync(A.node_lr, P.node_lr.data(), sizeof(int64_t) * P.node_lr.size(), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(A.lvl, P.lvl.data(), sizeof(int64_t) * P.lvl.size(), cudaMemcpyHostToDevice, st);
+    if (e != cudaSuccess) return fail("seed_afkmc2 plan upload", e);
+    seed::k_pw_leaves<<<(unsigned)((L + 255) / 256), 256, 0, st>>>(A, L);
+    seed::k_pw_tree<<<1, 1024, 0, st>>>(A, A.lvl, H, L);
+    seed::k_afk_q<<<(unsigned)((A.n + 255) / 256), 256, 0, st>>>(A);
+    seed::k_afk_cumq<<<1, 32, 0, st>>>(A);
+    for (int64_t t = 1; t < k; ++t) {
+        seed::k_partials<<<(unsigned)A.nb, 256, 0, st>>>(A.ms, A.n, A.part);
+        seed::k_select<<<1, seed::kSelThreads, 0, st>>>(A, seed::SEL_AFK, t, chain_length);
+        if (t + 1 < k) {
+            seed::k_scatter<<<1, 256, 0, st>>>(A, t);
+            seed::k_sims<<<gs, 256, 0, st>>>(A, seed::SIM_AFK_UPDATE, t, alpha);
+        }
+    }
+    CHECK_LAUNCH("seed_afkmc2");
+    // the host plan vectors are freed on return: wait for the uploads
+    e = cudaStreamSynchronize(st);
+    return e == cudaSuccess ? 0 : fail("seed_afkmc2", e);
+}
+
+// SparseVector.norm (sparse.py:52) for every CSR row on the host, in the
+// reference's np.dot order (the ddot order of seed::warp_ddot): lets
+// Dataset.from_csr normalise rows bit-identically to Dataset.from_rows.
+int spkm_host_row_norms(int64_t n, const int64_t *indptr, const double *values, double *out) {
+    for (int64_t r = 0; r < n; ++r) {
+        const double *x = values + indptr[r];
+        const int64_t m = indptr[r + 1] - indptr[r];
+        const int64_t n32 = m & ~int64_t(31), n1 = m & ~int64_t(15);
+        double z[32] = {0};
+        for (int64_t b = 0; b < n32; b += 32)
+            for (int L = 0; L < 32; ++L) z[L] = fma(x[b + L], x[b + L], z[L]);
+        double a[16];
+        for (int bb = 0; bb < 4; ++bb)
+            for (int l = 0; l < 4; ++l) a[4 * bb + l] = z[8 * bb + l] + z[8 * bb + l + 4];
+        if (n1 > n32)
+            for (int mm = 0; mm < 16; ++mm) a[mm] = fma(x[n32 + mm], x[n32 + mm], a[mm]);
+        double t[4];
+        for (int l = 0; l < 4; ++l) t[l] = ((a[l] + a[4 + l]) + a[8 + l]) + a[12 + l];
+        const double h0 = t[0] + t[2], h1 = t[1] + t[3];
+        double dot = h0 + h1;
+        for (int64_t i = n1; i < m; ++i) dot = fma(x[i], x[i], dot);
+        out[r] = sqrt(dot);
+    }
     return 0;
 }
 

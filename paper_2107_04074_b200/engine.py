@@ -251,9 +251,7 @@ class DeviceCorpus:
         plen = lens[self.row_perm]
         ip = np.zeros(self.n + 1, np.int64)
         np.cumsum(plen, out=ip[1:])
-        src = data.indptr[r0:r1][self.row_perm]
-        sel = (np.repeat(src - ip[:-1], plen) + np.arange(int(ip[-1]), dtype=np.int64)) if self.n else \
-            np.zeros(0, np.int64)
+        sel = self._device_order(data, ip, plen)
         host = [torch.from_numpy(ip),
                 torch.from_numpy(self.new_id[data.indices[sel]].astype(np.int32)),
                 torch.from_numpy(np.ascontiguousarray(data.data[sel], np.float32)),
@@ -277,6 +275,36 @@ class DeviceCorpus:
                       ctypes_void(torch.cuda.current_stream(device).cuda_stream))
         self.struct = CSR(self.n, self.d, self.nnz, _ptr(self.indptr), _ptr(self.indices), _ptr(self.values),
                           _ptr(self.reps))
+        self._seed = None
+
+    def _device_order(self, data: Dataset, ip=None, plen=None) -> np.ndarray:
+        """nnz positions of the host CSR in device order (rows longest first)."""
+        r0, r1 = self.rows
+        if plen is None:
+            plen = np.diff(data.indptr[r0:r1 + 1])[self.row_perm]
+            ip = np.zeros(self.n + 1, np.int64)
+            np.cumsum(plen, out=ip[1:])
+        src = data.indptr[r0:r1][self.row_perm]
+        return (np.repeat(src - ip[:-1], plen) + np.arange(int(ip[-1]), dtype=np.int64)) if self.n else \
+            np.zeros(0, np.int64)
+
+    def seed_struct(self, data: Dataset):
+        """spkm_seed inputs (built once): float64 rows in device order, the row
+        maps and the seeding scratch.  Needs the whole corpus (not a shard)."""
+        if self.rows != (0, data.n):
+            raise ConfigError("device seeding needs the whole corpus on one device")
+        if self._seed is None:
+            dev = self.indptr.device
+            with torch.cuda.stream(torch.cuda.current_stream(dev)):
+                v64 = torch.from_numpy(np.ascontiguousarray(data.data[self._device_order(data)])).to(dev)
+                row_host = torch.from_numpy(self.row_perm.astype(np.int64)).to(dev)
+                row_dev = torch.from_numpy(self.row_pos.astype(np.int64)).to(dev)
+            scratch = torch.empty(int(_lib.lib().spkm_seed_scratch_doubles(self.n, self.d)), dtype=torch.float64,
+                                  device=dev)
+            st = _lib.Seed(self.n, self.d, _ptr(self.indptr), _ptr(self.indices), _ptr(v64), _ptr(row_host),
+                           _ptr(row_dev), _ptr(scratch))
+            self._seed = (st, v64, row_host, row_dev, scratch)
+        return self._seed[0]
 
 
 def device_corpus(data: Dataset, device=None, cache: bool = True) -> DeviceCorpus:
@@ -679,17 +707,13 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
         init_centers: np.ndarray | None = None, comm=None, n_total: int | None = None,
         seed_indices=None, use_graphs: bool = True) -> ClusteringResult:
     """Cluster ``data`` into ``k`` groups (reference engine.run, engine.py:201-346)."""
-    from .seeding import SeedConfig, make_centroids, uniform_rows
+    from .seeding import SeedConfig, seed_rows_for
 
     _validate(data, k, variant, hamerly_update)
     cfg = seeding if seeding is not None else SeedConfig()
     if init_centers is None:
         cfg.validate()
-        if cfg.method == "uniform":
-            seed_indices = np.asarray(uniform_rows(data.n, k, cfg.seed), dtype=np.int64)
-        else:
-            cents0 = make_centroids(data, k, cfg)
-            init_centers, seed_indices = cents0.centers, cents0.seed_indices
+        seed_indices = seed_rows_for(data, k, cfg, device=device, corpus=corpus)
     eng = _engine_for(data, k, variant, device, hamerly_update, corpus, comm, n_total, use_graphs)
     if init_centers is None:
         eng.seed_rows(data, seed_indices)

@@ -87,13 +87,28 @@ def normalize(v):
 
 
 def _row_norms(indptr, data):
-    sq = np.square(data)
+    """|row| of every CSR row exactly as SparseVector.norm computes it
+    (np.sqrt(np.dot(v, v)), sparse.py:52): the library's host helper replays
+    numpy's ddot order, so from_csr and from_rows give identical values."""
     n = indptr.size - 1
     out = np.zeros(n)
-    nonempty = indptr[1:] > indptr[:-1]
-    if sq.size:
-        out[nonempty] = np.add.reduceat(sq, indptr[:-1][nonempty])
-    return np.sqrt(out)
+    if n == 0:
+        return out
+    from .errors import DeviceError
+    try:
+        from . import _lib
+        L = _lib.lib()
+    except DeviceError:
+        L = None
+    ip = np.ascontiguousarray(indptr, np.int64)
+    dv = np.ascontiguousarray(data, np.float64)
+    if L is not None:
+        L.spkm_host_row_norms(n, ip.ctypes.data, dv.ctypes.data, out.ctypes.data)
+        return out
+    for i in range(n):   # same values, one np.dot per row
+        v = dv[ip[i]:ip[i + 1]]
+        out[i] = np.sqrt(np.dot(v, v))
+    return out
 
 
 class Dataset:

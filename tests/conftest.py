@@ -43,3 +43,29 @@ def oracle_mod():
     from oracle import oracle as O
     O.lib()
     return O
+
+
+def seeding_golden():
+    """tests/golden/seeding.npz (reference init_kmpp / init_afkmc2 picks)."""
+    return np.load(GOLDEN / "seeding.npz")
+
+
+def seeding_cases(z):
+    """[(key, method, corpus, k, alpha, chain_length, seed)]."""
+    out = []
+    for key in z.files:
+        p = key.split("__")
+        if p[0] == "kmpp":
+            out.append((key, "kmpp", p[1], int(p[2]), float(p[3]), 0, int(p[4])))
+        elif p[0] == "afk":
+            out.append((key, "afkmc2", p[1], int(p[2]), float(p[3]), int(p[4]), int(p[5])))
+    return out
+
+
+def seeding_corpus(z, name):
+    """(indptr, indices, data, dim) of a seeding golden corpus."""
+    if f"corpus__{name}__indptr" in z.files:
+        return (z[f"corpus__{name}__indptr"], z[f"corpus__{name}__indices"], z[f"corpus__{name}__data"],
+                int(z[f"corpus__{name}__dim"]))
+    g = load_golden(name)
+    return g["indptr"], g["indices"], g["data"], int(g["dim"])

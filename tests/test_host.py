@@ -219,3 +219,19 @@ def test_device_corpus_permutations_roundtrip():
         assert np.array_equal(dc.to_host_rows(dc.to_device_rows(x)), x)
     df = np.bincount(data.indices, minlength=data.dim)
     assert np.all(np.diff(df[dc.order]) <= 0)                  # hottest terms first
+
+
+def test_from_csr_normalises_like_from_rows():
+    """Dataset.from_csr row norms use the reference's np.dot order, so the
+    normalised values are bit-identical to Dataset.from_rows (sparse.py:52-58)."""
+    from paper_2107_04074_b200.sparse import Dataset, SparseVector
+    g = np.random.default_rng(3)
+    lens = g.integers(1, 420, 400)
+    ip = np.zeros(lens.size + 1, np.int64)
+    np.cumsum(lens, out=ip[1:])
+    idx = np.concatenate([np.sort(g.choice(5000, m, replace=False)) for m in lens]).astype(np.int64)
+    val = g.standard_normal(ip[-1]) * g.random(ip[-1]) ** 3 + 1e-3
+    a = Dataset.from_csr(ip, idx, val, 5000)
+    rows = [SparseVector(idx[ip[i]:ip[i + 1]], val[ip[i]:ip[i + 1]]) for i in range(lens.size)]
+    b = Dataset.from_rows(rows, dim=5000)
+    assert np.array_equal(a.data, np.concatenate([r.values for r in b.rows]))

@@ -110,3 +110,38 @@ def test_pruning_efficacy_clustered(oracle_mod):
            ("standard", "elkan", "hamerly")}
     assert tot["elkan"] / tot["standard"] < 0.5
     assert tot["hamerly"] / tot["standard"] < 1.0
+
+
+# ------------------------------------------------------------------ seeding
+from conftest import seeding_cases, seeding_corpus, seeding_golden  # noqa: E402
+
+_SZ = seeding_golden()
+
+
+@pytest.mark.parametrize("case", seeding_cases(_SZ), ids=lambda c: c[0])
+def test_oracle_seeding_matches_reference(oracle_mod, case):
+    """init_kmpp / init_afkmc2 picks (seeding.py:64-146) equal the reference's."""
+    key, method, name, k, alpha, chain, seed = case
+    X = oracle_mod.CSR(*seeding_corpus(_SZ, name))
+    tkey = f"trace__{name}__{k}__{alpha}__{seed}"
+    if method == "kmpp":
+        if tkey in _SZ.files:
+            picks, tr = oracle_mod.seed_kmpp(X, k, alpha, seed, trace=True)
+            assert np.array_equal(tr, _SZ[tkey])        # every weight vector bit-exact
+        else:
+            picks = oracle_mod.seed_kmpp(X, k, alpha, seed)
+    else:
+        picks = oracle_mod.seed_afkmc2(X, k, alpha, chain, seed)
+    assert np.array_equal(picks, _SZ[key])
+
+
+def test_numpy_reduction_orders(oracle_mod):
+    """The oracle's np.dot (OpenBLAS ddot, single-threaded sizes: rows have
+    <= 400 nnz here) and np.sum (pairwise) orders are numpy's."""
+    g = np.random.default_rng(5)
+    for n in list(range(0, 300)) + [511, 1024, 4097, 100_003]:
+        x, y = g.standard_normal(n), g.standard_normal(n)
+        if n <= 4097:
+            assert oracle_mod.np_ddot(x, y) == float(np.dot(x, y)), n
+        a = g.random(n) * g.random(n) ** 6
+        assert oracle_mod.np_sum(a) == float(a.sum()), n

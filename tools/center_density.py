@@ -1,0 +1,24 @@
+"""Center sparsity of the term-major copy after a few iterations (for the sparse-center design)."""
+import sys
+sys.path.insert(0, ".")
+import numpy as np, torch
+from paper_2107_04074_b200 import synth, engine as E
+cfg, k, its = sys.argv[1], int(sys.argv[2]), int(sys.argv[3])
+data = synth.config_dataset(cfg)
+eng = E.Engine(data, k, "hamerly", use_graphs=False)
+from paper_2107_04074_b200.seeding import uniform_rows
+eng.seed_rows(data, uniform_rows(data.n, k, 2))
+eng.reset()
+for it in range(1, its + 1):
+    eng.iteration(it)
+torch.cuda.synchronize()
+ct = eng.C.ct32.view(data.dim, eng.C.kp)[:, :k]
+nz = (ct != 0).sum(dim=1).double().cpu().numpy()
+df = np.bincount(data.indices, minlength=data.dim).astype(np.float64)[eng.corpus.order]
+w = df / df.sum()
+print(cfg, "k", k, "after", its, "its: center density", float((nz.sum()) / (k * data.dim)),
+      "nnz-weighted nz/k", float((w * nz).sum() / k))
+for thr in (0.05, 0.1, 0.25, 0.5):
+    dense_rows = nz > thr * k
+    cost = (w * np.where(dense_rows, 4 * k, 8 * nz)).sum()
+    print(f"  hybrid (dense if nz > {thr}k): bytes/nnz {cost:.0f} vs dense {4*k}; dense-row frac of nnz {w[dense_rows].sum():.3f}")

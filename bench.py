@@ -11,7 +11,9 @@ the pruned fraction as extra keys).
 
   value      device-timed (CUDA events per step, inputs resident in HBM)
   e2e        same work through the public API from pinned HOST buffers:
-             CSR + seed centers copied H2D and assignments D2H every step
+             every step the raw CSR rows are copied H2D into the serving
+             buffers (device layout rebuilt on the GPU), seed row ids H2D,
+             stats + assignments D2H
   roofline   the dominant kernel's algorithmic bytes / its event time
   cpu_baseline  the CPU oracle (C port of the reference loop, OpenMP over
              points) on a bounded sample, rank 0 at N=1 only
@@ -265,29 +267,38 @@ def main_ours(args):
     launches_per_step = prof.launches // max(args.steps, 1)
 
     # ---- e2e through the public API from host buffers ----
-    # every step: CSR shard H2D (pinned staging), then the user's call
-    # spk.run(...) per variant (seeding on the host, seed centers H2D,
-    # assignments D2H); the device corpus cache is dropped between steps.
+    # every step: the CSR shard's host arrays are staged in pinned memory and
+    # uploaded (raw rows H2D; device-order layout, term renumbering and
+    # float32 conversion rebuilt on the GPU) into the serving buffers of a
+    # persistent DeviceCorpus, then the user's call spk.run(...) per variant
+    # (seed row ids H2D, stats + assignments D2H).  One untimed warm-up fills
+    # the engine cache for that corpus.
     e2e_times, h2d, d2h = [], 0, 0
-    barrier()
-    for _ in range(args.steps):
-        flush.fill_(1)
-        data._device_cache.clear()
-        barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        c = DeviceCorpus(data, dev, rows=rows, pinned_host=True)
-        h2d, d2h = c.h2d_bytes, 0
+    c = DeviceCorpus(data, dev, rows=rows, pinned_host=True)
+
+    def e2e_step():
+        c.refresh(data)
+        b_in, b_out = c.h2d_bytes, 0
         for v in variants:
             comm = Exchange(k, data.dim, dev) if world > 1 else None
             r = spk.run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=c,
                         comm=comm, n_total=data.n)
-            h2d += int(k * 8 + sum(int(data.indptr[j + 1] - data.indptr[j]) for j in seed_rows) * 12)
-            d2h += r.assignments.nbytes
+            b_in += int(k * 8)
+            b_out += r.assignments.nbytes + 8 * len(r.iterations) * _lib.ST_COUNT
+        return b_in, b_out
+
+    e2e_step()
+    barrier()
+    for _ in range(args.steps):
+        flush.fill_(1)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        h2d, d2h = e2e_step()
         e1.record()
         barrier()
         e2e_times.append(e0.elapsed_time(e1))
-        del c
+    del c
     e2e_ms = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)

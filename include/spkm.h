@@ -134,7 +134,10 @@ enum {
 enum {
     SPKM_ST_SIMS = 0, SPKM_ST_REASSIGN = 1, SPKM_ST_OBJECTIVE = 2, SPKM_ST_ALLONE = 3,
     SPKM_ST_SURV1 = 4, SPKM_ST_SURV2 = 5, SPKM_ST_TOUCHED = 6, SPKM_ST_NNZ_TIGHTEN = 7,
-    SPKM_ST_NNZ_RESCAN = 8, SPKM_ST_NNZ_ELKAN = 9, SPKM_ST_ITER = 10, SPKM_ST_COUNT = 16
+    SPKM_ST_NNZ_RESCAN = 8, SPKM_ST_NNZ_ELKAN = 9, SPKM_ST_ITER = 10,
+    SPKM_ST_TSTAMP = 11,  /* device %globaltimer (ns) at the end of the iteration */
+    SPKM_ST_T0 = 12,      /* %globaltimer at spkm_reset_counters (start of the fit) */
+    SPKM_ST_COUNT = 16
 };
 
 int spkm_abi_version(void);
@@ -146,7 +149,7 @@ int64_t spkm_center_scratch_doubles(int64_t k, int64_t d);
 /* padded k (kp) of the term-major copy for a given k */
 int64_t spkm_padded_k(int64_t k);
 
-/* Zero counters (ctr) before an iteration. */
+/* Zero counters (ctr) and stamp stats[SPKM_ST_T0] at the start of a fit. */
 int spkm_reset_counters(spkm_work *w, void *stream);
 
 /* Full pass over rows [row_begin,row_end): every <x_i, c_j> in the canonical
@@ -172,6 +175,11 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
  * recorded moves into `sums_target`/`counts_target`, marks touched. */
 int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
                         long long *sums_target, long long *counts_target, void *stream);
+/* The same, gated on the device: a no-op unless the iteration in flight
+ * (ctl[0] + 1) is a multiple of period (engine.py:317-320 scratch rebuild,
+ * for the device-driven loop). */
+int spkm_aggregate_sums_gated(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
+                              long long *sums_target, long long *counts_target, int period, void *stream);
 int spkm_apply_moves(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
                      const spkm_work *W, long long *sums_target, long long *counts_target,
                      int32_t *touched, void *stream);
@@ -238,6 +246,28 @@ int spkm_seed_kmpp(const spkm_seed *S, int64_t k, double alpha, uint64_t seed, i
                    double *trace, void *stream);
 int spkm_seed_afkmc2(const spkm_seed *S, int64_t k, double alpha, int64_t chain_length, uint64_t seed,
                      int64_t *picks, void *stream);
+/* Seed centers = data rows given by reference row id (device rows[k]),
+ * gathered from the spkm_seed corpus (init_uniform + from_data_rows). */
+int spkm_seed_rows_csr(const spkm_centers *C, const spkm_seed *S, const int64_t *rows, void *stream);
+
+/* Device-driven fit loop (engine.py:239-337 without a host round trip per
+ * iteration): a CUDA graph whose conditional WHILE node repeats one
+ * iteration while ctl says "not converged" and ctl[0] < *limit.  begin()
+ * starts capturing the body on `stream` (the caller then issues one
+ * iteration's calls on it); end() closes and instantiates the graph. */
+int spkm_loop_begin(const long long *ctl, const long long *limit, void *stream, void **loop_out);
+int spkm_loop_end(void *loop);
+int spkm_loop_launch(void *loop, void *stream);
+int spkm_loop_destroy(void *loop);
+
+/* Corpus upload: write the rows of a raw CSR (ip_raw[n+1] relative offsets,
+ * int32 ids, float64 values) in device order: device row r = raw row
+ * perm[r] at ip_new[r], ids mapped through new_id, float32 values (round to
+ * nearest), optional float64 copy (val64) and row_eps (reps) of spkm_csr. */
+int spkm_permute_rows(int64_t n, const int64_t *ip_raw, const int32_t *idx_raw, const double *val_raw,
+                      const int64_t *perm, const int64_t *ip_new, const int64_t *new_id, int32_t *idx, float *val,
+                      double *val64, float *reps, void *stream);
+
 /* Host helper (no GPU): |row| of every CSR row in the reference's np.dot
  * order (sparse.py:52), for Dataset.from_csr. */
 int spkm_host_row_norms(int64_t n, const int64_t *indptr, const double *values, double *out);

@@ -64,7 +64,7 @@ MODE_INIT_PLAIN, MODE_INIT_ELKAN, MODE_INIT_HAMERLY, MODE_LLOYD = 0, 1, 2, 3
 MODE_PREDICT, DMODE_RESCAN_H = 5, 6
 CTR_SURV1, CTR_SURV2, CTR_MOVES, CTR_SIMS, CTR_NNZ_TIGHTEN, CTR_NNZ_RESCAN, CTR_NNZ_ELKAN = range(7)
 (ST_SIMS, ST_REASSIGN, ST_OBJECTIVE, ST_ALLONE, ST_SURV1, ST_SURV2, ST_TOUCHED, ST_NNZ_TIGHTEN, ST_NNZ_RESCAN,
- ST_NNZ_ELKAN, ST_ITER) = range(11)
+ ST_NNZ_ELKAN, ST_ITER, ST_TSTAMP, ST_T0) = range(13)
 ST_COUNT = 16
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
@@ -94,6 +94,13 @@ _SIGS = {
     "spkm_load_centers": [_P(Centers), c_vp, c_vp],
     "spkm_geometry": [ctypes.c_int, c_i64, c_vp, c_vp, c_vp, c_vp],
     "spkm_seed_scratch_doubles": [c_i64, c_i64],
+    "spkm_seed_rows_csr": [_P(Centers), _P(Seed), c_vp, c_vp],
+    "spkm_aggregate_sums_gated": [_P(CSR), _P(Centers), _P(Bounds), c_vp, c_vp, ctypes.c_int, c_vp],
+    "spkm_loop_begin": [c_vp, c_vp, c_vp, _P(c_vp)],
+    "spkm_permute_rows": [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
+    "spkm_loop_end": [c_vp],
+    "spkm_loop_launch": [c_vp, c_vp],
+    "spkm_loop_destroy": [c_vp],
     "spkm_seed_kmpp": [_P(Seed), c_i64, ctypes.c_double, ctypes.c_uint64, c_vp, c_vp, c_vp],
     "spkm_seed_afkmc2": [_P(Seed), c_i64, ctypes.c_double, c_i64, ctypes.c_uint64, c_vp, c_vp],
     "spkm_host_row_norms": [c_i64, c_vp, c_vp, c_vp],
@@ -119,7 +126,8 @@ KERNELS_PER_CALL = {
     "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
     "spkm_move_centers": 5, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
-    "spkm_dense_split": 1, "spkm_dense_centers": 1, "spkm_dense_assign": 1,
+    "spkm_dense_split": 1, "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
+    "spkm_seed_rows_csr": 1, "spkm_aggregate_sums_gated": 2, "spkm_permute_rows": 1,
 }
 
 _lib = None

@@ -116,6 +116,12 @@ __device__ __forceinline__ float store_upper(double v) {
     return __double2float_ru(v);
 }
 
+// gated scratch rebuild: only on iterations it with it % period == 0 (it =
+// ctl[0] + 1, the iteration in flight); period 0 = always
+__device__ __forceinline__ bool gate_off(const long long *ctl, int period) {
+    return period > 0 && ((ctl[0] + 1) % period) != 0;
+}
+
 // ------------------------------------------------------- canonical similarity
 // s~(i,j) = float32 FMA chain over row i's nnz in CSR order, starting at 0:
 //   acc = fma(val[t], ct[idx[t] * kp + j], acc)   for t = indptr[i] .. indptr[i+1]-1
@@ -808,8 +814,9 @@ __global__ void __launch_bounds__(256) k_aggregate(int64_t n, int64_t d, const i
                                                    const int32_t *__restrict__ indices,
                                                    const float *__restrict__ values,
                                                    const int32_t *__restrict__ a, long long *sums,
-                                                   long long *counts, double scale, const long long *__restrict__ ctl) {
-    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+                                                   long long *counts, double scale, const long long *__restrict__ ctl,
+                                                   int period) {
+    if (ctl[1] || gate_off(ctl, period)) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
@@ -1120,6 +1127,73 @@ __device__ __forceinline__ Low2 low2_shfl(const Low2 &t, int o) {
                 __shfl_down_sync(FULL, t.i2, o)};
 }
 
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+// zero the counters and stamp the start of a fit (stats[ST_T0])
+__global__ void k_reset(long long *ctr, double *stats) {
+    if (threadIdx.x < 8) ctr[threadIdx.x] = 0;
+    if (threadIdx.x == 0) stats[SPKM_ST_T0] = (double)globaltimer_ns();
+}
+
+// Condition of the device-driven fit loop: run another iteration while not
+// converged and fewer than *limit iterations are done (engine.py:239, 335-337).
+__global__ void k_loop_cond(cudaGraphConditionalHandle h, const long long *ctl, const long long *limit) {
+    cudaGraphSetConditional(h, (ctl[1] == 0 && ctl[0] < *limit) ? 1u : 0u);
+}
+
+__global__ void k_zero_sums_gated(long long *sums, int64_t count, long long *counts, int64_t k,
+                                  const long long *__restrict__ ctl, int period) {
+    if (ctl[1] || gate_off(ctl, period)) return;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) sums[i] = 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) counts[i] = 0;
+}
+
+// centers = data rows (CentroidSet.from_data_rows, engine.py:46-58) gathered
+// from the device CSR: one CTA per center
+__global__ void k_seed_rows_csr(int64_t d, int64_t kp, const int64_t *__restrict__ indptr,
+                                const int32_t *__restrict__ indices, const double *__restrict__ v64,
+                                const int64_t *__restrict__ row_dev, const int64_t *__restrict__ rows,
+                                double *cent64, float *ct32) {
+    const int64_t j = blockIdx.x;
+    const int64_t r = row_dev[rows[j]];
+    for (int64_t e = indptr[r] + threadIdx.x; e < indptr[r + 1]; e += blockDim.x) {
+        const int c = indices[e];
+        const double v = v64[e];
+        cent64[j * d + c] = v;
+        ct32[(int64_t)c * kp + j] = (float)v;
+    }
+}
+
+// corpus upload: raw CSR rows -> device order (longest first), term ids
+// renumbered, float32 values (round to nearest), optional float64 copy and
+// row_eps = (nnz + 6) * 6.1e-8 rounded up (spkm_csr.row_eps); warp per row
+__global__ void __launch_bounds__(256) k_permute_rows(int64_t n, const int64_t *__restrict__ ip_raw,
+                                                      const int32_t *__restrict__ idx_raw,
+                                                      const double *__restrict__ val_raw,
+                                                      const int64_t *__restrict__ perm,
+                                                      const int64_t *__restrict__ ip_new,
+                                                      const int64_t *__restrict__ new_id, int32_t *idx, float *val,
+                                                      double *val64, float *reps) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t r = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < n; r += warps) {
+        const int64_t src = perm[r];
+        const int64_t s0 = ip_raw[src], len = ip_raw[src + 1] - s0, d0 = ip_new[r];
+        for (int64_t q = lane; q < len; q += 32) {
+            const double v = val_raw[s0 + q];
+            idx[d0 + q] = (int32_t)new_id[idx_raw[s0 + q]];
+            val[d0 + q] = __double2float_rn(v);
+            if (val64) val64[d0 + q] = v;
+        }
+        if (lane == 0 && reps) reps[r] = __double2float_ru(((double)len + 6.0) * 6.1e-8);
+    }
+}
+
 constexpr int kFinThreads = 256;
 __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *touched,
                                                           const int32_t *__restrict__ tcount, double *drift,
@@ -1196,6 +1270,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
         // evaluated on the device so the host can enqueue iterations ahead
         const long long it = ctl[0];
         stats[SPKM_ST_ITER] = (double)(it + 1);
+        stats[SPKM_ST_TSTAMP] = (double)globaltimer_ns();
         if (it < hist_cap)
             for (int q = 0; q < SPKM_ST_COUNT; ++q) stats_hist[it * SPKM_ST_COUNT + q] = stats[q];
         const bool conv = (k == 1) || (no == 0) || (it >= 1 && ctr[SPKM_CTR_MOVES] == 0);
@@ -1984,8 +2059,9 @@ int64_t spkm_padded_k(int64_t k) {
 }
 
 int spkm_reset_counters(spkm_work *W, void *stream) {
-    cudaError_t e = cudaMemsetAsync(W->ctr, 0, 8 * sizeof(long long), S(stream));
-    return e == cudaSuccess ? 0 : fail("reset_counters", e);
+    k_reset<<<1, 32, 0, S(stream)>>>(W->ctr, W->stats);
+    CHECK_LAUNCH("reset_counters");
+    return 0;
 }
 
 int spkm_full_assign(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int mode,
@@ -2079,7 +2155,20 @@ int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bou
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
     k_aggregate<<<grid, 256, 0, st>>>(X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
-                                      counts_target, ldexp(1.0, C->scale_bits), C->ctl);
+                                      counts_target, ldexp(1.0, C->scale_bits), C->ctl, 0);
+    CHECK_LAUNCH("aggregate");
+    return 0;
+}
+
+int spkm_aggregate_sums_gated(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
+                              long long *sums_target, long long *counts_target, int period, void *stream) {
+    cudaStream_t st = S(stream);
+    k_zero_sums_gated<<<num_sms() * 4, 256, 0, st>>>(sums_target, C->k * C->d, counts_target, C->k, C->ctl, period);
+    CHECK_LAUNCH("aggregate zero");
+    if (X->n == 0) return 0;
+    const int grid = grid_for(X->n, 8);
+    k_aggregate<<<grid, 256, 0, st>>>(X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
+                                      counts_target, ldexp(1.0, C->scale_bits), C->ctl, period);
     CHECK_LAUNCH("aggregate");
     return 0;
 }
@@ -2396,6 +2485,106 @@ int spkm_host_row_norms(int64_t n, const int64_t *indptr, const double *values, 
         for (int64_t i = n1; i < m; ++i) dot = fma(x[i], x[i], dot);
         out[r] = sqrt(dot);
     }
+    return 0;
+}
+
+
+int spkm_seed_rows_csr(const spkm_centers *C, const spkm_seed *Sd, const int64_t *rows, void *stream) {
+    cudaStream_t st = S(stream);
+    cudaError_t e = cudaMemsetAsync(C->cent64, 0, sizeof(double) * C->k * C->d, st);
+    if (e == cudaSuccess) e = cudaMemsetAsync(C->ct32, 0, sizeof(float) * C->kp * C->d, st);
+    if (e != cudaSuccess) return fail("seed_rows_csr memset", e);
+    k_seed_rows_csr<<<(unsigned)C->k, 128, 0, st>>>(C->d, C->kp, Sd->indptr, Sd->indices, Sd->values, Sd->row_dev,
+                                                     rows, C->cent64, C->ct32);
+    CHECK_LAUNCH("seed_rows_csr");
+    return 0;
+}
+
+int spkm_permute_rows(int64_t n, const int64_t *ip_raw, const int32_t *idx_raw, const double *val_raw,
+                      const int64_t *perm, const int64_t *ip_new, const int64_t *new_id, int32_t *idx, float *val,
+                      double *val64, float *reps, void *stream) {
+    if (n == 0) return 0;
+    k_permute_rows<<<grid_for(n, 8), 256, 0, S(stream)>>>(n, ip_raw, idx_raw, val_raw, perm, ip_new, new_id, idx, val,
+                                                         val64, reps);
+    CHECK_LAUNCH("permute_rows");
+    return 0;
+}
+
+// ---------------------------------------------------- device-driven fit loop
+// One CUDA graph per engine: [k_loop_cond] -> WHILE(cond) { one iteration's
+// kernels (captured from the host's own calls) ; k_loop_cond }.  A fit is
+// then iteration 1 + one graph launch, with no host round trip per iteration.
+struct spkm_loop {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    cudaGraphConditionalHandle handle = 0;
+    const long long *ctl = nullptr;
+    const long long *limit = nullptr;
+    cudaStream_t stream = nullptr;
+};
+
+int spkm_loop_begin(const long long *ctl, const long long *limit, void *stream, void **out) {
+    spkm_loop *L = new spkm_loop();
+    L->ctl = ctl;
+    L->limit = limit;
+    L->stream = S(stream);
+    cudaError_t e = cudaGraphCreate(&L->graph, 0);
+    if (e == cudaSuccess) e = cudaGraphConditionalHandleCreate(&L->handle, L->graph, 0, 0);
+    cudaGraphNode_t pre = nullptr, loop = nullptr;
+    if (e == cudaSuccess) {
+        cudaKernelNodeParams kp = {};
+        void *args[] = {&L->handle, &L->ctl, &L->limit};
+        kp.func = (void *)k_loop_cond;
+        kp.gridDim = dim3(1);
+        kp.blockDim = dim3(1);
+        kp.kernelParams = args;
+        e = cudaGraphAddKernelNode(&pre, L->graph, nullptr, 0, &kp);
+    }
+    cudaGraph_t body = nullptr;
+    if (e == cudaSuccess) {
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = L->handle;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        e = cudaGraphAddNode(&loop, L->graph, &pre, 1, &np);
+        if (e == cudaSuccess) body = np.conditional.phGraph_out[0];
+    }
+    if (e == cudaSuccess) e = cudaStreamBeginCaptureToGraph(L->stream, body, nullptr, nullptr, 0,
+                                                            cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        if (L->graph) cudaGraphDestroy(L->graph);
+        delete L;
+        return fail("loop_begin", e);
+    }
+    *out = L;
+    return 0;
+}
+
+int spkm_loop_end(void *loop) {
+    spkm_loop *L = static_cast<spkm_loop *>(loop);
+    k_loop_cond<<<1, 1, 0, L->stream>>>(L->handle, L->ctl, L->limit);
+    cudaError_t e0 = cudaGetLastError();
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(L->stream, &g);
+    if (e0 != cudaSuccess) return fail("loop_end cond", e0);
+    if (e != cudaSuccess) return fail("loop_end capture", e);
+    e = cudaGraphInstantiate(&L->exec, L->graph, 0);
+    return e == cudaSuccess ? 0 : fail("loop_end instantiate", e);
+}
+
+int spkm_loop_launch(void *loop, void *stream) {
+    spkm_loop *L = static_cast<spkm_loop *>(loop);
+    cudaError_t e = cudaGraphLaunch(L->exec, S(stream));
+    return e == cudaSuccess ? 0 : fail("loop_launch", e);
+}
+
+int spkm_loop_destroy(void *loop) {
+    spkm_loop *L = static_cast<spkm_loop *>(loop);
+    if (!L) return 0;
+    if (L->exec) cudaGraphExecDestroy(L->exec);
+    if (L->graph) cudaGraphDestroy(L->graph);
+    delete L;
     return 0;
 }
 

@@ -240,10 +240,35 @@ class DeviceCorpus:
         s, e = int(data.indptr[r0]), int(data.indptr[r1])
         self.n, self.d, self.nnz = r1 - r0, data.dim, e - s
         self.rows = (r0, r1)
+        self.device = torch.device(device)
+        self.pinned_host = pinned_host
+        self._stage = None
+        self._seed = None
+        self.dense_dim = getattr(data, "dense_dim", None) if self.device.type == "cuda" else None
+        if self.dense_dim is not None and self.dense_dim % 32 != 0:
+            self.dense_dim = None
+        if self.device.type != "cuda":
+            self._host_prepare(data)
+        else:
+            i32, f32 = dict(dtype=torch.int32, device=self.device), dict(dtype=torch.float32, device=self.device)
+            self.indptr = torch.empty(self.n + 1, dtype=torch.int64, device=self.device)
+            self.indices = torch.empty(max(self.nnz, 1), **i32)
+            self.values = torch.empty(max(self.nnz, 1), **f32)
+            self.reps = torch.empty(max(self.n, 1), **f32)
+            # float64 rows in device order (seeding); dense corpora skip it
+            self.values64 = (torch.empty(max(self.nnz, 1), dtype=torch.float64, device=self.device)
+                             if self.dense_dim is None else None)
+            if self.dense_dim is not None:
+                self.xhi = torch.empty(max(self.nnz, 1), **f32)
+                self.xlo = torch.empty_like(self.xhi)
+            self._device_prepare(data)
+        self.struct = CSR(self.n, self.d, self.nnz, _ptr(self.indptr), _ptr(self.indices), _ptr(self.values),
+                          _ptr(self.reps))
+
+    def _host_prepare(self, data: Dataset):
+        """numpy path (CPU devices: host-logic tests)."""
+        r0, r1 = self.rows
         self.order, self.new_id = term_order(data)
-        # Rows are stored longest first: warps take rows in index order, so
-        # the lognormal tail of long rows no longer finishes last (41% faster
-        # full pass on C2).  row_perm[device position] = host row - r0.
         lens = np.diff(data.indptr[r0:r1 + 1])
         self.row_perm = np.argsort(-lens, kind="stable").astype(np.int64)
         self.row_pos = np.empty_like(self.row_perm)
@@ -256,26 +281,72 @@ class DeviceCorpus:
                 torch.from_numpy(self.new_id[data.indices[sel]].astype(np.int32)),
                 torch.from_numpy(np.ascontiguousarray(data.data[sel], np.float32)),
                 torch.from_numpy(row_eps(plen))]
-        if pinned_host:
-            host = [h.pin_memory() for h in host]
-        self.host = host
-        self.dense_dim = getattr(data, "dense_dim", None) if device.type == "cuda" else None
-        if self.dense_dim is not None and self.dense_dim % 32 != 0:
-            self.dense_dim = None
-        if self.dense_dim is not None:
+        self.indptr, self.indices, self.values, self.reps = [h.to(self.device) for h in host]
+        self.h2d_bytes = sum(h.numel() * h.element_size() for h in host)
+
+    def _device_prepare(self, data: Dataset):
+        """Upload the raw CSR rows once and build the device layout on the GPU:
+        rows longest first (stable), term ids renumbered by document frequency
+        (stable), float32 values, row_eps (spkm_permute_rows)."""
+        r0, r1 = self.rows
+        s, e = int(data.indptr[r0]), int(data.indptr[r1])
+        dev = self.device
+        stream = torch.cuda.current_stream(dev)
+        sp = ctypes_void(stream.cuda_stream)
+        ip_h = torch.from_numpy(np.asarray(data.indptr[r0:r1 + 1], dtype=np.int64) - s)
+        idx_h = torch.from_numpy(np.ascontiguousarray(data.indices[s:e], dtype=np.int32))
+        val_h = torch.from_numpy(np.ascontiguousarray(data.data[s:e], dtype=np.float64))
+        if self.pinned_host:
+            if self._stage is None:
+                self._stage = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (ip_h, idx_h, val_h)]
+            for dst, src in zip(self._stage, (ip_h, idx_h, val_h)):
+                dst.copy_(src)
+            ip_h, idx_h, val_h = self._stage
+        ip_raw = ip_h.to(dev, non_blocking=True)
+        idx_raw = idx_h.to(dev, non_blocking=True)
+        val_raw = val_h.to(dev, non_blocking=True)
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in (ip_h, idx_h, val_h))
+        lens = ip_raw[1:] - ip_raw[:-1]
+        perm = torch.sort(-lens, stable=True).indices
+        self.indptr[0] = 0
+        torch.cumsum(lens[perm], 0, out=self.indptr[1:])
+        cached = getattr(data, "_term_order", None)
+        if cached is None and self.rows == (0, data.n):
+            df = torch.bincount(idx_raw.to(torch.int64), minlength=self.d)
+            order_d = torch.sort(-df, stable=True).indices
+            new_id_d = torch.empty_like(order_d)
+            new_id_d[order_d] = torch.arange(self.d, device=dev)
+            order_h, new_id_h = order_d.cpu().numpy(), new_id_d.cpu().numpy()
+            data._term_order = (order_h, new_id_h)
+        else:
+            order_h, new_id_h = term_order(data)
+            new_id_d = torch.from_numpy(new_id_h).to(dev, non_blocking=True)
+        self.order, self.new_id = order_h, new_id_h
+        dense = self.dense_dim is not None
+        _lib.call("spkm_permute_rows", self.n, _ptr(ip_raw), _ptr(idx_raw), _ptr(val_raw), _ptr(perm),
+                  _ptr(self.indptr), _ptr(new_id_d), _ptr(self.indices), _ptr(self.values), _ptr(self.values64),
+                  None if dense else _ptr(self.reps), sp)
+        if dense:
             # tensor-core path: every similarity is the 3xTF32 tcgen05 value
             # with error <= (3D/8 + 8) 2^-22 + 3e-7 (spkm.cu, dense rows)
-            host[3] = torch.from_numpy(row_eps_dense(self.dense_dim, self.n))
-        self.indptr, self.indices, self.values, self.reps = [h.to(device, non_blocking=True) for h in host]
-        self.h2d_bytes = sum(h.numel() * h.element_size() for h in host)
-        if self.dense_dim is not None:
-            self.xhi = torch.empty(self.nnz, dtype=torch.float32, device=device)
-            self.xlo = torch.empty_like(self.xhi)
-            _lib.call("spkm_dense_split", _ptr(self.values), self.nnz, _ptr(self.xhi), _ptr(self.xlo),
-                      ctypes_void(torch.cuda.current_stream(device).cuda_stream))
-        self.struct = CSR(self.n, self.d, self.nnz, _ptr(self.indptr), _ptr(self.indices), _ptr(self.values),
-                          _ptr(self.reps))
-        self._seed = None
+            self.reps.fill_(float(row_eps_dense(self.dense_dim, 1)[0]))
+            _lib.call("spkm_dense_split", _ptr(self.values), self.nnz, _ptr(self.xhi), _ptr(self.xlo), sp)
+        self.perm_dev = perm
+        self.row_perm = perm.cpu().numpy()
+        self.row_pos = np.empty_like(self.row_perm)
+        self.row_pos[self.row_perm] = np.arange(self.n, dtype=np.int64)
+        if self._seed is not None:          # refresh: the seeding maps follow the new rows
+            self._seed[2].copy_(perm)
+            self._seed[3].copy_(torch.from_numpy(self.row_pos).to(dev))
+        del ip_raw, idx_raw, val_raw        # stream-ordered frees (caching allocator)
+
+    def refresh(self, data: Dataset):
+        """Upload new rows of the same shape (n, nnz, d) into the same device
+        buffers: every pointer an engine or a captured loop holds stays valid."""
+        r0, r1 = self.rows
+        if (r1 - r0, int(data.indptr[r1] - data.indptr[r0]), data.dim) != (self.n, self.nnz, self.d):
+            raise ValueError("refresh needs a corpus of the same shape (n, nnz, d)")
+        self._device_prepare(data)
 
     def _device_order(self, data: Dataset, ip=None, plen=None) -> np.ndarray:
         """nnz positions of the host CSR in device order (rows longest first)."""
@@ -295,10 +366,11 @@ class DeviceCorpus:
             raise ConfigError("device seeding needs the whole corpus on one device")
         if self._seed is None:
             dev = self.indptr.device
-            with torch.cuda.stream(torch.cuda.current_stream(dev)):
+            v64 = self.values64
+            if v64 is None:     # dense corpora: float64 rows on demand
                 v64 = torch.from_numpy(np.ascontiguousarray(data.data[self._device_order(data)])).to(dev)
-                row_host = torch.from_numpy(self.row_perm.astype(np.int64)).to(dev)
-                row_dev = torch.from_numpy(self.row_pos.astype(np.int64)).to(dev)
+            row_host = self.perm_dev.clone()
+            row_dev = torch.from_numpy(self.row_pos).to(dev)
             scratch = torch.empty(int(_lib.lib().spkm_seed_scratch_doubles(self.n, self.d)), dtype=torch.float64,
                                   device=dev)
             st = _lib.Seed(self.n, self.d, _ptr(self.indptr), _ptr(self.indices), _ptr(v64), _ptr(row_host),
@@ -497,9 +569,25 @@ class Engine:
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.sp = ctypes_void(self.stream.cuda_stream)
         self.use_graphs = use_graphs and comm is None
-        self.graph = None
-        self.graph_kernels = 0
+        self.loop = None                 # device-driven fit loop (CUDA graph with a WHILE node)
+        self.loop_kernels = 0            # kernels per loop-body iteration
+        self.limit = torch.zeros(1, dtype=torch.int64, device=self.device)
+        self.a_host = torch.empty(max(self.corpus.n, 1), dtype=torch.int32).pin_memory()
+        self.rows_host = None
+        self._keep = None                # host->device staging kept alive until the stream passes
         self.runs = 0
+
+    def drop_loop(self):
+        if getattr(self, "loop", None) is not None:
+            self.stream.synchronize()
+            _lib.lib().spkm_loop_destroy(self.loop)
+            self.loop = None
+
+    def __del__(self):
+        try:
+            self.drop_loop()
+        except Exception:
+            pass
 
     # -- phases --------------------------------------------------------------
     def load_centers(self, centers: np.ndarray):
@@ -510,20 +598,36 @@ class Engine:
         del keep
 
     def seed_rows(self, data: Dataset, rows):
-        """Seed centers = the given data rows (CentroidSet.from_data_rows) built on the device."""
+        """Seed centers = the given data rows (CentroidSet.from_data_rows) built on the device.
+
+        Sparse corpora: only the k row ids travel (pinned, async); the rows
+        are gathered from the corpus's float64 device copy.  No host sync."""
         rows = np.asarray(rows, dtype=np.int64)
-        starts, ends = data.indptr[rows], data.indptr[rows + 1]
-        sptr = np.zeros(rows.size + 1, np.int64)
-        np.cumsum(ends - starts, out=sptr[1:])
-        sel = np.concatenate([np.arange(s, e) for s, e in zip(starts, ends)]) if rows.size else np.zeros(0, np.int64)
         dev = self.device
+        if self.corpus.dense_dim is None and self.corpus.rows == (0, data.n):
+            st = self.corpus.seed_struct(data)
+            if self.rows_host is None or self.rows_host.numel() < rows.size:
+                self.rows_host = torch.empty(max(rows.size, 1), dtype=torch.int64).pin_memory()
+            self.stream.synchronize()          # the pinned staging may still feed the previous fit
+            self.rows_host[:rows.size].copy_(torch.from_numpy(rows))
+            with torch.cuda.stream(self.stream):
+                t_rows = self.rows_host[:rows.size].to(dev, non_blocking=True)
+                _lib.call("spkm_seed_rows_csr", self.C.struct, st, _ptr(t_rows), self.sp)
+            self._keep = (t_rows,)
+            self.seed_h2d_bytes = int(rows.nbytes)
+            return
+        starts, ends = data.indptr[rows], data.indptr[rows + 1]
+        lens = ends - starts
+        sptr = np.zeros(rows.size + 1, np.int64)
+        np.cumsum(lens, out=sptr[1:])
+        sel = np.repeat(starts - sptr[:-1], lens) + np.arange(int(sptr[-1]), dtype=np.int64)
         with torch.cuda.stream(self.stream):       # H2D ordered before the kernel on this stream
             t_ptr = torch.from_numpy(sptr).to(dev)
             t_idx = torch.from_numpy(self.corpus.new_id[data.indices[sel]].astype(np.int32)).to(dev)
             t_val = torch.from_numpy(np.ascontiguousarray(data.data[sel], np.float64)).to(dev)
             _lib.call("spkm_seed_rows", self.C.struct, _ptr(t_ptr), _ptr(t_idx), _ptr(t_val), self.sp)
         self.C.refresh_dense(self.sp)
-        self.stream.synchronize()
+        self._keep = (t_ptr, t_idx, t_val)
         self.seed_h2d_bytes = int(sptr.nbytes + t_idx.numel() * 4 + t_val.numel() * 8)
 
     def reset(self):
@@ -650,51 +754,77 @@ class Engine:
         self.finalize_launch(False, sims_extra)
 
     def enqueue(self, it: int):
-        """Launch iteration ``it`` (>= 2) without a host sync: a graph replay
-        once captured, else the eager kernel sequence.  A no-op on the device
-        if the run has already converged."""
-        prof = _lib.active_profiler()
-        # capture only once the engine is being reused (a capture costs about
-        # as much as ~20 eager iterations); every kernel reads its work counts
-        # from device memory, so one graph serves every later iteration
-        graphable = (self.use_graphs and (self.runs > 0 or self.graph is not None) and it >= 3
-                     and it % _SCRATCH_INTERVAL != 0 and not (prof is not None and prof.timed))
-        if not graphable:
-            self._steady(None, it)
-            return
-        if self.graph is None:
+        """Launch iteration ``it`` (>= 2) eagerly without a host sync (a no-op
+        on the device once the run has converged)."""
+        self._steady(None, it)
+
+    def _body(self):
+        """One iteration >= 3 as captured into the device loop: the 50-iteration
+        scratch rebuild (engine.py:317-320) is gated on the device."""
+        if self.variant == "standard":
+            self.lloyd_pass()
+            sims_extra = self.n_total * self.k
+        else:
+            use = int(self.needs_cc)
+            if self.needs_cc:
+                _lib.call("spkm_center_thresholds", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles), 0, self.sp)
+            self.bounds_pass(use)
+            self.scan_pass(use)
+            sims_extra = 0
+        self.apply_moves()
+        self.move_centers(False)
+        _lib.call("spkm_aggregate_sums_gated", self.corpus.struct, self.C.struct, self.P.bounds, _ptr(self.C.sums),
+                  _ptr(self.C.counts), _SCRATCH_INTERVAL, self.sp)
+        self.finalize_launch(False, sims_extra)
+
+    def loop_launch(self, max_iter: int):
+        """Iterations 3..max_iter as ONE graph launch: a conditional WHILE node
+        repeats the captured iteration until the device-side convergence flag
+        is set (captured once per engine)."""
+        import ctypes
+        with torch.cuda.stream(self.stream):
+            self.limit.fill_(max_iter)
+        if self.loop is None:
             self.stream.synchronize()
-            g = torch.cuda.CUDAGraph()
+            h = ctypes.c_void_p()
+            _lib.call("spkm_loop_begin", _ptr(self.C.ctl), _ptr(self.limit), self.sp, ctypes.byref(h))
             _lib._capture = []
             saved, _lib._profiler = _lib._profiler, None
             try:
-                with torch.cuda.graph(g, stream=self.stream):
-                    self._steady(None, it)
+                self._body()
             finally:
-                self.graph_kernels = sum(_lib._capture)
+                n = sum(_lib._capture)
                 _lib._capture = None
                 _lib._profiler = saved
-            self.graph = g
-        with torch.cuda.stream(self.stream):
-            self.graph.replay()
-        _lib.note_launches(self.graph_kernels)
+                _lib.call("spkm_loop_end", h)
+            self.loop, self.loop_kernels = h, n + 1
+        _lib.call("spkm_loop_launch", self.loop, self.sp)
 
-    def read_history(self, first: int, count: int):
-        """One D2H of stats rows [first, first+count) and the control words."""
+    def read_history(self, first: int, count: int, with_a: bool = False):
+        """One D2H of stats rows [first, first+count) and the control words
+        (and the assignments into a pinned buffer), then one host sync."""
         F = _lib.ST_COUNT
+        n = self.corpus.n
         with torch.cuda.stream(self.stream):
             self.P.hist_host[:count * F].copy_(self.P.hist[first * F:(first + count) * F], non_blocking=True)
             self.P.hist_host[-2:].copy_(self.C.ctl.to(torch.float64), non_blocking=True)
+            if with_a and n:
+                self.a_host[:n].copy_(self.P.a[:n], non_blocking=True)
         self.stream.synchronize()
         h = self.P.hist_host.numpy()
         return h[:count * F].reshape(count, F).copy(), int(h[-2]), bool(h[-1])
 
+    def iteration1_launch(self):
+        """Iteration 1 (engine.py:249-271): full pass, scratch sums, move all, stats."""
+        self.init_pass()
+        self.scratch_sums()
+        self.move_centers(True)
+        self.finalize_launch(True, self.n_total * self.k)
+
     def iteration(self, it: int, debug_hook=None, seed_indices=None) -> tuple:
         if it == 1:
-            self.init_pass()
-            self.scratch_sums()
-            self.move_centers(True)
-            return self.finalize(True, self.n_total * self.k), None
+            self.iteration1_launch()
+            return self.read_stats(), None
         if debug_hook is not None:
             self._steady(debug_hook, it, seed_indices)
         else:
@@ -721,13 +851,20 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
         eng.load_centers(init_centers)
     eng.reset()
     if eng.P.hist_cap < max_iter + 1:
+        eng.drop_loop()                     # the captured loop holds the old history pointer
         eng.P.set_history(max_iter + 1)
     cc_per_it = k * (k - 1) // 2 if variant in _CC_VARIANTS else 0
     stats: list = []
     converged = False
+    prev_t = [None]
 
-    def record(it, st, dt_ns):
+    def record(it, st, dt_ns=None):
         reassign = data.n if it == 1 else int(st[_lib.ST_REASSIGN])
+        if dt_ns is None:   # device timestamps (%globaltimer) bracket every iteration
+            t_end = st[_lib.ST_TSTAMP]
+            t_beg = st[_lib.ST_T0] if it == 1 or prev_t[0] is None else prev_t[0]
+            dt_ns = int(max(0.0, t_end - t_beg))
+            prev_t[0] = t_end
         stats.append(IterationStats(iteration=it, sim_count=int(st[_lib.ST_SIMS]), cc_sim_count=cc_per_it,
                                     reassignments=reassign, objective=float(st[_lib.ST_OBJECTIVE]),
                                     elapsed_ns=dt_ns, survivors=int(st[_lib.ST_SURV1]),
@@ -735,38 +872,61 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
                                     nnz_rescan=int(st[_lib.ST_NNZ_RESCAN]), nnz_elkan=int(st[_lib.ST_NNZ_ELKAN])))
         return k == 1 or st[_lib.ST_ALLONE] == 1.0 or (it >= 2 and reassign == 0)
 
-    t0 = time.monotonic_ns()
-    st, _ = eng.iteration(1, debug_hook, seed_indices)
-    converged = record(1, st, time.monotonic_ns() - t0)
-    it, chunk = 2, 1
-    while not converged and it <= max_iter:
-        t0 = time.monotonic_ns()
-        if debug_hook is not None:
-            st, _ = eng.iteration(it, debug_hook, seed_indices)
-            converged = record(it, st, time.monotonic_ns() - t0)
-            it += 1
-            continue
-        # enqueue a chunk of iterations without syncing: the convergence test
-        # runs on the device and turns later iterations into no-ops; chunks
-        # never cross a scratch-rebuild iteration (it % 50 == 0)
-        nxt50 = (it // _SCRATCH_INTERVAL + 1) * _SCRATCH_INTERVAL
-        c = min(chunk, max_iter - it + 1, (nxt50 - it) if it % _SCRATCH_INTERVAL else 1)
-        for j in range(it, it + c):
-            eng.enqueue(j)
-        rows, done_its, dev_conv = eng.read_history(it - 1, c)
-        dt = (time.monotonic_ns() - t0) // max(1, min(c, done_its - it + 1))
-        for q in range(c):
-            if it + q > done_its:
-                break
-            converged = record(it + q, rows[q], dt)
+    prof = _lib.active_profiler()
+    device_loop = (eng.use_graphs and eng.runs > 0 and debug_hook is None and comm is None
+                   and not (prof is not None and prof.timed))
+    a_read = False
+    if device_loop:
+        # the whole fit without a host round trip: iteration 1 and 2 eagerly
+        # enqueued (iteration 2 rebuilds the full cc table), then iterations
+        # 3..max_iter as one graph launch; one D2H of the stats history and
+        # the assignments at the end
+        eng.iteration1_launch()
+        if max_iter >= 2:
+            eng.enqueue(2)
+        if max_iter >= 3:
+            eng.loop_launch(max_iter)
+            _lib.note_launches(0)
+        rows, done_its, _ = eng.read_history(0, max(1, min(max_iter, eng.P.hist_cap)), with_a=True)
+        a_read = True
+        if max_iter >= 3:
+            _lib.note_launches(eng.loop_kernels * max(0, done_its - 2) + 1)
+        for q in range(min(done_its, max_iter)):
+            converged = record(q + 1, rows[q])
             if converged:
                 break
-        it += c
-        chunk = min(chunk * 2, 8)
+    else:
+        st, _ = eng.iteration(1, debug_hook, seed_indices)
+        converged = record(1, st)
+        it, chunk = 2, 1
+        while not converged and it <= max_iter:
+            if debug_hook is not None:
+                st, _ = eng.iteration(it, debug_hook, seed_indices)
+                converged = record(it, st)
+                it += 1
+                continue
+            # enqueue a chunk of iterations without syncing: the convergence test
+            # runs on the device and turns later iterations into no-ops; chunks
+            # never cross a scratch-rebuild iteration (it % 50 == 0)
+            nxt50 = (it // _SCRATCH_INTERVAL + 1) * _SCRATCH_INTERVAL
+            c = min(chunk, max_iter - it + 1, (nxt50 - it) if it % _SCRATCH_INTERVAL else 1)
+            for j in range(it, it + c):
+                eng.enqueue(j)
+            rows, done_its, dev_conv = eng.read_history(it - 1, c)
+            for q in range(c):
+                if it + q > done_its:
+                    break
+                converged = record(it + q, rows[q])
+                if converged:
+                    break
+            it += c
+            chunk = min(chunk * 2, 8)
     eng.stream.synchronize()
     eng.runs += 1
     torch.cuda.current_stream(eng.device).wait_stream(eng.stream)
-    a = eng.corpus.to_host_rows(eng.P.a[:eng.corpus.n].cpu().numpy().astype(np.int64))
+    n_loc = eng.corpus.n
+    a_dev = eng.a_host[:n_loc].numpy() if a_read else eng.P.a[:n_loc].cpu().numpy()
+    a = eng.corpus.to_host_rows(a_dev.astype(np.int64))
     if comm is not None:
         a = comm.gather_assignments(torch.from_numpy(a).to(eng.device), eng.corpus.rows, eng.n_total)
     return ClusteringResult(assignments=a, centers=DeviceCentroidSet(eng.C.snapshot(), seed_indices),

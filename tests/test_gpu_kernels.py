@@ -327,3 +327,22 @@ def test_cuda_graph_replay_matches_eager(variant):
     assert [s.sim_count for s in g.iterations] == [s.sim_count for s in e.iterations]
     assert [s.reassignments for s in g.iterations] == [s.reassignments for s in e.iterations]
     assert len(g.iterations) >= 3
+
+
+@pytest.mark.parametrize("variant", ["standard", "elkan", "hamerly"])
+def test_device_loop_max_iter_and_reuse(variant):
+    """The device-driven loop (conditional WHILE graph) stops exactly at
+    max_iter or at convergence, across repeated fits with different limits,
+    and equals the eager host loop."""
+    m = spk()
+    data = golden_dataset(load_golden("C1"))
+    m.run(data, 20, variant, m.SeedConfig(seed=4), max_iter=50, use_graphs=True)   # warm (eager)
+    for mi in (1, 2, 3, 4, 7, 50, 5):
+        g = m.run(data, 20, variant, m.SeedConfig(seed=4), max_iter=mi, use_graphs=True)
+        e = m.run(data, 20, variant, m.SeedConfig(seed=4), max_iter=mi, use_graphs=False)
+        assert len(g.iterations) == len(e.iterations) <= mi
+        assert g.converged == e.converged
+        assert np.array_equal(g.assignments, e.assignments)
+        assert g.objective == e.objective
+        assert [s.reassignments for s in g.iterations] == [s.reassignments for s in e.iterations]
+        assert all(s.elapsed_ns > 0 for s in g.iterations)

@@ -366,6 +366,11 @@ def roofline(args, data, corpus, dev, world):
             if v in ("elkan", "simp_elkan"):
                 bytes_by[("spkm_elkan_bounds", v)] = (8 * ku + 16) * n * (len(its) - 1)
                 bytes_by[("spkm_elkan_scan", v)] = sum(8 * s.nnz_elkan + (8 * ku + 16) * s.survivors for s in its[1:])
+            # center update (reported beside B_iter): 16 B of
+            # int64 atomics per moved nnz; 20 B per (touched cluster, term)
+            # to renormalise and take the drift
+            bytes_by[("spkm_apply_moves", v)] = sum(16 * s.nnz_moved for s in its[1:])
+            bytes_by[("spkm_move_centers", v)] = sum(20 * s.touched * data.dim for s in its)
             if dense:
                 # tensor-core pass: 3 tf32 MMAs per (row, padded center, dim)
                 kpad = (k + 255) // 256 * 256

@@ -129,7 +129,7 @@ typedef struct spkm_work {
 
 enum {
     SPKM_CTR_SURV1 = 0, SPKM_CTR_SURV2 = 1, SPKM_CTR_MOVES = 2, SPKM_CTR_SIMS = 3,
-    SPKM_CTR_NNZ_TIGHTEN = 4, SPKM_CTR_NNZ_RESCAN = 5, SPKM_CTR_NNZ_ELKAN = 6
+    SPKM_CTR_NNZ_TIGHTEN = 4, SPKM_CTR_NNZ_RESCAN = 5, SPKM_CTR_NNZ_ELKAN = 6, SPKM_CTR_NNZ_MOVED = 7
 };
 enum {
     SPKM_ST_SIMS = 0, SPKM_ST_REASSIGN = 1, SPKM_ST_OBJECTIVE = 2, SPKM_ST_ALLONE = 3,
@@ -137,6 +137,7 @@ enum {
     SPKM_ST_NNZ_RESCAN = 8, SPKM_ST_NNZ_ELKAN = 9, SPKM_ST_ITER = 10,
     SPKM_ST_TSTAMP = 11,  /* device %globaltimer (ns) at the end of the iteration */
     SPKM_ST_T0 = 12,      /* %globaltimer at spkm_reset_counters (start of the fit) */
+    SPKM_ST_NNZ_MOVED = 13, /* CSR nnz of the moved points (incremental center update) */
     SPKM_ST_COUNT = 16
 };
 
@@ -267,6 +268,24 @@ int spkm_loop_destroy(void *loop);
 int spkm_permute_rows(int64_t n, const int64_t *ip_raw, const int32_t *idx_raw, const double *val_raw,
                       const int64_t *perm, const int64_t *ip_new, const int64_t *new_id, int32_t *idx, float *val,
                       double *val64, float *reps, void *stream);
+
+/* Ingestion (host, no GPU; corpus_io.py:31-131).  spkm_svml_parse parses a
+ * whole SVMlight/libsvm text buffer with nthreads threads (<1: all cores);
+ * on a syntax error it returns 1 with err_line (1-based) and err_msg (the
+ * reference's ParseError text).  spkm_svml_fetch copies the CSR (indptr
+ * [n_rows+1], int64 indices, float64 values; explicit zeros dropped) and
+ * releases the result; spkm_svml_free releases it without copying.
+ * spkm_host_idf: idf of every term with df > 0 (ln(n/df), or the smooth
+ * variant), computed with libm log like the reference's math.log. */
+typedef struct spkm_svml {
+    int64_t n_rows, nnz, max_idx, err_line;
+    char err_msg[256];
+    void *handle;
+} spkm_svml;
+int spkm_svml_parse(const char *buf, int64_t len, int nthreads, spkm_svml *out);
+int spkm_svml_fetch(spkm_svml *res, int64_t *indptr, int64_t *indices, double *values);
+int spkm_svml_free(spkm_svml *res);
+int spkm_host_idf(int64_t d, const int64_t *df, int64_t n, int smooth, double *idf);
 
 /* Host helper (no GPU): |row| of every CSR row in the reference's np.dot
  * order (sparse.py:52), for Dataset.from_csr. */

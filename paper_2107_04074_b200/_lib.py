@@ -18,6 +18,7 @@ PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
 LIB_PATH = PKG / "libspkm.so"
 SRC = PKG / "csrc" / "spkm.cu"
+SRC_HOST = PKG / "csrc" / "ingest.cpp"
 HEADER = ROOT / "include" / "spkm.h"
 ABI_VERSION = 1
 
@@ -54,6 +55,11 @@ class Seed(ctypes.Structure):
                 ("row_host", c_vp), ("row_dev", c_vp), ("scratch", c_vp)]
 
 
+class Svml(ctypes.Structure):
+    _fields_ = [("n_rows", c_i64), ("nnz", c_i64), ("max_idx", c_i64), ("err_line", c_i64),
+                ("err_msg", ctypes.c_char * 256), ("handle", c_vp)]
+
+
 class Work(ctypes.Structure):
     _fields_ = [("surv1", c_vp), ("surv2", c_vp), ("mv_i", c_vp), ("mv_old", c_vp), ("ctr", c_vp),
                 ("stats", c_vp), ("stats_hist", c_vp), ("hist_cap", c_i64)]
@@ -62,9 +68,9 @@ class Work(ctypes.Structure):
 # modes / enums (include/spkm.h)
 MODE_INIT_PLAIN, MODE_INIT_ELKAN, MODE_INIT_HAMERLY, MODE_LLOYD = 0, 1, 2, 3
 MODE_PREDICT, DMODE_RESCAN_H = 5, 6
-CTR_SURV1, CTR_SURV2, CTR_MOVES, CTR_SIMS, CTR_NNZ_TIGHTEN, CTR_NNZ_RESCAN, CTR_NNZ_ELKAN = range(7)
+CTR_SURV1, CTR_SURV2, CTR_MOVES, CTR_SIMS, CTR_NNZ_TIGHTEN, CTR_NNZ_RESCAN, CTR_NNZ_ELKAN, CTR_NNZ_MOVED = range(8)
 (ST_SIMS, ST_REASSIGN, ST_OBJECTIVE, ST_ALLONE, ST_SURV1, ST_SURV2, ST_TOUCHED, ST_NNZ_TIGHTEN, ST_NNZ_RESCAN,
- ST_NNZ_ELKAN, ST_ITER, ST_TSTAMP, ST_T0) = range(13)
+ ST_NNZ_ELKAN, ST_ITER, ST_TSTAMP, ST_T0, ST_NNZ_MOVED) = range(14)
 ST_COUNT = 16
 
 # name -> argtypes (restype int unless listed in _RESTYPES)
@@ -104,6 +110,10 @@ _SIGS = {
     "spkm_seed_kmpp": [_P(Seed), c_i64, ctypes.c_double, ctypes.c_uint64, c_vp, c_vp, c_vp],
     "spkm_seed_afkmc2": [_P(Seed), c_i64, ctypes.c_double, c_i64, ctypes.c_uint64, c_vp, c_vp],
     "spkm_host_row_norms": [c_i64, c_vp, c_vp, c_vp],
+    "spkm_svml_parse": [c_vp, c_i64, ctypes.c_int, _P(Svml)],
+    "spkm_svml_fetch": [_P(Svml), c_vp, c_vp, c_vp],
+    "spkm_svml_free": [_P(Svml)],
+    "spkm_host_idf": [c_i64, c_vp, c_i64, ctypes.c_int, c_vp],
     "spkm_seed_rows": [_P(Centers), c_vp, c_vp, c_vp, c_vp],
     "spkm_dense_split": [c_vp, c_i64, c_vp, c_vp, c_vp],
     "spkm_dense_centers": [_P(Centers), _P(Dense), c_vp],
@@ -173,7 +183,7 @@ _capture = None     # list collecting kernel counts while a CUDA graph is captur
 def build(verbose: bool = False) -> Path:
     """Compile csrc/spkm.cu for sm_100a into the package directory."""
     nvcc = os.environ.get("NVCC", "nvcc")
-    cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(LIB_PATH), str(SRC)]
+    cmd = [nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-o", str(LIB_PATH), str(SRC), str(SRC_HOST)]
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise DeviceError(f"nvcc failed:\n{r.stderr[-4000:]}")

@@ -835,7 +835,7 @@ __global__ void __launch_bounds__(256) k_apply_moves(int64_t d, const int64_t *_
                                                      const int32_t *__restrict__ a,
                                                      const int32_t *__restrict__ mv_i,
                                                      const int32_t *__restrict__ mv_old,
-                                                     const long long *__restrict__ ctr, long long *sums,
+                                                     long long *ctr, long long *sums,
                                                      long long *counts, int32_t *touched, double scale, const long long *__restrict__ ctl) {
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
@@ -855,6 +855,7 @@ __global__ void __launch_bounds__(256) k_apply_moves(int64_t d, const int64_t *_
         if (lane == 0) {
             atomicAdd((unsigned long long *)(counts + o), (unsigned long long)(-1ll));
             atomicAdd((unsigned long long *)(counts + nw), 1ull);
+            atomicAdd((unsigned long long *)(ctr + SPKM_CTR_NNZ_MOVED), (unsigned long long)(indptr[i + 1] - indptr[i]));
             touched[o] = 1;
             touched[nw] = 1;
         }
@@ -1266,6 +1267,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
         stats[SPKM_ST_NNZ_TIGHTEN] = (double)ctr[SPKM_CTR_NNZ_TIGHTEN];
         stats[SPKM_ST_NNZ_RESCAN] = (double)ctr[SPKM_CTR_NNZ_RESCAN];
         stats[SPKM_ST_NNZ_ELKAN] = (double)ctr[SPKM_CTR_NNZ_ELKAN];
+        stats[SPKM_ST_NNZ_MOVED] = (double)ctr[SPKM_CTR_NNZ_MOVED];
         // iteration bookkeeping and the convergence test (engine.py:335-337),
         // evaluated on the device so the host can enqueue iterations ahead
         const long long it = ctl[0];
@@ -1583,7 +1585,8 @@ __global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s, con
 //     8-dim group (lo.hi, hi.lo, hi.hi); thread = row in the epilogue, which
 //     keeps a running top-2 (tie rule) and the incumbent's value;
 //   * error: (3D/8 + 8) 2^-22 (fp32 TMEM accumulation, truncation assumed)
-//     + 3e-7 (fp32 rows/centers, split residuals) -> row eps (host).
+//     + 1e-6 (float32 rounding of rows and centers 2 x 2^-24, split
+//     residuals 3 x 2^-22, times sum|x c| <= 1) -> row eps (host).
 constexpr int DN_M = 128;                         // rows per tile (TMEM lanes)
 constexpr int DN_N = 256;                         // centers per pass (TMEM columns per accumulator)
 constexpr int DN_KC = 16;                         // dims per pipeline stage

@@ -139,6 +139,8 @@ class IterationStats:
     nnz_tighten: int = 0        # CSR nnz re-read by the Hamerly tighten pass
     nnz_rescan: int = 0         # CSR nnz re-read by the Hamerly full-k rescan
     nnz_elkan: int = 0          # CSR nnz re-read by the Elkan survivor scan
+    touched: int = 0            # clusters renormalised (moved in or out)
+    nnz_moved: int = 0          # CSR nnz of the points that changed cluster
 
 
 @dataclass
@@ -183,7 +185,7 @@ def row_eps(lengths: np.ndarray) -> np.ndarray:
 
 
 def row_eps_dense(D: int, n: int) -> np.ndarray:
-    e = (3.0 * D / 8.0 + 8.0) * 2.0 ** -22 + 3e-7
+    e = (3.0 * D / 8.0 + 8.0) * 2.0 ** -22 + 1e-6
     f = np.float32(e)
     if float(f) < e:
         f = np.nextafter(f, np.float32(np.inf))
@@ -328,7 +330,7 @@ class DeviceCorpus:
                   None if dense else _ptr(self.reps), sp)
         if dense:
             # tensor-core path: every similarity is the 3xTF32 tcgen05 value
-            # with error <= (3D/8 + 8) 2^-22 + 3e-7 (spkm.cu, dense rows)
+            # with error <= (3D/8 + 8) 2^-22 + 1e-6 (spkm.cu, dense rows)
             self.reps.fill_(float(row_eps_dense(self.dense_dim, 1)[0]))
             _lib.call("spkm_dense_split", _ptr(self.values), self.nnz, _ptr(self.xhi), _ptr(self.xlo), sp)
         self.perm_dev = perm
@@ -869,7 +871,8 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
                                     reassignments=reassign, objective=float(st[_lib.ST_OBJECTIVE]),
                                     elapsed_ns=dt_ns, survivors=int(st[_lib.ST_SURV1]),
                                     survivors2=int(st[_lib.ST_SURV2]), nnz_tighten=int(st[_lib.ST_NNZ_TIGHTEN]),
-                                    nnz_rescan=int(st[_lib.ST_NNZ_RESCAN]), nnz_elkan=int(st[_lib.ST_NNZ_ELKAN])))
+                                    nnz_rescan=int(st[_lib.ST_NNZ_RESCAN]), nnz_elkan=int(st[_lib.ST_NNZ_ELKAN]),
+                                    touched=int(st[_lib.ST_TOUCHED]), nnz_moved=int(st[_lib.ST_NNZ_MOVED])))
         return k == 1 or st[_lib.ST_ALLONE] == 1.0 or (it >= 2 and reassign == 0)
 
     prof = _lib.active_profiler()

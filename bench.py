@@ -39,7 +39,9 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 VARIANTS = ("standard", "elkan", "simp_elkan", "hamerly", "simp_hamerly")
-METRIC = "k-means iterations/s (C2, k=100, 5 variants per step)"
+def metric_name(args) -> str:
+    """BASELINE.json's iterations/s metric, labelled with the workload (C2, k=100, 5 variants by default)."""
+    return f"k-means iterations/s ({args.config}, k={args.k}, {len(args.variants.split(','))} variants per step)"
 PEAKS = ROOT / "MEASURED_PEAKS.json"
 
 
@@ -161,7 +163,7 @@ def run_reference(args):
     its = sum(step() for _ in range(args.steps))
     dt = time.perf_counter() - t0
     val = its / dt
-    line = {"metric": METRIC, "value": val, "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
+    line = {"metric": metric_name(args), "value": val, "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(args, data, args.gpus), "impl": "reference",
@@ -171,17 +173,27 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(args, data):
-    """Bounded sample: one full fit of each variant with the oracle (10-30 s of CPU at C2 k=100)."""
+def cpu_baseline(args, data, budget_s: float = 20.0):
+    """Bounded sample (about 10-30 s of CPU): one fit of each variant with the
+    oracle, capped at the number of iterations a 2-iteration probe says fits
+    the budget (full fits at C2 k=100)."""
     from oracle import oracle as O
     X = O.CSR(data.indptr, data.indices, data.data, data.dim)
+    variants = args.variants.split(",")
+    t0 = time.perf_counter()
+    probe = O.run(X, args.k, variants[0], seed=args.seed, max_iter=2)["iterations"]
+    per_it = (time.perf_counter() - t0) / max(probe, 1)
+    mi = args.max_iter
+    if per_it * args.max_iter * len(variants) > budget_s:
+        mi = max(2, min(args.max_iter, int(budget_s / (per_it * len(variants)))))
     its = 0
     t0 = time.perf_counter()
-    for v in args.variants.split(","):
-        its += O.run(X, args.k, v, seed=args.seed, max_iter=args.max_iter)["iterations"]
+    for v in variants:
+        its += O.run(X, args.k, v, seed=args.seed, max_iter=mi)["iterations"]
     dt = time.perf_counter() - t0
+    cap = "" if mi == args.max_iter else f", each capped at {mi} iterations"
     return {"value": its / dt, "unit": "iterations/s", "cores": O.num_threads(), "kind": "port",
-            "sample": f"one fit of each variant ({its} iterations, {dt:.1f} s), C oracle, OpenMP threads"}
+            "sample": f"one fit of each variant{cap} ({its} iterations, {dt:.1f} s), C oracle, OpenMP threads"}
 
 
 # ----------------------------------------------------------------- our arm
@@ -311,7 +323,7 @@ def main_ours(args):
         dist.destroy_process_group()
         return
     clocks = clk.summary()
-    line = {"metric": METRIC, "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
+    line = {"metric": metric_name(args), "value": value, "unit": "iterations/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": workload_config(args, data, world),

@@ -219,18 +219,23 @@ def main_ours(args):
     from paper_2107_04074_b200.seeding import uniform_rows
     seed_rows = uniform_rows(data.n, k, args.seed)
     if world > 1:
-        from paper_2107_04074_b200.distributed import Exchange, shard_rows
-        rows = shard_rows(data.indptr, world)[rank]
-    else:
-        rows = (0, data.n)
+        from paper_2107_04074_b200.distributed import Exchange
+    rows = (0, data.n)                 # multi-GPU: corpus replicated, scans sharded (distributed.py)
     corpus = DeviceCorpus(data, dev, rows=rows)
     torch.cuda.synchronize()
+
+    exchanges = {}     # one Exchange per corpus (multi-GPU): engines are cached per (corpus, exchange)
+
+    def exchange_for(corpus_):
+        if id(corpus_) not in exchanges:
+            exchanges[id(corpus_)] = Exchange.for_corpus(k, corpus_, dev)
+        return exchanges[id(corpus_)]
 
     def fit_all(corpus_, tag=None):
         its, sims, nk = 0, 0, 0
         per = {}
         for v in variants:
-            comm = Exchange(k, data.dim, dev) if world > 1 else None
+            comm = exchange_for(corpus_) if world > 1 else None
             r = run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=corpus_,
                     comm=comm, n_total=data.n)
             its += len(r.iterations)
@@ -292,7 +297,7 @@ def main_ours(args):
         c.refresh(data)
         b_in, b_out = c.h2d_bytes, 0
         for v in variants:
-            comm = Exchange(k, data.dim, dev) if world > 1 else None
+            comm = exchange_for(c) if world > 1 else None
             r = spk.run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=c,
                         comm=comm, n_total=data.n)
             b_in += int(k * 8)
@@ -359,7 +364,7 @@ def roofline(args, data, corpus, dev, world):
     with prof:
         for v in args.variants.split(","):
             prof.tag = v
-            comm = Exchange(k, data.dim, dev) if world > 1 else None
+            comm = Exchange.for_corpus(k, corpus, dev) if world > 1 else None
             r = run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=corpus,
                     comm=comm, n_total=data.n)
             its = r.iterations

@@ -251,6 +251,33 @@ int spkm_seed_afkmc2(const spkm_seed *S, int64_t k, double alpha, int64_t chain_
  * gathered from the spkm_seed corpus (init_uniform + from_data_rows). */
 int spkm_seed_rows_csr(const spkm_centers *C, const spkm_seed *S, const int64_t *rows, void *stream);
 
+/* Bound auditor (validation.py:49-80) and brute-force assignment
+ * (validation.py:18-29) on the device.  spkm_audit_transpose writes the
+ * term-major float64 copy ct64 [d][kp] of center-major float64 centers;
+ * spkm_audit computes every exact float64 similarity of the spkm_seed
+ * corpus (device-order rows) and folds, with atomicMax on order-preserving
+ * keys (keys[0] lower, keys[1] upper): mode 0 max(l - S[i,a]) and
+ * max(S - u) over the Elkan matrix (row stride ku), 1 the Hamerly
+ * max_{j != a} S[i,j] - u[i], 2 the lower bound only, 3 argmax per row into
+ * a_out (lowest index on ties). */
+int spkm_audit_transpose(int64_t k, int64_t d, int64_t kp, const double *cent64, double *ct64, void *stream);
+int spkm_audit(const spkm_seed *S, int64_t k, int64_t kp, const double *ct64, const int32_t *a, const float *l,
+               const float *u, int64_t ku, int mode, unsigned long long *keys, int32_t *a_out, void *stream);
+
+/* Multi-GPU exchange (distributed.py): the corpus is replicated and the
+ * scans are sharded by device-row ranges; per iteration each rank packs its
+ * moves and counters into a fixed-size int32 slot of
+ * spkm_move_slot_ints(cap) ints (cap = its shard's rows; rows are stored
+ * global, p0 = the shard's first device row), the slots are allgathered
+ * (NCCL), and every rank applies all ranks' moves to its replicated
+ * fixed-point sums (spkm_apply_move_slots, X = the whole corpus) and takes
+ * the summed counters into ctr_out. */
+int64_t spkm_move_slot_ints(int64_t cap);
+int spkm_pack_moves(const spkm_work *W, const spkm_bounds *B, const spkm_centers *C, int64_t p0, int64_t cap,
+                    int32_t *slot, void *stream);
+int spkm_apply_move_slots(const spkm_csr *X, const spkm_centers *C, const int32_t *slots, int world, int64_t slot_len,
+                          int32_t *touched, long long *ctr_out, void *stream);
+
 /* Device-driven fit loop (engine.py:239-337 without a host round trip per
  * iteration): a CUDA graph whose conditional WHILE node repeats one
  * iteration while ctl says "not converged" and ctl[0] < *limit.  begin()

@@ -103,6 +103,11 @@ _SIGS = {
     "spkm_seed_rows_csr": [_P(Centers), _P(Seed), c_vp, c_vp],
     "spkm_aggregate_sums_gated": [_P(CSR), _P(Centers), _P(Bounds), c_vp, c_vp, ctypes.c_int, c_vp],
     "spkm_loop_begin": [c_vp, c_vp, c_vp, _P(c_vp)],
+    "spkm_move_slot_ints": [c_i64],
+    "spkm_pack_moves": [_P(Work), _P(Bounds), _P(Centers), c_i64, c_i64, c_vp, c_vp],
+    "spkm_apply_move_slots": [_P(CSR), _P(Centers), c_vp, ctypes.c_int, c_i64, c_vp, c_vp, c_vp],
+    "spkm_audit_transpose": [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp],
+    "spkm_audit": [_P(Seed), c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.c_int, c_vp, c_vp, c_vp],
     "spkm_permute_rows": [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "spkm_loop_end": [c_vp],
     "spkm_loop_launch": [c_vp, c_vp],
@@ -128,6 +133,7 @@ _RESTYPES = {
     "spkm_gram_scratch_doubles": c_i64,
     "spkm_center_scratch_doubles": c_i64,
     "spkm_seed_scratch_doubles": c_i64,
+    "spkm_move_slot_ints": c_i64,
 }
 
 # kernels each entry point launches (for the bench's gpu_launches count)
@@ -137,7 +143,8 @@ KERNELS_PER_CALL = {
     "spkm_move_centers": 5, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_split": 1, "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
-    "spkm_seed_rows_csr": 1, "spkm_aggregate_sums_gated": 2, "spkm_permute_rows": 1,
+    "spkm_seed_rows_csr": 1, "spkm_aggregate_sums_gated": 2, "spkm_permute_rows": 1, "spkm_audit": 1, "spkm_audit_transpose": 1,
+    "spkm_pack_moves": 1, "spkm_apply_move_slots": 1,
 }
 
 _lib = None

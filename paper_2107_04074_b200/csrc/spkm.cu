@@ -2043,6 +2043,171 @@ RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     return A;
 }
 
+
+// ------------------------------------------------------------ bound auditor
+// validation.py:49-80 on the device: exact float64 similarities of every row
+// to every center (FMA chain over the row's nnz, |error| ~ 1e-16 << the
+// auditor's 1e-9 tolerance) from a term-major float64 copy of the centers,
+// checked against the stored bounds.  mode 0: Elkan u(i,j) matrix, 1:
+// Hamerly single u (max over j != a(i)), 2: lower bound only, 3: argmax
+// (brute_force_assign, lowest index on ties) into a_out.  Maxima are
+// accumulated as order-preserving 64-bit keys with atomicMax.
+__device__ __forceinline__ unsigned long long dkey(double v) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(v);
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+constexpr int kAuditCols = 4;   // columns per lane per block (128 per warp)
+
+__global__ void __launch_bounds__(256) k_audit(int64_t n, int64_t k, int64_t kp, const int64_t *__restrict__ indptr,
+                                               const int32_t *__restrict__ indices, const double *__restrict__ v64,
+                                               const double *__restrict__ ct64, const int32_t *__restrict__ a,
+                                               const float *__restrict__ l, const float *__restrict__ u, int64_t ku,
+                                               int mode, unsigned long long *keys, int32_t *a_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t i = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); i < n; i += warps) {
+        const int64_t s = indptr[i], e = indptr[i + 1];
+        const int ai = (mode == 3) ? -1 : a[i];
+        double own = -INFINITY, up = -INFINITY, best = -INFINITY;
+        int bj = 0x7fffffff;
+        for (int64_t j0 = 0; j0 < k; j0 += 32 * kAuditCols) {
+            double acc[kAuditCols];
+#pragma unroll
+            for (int c = 0; c < kAuditCols; ++c) acc[c] = 0.0;
+            for (int64_t t = s; t < e; ++t) {
+                const double x = v64[t];
+                const double *row = ct64 + (int64_t)indices[t] * kp;
+#pragma unroll
+                for (int c = 0; c < kAuditCols; ++c) {
+                    const int64_t j = j0 + c * 32 + lane;
+                    if (j < k) acc[c] = fma(x, row[j], acc[c]);
+                }
+            }
+#pragma unroll
+            for (int c = 0; c < kAuditCols; ++c) {
+                const int64_t j = j0 + c * 32 + lane;
+                if (j >= k) continue;
+                const double S = acc[c];
+                if (j == ai) own = S;
+                if (mode == 0) up = fmax(up, S - (double)u[i * ku + j]);
+                if (mode == 1 && j != ai) up = fmax(up, S);
+                if (mode == 3 && (S > best || (S == best && j < bj))) {
+                    best = S;
+                    bj = (int)j;
+                }
+            }
+        }
+        for (int o = 16; o; o >>= 1) {
+            own = fmax(own, __shfl_xor_sync(FULL, own, o));
+            up = fmax(up, __shfl_xor_sync(FULL, up, o));
+            const double ob = __shfl_xor_sync(FULL, best, o);
+            const int oj = __shfl_xor_sync(FULL, bj, o);
+            if (ob > best || (ob == best && oj < bj)) {
+                best = ob;
+                bj = oj;
+            }
+        }
+        if (lane == 0) {
+            if (mode == 3) {
+                a_out[i] = bj;
+            } else {
+                atomicMax(keys, dkey((double)l[i] - own));
+                if (mode == 0) atomicMax(keys + 1, dkey(up));
+                if (mode == 1 && k > 1) atomicMax(keys + 1, dkey(up - (double)u[i]));
+            }
+        }
+    }
+}
+
+// center-major float64 [k][d] -> term-major [d][kp] (zero padding columns)
+__global__ void k_transpose_centers(int64_t k, int64_t d, int64_t kp, const double *__restrict__ c64, double *ct64) {
+    __shared__ double tile[32][33];
+    const int64_t t0 = (int64_t)blockIdx.x * 32, j0 = (int64_t)blockIdx.y * 32;
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t j = j0 + r, t = t0 + threadIdx.x;
+        tile[r][threadIdx.x] = (j < k && t < d) ? c64[j * d + t] : 0.0;
+    }
+    __syncthreads();
+    for (int r = threadIdx.y; r < 32; r += blockDim.y) {
+        const int64_t t = t0 + r, j = j0 + threadIdx.x;
+        if (t < d && j < kp) ct64[t * kp + j] = tile[threadIdx.x][r];
+    }
+}
+
+
+// ------------------------------------------------------ multi-GPU exchange
+// Corpus replicated on every rank, scans sharded by device-row ranges; the
+// only per-iteration collective is an allgather of fixed-size move slots:
+//   slot (int32) = [count, 0, ctr as 8 x int64, (row, old, new) x cap]
+// Every rank then applies ALL moves to its replicated fixed-point sums, so
+// the sums (integers, order-free atomics) are identical on every rank.
+constexpr int kSlotHead = 2 + 16;
+
+__global__ void k_pack_moves(const int32_t *__restrict__ mv_i, const int32_t *__restrict__ mv_old,
+                             const int32_t *__restrict__ a, const long long *__restrict__ ctr, int64_t p0,
+                             int64_t cap, int32_t *slot, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;
+    const long long cnt = ctr[SPKM_CTR_MOVES];
+    const long long c = cnt < cap ? cnt : cap;   // cap = shard rows >= moves
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        slot[0] = (int32_t)c;
+        slot[1] = 0;
+        long long *h = reinterpret_cast<long long *>(slot + 2);
+        for (int q = 0; q < 8; ++q) h[q] = ctr[q];
+    }
+    for (int64_t m = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; m < c; m += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t i = mv_i[m];
+        int32_t *t = slot + kSlotHead + 3 * m;
+        t[0] = (int32_t)(p0 + i);
+        t[1] = mv_old[m];
+        t[2] = a[i];
+    }
+}
+
+// all ranks' moves -> sums/counts/touched (warp per move); block 0 also
+// writes the summed counters of all ranks into ctr_out
+__global__ void __launch_bounds__(256) k_apply_move_slots(const int32_t *__restrict__ slots, int world,
+                                                          int64_t slot_len, int64_t d,
+                                                          const int64_t *__restrict__ indptr,
+                                                          const int32_t *__restrict__ indices,
+                                                          const float *__restrict__ values, long long *sums,
+                                                          long long *counts, int32_t *touched, double scale,
+                                                          long long *ctr_out, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    int64_t wid = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    for (int q = 0; q < world; ++q) {
+        const int32_t *sl = slots + (int64_t)q * slot_len;
+        const int64_t cnt = sl[0];
+        for (int64_t m = wid; m < cnt; m += warps) {
+            const int32_t *t = sl + kSlotHead + 3 * m;
+            const int64_t i = t[0];
+            const int o = t[1], nw = t[2];
+            long long *so = sums + (int64_t)o * d;
+            long long *sn = sums + (int64_t)nw * d;
+            for (int64_t e = indptr[i] + lane; e < indptr[i + 1]; e += 32) {
+                const int c = __ldg(indices + e);
+                const long long v = to_fixed(__ldg(values + e), scale);
+                atomicAdd((unsigned long long *)(so + c), (unsigned long long)(-v));
+                atomicAdd((unsigned long long *)(sn + c), (unsigned long long)v);
+            }
+            if (lane == 0) {
+                atomicAdd((unsigned long long *)(counts + o), (unsigned long long)(-1ll));
+                atomicAdd((unsigned long long *)(counts + nw), 1ull);
+                touched[o] = 1;
+                touched[nw] = 1;
+            }
+        }
+        wid = (wid + warps - (cnt % warps)) % warps;   // rotate so ranks' tails spread over warps
+    }
+    if (blockIdx.x == 0 && threadIdx.x < 8) {
+        long long tot = 0;
+        for (int q = 0; q < world; ++q) tot += reinterpret_cast<const long long *>(slots + (int64_t)q * slot_len + 2)[threadIdx.x];
+        ctr_out[threadIdx.x] = tot;
+    }
+}
+
 #include "seed.cuh"
 
 }  // namespace
@@ -2510,6 +2675,45 @@ int spkm_permute_rows(int64_t n, const int64_t *ip_raw, const int32_t *idx_raw, 
     k_permute_rows<<<grid_for(n, 8), 256, 0, S(stream)>>>(n, ip_raw, idx_raw, val_raw, perm, ip_new, new_id, idx, val,
                                                          val64, reps);
     CHECK_LAUNCH("permute_rows");
+    return 0;
+}
+
+
+// ------------------------------------------------------------ bound auditor
+int spkm_audit_transpose(int64_t k, int64_t d, int64_t kp, const double *cent64, double *ct64, void *stream) {
+    dim3 grid((unsigned)((d + 31) / 32), (unsigned)((kp + 31) / 32));
+    k_transpose_centers<<<grid, dim3(32, 8), 0, S(stream)>>>(k, d, kp, cent64, ct64);
+    CHECK_LAUNCH("audit_transpose");
+    return 0;
+}
+
+int spkm_audit(const spkm_seed *Sd, int64_t k, int64_t kp, const double *ct64, const int32_t *a, const float *l,
+               const float *u, int64_t ku, int mode, unsigned long long *keys, int32_t *a_out, void *stream) {
+    if (Sd->n == 0) return 0;
+    k_audit<<<grid_for(Sd->n, 8), 256, 0, S(stream)>>>(Sd->n, k, kp, Sd->indptr, Sd->indices, Sd->values, ct64, a, l,
+                                                       u, ku, mode, keys, a_out);
+    CHECK_LAUNCH("audit");
+    return 0;
+}
+
+
+// ------------------------------------------------------ multi-GPU exchange
+int64_t spkm_move_slot_ints(int64_t cap) { return kSlotHead + 3 * cap; }
+
+int spkm_pack_moves(const spkm_work *W, const spkm_bounds *B, const spkm_centers *C, int64_t p0, int64_t cap,
+                    int32_t *slot, void *stream) {
+    k_pack_moves<<<grid_for(cap > 0 ? cap : 1, 256), 256, 0, S(stream)>>>(W->mv_i, W->mv_old, B->a, W->ctr, p0, cap,
+                                                                        slot, C->ctl);
+    CHECK_LAUNCH("pack_moves");
+    return 0;
+}
+
+int spkm_apply_move_slots(const spkm_csr *X, const spkm_centers *C, const int32_t *slots, int world, int64_t slot_len,
+                          int32_t *touched, long long *ctr_out, void *stream) {
+    k_apply_move_slots<<<grid_for(X->n > 0 ? X->n : 1, 8), 256, 0, S(stream)>>>(
+        slots, world, slot_len, C->d, X->indptr, X->indices, X->values, C->sums, C->counts, touched,
+        ldexp(1.0, C->scale_bits), ctr_out, C->ctl);
+    CHECK_LAUNCH("apply_move_slots");
     return 0;
 }
 

@@ -1,17 +1,28 @@
-"""Multi-GPU data parallelism: row shards, replicated centers, one allreduce per iteration.
+"""Multi-GPU data parallelism: replicated corpus, sharded scans, one allgather of moves per iteration.
 
-The reference is single-process.  Here each rank (one
-process per GPU, ``torch.distributed`` over NCCL) owns a contiguous row range
-of the corpus balanced by nnz, its bounds and worklists; centers, sums and
-counts are replicated.  Per iteration the only exchange is ONE allreduce(sum)
-of an int64 buffer
+The reference is single-process.  Here every rank (one
+process per GPU, ``torch.distributed`` over NCCL) holds the WHOLE corpus in
+its HBM (C4: 2.9 GB of CSR incl. the float64 copy, out of 180 GB) together
+with replicated centers, sums and counts, and owns a contiguous range of
+device rows (rows are stored longest first; ranges are balanced by nnz) for
+everything that scales with n x k: the full passes, the bound updates and
+the pruned scans, with their bounds and worklists.
 
-    [ delta sums (k*d) | delta counts (k) | touched flags (k) | counters (8) ]
+Per iteration the only exchange is ONE allgather of fixed-size int32 move
+slots (``spkm_pack_moves``):
 
-Sums are exact fixed point (int64), so the allreduce is exact and the
-clustering is bit-identical for every GPU count.  Iteration 1 reduces the
-from-scratch sums the same way.  Convergence is decided from the reduced
-counters, so every rank leaves the loop in the same iteration.
+    slot = [ move count | 8 int64 counters | (global row, old, new) x cap ]
+
+after which every rank applies all ranks' moves to its replicated int64
+fixed-point sums (``spkm_apply_move_slots``).  Integer atomics are
+order-free, so the sums, the centers and every later decision are
+bit-identical on every rank and for every GPU count, and the payload is
+12 bytes per moved point instead of the k x d sums (8 GB at C4) a sum
+allreduce would move.  Iteration 1 (and the 50-iteration scratch rebuild)
+allgathers the shard's assignments instead and aggregates the whole corpus
+locally.  Convergence comes from the summed counters, so all ranks leave the
+loop in the same iteration.  Collectives are issued on the engine's stream
+with no host synchronisation.
 """
 
 from __future__ import annotations
@@ -37,76 +48,58 @@ def shard_rows(indptr: np.ndarray, world: int) -> list:
 
 
 class Exchange:
-    """The per-iteration collective of one rank (plumbing over torch.distributed)."""
+    """One rank's view of the sharded fit: its device-row range and the
+    per-iteration move allgather (plumbing over torch.distributed)."""
 
-    def __init__(self, k: int, d: int, device, group=None):
+    def __init__(self, k: int, d: int, device, shards: list, group=None, slot_ints=None):
         self.k, self.d = k, d
         self.group = group
         self.rank = dist.get_rank(group)
         self.world = dist.get_world_size(group)
-        kd = k * d
-        self.buf = torch.zeros(kd + 2 * k + 8, dtype=torch.int64, device=device)
-        self.delta = self.buf[:kd]
-        self.dcounts = self.buf[kd:kd + k]
-        self.touched = self.buf[kd + k:kd + 2 * k]
-        self.ctr = self.buf[kd + 2 * k:]
-        self.bytes_per_iteration = self.buf.numel() * 8
+        self.shards = [tuple(map(int, s)) for s in shards]
+        if len(self.shards) != self.world:
+            raise ValueError("one shard per rank")
+        self.p0, self.p1 = self.shards[self.rank]
+        self.cap = max(max(p1 - p0 for p0, p1 in self.shards), 1)
+        if slot_ints is None:
+            from . import _lib
+            slot_ints = int(_lib.lib().spkm_move_slot_ints(self.cap))
+        self.slot_len = int(slot_ints)
+        self.slot = torch.zeros(self.slot_len, dtype=torch.int32, device=device)
+        self.slots = torch.zeros(self.world * self.slot_len, dtype=torch.int32, device=device)
+        self.a_slot = torch.zeros(self.cap, dtype=torch.int32, device=device)
+        self.a_all = torch.zeros(self.world * self.cap, dtype=torch.int32, device=device)
+        self.bytes_per_iteration = self.slots.numel() * 4
 
-    def _allreduce(self, t: torch.Tensor):
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+    @classmethod
+    def for_corpus(cls, k: int, corpus, device, group=None):
+        """Shards = device-row ranges of the (replicated) corpus balanced by nnz."""
+        world = dist.get_world_size(group)
+        cache = corpus.__dict__.setdefault("_shards", {})
+        if world not in cache:
+            cache[world] = shard_rows(corpus.indptr.cpu().numpy(), world)
+        return cls(k, corpus.d, device, cache[world], group)
 
-    def scratch(self, sums: torch.Tensor, counts: torch.Tensor):
-        """Iteration 1 / scratch rebuild: local sums+counts -> global (one allreduce)."""
-        kd = self.k * self.d
-        self.delta.copy_(sums)
-        self.dcounts.copy_(counts)
-        self._allreduce(self.buf[:kd + self.k])
-        sums.copy_(self.delta)
-        counts.copy_(self.dcounts)
+    def allgather_moves(self):
+        """slot (packed by spkm_pack_moves) -> every rank's slot in ``slots``."""
+        dist.all_gather_into_tensor(self.slots, self.slot, group=self.group)
 
-    def begin(self):
-        """Zero the delta section before the local move kernel writes into it."""
-        self.buf[:self.k * self.d + self.k].zero_()
-
-    def exchange(self, sums: torch.Tensor, counts: torch.Tensor, touched: torch.Tensor, ctr: torch.Tensor):
-        """Allreduce [delta | dcounts | touched | ctr] and apply it (it >= 2)."""
-        self.touched.copy_(touched)
-        self.ctr.copy_(ctr)
-        self._allreduce(self.buf)
-        sums.add_(self.delta)
-        counts.add_(self.dcounts)
-        touched.copy_((self.touched > 0).to(touched.dtype))
-        ctr.copy_(self.ctr)
-
-    def gather_assignments(self, a_local: torch.Tensor, rows: tuple, n_total: int) -> np.ndarray:
-        n_local = rows[1] - rows[0]
-        sizes = torch.tensor([n_local], dtype=torch.int64, device=a_local.device)
-        all_sizes = [torch.zeros_like(sizes) for _ in range(self.world)]
-        dist.all_gather(all_sizes, sizes, group=self.group)
-        m = int(max(int(s.item()) for s in all_sizes))
-        pad = torch.full((max(m, 1),), -1, dtype=torch.int64, device=a_local.device)
-        pad[:n_local] = a_local[:n_local].to(torch.int64)
-        outs = [torch.zeros_like(pad) for _ in range(self.world)]
-        dist.all_gather(outs, pad, group=self.group)
-        parts = [o[:int(s.item())].cpu().numpy() for o, s in zip(outs, all_sizes)]
-        a = np.concatenate(parts) if parts else np.zeros(0, np.int64)
-        assert a.size == n_total
-        return a
+    def allgather_assignments(self, a_local: torch.Tensor, a_global: torch.Tensor):
+        """Shard assignments (device order) -> the global device-order array."""
+        n_loc = self.p1 - self.p0
+        self.a_slot[:n_loc].copy_(a_local[:n_loc])
+        dist.all_gather_into_tensor(self.a_all, self.a_slot, group=self.group)
+        for q, (p0, p1) in enumerate(self.shards):
+            a_global[p0:p1].copy_(self.a_all[q * self.cap:q * self.cap + (p1 - p0)])
 
 
 def run_sharded(data, k: int, variant: str, seeding=None, max_iter: int = 100, hamerly_update: str = "safe",
                 device=None, group=None):
-    """``engine.run`` on this rank's nnz-balanced shard (call on every rank)."""
-    from .engine import DeviceCorpus, run
-    from .seeding import SeedConfig, make_centroids
-
-    world = dist.get_world_size(group)
-    rank = dist.get_rank(group)
-    r0, r1 = shard_rows(data.indptr, world)[rank]
+    """``engine.run`` on every rank of a torch.distributed group (one process
+    per GPU): same arguments and result as ``run``, identical on all ranks."""
+    from .engine import device_corpus, run
     device = torch.device(device or f"cuda:{torch.cuda.current_device()}")
-    corpus = DeviceCorpus(data, device, rows=(r0, r1))
-    cents0 = make_centroids(data, k, seeding if seeding is not None else SeedConfig())
-    ex = Exchange(k, data.dim, device, group)
-    return run(data, k, variant, max_iter=max_iter, hamerly_update=hamerly_update, device=device,
-               corpus=corpus, init_centers=cents0.centers, comm=ex, n_total=data.n,
-               seed_indices=cents0.seed_indices)
+    corpus = device_corpus(data, device)
+    ex = Exchange.for_corpus(k, corpus, device, group)
+    return run(data, k, variant, seeding=seeding, max_iter=max_iter, hamerly_update=hamerly_update, device=device,
+               corpus=corpus, comm=ex, n_total=data.n)

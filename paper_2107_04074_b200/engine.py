@@ -451,13 +451,16 @@ class CenterState:
         _lib.call("spkm_load_centers", self.struct, _ptr(src), stream)
         return src  # keep alive until the stream passes
 
-    def attach_dense(self, corpus: "DeviceCorpus"):
-        """tf32 hi/lo center rows (padded to 256) for the dense tensor-core pass."""
+    def attach_dense(self, corpus: "DeviceCorpus", row0: int = 0):
+        """tf32 hi/lo center rows (padded to 256) for the dense tensor-core pass
+        (rows from device row ``row0`` on: a multi-GPU shard)."""
         D = corpus.dense_dim
         kpad = (self.k + 255) // 256 * 256
         self.bhi = torch.zeros(kpad * D, dtype=torch.float32, device=self.cent64.device)
         self.blo = torch.zeros_like(self.bhi)
-        self.dense = _lib.Dense(D, kpad, _ptr(corpus.xhi), _ptr(corpus.xlo), _ptr(self.bhi), _ptr(self.blo))
+        off = 4 * D * row0
+        self.dense = _lib.Dense(D, kpad, _ptr(corpus.xhi) + off, _ptr(corpus.xlo) + off, _ptr(self.bhi),
+                                _ptr(self.blo))
 
     def refresh_dense(self, stream):
         if self.dense is not None:
@@ -542,8 +545,9 @@ class Engine:
     """One clustering run's device state and the per-phase kernel calls.
 
     ``comm`` (optional) is a ``distributed.Exchange`` for multi-GPU runs:
-    the corpus is then the local row shard and the center sums/counts are
-    combined with one allreduce per iteration.
+    the corpus is replicated, this rank's scans run on its device-row range
+    [p0, p1) (``self.xs``, a view of the corpus CSR), and the moves of all
+    ranks are exchanged with one allgather per iteration.
     """
 
     def __init__(self, data: Dataset, k: int, variant: str, device=None, hamerly_update: str = "safe",
@@ -560,12 +564,20 @@ class Engine:
         self.needs_cc = variant in _CC_VARIANTS
         self.C = CenterState(k, data.dim, self.n_total, self.device, self.needs_cc, order=self.corpus.order)
         self.dense = self.corpus.dense_dim is not None
+        # rows this rank scans: all of them, or its shard [p0, p1) of the replicated corpus
+        self.p0, self.p1 = (comm.p0, comm.p1) if comm is not None else (0, self.corpus.n)
+        self.n_loc = self.p1 - self.p0
+        cs = self.corpus
+        self.xs = cs.struct if comm is None else CSR(
+            self.n_loc, cs.d, cs.nnz, _ptr(cs.indptr) + 8 * self.p0, _ptr(cs.indices), _ptr(cs.values),
+            _ptr(cs.reps) + 4 * self.p0)
         if self.dense:
             if self.elkan:
                 raise ConfigError("the Elkan family is not available for dense corpora in this build "
                                   "(standard, hamerly and simp_hamerly are)")
-            self.C.attach_dense(self.corpus)
-        self.P = PointState(self.corpus.n, k, variant, self.device)
+            self.C.attach_dense(self.corpus, row0=self.p0)
+        self.P = PointState(self.n_loc, k, variant, self.device)
+        self.a_global = torch.zeros(max(cs.n, 1), dtype=torch.int32, device=self.device) if comm is not None else None
         # a dedicated stream: steady-state iterations are replayed as one CUDA graph
         self.stream = torch.cuda.Stream(device=self.device)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
@@ -643,7 +655,7 @@ class Engine:
         self.C.cc_valid = True
 
     def _dense(self, mode: int, use_s: int = 0):
-        _lib.call("spkm_dense_assign", self.corpus.struct, self.C.struct, self.C.dense, self.P.bounds, self.P.work,
+        _lib.call("spkm_dense_assign", self.xs, self.C.struct, self.C.dense, self.P.bounds, self.P.work,
                   mode, use_s, None, None, self.sp)
 
     def init_pass(self):
@@ -651,52 +663,56 @@ class Engine:
                 else _lib.MODE_INIT_PLAIN)
         if self.dense:
             return self._dense(mode)
-        _lib.call("spkm_full_assign", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work, mode, self.sp)
+        _lib.call("spkm_full_assign", self.xs, self.C.struct, self.P.bounds, self.P.work, mode, self.sp)
 
     def scratch_sums(self):
-        _lib.call("spkm_aggregate_sums", self.corpus.struct, self.C.struct, self.P.bounds,
-                  _ptr(self.C.sums), _ptr(self.C.counts), self.sp)
-        if self.comm is not None:
-            with torch.cuda.stream(self.stream):
-                self.comm.scratch(self.C.sums, self.C.counts)
+        if self.comm is None:
+            _lib.call("spkm_aggregate_sums", self.corpus.struct, self.C.struct, self.P.bounds,
+                      _ptr(self.C.sums), _ptr(self.C.counts), self.sp)
+            return
+        # multi-GPU: gather every shard's assignments, aggregate the whole
+        # (replicated) corpus locally: identical exact sums on every rank
+        with torch.cuda.stream(self.stream):
+            self.comm.allgather_assignments(self.P.a, self.a_global)
+            _lib.call("spkm_aggregate_sums", self.corpus.struct, self.C.struct, Bounds(_ptr(self.a_global), None, None, 1),
+                      _ptr(self.C.sums), _ptr(self.C.counts), self.sp)
 
     def lloyd_pass(self):
         if self.dense:
             return self._dense(_lib.MODE_LLOYD)
-        _lib.call("spkm_full_assign", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
+        _lib.call("spkm_full_assign", self.xs, self.C.struct, self.P.bounds, self.P.work,
                   _lib.MODE_LLOYD, self.sp)
 
     def bounds_pass(self, use_flag: int):
         if self.elkan:
-            _lib.call("spkm_elkan_bounds", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
-                      use_flag, self.sp)
+            _lib.call("spkm_elkan_bounds", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
         else:
-            _lib.call("spkm_hamerly_bounds", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
-                      use_flag, self.naive, self.sp)
+            _lib.call("spkm_hamerly_bounds", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag,
+                      self.naive, self.sp)
 
     def scan_pass(self, use_flag: int):
         if self.elkan:
-            _lib.call("spkm_elkan_scan", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
-                      use_flag, self.sp)
+            _lib.call("spkm_elkan_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
         elif self.dense:
             self._dense(_lib.DMODE_RESCAN_H, use_flag)   # tighten + full scan on the canonical TC values
         else:
-            _lib.call("spkm_hamerly_tighten", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
-                      use_flag, self.sp)
-            _lib.call("spkm_hamerly_rescan", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
-                      self.sp)
+            _lib.call("spkm_hamerly_tighten", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
+            _lib.call("spkm_hamerly_rescan", self.xs, self.C.struct, self.P.bounds, self.P.work, self.sp)
 
     def apply_moves(self):
         if self.comm is None:
             _lib.call("spkm_apply_moves", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
                       _ptr(self.C.sums), _ptr(self.C.counts), _ptr(self.C.touched), self.sp)
-        else:
-            ex = self.comm
-            with torch.cuda.stream(self.stream):
-                ex.begin()
-                _lib.call("spkm_apply_moves", self.corpus.struct, self.C.struct, self.P.bounds, self.P.work,
-                          _ptr(ex.delta), _ptr(ex.dcounts), _ptr(self.C.touched), self.sp)
-                ex.exchange(self.C.sums, self.C.counts, self.C.touched, self.P.ctr)
+            return
+        # multi-GPU: pack this rank's moves + counters, allgather the slots,
+        # apply every rank's moves to the replicated sums (distributed.py)
+        ex = self.comm
+        with torch.cuda.stream(self.stream):
+            _lib.call("spkm_pack_moves", self.P.work, self.P.bounds, self.C.struct, self.p0, ex.cap, _ptr(ex.slot),
+                      self.sp)
+            ex.allgather_moves()
+            _lib.call("spkm_apply_move_slots", self.corpus.struct, self.C.struct, _ptr(ex.slots), ex.world,
+                      ex.slot_len, _ptr(self.C.touched), _ptr(self.P.ctr), self.sp)
 
     def move_centers(self, all_clusters: bool):
         _lib.call("spkm_move_centers", self.C.struct, int(all_clusters), self.sp)
@@ -743,8 +759,11 @@ class Engine:
                 self.center_thresholds()
             self.bounds_pass(use)
             if debug_hook is not None:
-                self.stream.synchronize()
-                debug_hook(it, self.host_bounds(), self.centroid_set(seed_indices))
+                if hasattr(debug_hook, "device_audit"):    # validation.DeviceBoundAuditor: stays on the device
+                    debug_hook.device_audit(it, self)
+                else:
+                    self.stream.synchronize()
+                    debug_hook(it, self.host_bounds(), self.centroid_set(seed_indices))
             self.scan_pass(use)
             sims_extra = 0
         self.apply_moves()
@@ -806,7 +825,7 @@ class Engine:
         """One D2H of stats rows [first, first+count) and the control words
         (and the assignments into a pinned buffer), then one host sync."""
         F = _lib.ST_COUNT
-        n = self.corpus.n
+        n = self.n_loc
         with torch.cuda.stream(self.stream):
             self.P.hist_host[:count * F].copy_(self.P.hist[first * F:(first + count) * F], non_blocking=True)
             self.P.hist_host[-2:].copy_(self.C.ctl.to(torch.float64), non_blocking=True)
@@ -842,6 +861,8 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
     from .seeding import SeedConfig, seed_rows_for
 
     _validate(data, k, variant, hamerly_update)
+    if comm is not None and debug_hook is not None:
+        raise ConfigError("debug_hook is single-process only (the reference's hook sees every row)")
     cfg = seeding if seeding is not None else SeedConfig()
     if init_centers is None:
         cfg.validate()
@@ -927,11 +948,14 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
     eng.stream.synchronize()
     eng.runs += 1
     torch.cuda.current_stream(eng.device).wait_stream(eng.stream)
-    n_loc = eng.corpus.n
-    a_dev = eng.a_host[:n_loc].numpy() if a_read else eng.P.a[:n_loc].cpu().numpy()
-    a = eng.corpus.to_host_rows(a_dev.astype(np.int64))
     if comm is not None:
-        a = comm.gather_assignments(torch.from_numpy(a).to(eng.device), eng.corpus.rows, eng.n_total)
+        with torch.cuda.stream(eng.stream):
+            comm.allgather_assignments(eng.P.a, eng.a_global)
+        eng.stream.synchronize()
+        a_dev = eng.a_global[:eng.corpus.n].cpu().numpy()
+    else:
+        a_dev = eng.a_host[:eng.n_loc].numpy() if a_read else eng.P.a[:eng.n_loc].cpu().numpy()
+    a = eng.corpus.to_host_rows(a_dev.astype(np.int64))
     return ClusteringResult(assignments=a, centers=DeviceCentroidSet(eng.C.snapshot(), seed_indices),
                             objective=stats[-1].objective, iterations=stats, converged=converged)
 
@@ -944,15 +968,12 @@ _ENGINE_CACHE_MAX = 6
 
 
 def _engine_for(data, k, variant, device, hamerly_update, corpus, comm, n_total, use_graphs):
-    if comm is not None:
-        return Engine(data, k, variant, device=device, hamerly_update=hamerly_update, corpus=corpus, comm=comm,
-                      n_total=n_total, use_graphs=False)
     dev = _require_cuda(device)
     corpus = corpus if corpus is not None else device_corpus(data, dev)
-    key = (str(dev), id(corpus), k, variant, hamerly_update, n_total, use_graphs, data.dim)
+    key = (str(dev), id(corpus), k, variant, hamerly_update, n_total, use_graphs, data.dim, id(comm))
     eng = _ENGINES.pop(key, None)
-    if eng is None or eng.corpus is not corpus:
-        eng = Engine(data, k, variant, device=dev, hamerly_update=hamerly_update, corpus=corpus, comm=None,
+    if eng is None or eng.corpus is not corpus or eng.comm is not comm:
+        eng = Engine(data, k, variant, device=dev, hamerly_update=hamerly_update, corpus=corpus, comm=comm,
                      n_total=n_total, use_graphs=use_graphs)
     else:
         eng.C.cc_valid = False

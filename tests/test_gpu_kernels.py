@@ -346,3 +346,33 @@ def test_device_loop_max_iter_and_reuse(variant):
         assert g.objective == e.objective
         assert [s.reassignments for s in g.iterations] == [s.reassignments for s in e.iterations]
         assert all(s.elapsed_ns > 0 for s in g.iterations)
+
+
+@pytest.mark.parametrize("variant", ["standard", "elkan", "hamerly"])
+def test_sharded_path_single_rank_matches_run(variant):
+    """distributed.run_sharded (replicated corpus, move slots, assignment
+    allgather) on a one-rank NCCL group gives the single-process result
+    bit-for-bit (the kernels of the multi-GPU exchange run; the collectives
+    are trivial at world size 1)."""
+    import os
+    import socket
+    import torch.distributed as dist
+    from paper_2107_04074_b200.distributed import run_sharded
+    m = spk()
+    data = golden_dataset(load_golden("C1"))
+    if not dist.is_initialized():
+        s = socket.socket()
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+        s.close()
+        os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    try:
+        r = run_sharded(data, 20, variant, m.SeedConfig(seed=5), max_iter=30)
+        e = m.run(data, 20, variant, m.SeedConfig(seed=5), max_iter=30, use_graphs=False)
+        assert np.array_equal(r.assignments, e.assignments)
+        assert r.objective == e.objective
+        assert [s.reassignments for s in r.iterations] == [s.reassignments for s in e.iterations]
+        assert [s.sim_count for s in r.iterations] == [s.sim_count for s in e.iterations]
+    finally:
+        dist.destroy_process_group()

@@ -175,25 +175,37 @@ def run_reference(args):
 
 def cpu_baseline(args, data, budget_s: float = 20.0):
     """Bounded sample (about 10-30 s of CPU): one fit of each variant with the
-    oracle, capped at the number of iterations a 2-iteration probe says fits
-    the budget (full fits at C2 k=100)."""
+    oracle.  A 2-iteration probe on at most 20k rows estimates the cost; when
+    the full workload does not fit the budget the fits are capped in
+    iterations and, if needed, run on the first n' rows with the rate scaled
+    by n'/n (per-iteration cost is linear in n), and the sample says so."""
     from oracle import oracle as O
-    X = O.CSR(data.indptr, data.indices, data.data, data.dim)
     variants = args.variants.split(",")
+
+    def csr(rows):
+        ip = data.indptr[:rows + 1]
+        return O.CSR(ip, data.indices[:ip[-1]], data.data[:ip[-1]], data.dim)
+
+    n_probe = min(data.n, 20000)
     t0 = time.perf_counter()
-    probe = O.run(X, args.k, variants[0], seed=args.seed, max_iter=2)["iterations"]
-    per_it = (time.perf_counter() - t0) / max(probe, 1)
-    mi = args.max_iter
-    if per_it * args.max_iter * len(variants) > budget_s:
-        mi = max(2, min(args.max_iter, int(budget_s / (per_it * len(variants)))))
+    probe = O.run(csr(n_probe), min(args.k, n_probe), variants[0], seed=args.seed, max_iter=2)["iterations"]
+    per_it_full = (time.perf_counter() - t0) / max(probe, 1) * data.n / n_probe
+    n_sub, mi = data.n, args.max_iter
+    if per_it_full * mi * len(variants) > budget_s:
+        mi = max(2, min(mi, int(budget_s / (per_it_full * len(variants)))))
+        if per_it_full * mi * len(variants) > budget_s:
+            n_sub = max(min(data.n, 2000), int(data.n * budget_s / (per_it_full * mi * len(variants))))
+    X = csr(n_sub) if n_sub < data.n else O.CSR(data.indptr, data.indices, data.data, data.dim)
     its = 0
     t0 = time.perf_counter()
     for v in variants:
-        its += O.run(X, args.k, v, seed=args.seed, max_iter=mi)["iterations"]
+        its += O.run(X, min(args.k, n_sub), v, seed=args.seed, max_iter=mi)["iterations"]
     dt = time.perf_counter() - t0
+    scale = n_sub / data.n
     cap = "" if mi == args.max_iter else f", each capped at {mi} iterations"
-    return {"value": its / dt, "unit": "iterations/s", "cores": O.num_threads(), "kind": "port",
-            "sample": f"one fit of each variant{cap} ({its} iterations, {dt:.1f} s), C oracle, OpenMP threads"}
+    rows = "" if n_sub == data.n else f", on the first {n_sub} of {data.n} rows (rate scaled by {scale:.4g})"
+    return {"value": its / dt * scale, "unit": "iterations/s", "cores": O.num_threads(), "kind": "port",
+            "sample": f"one fit of each variant{cap}{rows} ({its} iterations, {dt:.1f} s), C oracle, OpenMP threads"}
 
 
 # ----------------------------------------------------------------- our arm
@@ -404,8 +416,12 @@ def roofline(args, data, corpus, dev, world):
         calls[name][1] += 1
     total = sum(v[0] for v in calls.values())
     share = {nm: round(v[0] / total, 4) for nm, v in sorted(calls.items(), key=lambda x: -x[1][0])}
-    # dominant kernel among those with a byte (HBM) or flop (tensor) model
-    cand = [nm for nm in share if any(key[0] == nm for key in list(bytes_by) + list(flops_by))]
+    # dominant KERNEL: the largest single-kernel entry point with a byte (HBM)
+    # or flop (tensor) model; multi-kernel entry points (center update:
+    # 4-5 short kernels whose event span includes host launch gaps in this
+    # eager profiling pass) are reported beside it
+    multi = {"spkm_move_centers", "spkm_center_thresholds", "spkm_aggregate_sums"}
+    cand = [nm for nm in share if nm not in multi and any(key[0] == nm for key in list(bytes_by) + list(flops_by))]
     dom = cand[0] if cand else None
     out = {"bound": "hbm", "peak": pk.get("hbm_gbs"), "unit": "GB/s", "peak_source": src,
            "time_share": share, "traffic": None}
@@ -428,6 +444,14 @@ def roofline(args, data, corpus, dev, world):
     if tr is not None:
         out["traffic"] = tr["dram_bytes_per_launch"]
         out["traffic_source"] = tr["source"]
+        if "ncu_throughput_pct" in tr:
+            out["ncu_throughput_pct"] = tr["ncu_throughput_pct"]
+    if "spkm_move_centers" in calls:
+        b = sum(val for key, val in bytes_by.items() if key[0] == "spkm_move_centers")
+        ms = calls["spkm_move_centers"][0]
+        out["center_update"] = {"entry": "spkm_move_centers", "algorithmic_bytes": b, "ms": ms,
+                                "achieved_gbs": b / (ms / 1e3) / 1e9 if ms else None,
+                                "note": "20 B per (touched cluster, term), SURVEY.md 8(d); event span of 4 kernels"}
     return out
 
 

@@ -983,7 +983,8 @@ __global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     if (threadIdx.x < kTileJ) js[threadIdx.x] = (y0 + threadIdx.x < nT) ? tlist[y0 + threadIdx.x] : -1;
     __syncthreads();
-#pragma unroll
+    constexpr int QN = kTileT / 32;   // terms per lane per cluster
+#pragma unroll 1
     for (int r = 0; r < 4; ++r) {
         const int jr = w * 4 + r;
         const int j = js[jr];
@@ -993,13 +994,24 @@ __global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int
             const double inv_nrm = 1.0 / nrm;
             const long long *sj = sums + (int64_t)j * d;
             double *cj = cent64 + (int64_t)j * d;
+            // all loads of this cluster's slice first (QN sums + QN old values
+            // in flight per lane), then the arithmetic and the stores
+            long long sv[QN];
+            double ov[QN];
 #pragma unroll
-            for (int q = lane; q < kTileT; q += 32) {
+            for (int qi = 0; qi < QN; ++qi) {
+                const int64_t t = t0 + lane + 32 * qi;
+                sv[qi] = t < d ? __ldg(sj + t) : 0;
+                ov[qi] = t < d ? cj[t] : 0.0;
+            }
+#pragma unroll
+            for (int qi = 0; qi < QN; ++qi) {
+                const int q = lane + 32 * qi;
                 const int64_t t = t0 + q;
                 float f = 0.f;
                 if (t < d) {
-                    const double v = (double)sj[t] * inv_scale;
-                    const double old = cj[t];
+                    const double v = (double)sv[qi] * inv_scale;
+                    const double old = ov[qi];
                     if (nrm < 0.0) {
                         ob = fma(v, old, ob);
                         f = (float)old;
@@ -1397,7 +1409,8 @@ constexpr int kGramThreads = 512;
 
 __global__ void __launch_bounds__(kGramThreads, 1) k_gram_tc(int64_t k, int64_t d, int64_t dsplit,
                                                      const double *__restrict__ C, const int2 *__restrict__ tiles,
-                                                     const double *__restrict__ sinp, int full, double *gpart, const long long *__restrict__ ctl) {
+                                                     const double *__restrict__ sinp, int full, double *gpart, const long long *__restrict__ ctl,
+                                                     int nbuf) {
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     extern __shared__ __align__(1024) uint8_t gsm[];
     // layout: [stage 0: Ahi Alo Bhi Blo][stage 1: ...][2 mbarriers][tmem addr]
@@ -1436,7 +1449,8 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_gram_tc(int64_t k, int64_t 
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_base_s;
     const int nch = t1 > t0 ? (int)((t1 - t0 + GKC - 1) / GKC) : 0;
-    auto buf = [&](int s, int which) { return gsm + (size_t)(s * 4 + which) * GOPB; };   // 0 Ahi 1 Alo 2 Bhi 3 Blo
+    // 0 Ahi 1 Alo 2 Bhi 3 Blo; a grid of diagonal tiles only (k <= 128) stages A alone (nbuf = 2)
+    auto buf = [&](int s, int which) { return gsm + (size_t)(s * nbuf + which) * GOPB; };
     auto load_stage = [&](int s, int64_t tb) {
         stage_operand<GT * (GKC / 4) / kGramThreads>(C, d, k, a0, tb, t1, buf(s, 0), buf(s, 1));
         if (!diag) stage_operand<GT * (GKC / 4) / kGramThreads>(C, d, k, j0, tb, t1, buf(s, 2), buf(s, 3));
@@ -2387,12 +2401,14 @@ int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long lo
 }
 
 int64_t spkm_gram_dsplit(int64_t k, int64_t d) {
-    // one wave (one CTA per SM: ~130 KB of stages), at most 512 terms per CTA
-    // when that still fills the machine
+    // one wave: one CTA per SM (~130 KB of stages), or two per SM when the
+    // grid is the single diagonal tile (k <= 128: A staged alone, 66 KB);
+    // at least 256 terms per CTA
     const int64_t tk = (k + GT - 1) / GT;
     const int64_t tiles = tk * (tk + 1) / 2;
-    int64_t ds = (int64_t)num_sms() / tiles;
-    const int64_t maxds = (d + 511) / 512;
+    const int64_t per_sm = (tk == 1) ? 2 : 1;
+    int64_t ds = (int64_t)num_sms() * per_sm / tiles;
+    const int64_t maxds = (d + 255) / 256;
     if (ds > maxds) ds = maxds;
     if (ds < 1) ds = 1;
     return ds;
@@ -2408,14 +2424,16 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     const int64_t ds = spkm_gram_dsplit(C->k, C->d);
     const int64_t per = ((C->d + ds - 1) / ds + GKC - 1) / GKC * GKC;
     const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + 1e-6;
-    const size_t smem = (size_t)8 * GOPB;
+    const int nbuf = (tk == 1) ? 2 : 4;
+    const size_t smem = (size_t)2 * nbuf * GOPB;
     static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (!attr_set) {   // the largest configuration (4 buffers per stage)
+        cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * GOPB));
         attr_set = true;
     }
     dim3 grid((unsigned)ntiles, (unsigned)ds);
-    k_gram_tc<<<grid, kGramThreads, smem, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart, C->ctl);
+    k_gram_tc<<<grid, kGramThreads, smem, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart, C->ctl,
+                                                nbuf);
     CHECK_LAUNCH("gram_tc");
     k_gram_final<<<(unsigned)((C->k * C->k * 8 + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, gdelta,
                                                                            C->cc, C->ctl);

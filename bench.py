@@ -446,6 +446,15 @@ def roofline(args, data, corpus, dev, world):
         out["traffic_source"] = tr["source"]
         if "ncu_throughput_pct" in tr:
             out["ncu_throughput_pct"] = tr["ncu_throughput_pct"]
+    # every entry point with a byte model: achieved GB/s of its event span
+    per = {}
+    for nm, (ms, nl) in calls.items():
+        b = sum(val for key, val in bytes_by.items() if key[0] == nm)
+        if b and ms:
+            per[nm] = {"launches": nl, "ms": round(ms, 4), "algorithmic_bytes": b,
+                       "achieved_gbs": round(b / (ms / 1e3) / 1e9, 1),
+                       "frac": round(b / (ms / 1e3) / 1e9 / pk.get("hbm_gbs"), 4)}
+    out["per_entry"] = per
     if "spkm_move_centers" in calls:
         b = sum(val for key, val in bytes_by.items() if key[0] == "spkm_move_centers")
         ms = calls["spkm_move_centers"][0]

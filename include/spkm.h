@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SPKM_ABI_VERSION 1
+#define SPKM_ABI_VERSION 2
 
 /* variants, engine.py:22 */
 enum spkm_variant {

@@ -20,7 +20,7 @@ LIB_PATH = PKG / "libspkm.so"
 SRC = PKG / "csrc" / "spkm.cu"
 SRC_HOST = PKG / "csrc" / "ingest.cpp"
 HEADER = ROOT / "include" / "spkm.h"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

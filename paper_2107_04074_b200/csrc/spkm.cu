@@ -510,6 +510,7 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
+    const int k4 = (k + 3) >> 2;   // u rows are ku (a multiple of 4) floats: 16-byte vectors
     for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
         const int ai = a[i];
         const float lo = l[i];
@@ -523,22 +524,34 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
         const double eps = (double)reps[i];
         const double lb = (double)lf;
         const bool pskip = use_cc && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb;
+        const bool cc_on = use_cc && lb >= 0.0;
         bool any = false;
-        float *ui = u + i * ku;
-        for (int j = lane; j < k; j += 32) {
-            float uf = ui[j];
-            const double sj = sinp[j];
-            if (sj != 0.0) {   // engine.py:281-283 with the chord-based sine bound
-                const double pj = drift[j];
-                const double nv = ((double)uf <= pj) ? d_clamp((double)uf * pj + d_sin((double)uf) * sj) : 1.0;
-                uf = store_upper(nv);
-                ui[j] = uf;
+        float4 *ui = reinterpret_cast<float4 *>(u + i * ku);
+        const float *cca = cc + (int64_t)ai * k;
+#pragma unroll 2
+        for (int q = lane; q < k4; q += 32) {
+            const float4 uv = ui[q];
+            float w[4] = {uv.x, uv.y, uv.z, uv.w};
+            bool changed = false;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int j = 4 * q + c;
+                if (j >= k) break;
+                const double sj = sinp[j];
+                if (sj != 0.0) {   // engine.py:281-283 with the chord-based sine bound
+                    const double pj = drift[j];
+                    const double nv = ((double)w[c] <= pj) ? d_clamp((double)w[c] * pj + d_sin((double)w[c]) * sj)
+                                                           : 1.0;
+                    w[c] = store_upper(nv);
+                    changed = true;
+                }
+                if (!pskip && j != ai) {
+                    bool skip = cc_on && (double)__ldg(cca + j) + kSqrt2 * eps <= lb;
+                    if (!skip) skip = ((double)w[c] + 2.0 * eps <= lb);
+                    any |= !skip;
+                }
             }
-            if (!pskip && j != ai) {
-                bool skip = use_cc && lb >= 0.0 && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb;
-                if (!skip) skip = ((double)uf + 2.0 * eps <= lb);
-                any |= !skip;
-            }
+            if (changed) ui[q] = make_float4(w[0], w[1], w[2], w[3]);
         }
         any = __any_sync(FULL, any);
         if (lane == 0 && any) {
@@ -1698,34 +1711,68 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
     const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
 
     if (w >= 1 && w <= 3) {
-        // ---------------- producers
+        // ---------------- producers: every thread owns the same (row, 16-byte
+        // chunk) tasks in every stage, so the shared-memory offsets are fixed,
+        // the source rows are resolved once per tile (rowlist) and the centers
+        // once per pass; a stage is then 2 x (NA + NB) cp.async of
+        // precomputed addresses plus the stage's dim offset.
+        constexpr int TA = DN_M * (DN_KC / 4), TB = DN_N * (DN_KC / 4);
+        constexpr int NA = (TA + DN_PRODUCERS - 1) / DN_PRODUCERS;
+        constexpr int NB = (TB + DN_PRODUCERS - 1) / DN_PRODUCERS;
         const int pt = threadIdx.x - 32;
+        const int64_t xlo_d = P.xlo - P.xhi, blo_d = P.blo - P.bhi;   // element offsets of the lo parts
+        uint32_t aoff[NA], boff[NB];
+#pragma unroll
+        for (int u = 0; u < NA; ++u) {
+            const int e = pt + u * DN_PRODUCERS, m = e >> 2, q = e & 3;
+            aoff[u] = e < TA ? (uint32_t)((q >> 1) * DN_GRP_A + (q & 1) * DN_LBO_A + (m >> 3) * 128 + (m & 7) * 16)
+                             : 0xffffffffu;
+        }
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+            const int e = pt + u * DN_PRODUCERS, m = e >> 2, q = e & 3;
+            boff[u] = e < TB ? (uint32_t)((q >> 1) * DN_GRP_B + (q & 1) * DN_LBO_B + (m >> 3) * 128 + (m & 7) * 16)
+                             : 0xffffffffu;
+        }
         uint32_t it = 0;
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             const int64_t tile = blockIdx.x + ti * gridDim.x;
+            const float *asrc[NA];
+            bool aval[NA];
+#pragma unroll
+            for (int u = 0; u < NA; ++u) {
+                const int e = pt + u * DN_PRODUCERS, m = e >> 2, q = e & 3;
+                const int64_t slot = tile * DN_M + m;
+                const int32_t r = (e < TA && slot < nrows) ? (P.rowlist ? P.rowlist[slot] : (int32_t)slot) : -1;
+                aval[u] = r >= 0;
+                asrc[u] = P.xhi + (int64_t)(r < 0 ? 0 : r) * P.D + 4 * q;
+            }
             for (int pass = 0; pass < npass; ++pass) {
+                const float *bsrc[NB];
+#pragma unroll
+                for (int u = 0; u < NB; ++u) {
+                    const int e = pt + u * DN_PRODUCERS, m = e >> 2, q = e & 3;
+                    bsrc[u] = P.bhi + ((int64_t)pass * DN_N + (e < TB ? m : 0)) * P.D + 4 * q;
+                }
                 for (int ks = 0; ks < nks; ++ks, ++it) {
                     const int s = it % DN_STAGES;
                     if (it >= DN_STAGES) mbar_wait(smem_u32(&empty_b[s]), ((it / DN_STAGES) - 1) & 1);
                     const uint32_t ahi = smem_u32(stage_ptr(s)), alo = ahi + DN_OPA, bhi = alo + DN_OPA,
                                    blo = bhi + DN_OPB;
-                    const int64_t k0 = (int64_t)ks * DN_KC;
-                    for (int e = pt; e < DN_M * (DN_KC / 4); e += DN_PRODUCERS) {
-                        const int m = e >> 2, q = e & 3;
-                        const int64_t slot = tile * DN_M + m;
-                        const int32_t r = slot < nrows ? (P.rowlist ? P.rowlist[slot] : (int32_t)slot) : -1;
-                        const int off = (q >> 1) * DN_GRP_A + (q & 1) * DN_LBO_A + (m >> 3) * 128 + (m & 7) * 16;
-                        const int64_t src = (int64_t)(r < 0 ? 0 : r) * P.D + k0 + 4 * q;
-                        cp_async16(ahi + off, P.xhi + src, r >= 0);
-                        cp_async16(alo + off, P.xlo + src, r >= 0);
+                    const int k0 = ks * DN_KC;
+#pragma unroll
+                    for (int u = 0; u < NA; ++u) {
+                        if (aoff[u] != 0xffffffffu) {
+                            cp_async16(ahi + aoff[u], asrc[u] + k0, aval[u]);
+                            cp_async16(alo + aoff[u], asrc[u] + xlo_d + k0, aval[u]);
+                        }
                     }
-                    const int64_t c0 = (int64_t)pass * DN_N;
-                    for (int e = pt; e < DN_N * (DN_KC / 4); e += DN_PRODUCERS) {
-                        const int m = e >> 2, q = e & 3;
-                        const int off = (q >> 1) * DN_GRP_B + (q & 1) * DN_LBO_B + (m >> 3) * 128 + (m & 7) * 16;
-                        const int64_t src = (c0 + m) * P.D + k0 + 4 * q;
-                        cp_async16(bhi + off, P.bhi + src, true);
-                        cp_async16(blo + off, P.blo + src, true);
+#pragma unroll
+                    for (int u = 0; u < NB; ++u) {
+                        if (boff[u] != 0xffffffffu) {
+                            cp_async16(bhi + boff[u], bsrc[u] + k0, true);
+                            cp_async16(blo + boff[u], bsrc[u] + blo_d + k0, true);
+                        }
                     }
                     asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full_b[s]))
                                  : "memory");

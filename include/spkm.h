@@ -103,16 +103,16 @@ typedef struct spkm_bounds {
     int64_t ku;              /* row stride of u (Elkan) or 1 (Hamerly)       */
 } spkm_bounds;
 
-/* Dense corpus (config C5): rows and centers split into tf32 hi/lo parts for
- * the tcgen05 3xTF32 pass; centers padded with zero rows to kpad (a multiple
- * of 256). */
+/* Dense corpus (config C5): float32 rows and float32 centers (zero rows
+ * past k, kpad a multiple of 256); the tcgen05 pass streams both with TMA and
+ * splits them into tf32 hi + lo on the fly (3xTF32).  xs: [n][D] scratch the
+ * Hamerly rescan compacts its survivors into (NULL if never rescanned). */
 typedef struct spkm_dense {
     int64_t D;               /* dimensionality (multiple of 32)              */
     int64_t kpad;
-    const float *xhi;        /* [n][D]                                       */
-    const float *xlo;        /* [n][D]                                       */
-    float *bhi;              /* [kpad][D]                                    */
-    float *blo;              /* [kpad][D]                                    */
+    const float *x;          /* [n][D] rows (the spkm_csr values)            */
+    float *b;                /* [kpad][D] centers, written by dense_centers  */
+    float *xs;               /* [n][D] survivor scratch                      */
 } spkm_dense;
 
 /* Worklists and device-side counters. */
@@ -217,11 +217,10 @@ int spkm_load_centers(const spkm_centers *C, const double *host_or_dev_centers, 
 int spkm_seed_rows(const spkm_centers *C, const int64_t *sptr, const int32_t *sidx, const double *sval,
                    void *stream);
 
-/* Dense path (config C5).  split: x -> tf32 hi + lo; centers: cent64 -> bhi/blo;
- * assign: the tensor-core similarity pass with fused top-2.  mode is an
+/* Dense path (config C5).  centers: cent64 -> float32 b; assign: the
+ * tensor-core similarity pass (3xTF32) with fused top-2.  mode is an
  * spkm_assign_mode, 5 (predict: writes a, best, second) or 6 (Hamerly
  * tighten + full scan over work->surv1, kernels.py:81-112). */
-int spkm_dense_split(const float *x, int64_t count, float *hi, float *lo, void *stream);
 int spkm_dense_centers(const spkm_centers *C, const spkm_dense *Dn, void *stream);
 int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense *Dn, spkm_bounds *B,
                       spkm_work *W, int mode, int use_s, double *best, double *second, void *stream);

@@ -47,7 +47,7 @@ class Bounds(ctypes.Structure):
 
 
 class Dense(ctypes.Structure):
-    _fields_ = [("D", c_i64), ("kpad", c_i64), ("xhi", c_vp), ("xlo", c_vp), ("bhi", c_vp), ("blo", c_vp)]
+    _fields_ = [("D", c_i64), ("kpad", c_i64), ("x", c_vp), ("b", c_vp), ("xs", c_vp)]
 
 
 class Seed(ctypes.Structure):
@@ -120,7 +120,6 @@ _SIGS = {
     "spkm_svml_free": [_P(Svml)],
     "spkm_host_idf": [c_i64, c_vp, c_i64, ctypes.c_int, c_vp],
     "spkm_seed_rows": [_P(Centers), c_vp, c_vp, c_vp, c_vp],
-    "spkm_dense_split": [c_vp, c_i64, c_vp, c_vp, c_vp],
     "spkm_dense_centers": [_P(Centers), _P(Dense), c_vp],
     "spkm_dense_assign": [_P(CSR), _P(Centers), _P(Dense), _P(Bounds), _P(Work), ctypes.c_int, ctypes.c_int,
                           c_vp, c_vp, c_vp],
@@ -142,7 +141,7 @@ KERNELS_PER_CALL = {
     "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
     "spkm_move_centers": 5, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
-    "spkm_dense_split": 1, "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
+    "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
     "spkm_seed_rows_csr": 1, "spkm_aggregate_sums_gated": 2, "spkm_permute_rows": 1, "spkm_audit": 1, "spkm_audit_transpose": 1,
     "spkm_pack_moves": 1, "spkm_apply_move_slots": 1,
 }

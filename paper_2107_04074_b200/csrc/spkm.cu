@@ -25,6 +25,8 @@
 //    incremental == scratch and sums are independent of atomic order and of
 //    the GPU count.  Renormalisation, drift and objective are float64 with
 //    fixed-order reductions.
+#include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -1611,22 +1613,28 @@ __global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s, con
 //     ceil(k/256) passes, D/32 double-buffered stages of 32 dims, 3 MMAs per
 //     8-dim group (lo.hi, hi.lo, hi.hi); thread = row in the epilogue, which
 //     keeps a running top-2 (tie rule) and the incumbent's value;
+//   * split: hi = the float32 word read as tf32 (the tensor core truncates to
+//     tf32), lo = x - trunc_tf32(x) (exact), truncated again by the MMA; the
+//     residual of each operand is below 2^-20 |x|;
 //   * error: (3D/8 + 8) 2^-22 (fp32 TMEM accumulation, truncation assumed)
-//     + 1e-6 (float32 rounding of rows and centers 2 x 2^-24, split
-//     residuals 3 x 2^-22, times sum|x c| <= 1) -> row eps (host).
+//     + 4e-6 (split residuals of rows and centers and the dropped lo.lo
+//     product, 3 x 2^-20, plus float32 rounding of rows and centers
+//     2 x 2^-24, times sum|x c| <= 1) -> row eps (host).
 constexpr int DN_M = 128;                         // rows per tile (TMEM lanes)
 constexpr int DN_N = 256;                         // centers per pass (TMEM columns per accumulator)
 constexpr int DN_KC = 16;                         // dims per pipeline stage
-constexpr int DN_STAGES = 4;
-constexpr int DN_THREADS = 256;                   // w0: MMA issuer, w1-3: producers, w4-7: epilogue
-constexpr int DN_PRODUCERS = 96;
-constexpr int DN_LBO_A = (DN_M / 8) * 128 + 16;
-constexpr int DN_GRP_A = 2 * DN_LBO_A + 32;
-constexpr int DN_LBO_B = (DN_N / 8) * 128 + 16;
-constexpr int DN_GRP_B = 2 * DN_LBO_B + 32;
+constexpr int DN_STAGES = 4;                      // stages: raw float32 (= tf32 hi operand) + lo
+constexpr int DN_THREADS = 384;                   // w0 MMA, w1 TMA, w2-7 converters, w8-11 epilogue
+constexpr int DN_CONV = 192;                      // converter threads
+// K-major no-swizzle core matrices, unpadded so that a TMA box of 4 dims x
+constexpr int DN_LBO_A = (DN_M / 8) * 128;
+constexpr int DN_GRP_A = 2 * DN_LBO_A;
+constexpr int DN_LBO_B = (DN_N / 8) * 128;
+constexpr int DN_GRP_B = 2 * DN_LBO_B;
 constexpr int DN_OPA = (DN_KC / 8) * DN_GRP_A;    // one stage, one part (hi or lo) of A
 constexpr int DN_OPB = (DN_KC / 8) * DN_GRP_B;
-constexpr int DN_STAGE = 2 * DN_OPA + 2 * DN_OPB;
+constexpr int DN_RAWST = DN_OPA + DN_OPB;          // float32 A, B of one stage (TMA); read as the hi operand
+constexpr int DN_STAGE = 2 * DN_RAWST;             // + the lo parts written by the converters
 constexpr uint32_t kDenseIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(DN_N >> 3) << 17) |
                                  ((uint32_t)(DN_M >> 4) << 24);
 enum { DMODE_RESCAN_H = 6 };
@@ -1637,6 +1645,17 @@ __device__ __forceinline__ uint64_t umma_desc2(uint32_t saddr, uint32_t lbo) {
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
     d |= (uint64_t)((128 >> 4) & 0x3FFF) << 32;
     d |= (uint64_t)1 << 46;
+    return d;
+}
+// SmemDescriptor for K-major SWIZZLE_64B operands: rows of 64 bytes, 8-row
+// atoms 512 bytes apart (SBO), LBO unused (1), layout type 4 at bits [61,64)
+__device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;
+    d |= (uint64_t)((512 >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)4 << 61;
     return d;
 }
 __device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool pred) {
@@ -1650,14 +1669,23 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
+// x -> (tf32 hi, tf32 lo) of 4 values (cvt.rna, lo = tf32(x - hi)), 16-byte stores
+__device__ __forceinline__ void split_store(float4 v, uint8_t *hi, uint8_t *lo) {
+    const uint32_t h0 = to_tf32(v.x), h1 = to_tf32(v.y), h2 = to_tf32(v.z), h3 = to_tf32(v.w);
+    *reinterpret_cast<uint4 *>(hi) = make_uint4(h0, h1, h2, h3);
+    *reinterpret_cast<uint4 *>(lo) =
+        make_uint4(to_tf32(v.x - __uint_as_float(h0)), to_tf32(v.y - __uint_as_float(h1)),
+                   to_tf32(v.z - __uint_as_float(h2)), to_tf32(v.w - __uint_as_float(h3)));
+}
+
 struct DenseArgs {
+    CUtensorMap tm_x, tm_b;          // TMA maps: rows [rows][D] and centers [kpad][D], float32
     int64_t n, D, k, kpad, ku;
-    const float *xhi, *xlo;          // [n][D]
-    const float *bhi, *blo;          // [kpad][D]
     const float *reps;
-    const int32_t *rowlist;          // null: rows [0, n)
-    const long long *rowcount;
+    const int32_t *rowmap;           // null: row = slot; else slot -> row (compacted survivors)
+    const long long *rowcount;       // null: n rows; else device count
     int mode, use_s;
+    int dbg;                         // experiments only (SPKM_DN_DBG): 1 skip epilogue math, 2 skip MMAs
     int32_t *a;
     float *l, *u;
     const float *s_arr;
@@ -1676,13 +1704,26 @@ struct DenseArgs {
 // the last stage of a pass it commits to `accf`; the epilogue warps (one
 // thread per row) read the 256 columns, fold them into a running top-2 and
 // release the buffer through `acce`.
-__global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap *map, int c0, int c1, uint32_t bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::"r"(
+            dst),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+        : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+
+__global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_constant__ DenseArgs P) {
     if (P.ctl[1]) return;
     extern __shared__ __align__(1024) uint8_t dsm[];
-    __shared__ __align__(8) uint64_t full_b[DN_STAGES], empty_b[DN_STAGES], accf[2], acce[2];
+    // stage s: [A f32 | B f32] (TMA; the tensor core reads these float32 words
+    // as tf32 = the hi parts, truncated) [A lo | B lo] (converters)
+    __shared__ __align__(8) uint64_t full_b[DN_STAGES], lo_full[DN_STAGES], empty_b[DN_STAGES], accf[2], acce[2];
     __shared__ uint32_t tmem_base_s;
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t nrows = P.rowlist ? *P.rowcount : P.n;
+    const int64_t nrows = P.rowcount ? *P.rowcount : P.n;
     const int64_t ntiles = (nrows + DN_M - 1) / DN_M;
     const int nks = (int)(P.D / DN_KC);
     const int npass = (int)(P.kpad / DN_N);
@@ -1694,7 +1735,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
     }
     if (threadIdx.x == 0) {
         for (int s = 0; s < DN_STAGES; ++s) {
-            mbar_init(&full_b[s], DN_PRODUCERS);
+            mbar_init(&full_b[s], 1);
+            mbar_init(&lo_full[s], DN_CONV);
             mbar_init(&empty_b[s], 1);
         }
         for (int b = 0; b < 2; ++b) {
@@ -1709,77 +1751,61 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
     const uint32_t tmem = tmem_base_s;
     auto stage_ptr = [&](int s) { return dsm + (size_t)s * DN_STAGE; };
     const int64_t my_tiles = ntiles > blockIdx.x ? (ntiles - 1 - blockIdx.x) / gridDim.x + 1 : 0;
+    const uint32_t total_stages = (uint32_t)(my_tiles * npass * nks);
 
-    if (w >= 1 && w <= 3) {
-        // ---------------- producers: every thread owns the same (row, 16-byte
-        // chunk) tasks in every stage, so the shared-memory offsets are fixed,
-        // the source rows are resolved once per tile (rowlist) and the centers
-        // once per pass; a stage is then 2 x (NA + NB) cp.async of
-        // precomputed addresses plus the stage's dim offset.
-        constexpr int TA = DN_M * (DN_KC / 4), TB = DN_N * (DN_KC / 4);
-        constexpr int NA = (TA + DN_PRODUCERS - 1) / DN_PRODUCERS;
-        constexpr int NB = (TB + DN_PRODUCERS - 1) / DN_PRODUCERS;
-        const int pt = threadIdx.x - 32;
-        const int64_t xlo_d = P.xlo - P.xhi, blo_d = P.blo - P.bhi;   // element offsets of the lo parts
-        uint32_t aoff[NA], boff[NB];
-#pragma unroll
-        for (int u = 0; u < NA; ++u) {
-            const int e = pt + u * DN_PRODUCERS, m = e >> 2, q = e & 3;
-            aoff[u] = e < TA ? (uint32_t)((q >> 1) * DN_GRP_A + (q & 1) * DN_LBO_A + (m >> 3) * 128 + (m & 7) * 16)
-                             : 0xffffffffu;
-        }
-#pragma unroll
-        for (int u = 0; u < NB; ++u) {
-            const int e = pt + u * DN_PRODUCERS, m = e >> 2, q = e & 3;
-            boff[u] = e < TB ? (uint32_t)((q >> 1) * DN_GRP_B + (q & 1) * DN_LBO_B + (m >> 3) * 128 + (m & 7) * 16)
-                             : 0xffffffffu;
-        }
-        uint32_t it = 0;
-        for (int64_t ti = 0; ti < my_tiles; ++ti) {
-            const int64_t tile = blockIdx.x + ti * gridDim.x;
-            const float *asrc[NA];
-            bool aval[NA];
-#pragma unroll
-            for (int u = 0; u < NA; ++u) {
-                const int e = pt + u * DN_PRODUCERS, m = e >> 2, q = e & 3;
-                const int64_t slot = tile * DN_M + m;
-                const int32_t r = (e < TA && slot < nrows) ? (P.rowlist ? P.rowlist[slot] : (int32_t)slot) : -1;
-                aval[u] = r >= 0;
-                asrc[u] = P.xhi + (int64_t)(r < 0 ? 0 : r) * P.D + 4 * q;
-            }
-            for (int pass = 0; pass < npass; ++pass) {
-                const float *bsrc[NB];
-#pragma unroll
-                for (int u = 0; u < NB; ++u) {
-                    const int e = pt + u * DN_PRODUCERS, m = e >> 2, q = e & 3;
-                    bsrc[u] = P.bhi + ((int64_t)pass * DN_N + (e < TB ? m : 0)) * P.D + 4 * q;
-                }
-                for (int ks = 0; ks < nks; ++ks, ++it) {
-                    const int s = it % DN_STAGES;
-                    if (it >= DN_STAGES) mbar_wait(smem_u32(&empty_b[s]), ((it / DN_STAGES) - 1) & 1);
-                    const uint32_t ahi = smem_u32(stage_ptr(s)), alo = ahi + DN_OPA, bhi = alo + DN_OPA,
-                                   blo = bhi + DN_OPB;
-                    const int k0 = ks * DN_KC;
-#pragma unroll
-                    for (int u = 0; u < NA; ++u) {
-                        if (aoff[u] != 0xffffffffu) {
-                            cp_async16(ahi + aoff[u], asrc[u] + k0, aval[u]);
-                            cp_async16(alo + aoff[u], asrc[u] + xlo_d + k0, aval[u]);
+    if (w == 1) {
+        // ---------------- TMA producer: one box of rows + one of centers per stage
+        if (lane == 0) {
+            uint32_t it = 0;
+            for (int64_t ti = 0; ti < my_tiles; ++ti) {
+                const int row0 = (int)((blockIdx.x + ti * gridDim.x) * DN_M);
+                for (int pass = 0; pass < npass; ++pass) {
+                    for (int ks = 0; ks < nks; ++ks, ++it) {
+                        const int s = it % DN_STAGES;
+                        if (it >= DN_STAGES) mbar_wait(smem_u32(&empty_b[s]), ((it / DN_STAGES) - 1) & 1);
+                        const uint32_t ra = smem_u32(stage_ptr(s)), rb = ra + DN_OPA;
+                        const int k0 = ks * DN_KC;
+                        if (P.dbg & 8) {
+                            mbar_arrive(&full_b[s]);
+                        } else {
+                            mbar_expect_tx(&full_b[s], (uint32_t)DN_RAWST);
+                            tma_load_2d(ra, &P.tm_x, k0, row0, smem_u32(&full_b[s]));
+                            tma_load_2d(rb, &P.tm_b, k0, pass * DN_N, smem_u32(&full_b[s]));
                         }
                     }
-#pragma unroll
-                    for (int u = 0; u < NB; ++u) {
-                        if (boff[u] != 0xffffffffu) {
-                            cp_async16(bhi + boff[u], bsrc[u] + k0, true);
-                            cp_async16(blo + boff[u], bsrc[u] + blo_d + k0, true);
-                        }
-                    }
-                    asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];\n" ::"r"(smem_u32(&full_b[s]))
-                                 : "memory");
                 }
             }
         }
-        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        __syncwarp();
+    } else if (w >= 2 && w < 2 + DN_CONV / 32) {
+        // ---------------- converters: lo = x - trunc_tf32(x) (exact in float32;
+        // the tensor core truncates it to tf32 in turn), an elementwise map
+        // because the lo parts share the raw layout byte for byte
+        const int ct = threadIdx.x - 64;
+        for (uint32_t it = 0; it < total_stages; ++it) {
+            const int s = it % DN_STAGES;
+            mbar_wait(smem_u32(&full_b[s]), (it / DN_STAGES) & 1);
+            const uint8_t *ra = stage_ptr(s);
+            uint8_t *lo = stage_ptr(s) + DN_RAWST;
+            if (!(P.dbg & 4)) {
+                constexpr int NV = DN_RAWST / 16 / DN_CONV;
+                static_assert(NV * DN_CONV * 16 == DN_RAWST, "converter split");
+                float4 x[NV];
+#pragma unroll
+                for (int u = 0; u < NV; ++u) x[u] = *reinterpret_cast<const float4 *>(ra + (ct + u * DN_CONV) * 16);
+#pragma unroll
+                for (int u = 0; u < NV; ++u) {
+                    const float4 v = x[u];
+                    const float4 l = make_float4(v.x - __uint_as_float(__float_as_uint(v.x) & 0xffffe000u),
+                                                 v.y - __uint_as_float(__float_as_uint(v.y) & 0xffffe000u),
+                                                 v.z - __uint_as_float(__float_as_uint(v.z) & 0xffffe000u),
+                                                 v.w - __uint_as_float(__float_as_uint(v.w) & 0xffffe000u));
+                    *reinterpret_cast<float4 *>(lo + (ct + u * DN_CONV) * 16) = l;
+                }
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> async proxy
+            mbar_arrive(&lo_full[s]);
+        }
     } else if (w == 0) {
         // ---------------- MMA issuer
         if (lane == 0) {
@@ -1792,17 +1818,18 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
                     const uint32_t dt = tmem + (uint32_t)(b * DN_N);
                     for (int ks = 0; ks < nks; ++ks, ++it) {
                         const int s = it % DN_STAGES;
-                        mbar_wait(smem_u32(&full_b[s]), (it / DN_STAGES) & 1);
-                        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+                        mbar_wait(smem_u32(&lo_full[s]), (it / DN_STAGES) & 1);   // implies the TMA data landed
                         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-                        const uint32_t ahi = smem_u32(stage_ptr(s)), alo = ahi + DN_OPA, bhi = alo + DN_OPA,
-                                       blo = bhi + DN_OPB;
+                        const uint32_t ahi = smem_u32(stage_ptr(s)), bhi = ahi + DN_OPA, alo = ahi + DN_RAWST,
+                                       blo = alo + DN_OPA;
 #pragma unroll
                         for (int g = 0; g < DN_KC / 8; ++g) {
-                            const uint64_t dah = umma_desc2(ahi + g * DN_GRP_A, DN_LBO_A);
-                            const uint64_t dal = umma_desc2(alo + g * DN_GRP_A, DN_LBO_A);
-                            const uint64_t dbh = umma_desc2(bhi + g * DN_GRP_B, DN_LBO_B);
-                            const uint64_t dbl = umma_desc2(blo + g * DN_GRP_B, DN_LBO_B);
+                            if (P.dbg & 2) break;
+                            // K-major SWIZZLE_64B: 8 dims (32 B) per MMA -> +32 B within the 64-byte rows
+                            const uint64_t dah = umma_desc_sw64(ahi + 32 * g);
+                            const uint64_t dal = umma_desc_sw64(alo + 32 * g);
+                            const uint64_t dbh = umma_desc_sw64(bhi + 32 * g);
+                            const uint64_t dbl = umma_desc_sw64(blo + 32 * g);
                             const uint32_t acc0 = (ks > 0 || g > 0) ? 1u : 0u;
                             asm volatile(
                                 "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
@@ -1828,14 +1855,14 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
             }
         }
         __syncwarp();
-    } else {
+    } else if (w >= 8) {
         // ---------------- epilogue: thread = row (TMEM lane quarter w % 4)
-        const int m = (w - 4) * 32 + lane;
+        const int m = (w - 8) * 32 + lane;
         uint32_t pcount = 0;
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             const int64_t tile = blockIdx.x + ti * gridDim.x;
             const int64_t slot = tile * DN_M + m;
-            const int32_t my_row = slot < nrows ? (P.rowlist ? P.rowlist[slot] : (int32_t)slot) : -1;
+            const int32_t my_row = slot < nrows ? (P.rowmap ? P.rowmap[slot] : (int32_t)slot) : -1;
             const int inc = (my_row >= 0 && (P.mode == SPKM_MODE_LLOYD || P.mode == DMODE_RESCAN_H)) ? P.a[my_row] : -1;
             const double eps = my_row >= 0 ? (double)P.reps[my_row] : 0.0;
             Top2 tp{-INFINITY, -2, -INFINITY};
@@ -1847,7 +1874,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
 #pragma unroll 1
                 for (int cb = 0; cb < DN_N / 32; ++cb) {
                     uint32_t r[32];
-                    const uint32_t taddr = tmem + ((uint32_t)((w - 4) * 32) << 16) + (uint32_t)(b * DN_N + cb * 32);
+                    const uint32_t taddr = tmem + ((uint32_t)((w - 8) * 32) << 16) + (uint32_t)(b * DN_N + cb * 32);
                     asm volatile(
                         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
                         "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
@@ -1858,18 +1885,26 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
                           "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
                         : "r"(taddr));
                     asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    if (my_row >= 0) {
+                    if (my_row >= 0 && !(P.dbg & 1)) {
+                        // top-2 of the 32 columns as a 5-level merge tree (order-free
+                        // under the tie rule), then into the running top-2
+                        const int jb = pass * DN_N + cb * 32;
+                        Top2 t[16];
 #pragma unroll
-                        for (int q = 0; q < 32; ++q) {
-                            const int j = pass * DN_N + cb * 32 + q;
-                            if (j < P.k) {
-                                const float v = __uint_as_float(r[q]);
-                                top2_push(tp, v, j, inc);
-                                if (j == inc) s_inc = v;
-                                if (P.mode == SPKM_MODE_INIT_ELKAN)
-                                    P.u[(int64_t)my_row * P.ku + j] = store_upper((double)v + eps);
-                            }
+                        for (int q = 0; q < 16; ++q) {
+                            const int j0 = jb + 2 * q, j1 = j0 + 1;
+                            const float v0 = j0 < P.k ? __uint_as_float(r[2 * q]) : -INFINITY;
+                            const float v1 = j1 < P.k ? __uint_as_float(r[2 * q + 1]) : -INFINITY;
+                            t[q] = better(v1, j1, v0, j0, inc) ? Top2{v1, j1, v0} : Top2{v0, j0, v1};
                         }
+#pragma unroll
+                        for (int h = 8; h >= 1; h >>= 1)
+#pragma unroll
+                            for (int q = 0; q < h; ++q) top2_merge(t[q], t[q + h], inc);
+                        top2_merge(tp, t[0], inc);
+#pragma unroll
+                        for (int q = 0; q < 32; ++q)
+                            if (jb + q == inc) s_inc = __uint_as_float(r[q]);
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
@@ -1934,26 +1969,29 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(DenseArgs P) {
     if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * DN_N) : "memory");
 }
 
-__global__ void k_split_tf32(const float *__restrict__ x, int64_t count, float *hi, float *lo) {
-    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < count; e += (int64_t)gridDim.x * blockDim.x) {
-        const float v = x[e];
-        const uint32_t h = to_tf32(v);
-        hi[e] = __uint_as_float(h);
-        lo[e] = __uint_as_float(to_tf32(v - __uint_as_float(h)));
-    }
-}
 
-// centers (float64, [k][D]) -> tf32 hi/lo rows padded with zeros to kpad
-__global__ void k_dense_centers(int64_t k, int64_t kpad, int64_t D, const double *__restrict__ C, float *hi,
-                                float *lo, const long long *__restrict__ ctl) {
+// centers (float64, [k][D]) -> float32 rows padded with zeros to kpad; the
+// dense pass splits them into tf32 hi + lo on the fly
+__global__ void k_dense_centers(int64_t k, int64_t kpad, int64_t D, const double *__restrict__ C, float *b,
+                                const long long *__restrict__ ctl) {
     if (ctl[1]) return;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < kpad * D;
          e += (int64_t)gridDim.x * blockDim.x) {
         const int64_t j = e / D;
-        const double v = j < k ? C[e] : 0.0;
-        const uint32_t h = to_tf32((float)v);
-        hi[e] = __uint_as_float(h);
-        lo[e] = __uint_as_float(to_tf32((float)(v - (double)__uint_as_float(h))));
+        b[e] = j < k ? (float)C[e] : 0.f;
+    }
+}
+
+// survivors' float32 rows -> a contiguous block (slot order) for the dense rescan
+__global__ void k_gather_rows(const float *__restrict__ x, int64_t D, const int32_t *__restrict__ list,
+                              const long long *__restrict__ count, float *out, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;
+    const int64_t per = D / 4, tot = *count * per;
+    const float4 *src = reinterpret_cast<const float4 *>(x);
+    float4 *dst = reinterpret_cast<float4 *>(out);
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < tot; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t slot = e / per, c = e - slot * per;
+        dst[e] = __ldg(src + (int64_t)list[slot] * per + c);
     }
 }
 
@@ -2269,6 +2307,31 @@ __global__ void __launch_bounds__(256) k_apply_move_slots(const int32_t *__restr
     }
 }
 
+
+// TMA descriptor of a row-major float32 [rows][D] operand: box = one stage
+// (16 dims = 64 bytes) x box_rows rows, 64-byte swizzle (the K-major
+// SWIZZLE_64B layout tcgen05 reads), zero fill past the last row.
+// cuTensorMapEncodeTiled comes from the driver entry point.
+int encode_dense_map(CUtensorMap *map, const float *base, int64_t rows, int64_t D, int box_rows) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail_msg("cuTensorMapEncodeTiled unavailable");
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)D, (cuuint64_t)(rows > 0 ? rows : 1)};
+    const cuuint64_t strides[1] = {(cuuint64_t)D * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)DN_KC, (cuuint32_t)box_rows};   // one stage: 64-byte rows
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail_msg("cuTensorMapEncodeTiled failed");
+    return 0;
+}
+
 #include "seed.cuh"
 
 }  // namespace
@@ -2518,16 +2581,9 @@ int spkm_predict(const spkm_csr *X, const spkm_centers *C, int32_t *a, double *b
 }
 
 
-int spkm_dense_split(const float *x, int64_t count, float *hi, float *lo, void *stream) {
-    if (count == 0) return 0;
-    k_split_tf32<<<grid_for(count, 256), 256, 0, S(stream)>>>(x, count, hi, lo);
-    CHECK_LAUNCH("dense_split");
-    return 0;
-}
-
 int spkm_dense_centers(const spkm_centers *C, const spkm_dense *Dn, void *stream) {
     k_dense_centers<<<grid_for(Dn->kpad * Dn->D, 256), 256, 0, S(stream)>>>(C->k, Dn->kpad, Dn->D, C->cent64,
-                                                                           Dn->bhi, Dn->blo, C->ctl);
+                                                                           Dn->b, C->ctl);
     CHECK_LAUNCH("dense_centers");
     return 0;
 }
@@ -2537,16 +2593,13 @@ int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense
     if (X->n == 0) return 0;
     if (Dn->D % 32 != 0) return fail_msg("dense dimension must be a multiple of 32");
     if (Dn->kpad % DN_N != 0 || Dn->kpad < C->k) return fail_msg("dense kpad must cover k in multiples of 256");
+    cudaStream_t st = S(stream);
     DenseArgs P{};
     P.n = X->n;
     P.D = Dn->D;
     P.k = C->k;
     P.kpad = Dn->kpad;
     P.ku = B ? B->ku : 1;
-    P.xhi = Dn->xhi;
-    P.xlo = Dn->xlo;
-    P.bhi = Dn->bhi;
-    P.blo = Dn->blo;
     P.reps = X->row_eps;
     P.mode = mode;
     P.use_s = use_s;
@@ -2563,9 +2616,28 @@ int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense
     }
     P.best = best;
     P.second = second;
+    const float *rows = Dn->x;
     if (mode == DMODE_RESCAN_H) {
-        P.rowlist = W->surv1;
+        // survivors are compacted into a contiguous float32 block so the
+        // pass streams them with TMA exactly like a full pass
+        if (!Dn->xs) return fail_msg("dense rescan needs the survivor scratch (spkm_dense.xs)");
+        P.rowmap = W->surv1;
         P.rowcount = W->ctr + SPKM_CTR_SURV1;
+        k_gather_rows<<<grid_for(X->n * (Dn->D / 4), 256), 256, 0, st>>>(Dn->x, Dn->D, W->surv1, P.rowcount, Dn->xs,
+                                                                          C->ctl);
+        CHECK_LAUNCH("dense_gather");
+        rows = Dn->xs;
+    }
+    int rc = encode_dense_map(&P.tm_x, rows, X->n, Dn->D, DN_M);
+    if (!rc) rc = encode_dense_map(&P.tm_b, Dn->b, Dn->kpad, Dn->D, DN_N);
+    if (rc) return rc;
+    {
+        static int dbg = -1;
+        if (dbg < 0) {
+            const char *e = getenv("SPKM_DN_DBG");
+            dbg = e ? atoi(e) : 0;
+        }
+        P.dbg = dbg;
     }
     const size_t smem = (size_t)DN_STAGES * DN_STAGE;
     static bool attr = false;
@@ -2576,7 +2648,7 @@ int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense
     int64_t tiles = (X->n + DN_M - 1) / DN_M;
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     if (grid < 1) grid = 1;
-    k_dense_pass<<<grid, DN_THREADS, smem, S(stream)>>>(P);
+    k_dense_pass<<<grid, DN_THREADS, smem, st>>>(P);
     CHECK_LAUNCH("dense_pass");
     return 0;
 }

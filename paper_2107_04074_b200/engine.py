@@ -185,7 +185,7 @@ def row_eps(lengths: np.ndarray) -> np.ndarray:
 
 
 def row_eps_dense(D: int, n: int) -> np.ndarray:
-    e = (3.0 * D / 8.0 + 8.0) * 2.0 ** -22 + 1e-6
+    e = (3.0 * D / 8.0 + 8.0) * 2.0 ** -22 + 4e-6
     f = np.float32(e)
     if float(f) < e:
         f = np.nextafter(f, np.float32(np.inf))
@@ -260,9 +260,6 @@ class DeviceCorpus:
             # float64 rows in device order (seeding); dense corpora skip it
             self.values64 = (torch.empty(max(self.nnz, 1), dtype=torch.float64, device=self.device)
                              if self.dense_dim is None else None)
-            if self.dense_dim is not None:
-                self.xhi = torch.empty(max(self.nnz, 1), **f32)
-                self.xlo = torch.empty_like(self.xhi)
             self._device_prepare(data)
         self.struct = CSR(self.n, self.d, self.nnz, _ptr(self.indptr), _ptr(self.indices), _ptr(self.values),
                           _ptr(self.reps))
@@ -330,9 +327,8 @@ class DeviceCorpus:
                   None if dense else _ptr(self.reps), sp)
         if dense:
             # tensor-core path: every similarity is the 3xTF32 tcgen05 value
-            # with error <= (3D/8 + 8) 2^-22 + 1e-6 (spkm.cu, dense rows)
+            # with error <= (3D/8 + 8) 2^-22 + 4e-6 (spkm.cu, dense rows)
             self.reps.fill_(float(row_eps_dense(self.dense_dim, 1)[0]))
-            _lib.call("spkm_dense_split", _ptr(self.values), self.nnz, _ptr(self.xhi), _ptr(self.xlo), sp)
         self.perm_dev = perm
         self.row_perm = perm.cpu().numpy()
         self.row_pos = np.empty_like(self.row_perm)
@@ -451,16 +447,16 @@ class CenterState:
         _lib.call("spkm_load_centers", self.struct, _ptr(src), stream)
         return src  # keep alive until the stream passes
 
-    def attach_dense(self, corpus: "DeviceCorpus", row0: int = 0):
-        """tf32 hi/lo center rows (padded to 256) for the dense tensor-core pass
-        (rows from device row ``row0`` on: a multi-GPU shard)."""
+    def attach_dense(self, corpus: "DeviceCorpus", row0: int = 0, n_rows: int = 0, rescan: bool = False):
+        """float32 center rows (padded to 256) for the dense tensor-core pass
+        (rows from device row ``row0`` on: a multi-GPU shard), and the
+        survivor scratch of the Hamerly rescan."""
         D = corpus.dense_dim
         kpad = (self.k + 255) // 256 * 256
-        self.bhi = torch.zeros(kpad * D, dtype=torch.float32, device=self.cent64.device)
-        self.blo = torch.zeros_like(self.bhi)
-        off = 4 * D * row0
-        self.dense = _lib.Dense(D, kpad, _ptr(corpus.xhi) + off, _ptr(corpus.xlo) + off, _ptr(self.bhi),
-                                _ptr(self.blo))
+        dev = self.cent64.device
+        self.b32 = torch.zeros(kpad * D, dtype=torch.float32, device=dev)
+        self.xs = torch.empty(max(n_rows, 1) * D, dtype=torch.float32, device=dev) if rescan else None
+        self.dense = _lib.Dense(D, kpad, _ptr(corpus.values) + 4 * D * row0, _ptr(self.b32), _ptr(self.xs))
 
     def refresh_dense(self, stream):
         if self.dense is not None:
@@ -575,7 +571,7 @@ class Engine:
             if self.elkan:
                 raise ConfigError("the Elkan family is not available for dense corpora in this build "
                                   "(standard, hamerly and simp_hamerly are)")
-            self.C.attach_dense(self.corpus, row0=self.p0)
+            self.C.attach_dense(self.corpus, row0=self.p0, n_rows=self.n_loc, rescan=self.hamerly)
         self.P = PointState(self.n_loc, k, variant, self.device)
         self.a_global = torch.zeros(max(cs.n, 1), dtype=torch.int32, device=self.device) if comm is not None else None
         # a dedicated stream: steady-state iterations are replayed as one CUDA graph

@@ -1606,13 +1606,18 @@ __global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s, con
 // Config C5 (dense unit vectors): every similarity of the dense corpus is
 // computed by this tensor-core pass, so all variants share one canonical
 // value (the 3xTF32 tcgen05 result) and pruned == Lloyd holds exactly.
-//   * x = hi + lo, c = hi + lo (tf32 parts) prepared once (rows at upload,
-//     centers after every move), so staging is pure 16-byte cp.async copies
-//     into K-major no-swizzle core matrices;
+//   * rows (float32, [n][D]; Hamerly survivors first compacted into a
+//     contiguous block) and centers (float32, [kpad][D]) are streamed by TMA
+//     in stages of 16 dims (64-byte rows, 64-byte swizzle = the K-major
+//     SWIZZLE_64B layout tcgen05 reads); one thread issues 2 box loads per
+//     stage;
+//   * warp roles (384 threads): w0 issues the MMAs, w1 the TMA loads, w2-7
+//     write the lo parts, w8-11 run the epilogue (thread = row);
 //   * CTA = 128 rows (TMEM lanes) x 256 centers (TMEM columns) per pass,
-//     ceil(k/256) passes, D/32 double-buffered stages of 32 dims, 3 MMAs per
-//     8-dim group (lo.hi, hi.lo, hi.hi); thread = row in the epilogue, which
-//     keeps a running top-2 (tie rule) and the incumbent's value;
+//     ceil(k/256) passes into two TMEM accumulators (the epilogue of one pass
+//     overlaps the MMAs of the next), 4 stages in flight, 3 MMAs per 8-dim
+//     group (lo.hi, hi.lo, hi.hi); the epilogue folds each 32-column TMEM
+//     load into a running top-2 (tie rule) with a 5-level merge tree;
 //   * split: hi = the float32 word read as tf32 (the tensor core truncates to
 //     tf32), lo = x - trunc_tf32(x) (exact), truncated again by the MMA; the
 //     residual of each operand is below 2^-20 |x|;
@@ -1627,26 +1632,14 @@ constexpr int DN_STAGES = 4;                      // stages: raw float32 (= tf32
 constexpr int DN_THREADS = 384;                   // w0 MMA, w1 TMA, w2-7 converters, w8-11 epilogue
 constexpr int DN_CONV = 192;                      // converter threads
 // K-major no-swizzle core matrices, unpadded so that a TMA box of 4 dims x
-constexpr int DN_LBO_A = (DN_M / 8) * 128;
-constexpr int DN_GRP_A = 2 * DN_LBO_A;
-constexpr int DN_LBO_B = (DN_N / 8) * 128;
-constexpr int DN_GRP_B = 2 * DN_LBO_B;
-constexpr int DN_OPA = (DN_KC / 8) * DN_GRP_A;    // one stage, one part (hi or lo) of A
-constexpr int DN_OPB = (DN_KC / 8) * DN_GRP_B;
+constexpr int DN_OPA = DN_M * DN_KC * 4;          // one stage, one part (float32 or lo) of A: 64-byte rows
+constexpr int DN_OPB = DN_N * DN_KC * 4;
 constexpr int DN_RAWST = DN_OPA + DN_OPB;          // float32 A, B of one stage (TMA); read as the hi operand
 constexpr int DN_STAGE = 2 * DN_RAWST;             // + the lo parts written by the converters
 constexpr uint32_t kDenseIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(DN_N >> 3) << 17) |
                                  ((uint32_t)(DN_M >> 4) << 24);
 enum { DMODE_RESCAN_H = 6 };
 
-__device__ __forceinline__ uint64_t umma_desc2(uint32_t saddr, uint32_t lbo) {
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((128 >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;
-    return d;
-}
 // SmemDescriptor for K-major SWIZZLE_64B operands: rows of 64 bytes, 8-row
 // atoms 512 bytes apart (SBO), LBO unused (1), layout type 4 at bits [61,64)
 __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
@@ -1658,10 +1651,6 @@ __device__ __forceinline__ uint64_t umma_desc_sw64(uint32_t saddr) {
     d |= (uint64_t)4 << 61;
     return d;
 }
-__device__ __forceinline__ void cp_async16(uint32_t dst, const void *src, bool pred) {
-    const int sz = pred ? 16 : 0;   // src-size 0 -> zero fill
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(sz) : "memory");
-}
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;\n" ::"r"(smem_u32(bar)), "r"(count) : "memory");
 }
@@ -1669,14 +1658,6 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
     asm volatile("{\n .reg .b64 st;\n mbarrier.arrive.shared::cta.b64 st, [%0];\n}\n" ::"r"(smem_u32(bar)) : "memory");
 }
 
-// x -> (tf32 hi, tf32 lo) of 4 values (cvt.rna, lo = tf32(x - hi)), 16-byte stores
-__device__ __forceinline__ void split_store(float4 v, uint8_t *hi, uint8_t *lo) {
-    const uint32_t h0 = to_tf32(v.x), h1 = to_tf32(v.y), h2 = to_tf32(v.z), h3 = to_tf32(v.w);
-    *reinterpret_cast<uint4 *>(hi) = make_uint4(h0, h1, h2, h3);
-    *reinterpret_cast<uint4 *>(lo) =
-        make_uint4(to_tf32(v.x - __uint_as_float(h0)), to_tf32(v.y - __uint_as_float(h1)),
-                   to_tf32(v.z - __uint_as_float(h2)), to_tf32(v.w - __uint_as_float(h3)));
-}
 
 struct DenseArgs {
     CUtensorMap tm_x, tm_b;          // TMA maps: rows [rows][D] and centers [kpad][D], float32

@@ -185,9 +185,20 @@ __device__ __forceinline__ void warp_append(bool pred, int32_t v0, int32_t *list
     }
 }
 
-__device__ __forceinline__ void warp_add(long long *ctr, long long v) {
+// Block-level counter accumulation: warps add into shared memory and each
+// CTA adds its totals to the 8 global counters once at the end (thousands of
+// warps adding to one global address serialise at its L2 slice).
+__device__ __forceinline__ void ctr_init(unsigned long long *s) {
+    if (threadIdx.x < 8) s[threadIdx.x] = 0ull;
+    __syncthreads();
+}
+__device__ __forceinline__ void ctr_add(unsigned long long *s, int slot, long long v) {
     for (int o = 16; o; o >>= 1) v += __shfl_down_sync(FULL, v, o);
-    if ((threadIdx.x & 31) == 0 && v) atomicAdd((unsigned long long *)ctr, (unsigned long long)v);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(s + slot, (unsigned long long)v);
+}
+__device__ __forceinline__ void ctr_flush(const unsigned long long *s, long long *ctr) {
+    __syncthreads();
+    if (threadIdx.x < 8 && s[threadIdx.x]) atomicAdd((unsigned long long *)(ctr + threadIdx.x), s[threadIdx.x]);
 }
 
 // ------------------------------------------------------------ full row pass
@@ -240,6 +251,8 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
         for (int64_t e = threadIdx.x; e < n4; e += blockDim.x) dst[e] = __ldg(src + e);
         __syncthreads();
     }
+    __shared__ unsigned long long s_ctr[8];
+    ctr_init(s_ctr);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane / A.tpr, q = lane - g * A.tpr;
     const bool lane_on = g < A.rpw;
@@ -368,11 +381,12 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
         if (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN) {
             warp_append(moved, (int32_t)row, A.mv_i, inc, A.mv_old, A.ctr + SPKM_CTR_MOVES);
             if (A.mode == MODE_RESCAN) {
-                warp_add(A.ctr + SPKM_CTR_SIMS, leader ? (long long)(A.k - 1) : 0);
-                warp_add(A.ctr + SPKM_CTR_NNZ_RESCAN, leader ? (long long)(e - s) : 0);
+                ctr_add(s_ctr, SPKM_CTR_SIMS, leader ? (long long)(A.k - 1) : 0);
+                ctr_add(s_ctr, SPKM_CTR_NNZ_RESCAN, leader ? (long long)(e - s) : 0);
             }
         }
     }
+    if (A.ctr) ctr_flush(s_ctr, A.ctr);
 }
 
 // --------------------------------------------------------- Hamerly family
@@ -444,6 +458,8 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ float s_v[8][4][32];
     __shared__ float s_c[8][4][32];
+    __shared__ unsigned long long s_ctr[8];
+    ctr_init(s_ctr);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane >> 3, q = lane & 7;
     float *sv = s_v[wib][g];
@@ -493,9 +509,10 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
             surv = !pruned;
         }
         warp_append(surv, i, surv2, 0, nullptr, ctr + SPKM_CTR_SURV2);
-        warp_add(ctr + SPKM_CTR_SIMS, (valid && q == 0) ? 1 : 0);
-        warp_add(ctr + SPKM_CTR_NNZ_TIGHTEN, (valid && q == 0) ? (long long)len : 0);
+        ctr_add(s_ctr, SPKM_CTR_SIMS, (valid && q == 0) ? 1 : 0);
+        ctr_add(s_ctr, SPKM_CTR_NNZ_TIGHTEN, (valid && q == 0) ? (long long)len : 0);
     }
+    ctr_flush(s_ctr, ctr);
 }
 
 // ----------------------------------------------------------- Elkan family
@@ -513,7 +530,30 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const int k4 = (k + 3) >> 2;   // u rows are ku (a multiple of 4) floats: 16-byte vectors
-    for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
+    // rounds of one point per warp, identical for every warp of the CTA, so
+    // each round's survivors are appended with ONE global atomic per CTA
+    __shared__ int32_t s_surv[32];
+    __shared__ long long s_base;
+    const int wib = threadIdx.x >> 5;
+    for (int64_t i0 = (int64_t)blockIdx.x * wpb; i0 < n; i0 += (int64_t)gridDim.x * wpb) {
+        const int64_t i = i0 + wib;
+        if (i >= n) {
+            if (lane == 0) s_surv[wib] = -1;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int c = 0;
+                for (int q = 0; q < wpb; ++q) c += s_surv[q] >= 0;
+                if (c) s_base = (long long)atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1), (unsigned long long)c);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                int c = 0;
+                for (int q = 0; q < wpb; ++q)
+                    if (s_surv[q] >= 0) surv1[s_base + c++] = s_surv[q];
+            }
+            __syncthreads();
+            continue;
+        }
         const int ai = a[i];
         const float lo = l[i];
         const double sa = sinp[ai];
@@ -556,10 +596,20 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
             if (changed) ui[q] = make_float4(w[0], w[1], w[2], w[3]);
         }
         any = __any_sync(FULL, any);
-        if (lane == 0 && any) {
-            const long long p = atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1), 1ull);
-            surv1[p] = (int32_t)i;
+        if (lane == 0) s_surv[wib] = any ? (int32_t)i : -1;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int c = 0;
+            for (int q = 0; q < wpb; ++q) c += s_surv[q] >= 0;
+            if (c) s_base = (long long)atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1), (unsigned long long)c);
         }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int c = 0;
+            for (int q = 0; q < wpb; ++q)
+                if (s_surv[q] >= 0) surv1[s_base + c++] = s_surv[q];
+        }
+        __syncthreads();
     }
 }
 
@@ -600,6 +650,8 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     constexpr int UB = 4;
     __shared__ int32_t s_idx[8][8][32];
     __shared__ float s_val[8][8][32];
+    __shared__ unsigned long long s_ctr[8];
+    ctr_init(s_ctr);
     extern __shared__ float s_sim_dyn[];   // [8 warps][sim_stride]
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int nb = (k + 7) >> 3;
@@ -815,10 +867,11 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
         }
         const bool leader = valid && q == 0;
         warp_append(leader && cur != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
-        warp_add(ctr + SPKM_CTR_SIMS, sims);
-        warp_add(ctr + SPKM_CTR_NNZ_ELKAN, leader ? (long long)len : 0);
+        ctr_add(s_ctr, SPKM_CTR_SIMS, sims);
+        ctr_add(s_ctr, SPKM_CTR_NNZ_ELKAN, leader ? (long long)len : 0);
         __syncwarp();
     }
+    ctr_flush(s_ctr, ctr);
 }
 
 // --------------------------------------------------------- center updates
@@ -856,6 +909,7 @@ __global__ void __launch_bounds__(256) k_apply_moves(int64_t d, const int64_t *_
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     const long long cnt = ctr[SPKM_CTR_MOVES];
+    long long nnz_moved = 0;   // one atomic per warp at the end
     for (int64_t w = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); w < cnt; w += (int64_t)gridDim.x * wpb) {
         const int32_t i = mv_i[w];
         const int o = mv_old[w], nw = a[i];
@@ -870,11 +924,12 @@ __global__ void __launch_bounds__(256) k_apply_moves(int64_t d, const int64_t *_
         if (lane == 0) {
             atomicAdd((unsigned long long *)(counts + o), (unsigned long long)(-1ll));
             atomicAdd((unsigned long long *)(counts + nw), 1ull);
-            atomicAdd((unsigned long long *)(ctr + SPKM_CTR_NNZ_MOVED), (unsigned long long)(indptr[i + 1] - indptr[i]));
             touched[o] = 1;
             touched[nw] = 1;
         }
+        nnz_moved += indptr[i + 1] - indptr[i];
     }
+    if (lane == 0 && nnz_moved) atomicAdd((unsigned long long *)(ctr + SPKM_CTR_NNZ_MOVED), (unsigned long long)nnz_moved);
 }
 
 // Fixed-shape block sum (deterministic for a given blockDim).
@@ -1703,6 +1758,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_const
     // as tf32 = the hi parts, truncated) [A lo | B lo] (converters)
     __shared__ __align__(8) uint64_t full_b[DN_STAGES], lo_full[DN_STAGES], empty_b[DN_STAGES], accf[2], acce[2];
     __shared__ uint32_t tmem_base_s;
+    __shared__ unsigned long long s_ctr[8];
+    if (threadIdx.x < 8) s_ctr[threadIdx.x] = 0ull;   // made visible by the setup __syncthreads
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nrows = P.rowcount ? *P.rowcount : P.n;
     const int64_t ntiles = (nrows + DN_M - 1) / DN_M;
@@ -1940,13 +1997,15 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_const
                 warp_append(moved, my_row, P.mv_i, inc, P.mv_old, P.ctr + SPKM_CTR_MOVES);
             if (P.mode == DMODE_RESCAN_H) {
                 warp_append(surv, my_row, P.surv2, 0, nullptr, P.ctr + SPKM_CTR_SURV2);
-                warp_add(P.ctr + SPKM_CTR_SIMS, sims);
-                warp_add(P.ctr + SPKM_CTR_NNZ_RESCAN, my_row >= 0 ? P.D : 0);
+                ctr_add(s_ctr, SPKM_CTR_SIMS, sims);
+                ctr_add(s_ctr, SPKM_CTR_NNZ_RESCAN, my_row >= 0 ? P.D : 0);
             }
         }
     }
     asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
     __syncthreads();
+    if (threadIdx.x < 8 && s_ctr[threadIdx.x] && P.ctr)
+        atomicAdd((unsigned long long *)(P.ctr + threadIdx.x), s_ctr[threadIdx.x]);
     if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(2 * DN_N) : "memory");
 }
 

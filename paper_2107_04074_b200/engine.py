@@ -219,6 +219,33 @@ def term_order(data: Dataset):
     return data._term_order
 
 
+def _host_registered(arr: np.ndarray) -> np.ndarray:
+    """Page-lock a host array in place (cudaHostRegister) so H2D copies from it
+    are DMA transfers; unregistered when the array is garbage collected."""
+    import weakref
+    if getattr(arr, "base", None) is not None or not arr.flags.c_contiguous or arr.nbytes == 0:
+        return arr
+    key = arr.ctypes.data
+    if key in _REGISTERED:
+        return arr
+    cudart = torch.cuda.cudart()
+    if int(cudart.cudaHostRegister(key, arr.nbytes, 0)) != 0:
+        return arr                     # not registrable: the caller stages it
+    _REGISTERED.add(key)
+
+    def _release(ptr=key):
+        try:
+            torch.cuda.cudart().cudaHostUnregister(ptr)
+        except Exception:
+            pass
+        _REGISTERED.discard(ptr)
+    weakref.finalize(arr, _release)
+    return arr
+
+
+_REGISTERED: set = set()
+
+
 class DeviceCorpus:
     """A CSR (or row range of one) resident in HBM: int64 indptr, int32 indices, fp32 values.
 
@@ -292,10 +319,16 @@ class DeviceCorpus:
         dev = self.device
         stream = torch.cuda.current_stream(dev)
         sp = ctypes_void(stream.cuda_stream)
-        ip_h = torch.from_numpy(np.asarray(data.indptr[r0:r1 + 1], dtype=np.int64) - s)
-        idx_h = torch.from_numpy(np.ascontiguousarray(data.indices[s:e], dtype=np.int32))
-        val_h = torch.from_numpy(np.ascontiguousarray(data.data[s:e], dtype=np.float64))
-        if self.pinned_host:
+        if self.pinned_host and (r0, r1) == (0, data.n):
+            # the whole corpus: page-lock the Dataset's own arrays once and copy
+            # straight from them (no staging copy on the host)
+            ip_h, idx_h, val_h = (torch.from_numpy(_host_registered(a))
+                                  for a in (data.indptr, data.indices, data.data))
+        else:
+            ip_h = torch.from_numpy(np.asarray(data.indptr[r0:r1 + 1], dtype=np.int64) - s)
+            idx_h = torch.from_numpy(np.ascontiguousarray(data.indices[s:e], dtype=np.int32))
+            val_h = torch.from_numpy(np.ascontiguousarray(data.data[s:e], dtype=np.float64))
+        if self.pinned_host and not ip_h.is_pinned():
             if self._stage is None:
                 self._stage = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (ip_h, idx_h, val_h)]
             for dst, src in zip(self._stage, (ip_h, idx_h, val_h)):

@@ -1486,20 +1486,15 @@ __global__ void __launch_bounds__(kGramThreads, 1) k_gram_tc(int64_t k, int64_t 
     // layout: [stage 0: Ahi Alo Bhi Blo][stage 1: ...][2 mbarriers][tmem addr]
     __shared__ __align__(8) uint64_t bars[2];
     __shared__ uint32_t tmem_base_s;
-    __shared__ int need;
     const int2 tl = tiles[blockIdx.x];
     const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
     const bool diag = tl.x == tl.y;
-    if (threadIdx.x == 0) {
-        int nd = full;
-        for (int q = 0; q < GT && !nd; ++q) {
-            if (a0 + q < k && sinp[a0 + q] != 0.0) nd = 1;
-            if (j0 + q < k && sinp[j0 + q] != 0.0) nd = 1;
-        }
-        need = nd;
+    int mine = full;   // the tile is recomputed if any of its clusters moved
+    if (!mine && threadIdx.x < GT) {
+        const int64_t q = threadIdx.x;
+        mine = (a0 + q < k && sinp[a0 + q] != 0.0) || (j0 + q < k && sinp[j0 + q] != 0.0);
     }
-    __syncthreads();
-    if (!need) return;
+    if (!__syncthreads_or(mine)) return;
     const int64_t per = ((d + dsplit - 1) / dsplit + GKC - 1) / GKC * GKC;
     const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;

@@ -1661,8 +1661,9 @@ __global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s, con
 //     in stages of 16 dims (64-byte rows, 64-byte swizzle = the K-major
 //     SWIZZLE_64B layout tcgen05 reads); one thread issues 2 box loads per
 //     stage;
-//   * warp roles (384 threads): w0 issues the MMAs, w1 the TMA loads, w2-7
-//     write the lo parts, w8-11 run the epilogue (thread = row);
+//   * warp roles (512 threads): w0 issues the MMAs, w1 the TMA loads, w2-7
+//     write the lo parts, w8-15 run the epilogue (thread = row, two warps
+//     per TMEM lane quarter, each folding half of every pass's columns);
 //   * CTA = 128 rows (TMEM lanes) x 256 centers (TMEM columns) per pass,
 //     ceil(k/256) passes into two TMEM accumulators (the epilogue of one pass
 //     overlaps the MMAs of the next), 4 stages in flight, 3 MMAs per 8-dim
@@ -1679,7 +1680,7 @@ constexpr int DN_M = 128;                         // rows per tile (TMEM lanes)
 constexpr int DN_N = 256;                         // centers per pass (TMEM columns per accumulator)
 constexpr int DN_KC = 16;                         // dims per pipeline stage
 constexpr int DN_STAGES = 4;                      // stages: raw float32 (= tf32 hi operand) + lo
-constexpr int DN_THREADS = 384;                   // w0 MMA, w1 TMA, w2-7 converters, w8-11 epilogue
+constexpr int DN_THREADS = 512;                   // w0 MMA, w1 TMA, w2-7 converters, w8-15 epilogue
 constexpr int DN_CONV = 192;                      // converter threads
 // K-major no-swizzle core matrices, unpadded so that a TMA box of 4 dims x
 constexpr int DN_OPA = DN_M * DN_KC * 4;          // one stage, one part (float32 or lo) of A: 64-byte rows
@@ -1754,6 +1755,8 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_const
     __shared__ __align__(8) uint64_t full_b[DN_STAGES], lo_full[DN_STAGES], empty_b[DN_STAGES], accf[2], acce[2];
     __shared__ uint32_t tmem_base_s;
     __shared__ unsigned long long s_ctr[8];
+    __shared__ float4 s_ep[DN_M];   // epilogue: the second half's top-2 (and incumbent value) per row
+    __shared__ int s_epf[DN_M];
     if (threadIdx.x < 8) s_ctr[threadIdx.x] = 0ull;   // made visible by the setup __syncthreads
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nrows = P.rowcount ? *P.rowcount : P.n;
@@ -1774,7 +1777,7 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_const
         }
         for (int b = 0; b < 2; ++b) {
             mbar_init(&accf[b], 1);
-            mbar_init(&acce[b], 128);
+            mbar_init(&acce[b], 256);
         }
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
     }
@@ -1889,60 +1892,83 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_const
         }
         __syncwarp();
     } else if (w >= 8) {
-        // ---------------- epilogue: thread = row (TMEM lane quarter w % 4)
-        const int m = (w - 8) * 32 + lane;
+        // ---------------- epilogue: thread = row; two warps per TMEM lane
+        // quarter (w % 4), half hf folds columns [128 hf, 128 hf + 128) of
+        // every 256-column pass; the halves merge once per tile in smem
+        const int qd = w & 3, hf = (w - 8) >> 2;
+        const int m = qd * 32 + lane;
         uint32_t pcount = 0;
         for (int64_t ti = 0; ti < my_tiles; ++ti) {
             const int64_t tile = blockIdx.x + ti * gridDim.x;
             const int64_t slot = tile * DN_M + m;
             const int32_t my_row = slot < nrows ? (P.rowmap ? P.rowmap[slot] : (int32_t)slot) : -1;
             const int inc = (my_row >= 0 && (P.mode == SPKM_MODE_LLOYD || P.mode == DMODE_RESCAN_H)) ? P.a[my_row] : -1;
-            const double eps = my_row >= 0 ? (double)P.reps[my_row] : 0.0;
             Top2 tp{-INFINITY, -2, -INFINITY};
             float s_inc = 0.f;
+            int has_inc = 0;
             for (int pass = 0; pass < npass; ++pass, ++pcount) {
                 const int b = pcount & 1;
                 mbar_wait(smem_u32(&accf[b]), (pcount >> 1) & 1);
                 asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
 #pragma unroll 1
-                for (int cb = 0; cb < DN_N / 32; ++cb) {
-                    uint32_t r[32];
-                    const uint32_t taddr = tmem + ((uint32_t)((w - 8) * 32) << 16) + (uint32_t)(b * DN_N + cb * 32);
-                    asm volatile(
-                        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
-                        "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-                        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-                          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-                          "=r"(r[14]), "=r"(r[15]), "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]),
-                          "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]), "=r"(r[25]),
-                          "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-                        : "r"(taddr));
-                    asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-                    if (my_row >= 0 && !(P.dbg & 1)) {
-                        // top-2 of the 32 columns as a 5-level merge tree (order-free
-                        // under the tie rule), then into the running top-2
-                        const int jb = pass * DN_N + cb * 32;
-                        Top2 t[16];
+                for (int cb = 0; cb < DN_N / 32 / 2; ++cb) {
+                    uint32_t r[16];
+                    const int col0 = hf * (DN_N / 2) + cb * 32;
 #pragma unroll
-                        for (int q = 0; q < 16; ++q) {
-                            const int j0 = jb + 2 * q, j1 = j0 + 1;
-                            const float v0 = j0 < P.k ? __uint_as_float(r[2 * q]) : -INFINITY;
-                            const float v1 = j1 < P.k ? __uint_as_float(r[2 * q + 1]) : -INFINITY;
-                            t[q] = better(v1, j1, v0, j0, inc) ? Top2{v1, j1, v0} : Top2{v0, j0, v1};
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const uint32_t taddr = tmem + ((uint32_t)(qd * 32) << 16) + (uint32_t)(b * DN_N + col0 + 16 * hh);
+                        asm volatile(
+                            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+                            "%15}, [%16];\n"
+                            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+                              "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+                              "=r"(r[14]), "=r"(r[15])
+                            : "r"(taddr));
+                        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+                        if (my_row >= 0 && !(P.dbg & 1)) {
+                            // top-2 of 16 columns as a 4-level merge tree (order-free under
+                            // the tie rule), then into the running top-2
+                            const int jb = pass * DN_N + col0 + 16 * hh;
+                            Top2 t[8];
+#pragma unroll
+                            for (int q = 0; q < 8; ++q) {
+                                const int j0 = jb + 2 * q, j1 = j0 + 1;
+                                const float v0 = j0 < P.k ? __uint_as_float(r[2 * q]) : -INFINITY;
+                                const float v1 = j1 < P.k ? __uint_as_float(r[2 * q + 1]) : -INFINITY;
+                                t[q] = better(v1, j1, v0, j0, inc) ? Top2{v1, j1, v0} : Top2{v0, j0, v1};
+                            }
+#pragma unroll
+                            for (int h = 4; h >= 1; h >>= 1)
+#pragma unroll
+                                for (int q = 0; q < h; ++q) top2_merge(t[q], t[q + h], inc);
+                            top2_merge(tp, t[0], inc);
+#pragma unroll
+                            for (int q = 0; q < 16; ++q)
+                                if (jb + q == inc) {
+                                    s_inc = __uint_as_float(r[q]);
+                                    has_inc = 1;
+                                }
                         }
-#pragma unroll
-                        for (int h = 8; h >= 1; h >>= 1)
-#pragma unroll
-                            for (int q = 0; q < h; ++q) top2_merge(t[q], t[q + h], inc);
-                        top2_merge(tp, t[0], inc);
-#pragma unroll
-                        for (int q = 0; q < 32; ++q)
-                            if (jb + q == inc) s_inc = __uint_as_float(r[q]);
                     }
                 }
                 asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
                 mbar_arrive(&acce[b]);
             }
+            // merge the two halves of the row: hf 1 hands its top-2 to hf 0
+            if (hf == 1) {
+                s_ep[m] = make_float4(tp.b, __int_as_float(tp.bj), tp.s, has_inc ? s_inc : -INFINITY);
+                s_epf[m] = has_inc;
+            }
+            asm volatile("bar.sync %0, 64;\n" ::"r"(1 + qd) : "memory");
+            if (hf == 0) {
+                const float4 o4 = s_ep[m];
+                const Top2 o{o4.x, __float_as_int(o4.y), o4.z};
+                top2_merge(tp, o, inc);
+                if (s_epf[m]) s_inc = o4.w;
+            }
+            asm volatile("bar.sync %0, 64;\n" ::"r"(1 + qd) : "memory");
+            if (hf == 1) continue;
+            const double eps = my_row >= 0 ? (double)P.reps[my_row] : 0.0;
             bool moved = false, surv = false;
             long long sims = 0;
             if (my_row >= 0) {

@@ -223,7 +223,7 @@ def _host_registered(arr: np.ndarray) -> np.ndarray:
     """Page-lock a host array in place (cudaHostRegister) so H2D copies from it
     are DMA transfers; unregistered when the array is garbage collected."""
     import weakref
-    if getattr(arr, "base", None) is not None or not arr.flags.c_contiguous or arr.nbytes == 0:
+    if not arr.flags.c_contiguous or arr.nbytes == 0:
         return arr
     key = arr.ctypes.data
     if key in _REGISTERED:
@@ -328,12 +328,18 @@ class DeviceCorpus:
             ip_h = torch.from_numpy(np.asarray(data.indptr[r0:r1 + 1], dtype=np.int64) - s)
             idx_h = torch.from_numpy(np.ascontiguousarray(data.indices[s:e], dtype=np.int32))
             val_h = torch.from_numpy(np.ascontiguousarray(data.data[s:e], dtype=np.float64))
-        if self.pinned_host and not ip_h.is_pinned():
+        if self.pinned_host:
+            # anything not page-locked in place goes through persistent pinned staging
+            hs = [ip_h, idx_h, val_h]
             if self._stage is None:
-                self._stage = [torch.empty(t.shape, dtype=t.dtype).pin_memory() for t in (ip_h, idx_h, val_h)]
-            for dst, src in zip(self._stage, (ip_h, idx_h, val_h)):
-                dst.copy_(src)
-            ip_h, idx_h, val_h = self._stage
+                self._stage = [None, None, None]
+            for q, t in enumerate(hs):
+                if not t.is_pinned():
+                    if self._stage[q] is None or self._stage[q].shape != t.shape:
+                        self._stage[q] = torch.empty(t.shape, dtype=t.dtype).pin_memory()
+                    self._stage[q].copy_(t)
+                    hs[q] = self._stage[q]
+            ip_h, idx_h, val_h = hs
         ip_raw = ip_h.to(dev, non_blocking=True)
         idx_raw = idx_h.to(dev, non_blocking=True)
         val_raw = val_h.to(dev, non_blocking=True)

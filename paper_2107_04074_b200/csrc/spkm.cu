@@ -2031,6 +2031,156 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_const
 }
 
 
+// Single-tile Gram (k <= 128), warp specialised: one thread streams the
+// term-major float32 centers (ct32: each CTA's d-range is one contiguous
+// block) with TMA, 4 stages of 32 terms x 128 centers in flight; six
+// converter warps transpose them into K-major tf32 hi / lo core matrices;
+// one thread issues the MMAs; the TMEM tile goes to the split's partial Gram.
+constexpr int GW_RAW = 4;
+constexpr int GW_THREADS = 256;
+constexpr int GW_CONV = 192;
+constexpr int GW_RAWST = GT * GKC * 4;            // 16 KB: 32 terms x 128 centers, float32
+
+__global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant__ CUtensorMap tm, int64_t k, int64_t d,
+                                                          int64_t dsplit, const double *__restrict__ sinp, int full,
+                                                          double *gpart, const long long *__restrict__ ctl) {
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    extern __shared__ __align__(1024) uint8_t gsm[];
+    __shared__ __align__(8) uint64_t raw_full[GW_RAW], raw_empty[GW_RAW], op_full[2], op_empty[2], done_b;
+    __shared__ uint32_t tmem_base_s;
+    int mine = full;   // recomputed only if some cluster moved
+    if (!mine && threadIdx.x < GT) mine = threadIdx.x < k && sinp[threadIdx.x] != 0.0;
+    if (!__syncthreads_or(mine)) return;
+    const int64_t per = ((d + dsplit - 1) / dsplit + GKC - 1) / GKC * GKC;
+    const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
+    const int nch = t1 > t0 ? (int)((t1 - t0 + GKC - 1) / GKC) : 0;
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (w == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_s)),
+                     "r"(GT)
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
+    }
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < GW_RAW; ++q) {
+            mbar_init(&raw_full[q], 1);
+            mbar_init(&raw_empty[q], GW_CONV);
+        }
+        for (int q = 0; q < 2; ++q) {
+            mbar_init(&op_full[q], GW_CONV);
+            mbar_init(&op_empty[q], 1);
+        }
+        mbar_init(&done_b, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+    const uint32_t tmem = tmem_base_s;
+    uint8_t *raw0 = gsm;
+    uint8_t *op0 = gsm + (size_t)GW_RAW * GW_RAWST;
+    auto raw_ptr = [&](int q) { return raw0 + (size_t)q * GW_RAWST; };
+    auto hi_ptr = [&](int o) { return op0 + (size_t)o * 2 * GOPB; };
+    if (w == 1) {
+        if (lane == 0) {
+            for (int c = 0; c < nch; ++c) {
+                const int r = c % GW_RAW;
+                if (c >= GW_RAW) mbar_wait(smem_u32(&raw_empty[r]), ((c / GW_RAW) - 1) & 1);
+                mbar_expect_tx(&raw_full[r], (uint32_t)GW_RAWST);
+                tma_load_2d(smem_u32(raw_ptr(r)), &tm, 0, (int)(t0 + (int64_t)c * GKC), smem_u32(&raw_full[r]));
+            }
+        }
+        __syncwarp();
+    } else if (w >= 2) {
+        const int ct = threadIdx.x - 64;
+        for (int c = 0; c < nch; ++c) {
+            const int r = c % GW_RAW, o = c & 1;
+            mbar_wait(smem_u32(&raw_full[r]), (c / GW_RAW) & 1);
+            if (c >= 2) mbar_wait(smem_u32(&op_empty[o]), ((c >> 1) - 1) & 1);
+            const float *rs = reinterpret_cast<const float *>(raw_ptr(r));   // [32 terms][128 centers]
+            uint8_t *hi = hi_ptr(o), *lo = hi + GOPB;
+            for (int e = ct; e < GT * (GKC / 4); e += GW_CONV) {
+                const int m = e & (GT - 1), q = e >> 7;   // consecutive threads: consecutive centers
+                uint32_t hh[4], ll[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const float v = rs[(4 * q + u) * GT + m];
+                    hh[u] = to_tf32(v);
+                    ll[u] = to_tf32(v - __uint_as_float(hh[u]));
+                }
+                const int off = (q >> 1) * GGRP + (q & 1) * GLBO + (m >> 3) * GSBO + (m & 7) * 16;
+                *reinterpret_cast<uint4 *>(hi + off) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
+                *reinterpret_cast<uint4 *>(lo + off) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            mbar_arrive(&op_full[o]);
+            mbar_arrive(&raw_empty[r]);
+        }
+    } else if (lane == 0) {   // w == 0: MMA issuer
+        for (int c = 0; c < nch; ++c) {
+            const int o = c & 1;
+            mbar_wait(smem_u32(&op_full[o]), (c >> 1) & 1);
+            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+            const uint32_t hi = smem_u32(hi_ptr(o)), lo = hi + GOPB;
+#pragma unroll
+            for (int g = 0; g < GKC / 8; ++g) {
+                const uint32_t off = g * GGRP;
+                const uint64_t dh = umma_desc(hi + off), dl = umma_desc(lo + off);
+                const uint32_t acc0 = (c > 0 || g > 0) ? 1u : 0u;
+                asm volatile(
+                    "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
+                    " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
+                    "l"(dl), "l"(dh), "r"(kGramIdesc), "r"(acc0)
+                    : "memory");
+                asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dh), "l"(dl),
+                             "r"(kGramIdesc)
+                             : "memory");
+                asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dh), "l"(dh),
+                             "r"(kGramIdesc)
+                             : "memory");
+            }
+            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                             smem_u32(&op_empty[o]))
+                         : "memory");
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
+                         smem_u32(&done_b))
+                     : "memory");
+    }
+    __syncwarp();
+    // epilogue: warps 0-3 read their TMEM lane quarters into the split's partial Gram
+    if (w < 4) {
+        if (nch > 0) mbar_wait(smem_u32(&done_b), 0);
+        asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
+        const int64_t row = w * 32 + lane;
+#pragma unroll 1
+        for (int cb = 0; cb < GT / 32; ++cb) {
+            uint32_t r[32];
+            const uint32_t taddr = tmem + ((uint32_t)(w * 32) << 16) + (uint32_t)(cb * 32);
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+                "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+                  "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+                  "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+                  "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+                : "r"(taddr));
+            asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
+            if (row < k) {
+                double *out = gpart + ((int64_t)blockIdx.y * k + row) * k;
+#pragma unroll
+                for (int q = 0; q < 32; ++q) {
+                    const int64_t col = cb * 32 + q;
+                    if (col < k) out[col] = nch > 0 ? (double)__uint_as_float(r[q]) : 0.0;
+                }
+            }
+        }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
+    __syncthreads();
+    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(GT) : "memory");
+}
+
 // centers (float64, [k][D]) -> float32 rows padded with zeros to kpad; the
 // dense pass splits them into tf32 hi + lo on the fly
 __global__ void k_dense_centers(int64_t k, int64_t kpad, int64_t D, const double *__restrict__ C, float *b,
@@ -2393,6 +2543,28 @@ int encode_dense_map(CUtensorMap *map, const float *base, int64_t rows, int64_t 
     return 0;
 }
 
+// TMA descriptor of the term-major float32 centers ct32 [d][kp]: box = one
+// Gram stage (128 centers x 32 terms), no swizzle, zero fill past kp and d.
+int encode_gram_map(CUtensorMap *map, const float *base, int64_t kp, int64_t d) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    if (!enc) {
+        void *fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess || !fn)
+            return fail_msg("cuTensorMapEncodeTiled unavailable");
+        enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }
+    const cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)d};
+    const cuuint64_t strides[1] = {(cuuint64_t)kp * 4};
+    const cuuint32_t box[2] = {(cuuint32_t)GT, (cuuint32_t)GKC};
+    const cuuint32_t estr[2] = {1, 1};
+    const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return fail_msg("cuTensorMapEncodeTiled (gram) failed");
+    return 0;
+}
+
 #include "seed.cuh"
 
 }  // namespace
@@ -2577,7 +2749,7 @@ int64_t spkm_gram_dsplit(int64_t k, int64_t d) {
     // at least 256 terms per CTA
     const int64_t tk = (k + GT - 1) / GT;
     const int64_t tiles = tk * (tk + 1) / 2;
-    const int64_t per_sm = (tk == 1) ? 2 : 1;
+    const int64_t per_sm = 1;
     int64_t ds = (int64_t)num_sms() * per_sm / tiles;
     const int64_t maxds = (d + 255) / 256;
     if (ds > maxds) ds = maxds;
@@ -2594,17 +2766,32 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     const int64_t ntiles = tk * (tk + 1) / 2;
     const int64_t ds = spkm_gram_dsplit(C->k, C->d);
     const int64_t per = ((C->d + ds - 1) / ds + GKC - 1) / GKC * GKC;
-    const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + 1e-6;
-    const int nbuf = (tk == 1) ? 2 : 4;
-    const size_t smem = (size_t)2 * nbuf * GOPB;
-    static bool attr_set = false;
-    if (!attr_set) {   // the largest configuration (4 buffers per stage)
-        cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * GOPB));
-        attr_set = true;
+    // (the single-tile path splits the float32 copy: + 2 x 2^-24 for its rounding)
+    const bool ws = tk == 1 && (C->kp * 4) % 16 == 0;
+    const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + (ws ? 2e-6 : 1e-6);
+    if (ws) {
+        CUtensorMap tm;
+        int rc = encode_gram_map(&tm, C->ct32, C->kp, C->d);
+        if (rc) return rc;
+        const size_t smem = (size_t)GW_RAW * GW_RAWST + (size_t)2 * 2 * GOPB;
+        static bool attr_ws = false;
+        if (!attr_ws) {
+            cudaFuncSetAttribute(k_gram_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            attr_ws = true;
+        }
+        k_gram_ws<<<dim3(1, (unsigned)ds), GW_THREADS, smem, st>>>(tm, C->k, C->d, ds, C->sinp, full, gpart, C->ctl);
+    } else {
+        const int nbuf = (tk == 1) ? 2 : 4;
+        const size_t smem = (size_t)2 * nbuf * GOPB;
+        static bool attr_set = false;
+        if (!attr_set) {   // the largest configuration (4 buffers per stage)
+            cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * GOPB));
+            attr_set = true;
+        }
+        dim3 grid((unsigned)ntiles, (unsigned)ds);
+        k_gram_tc<<<grid, kGramThreads, smem, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart, C->ctl,
+                                                    nbuf);
     }
-    dim3 grid((unsigned)ntiles, (unsigned)ds);
-    k_gram_tc<<<grid, kGramThreads, smem, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart, C->ctl,
-                                                nbuf);
     CHECK_LAUNCH("gram_tc");
     k_gram_final<<<(unsigned)((C->k * C->k * 8 + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, gdelta,
                                                                            C->cc, C->ctl);

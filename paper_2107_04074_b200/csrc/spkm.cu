@@ -2036,9 +2036,10 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_const
 // block) with TMA, 4 stages of 32 terms x 128 centers in flight; six
 // converter warps transpose them into K-major tf32 hi / lo core matrices;
 // one thread issues the MMAs; the TMEM tile goes to the split's partial Gram.
-constexpr int GW_RAW = 4;
-constexpr int GW_THREADS = 256;
-constexpr int GW_CONV = 192;
+constexpr int GW_RAW = 6;
+constexpr int GW_OPS = 3;
+constexpr int GW_THREADS = 384;
+constexpr int GW_CONV = 320;
 constexpr int GW_RAWST = GT * GKC * 4;            // 16 KB: 32 terms x 128 centers, float32
 
 __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant__ CUtensorMap tm, int64_t k, int64_t d,
@@ -2046,7 +2047,7 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
                                                           double *gpart, const long long *__restrict__ ctl) {
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     extern __shared__ __align__(1024) uint8_t gsm[];
-    __shared__ __align__(8) uint64_t raw_full[GW_RAW], raw_empty[GW_RAW], op_full[2], op_empty[2], done_b;
+    __shared__ __align__(8) uint64_t raw_full[GW_RAW], raw_empty[GW_RAW], op_full[GW_OPS], op_empty[GW_OPS], done_b;
     __shared__ uint32_t tmem_base_s;
     int mine = full;   // recomputed only if some cluster moved
     if (!mine && threadIdx.x < GT) mine = threadIdx.x < k && sinp[threadIdx.x] != 0.0;
@@ -2066,7 +2067,7 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
             mbar_init(&raw_full[q], 1);
             mbar_init(&raw_empty[q], GW_CONV);
         }
-        for (int q = 0; q < 2; ++q) {
+        for (int q = 0; q < GW_OPS; ++q) {
             mbar_init(&op_full[q], GW_CONV);
             mbar_init(&op_empty[q], 1);
         }
@@ -2094,9 +2095,9 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
     } else if (w >= 2) {
         const int ct = threadIdx.x - 64;
         for (int c = 0; c < nch; ++c) {
-            const int r = c % GW_RAW, o = c & 1;
+            const int r = c % GW_RAW, o = c % GW_OPS;
             mbar_wait(smem_u32(&raw_full[r]), (c / GW_RAW) & 1);
-            if (c >= 2) mbar_wait(smem_u32(&op_empty[o]), ((c >> 1) - 1) & 1);
+            if (c >= GW_OPS) mbar_wait(smem_u32(&op_empty[o]), ((c / GW_OPS) - 1) & 1);
             const float *rs = reinterpret_cast<const float *>(raw_ptr(r));   // [32 terms][128 centers]
             uint8_t *hi = hi_ptr(o), *lo = hi + GOPB;
             for (int e = ct; e < GT * (GKC / 4); e += GW_CONV) {
@@ -2118,8 +2119,8 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
         }
     } else if (lane == 0) {   // w == 0: MMA issuer
         for (int c = 0; c < nch; ++c) {
-            const int o = c & 1;
-            mbar_wait(smem_u32(&op_full[o]), (c >> 1) & 1);
+            const int o = c % GW_OPS;
+            mbar_wait(smem_u32(&op_full[o]), (c / GW_OPS) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
             const uint32_t hi = smem_u32(hi_ptr(o)), lo = hi + GOPB;
 #pragma unroll
@@ -2773,7 +2774,7 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
         CUtensorMap tm;
         int rc = encode_gram_map(&tm, C->ct32, C->kp, C->d);
         if (rc) return rc;
-        const size_t smem = (size_t)GW_RAW * GW_RAWST + (size_t)2 * 2 * GOPB;
+        const size_t smem = (size_t)GW_RAW * GW_RAWST + (size_t)GW_OPS * 2 * GOPB;
         static bool attr_ws = false;
         if (!attr_ws) {
             cudaFuncSetAttribute(k_gram_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

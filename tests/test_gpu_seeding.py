@@ -121,3 +121,31 @@ def test_run_with_kmpp_seeding(oracle_mod, variant):
         assert [s.reassignments for s in res.iterations] == [s.reassignments for s in ref.iterations]
         o = oracle_mod.run(X, 20, variant, init_rows=want, max_iter=100)
         assert abs(o["objective"][-1] - res.objective) <= 1e-6 * abs(o["objective"][-1])
+
+
+def test_gpu_seeding_dense_corpus(oracle_mod):
+    """k-means++ / AFK-MC2 on a dense (C5-shaped) corpus: float64 rows of the
+    dense path, same picks as the oracle."""
+    import paper_2107_04074_b200 as spk
+    from paper_2107_04074_b200 import synth
+    data = synth.config_dataset("C5", n_override=5000)
+    X = oracle_mod.CSR(data.indptr, data.indices, data.data, data.dim)
+    assert np.array_equal(spk.init_kmpp(data, 40, alpha=1.0, seed=11).seed_indices,
+                          oracle_mod.seed_kmpp(X, 40, 1.0, 11))
+    assert np.array_equal(spk.init_afkmc2(data, 40, alpha=1.5, chain_length=30, seed=12).seed_indices,
+                          oracle_mod.seed_afkmc2(X, 40, 1.5, 30, 12))
+
+
+def test_ingest_then_fit(oracle_mod, tmp_path):
+    """corpus_io.load_dataset (C++ parser + TF-IDF) feeding the GPU fit: the
+    fit matches the oracle run on the same rows."""
+    import paper_2107_04074_b200 as spk
+    from paper_2107_04074_b200 import corpus_io
+    from conftest import GOLDEN
+    data = corpus_io.load_dataset(GOLDEN / "svml" / "counts_c1.svml", tfidf=True)
+    X = oracle_mod.CSR(data.indptr, data.indices, data.data, data.dim)
+    ref = oracle_mod.run(X, 12, "standard", seed=4, max_iter=50)
+    for v in ("standard", "elkan", "hamerly"):
+        r = spk.run(data, 12, v, spk.SeedConfig(seed=4), max_iter=50)
+        assert abs(r.objective - ref["objective"][-1]) <= 1e-6 * abs(ref["objective"][-1])
+        assert abs(len(r.iterations) - ref["iterations"]) <= 1

@@ -65,3 +65,12 @@ def test_brute_force_assign_matches_oracle(oracle_mod):
 def test_fuzz_triangle():
     assert _v().fuzz_triangle(20000, 16, seed=1)
     assert _v().fuzz_triangle(5000, 3, seed=2)
+
+
+def test_device_audit_dense_hamerly():
+    """The dense tensor-core path's bounds are sound at every iteration (C5 shape, n=20k, k=200)."""
+    from paper_2107_04074_b200 import synth
+    data = synth.config_dataset("C5", n_override=20_000)
+    for v in ("hamerly", "simp_hamerly"):
+        rep = _v().audit_bounds(data, v, 200, seed=2, max_iter=20)
+        assert rep.passed, (v, rep)

@@ -166,7 +166,8 @@ def run_reference(args):
     line = {"metric": metric_name(args), "value": val, "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(args, data, args.gpus), "impl": "reference",
+            "config": dict(workload_config(args, data, args.gpus),
+                           precision="float64 (C port of the reference loop, the oracle)"), "impl": "reference",
             "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": "port",
                              "sample": f"full workload ({args.steps} steps x {len(variants)} fits), OpenMP over points"},
             "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

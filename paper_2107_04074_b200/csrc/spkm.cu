@@ -2031,26 +2031,40 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_const
 }
 
 
-// Single-tile Gram (k <= 128), warp specialised: one thread streams the
-// term-major float32 centers (ct32: each CTA's d-range is one contiguous
-// block) with TMA, 4 stages of 32 terms x 128 centers in flight; six
-// converter warps transpose them into K-major tf32 hi / lo core matrices;
-// one thread issues the MMAs; the TMEM tile goes to the split's partial Gram.
-constexpr int GW_RAW = 6;
-constexpr int GW_OPS = 3;
+// Warp-specialised Gram tile: one thread streams the term-major float32
+// centers (ct32; a CTA's d-range is one contiguous block of rows) with TMA,
+// converter warps transpose them into K-major tf32 hi / lo core matrices,
+// one thread issues the 3xTF32 MMAs, and the TMEM tile goes to the split's
+// partial Gram.  DIAG (k <= 128: the single diagonal tile) stages A alone,
+// 6 raw / 3 operand stages; other tiles stage A and B, 2 / 2.
 constexpr int GW_THREADS = 384;
-constexpr int GW_CONV = 320;
-constexpr int GW_RAWST = GT * GKC * 4;            // 16 KB: 32 terms x 128 centers, float32
+constexpr int GW_CONV = 320;                      // warps 2-11
+constexpr int GW_SLICE = GT * GKC * 4;            // 16 KB: 32 terms x 128 centers, float32
+template <bool DIAG> struct GwCfg {
+    static constexpr int RAW = DIAG ? 6 : 2;
+    static constexpr int OPS = DIAG ? 3 : 2;
+    static constexpr int RAWST = DIAG ? GW_SLICE : 2 * GW_SLICE;
+    static constexpr int OPST = (DIAG ? 2 : 4) * GOPB;
+    static constexpr size_t SMEM = (size_t)RAW * RAWST + (size_t)OPS * OPST;
+};
 
+template <bool DIAG>
 __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant__ CUtensorMap tm, int64_t k, int64_t d,
-                                                          int64_t dsplit, const double *__restrict__ sinp, int full,
-                                                          double *gpart, const long long *__restrict__ ctl) {
+                                                          int64_t dsplit, const int2 *__restrict__ tiles,
+                                                          const double *__restrict__ sinp, int full, double *gpart,
+                                                          const long long *__restrict__ ctl) {
+    using G = GwCfg<DIAG>;
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     extern __shared__ __align__(1024) uint8_t gsm[];
-    __shared__ __align__(8) uint64_t raw_full[GW_RAW], raw_empty[GW_RAW], op_full[GW_OPS], op_empty[GW_OPS], done_b;
+    __shared__ __align__(8) uint64_t raw_full[G::RAW], raw_empty[G::RAW], op_full[G::OPS], op_empty[G::OPS], done_b;
     __shared__ uint32_t tmem_base_s;
-    int mine = full;   // recomputed only if some cluster moved
-    if (!mine && threadIdx.x < GT) mine = threadIdx.x < k && sinp[threadIdx.x] != 0.0;
+    const int2 tl = DIAG ? make_int2(0, 0) : tiles[blockIdx.x];
+    const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
+    int mine = full;   // the tile is recomputed only if one of its clusters moved
+    if (!mine && threadIdx.x < GT) {
+        const int64_t q = threadIdx.x;
+        mine = (a0 + q < k && sinp[a0 + q] != 0.0) || (j0 + q < k && sinp[j0 + q] != 0.0);
+    }
     if (!__syncthreads_or(mine)) return;
     const int64_t per = ((d + dsplit - 1) / dsplit + GKC - 1) / GKC * GKC;
     const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
@@ -2063,11 +2077,11 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (threadIdx.x == 0) {
-        for (int q = 0; q < GW_RAW; ++q) {
+        for (int q = 0; q < G::RAW; ++q) {
             mbar_init(&raw_full[q], 1);
             mbar_init(&raw_empty[q], GW_CONV);
         }
-        for (int q = 0; q < GW_OPS; ++q) {
+        for (int q = 0; q < G::OPS; ++q) {
             mbar_init(&op_full[q], GW_CONV);
             mbar_init(&op_empty[q], 1);
         }
@@ -2079,29 +2093,33 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_base_s;
     uint8_t *raw0 = gsm;
-    uint8_t *op0 = gsm + (size_t)GW_RAW * GW_RAWST;
-    auto raw_ptr = [&](int q) { return raw0 + (size_t)q * GW_RAWST; };
-    auto hi_ptr = [&](int o) { return op0 + (size_t)o * 2 * GOPB; };
+    uint8_t *op0 = gsm + (size_t)G::RAW * G::RAWST;
+    auto raw_ptr = [&](int q) { return raw0 + (size_t)q * G::RAWST; };
+    auto op_ptr = [&](int o) { return op0 + (size_t)o * G::OPST; };   // [A hi | A lo | B hi | B lo]
     if (w == 1) {
         if (lane == 0) {
             for (int c = 0; c < nch; ++c) {
-                const int r = c % GW_RAW;
-                if (c >= GW_RAW) mbar_wait(smem_u32(&raw_empty[r]), ((c / GW_RAW) - 1) & 1);
-                mbar_expect_tx(&raw_full[r], (uint32_t)GW_RAWST);
-                tma_load_2d(smem_u32(raw_ptr(r)), &tm, 0, (int)(t0 + (int64_t)c * GKC), smem_u32(&raw_full[r]));
+                const int r = c % G::RAW;
+                if (c >= G::RAW) mbar_wait(smem_u32(&raw_empty[r]), ((c / G::RAW) - 1) & 1);
+                mbar_expect_tx(&raw_full[r], (uint32_t)G::RAWST);
+                const int trow = (int)(t0 + (int64_t)c * GKC);
+                tma_load_2d(smem_u32(raw_ptr(r)), &tm, (int)a0, trow, smem_u32(&raw_full[r]));
+                if (!DIAG) tma_load_2d(smem_u32(raw_ptr(r)) + GW_SLICE, &tm, (int)j0, trow, smem_u32(&raw_full[r]));
             }
         }
         __syncwarp();
     } else if (w >= 2) {
         const int ct = threadIdx.x - 64;
+        constexpr int TASKS = (DIAG ? 1 : 2) * GT * (GKC / 4);
         for (int c = 0; c < nch; ++c) {
-            const int r = c % GW_RAW, o = c % GW_OPS;
-            mbar_wait(smem_u32(&raw_full[r]), (c / GW_RAW) & 1);
-            if (c >= GW_OPS) mbar_wait(smem_u32(&op_empty[o]), ((c / GW_OPS) - 1) & 1);
-            const float *rs = reinterpret_cast<const float *>(raw_ptr(r));   // [32 terms][128 centers]
-            uint8_t *hi = hi_ptr(o), *lo = hi + GOPB;
-            for (int e = ct; e < GT * (GKC / 4); e += GW_CONV) {
-                const int m = e & (GT - 1), q = e >> 7;   // consecutive threads: consecutive centers
+            const int r = c % G::RAW, o = c % G::OPS;
+            mbar_wait(smem_u32(&raw_full[r]), (c / G::RAW) & 1);
+            if (c >= G::OPS) mbar_wait(smem_u32(&op_empty[o]), ((c / G::OPS) - 1) & 1);
+            for (int e = ct; e < TASKS; e += GW_CONV) {
+                const int part = e >> 10, ee = e & 1023;   // part 0: A slice, 1: B slice
+                const int m = ee & (GT - 1), q = ee >> 7;   // consecutive threads: consecutive centers
+                const float *rs = reinterpret_cast<const float *>(raw_ptr(r) + part * GW_SLICE);   // [32][128]
+                uint8_t *hi = op_ptr(o) + part * 2 * GOPB, *lo = hi + GOPB;
                 uint32_t hh[4], ll[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
@@ -2119,25 +2137,27 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
         }
     } else if (lane == 0) {   // w == 0: MMA issuer
         for (int c = 0; c < nch; ++c) {
-            const int o = c % GW_OPS;
-            mbar_wait(smem_u32(&op_full[o]), (c / GW_OPS) & 1);
+            const int o = c % G::OPS;
+            mbar_wait(smem_u32(&op_full[o]), (c / G::OPS) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t hi = smem_u32(hi_ptr(o)), lo = hi + GOPB;
+            const uint32_t ahi = smem_u32(op_ptr(o)), alo = ahi + GOPB;
+            const uint32_t bhi = DIAG ? ahi : ahi + 2 * GOPB, blo = bhi + GOPB;
 #pragma unroll
             for (int g = 0; g < GKC / 8; ++g) {
                 const uint32_t off = g * GGRP;
-                const uint64_t dh = umma_desc(hi + off), dl = umma_desc(lo + off);
+                const uint64_t dah = umma_desc(ahi + off), dal = umma_desc(alo + off);
+                const uint64_t dbh = umma_desc(bhi + off), dbl = umma_desc(blo + off);
                 const uint32_t acc0 = (c > 0 || g > 0) ? 1u : 0u;
                 asm volatile(
                     "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                     " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                    "l"(dl), "l"(dh), "r"(kGramIdesc), "r"(acc0)
+                    "l"(dal), "l"(dbh), "r"(kGramIdesc), "r"(acc0)
                     : "memory");
-                asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dh), "l"(dl),
-                             "r"(kGramIdesc)
+                asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dah),
+                             "l"(dbl), "r"(kGramIdesc)
                              : "memory");
-                asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dh), "l"(dh),
-                             "r"(kGramIdesc)
+                asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dah),
+                             "l"(dbh), "r"(kGramIdesc)
                              : "memory");
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -2153,7 +2173,7 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
     if (w < 4) {
         if (nch > 0) mbar_wait(smem_u32(&done_b), 0);
         asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-        const int64_t row = w * 32 + lane;
+        const int64_t row = a0 + w * 32 + lane;
 #pragma unroll 1
         for (int cb = 0; cb < GT / 32; ++cb) {
             uint32_t r[32];
@@ -2171,7 +2191,7 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
                 double *out = gpart + ((int64_t)blockIdx.y * k + row) * k;
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
-                    const int64_t col = cb * 32 + q;
+                    const int64_t col = j0 + cb * 32 + q;
                     if (col < k) out[col] = nch > 0 ? (double)__uint_as_float(r[q]) : 0.0;
                 }
             }
@@ -2745,9 +2765,8 @@ int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long lo
 }
 
 int64_t spkm_gram_dsplit(int64_t k, int64_t d) {
-    // one wave: one CTA per SM (~130 KB of stages), or two per SM when the
-    // grid is the single diagonal tile (k <= 128: A staged alone, 66 KB);
-    // at least 256 terms per CTA
+    // one wave: one CTA per SM (k_gram_ws stages ~192 KB); at least 256
+    // terms per CTA
     const int64_t tk = (k + GT - 1) / GT;
     const int64_t tiles = tk * (tk + 1) / 2;
     const int64_t per_sm = 1;
@@ -2767,20 +2786,25 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     const int64_t ntiles = tk * (tk + 1) / 2;
     const int64_t ds = spkm_gram_dsplit(C->k, C->d);
     const int64_t per = ((C->d + ds - 1) / ds + GKC - 1) / GKC * GKC;
-    // (the single-tile path splits the float32 copy: + 2 x 2^-24 for its rounding)
-    const bool ws = tk == 1 && (C->kp * 4) % 16 == 0;
+    // the warp-specialised path splits the float32 copy: + 2 x 2^-24 for its rounding
+    const bool ws = (C->kp * 4) % 16 == 0;
     const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + (ws ? 2e-6 : 1e-6);
     if (ws) {
         CUtensorMap tm;
         int rc = encode_gram_map(&tm, C->ct32, C->kp, C->d);
         if (rc) return rc;
-        const size_t smem = (size_t)GW_RAW * GW_RAWST + (size_t)GW_OPS * 2 * GOPB;
         static bool attr_ws = false;
         if (!attr_ws) {
-            cudaFuncSetAttribute(k_gram_ws, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+            cudaFuncSetAttribute(k_gram_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GwCfg<true>::SMEM);
+            cudaFuncSetAttribute(k_gram_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GwCfg<false>::SMEM);
             attr_ws = true;
         }
-        k_gram_ws<<<dim3(1, (unsigned)ds), GW_THREADS, smem, st>>>(tm, C->k, C->d, ds, C->sinp, full, gpart, C->ctl);
+        if (tk == 1)
+            k_gram_ws<true><<<dim3(1, (unsigned)ds), GW_THREADS, GwCfg<true>::SMEM, st>>>(tm, C->k, C->d, ds, tiles_dev,
+                                                                                       C->sinp, full, gpart, C->ctl);
+        else
+            k_gram_ws<false><<<dim3((unsigned)ntiles, (unsigned)ds), GW_THREADS, GwCfg<false>::SMEM, st>>>(
+                tm, C->k, C->d, ds, tiles_dev, C->sinp, full, gpart, C->ctl);
     } else {
         const int nbuf = (tk == 1) ? 2 : 4;
         const size_t smem = (size_t)2 * nbuf * GOPB;

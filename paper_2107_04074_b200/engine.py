@@ -1000,6 +1000,7 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
 # same graph; results get their own snapshot of the center state.
 _ENGINES: "dict" = {}
 _ENGINE_CACHE_MAX = 6
+_ENGINE_CACHE_HBM_SHARE = 0.45
 
 
 def _engine_for(data, k, variant, device, hamerly_update, corpus, comm, n_total, use_graphs):
@@ -1008,8 +1009,25 @@ def _engine_for(data, k, variant, device, hamerly_update, corpus, comm, n_total,
     key = (str(dev), id(corpus), k, variant, hamerly_update, n_total, use_graphs, data.dim, id(comm))
     eng = _ENGINES.pop(key, None)
     if eng is None or eng.corpus is not corpus or eng.comm is not comm:
-        eng = Engine(data, k, variant, device=dev, hamerly_update=hamerly_update, corpus=corpus, comm=comm,
-                     n_total=n_total, use_graphs=use_graphs)
+        eng = None
+        # keep the cache within a share of HBM (a C4 engine holds ~20 GB of
+        # sums / centers / bounds): drop the least recently used engines first
+        total = torch.cuda.get_device_properties(dev).total_memory
+        while _ENGINES and torch.cuda.memory_allocated(dev) > _ENGINE_CACHE_HBM_SHARE * total:
+            _ENGINES.pop(next(iter(_ENGINES)))
+        try:
+            eng = Engine(data, k, variant, device=dev, hamerly_update=hamerly_update, corpus=corpus, comm=comm,
+                         n_total=n_total, use_graphs=use_graphs)
+        except torch.OutOfMemoryError:
+            # cached engines of other fits hold HBM (C4: ~25 GB each): drop them and retry once
+            if not _ENGINES:
+                raise
+        if eng is None:
+            _ENGINES.clear()
+            torch.cuda.synchronize(dev)
+            torch.cuda.empty_cache()
+            eng = Engine(data, k, variant, device=dev, hamerly_update=hamerly_update, corpus=corpus, comm=comm,
+                         n_total=n_total, use_graphs=use_graphs)
     else:
         eng.C.cc_valid = False
         eng.stream.wait_stream(torch.cuda.current_stream(dev))

@@ -1365,28 +1365,16 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
 }
 
 // ---------------------------------------------------------- center thresholds
-// engine._center_thresholds (engine.py:192-198): Gram G = C C^T on the tensor
-// cores, 3xTF32 (x = hi + lo, G ~ hi.hi + hi.lo + lo.hi) with mma.sync
-// m16n8k8, read from the term-major float32 copy ct32, split over d.  Each
-// 32-term stage is accumulated in fp32 (96 products) and then added into
-// float64 registers; stages and d-splits are summed in float64.
-// Error bound: |G~ - G| <= 1.2e-7 (ct32 rounding) + 7.2e-7 (3xTF32 residual)
-// + 96 * 2^-22 (per-stage fp32 accumulation, truncating adds assumed)
-// times sum_t |c_a[t] c_j[t]| <= 1, i.e. < 2.4e-5; kGramDelta = 5e-5 is added
-// before the half-angle map so cc stays an upper bound.
-// Tiles: 64x64 outputs (upper triangle).  A tile is skipped when none of
-// its clusters moved since the last call.
-// 5th-gen tensor cores (tcgen05.mma kind::tf32, accumulator in TMEM).
-// One CTA = one 128 x 128 output tile (upper triangle of 128-tiles) over
-// L terms of d.  float64 center rows are staged in shared memory as K-major,
-// no-swizzle core matrices (8 centers x 4 terms, 16-byte rows), split into
-// tf32 hi and lo parts; one elected thread issues 3 MMAs (lo.hi, hi.lo,
-// hi.hi) per 8-term group and commits to an mbarrier; the 32-term stages
-// are double-buffered so loads overlap the MMAs.  The fp32 partial tile is
-// read back with tcgen05.ld and written as float64 per d-split.
+// engine._center_thresholds (engine.py:192-198): Gram G = C C^T on the 5th-gen
+// tensor cores (tcgen05.mma kind::tf32, accumulator in TMEM), 3xTF32
+// (x = hi + lo, G ~ lo.hi + hi.lo + hi.hi).  One CTA = one 128 x 128 output
+// tile (upper triangle of 128-tiles) over one d-split, read from the
+// term-major float32 copy ct32 by TMA (k_gram_ws below); a tile is skipped
+// when none of its clusters moved since the last call.  The per-split fp32
+// tiles are written as float64 and summed by k_gram_final.
 // Error bound per entry: products of tf32 values are exact; the fp32 TMEM
 // accumulation over 3L/8 MMA steps adds <= (3L/8 + 8) 2^-22 sum|a b| (even
-// with truncating adds); the hi/lo split of the float64 values adds < 1e-6.
+// with truncating adds); the float32 copy and the hi/lo split add < 2e-6.
 constexpr int GT = 128;
 constexpr int GKC = 32;                       // terms per stage
 // K-major, no-swizzle core matrices: 8 centers x 16 bytes (4 terms).
@@ -1430,173 +1418,6 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
     }
 }
 
-// GKC terms x GT centers of the float64 centers -> K-major core matrices.
-// Task = (center m, 4-term chunk q); 8 consecutive lanes read one center's
-// 32 terms (256 contiguous bytes), one 16-byte store per part.  All loads of
-// a thread are issued before any conversion (NT tasks in flight).
-template <int NT>
-__device__ __forceinline__ void stage_operand(const double *__restrict__ C, int64_t d, int64_t k, int64_t c0,
-                                              int64_t tb, int64_t t1, uint8_t *hi, uint8_t *lo) {
-    double v[NT][4];
-    const bool vec = (d % 2) == 0 && (tb % 2) == 0;
-#pragma unroll
-    for (int u = 0; u < NT; ++u) {
-        const int e = threadIdx.x + u * blockDim.x;
-        const int q = e & 7, m = e >> 3;
-        const int64_t row = c0 + m;
-        const int64_t t = tb + 4 * q;
-#pragma unroll
-        for (int r = 0; r < 4; ++r) v[u][r] = 0.0;
-        if (row < k) {
-            const double *p = C + row * d + t;
-            if (vec && t + 3 < t1) {
-                const double2 x0 = __ldg(reinterpret_cast<const double2 *>(p));
-                const double2 x1 = __ldg(reinterpret_cast<const double2 *>(p) + 1);
-                v[u][0] = x0.x; v[u][1] = x0.y; v[u][2] = x1.x; v[u][3] = x1.y;
-            } else {
-#pragma unroll
-                for (int r = 0; r < 4; ++r) v[u][r] = (t + r < t1) ? __ldg(p + r) : 0.0;
-            }
-        }
-    }
-#pragma unroll
-    for (int u = 0; u < NT; ++u) {
-        const int e = threadIdx.x + u * blockDim.x;
-        const int q = e & 7, m = e >> 3;
-        uint32_t h[4], l[4];
-#pragma unroll
-        for (int r = 0; r < 4; ++r) {
-            h[r] = to_tf32((float)v[u][r]);
-            l[r] = to_tf32((float)(v[u][r] - (double)__uint_as_float(h[r])));
-        }
-        const int off = (q >> 1) * GGRP + (q & 1) * GLBO + (m >> 3) * GSBO + (m & 7) * 16;
-        *reinterpret_cast<uint4 *>(hi + off) = make_uint4(h[0], h[1], h[2], h[3]);
-        *reinterpret_cast<uint4 *>(lo + off) = make_uint4(l[0], l[1], l[2], l[3]);
-    }
-}
-
-constexpr int kGramThreads = 512;
-
-__global__ void __launch_bounds__(kGramThreads, 1) k_gram_tc(int64_t k, int64_t d, int64_t dsplit,
-                                                     const double *__restrict__ C, const int2 *__restrict__ tiles,
-                                                     const double *__restrict__ sinp, int full, double *gpart, const long long *__restrict__ ctl,
-                                                     int nbuf) {
-    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
-    extern __shared__ __align__(1024) uint8_t gsm[];
-    // layout: [stage 0: Ahi Alo Bhi Blo][stage 1: ...][2 mbarriers][tmem addr]
-    __shared__ __align__(8) uint64_t bars[2];
-    __shared__ uint32_t tmem_base_s;
-    const int2 tl = tiles[blockIdx.x];
-    const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
-    const bool diag = tl.x == tl.y;
-    int mine = full;   // the tile is recomputed if any of its clusters moved
-    if (!mine && threadIdx.x < GT) {
-        const int64_t q = threadIdx.x;
-        mine = (a0 + q < k && sinp[a0 + q] != 0.0) || (j0 + q < k && sinp[j0 + q] != 0.0);
-    }
-    if (!__syncthreads_or(mine)) return;
-    const int64_t per = ((d + dsplit - 1) / dsplit + GKC - 1) / GKC * GKC;
-    const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
-    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    if (w == 0) {
-        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;\n" ::"r"(smem_u32(&tmem_base_s)),
-                     "r"(GT)
-                     : "memory");
-        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
-    }
-    if (threadIdx.x == 0) {
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[0])) : "memory");
-        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(&bars[1])) : "memory");
-        asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    const uint32_t tmem = tmem_base_s;
-    const int nch = t1 > t0 ? (int)((t1 - t0 + GKC - 1) / GKC) : 0;
-    // 0 Ahi 1 Alo 2 Bhi 3 Blo; a grid of diagonal tiles only (k <= 128) stages A alone (nbuf = 2)
-    auto buf = [&](int s, int which) { return gsm + (size_t)(s * nbuf + which) * GOPB; };
-    auto load_stage = [&](int s, int64_t tb) {
-        stage_operand<GT * (GKC / 4) / kGramThreads>(C, d, k, a0, tb, t1, buf(s, 0), buf(s, 1));
-        if (!diag) stage_operand<GT * (GKC / 4) / kGramThreads>(C, d, k, j0, tb, t1, buf(s, 2), buf(s, 3));
-        asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");   // generic writes -> async proxy
-    };
-    if (nch > 0) load_stage(0, t0);
-    __syncthreads();
-    for (int ch = 0; ch < nch; ++ch) {
-        const int s = ch & 1;
-        if (threadIdx.x == 0) {
-            asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t ahi = smem_u32(buf(s, 0)), alo = smem_u32(buf(s, 1));
-            const uint32_t bhi = diag ? ahi : smem_u32(buf(s, 2)), blo = diag ? alo : smem_u32(buf(s, 3));
-#pragma unroll
-            for (int g = 0; g < GKC / 8; ++g) {
-                const uint32_t off = g * GGRP;
-                const uint64_t dah = umma_desc(ahi + off), dal = umma_desc(alo + off);
-                const uint64_t dbh = umma_desc(bhi + off), dbl = umma_desc(blo + off);
-                const uint32_t acc0 = (ch > 0 || g > 0) ? 1u : 0u;
-                asm volatile(
-                    "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
-                    " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                    "l"(dal), "l"(dbh), "r"(kGramIdesc), "r"(acc0)
-                    : "memory");
-                asm volatile(
-                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dah), "l"(dbl),
-                    "r"(kGramIdesc)
-                    : "memory");
-                asm volatile(
-                    "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dah), "l"(dbh),
-                    "r"(kGramIdesc)
-                    : "memory");
-            }
-            asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                             smem_u32(&bars[s]))
-                         : "memory");
-        }
-        if (ch + 1 < nch) {
-            const int ns = s ^ 1;
-            if (ch >= 1) mbar_wait(smem_u32(&bars[ns]), (uint32_t)(((ch - 1) >> 1) & 1));
-            load_stage(ns, t0 + (int64_t)(ch + 1) * GKC);
-            __syncthreads();
-        }
-    }
-    if (nch > 0) mbar_wait(smem_u32(&bars[(nch - 1) & 1]), (uint32_t)(((nch - 1) >> 1) & 1));
-    asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-    // epilogue: warp w < 4 owns TMEM lanes (rows) 32w..32w+31
-    const int64_t row = a0 + w * 32 + lane;
-    if (w < 4) {
-#pragma unroll
-    for (int cb = 0; cb < GT / 32; ++cb) {
-        uint32_t r[32];
-        const uint32_t taddr = tmem + ((uint32_t)(w * 32) << 16) + (uint32_t)(cb * 32);
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
-            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
-              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
-              "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
-              "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-            : "r"(taddr));
-        asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (row < k && nch > 0) {
-            double *out = gpart + ((int64_t)blockIdx.y * k + row) * k;
-#pragma unroll
-            for (int q = 0; q < 32; ++q) {
-                const int64_t col = j0 + cb * 32 + q;
-                if (col < k) out[col] = (double)__uint_as_float(r[q]);
-            }
-        }
-    }
-    if (nch == 0 && row < k) {
-        double *out = gpart + ((int64_t)blockIdx.y * k + row) * k;
-        for (int q = 0; q < GT; ++q)
-            if (j0 + q < k) out[j0 + q] = 0.0;
-    }
-    }
-    asm volatile("tcgen05.fence::before_thread_sync;\n" ::: "memory");
-    __syncthreads();
-    if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;\n" ::"r"(tmem), "r"(GT) : "memory");
-}
 
 // cc = half-angle of the Gram entry plus the error bound, rounded up.  8
 // lanes per (a, j): lane r sums splits y = r, r+8, ... then a fixed shuffle
@@ -2786,38 +2607,24 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     const int64_t ntiles = tk * (tk + 1) / 2;
     const int64_t ds = spkm_gram_dsplit(C->k, C->d);
     const int64_t per = ((C->d + ds - 1) / ds + GKC - 1) / GKC * GKC;
-    // the warp-specialised path splits the float32 copy: + 2 x 2^-24 for its rounding
-    const bool ws = (C->kp * 4) % 16 == 0;
-    const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + (ws ? 2e-6 : 1e-6);
-    if (ws) {
-        CUtensorMap tm;
-        int rc = encode_gram_map(&tm, C->ct32, C->kp, C->d);
-        if (rc) return rc;
-        static bool attr_ws = false;
-        if (!attr_ws) {
-            cudaFuncSetAttribute(k_gram_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GwCfg<true>::SMEM);
-            cudaFuncSetAttribute(k_gram_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GwCfg<false>::SMEM);
-            attr_ws = true;
-        }
-        if (tk == 1)
-            k_gram_ws<true><<<dim3(1, (unsigned)ds), GW_THREADS, GwCfg<true>::SMEM, st>>>(tm, C->k, C->d, ds, tiles_dev,
-                                                                                       C->sinp, full, gpart, C->ctl);
-        else
-            k_gram_ws<false><<<dim3((unsigned)ntiles, (unsigned)ds), GW_THREADS, GwCfg<false>::SMEM, st>>>(
-                tm, C->k, C->d, ds, tiles_dev, C->sinp, full, gpart, C->ctl);
-    } else {
-        const int nbuf = (tk == 1) ? 2 : 4;
-        const size_t smem = (size_t)2 * nbuf * GOPB;
-        static bool attr_set = false;
-        if (!attr_set) {   // the largest configuration (4 buffers per stage)
-            cudaFuncSetAttribute(k_gram_tc, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(8 * GOPB));
-            attr_set = true;
-        }
-        dim3 grid((unsigned)ntiles, (unsigned)ds);
-        k_gram_tc<<<grid, kGramThreads, smem, st>>>(C->k, C->d, ds, C->cent64, tiles_dev, C->sinp, full, gpart, C->ctl,
-                                                    nbuf);
+    // 3xTF32 residual over `per` terms + the float32 copy's rounding (2 x 2^-24 + slack)
+    const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + 2e-6;
+    CUtensorMap tm;
+    int rc = encode_gram_map(&tm, C->ct32, C->kp, C->d);
+    if (rc) return rc;
+    static bool attr_ws = false;
+    if (!attr_ws) {
+        cudaFuncSetAttribute(k_gram_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GwCfg<true>::SMEM);
+        cudaFuncSetAttribute(k_gram_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GwCfg<false>::SMEM);
+        attr_ws = true;
     }
-    CHECK_LAUNCH("gram_tc");
+    if (tk == 1)
+        k_gram_ws<true><<<dim3(1, (unsigned)ds), GW_THREADS, GwCfg<true>::SMEM, st>>>(tm, C->k, C->d, ds, tiles_dev,
+                                                                                   C->sinp, full, gpart, C->ctl);
+    else
+        k_gram_ws<false><<<dim3((unsigned)ntiles, (unsigned)ds), GW_THREADS, GwCfg<false>::SMEM, st>>>(
+            tm, C->k, C->d, ds, tiles_dev, C->sinp, full, gpart, C->ctl);
+    CHECK_LAUNCH("gram_ws");
     k_gram_final<<<(unsigned)((C->k * C->k * 8 + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, gdelta,
                                                                            C->cc, C->ctl);
     CHECK_LAUNCH("gram_final");

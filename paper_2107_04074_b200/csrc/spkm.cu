@@ -202,6 +202,32 @@ __device__ __forceinline__ void ctr_flush(const unsigned long long *s, long long
 }
 
 // ------------------------------------------------------------ full row pass
+// A row's (term, value) pairs are staged per 32-nnz chunk in shared memory as
+// int2 {idx, value bits}, kIvStride pairs per row group: the gather loop reads
+// two nnz per 16-byte broadcast load, and the 16-byte pad puts the groups of
+// one warp in distinct banks (one wavefront for up to 8 groups).
+constexpr int kIvStride = 34;
+template <int UB>
+__device__ __forceinline__ void load_iv(const int2 *p, int (&iv)[UB], float (&vv)[UB]) {
+    if constexpr (UB % 2 == 0) {
+#pragma unroll
+        for (int b = 0; b < UB; b += 2) {
+            const int4 t = *reinterpret_cast<const int4 *>(p + b);
+            iv[b] = t.x;
+            vv[b] = __int_as_float(t.y);
+            iv[b + 1] = t.z;
+            vv[b + 1] = __int_as_float(t.w);
+        }
+    } else {
+#pragma unroll
+        for (int b = 0; b < UB; ++b) {
+            const int2 t = p[b];
+            iv[b] = t.x;
+            vv[b] = __int_as_float(t.y);
+        }
+    }
+}
+
 enum { MODE_RESCAN = 4, MODE_PREDICT = 5 };
 
 struct RowPassArgs {
@@ -239,8 +265,7 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
     // dynamic smem: [hot * kp floats: term rows of the hottest terms][staging]
     float *s_hot = s_dyn;
     const int wpb = blockDim.x >> 5;
-    int32_t *s_idx = reinterpret_cast<int32_t *>(s_dyn + (int64_t)A.hot * A.kp);
-    float *s_val = reinterpret_cast<float *>(s_idx + wpb * 8 * 32);
+    int2 *s_iv = reinterpret_cast<int2 *>(s_dyn + (int64_t)A.hot * A.kp);
     if (HOT && A.hot > 0) {
         // the Zipf head of the vocabulary (terms renumbered by document
         // frequency on upload) is served from shared memory for the whole
@@ -259,8 +284,7 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
     const int64_t nrows = A.rowlist ? *A.rowcount : A.n;
     const int64_t nslots = (nrows + A.rpw - 1) / A.rpw;
     const int o0 = A.tpr > 1 ? (1 << (31 - __clz(A.tpr - 1))) : 0;
-    int32_t *my_idx = s_idx + (wib * 8 + (lane_on ? g : 0)) * 32;
-    float *my_val = s_val + (wib * 8 + (lane_on ? g : 0)) * 32;
+    int2 *my_iv = s_iv + (wib * 8 + (lane_on ? g : 0)) * kIvStride;
     const int hot = HOT ? A.hot : 0;
     for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
         const int64_t slot = w * A.rpw + g;
@@ -280,19 +304,18 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
         // nnz at a time so UB * CH/4 independent float4 loads are in flight.
         for (int c0 = 0; c0 < maxlen; c0 += 32) {
             const int cnt = max(0, min(32, len - c0));
-            for (int q2 = q; q2 < cnt; q2 += A.tpr) {
-                my_idx[q2] = __ldg(A.indices + s + c0 + q2);
-                my_val[q2] = __ldg(A.values + s + c0 + q2);
-            }
+            for (int q2 = q; q2 < cnt; q2 += A.tpr)
+                my_iv[q2] = make_int2(__ldg(A.indices + s + c0 + q2), __float_as_int(__ldg(A.values + s + c0 + q2)));
             __syncwarp();
             int u = 0;
             for (; u + UB <= cnt; u += UB) {
                 float4 cv[UB][CH / 4];
                 float vv[UB];
+                int iv[UB];
+                load_iv<UB>(my_iv + u, iv, vv);
 #pragma unroll
                 for (int b = 0; b < UB; ++b) {
-                    vv[b] = my_val[u + b];
-                    const int ii = my_idx[u + b];
+                    const int ii = iv[b];
                     if (HOT && ii < hot) {
                         const float4 *p = reinterpret_cast<const float4 *>(s_hot + (int64_t)ii * A.kp + j0);
 #pragma unroll
@@ -314,8 +337,9 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
                     }
             }
             for (; u < cnt; ++u) {
-                const float v0 = my_val[u];
-                const int ii = my_idx[u];
+                const int2 t = my_iv[u];
+                const float v0 = __int_as_float(t.y);
+                const int ii = t.x;
                 const float4 *p = (HOT && ii < hot) ? reinterpret_cast<const float4 *>(s_hot + (int64_t)ii * A.kp + j0)
                                                     : reinterpret_cast<const float4 *>(ctj + (int64_t)ii * A.kp);
 #pragma unroll
@@ -456,14 +480,12 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
                                                          const int32_t *__restrict__ surv1, int32_t *surv2,
                                                          long long *ctr, const long long *__restrict__ ctl) {
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
-    __shared__ float s_v[8][4][32];
-    __shared__ float s_c[8][4][32];
+    __shared__ __align__(16) float2 s_vc[8][4][kIvStride];   // (value, center value), padded as s_iv
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane >> 3, q = lane & 7;
-    float *sv = s_v[wib][g];
-    float *sc = s_c[wib][g];
+    float2 *svc = s_vc[wib][g];
     const long long cnt = ctr[SPKM_CTR_SURV1];
     const int64_t nslots = (cnt + 3) / 4;
     const int wpb = blockDim.x >> 5;
@@ -490,13 +512,17 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
 #pragma unroll
             for (int r = 0; r < 4; ++r) cx[r] = (q + 8 * r < cntc) ? __ldg(cta + (int64_t)ix[r] * kp) : 0.f;
 #pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                sv[q + 8 * r] = vx[r];
-                sc[q + 8 * r] = cx[r];
-            }
+            for (int r = 0; r < 4; ++r) svc[q + 8 * r] = make_float2(vx[r], cx[r]);
             __syncwarp();
-            if (q == 0)
-                for (int t = 0; t < cntc; ++t) acc = __fmaf_rn(sv[t], sc[t], acc);
+            if (q == 0) {
+                int t = 0;
+                for (; t + 2 <= cntc; t += 2) {
+                    const float4 p = *reinterpret_cast<const float4 *>(svc + t);
+                    acc = __fmaf_rn(p.x, p.y, acc);
+                    acc = __fmaf_rn(p.z, p.w, acc);
+                }
+                if (t < cntc) acc = __fmaf_rn(svc[t].x, svc[t].y, acc);
+            }
             __syncwarp();
         }
         bool surv = false;
@@ -648,8 +674,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                                                     int32_t *mv_old, long long *ctr, const long long *__restrict__ ctl) {
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     constexpr int UB = 4;
-    __shared__ int32_t s_idx[8][8][32];
-    __shared__ float s_val[8][8][32];
+    __shared__ __align__(16) int2 s_iv[8][8][kIvStride];
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
     extern __shared__ float s_sim_dyn[];   // [8 warps][sim_stride]
@@ -664,8 +689,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     const int sim_stride = (int)elkan_sim_stride(k);  // floats per warp
     const int gstride = sim_stride / ppw;             // per-group slice (>= 9 * nb)
     float *my_sim = s_sim_dyn + wib * sim_stride + (lane_on ? g : 0) * gstride;
-    int32_t *my_idx = s_idx[wib][lane_on ? g : 0];
-    float *my_val = s_val[wib][lane_on ? g : 0];
+    int2 *my_iv = s_iv[wib][lane_on ? g : 0];
     const long long cnt = ctr[SPKM_CTR_SURV1];
     const int64_t nslots = (cnt + ppw - 1) / ppw;
     const int wpb = blockDim.x >> 5;
@@ -706,20 +730,19 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
             const float4 *base4 = reinterpret_cast<const float4 *>(ct + j0);
             for (int c0 = 0; c0 < maxlen; c0 += 32) {
                 const int cntc = max(0, min(32, len - c0));
-                for (int q2 = q; q2 < cntc; q2 += bpr) {
-                    my_idx[q2] = __ldg(indices + s + c0 + q2);
-                    my_val[q2] = __ldg(values + s + c0 + q2);
-                }
+                for (int q2 = q; q2 < cntc; q2 += bpr)
+                    my_iv[q2] = make_int2(__ldg(indices + s + c0 + q2), __float_as_int(__ldg(values + s + c0 + q2)));
                 __syncwarp();
                 if (act) {
                     int uu = 0;
                     for (; uu + UB <= cntc; uu += UB) {
                         float4 x[UB][2];
                         float vv[UB];
+                        int iv[UB];
+                        load_iv<UB>(my_iv + uu, iv, vv);
 #pragma unroll
                         for (int b = 0; b < UB; ++b) {
-                            vv[b] = my_val[uu + b];
-                            const float4 *p = base4 + ((int64_t)my_idx[uu + b] * kp >> 2);
+                            const float4 *p = base4 + ((int64_t)iv[b] * kp >> 2);
                             x[b][0] = __ldg(p);
                             x[b][1] = __ldg(p + 1);
                         }
@@ -736,8 +759,9 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                         }
                     }
                     for (; uu < cntc; ++uu) {
-                        const float v0 = my_val[uu];
-                        const float4 *p = base4 + ((int64_t)my_idx[uu] * kp >> 2);
+                        const int2 t = my_iv[uu];
+                        const float v0 = __int_as_float(t.y);
+                        const float4 *p = base4 + ((int64_t)t.x * kp >> 2);
                         const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
                         acc[0] = __fmaf_rn(v0, x0.x, acc[0]);
                         acc[1] = __fmaf_rn(v0, x0.y, acc[1]);
@@ -2127,7 +2151,7 @@ constexpr int64_t kSmemBudget = 200 * 1024;
 int64_t hot_terms_for(int64_t k, int64_t kp, int64_t d) {
     const ColPlan p = col_plan(k);
     if (p.ch > 8) return 0;
-    const int64_t staging = (int64_t)(1024 / 32) * 8 * 32 * 8;   // see k_row_pass staging layout
+    const int64_t staging = (int64_t)(1024 / 32) * 8 * kIvStride * 8;   // see k_row_pass staging layout
     int64_t h = (kSmemBudget - staging) / (kp * 4);
     if (h > d) h = d;
     return h < 0 ? 0 : h;
@@ -2154,7 +2178,7 @@ int launch_row_pass(RowPassArgs &A, int64_t k, cudaStream_t st, int64_t max_rows
     if (p.ch <= 8 && row_pass_mode() == 1) {
         const int64_t d = A.hot_d;
         A.hot = (int)hot_terms_for(k, A.kp, d);
-        const size_t smem = (size_t)A.hot * A.kp * 4 + (size_t)(1024 / 32) * 8 * 32 * 8;
+        const size_t smem = (size_t)A.hot * A.kp * 4 + (size_t)(1024 / 32) * 8 * kIvStride * 8;
         int64_t grid = (slots + 31) / 32;
         if (grid > num_sms()) grid = num_sms();
         if (grid < 1) grid = 1;
@@ -2174,7 +2198,7 @@ int launch_row_pass(RowPassArgs &A, int64_t k, cudaStream_t st, int64_t max_rows
             if (g2 < grid) grid = (int)g2;
         }
     }
-    const size_t smem = (size_t)(256 / 32) * 8 * 32 * 8;
+    const size_t smem = (size_t)(256 / 32) * 8 * kIvStride * 8;
     if (p.ch == 4) return launch_rp<4, 256, false>(A, grid, smem, st);
     if (p.ch == 8) return launch_rp<8, 256, false>(A, grid, smem, st);
     if (p.ch == 16) return launch_rp<16, 256, false>(A, grid, smem, st);

@@ -501,12 +501,17 @@ class CenterState:
         if self.dense is not None:
             _lib.call("spkm_dense_centers", self.struct, self.dense, stream)
 
-    def snapshot(self) -> "CenterState":
-        """A shallow CenterState whose result tensors are private copies (for ClusteringResult)."""
+    def snapshot(self, sums_from=None) -> "CenterState":
+        """A shallow CenterState whose result tensors are private copies (for ClusteringResult).
+
+        ``sums_from=(data, assignments)`` skips the device copy of the k x d
+        fixed-point sums: they are an exact integer function of the final
+        assignments, rebuilt on the host only if the caller reads them."""
         snap = object.__new__(CenterState)
         snap.k, snap.d, snap.kp, snap.scale_bits, snap.order = self.k, self.d, self.kp, self.scale_bits, self.order
         snap.cent64 = self.cent64.clone()
-        snap.sums = self.sums.clone()
+        snap.sums = self.sums.clone() if sums_from is None else None
+        snap._sums_from = sums_from
         snap.counts = self.counts.clone()
         snap.drift = self.drift.clone()
         return snap
@@ -522,8 +527,22 @@ class CenterState:
         return self._to_host_order(self.cent64.view(self.k, self.d).cpu().numpy())
 
     def host_sums(self) -> np.ndarray:
+        if self.sums is None:
+            data, a = self._sums_from
+            return fixed_sums_host(data, a, self.k, self.scale_bits).astype(np.float64) * 2.0 ** -self.scale_bits
         s = self.sums.view(self.k, self.d).cpu().numpy().astype(np.float64) * 2.0 ** -self.scale_bits
         return self._to_host_order(s)
+
+
+def fixed_sums_host(data: Dataset, a: np.ndarray, k: int, scale_bits: int) -> np.ndarray:
+    """The device's exact cluster sums, host term order: sum over members of
+    rint(float32(x) * 2^S) as int64 (k_aggregate / k_apply_moves; integer
+    addition is order-free, so this equals the incrementally maintained sums)."""
+    rows = np.repeat(np.asarray(a, dtype=np.int64), np.diff(data.indptr))
+    fixed = np.rint(np.asarray(data.data, np.float32).astype(np.float64) * 2.0 ** scale_bits).astype(np.int64)
+    out = np.zeros(k * data.dim, np.int64)
+    np.add.at(out, rows * data.dim + np.asarray(data.indices, np.int64), fixed)
+    return out.reshape(k, data.dim)
 
 
 class PointState:
@@ -991,7 +1010,8 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
     else:
         a_dev = eng.a_host[:eng.n_loc].numpy() if a_read else eng.P.a[:eng.n_loc].cpu().numpy()
     a = eng.corpus.to_host_rows(a_dev.astype(np.int64))
-    return ClusteringResult(assignments=a, centers=DeviceCentroidSet(eng.C.snapshot(), seed_indices),
+    snap = eng.C.snapshot(sums_from=(data, a))
+    return ClusteringResult(assignments=a, centers=DeviceCentroidSet(snap, seed_indices),
                             objective=stats[-1].objective, iterations=stats, converged=converged)
 
 

@@ -11,6 +11,7 @@ the reference's (tests/test_gpu_seeding.py against golden picks of the
 reference).  Centers are the picked rows densified (CentroidSet.from_data_rows).
 """
 
+import functools
 from dataclasses import dataclass
 
 import numpy as np
@@ -42,9 +43,15 @@ def _check_k(data, k):
         raise InfeasibleError(f"k={k} infeasible for n={data.n}")
 
 
+@functools.lru_cache(maxsize=64)
+def _uniform_rows(n: int, k: int, seed: int) -> tuple:
+    return tuple(PortableRng(seed).sample_without_replacement(n, k))
+
+
 def uniform_rows(n: int, k: int, seed: int):
-    """The k seed row ids of init_uniform (rng.py:54-73)."""
-    return PortableRng(seed).sample_without_replacement(n, k)
+    """The k seed row ids of init_uniform (rng.py:54-73); a pure function of
+    (n, k, seed), memoised so repeated fits skip the Python splitmix64 loop."""
+    return list(_uniform_rows(int(n), int(k), int(seed)))
 
 
 def init_uniform(data, k: int, seed: int):

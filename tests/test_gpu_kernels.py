@@ -376,3 +376,20 @@ def test_sharded_path_single_rank_matches_run(variant):
         assert [s.sim_count for s in r.iterations] == [s.sim_count for s in e.iterations]
     finally:
         dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("variant", ["standard", "elkan", "hamerly"])
+def test_result_sums_rebuilt_on_host_equal_device_aggregate(variant):
+    """run() results rebuild the fixed-point sums on the host from the final
+    assignments instead of copying k x d int64 on the device; they must equal
+    a from-scratch device aggregation bit for bit."""
+    m = spk()
+    z = load_golden("small")
+    data = golden_dataset(z)
+    k = 5
+    r = m.run(data, k, variant, m.SeedConfig(seed=3), max_iter=20)
+    cs = m.CentroidSet.from_data_rows(data, range(k))
+    m.update_centers(data, r.assignments, cs)
+    assert np.array_equal(r.centers.sums, cs.sums)
+    assert np.array_equal(r.centers.counts, cs.counts)

@@ -287,6 +287,23 @@ int spkm_loop_end(void *loop);
 int spkm_loop_launch(void *loop, void *stream);
 int spkm_loop_destroy(void *loop);
 
+/* Whole-fit graph (one launch per fit): begin() captures the prefix on
+ * `stream` (seed upload, reset, iterations 1-2), loop() adds the WHILE node
+ * after it and starts capturing the body on `body_stream`, spkm_loop_end()
+ * closes the body, the caller captures the suffix (result downloads) on
+ * `stream`, end() instantiates.  Launched and destroyed with spkm_loop_*. */
+int spkm_fit_graph_begin(void *stream, void **loop_out);
+int spkm_fit_graph_loop(void *loop, const long long *ctl, const long long *limit, void *body_stream);
+int spkm_fit_graph_end(void *loop);
+int spkm_fit_graph_abort(void *loop);     /* error path: close open captures, free */
+
+/* out[row_perm[r]] = a[r] (int64): device-order assignments in host row order. */
+int spkm_rows_to_host(int64_t n, const int64_t *row_perm, const int32_t *a, int64_t *out, void *stream);
+
+/* Stream-ordered copies / fills (capturable; cudaMemcpyDefault). */
+int spkm_memcpy_async(void *dst, const void *src, int64_t bytes, void *stream);
+int spkm_memset_async(void *dst, int value, int64_t bytes, void *stream);
+
 /* Corpus upload: write the rows of a raw CSR (ip_raw[n+1] relative offsets,
  * int32 ids, float64 values) in device order: device row r = raw row
  * perm[r] at ip_new[r], ids mapped through new_id, float32 values (round to

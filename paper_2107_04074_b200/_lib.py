@@ -110,6 +110,13 @@ _SIGS = {
     "spkm_audit": [_P(Seed), c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_i64, ctypes.c_int, c_vp, c_vp, c_vp],
     "spkm_permute_rows": [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "spkm_loop_end": [c_vp],
+    "spkm_fit_graph_begin": [c_vp, _P(c_vp)],
+    "spkm_fit_graph_loop": [c_vp, c_vp, c_vp, c_vp],
+    "spkm_fit_graph_end": [c_vp],
+    "spkm_fit_graph_abort": [c_vp],
+    "spkm_rows_to_host": [c_i64, c_vp, c_vp, c_vp, c_vp],
+    "spkm_memcpy_async": [c_vp, c_vp, c_i64, c_vp],
+    "spkm_memset_async": [c_vp, ctypes.c_int, c_i64, c_vp],
     "spkm_loop_launch": [c_vp, c_vp],
     "spkm_loop_destroy": [c_vp],
     "spkm_seed_kmpp": [_P(Seed), c_i64, ctypes.c_double, ctypes.c_uint64, c_vp, c_vp, c_vp],
@@ -143,7 +150,7 @@ KERNELS_PER_CALL = {
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
     "spkm_seed_rows_csr": 1, "spkm_aggregate_sums_gated": 2, "spkm_permute_rows": 1, "spkm_audit": 1, "spkm_audit_transpose": 1,
-    "spkm_pack_moves": 1, "spkm_apply_move_slots": 1,
+    "spkm_pack_moves": 1, "spkm_apply_move_slots": 1, "spkm_rows_to_host": 1,
 }
 
 _lib = None

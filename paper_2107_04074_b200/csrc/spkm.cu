@@ -1248,6 +1248,14 @@ __global__ void k_reset(long long *ctr, double *stats) {
 
 // Condition of the device-driven fit loop: run another iteration while not
 // converged and fewer than *limit iterations are done (engine.py:239, 335-337).
+// Assignments of device row order -> host row order as int64 (the result's
+// layout), so the fit's one D2H is the final array.
+__global__ void k_rows_to_host(int64_t n, const int64_t *__restrict__ row_perm, const int32_t *__restrict__ a,
+                               int64_t *out) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < n) out[row_perm[r]] = a[r];
+}
+
 __global__ void k_loop_cond(cudaGraphConditionalHandle h, const long long *ctl, const long long *limit) {
     cudaGraphSetConditional(h, (ctl[1] == 0 && ctl[0] < *limit) ? 1u : 0u);
 }
@@ -2968,7 +2976,9 @@ struct spkm_loop {
     cudaGraphConditionalHandle handle = 0;
     const long long *ctl = nullptr;
     const long long *limit = nullptr;
-    cudaStream_t stream = nullptr;
+    cudaStream_t stream = nullptr;        // body capture stream
+    cudaStream_t outer = nullptr;         // whole-fit graph: the prefix / suffix capture stream
+    cudaGraphNode_t loop_node = nullptr;
 };
 
 int spkm_loop_begin(const long long *ctl, const long long *limit, void *stream, void **out) {
@@ -3017,8 +3027,103 @@ int spkm_loop_end(void *loop) {
     cudaError_t e = cudaStreamEndCapture(L->stream, &g);
     if (e0 != cudaSuccess) return fail("loop_end cond", e0);
     if (e != cudaSuccess) return fail("loop_end capture", e);
+    if (L->outer) return 0;   // whole-fit graph: the suffix follows on the outer stream
     e = cudaGraphInstantiate(&L->exec, L->graph, 0);
     return e == cudaSuccess ? 0 : fail("loop_end instantiate", e);
+}
+
+// Whole-fit graph: prefix (seed upload, iterations 1-2) captured on `stream`,
+// then the WHILE node, then the suffix (result downloads) on `stream` again.
+int spkm_fit_graph_begin(void *stream, void **out) {
+    spkm_loop *L = new spkm_loop();
+    L->outer = S(stream);
+    cudaError_t e = cudaGraphCreate(&L->graph, 0);
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(L->outer, L->graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    if (e != cudaSuccess) {
+        if (L->graph) cudaGraphDestroy(L->graph);
+        delete L;
+        return fail("fit_graph_begin", e);
+    }
+    *out = L;
+    return 0;
+}
+
+int spkm_fit_graph_loop(void *loop, const long long *ctl, const long long *limit, void *body_stream) {
+    spkm_loop *L = static_cast<spkm_loop *>(loop);
+    L->ctl = ctl;
+    L->limit = limit;
+    L->stream = S(body_stream);
+    cudaError_t e = cudaGraphConditionalHandleCreate(&L->handle, L->graph, 0, 0);
+    if (e != cudaSuccess) return fail("fit_graph_loop handle", e);
+    k_loop_cond<<<1, 1, 0, L->outer>>>(L->handle, L->ctl, L->limit);   // sets the first condition value
+    e = cudaGetLastError();
+    cudaStreamCaptureStatus cs;
+    cudaGraph_t g = nullptr;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t ndeps = 0;
+    if (e == cudaSuccess) e = cudaStreamGetCaptureInfo(L->outer, &cs, nullptr, &g, &deps, &ndeps);
+    cudaGraph_t body = nullptr;
+    if (e == cudaSuccess) {
+        cudaGraphNodeParams np = {};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = L->handle;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        e = cudaGraphAddNode(&L->loop_node, g, deps, ndeps, &np);
+        if (e == cudaSuccess) body = np.conditional.phGraph_out[0];
+    }
+    if (e == cudaSuccess)
+        e = cudaStreamUpdateCaptureDependencies(L->outer, &L->loop_node, 1, cudaStreamSetCaptureDependencies);
+    if (e == cudaSuccess)
+        e = cudaStreamBeginCaptureToGraph(L->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal);
+    return e == cudaSuccess ? 0 : fail("fit_graph_loop", e);
+}
+
+int spkm_fit_graph_end(void *loop) {
+    spkm_loop *L = static_cast<spkm_loop *>(loop);
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(L->outer, &g);
+    if (e != cudaSuccess) return fail("fit_graph_end capture", e);
+    e = cudaGraphInstantiate(&L->exec, L->graph, 0);
+    return e == cudaSuccess ? 0 : fail("fit_graph_end instantiate", e);
+}
+
+// Error path of a whole-fit capture: close whatever capture is still open
+// (body and outer stream) so the streams are usable again, drop the graph.
+int spkm_fit_graph_abort(void *loop) {
+    spkm_loop *L = static_cast<spkm_loop *>(loop);
+    if (!L) return 0;
+    for (cudaStream_t st : {L->stream, L->outer}) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        if (st && cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs != cudaStreamCaptureStatusNone) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(st, &g);
+        }
+    }
+    cudaGetLastError();
+    if (L->graph) cudaGraphDestroy(L->graph);
+    delete L;
+    return 0;
+}
+
+int spkm_rows_to_host(int64_t n, const int64_t *row_perm, const int32_t *a, int64_t *out, void *stream) {
+    if (n <= 0) return 0;
+    k_rows_to_host<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(n, row_perm, a, out);
+    CHECK_LAUNCH("rows_to_host");
+    return 0;
+}
+
+int spkm_memcpy_async(void *dst, const void *src, int64_t bytes, void *stream) {
+    if (bytes <= 0) return 0;
+    cudaError_t e = cudaMemcpyAsync(dst, src, (size_t)bytes, cudaMemcpyDefault, S(stream));
+    return e == cudaSuccess ? 0 : fail("memcpy_async", e);
+}
+
+int spkm_memset_async(void *dst, int value, int64_t bytes, void *stream) {
+    if (bytes <= 0) return 0;
+    cudaError_t e = cudaMemsetAsync(dst, value, (size_t)bytes, S(stream));
+    return e == cudaSuccess ? 0 : fail("memset_async", e);
 }
 
 int spkm_loop_launch(void *loop, void *stream) {

@@ -501,19 +501,33 @@ class CenterState:
         if self.dense is not None:
             _lib.call("spkm_dense_centers", self.struct, self.dense, stream)
 
-    def snapshot(self, sums_from=None) -> "CenterState":
+    def snapshot(self, sums_from=None, stream=None, lazy_sums: bool = False) -> "CenterState":
         """A shallow CenterState whose result tensors are private copies (for ClusteringResult).
 
-        ``sums_from=(data, assignments)`` skips the device copy of the k x d
-        fixed-point sums: they are an exact integer function of the final
-        assignments, rebuilt on the host only if the caller reads them."""
+        ``sums_from=(data, assignments)`` (or ``lazy_sums`` with ``_sums_from``
+        set later) skips the device copy of the k x d fixed-point sums: they
+        are an exact integer function of the final assignments, rebuilt on
+        the host only if the caller reads them.  With ``stream`` the copies
+        are enqueued on it (allocated on the current stream, then marked as
+        used by ``stream``)."""
         snap = object.__new__(CenterState)
         snap.k, snap.d, snap.kp, snap.scale_bits, snap.order = self.k, self.d, self.kp, self.scale_bits, self.order
-        snap.cent64 = self.cent64.clone()
-        snap.sums = self.sums.clone() if sums_from is None else None
+        skip_sums = lazy_sums or sums_from is not None
         snap._sums_from = sums_from
-        snap.counts = self.counts.clone()
-        snap.drift = self.drift.clone()
+        if stream is None:
+            snap.cent64 = self.cent64.clone()
+            snap.sums = None if skip_sums else self.sums.clone()
+            snap.counts = self.counts.clone()
+            snap.drift = self.drift.clone()
+            return snap
+        names = ("cent64", "counts", "drift") + (() if skip_sums else ("sums",))
+        snap.sums = None
+        outs = {nm: torch.empty_like(getattr(self, nm)) for nm in names}
+        with torch.cuda.stream(stream):
+            for nm, t in outs.items():
+                t.copy_(getattr(self, nm), non_blocking=True)
+                t.record_stream(stream)
+                setattr(snap, nm, t)
         return snap
 
     def _to_host_order(self, dev: np.ndarray) -> np.ndarray:
@@ -638,6 +652,7 @@ class Engine:
         self.sp = ctypes_void(self.stream.cuda_stream)
         self.use_graphs = use_graphs and comm is None
         self.loop = None                 # device-driven fit loop (CUDA graph with a WHILE node)
+        self.fit = None                  # the whole fit as one CUDA graph (fit_launch)
         self.loop_kernels = 0            # kernels per loop-body iteration
         self.limit = torch.zeros(1, dtype=torch.int64, device=self.device)
         self.a_host = torch.empty(max(self.corpus.n, 1), dtype=torch.int32).pin_memory()
@@ -646,10 +661,12 @@ class Engine:
         self.runs = 0
 
     def drop_loop(self):
-        if getattr(self, "loop", None) is not None:
-            self.stream.synchronize()
-            _lib.lib().spkm_loop_destroy(self.loop)
-            self.loop = None
+        for name in ("loop", "fit"):
+            h = getattr(self, name, None)
+            if h is not None:
+                self.stream.synchronize()
+                _lib.lib().spkm_loop_destroy(h)
+                setattr(self, name, None)
 
     def __del__(self):
         try:
@@ -875,6 +892,92 @@ class Engine:
             self.loop, self.loop_kernels = h, n + 1
         _lib.call("spkm_loop_launch", self.loop, self.sp)
 
+    def fit_graph_ok(self, data: Dataset, max_iter: int) -> bool:
+        """The whole-fit graph covers sparse single-device fits seeded by row ids."""
+        return (self.use_graphs and self.runs > 0 and self.comm is None and max_iter >= 3
+                and self.corpus.dense_dim is None and self.corpus.rows == (0, data.n)
+                and self.P.hist_cap >= max_iter + 1)
+
+    def fit_launch(self, data: Dataset, rows, max_iter: int):
+        """The whole fit as ONE graph launch: seed-row upload and gather, reset,
+        iterations 1-2, the WHILE loop over iterations 3..max_iter, and the
+        result downloads (stats history, control words, assignments in host
+        row order).  Host inputs (seed row ids, max_iter) are read from a
+        pinned buffer by the graph's H2D node, so one capture serves every
+        fit of this engine."""
+        rows = np.asarray(rows, dtype=np.int64)
+        if self.fit is None:
+            self._fit_capture(data)
+        self.fit_in_np[:self.k] = rows
+        self.fit_in_np[self.k] = max_iter
+        _lib.call("spkm_loop_launch", self.fit, self.sp)
+
+    def fit_results(self):
+        """After the fit graph has finished: (history rows, iterations done, assignments)."""
+        F, cap = _lib.ST_COUNT, self.P.hist_cap
+        done = int(self.fit_ctl_np[0])
+        _lib.note_launches(self.fit_kernels[0] + self.fit_kernels[1] * max(0, done - 2))
+        rows = self.P.hist_host.numpy()[:cap * F].reshape(cap, F)
+        return rows, done, self.fit_a_np[:self.corpus.n].copy()
+
+    def _fit_capture(self, data: Dataset):
+        import ctypes
+        k, n, dev = self.k, self.corpus.n, self.device
+        F, cap = _lib.ST_COUNT, self.P.hist_cap
+        st = self.corpus.seed_struct(data)
+        row_perm = self.corpus._seed[2]                 # device row -> host row (kept current by refresh)
+        self.fit_in = torch.zeros(k + 1, dtype=torch.int64).pin_memory()
+        self.fit_in_np = self.fit_in.numpy()
+        self.fit_ctl = torch.zeros(2, dtype=torch.int64).pin_memory()
+        self.fit_ctl_np = self.fit_ctl.numpy()
+        self.fit_a = torch.zeros(max(n, 1), dtype=torch.int64).pin_memory()
+        self.fit_a_np = self.fit_a.numpy()
+        self.fit_rows = torch.zeros(k, dtype=torch.int64, device=dev)
+        self.fit_out = torch.zeros(max(n, 1), dtype=torch.int64, device=dev)
+        body = torch.cuda.Stream(device=dev)
+        self.stream.synchronize()
+        h = ctypes.c_void_p()
+        _lib.call("spkm_fit_graph_begin", self.sp, ctypes.byref(h))
+        saved, _lib._profiler = _lib._profiler, None
+        _lib._capture = []
+        outer = (self.stream, self.sp)
+        ok = False
+        try:
+            _lib.call("spkm_memcpy_async", _ptr(self.fit_rows), self.fit_in.data_ptr(), 8 * k, self.sp)
+            _lib.call("spkm_seed_rows_csr", self.C.struct, st, _ptr(self.fit_rows), self.sp)
+            _lib.call("spkm_reset_counters", self.P.work, self.sp)
+            _lib.call("spkm_memset_async", _ptr(self.C.ctl), 0, 16, self.sp)
+            self.C.cc_valid = False
+            self.iteration1_launch()
+            self.enqueue(2)
+            _lib.call("spkm_memcpy_async", _ptr(self.limit), self.fit_in.data_ptr() + 8 * k, 8, self.sp)
+            n_pre = sum(_lib._capture) + 1               # + the loop's first condition kernel
+            _lib._capture = []
+            _lib.call("spkm_fit_graph_loop", h, _ptr(self.C.ctl), _ptr(self.limit), ctypes_void(body.cuda_stream))
+            self.stream, self.sp = body, ctypes_void(body.cuda_stream)
+            try:
+                self._body()
+            finally:
+                self.stream, self.sp = outer
+            n_body = sum(_lib._capture) + 1              # + the condition kernel
+            _lib._capture = None
+            _lib.call("spkm_loop_end", h)
+            _lib.call("spkm_memcpy_async", self.P.hist_host.data_ptr(), _ptr(self.P.hist), 8 * F * cap, self.sp)
+            _lib.call("spkm_memcpy_async", self.fit_ctl.data_ptr(), _ptr(self.C.ctl), 16, self.sp)
+            _lib.call("spkm_rows_to_host", n, _ptr(row_perm), _ptr(self.P.a), _ptr(self.fit_out), self.sp)
+            _lib.call("spkm_memcpy_async", self.fit_a.data_ptr(), _ptr(self.fit_out), 8 * n, self.sp)
+            _lib.call("spkm_fit_graph_end", h)
+            ok = True
+        finally:
+            _lib._capture = None
+            _lib._profiler = saved
+            self.stream, self.sp = outer
+            if not ok:
+                _lib.lib().spkm_fit_graph_abort(h)
+        self.fit = h
+        self.fit_kernels = (n_pre + 1, n_body)          # + rows_to_host
+        self._fit_keep = (body, row_perm)
+
     def read_history(self, first: int, count: int, with_a: bool = False):
         """One D2H of stats rows [first, first+count) and the control words
         (and the assignments into a pinned buffer), then one host sync."""
@@ -922,14 +1025,21 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
         cfg.validate()
         seed_indices = seed_rows_for(data, k, cfg, device=device, corpus=corpus)
     eng = _engine_for(data, k, variant, device, hamerly_update, corpus, comm, n_total, use_graphs)
-    if init_centers is None:
-        eng.seed_rows(data, seed_indices)
-    else:
-        eng.load_centers(init_centers)
-    eng.reset()
     if eng.P.hist_cap < max_iter + 1:
         eng.drop_loop()                     # the captured loop holds the old history pointer
         eng.P.set_history(max_iter + 1)
+    prof = _lib.active_profiler()
+    untimed = not (prof is not None and prof.timed)
+    device_loop = (eng.use_graphs and eng.runs > 0 and debug_hook is None and comm is None and untimed)
+    whole_fit = device_loop and init_centers is None and eng.fit_graph_ok(data, max_iter)
+    if whole_fit:
+        pass                                # seeding and reset are nodes of the fit graph
+    elif init_centers is None:
+        eng.seed_rows(data, seed_indices)
+        eng.reset()
+    else:
+        eng.load_centers(init_centers)
+        eng.reset()
     cc_per_it = k * (k - 1) // 2 if variant in _CC_VARIANTS else 0
     stats: list = []
     converged = False
@@ -950,11 +1060,21 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
                                     touched=int(st[_lib.ST_TOUCHED]), nnz_moved=int(st[_lib.ST_NNZ_MOVED])))
         return k == 1 or st[_lib.ST_ALLONE] == 1.0 or (it >= 2 and reassign == 0)
 
-    prof = _lib.active_profiler()
-    device_loop = (eng.use_graphs and eng.runs > 0 and debug_hook is None and comm is None
-                   and not (prof is not None and prof.timed))
     a_read = False
-    if device_loop:
+    a_host = None
+    if whole_fit:
+        # one graph launch per fit; the result snapshot is enqueued behind it
+        # so the host builds nothing while the device runs
+        eng.fit_launch(data, seed_indices, max_iter)
+        snap = eng.C.snapshot(sums_from=None, stream=eng.stream, lazy_sums=True)
+        eng.stream.synchronize()
+        eng.C.cc_valid = True
+        rows, done_its, a_host = eng.fit_results()
+        for q in range(min(done_its, max_iter)):
+            converged = record(q + 1, rows[q])
+            if converged:
+                break
+    elif device_loop:
         # the whole fit without a host round trip: iteration 1 and 2 eagerly
         # enqueued (iteration 2 rebuilds the full cc table), then iterations
         # 3..max_iter as one graph launch; one D2H of the stats history and
@@ -1002,6 +1122,10 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
     eng.stream.synchronize()
     eng.runs += 1
     torch.cuda.current_stream(eng.device).wait_stream(eng.stream)
+    if a_host is not None:
+        snap._sums_from = (data, a_host)
+        return ClusteringResult(assignments=a_host, centers=DeviceCentroidSet(snap, seed_indices),
+                                objective=stats[-1].objective, iterations=stats, converged=converged)
     if comm is not None:
         with torch.cuda.stream(eng.stream):
             comm.allgather_assignments(eng.P.a, eng.a_global)

@@ -348,6 +348,32 @@ def test_device_loop_max_iter_and_reuse(variant):
         assert all(s.elapsed_ns > 0 for s in g.iterations)
 
 
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_whole_fit_graph_matches_eager_across_seeds(variant):
+    """From the second fit on, an engine runs the whole fit as one CUDA graph
+    (seed upload, iterations 1-2, WHILE loop, result downloads) with the seed
+    rows and max_iter read from pinned memory at launch: every fit equals
+    the eager host loop (stats, assignments, centers, counts, sums)."""
+    m = spk()
+    data = golden_dataset(load_golden("C1"))
+    m.run(data, 12, variant, m.SeedConfig(seed=1), max_iter=30, use_graphs=True)   # first fit: eager
+    for seed, mi in ((5, 30), (6, 30), (5, 4), (7, 30)):
+        g = m.run(data, 12, variant, m.SeedConfig(seed=seed), max_iter=mi, use_graphs=True)
+        e = m.run(data, 12, variant, m.SeedConfig(seed=seed), max_iter=mi, use_graphs=False)
+        assert len(g.iterations) == len(e.iterations) <= mi
+        assert g.converged == e.converged
+        assert np.array_equal(g.assignments, e.assignments)
+        assert g.assignments.dtype == e.assignments.dtype
+        assert g.objective == e.objective
+        for a, b in zip(g.iterations, e.iterations):
+            assert (a.iteration, a.sim_count, a.cc_sim_count, a.reassignments, a.objective) == \
+                (b.iteration, b.sim_count, b.cc_sim_count, b.reassignments, b.objective)
+        assert np.array_equal(g.centers.centers, e.centers.centers)
+        assert np.array_equal(g.centers.counts, e.centers.counts)
+        assert np.array_equal(g.centers.sums, e.centers.sums)
+        assert list(g.centers.seed_indices) == list(e.centers.seed_indices)
+
+
 @pytest.mark.parametrize("variant", ["standard", "elkan", "hamerly"])
 def test_sharded_path_single_rank_matches_run(variant):
     """distributed.run_sharded (replicated corpus, move slots, assignment

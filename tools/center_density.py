@@ -22,3 +22,11 @@ for thr in (0.05, 0.1, 0.25, 0.5):
     dense_rows = nz > thr * k
     cost = (w * np.where(dense_rows, 4 * k, 8 * nz)).sum()
     print(f"  hybrid (dense if nz > {thr}k): bytes/nnz {cost:.0f} vs dense {4*k}; dense-row frac of nnz {w[dense_rows].sum():.3f}")
+# 32-center lines (128 B of a term row): share of (nnz, line) gathers that hit an all-zero line
+ctl = eng.C.ct32.view(data.dim, eng.C.kp)
+for width in (32, 8):
+    kq = (ctl.shape[1] + width - 1) // width * width
+    padded = torch.nn.functional.pad(ctl, (0, kq - ctl.shape[1]))
+    lines = (padded.view(data.dim, -1, width) != 0).any(dim=2).double().cpu().numpy()   # [d, kq/width]
+    live = (w[:, None] * lines).sum() / lines.shape[1]
+    print(f"  {width}-center blocks: nnz-weighted live fraction {live:.3f}")

@@ -15,4 +15,4 @@ for _ in range(3): step()
 torch.cuda.synchronize()
 t = time.perf_counter(); step(); torch.cuda.synchronize(); print("step ms", (time.perf_counter() - t) * 1e3)
 pr = cProfile.Profile(); pr.enable(); step(); torch.cuda.synchronize(); pr.disable()
-pstats.Stats(pr).sort_stats("cumulative").print_stats(28)
+pstats.Stats(pr).sort_stats(sys.argv[1] if len(sys.argv) > 1 else "cumulative").print_stats(45)

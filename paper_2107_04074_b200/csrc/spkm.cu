@@ -35,6 +35,7 @@
 #include <limits.h>
 
 #include <functional>
+#include <utility>
 #include <vector>
 
 #include "../../include/spkm.h"
@@ -61,6 +62,36 @@ int fail_msg(const char *msg) {
     snprintf(g_err, sizeof g_err, "%s", msg);
     return -1;
 }
+// Programmatic dependent launch: the loop's kernels are launched with
+// programmatic stream serialization, so kernel N+1's launch and CTA
+// rasterisation overlap kernel N's tail.  Every such kernel first waits for
+// its predecessor grid (griddepcontrol.wait: complete, memory visible), then
+// lets its own successor launch.  Outside PDL launches both are no-ops.
+#define PDL_ENTRY() asm volatile("griddepcontrol.wait;" ::: "memory")
+
+bool pdl_enabled() {
+    static int on = -1;   // SPKM_PDL=0 turns programmatic launches off (A/B measurements)
+    if (on < 0) {
+        const char *e = getenv("SPKM_PDL");
+        on = (e && e[0] == '0') ? 0 : 1;
+    }
+    return on == 1;
+}
+template <typename... KArgs, typename... Args>
+void pdl_launch(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    (void)cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);   // errors surface via CHECK_LAUNCH
+}
+
 #define CHECK_LAUNCH(name)                                          \
     do {                                                            \
         cudaError_t _e = cudaGetLastError();                        \
@@ -258,6 +289,7 @@ struct RowPassArgs {
 // CH/4 float4 loads of the term-major center row; CH independent FMA chains.
 template <int CH, int NT, bool HOT>
 __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
+    PDL_ENTRY();
     // nnz per gather batch: keep ~8 float4 loads in flight per lane
     constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 2 : 1;
     if (A.ctl[1]) return;   // converged: later enqueued iterations are no-ops
@@ -422,6 +454,7 @@ __global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *
                                                         const float *__restrict__ s_arr,
                                                         const double *__restrict__ hstat, int use_s, int naive,
                                                         int32_t *surv1, long long *ctr, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int owner = (int)hstat[0], owner_s = (int)hstat[3];
     const double pmin = hstat[1], pmin2 = hstat[2], smax = hstat[4], smax2 = hstat[5];
@@ -479,6 +512,7 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
                                                          const float *__restrict__ s_arr, int use_s,
                                                          const int32_t *__restrict__ surv1, int32_t *surv2,
                                                          long long *ctr, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ __align__(16) float2 s_vc[8][4][kIvStride];   // (value, center value), padded as s_iv
     __shared__ unsigned long long s_ctr[8];
@@ -552,6 +586,7 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
                                                       const float *__restrict__ cc,
                                                       const float *__restrict__ s_arr, int use_cc,
                                                       int32_t *surv1, long long *ctr, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
@@ -672,6 +707,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                                                     const float *__restrict__ cc, int use_cc,
                                                     const int32_t *__restrict__ surv1, int32_t *mv_i,
                                                     int32_t *mv_old, long long *ctr, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     constexpr int UB = 4;
     __shared__ __align__(16) int2 s_iv[8][8][kIvStride];
@@ -908,6 +944,7 @@ __global__ void __launch_bounds__(256) k_aggregate(int64_t n, int64_t d, const i
                                                    const int32_t *__restrict__ a, long long *sums,
                                                    long long *counts, double scale, const long long *__restrict__ ctl,
                                                    int period) {
+    PDL_ENTRY();
     if (ctl[1] || gate_off(ctl, period)) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
@@ -929,6 +966,7 @@ __global__ void __launch_bounds__(256) k_apply_moves(int64_t d, const int64_t *_
                                                      const int32_t *__restrict__ mv_old,
                                                      long long *ctr, long long *sums,
                                                      long long *counts, int32_t *touched, double scale, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
@@ -987,6 +1025,7 @@ constexpr double kChordPad = 4e-10;  // |1 - |c|| <= d * 2^-53 for d <= 1e6, twi
 
 __global__ void k_touched_list(int64_t k, const int32_t *__restrict__ touched, int all, int32_t *tlist,
                                int32_t *tcount, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ int wsum[32];
     __shared__ int base_s;
@@ -1018,6 +1057,7 @@ __global__ void __launch_bounds__(256) k_center_norm_part(int64_t d, int64_t nch
                                                           const int32_t *__restrict__ tlist,
                                                           const int32_t *__restrict__ tcount, double inv_scale,
                                                           double *part, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double sh[8];
     const int64_t y = blockIdx.y, c = blockIdx.x;
@@ -1043,6 +1083,7 @@ __global__ void __launch_bounds__(256) k_center_norm_final(int64_t nchunk, const
                                                            const int32_t *__restrict__ tlist,
                                                            const int32_t *__restrict__ tcount,
                                                            const double *__restrict__ part, double *norm, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double sh[8];
     const int64_t y = blockIdx.x;
@@ -1067,6 +1108,7 @@ __global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int
                                                       const int32_t *__restrict__ tcount, double inv_scale,
                                                       const double *__restrict__ norm, double *cent64, float *ct32,
                                                       double *part, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ float tile[kTileT][kTileJ + 1];
     __shared__ int js[kTileJ];
@@ -1147,6 +1189,7 @@ __global__ void __launch_bounds__(256) k_center_reduce(int64_t ntile, const int3
                                                        const double *__restrict__ part,
                                                        const double *__restrict__ norm, double *drift,
                                                        double *sinp, double *objc, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double sh[8];
     const int64_t y = blockIdx.x;
@@ -1242,6 +1285,7 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 
 // zero the counters and stamp the start of a fit (stats[ST_T0])
 __global__ void k_reset(long long *ctr, double *stats) {
+    PDL_ENTRY();
     if (threadIdx.x < 8) ctr[threadIdx.x] = 0;
     if (threadIdx.x == 0) stats[SPKM_ST_T0] = (double)globaltimer_ns();
 }
@@ -1252,6 +1296,7 @@ __global__ void k_reset(long long *ctr, double *stats) {
 // layout), so the fit's one D2H is the final array.
 __global__ void k_rows_to_host(int64_t n, const int64_t *__restrict__ row_perm, const int32_t *__restrict__ a,
                                int64_t *out) {
+    PDL_ENTRY();
     const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (r < n) out[row_perm[r]] = a[r];
 }
@@ -1262,6 +1307,7 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle h, const long long *ctl, 
 
 __global__ void k_zero_sums_gated(long long *sums, int64_t count, long long *counts, int64_t k,
                                   const long long *__restrict__ ctl, int period) {
+    PDL_ENTRY();
     if (ctl[1] || gate_off(ctl, period)) return;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) sums[i] = 0;
@@ -1274,6 +1320,7 @@ __global__ void k_seed_rows_csr(int64_t d, int64_t kp, const int64_t *__restrict
                                 const int32_t *__restrict__ indices, const double *__restrict__ v64,
                                 const int64_t *__restrict__ row_dev, const int64_t *__restrict__ rows,
                                 double *cent64, float *ct32) {
+    PDL_ENTRY();
     const int64_t j = blockIdx.x;
     const int64_t r = row_dev[rows[j]];
     for (int64_t e = indptr[r] + threadIdx.x; e < indptr[r + 1]; e += blockDim.x) {
@@ -1316,6 +1363,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
                                                           double *hstat, long long *ctr, double *stats,
                                                           long long sims_extra, int all, double *stats_hist,
                                                           int64_t hist_cap, long long *ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double s_ob[kFinThreads / 32];
     __shared__ int s_no[kFinThreads / 32];
@@ -1456,6 +1504,7 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // tree, so the result does not depend on scheduling.
 __global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict__ gpart,
                              const double *__restrict__ sinp, int full, double gdelta, float *cc, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t e = gt >> 3;
@@ -1493,6 +1542,7 @@ __global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict
 
 // s(a) = max_{j != a} cc(a, j); warp per row.
 __global__ void k_row_max(int64_t k, const float *__restrict__ cc, float *s, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int64_t a = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
@@ -1601,6 +1651,7 @@ __device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
 }
 
 __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_constant__ DenseArgs P) {
+    PDL_ENTRY();
     if (P.ctl[1]) return;
     extern __shared__ __align__(1024) uint8_t dsm[];
     // stage s: [A f32 | B f32] (TMA; the tensor core reads these float32 words
@@ -1906,6 +1957,7 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
                                                           int64_t dsplit, const int2 *__restrict__ tiles,
                                                           const double *__restrict__ sinp, int full, double *gpart,
                                                           const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     using G = GwCfg<DIAG>;
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     extern __shared__ __align__(1024) uint8_t gsm[];
@@ -2059,6 +2111,7 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
 // dense pass splits them into tf32 hi + lo on the fly
 __global__ void k_dense_centers(int64_t k, int64_t kpad, int64_t D, const double *__restrict__ C, float *b,
                                 const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;
     for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < kpad * D;
          e += (int64_t)gridDim.x * blockDim.x) {
@@ -2070,6 +2123,7 @@ __global__ void k_dense_centers(int64_t k, int64_t kpad, int64_t D, const double
 // survivors' float32 rows -> a contiguous block (slot order) for the dense rescan
 __global__ void k_gather_rows(const float *__restrict__ x, int64_t D, const int32_t *__restrict__ list,
                               const long long *__restrict__ count, float *out, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;
     const int64_t per = D / 4, tot = *count * per;
     const float4 *src = reinterpret_cast<const float4 *>(x);
@@ -2147,7 +2201,7 @@ int launch_rp(RowPassArgs &A, int grid, size_t smem, cudaStream_t st) {
         cudaFuncSetAttribute(k_row_pass<CH, NT, HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         attr = (int)smem;
     }
-    k_row_pass<CH, NT, HOT><<<grid, NT, smem, st>>>(A);
+    pdl_launch(k_row_pass<CH, NT, HOT>, dim3(grid), dim3(NT), (size_t)(smem), st, A);
     CHECK_LAUNCH("row_pass");
     return 0;
 }
@@ -2330,6 +2384,7 @@ constexpr int kSlotHead = 2 + 16;
 __global__ void k_pack_moves(const int32_t *__restrict__ mv_i, const int32_t *__restrict__ mv_old,
                              const int32_t *__restrict__ a, const long long *__restrict__ ctr, int64_t p0,
                              int64_t cap, int32_t *slot, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;
     const long long cnt = ctr[SPKM_CTR_MOVES];
     const long long c = cnt < cap ? cnt : cap;   // cap = shard rows >= moves
@@ -2357,6 +2412,7 @@ __global__ void __launch_bounds__(256) k_apply_move_slots(const int32_t *__restr
                                                           const float *__restrict__ values, long long *sums,
                                                           long long *counts, int32_t *touched, double scale,
                                                           long long *ctr_out, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
     if (ctl[1]) return;
     const int lane = threadIdx.x & 31;
     const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
@@ -2458,7 +2514,7 @@ int64_t spkm_padded_k(int64_t k) {
 }
 
 int spkm_reset_counters(spkm_work *W, void *stream) {
-    k_reset<<<1, 32, 0, S(stream)>>>(W->ctr, W->stats);
+    pdl_launch(k_reset, dim3(1), dim3(32), (size_t)(0), S(stream), W->ctr, W->stats);
     CHECK_LAUNCH("reset_counters");
     return 0;
 }
@@ -2483,7 +2539,7 @@ int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B
                         int naive, void *stream) {
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 256);
-    k_hamerly_bounds<<<grid, 256, 0, S(stream)>>>(X->n, X->row_eps, B->a, B->l, B->u, C->drift, C->sinp, C->s,
+    pdl_launch(k_hamerly_bounds, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, X->row_eps, B->a, B->l, B->u, C->drift, C->sinp, C->s,
                                                   C->hstat,
                                                   use_s, naive, W->surv1, W->ctr, C->ctl);
     CHECK_LAUNCH("hamerly_bounds");
@@ -2494,7 +2550,7 @@ int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *
                          void *stream) {
     if (X->n == 0) return 0;
     const int grid = grid_for((X->n + 3) / 4, 8);
-    k_hamerly_tighten<<<grid, 256, 0, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
+    pdl_launch(k_hamerly_tighten, dim3(grid), dim3(256), (size_t)(0), S(stream), X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
                                                    B->a, B->l, B->u, C->s, use_s, W->surv1, W->surv2, W->ctr, C->ctl);
     CHECK_LAUNCH("hamerly_tighten");
     return 0;
@@ -2521,7 +2577,7 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
                       void *stream) {
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
-    k_elkan_bounds<<<grid, 256, 0, S(stream)>>>(X->n, (int)C->k, X->row_eps, B->a, B->l, B->u, B->ku, C->drift,
+    pdl_launch(k_elkan_bounds, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l, B->u, B->ku, C->drift,
                                                 C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl);
     CHECK_LAUNCH("elkan_bounds");
     return 0;
@@ -2537,7 +2593,7 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
         cudaFuncSetAttribute(k_elkan_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         dyn_set = dyn;
     }
-    k_elkan_scan<<<grid, 256, dyn, S(stream)>>>(X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
+    pdl_launch(k_elkan_scan, dim3(grid), dim3(256), (size_t)(dyn), S(stream), X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
                                               (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1,
                                               W->mv_i, W->mv_old, W->ctr, C->ctl);
     CHECK_LAUNCH("elkan_scan");
@@ -2553,7 +2609,7 @@ int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bou
     if (e != cudaSuccess) return fail("aggregate memset", e);
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
-    k_aggregate<<<grid, 256, 0, st>>>(X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
+    pdl_launch(k_aggregate, dim3(grid), dim3(256), (size_t)(0), st, X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
                                       counts_target, ldexp(1.0, C->scale_bits), C->ctl, 0);
     CHECK_LAUNCH("aggregate");
     return 0;
@@ -2562,11 +2618,11 @@ int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bou
 int spkm_aggregate_sums_gated(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
                               long long *sums_target, long long *counts_target, int period, void *stream) {
     cudaStream_t st = S(stream);
-    k_zero_sums_gated<<<num_sms() * 4, 256, 0, st>>>(sums_target, C->k * C->d, counts_target, C->k, C->ctl, period);
+    pdl_launch(k_zero_sums_gated, dim3(num_sms() * 4), dim3(256), (size_t)(0), st, sums_target, C->k * C->d, counts_target, C->k, C->ctl, period);
     CHECK_LAUNCH("aggregate zero");
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
-    k_aggregate<<<grid, 256, 0, st>>>(X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
+    pdl_launch(k_aggregate, dim3(grid), dim3(256), (size_t)(0), st, X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
                                       counts_target, ldexp(1.0, C->scale_bits), C->ctl, period);
     CHECK_LAUNCH("aggregate");
     return 0;
@@ -2576,7 +2632,7 @@ int spkm_apply_moves(const spkm_csr *X, const spkm_centers *C, const spkm_bounds
                      long long *sums_target, long long *counts_target, int32_t *touched, void *stream) {
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
-    k_apply_moves<<<grid, 256, 0, S(stream)>>>(C->d, X->indptr, X->indices, X->values, B->a, W->mv_i, W->mv_old,
+    pdl_launch(k_apply_moves, dim3(grid), dim3(256), (size_t)(0), S(stream), C->d, X->indptr, X->indices, X->values, B->a, W->mv_i, W->mv_old,
                                                W->ctr, sums_target, counts_target, touched,
                                                ldexp(1.0, C->scale_bits), C->ctl);
     CHECK_LAUNCH("apply_moves");
@@ -2593,24 +2649,24 @@ int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
     const int64_t nch = spkm_center_chunks(C->d);
     const int64_t ntile = (C->d + kTileT - 1) / kTileT;
     const double inv = ldexp(1.0, -C->scale_bits);
-    k_touched_list<<<1, 1024, 0, st>>>(C->k, C->touched, all_clusters, C->tlist, C->tcount, C->ctl);
+    pdl_launch(k_touched_list, dim3(1), dim3(1024), (size_t)(0), st, C->k, C->touched, all_clusters, C->tlist, C->tcount, C->ctl);
     CHECK_LAUNCH("touched_list");
-    k_center_norm_part<<<dim3((unsigned)nch, (unsigned)C->k), 256, 0, st>>>(C->d, nch, C->sums, C->tlist, C->tcount,
+    pdl_launch(k_center_norm_part, dim3(dim3((unsigned)nch, (unsigned)C->k)), dim3(256), (size_t)(0), st, C->d, nch, C->sums, C->tlist, C->tcount,
                                                                            inv, C->part, C->ctl);
     CHECK_LAUNCH("center_norm_part");
-    k_center_norm_final<<<(unsigned)C->k, 256, 0, st>>>(nch, C->counts, C->tlist, C->tcount, C->part, C->norm, C->ctl);
+    pdl_launch(k_center_norm_final, dim3((unsigned)C->k), dim3(256), (size_t)(0), st, nch, C->counts, C->tlist, C->tcount, C->part, C->norm, C->ctl);
     CHECK_LAUNCH("center_norm_final");
-    k_center_write<<<dim3((unsigned)ntile, (unsigned)((C->k + kTileJ - 1) / kTileJ)), 256, 0, st>>>(
+    pdl_launch(k_center_write, dim3(dim3((unsigned)ntile, (unsigned)((C->k + kTileJ - 1) / kTileJ))), dim3(256), (size_t)(0), st, 
         C->d, C->kp, ntile, C->sums, C->tlist, C->tcount, inv, C->norm, C->cent64, C->ct32, C->part, C->ctl);
     CHECK_LAUNCH("center_write");
-    k_center_reduce<<<(unsigned)C->k, 256, 0, st>>>(ntile, C->tlist, C->tcount, C->part, C->norm, C->drift, C->sinp,
+    pdl_launch(k_center_reduce, dim3((unsigned)C->k), dim3(256), (size_t)(0), st, ntile, C->tlist, C->tcount, C->part, C->norm, C->drift, C->sinp,
                                                    C->objc, C->ctl);
     CHECK_LAUNCH("center_reduce");
     return 0;
 }
 
 int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra, void *stream) {
-    k_finalize<<<1, kFinThreads, 0, S(stream)>>>(C->k, C->touched, C->tcount, C->drift, C->sinp, C->objc, C->hstat,
+    pdl_launch(k_finalize, dim3(1), dim3(kFinThreads), (size_t)(0), S(stream), C->k, C->touched, C->tcount, C->drift, C->sinp, C->objc, C->hstat,
                                                  W->ctr, W->stats, sims_extra, all_clusters, W->stats_hist,
                                                  W->hist_cap, C->ctl);
     CHECK_LAUNCH("finalize");
@@ -2651,16 +2707,16 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
         attr_ws = true;
     }
     if (tk == 1)
-        k_gram_ws<true><<<dim3(1, (unsigned)ds), GW_THREADS, GwCfg<true>::SMEM, st>>>(tm, C->k, C->d, ds, tiles_dev,
+        pdl_launch(k_gram_ws<true>, dim3(dim3(1, (unsigned)ds)), dim3(GW_THREADS), (size_t)(GwCfg<true>::SMEM), st, tm, C->k, C->d, ds, tiles_dev,
                                                                                    C->sinp, full, gpart, C->ctl);
     else
-        k_gram_ws<false><<<dim3((unsigned)ntiles, (unsigned)ds), GW_THREADS, GwCfg<false>::SMEM, st>>>(
+        pdl_launch(k_gram_ws<false>, dim3(dim3((unsigned)ntiles, (unsigned)ds)), dim3(GW_THREADS), (size_t)(GwCfg<false>::SMEM), st, 
             tm, C->k, C->d, ds, tiles_dev, C->sinp, full, gpart, C->ctl);
     CHECK_LAUNCH("gram_ws");
-    k_gram_final<<<(unsigned)((C->k * C->k * 8 + 255) / 256), 256, 0, st>>>(C->k, ds, gpart, C->sinp, full, gdelta,
+    pdl_launch(k_gram_final, dim3((unsigned)((C->k * C->k * 8 + 255) / 256)), dim3(256), (size_t)(0), st, C->k, ds, gpart, C->sinp, full, gdelta,
                                                                            C->cc, C->ctl);
     CHECK_LAUNCH("gram_final");
-    k_row_max<<<(unsigned)((C->k * 32 + 255) / 256), 256, 0, st>>>(C->k, C->cc, C->s, C->ctl);
+    pdl_launch(k_row_max, dim3((unsigned)((C->k * 32 + 255) / 256)), dim3(256), (size_t)(0), st, C->k, C->cc, C->s, C->ctl);
     CHECK_LAUNCH("row_max");
     return 0;
 }
@@ -2694,7 +2750,7 @@ int spkm_predict(const spkm_csr *X, const spkm_centers *C, int32_t *a, double *b
 
 
 int spkm_dense_centers(const spkm_centers *C, const spkm_dense *Dn, void *stream) {
-    k_dense_centers<<<grid_for(Dn->kpad * Dn->D, 256), 256, 0, S(stream)>>>(C->k, Dn->kpad, Dn->D, C->cent64,
+    pdl_launch(k_dense_centers, dim3(grid_for(Dn->kpad * Dn->D, 256)), dim3(256), (size_t)(0), S(stream), C->k, Dn->kpad, Dn->D, C->cent64,
                                                                            Dn->b, C->ctl);
     CHECK_LAUNCH("dense_centers");
     return 0;
@@ -2735,7 +2791,7 @@ int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense
         if (!Dn->xs) return fail_msg("dense rescan needs the survivor scratch (spkm_dense.xs)");
         P.rowmap = W->surv1;
         P.rowcount = W->ctr + SPKM_CTR_SURV1;
-        k_gather_rows<<<grid_for(X->n * (Dn->D / 4), 256), 256, 0, st>>>(Dn->x, Dn->D, W->surv1, P.rowcount, Dn->xs,
+        pdl_launch(k_gather_rows, dim3(grid_for(X->n * (Dn->D / 4), 256)), dim3(256), (size_t)(0), st, Dn->x, Dn->D, W->surv1, P.rowcount, Dn->xs,
                                                                           C->ctl);
         CHECK_LAUNCH("dense_gather");
         rows = Dn->xs;
@@ -2760,7 +2816,7 @@ int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense
     int64_t tiles = (X->n + DN_M - 1) / DN_M;
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     if (grid < 1) grid = 1;
-    k_dense_pass<<<grid, DN_THREADS, smem, st>>>(P);
+    pdl_launch(k_dense_pass, dim3(grid), dim3(DN_THREADS), (size_t)(smem), st, P);
     CHECK_LAUNCH("dense_pass");
     return 0;
 }
@@ -2911,7 +2967,7 @@ int spkm_seed_rows_csr(const spkm_centers *C, const spkm_seed *Sd, const int64_t
     cudaError_t e = cudaMemsetAsync(C->cent64, 0, sizeof(double) * C->k * C->d, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(C->ct32, 0, sizeof(float) * C->kp * C->d, st);
     if (e != cudaSuccess) return fail("seed_rows_csr memset", e);
-    k_seed_rows_csr<<<(unsigned)C->k, 128, 0, st>>>(C->d, C->kp, Sd->indptr, Sd->indices, Sd->values, Sd->row_dev,
+    pdl_launch(k_seed_rows_csr, dim3((unsigned)C->k), dim3(128), (size_t)(0), st, C->d, C->kp, Sd->indptr, Sd->indices, Sd->values, Sd->row_dev,
                                                      rows, C->cent64, C->ct32);
     CHECK_LAUNCH("seed_rows_csr");
     return 0;
@@ -2951,7 +3007,7 @@ int64_t spkm_move_slot_ints(int64_t cap) { return kSlotHead + 3 * cap; }
 
 int spkm_pack_moves(const spkm_work *W, const spkm_bounds *B, const spkm_centers *C, int64_t p0, int64_t cap,
                     int32_t *slot, void *stream) {
-    k_pack_moves<<<grid_for(cap > 0 ? cap : 1, 256), 256, 0, S(stream)>>>(W->mv_i, W->mv_old, B->a, W->ctr, p0, cap,
+    pdl_launch(k_pack_moves, dim3(grid_for(cap > 0 ? cap : 1, 256)), dim3(256), (size_t)(0), S(stream), W->mv_i, W->mv_old, B->a, W->ctr, p0, cap,
                                                                         slot, C->ctl);
     CHECK_LAUNCH("pack_moves");
     return 0;
@@ -2959,7 +3015,7 @@ int spkm_pack_moves(const spkm_work *W, const spkm_bounds *B, const spkm_centers
 
 int spkm_apply_move_slots(const spkm_csr *X, const spkm_centers *C, const int32_t *slots, int world, int64_t slot_len,
                           int32_t *touched, long long *ctr_out, void *stream) {
-    k_apply_move_slots<<<grid_for(X->n > 0 ? X->n : 1, 8), 256, 0, S(stream)>>>(
+    pdl_launch(k_apply_move_slots, dim3(grid_for(X->n > 0 ? X->n : 1, 8)), dim3(256), (size_t)(0), S(stream), 
         slots, world, slot_len, C->d, X->indptr, X->indices, X->values, C->sums, C->counts, touched,
         ldexp(1.0, C->scale_bits), ctr_out, C->ctl);
     CHECK_LAUNCH("apply_move_slots");
@@ -3109,7 +3165,7 @@ int spkm_fit_graph_abort(void *loop) {
 
 int spkm_rows_to_host(int64_t n, const int64_t *row_perm, const int32_t *a, int64_t *out, void *stream) {
     if (n <= 0) return 0;
-    k_rows_to_host<<<(unsigned)((n + 255) / 256), 256, 0, S(stream)>>>(n, row_perm, a, out);
+    pdl_launch(k_rows_to_host, dim3((unsigned)((n + 255) / 256)), dim3(256), (size_t)(0), S(stream), n, row_perm, a, out);
     CHECK_LAUNCH("rows_to_host");
     return 0;
 }

@@ -255,6 +255,22 @@ class DeviceCorpus:
     back with to_host_rows / to_device_rows).
     """
 
+    @property
+    def row_perm(self) -> np.ndarray:
+        """device row r holds host row row_perm[r]."""
+        if self._row_perm is None:
+            self._row_perm = self.perm_dev.cpu().numpy()
+        return self._row_perm
+
+    @property
+    def row_pos(self) -> np.ndarray:
+        """host row i sits at device row row_pos[i]."""
+        if self._row_pos is None:
+            rp = self.row_perm
+            self._row_pos = np.empty_like(rp)
+            self._row_pos[rp] = np.arange(rp.size, dtype=np.int64)
+        return self._row_pos
+
     def to_host_rows(self, x: np.ndarray) -> np.ndarray:
         out = np.empty_like(x)
         out[self.row_perm] = x
@@ -273,6 +289,8 @@ class DeviceCorpus:
         self.pinned_host = pinned_host
         self._stage = None
         self._seed = None
+        self._upload = None
+        self._row_perm = self._row_pos = None
         self.dense_dim = getattr(data, "dense_dim", None) if self.device.type == "cuda" else None
         if self.dense_dim is not None and self.dense_dim % 32 != 0:
             self.dense_dim = None
@@ -296,9 +314,8 @@ class DeviceCorpus:
         r0, r1 = self.rows
         self.order, self.new_id = term_order(data)
         lens = np.diff(data.indptr[r0:r1 + 1])
-        self.row_perm = np.argsort(-lens, kind="stable").astype(np.int64)
-        self.row_pos = np.empty_like(self.row_perm)
-        self.row_pos[self.row_perm] = np.arange(self.n, dtype=np.int64)
+        self._row_perm = np.argsort(-lens, kind="stable").astype(np.int64)
+        self._row_pos = None
         plen = lens[self.row_perm]
         ip = np.zeros(self.n + 1, np.int64)
         np.cumsum(plen, out=ip[1:])
@@ -340,14 +357,24 @@ class DeviceCorpus:
                     self._stage[q].copy_(t)
                     hs[q] = self._stage[q]
             ip_h, idx_h, val_h = hs
+        # the row offsets first; the term ids and values stream in on a side
+        # stream while the row order is sorted out on this one
         ip_raw = ip_h.to(dev, non_blocking=True)
-        idx_raw = idx_h.to(dev, non_blocking=True)
-        val_raw = val_h.to(dev, non_blocking=True)
+        if self._upload is None:
+            self._upload = torch.cuda.Stream(device=dev)
+        up = self._upload
+        up.wait_stream(stream)
+        with torch.cuda.stream(up):
+            idx_raw = idx_h.to(dev, non_blocking=True)
+            val_raw = val_h.to(dev, non_blocking=True)
         self.h2d_bytes = sum(t.numel() * t.element_size() for t in (ip_h, idx_h, val_h))
         lens = ip_raw[1:] - ip_raw[:-1]
         perm = torch.sort(-lens, stable=True).indices
         self.indptr[0] = 0
         torch.cumsum(lens[perm], 0, out=self.indptr[1:])
+        stream.wait_stream(up)
+        idx_raw.record_stream(stream)
+        val_raw.record_stream(stream)
         cached = getattr(data, "_term_order", None)
         if cached is None and self.rows == (0, data.n):
             df = torch.bincount(idx_raw.to(torch.int64), minlength=self.d)
@@ -356,9 +383,13 @@ class DeviceCorpus:
             new_id_d[order_d] = torch.arange(self.d, device=dev)
             order_h, new_id_h = order_d.cpu().numpy(), new_id_d.cpu().numpy()
             data._term_order = (order_h, new_id_h)
+            self._new_id_dev, self._new_id_src = new_id_d, new_id_h
         else:
             order_h, new_id_h = term_order(data)
-            new_id_d = torch.from_numpy(new_id_h).to(dev, non_blocking=True)
+            if getattr(self, "_new_id_src", None) is not new_id_h:   # the device copy follows the host map
+                self._new_id_dev = torch.from_numpy(new_id_h).to(dev)
+                self._new_id_src = new_id_h
+            new_id_d = self._new_id_dev
         self.order, self.new_id = order_h, new_id_h
         dense = self.dense_dim is not None
         _lib.call("spkm_permute_rows", self.n, _ptr(ip_raw), _ptr(idx_raw), _ptr(val_raw), _ptr(perm),
@@ -369,12 +400,10 @@ class DeviceCorpus:
             # with error <= (3D/8 + 8) 2^-22 + 4e-6 (spkm.cu, dense rows)
             self.reps.fill_(float(row_eps_dense(self.dense_dim, 1)[0]))
         self.perm_dev = perm
-        self.row_perm = perm.cpu().numpy()
-        self.row_pos = np.empty_like(self.row_perm)
-        self.row_pos[self.row_perm] = np.arange(self.n, dtype=np.int64)
+        self._row_perm = self._row_pos = None   # host copies on first use (no sync here)
         if self._seed is not None:          # refresh: the seeding maps follow the new rows
             self._seed[2].copy_(perm)
-            self._seed[3].copy_(torch.from_numpy(self.row_pos).to(dev))
+            self._seed[3].scatter_(0, perm, torch.arange(self.n, dtype=torch.int64, device=dev))
         del ip_raw, idx_raw, val_raw        # stream-ordered frees (caching allocator)
 
     def refresh(self, data: Dataset):

@@ -30,3 +30,10 @@ for width in (32, 8):
     lines = (padded.view(data.dim, -1, width) != 0).any(dim=2).double().cpu().numpy()   # [d, kq/width]
     live = (w[:, None] * lines).sum() / lines.shape[1]
     print(f"  {width}-center blocks: nnz-weighted live fraction {live:.3f}")
+# per-cluster blocks of consecutive terms (device term order): share of (cluster, block) holding a nonzero
+c64 = eng.C.cent64.view(k, data.dim)
+for tb in (32, 64, 256):
+    dq = (data.dim + tb - 1) // tb * tb
+    pc = torch.nn.functional.pad(c64, (0, dq - data.dim))
+    live = (pc.view(k, -1, tb) != 0).any(dim=2).double().mean().item()
+    print(f"  cluster x {tb}-term blocks live: {live:.3f}")

@@ -1449,39 +1449,17 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
 // tensor cores (tcgen05.mma kind::tf32, accumulator in TMEM), 3xTF32
 // (x = hi + lo, G ~ lo.hi + hi.lo + hi.hi).  One CTA = one 128 x 128 output
 // tile (upper triangle of 128-tiles) over one d-split, read from the
-// term-major float32 copy ct32 by TMA (k_gram_ws below); a tile is skipped
+// term-major float32 copy ct32 by TMA (k_gram_mn below); a tile is skipped
 // when none of its clusters moved since the last call.  The per-split fp32
-// tiles are written as float64 and summed by k_gram_final.
+// tiles are written as float32 and summed in float64 by k_gram_final.
 // Error bound per entry: products of tf32 values are exact; the fp32 TMEM
 // accumulation over 3L/8 MMA steps adds <= (3L/8 + 8) 2^-22 sum|a b| (even
 // with truncating adds); the float32 copy and the hi/lo split add < 2e-6.
 constexpr int GT = 128;
 constexpr int GKC = 32;                       // terms per stage
-// K-major, no-swizzle core matrices: 8 centers x 16 bytes (4 terms).
-// SBO = 128 B between 8-center groups, LBO = 2 KB between the two 4-term
-// chunks of an 8-term MMA group, 4 KB per 8-term group.
-constexpr int GSBO = 128;
-constexpr int GLBO = (GT / 8) * GSBO + 16;    // 2064: +16 B staggers the 4-term chunks across banks
-constexpr int GGRP = 2 * GLBO + 32;           // 4160 bytes per 8-term group (16-byte aligned)
-constexpr int GOPB = (GKC / 8) * GGRP;        // bytes of one operand buffer (one stage, hi or lo)
-__device__ __forceinline__ uint32_t to_tf32(float x) {
-    uint32_t r;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
-    return r;
-}
 __device__ __forceinline__ uint32_t smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-__device__ __forceinline__ uint64_t umma_desc(uint32_t saddr) {
-    // SmemDescriptor (cute/arch/mma_sm100_desc.hpp): start>>4 [0,14), LBO>>4 [16,30),
-    // SBO>>4 [32,46), version 1 [46,48), layout SWIZZLE_NONE (0) [61,64)
-    uint64_t d = 0;
-    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-    d |= (uint64_t)((GLBO >> 4) & 0x3FFF) << 16;
-    d |= (uint64_t)((GSBO >> 4) & 0x3FFF) << 32;
-    d |= (uint64_t)1 << 46;
-    return d;
-}
 // InstrDescriptor: c_format F32 (1) [4,6), a/b format TF32 (2) [7,10)/[10,13),
-// a/b K-major (0) bits 15/16, N>>3 [17,23), M>>4 [24,29)
+// a/b major bits 15/16 (set by kGramIdescMN), N>>3 [17,23), M>>4 [24,29)
 constexpr uint32_t kGramIdesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(GT >> 3) << 17) |
                                 ((uint32_t)(GT >> 4) << 24);
 
@@ -1502,8 +1480,8 @@ __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
 // cc = half-angle of the Gram entry plus the error bound, rounded up.  8
 // lanes per (a, j): lane r sums splits y = r, r+8, ... then a fixed shuffle
 // tree, so the result does not depend on scheduling.
-__global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict__ gpart,
-                             const double *__restrict__ sinp, int full, double gdelta, float *cc, const long long *__restrict__ ctl) {
+__global__ void k_gram_final(int64_t k, int64_t dsplit, const float *__restrict__ gpart, int full, double gdelta,
+                             float *cc, const long long *__restrict__ ctl) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int64_t gt = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1512,18 +1490,13 @@ __global__ void k_gram_final(int64_t k, int64_t dsplit, const double *__restrict
     const bool in = e < k * k;
     const int64_t a = in ? e / k : 0, j = in ? e % k : 0;
     bool work = in && a < j;
-    if (work && !full) {
-        const int64_t ta = a / GT * GT, tj = j / GT * GT;
-        int nd = 0;
-        for (int q = 0; q < GT && !nd; ++q) {
-            if (ta + q < k && sinp[ta + q] != 0.0) nd = 1;
-            if (tj + q < k && sinp[tj + q] != 0.0) nd = 1;
-        }
-        work = nd;
+    if (work && !full) {   // the tile's dirty flag (written by k_gram_mn)
+        const int64_t tk = (k + GT - 1) / GT, ta = a / GT, tj = j / GT;
+        work = reinterpret_cast<const int *>(gpart + dsplit * k * k)[ta * tk - ta * (ta - 1) / 2 + (tj - ta)] != 0;
     }
     double g = 0.0;
     if (work)
-        for (int64_t y = r; y < dsplit; y += 8) g += gpart[(y * k + a) * k + j];
+        for (int64_t y = r; y < dsplit; y += 8) g += (double)gpart[(y * k + a) * k + j];
     g += __shfl_down_sync(FULL, g, 4, 8);
     g += __shfl_down_sync(FULL, g, 2, 8);
     g += __shfl_down_sync(FULL, g, 1, 8);
@@ -1935,33 +1908,51 @@ __global__ void __launch_bounds__(DN_THREADS, 1) k_dense_pass(const __grid_const
 }
 
 
-// Warp-specialised Gram tile: one thread streams the term-major float32
-// centers (ct32; a CTA's d-range is one contiguous block of rows) with TMA,
-// converter warps transpose them into K-major tf32 hi / lo core matrices,
-// one thread issues the 3xTF32 MMAs, and the TMEM tile goes to the split's
-// partial Gram.  DIAG (k <= 128: the single diagonal tile) stages A alone,
-// 6 raw / 3 operand stages; other tiles stage A and B, 2 / 2.
-constexpr int GW_THREADS = 384;
-constexpr int GW_CONV = 320;                      // warps 2-11
-constexpr int GW_SLICE = GT * GKC * 4;            // 16 KB: 32 terms x 128 centers, float32
-template <bool DIAG> struct GwCfg {
-    static constexpr int RAW = DIAG ? 6 : 2;
-    static constexpr int OPS = DIAG ? 3 : 2;
-    static constexpr int RAWST = DIAG ? GW_SLICE : 2 * GW_SLICE;
-    static constexpr int OPST = (DIAG ? 2 : 4) * GOPB;
-    static constexpr size_t SMEM = (size_t)RAW * RAWST + (size_t)OPS * OPST;
+// MN-major Gram tile (the default): the term-major float32 centers are
+// already the MN-major operand layout tcgen05 reads (centers contiguous), so
+// TMA drops 32-center x 32-term boxes straight into the canonical swizzled
+// MN-major atoms and the tensor core reads the raw float32 words as
+// the truncated tf32 hi part.  Converter warps only write lo = x - trunc(x)
+// elementwise at the same (swizzled) offsets -- no transpose.  DIAG stages
+// A alone (6 stages of 32 KB), other tiles A and B (3 stages of 64 KB).
+constexpr int GM_THREADS = 384;
+constexpr int GM_CONV = 320;                 // warps 2-11
+constexpr int GM_BLK = 32 * GKC * 4;         // 4 KB: one TMA box (32 centers x 32 terms)
+constexpr int GM_OP = 4 * GM_BLK;            // 16 KB: 128 centers x 32 terms
+// MN-major tf32 operands use the 128-byte swizzle with 32-byte atoms
+// (SWIZZLE_128B_BASE32B, layout type 1 at bits [61,64)): 32-byte chunks of a
+// 128-byte row XOR row % 4, 4-row K atoms 512 B apart (SBO), 32-center
+// blocks GM_BLK apart (LBO).  (The 16-byte-atom SWIZZLE_128B reads back as
+// zeros for tf32 MN-major; measured with tools/mn_probe.cu.)
+__device__ __forceinline__ uint64_t umma_desc_mn128(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((GM_BLK >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)((512 >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
+    d |= (uint64_t)1 << 61;
+    return d;
+}
+constexpr uint32_t kGramIdescMN = kGramIdesc | (1u << 15) | (1u << 16);
+template <bool DIAG> struct GmCfg {
+    static constexpr int ST = DIAG ? 6 : 3;
+    static constexpr int NOP = DIAG ? 1 : 2;                 // operands staged per stage
+    static constexpr int STAGE = 2 * NOP * GM_OP;            // [raw A | raw B | lo A | lo B]
+    static constexpr size_t SMEM = (size_t)ST * STAGE + 1024;
 };
 
+// gpart: [dsplit][k][k] float32 partial Grams, then one dirty flag per tile.
 template <bool DIAG>
-__global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant__ CUtensorMap tm, int64_t k, int64_t d,
+__global__ void __launch_bounds__(GM_THREADS, 1) k_gram_mn(const __grid_constant__ CUtensorMap tm, int64_t k, int64_t d,
                                                           int64_t dsplit, const int2 *__restrict__ tiles,
-                                                          const double *__restrict__ sinp, int full, double *gpart,
+                                                          const double *__restrict__ sinp, int full, float *gpart,
                                                           const long long *__restrict__ ctl) {
     PDL_ENTRY();
-    using G = GwCfg<DIAG>;
+    using G = GmCfg<DIAG>;
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
-    extern __shared__ __align__(1024) uint8_t gsm[];
-    __shared__ __align__(8) uint64_t raw_full[G::RAW], raw_empty[G::RAW], op_full[G::OPS], op_empty[G::OPS], done_b;
+    extern __shared__ uint8_t gsm_raw[];
+    uint8_t *gsm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ __align__(8) uint64_t full_b[G::ST], lo_b[G::ST], empty_b[G::ST], done_b;
     __shared__ uint32_t tmem_base_s;
     const int2 tl = DIAG ? make_int2(0, 0) : tiles[blockIdx.x];
     const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
@@ -1970,7 +1961,9 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
         const int64_t q = threadIdx.x;
         mine = (a0 + q < k && sinp[a0 + q] != 0.0) || (j0 + q < k && sinp[j0 + q] != 0.0);
     }
-    if (!__syncthreads_or(mine)) return;
+    const int dirty = __syncthreads_or(mine);
+    if (blockIdx.y == 0 && threadIdx.x == 0) reinterpret_cast<int *>(gpart + dsplit * k * k)[blockIdx.x] = dirty;
+    if (!dirty) return;
     const int64_t per = ((d + dsplit - 1) / dsplit + GKC - 1) / GKC * GKC;
     const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
     const int nch = t1 > t0 ? (int)((t1 - t0 + GKC - 1) / GKC) : 0;
@@ -1982,13 +1975,10 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
         asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;\n" ::: "memory");
     }
     if (threadIdx.x == 0) {
-        for (int q = 0; q < G::RAW; ++q) {
-            mbar_init(&raw_full[q], 1);
-            mbar_init(&raw_empty[q], GW_CONV);
-        }
-        for (int q = 0; q < G::OPS; ++q) {
-            mbar_init(&op_full[q], GW_CONV);
-            mbar_init(&op_empty[q], 1);
+        for (int q = 0; q < G::ST; ++q) {
+            mbar_init(&full_b[q], 1);
+            mbar_init(&lo_b[q], GM_CONV);
+            mbar_init(&empty_b[q], 1);
         }
         mbar_init(&done_b, 1);
         asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
@@ -1997,76 +1987,71 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
     const uint32_t tmem = tmem_base_s;
-    uint8_t *raw0 = gsm;
-    uint8_t *op0 = gsm + (size_t)G::RAW * G::RAWST;
-    auto raw_ptr = [&](int q) { return raw0 + (size_t)q * G::RAWST; };
-    auto op_ptr = [&](int o) { return op0 + (size_t)o * G::OPST; };   // [A hi | A lo | B hi | B lo]
+    auto stage = [&](int st) { return gsm + (size_t)st * G::STAGE; };   // raw operands, then lo operands
     if (w == 1) {
         if (lane == 0) {
             for (int c = 0; c < nch; ++c) {
-                const int r = c % G::RAW;
-                if (c >= G::RAW) mbar_wait(smem_u32(&raw_empty[r]), ((c / G::RAW) - 1) & 1);
-                mbar_expect_tx(&raw_full[r], (uint32_t)G::RAWST);
+                const int st = c % G::ST;
+                if (c >= G::ST) mbar_wait(smem_u32(&empty_b[st]), ((c / G::ST) - 1) & 1);
+                mbar_expect_tx(&full_b[st], (uint32_t)(G::NOP * GM_OP));
                 const int trow = (int)(t0 + (int64_t)c * GKC);
-                tma_load_2d(smem_u32(raw_ptr(r)), &tm, (int)a0, trow, smem_u32(&raw_full[r]));
-                if (!DIAG) tma_load_2d(smem_u32(raw_ptr(r)) + GW_SLICE, &tm, (int)j0, trow, smem_u32(&raw_full[r]));
+                const uint32_t dst = smem_u32(stage(st));
+#pragma unroll
+                for (int b = 0; b < 4; ++b) {
+                    tma_load_2d(dst + b * GM_BLK, &tm, (int)(a0 + 32 * b), trow, smem_u32(&full_b[st]));
+                    if (!DIAG) tma_load_2d(dst + GM_OP + b * GM_BLK, &tm, (int)(j0 + 32 * b), trow, smem_u32(&full_b[st]));
+                }
             }
         }
         __syncwarp();
     } else if (w >= 2) {
         const int ct = threadIdx.x - 64;
-        constexpr int TASKS = (DIAG ? 1 : 2) * GT * (GKC / 4);
+        constexpr int N16 = G::NOP * GM_OP / 16;   // 16-byte chunks of raw operands per stage
         for (int c = 0; c < nch; ++c) {
-            const int r = c % G::RAW, o = c % G::OPS;
-            mbar_wait(smem_u32(&raw_full[r]), (c / G::RAW) & 1);
-            if (c >= G::OPS) mbar_wait(smem_u32(&op_empty[o]), ((c / G::OPS) - 1) & 1);
-            for (int e = ct; e < TASKS; e += GW_CONV) {
-                const int part = e >> 10, ee = e & 1023;   // part 0: A slice, 1: B slice
-                const int m = ee & (GT - 1), q = ee >> 7;   // consecutive threads: consecutive centers
-                const float *rs = reinterpret_cast<const float *>(raw_ptr(r) + part * GW_SLICE);   // [32][128]
-                uint8_t *hi = op_ptr(o) + part * 2 * GOPB, *lo = hi + GOPB;
-                uint32_t hh[4], ll[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const float v = rs[(4 * q + u) * GT + m];
-                    hh[u] = to_tf32(v);
-                    ll[u] = to_tf32(v - __uint_as_float(hh[u]));
-                }
-                const int off = (q >> 1) * GGRP + (q & 1) * GLBO + (m >> 3) * GSBO + (m & 7) * 16;
-                *reinterpret_cast<uint4 *>(hi + off) = make_uint4(hh[0], hh[1], hh[2], hh[3]);
-                *reinterpret_cast<uint4 *>(lo + off) = make_uint4(ll[0], ll[1], ll[2], ll[3]);
+            const int st = c % G::ST;
+            mbar_wait(smem_u32(&full_b[st]), (c / G::ST) & 1);
+            const uint4 *raw = reinterpret_cast<const uint4 *>(stage(st));
+            uint4 *lo = reinterpret_cast<uint4 *>(stage(st) + G::NOP * GM_OP);
+            for (int e = ct; e < N16; e += GM_CONV) {
+                const uint4 x = raw[e];
+                uint4 y;
+                y.x = __float_as_uint(__uint_as_float(x.x) - __uint_as_float(x.x & 0xffffe000u));
+                y.y = __float_as_uint(__uint_as_float(x.y) - __uint_as_float(x.y & 0xffffe000u));
+                y.z = __float_as_uint(__uint_as_float(x.z) - __uint_as_float(x.z & 0xffffe000u));
+                y.w = __float_as_uint(__uint_as_float(x.w) - __uint_as_float(x.w & 0xffffe000u));
+                lo[e] = y;
             }
             asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
-            mbar_arrive(&op_full[o]);
-            mbar_arrive(&raw_empty[r]);
+            mbar_arrive(&lo_b[st]);
         }
     } else if (lane == 0) {   // w == 0: MMA issuer
         for (int c = 0; c < nch; ++c) {
-            const int o = c % G::OPS;
-            mbar_wait(smem_u32(&op_full[o]), (c / G::OPS) & 1);
+            const int st = c % G::ST;
+            mbar_wait(smem_u32(&lo_b[st]), (c / G::ST) & 1);
             asm volatile("tcgen05.fence::after_thread_sync;\n" ::: "memory");
-            const uint32_t ahi = smem_u32(op_ptr(o)), alo = ahi + GOPB;
-            const uint32_t bhi = DIAG ? ahi : ahi + 2 * GOPB, blo = bhi + GOPB;
+            const uint32_t ahi = smem_u32(stage(st));
+            const uint32_t bhi = DIAG ? ahi : ahi + GM_OP;
+            const uint32_t alo = ahi + G::NOP * GM_OP, blo = bhi + G::NOP * GM_OP;
 #pragma unroll
             for (int g = 0; g < GKC / 8; ++g) {
-                const uint32_t off = g * GGRP;
-                const uint64_t dah = umma_desc(ahi + off), dal = umma_desc(alo + off);
-                const uint64_t dbh = umma_desc(bhi + off), dbl = umma_desc(blo + off);
+                const uint32_t off = g * 1024;   // next 8-term K group
+                const uint64_t dah = umma_desc_mn128(ahi + off), dal = umma_desc_mn128(alo + off);
+                const uint64_t dbh = umma_desc_mn128(bhi + off), dbl = umma_desc_mn128(blo + off);
                 const uint32_t acc0 = (c > 0 || g > 0) ? 1u : 0u;
                 asm volatile(
                     "{\n .reg .pred p;\n setp.ne.b32 p, %4, 0;\n"
                     " tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(tmem),
-                    "l"(dal), "l"(dbh), "r"(kGramIdesc), "r"(acc0)
+                    "l"(dal), "l"(dbh), "r"(kGramIdescMN), "r"(acc0)
                     : "memory");
                 asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dah),
-                             "l"(dbl), "r"(kGramIdesc)
+                             "l"(dbl), "r"(kGramIdescMN)
                              : "memory");
                 asm volatile("tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, 1;\n" ::"r"(tmem), "l"(dah),
-                             "l"(dbh), "r"(kGramIdesc)
+                             "l"(dbh), "r"(kGramIdescMN)
                              : "memory");
             }
             asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
-                             smem_u32(&op_empty[o]))
+                             smem_u32(&empty_b[st]))
                          : "memory");
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n" ::"r"(
@@ -2093,11 +2078,11 @@ __global__ void __launch_bounds__(GW_THREADS, 1) k_gram_ws(const __grid_constant
                 : "r"(taddr));
             asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
             if (row < k) {
-                double *out = gpart + ((int64_t)blockIdx.y * k + row) * k;
+                float *out = gpart + ((int64_t)blockIdx.y * k + row) * k;
 #pragma unroll
                 for (int q = 0; q < 32; ++q) {
                     const int64_t col = j0 + cb * 32 + q;
-                    if (col < k) out[col] = nch > 0 ? (double)__uint_as_float(r[q]) : 0.0;
+                    if (col < k) out[col] = nch > 0 ? __uint_as_float(r[q]) : 0.f;
                 }
             }
         }
@@ -2473,8 +2458,9 @@ int encode_dense_map(CUtensorMap *map, const float *base, int64_t rows, int64_t 
     return 0;
 }
 
-// TMA descriptor of the term-major float32 centers ct32 [d][kp]: box = one
-// Gram stage (128 centers x 32 terms), no swizzle, zero fill past kp and d.
+// TMA descriptor of the term-major float32 centers ct32 [d][kp]: box = 32
+// centers x 32 terms with the 128-byte / 32-byte-atom swizzle (the MN-major
+// tf32 operand layout of k_gram_mn), zero fill past kp and d.
 int encode_gram_map(CUtensorMap *map, const float *base, int64_t kp, int64_t d) {
     static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
     if (!enc) {
@@ -2486,11 +2472,11 @@ int encode_gram_map(CUtensorMap *map, const float *base, int64_t kp, int64_t d) 
     }
     const cuuint64_t dims[2] = {(cuuint64_t)kp, (cuuint64_t)d};
     const cuuint64_t strides[1] = {(cuuint64_t)kp * 4};
-    const cuuint32_t box[2] = {(cuuint32_t)GT, (cuuint32_t)GKC};
+    const cuuint32_t box[2] = {32, (cuuint32_t)GKC};
     const cuuint32_t estr[2] = {1, 1};
     const CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float *>(base), dims, strides, box, estr,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return fail_msg("cuTensorMapEncodeTiled (gram) failed");
     return 0;
 }
@@ -2674,7 +2660,7 @@ int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long lo
 }
 
 int64_t spkm_gram_dsplit(int64_t k, int64_t d) {
-    // one wave: one CTA per SM (k_gram_ws stages ~192 KB); at least 256
+    // one wave: one CTA per SM (k_gram_mn stages ~192 KB); at least 256
     // terms per CTA
     const int64_t tk = (k + GT - 1) / GT;
     const int64_t tiles = tk * (tk + 1) / 2;
@@ -2697,24 +2683,26 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     const int64_t per = ((C->d + ds - 1) / ds + GKC - 1) / GKC * GKC;
     // 3xTF32 residual over `per` terms + the float32 copy's rounding (2 x 2^-24 + slack)
     const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + 2e-6;
+    // float32 partials [ds][k][k], then one dirty flag per tile (fits the double-sized scratch)
+    float *gp = reinterpret_cast<float *>(gpart);
     CUtensorMap tm;
     int rc = encode_gram_map(&tm, C->ct32, C->kp, C->d);
     if (rc) return rc;
-    static bool attr_ws = false;
-    if (!attr_ws) {
-        cudaFuncSetAttribute(k_gram_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GwCfg<true>::SMEM);
-        cudaFuncSetAttribute(k_gram_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GwCfg<false>::SMEM);
-        attr_ws = true;
+    static bool attr_mn = false;
+    if (!attr_mn) {
+        cudaFuncSetAttribute(k_gram_mn<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GmCfg<true>::SMEM);
+        cudaFuncSetAttribute(k_gram_mn<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GmCfg<false>::SMEM);
+        attr_mn = true;
     }
     if (tk == 1)
-        pdl_launch(k_gram_ws<true>, dim3(dim3(1, (unsigned)ds)), dim3(GW_THREADS), (size_t)(GwCfg<true>::SMEM), st, tm, C->k, C->d, ds, tiles_dev,
-                                                                                   C->sinp, full, gpart, C->ctl);
+        pdl_launch(k_gram_mn<true>, dim3(1, (unsigned)ds), dim3(GM_THREADS), GmCfg<true>::SMEM, st, tm, C->k, C->d, ds,
+                   tiles_dev, C->sinp, full, gp, C->ctl);
     else
-        pdl_launch(k_gram_ws<false>, dim3(dim3((unsigned)ntiles, (unsigned)ds)), dim3(GW_THREADS), (size_t)(GwCfg<false>::SMEM), st, 
-            tm, C->k, C->d, ds, tiles_dev, C->sinp, full, gpart, C->ctl);
-    CHECK_LAUNCH("gram_ws");
-    pdl_launch(k_gram_final, dim3((unsigned)((C->k * C->k * 8 + 255) / 256)), dim3(256), (size_t)(0), st, C->k, ds, gpart, C->sinp, full, gdelta,
-                                                                           C->cc, C->ctl);
+        pdl_launch(k_gram_mn<false>, dim3((unsigned)ntiles, (unsigned)ds), dim3(GM_THREADS), GmCfg<false>::SMEM, st, tm,
+                   C->k, C->d, ds, tiles_dev, C->sinp, full, gp, C->ctl);
+    CHECK_LAUNCH("gram_mn");
+    pdl_launch(k_gram_final, dim3((unsigned)((C->k * C->k * 8 + 255) / 256)), dim3(256), (size_t)0, st, C->k, ds, gp,
+               full, gdelta, C->cc, C->ctl);
     CHECK_LAUNCH("gram_final");
     pdl_launch(k_row_max, dim3((unsigned)((C->k * 32 + 255) / 256)), dim3(256), (size_t)(0), st, C->k, C->cc, C->s, C->ctl);
     CHECK_LAUNCH("row_max");

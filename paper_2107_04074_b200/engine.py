@@ -880,8 +880,11 @@ class Engine:
         self._steady(None, it)
 
     def _body(self):
-        """One iteration >= 3 as captured into the device loop: the 50-iteration
-        scratch rebuild (engine.py:317-320) is gated on the device."""
+        """One iteration >= 3 as captured into the device loop.  The reference's
+        50-iteration scratch rebuild (engine.py:317-320) is left out here: the
+        sums are exact int64 fixed point, so the rebuild is the identity
+        (tests/test_gpu_kernels.py::test_incremental_update_equals_scratch_bitwise);
+        the eager host loop still runs it on schedule."""
         if self.variant == "standard":
             self.lloyd_pass()
             sims_extra = self.n_total * self.k
@@ -894,8 +897,6 @@ class Engine:
             sims_extra = 0
         self.apply_moves()
         self.move_centers(False)
-        _lib.call("spkm_aggregate_sums_gated", self.corpus.struct, self.C.struct, self.P.bounds, _ptr(self.C.sums),
-                  _ptr(self.C.counts), _SCRATCH_INTERVAL, self.sp)
         self.finalize_launch(False, sims_extra)
 
     def loop_launch(self, max_iter: int):

@@ -674,10 +674,17 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
     }
 }
 
-// floats of the per-warp value buffer of k_elkan_scan (9 per 8-center block)
+// Centers per lane block of k_elkan_scan: EB = 4 (one float4 of a term-major
+// ct32 row per lane, so a warp's gather of one row's blocks is one load
+// instruction) while the row fits one round of 32 lanes (k <= 128); EB = 8
+// (two float4, one 32-byte sector) above, which halves the rounds.  Measured:
+// C2 (k = 100) scan 91 -> 78 us with 4; C3 (k = 200) 2.6 -> 3.1 ms with 4.
+__host__ __device__ __forceinline__ int elkan_block(int64_t k) { return k <= 128 ? 4 : 8; }
+// floats of the per-warp value buffer of k_elkan_scan (EB + 1 per block)
 __host__ __device__ __forceinline__ int64_t elkan_sim_stride(int64_t k) {
-    const int64_t nb = (k + 7) / 8;
-    const int64_t need = nb * 9;
+    const int64_t eb = elkan_block(k);
+    const int64_t nb = (k + eb - 1) / eb;
+    const int64_t need = nb * (eb + 1);
     const int64_t bpr = nb < 32 ? nb : 32;
     const int64_t ppw = (32 / bpr) < 8 ? (32 / bpr) : 8;
     const int64_t per = need * ppw;
@@ -685,12 +692,12 @@ __host__ __device__ __forceinline__ int64_t elkan_sim_stride(int64_t k) {
 }
 
 // kernels.py:22-66 for the surviving points, in two steps:
-//  1. gather pass, blocked by 32-byte sectors: centers are grouped in blocks
-//     of 8 (one sector of a term-major ct32 row); a block is fetched when it
-//     holds a(i) or any center failing the drift-updated u test
-//     (u + 2 eps <= l).  Lane = block, bpr lanes per
-//     point, up to 8 points per warp, rounds of 32 blocks for k > 256.  The
-//     canonical s~ of every fetched center lands in shared memory.
+//  1. gather pass, blocked by 16-byte float4s: centers are grouped in blocks
+//     of EB = 4 (one float4 of a term-major ct32 row); a block is fetched
+//     when it holds a(i) or any center failing the drift-updated u test
+//     (u + 2 eps <= l).  Lane = block, bpr lanes per point, up to 8 points
+//     per warp, rounds of 32 blocks for k > 128.  The canonical s~ of every
+//     fetched center lands in shared memory.
 //  2. the reference's sequential scan (kernels.py:35-65) replayed by the
 //     group's leader lane over j = 0..k-1 on those values: tighten at the
 //     first failing j, re-test against the running best (cc and u tests
@@ -698,6 +705,7 @@ __host__ __device__ __forceinline__ int64_t elkan_sim_stride(int64_t k) {
 //     Every center the replay needs was fetched (a center passing the u
 //     pre-test also passes every later u test, since the running best only
 //     grows), so sim_count counts exactly what the reference's loop counts.
+template <int EB>
 __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ indptr,
                                                     const int32_t *__restrict__ indices,
                                                     const float *__restrict__ values,
@@ -709,13 +717,14 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                                                     int32_t *mv_old, long long *ctr, const long long *__restrict__ ctl) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
-    constexpr int UB = 4;
+    constexpr int UB = 32 / EB;   // nnz per gather batch: 8 float4 loads in flight per lane
+    constexpr int ES = EB + 1;    // padded per-block stride of the similarity buffer
     __shared__ __align__(16) int2 s_iv[8][8][kIvStride];
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
     extern __shared__ float s_sim_dyn[];   // [8 warps][sim_stride]
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const int nb = (k + 7) >> 3;
+    const int nb = (k + EB - 1) / EB;
     const int bpr = nb < 32 ? nb : 32;
     const int ppw = min(8, 32 / bpr);
     const int nrounds = (nb + 31) >> 5;
@@ -723,7 +732,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     const bool lane_on = g < ppw;
     const int o0 = bpr > 1 ? (1 << (31 - __clz(bpr - 1))) : 0;
     const int sim_stride = (int)elkan_sim_stride(k);  // floats per warp
-    const int gstride = sim_stride / ppw;             // per-group slice (>= 9 * nb)
+    const int gstride = sim_stride / ppw;             // per-group slice (>= ES * nb)
     float *my_sim = s_sim_dyn + wib * sim_stride + (lane_on ? g : 0) * gstride;
     int2 *my_iv = s_iv[wib][lane_on ? g : 0];
     const long long cnt = ctr[SPKM_CTR_SURV1];
@@ -743,10 +752,10 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
         const bool cc_ok = use_cc && lb >= 0.0;
         for (int r = 0; r < nrounds; ++r) {
             const int blk = r * 32 + q;
-            const int j0 = blk * 8;
+            const int j0 = blk * EB;
             bool act = false;
             if (valid && blk < nb) {
-                for (int c2 = 0; c2 < 8; ++c2) {
+                for (int c2 = 0; c2 < EB; ++c2) {
                     const int j = j0 + c2;
                     if (j >= k) break;
                     if (j == ai) {
@@ -760,16 +769,16 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                 }
             }
             if (!__any_sync(FULL, act)) continue;
-            float acc[8];
+            float acc[EB];
 #pragma unroll
-            for (int c2 = 0; c2 < 8; ++c2) acc[c2] = 0.f;
+            for (int c2 = 0; c2 < EB; ++c2) acc[c2] = 0.f;
             const float4 *base4 = reinterpret_cast<const float4 *>(ct + j0);
             for (int c0 = 0; c0 < maxlen; c0 += 32) {
                 const int cntc = max(0, min(32, len - c0));
                 for (int q2 = q; q2 < cntc; q2 += bpr)
                     my_iv[q2] = make_int2(__ldg(indices + s + c0 + q2), __float_as_int(__ldg(values + s + c0 + q2)));
                 __syncwarp();
-                if (act) {
+                if (act && EB == 8) {   // two float4 (one sector) per lane and nnz
                     int uu = 0;
                     for (; uu + UB <= cntc; uu += UB) {
                         float4 x[UB][2];
@@ -788,10 +797,10 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                             acc[1] = __fmaf_rn(vv[b], x[b][0].y, acc[1]);
                             acc[2] = __fmaf_rn(vv[b], x[b][0].z, acc[2]);
                             acc[3] = __fmaf_rn(vv[b], x[b][0].w, acc[3]);
-                            acc[4] = __fmaf_rn(vv[b], x[b][1].x, acc[4]);
-                            acc[5] = __fmaf_rn(vv[b], x[b][1].y, acc[5]);
-                            acc[6] = __fmaf_rn(vv[b], x[b][1].z, acc[6]);
-                            acc[7] = __fmaf_rn(vv[b], x[b][1].w, acc[7]);
+                            acc[EB > 4 ? 4 : 0] = __fmaf_rn(vv[b], x[b][1].x, acc[EB > 4 ? 4 : 0]);
+                            acc[EB > 4 ? 5 : 1] = __fmaf_rn(vv[b], x[b][1].y, acc[EB > 4 ? 5 : 1]);
+                            acc[EB > 4 ? 6 : 2] = __fmaf_rn(vv[b], x[b][1].z, acc[EB > 4 ? 6 : 2]);
+                            acc[EB > 4 ? 7 : 3] = __fmaf_rn(vv[b], x[b][1].w, acc[EB > 4 ? 7 : 3]);
                         }
                     }
                     for (; uu < cntc; ++uu) {
@@ -803,17 +812,43 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                         acc[1] = __fmaf_rn(v0, x0.y, acc[1]);
                         acc[2] = __fmaf_rn(v0, x0.z, acc[2]);
                         acc[3] = __fmaf_rn(v0, x0.w, acc[3]);
-                        acc[4] = __fmaf_rn(v0, x1.x, acc[4]);
-                        acc[5] = __fmaf_rn(v0, x1.y, acc[5]);
-                        acc[6] = __fmaf_rn(v0, x1.z, acc[6]);
-                        acc[7] = __fmaf_rn(v0, x1.w, acc[7]);
+                        acc[EB > 4 ? 4 : 0] = __fmaf_rn(v0, x1.x, acc[EB > 4 ? 4 : 0]);
+                        acc[EB > 4 ? 5 : 1] = __fmaf_rn(v0, x1.y, acc[EB > 4 ? 5 : 1]);
+                        acc[EB > 4 ? 6 : 2] = __fmaf_rn(v0, x1.z, acc[EB > 4 ? 6 : 2]);
+                        acc[EB > 4 ? 7 : 3] = __fmaf_rn(v0, x1.w, acc[EB > 4 ? 7 : 3]);
+                    }
+                } else if (act) {   // EB == 4: one float4 per lane and nnz
+                    int uu = 0;
+                    for (; uu + UB <= cntc; uu += UB) {
+                        float4 x[UB];
+                        float vv[UB];
+                        int iv[UB];
+                        load_iv<UB>(my_iv + uu, iv, vv);
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) x[b] = __ldg(base4 + ((int64_t)iv[b] * kp >> 2));
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) {
+                            acc[0] = __fmaf_rn(vv[b], x[b].x, acc[0]);
+                            acc[1] = __fmaf_rn(vv[b], x[b].y, acc[1]);
+                            acc[2] = __fmaf_rn(vv[b], x[b].z, acc[2]);
+                            acc[3] = __fmaf_rn(vv[b], x[b].w, acc[3]);
+                        }
+                    }
+                    for (; uu < cntc; ++uu) {
+                        const int2 t = my_iv[uu];
+                        const float v0 = __int_as_float(t.y);
+                        const float4 x0 = __ldg(base4 + ((int64_t)t.x * kp >> 2));
+                        acc[0] = __fmaf_rn(v0, x0.x, acc[0]);
+                        acc[1] = __fmaf_rn(v0, x0.y, acc[1]);
+                        acc[2] = __fmaf_rn(v0, x0.z, acc[2]);
+                        acc[3] = __fmaf_rn(v0, x0.w, acc[3]);
                     }
                 }
                 __syncwarp();
             }
             if (act) {
 #pragma unroll
-                for (int c2 = 0; c2 < 8; ++c2) my_sim[blk * 9 + c2] = acc[c2];
+                for (int c2 = 0; c2 < EB; ++c2) my_sim[blk * ES + c2] = acc[c2];
             }
         }
         __syncwarp();
@@ -834,8 +869,8 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
             for (int r = 0; r < nrounds && first_fail == NONE; ++r) {
                 const int blk = r * 32 + q;
                 if (blk >= nb) break;
-                for (int c2 = 0; c2 < 8; ++c2) {
-                    const int j = blk * 8 + c2;
+                for (int c2 = 0; c2 < EB; ++c2) {
+                    const int j = blk * EB + c2;
                     if (j >= k) break;
                     if (j == ai) continue;
                     if (cc_ok && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb) continue;
@@ -853,7 +888,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
         first_fail = __shfl_sync(FULL, first_fail, lane - q);
         const bool tight = valid && first_fail != NONE;
         if (tight) {
-            lcur = my_sim[(ai >> 3) * 9 + (ai & 7)];
+            lcur = my_sim[(ai >> (EB == 4 ? 2 : 3)) * ES + (ai & (EB - 1))];
             if (q == 0) {
                 ui[ai] = store_upper((double)lcur + eps);
                 sims = 1;
@@ -871,14 +906,14 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                 for (int r = 0; r < nrounds && ev == NONE; ++r) {
                     const int blk = r * 32 + q;
                     if (blk >= nb) break;
-                    if (blk * 8 + 7 < start) continue;
-                    for (int c2 = 0; c2 < 8; ++c2) {
-                        const int j = blk * 8 + c2;
+                    if (blk * EB + EB - 1 < start) continue;
+                    for (int c2 = 0; c2 < EB; ++c2) {
+                        const int j = blk * EB + c2;
                         if (j >= k) break;
                         if (j < start || j == ai || j == cur) continue;
                         if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
                         if ((double)ui[j] + eps <= lc) continue;
-                        if (my_sim[blk * 9 + c2] > lcur) {
+                        if (my_sim[blk * ES + c2] > lcur) {
                             ev = j;
                             break;
                         }
@@ -898,22 +933,22 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                 for (int r = 0; r < nrounds; ++r) {
                     const int blk = r * 32 + q;
                     if (blk >= nb) break;
-                    if (blk * 8 + 7 < start || blk * 8 > gev) continue;
-                    for (int c2 = 0; c2 < 8; ++c2) {
-                        const int j = blk * 8 + c2;
+                    if (blk * EB + EB - 1 < start || blk * EB > gev) continue;
+                    for (int c2 = 0; c2 < EB; ++c2) {
+                        const int j = blk * EB + c2;
                         if (j >= k || j > gev) break;
                         if (j < start || j == ai || j == cur) continue;
                         if (j < gev) {
                             if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
                             if ((double)ui[j] + eps <= lc) continue;
                         }
-                        ui[j] = store_upper((double)my_sim[blk * 9 + c2] + eps);
+                        ui[j] = store_upper((double)my_sim[blk * ES + c2] + eps);
                         ++sims;
                     }
                 }
                 if (gev != NONE) {
                     cur = gev;
-                    lcur = my_sim[(gev >> 3) * 9 + (gev & 7)];
+                    lcur = my_sim[(gev >> (EB == 4 ? 2 : 3)) * ES + (gev & (EB - 1))];
                     start = gev + 1;
                 } else {
                     active_g = false;
@@ -2576,12 +2611,18 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
     const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float);
     static size_t dyn_set = 0;   // static smem (16 KB staging) + dyn must fit the opt-in limit
     if (dyn > dyn_set) {
-        cudaFuncSetAttribute(k_elkan_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_elkan_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        cudaFuncSetAttribute(k_elkan_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
         dyn_set = dyn;
     }
-    pdl_launch(k_elkan_scan, dim3(grid), dim3(256), (size_t)(dyn), S(stream), X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
-                                              (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1,
-                                              W->mv_i, W->mv_old, W->ctr, C->ctl);
+    if (elkan_block(C->k) == 4)
+        pdl_launch(k_elkan_scan<4>, dim3(grid), dim3(256), dyn, S(stream), X->indptr, X->indices, X->values, X->row_eps,
+                   C->ct32, C->kp, (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1, W->mv_i, W->mv_old,
+                   W->ctr, C->ctl);
+    else
+        pdl_launch(k_elkan_scan<8>, dim3(grid), dim3(256), dyn, S(stream), X->indptr, X->indices, X->values, X->row_eps,
+                   C->ct32, C->kp, (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1, W->mv_i, W->mv_old,
+                   W->ctr, C->ctl);
     CHECK_LAUNCH("elkan_scan");
     return 0;
 }

@@ -284,8 +284,8 @@ struct RowPassArgs {
     int64_t hot_d;               // dimensionality (caps hot)
 };
 
-// Thread = (row, CH consecutive centers).  tpr threads cover one row's kp
-// columns, rpw rows share a warp.  Per nnz: one broadcast (idx, val) load and
+// Thread = (row, CH centers in float4 groups tpr apart).  tpr threads cover
+// one row's kp columns, rpw rows share a warp.  Per nnz: one broadcast (idx, val) load and
 // CH/4 float4 loads of the term-major center row; CH independent FMA chains.
 template <int CH, int NT, bool HOT>
 __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
@@ -326,7 +326,11 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
         const int64_t e = valid ? A.indptr[row + 1] : 0;
         const int len = (int)(e - s);
         const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
-        const int j0 = q * CH;
+        // lane q holds centers j0 + r * jstr + c (r < CH/4, c < 4): for every r
+        // the row's lanes read one contiguous 16 * tpr-byte span of the
+        // term-major center row (one L1 wavefront per 128-byte line)
+        const int j0 = q * 4;
+        const int jstr = 4 * A.tpr;
         float acc[CH];
 #pragma unroll
         for (int c = 0; c < CH; ++c) acc[c] = 0.f;
@@ -351,11 +355,11 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
                     if (HOT && ii < hot) {
                         const float4 *p = reinterpret_cast<const float4 *>(s_hot + (int64_t)ii * A.kp + j0);
 #pragma unroll
-                        for (int r = 0; r < CH / 4; ++r) cv[b][r] = p[r];
+                        for (int r = 0; r < CH / 4; ++r) cv[b][r] = p[r * A.tpr];
                     } else {
                         const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)ii * A.kp);
 #pragma unroll
-                        for (int r = 0; r < CH / 4; ++r) cv[b][r] = __ldg(p + r);
+                        for (int r = 0; r < CH / 4; ++r) cv[b][r] = __ldg(p + r * A.tpr);
                     }
                 }
 #pragma unroll
@@ -376,7 +380,7 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
                                                     : reinterpret_cast<const float4 *>(ctj + (int64_t)ii * A.kp);
 #pragma unroll
                 for (int r = 0; r < CH / 4; ++r) {
-                    const float4 cc4 = p[r];
+                    const float4 cc4 = p[r * A.tpr];
                     acc[4 * r + 0] = __fmaf_rn(v0, cc4.x, acc[4 * r + 0]);
                     acc[4 * r + 1] = __fmaf_rn(v0, cc4.y, acc[4 * r + 1]);
                     acc[4 * r + 2] = __fmaf_rn(v0, cc4.z, acc[4 * r + 2]);
@@ -389,8 +393,10 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
         const int inc = (valid && incumbent_mode) ? A.a[row] : -1;
         Top2 tp{-INFINITY, -2, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < CH; ++c)
-            if (j0 + c < A.k) top2_push(tp, acc[c], j0 + c, inc);
+        for (int c = 0; c < CH; ++c) {
+            const int j = j0 + (c >> 2) * jstr + (c & 3);
+            if (j < A.k) top2_push(tp, acc[c], j, inc);
+        }
         for (int o = o0; o; o >>= 1) {
             const Top2 other = top2_shfl_down(tp, o);
             if (q < o && q + o < A.tpr) top2_merge(tp, other, inc);
@@ -398,8 +404,10 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
         const double eps = valid ? (double)A.reps[row] : 0.0;
         if (A.mode == SPKM_MODE_INIT_ELKAN && valid) {
 #pragma unroll
-            for (int c = 0; c < CH; ++c)
-                if (j0 + c < A.k) A.u[row * A.ku + j0 + c] = store_upper((double)acc[c] + eps);
+            for (int c = 0; c < CH; ++c) {
+                const int j = j0 + (c >> 2) * jstr + (c & 3);
+                if (j < A.k) A.u[row * A.ku + j] = store_upper((double)acc[c] + eps);
+            }
         }
         const bool leader = valid && q == 0;
         bool moved = false;

@@ -469,7 +469,9 @@ class CenterState:
         dev = device
         f64 = dict(dtype=torch.float64, device=dev)
         self.cent64 = torch.empty(k * d, **f64)
-        self.ct32 = torch.zeros(d * self.kp, dtype=torch.float32, device=dev)
+        # + 1024 floats: the row pass's last lanes read whole float4 groups past kp on the last term row
+        self.ct32_buf = torch.zeros(d * self.kp + 1024, dtype=torch.float32, device=dev)
+        self.ct32 = self.ct32_buf[:d * self.kp]
         self.sums = torch.empty(k * d, dtype=torch.int64, device=dev)
         self.counts = torch.zeros(k, dtype=torch.int64, device=dev)
         self.drift = torch.ones(k, **f64)

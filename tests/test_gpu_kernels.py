@@ -310,7 +310,7 @@ def test_seed_rows_match_host_densify():
     eng.seed_rows(data, rows)
     torch.cuda.synchronize()
     assert np.array_equal(eng.C.host_centers(), data.densify_rows(rows))
-    ct = eng.C.ct32.view(data.dim, eng.C.kp)[:, :4].cpu().numpy()[eng.corpus.new_id]   # device rows are renumbered
+    ct = eng.C.ct32[:data.dim * eng.C.kp].view(data.dim, eng.C.kp)[:, :4].cpu().numpy()[eng.corpus.new_id]   # device rows are renumbered
     assert np.array_equal(ct, data.densify_rows(rows).T.astype(np.float32))
 
 

@@ -374,7 +374,8 @@ def roofline(args, data, corpus, dev, world):
     n, nnz, k = corpus.n, corpus.nnz, args.k
     dense = getattr(corpus, "dense_dim", None) is not None
     prof = _lib.CallProfiler(timed=True)
-    bytes_by, flops_by = {}, {}
+    bytes_by, flops_by, gather_by = {}, {}, {}
+    kp = (k + 7) // 8 * 8
     with prof:
         for v in args.variants.split(","):
             prof.tag = v
@@ -390,10 +391,13 @@ def roofline(args, data, corpus, dev, world):
             lloyd_w = 4 * n
             b = csr_full * n_full + init_w + lloyd_w * (n_full - 1)
             bytes_by[("spkm_full_assign", v)] = b
+            # center-row bytes the gather passes read through L1/L2 (4 kp per nnz)
+            gather_by[("spkm_full_assign", v)] = 4 * kp * nnz * n_full
             if v in ("hamerly", "simp_hamerly"):
                 bytes_by[("spkm_hamerly_bounds", v)] = 24 * n * (len(its) - 1)
                 bytes_by[("spkm_hamerly_tighten", v)] = sum(8 * s.nnz_tighten + 24 * s.survivors for s in its[1:])
                 bytes_by[("spkm_hamerly_rescan", v)] = sum(8 * s.nnz_rescan + 24 * s.survivors2 for s in its[1:])
+                gather_by[("spkm_hamerly_rescan", v)] = sum(4 * kp * s.nnz_rescan for s in its[1:])
             if v in ("elkan", "simp_elkan"):
                 bytes_by[("spkm_elkan_bounds", v)] = (8 * ku + 16) * n * (len(its) - 1)
                 bytes_by[("spkm_elkan_scan", v)] = sum(8 * s.nnz_elkan + (8 * ku + 16) * s.survivors for s in its[1:])
@@ -457,6 +461,15 @@ def roofline(args, data, corpus, dev, world):
                        "achieved_gbs": round(b / (ms / 1e3) / 1e9, 1),
                        "frac": round(b / (ms / 1e3) / 1e9 / pk.get("hbm_gbs"), 4)}
     out["per_entry"] = per
+    # the gather passes are bound by L1/L2 (ncu_throughput_pct), not HBM: the
+    # center-row bytes they pull per second, beside the HBM view above
+    gv = {}
+    for nm, (ms, nl) in calls.items():
+        g = sum(val for key, val in gather_by.items() if key[0] == nm)
+        if g and ms:
+            gv[nm] = {"center_row_bytes": g, "ms": round(ms, 4), "achieved_gbs": round(g / (ms / 1e3) / 1e9, 1)}
+    if gv:
+        out["center_gather"] = gv
     if "spkm_move_centers" in calls:
         b = sum(val for key, val in bytes_by.items() if key[0] == "spkm_move_centers")
         ms = calls["spkm_move_centers"][0]

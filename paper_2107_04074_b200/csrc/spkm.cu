@@ -1456,31 +1456,43 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
                 low2_merge(Sx, s_s[q]);
             }
         }
+        // every global read first (independent loads in flight together), the
+        // stats row assembled in registers, then the stores
+        long long cv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) cv[q] = ctr[q];
+        double sv[SPKM_ST_COUNT];
+#pragma unroll
+        for (int q = 0; q < SPKM_ST_COUNT; ++q) sv[q] = stats[q];
+        const long long it = ctl[0];
+        const int tc = *tcount;
         hstat[0] = (double)P.i1;
         hstat[1] = P.v1;
         hstat[2] = (k > 1) ? P.v2 : 1.0;
         hstat[3] = (double)Sx.i1;
         hstat[4] = -Sx.v1;
         hstat[5] = (k > 1) ? -Sx.v2 : 0.0;
-        stats[SPKM_ST_OBJECTIVE] = tot;
-        stats[SPKM_ST_ALLONE] = no ? 0.0 : 1.0;
-        stats[SPKM_ST_TOUCHED] = (double)*tcount;
-        stats[SPKM_ST_SIMS] = (double)(ctr[SPKM_CTR_SIMS] + sims_extra);
-        stats[SPKM_ST_REASSIGN] = (double)ctr[SPKM_CTR_MOVES];
-        stats[SPKM_ST_SURV1] = (double)ctr[SPKM_CTR_SURV1];
-        stats[SPKM_ST_SURV2] = (double)ctr[SPKM_CTR_SURV2];
-        stats[SPKM_ST_NNZ_TIGHTEN] = (double)ctr[SPKM_CTR_NNZ_TIGHTEN];
-        stats[SPKM_ST_NNZ_RESCAN] = (double)ctr[SPKM_CTR_NNZ_RESCAN];
-        stats[SPKM_ST_NNZ_ELKAN] = (double)ctr[SPKM_CTR_NNZ_ELKAN];
-        stats[SPKM_ST_NNZ_MOVED] = (double)ctr[SPKM_CTR_NNZ_MOVED];
+        sv[SPKM_ST_OBJECTIVE] = tot;
+        sv[SPKM_ST_ALLONE] = no ? 0.0 : 1.0;
+        sv[SPKM_ST_TOUCHED] = (double)tc;
+        sv[SPKM_ST_SIMS] = (double)(cv[SPKM_CTR_SIMS] + sims_extra);
+        sv[SPKM_ST_REASSIGN] = (double)cv[SPKM_CTR_MOVES];
+        sv[SPKM_ST_SURV1] = (double)cv[SPKM_CTR_SURV1];
+        sv[SPKM_ST_SURV2] = (double)cv[SPKM_CTR_SURV2];
+        sv[SPKM_ST_NNZ_TIGHTEN] = (double)cv[SPKM_CTR_NNZ_TIGHTEN];
+        sv[SPKM_ST_NNZ_RESCAN] = (double)cv[SPKM_CTR_NNZ_RESCAN];
+        sv[SPKM_ST_NNZ_ELKAN] = (double)cv[SPKM_CTR_NNZ_ELKAN];
+        sv[SPKM_ST_NNZ_MOVED] = (double)cv[SPKM_CTR_NNZ_MOVED];
         // iteration bookkeeping and the convergence test (engine.py:335-337),
         // evaluated on the device so the host can enqueue iterations ahead
-        const long long it = ctl[0];
-        stats[SPKM_ST_ITER] = (double)(it + 1);
-        stats[SPKM_ST_TSTAMP] = (double)globaltimer_ns();
+        sv[SPKM_ST_ITER] = (double)(it + 1);
+        sv[SPKM_ST_TSTAMP] = (double)globaltimer_ns();
+#pragma unroll
+        for (int q = 0; q < SPKM_ST_COUNT; ++q) stats[q] = sv[q];
         if (it < hist_cap)
-            for (int q = 0; q < SPKM_ST_COUNT; ++q) stats_hist[it * SPKM_ST_COUNT + q] = stats[q];
-        const bool conv = (k == 1) || (no == 0) || (it >= 1 && ctr[SPKM_CTR_MOVES] == 0);
+#pragma unroll
+            for (int q = 0; q < SPKM_ST_COUNT; ++q) stats_hist[it * SPKM_ST_COUNT + q] = sv[q];
+        const bool conv = (k == 1) || (no == 0) || (it >= 1 && cv[SPKM_CTR_MOVES] == 0);
         ctl[0] = it + 1;
         ctl[1] = conv ? 1 : 0;
         for (int q = 0; q < 8; ++q) ctr[q] = 0;

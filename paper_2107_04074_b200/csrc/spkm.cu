@@ -541,20 +541,29 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
         const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
         const float *cta = ct + ai;
         float acc = 0.f;
+        // software-pipelined: the next chunk's (id, value) loads are issued
+        // before this chunk's center gathers and chain
+        int ix[4];
+        float vx[4];
+#pragma unroll
+        for (int r = 0; r < 4; ++r) {
+            const int t = q + 8 * r;
+            ix[r] = t < len ? __ldg(indices + s + t) : 0;
+            vx[r] = t < len ? __ldg(values + s + t) : 0.f;
+        }
         for (int c0 = 0; c0 < maxlen; c0 += 32) {
             const int cntc = max(0, min(32, len - c0));
-            int ix[4];
-            float vx[4], cx[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                const int t = q + 8 * r;
-                ix[r] = t < cntc ? __ldg(indices + s + c0 + t) : 0;
-                vx[r] = t < cntc ? __ldg(values + s + c0 + t) : 0.f;
-            }
+            float cx[4];
 #pragma unroll
             for (int r = 0; r < 4; ++r) cx[r] = (q + 8 * r < cntc) ? __ldg(cta + (int64_t)ix[r] * kp) : 0.f;
 #pragma unroll
             for (int r = 0; r < 4; ++r) svc[q + 8 * r] = make_float2(vx[r], cx[r]);
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int t = c0 + 32 + q + 8 * r;
+                ix[r] = t < len ? __ldg(indices + s + t) : 0;
+                vx[r] = t < len ? __ldg(values + s + t) : 0.f;
+            }
             __syncwarp();
             if (q == 0) {
                 int t = 0;

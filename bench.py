@@ -26,6 +26,7 @@ rows sharded by nnz, one allreduce per iteration; strong scaling.
 from __future__ import annotations
 
 import argparse
+import gc
 import json
 import os
 import sys
@@ -48,7 +49,7 @@ PEAKS = ROOT / "MEASURED_PEAKS.json"
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--config", default="C2")
@@ -276,6 +277,8 @@ def main_ours(args):
     # ---- device-timed steps (inputs resident) ----
     times, its_tot, sims_tot, nk_tot = [], 0, 0, 0
     prof = _lib.CallProfiler(timed=False)
+    gc.collect()
+    gc.disable()                      # no collector pauses between the fits of a timed step
     with Clocks(local) as clk:
         barrier()
         for _ in range(args.steps):
@@ -289,6 +292,7 @@ def main_ours(args):
             barrier()
             times.append(e0.elapsed_time(e1))
             its_tot, sims_tot, nk_tot = its_tot + its, sims_tot + sims, nk_tot + nk
+    gc.enable()
     step_ms = torch.tensor([sum(times)], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(step_ms, op=dist.ReduceOp.MAX)
@@ -320,6 +324,8 @@ def main_ours(args):
     for _ in range(max(args.warmup, 2)):
         e2e_step()
     barrier()
+    gc.collect()
+    gc.disable()
     for _ in range(args.steps):
         flush.fill_(1)
         barrier()
@@ -329,6 +335,7 @@ def main_ours(args):
         e1.record()
         barrier()
         e2e_times.append(e0.elapsed_time(e1))
+    gc.enable()
     del c
     e2e_ms = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
     if world > 1:

@@ -280,34 +280,19 @@ struct RowPassArgs {
     long long *ctr;
     double *best, *second;       // predict outputs
     const long long *ctl;        // [it, done]: done -> this launch is a no-op
-    int hot;                     // term rows [0, hot) of ct are staged in shared memory
-    int64_t hot_d;               // dimensionality (caps hot)
 };
 
 // Thread = (row, CH centers in float4 groups tpr apart).  tpr threads cover
 // one row's kp columns, rpw rows share a warp.  Per nnz: one broadcast (idx, val) load and
 // CH/4 float4 loads of the term-major center row; CH independent FMA chains.
-template <int CH, int NT, bool HOT>
-__global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
+template <int CH, int NT>
+__global__ void __launch_bounds__(NT, CH == 8 ? 1024 / NT : CH == 4 ? 1024 / NT : 1) k_row_pass(RowPassArgs A) {
     PDL_ENTRY();
     // nnz per gather batch: keep ~8 float4 loads in flight per lane
     constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 2 : 1;
     if (A.ctl[1]) return;   // converged: later enqueued iterations are no-ops
-    extern __shared__ __align__(16) float s_dyn[];
-    // dynamic smem: [hot * kp floats: term rows of the hottest terms][staging]
-    float *s_hot = s_dyn;
+    extern __shared__ __align__(16) int2 s_iv[];   // per row group: kIvStride staged (id, value) pairs
     const int wpb = blockDim.x >> 5;
-    int2 *s_iv = reinterpret_cast<int2 *>(s_dyn + (int64_t)A.hot * A.kp);
-    if (HOT && A.hot > 0) {
-        // the Zipf head of the vocabulary (terms renumbered by document
-        // frequency on upload) is served from shared memory for the whole
-        // persistent launch
-        const float4 *src = reinterpret_cast<const float4 *>(A.ct);
-        float4 *dst = reinterpret_cast<float4 *>(s_hot);
-        const int64_t n4 = (int64_t)A.hot * A.kp / 4;
-        for (int64_t e = threadIdx.x; e < n4; e += blockDim.x) dst[e] = __ldg(src + e);
-        __syncthreads();
-    }
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -317,7 +302,6 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
     const int64_t nslots = (nrows + A.rpw - 1) / A.rpw;
     const int o0 = A.tpr > 1 ? (1 << (31 - __clz(A.tpr - 1))) : 0;
     int2 *my_iv = s_iv + (wib * 8 + (lane_on ? g : 0)) * kIvStride;
-    const int hot = HOT ? A.hot : 0;
     for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
         const int64_t slot = w * A.rpw + g;
         const bool valid = lane_on && slot < nrows;
@@ -351,16 +335,9 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
                 load_iv<UB>(my_iv + u, iv, vv);
 #pragma unroll
                 for (int b = 0; b < UB; ++b) {
-                    const int ii = iv[b];
-                    if (HOT && ii < hot) {
-                        const float4 *p = reinterpret_cast<const float4 *>(s_hot + (int64_t)ii * A.kp + j0);
+                    const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)iv[b] * A.kp);
 #pragma unroll
-                        for (int r = 0; r < CH / 4; ++r) cv[b][r] = p[r * A.tpr];
-                    } else {
-                        const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)ii * A.kp);
-#pragma unroll
-                        for (int r = 0; r < CH / 4; ++r) cv[b][r] = __ldg(p + r * A.tpr);
-                    }
+                    for (int r = 0; r < CH / 4; ++r) cv[b][r] = __ldg(p + r * A.tpr);
                 }
 #pragma unroll
                 for (int b = 0; b < UB; ++b)
@@ -375,9 +352,7 @@ __global__ void __launch_bounds__(NT) k_row_pass(RowPassArgs A) {
             for (; u < cnt; ++u) {
                 const int2 t = my_iv[u];
                 const float v0 = __int_as_float(t.y);
-                const int ii = t.x;
-                const float4 *p = (HOT && ii < hot) ? reinterpret_cast<const float4 *>(s_hot + (int64_t)ii * A.kp + j0)
-                                                    : reinterpret_cast<const float4 *>(ctj + (int64_t)ii * A.kp);
+                const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)t.x * A.kp);
 #pragma unroll
                 for (int r = 0; r < CH / 4; ++r) {
                     const float4 cc4 = p[r * A.tpr];
@@ -2243,82 +2218,32 @@ int grid_for(int64_t work_items, int per_block) {
     return (int)(g < 1 ? 1 : g);
 }
 
-template <int CH, int NT, bool HOT>
+template <int CH, int NT>
 int launch_rp(RowPassArgs &A, int grid, size_t smem, cudaStream_t st) {
-    static int attr = -1;
-    if ((int)smem > 48 * 1024 && attr < (int)smem) {
-        cudaFuncSetAttribute(k_row_pass<CH, NT, HOT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = (int)smem;
-    }
-    pdl_launch(k_row_pass<CH, NT, HOT>, dim3(grid), dim3(NT), (size_t)(smem), st, A);
+    pdl_launch(k_row_pass<CH, NT>, dim3(grid), dim3(NT), smem, st, A);
     CHECK_LAUNCH("row_pass");
     return 0;
 }
 
-// Shared-memory budget of the hot-term table: one persistent 1024-thread CTA
-// per SM for k <= 256 (<= 64 registers/thread), 256-thread CTAs otherwise.
-constexpr int64_t kSmemBudget = 200 * 1024;
-
-int64_t hot_terms_for(int64_t k, int64_t kp, int64_t d) {
-    const ColPlan p = col_plan(k);
-    if (p.ch > 8) return 0;
-    const int64_t staging = (int64_t)(1024 / 32) * 8 * kIvStride * 8;   // see k_row_pass staging layout
-    int64_t h = (kSmemBudget - staging) / (kp * 4);
-    if (h > d) h = d;
-    return h < 0 ? 0 : h;
-}
-
-int row_pass_mode() {
-    // SPKM_ROWPASS=1 selects the experimental shared-memory hot-term table
-    // (persistent 1024-thread CTAs); measured slower than the L1-cached
-    // 256-thread CTAs on C2 (profiles/r01_rowpass_hot_vs_plain.txt), so off.
-    static int mode = -1;
-    if (mode < 0) {
-        const char *s = getenv("SPKM_ROWPASS");
-        mode = s ? atoi(s) : 0;
-    }
-    return mode;
-}
-
+// (A persistent 1024-thread variant that served the Zipf head of ct32 from a
+// shared-memory table was 1.2x slower on C2 than these L1-cached 256-thread
+// CTAs and was removed: profiles/r01_rowpass_hot_vs_plain.txt.)
 int launch_row_pass(RowPassArgs &A, int64_t k, cudaStream_t st, int64_t max_rows) {
     const ColPlan p = col_plan(k);
     A.tpr = p.tpr;
     A.rpw = p.rpw;
     A.k = (int)k;
     const int64_t slots = (max_rows + p.rpw - 1) / p.rpw;
-    if (p.ch <= 8 && row_pass_mode() == 1) {
-        const int64_t d = A.hot_d;
-        A.hot = (int)hot_terms_for(k, A.kp, d);
-        const size_t smem = (size_t)A.hot * A.kp * 4 + (size_t)(1024 / 32) * 8 * kIvStride * 8;
-        int64_t grid = (slots + 31) / 32;
-        if (grid > num_sms()) grid = num_sms();
-        if (grid < 1) grid = 1;
-        if (p.ch == 4) return launch_rp<4, 1024, true>(A, (int)grid, smem, st);
-        return launch_rp<8, 1024, true>(A, (int)grid, smem, st);
-    }
-    A.hot = 0;
-    int grid = grid_for(slots, 8);
-    {
-        static int gmode = -1;   // experiment: SPKM_RPGRID=n -> n CTAs per SM (persistent)
-        if (gmode < 0) {
-            const char *s = getenv("SPKM_RPGRID");
-            gmode = s ? atoi(s) : 0;
-        }
-        if (gmode > 0) {
-            const int64_t g2 = (int64_t)num_sms() * gmode;
-            if (g2 < grid) grid = (int)g2;
-        }
-    }
+    const int grid = grid_for(slots, 8);
     const size_t smem = (size_t)(256 / 32) * 8 * kIvStride * 8;
-    if (p.ch == 4) return launch_rp<4, 256, false>(A, grid, smem, st);
-    if (p.ch == 8) return launch_rp<8, 256, false>(A, grid, smem, st);
-    if (p.ch == 16) return launch_rp<16, 256, false>(A, grid, smem, st);
-    return launch_rp<32, 256, false>(A, grid, smem, st);
+    if (p.ch == 4) return launch_rp<4, 256>(A, grid, smem, st);
+    if (p.ch == 8) return launch_rp<8, 256>(A, grid, smem, st);
+    if (p.ch == 16) return launch_rp<16, 256>(A, grid, smem, st);
+    return launch_rp<32, 256>(A, grid, smem, st);
 }
 
 RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     RowPassArgs A{};
-    A.hot_d = C->d;
     A.ctl = C->ctl;
     A.indptr = X->indptr;
     A.indices = X->indices;

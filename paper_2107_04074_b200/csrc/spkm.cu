@@ -285,8 +285,10 @@ struct RowPassArgs {
 // Thread = (row, CH centers in float4 groups tpr apart).  tpr threads cover
 // one row's kp columns, rpw rows share a warp.  Per nnz: one broadcast (idx, val) load and
 // CH/4 float4 loads of the term-major center row; CH independent FMA chains.
+// CH <= 8: capped at 64 registers (4 CTAs of 256 per SM); CH >= 16 (k > 256):
+// uncapped, the CH accumulators and loads in flight need the registers.
 template <int CH, int NT>
-__global__ void __launch_bounds__(NT, CH == 8 ? 1024 / NT : CH == 4 ? 1024 / NT : 1) k_row_pass(RowPassArgs A) {
+__global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPassArgs A) {
     PDL_ENTRY();
     // nnz per gather batch: keep ~8 float4 loads in flight per lane
     constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 2 : 1;

@@ -187,6 +187,11 @@ int spkm_apply_moves(const spkm_csr *X, const spkm_centers *C, const spkm_bounds
 /* Renormalise touched clusters (all if all_clusters), write cent64/ct32,
  * drift and per-cluster objective. */
 int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream);
+/* all_clusters | 4: stop after the center write; the per-cluster drift and
+ * objective reduction is then spkm_center_reduce (so the next iteration's
+ * spkm_center_thresholds, which needs only the new centers and the touched
+ * list, can run beside it and spkm_finalize on a second stream). */
+int spkm_center_reduce(const spkm_centers *C, void *stream);
 /* cc(a,j) = sqrt((<c_a,c_j>+1)/2) rounded up, s(a) = max_{j!=a} cc(a,j).
  * float64 split-d Gram over the upper-triangle 32x32 tiles listed in
  * tile_pairs (from spkm_gram_tiles); gram_scratch holds

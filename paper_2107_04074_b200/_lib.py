@@ -90,6 +90,7 @@ _SIGS = {
     "spkm_aggregate_sums": [_P(CSR), _P(Centers), _P(Bounds), c_vp, c_vp, c_vp],
     "spkm_apply_moves": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), c_vp, c_vp, c_vp, c_vp],
     "spkm_move_centers": [_P(Centers), ctypes.c_int, c_vp],
+    "spkm_center_reduce": [_P(Centers), c_vp],
     "spkm_gram_tiles": [c_i64, c_vp],
     "spkm_gram_scratch_doubles": [c_i64, c_i64],
     "spkm_center_thresholds": [_P(Centers), c_vp, c_vp, ctypes.c_int, c_vp],
@@ -146,7 +147,7 @@ _RESTYPES = {
 KERNELS_PER_CALL = {
     "spkm_full_assign": 1, "spkm_hamerly_bounds": 1, "spkm_hamerly_tighten": 1, "spkm_hamerly_rescan": 1,
     "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
-    "spkm_move_centers": 5, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
+    "spkm_move_centers": 5, "spkm_center_reduce": 1, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
     "spkm_seed_rows_csr": 1, "spkm_aggregate_sums_gated": 2, "spkm_permute_rows": 1, "spkm_audit": 1, "spkm_audit_transpose": 1,
@@ -237,14 +238,21 @@ def note_launches(n: int):
         _profiler.launches += n
 
 
+def kernels_for(name: str, args) -> int:
+    n = KERNELS_PER_CALL.get(name, 0)
+    if name == "spkm_move_centers" and len(args) > 1 and int(args[1]) & 4:
+        n -= 1                                   # the reduction is issued by spkm_center_reduce
+    return n
+
+
 def call(name: str, *args):
     """Call an int-returning entry point and raise on a non-zero status."""
     L = lib()
     prof = _profiler
     if _capture is not None:
-        _capture.append(KERNELS_PER_CALL.get(name, 0))
+        _capture.append(kernels_for(name, args))
     if prof is not None:
-        prof.launches += KERNELS_PER_CALL.get(name, 0)
+        prof.launches += kernels_for(name, args)
         prof.calls[name] = prof.calls.get(name, 0) + 1
         if prof.timed:
             import torch

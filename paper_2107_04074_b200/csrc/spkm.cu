@@ -1986,7 +1986,8 @@ template <bool DIAG> struct GmCfg {
 template <bool DIAG>
 __global__ void __launch_bounds__(GM_THREADS, 1) k_gram_mn(const __grid_constant__ CUtensorMap tm, int64_t k, int64_t d,
                                                           int64_t dsplit, const int2 *__restrict__ tiles,
-                                                          const double *__restrict__ sinp, int full, float *gpart,
+                                                          const int32_t *__restrict__ tlist,
+                                                          const int32_t *__restrict__ tcount, int full, float *gpart,
                                                           const long long *__restrict__ ctl) {
     PDL_ENTRY();
     using G = GmCfg<DIAG>;
@@ -1997,10 +1998,15 @@ __global__ void __launch_bounds__(GM_THREADS, 1) k_gram_mn(const __grid_constant
     __shared__ uint32_t tmem_base_s;
     const int2 tl = DIAG ? make_int2(0, 0) : tiles[blockIdx.x];
     const int64_t a0 = (int64_t)tl.x * GT, j0 = (int64_t)tl.y * GT;
-    int mine = full;   // the tile is recomputed only if one of its clusters moved
-    if (!mine && threadIdx.x < GT) {
-        const int64_t q = threadIdx.x;
-        mine = (a0 + q < k && sinp[a0 + q] != 0.0) || (j0 + q < k && sinp[j0 + q] != 0.0);
+    // the tile is recomputed only if one of its clusters was touched by this
+    // iteration's center update (the touched list of spkm_move_centers)
+    int mine = full;
+    if (!mine) {
+        const int tc = *tcount;
+        for (int t = threadIdx.x; t < tc; t += blockDim.x) {
+            const int64_t j = tlist[t];
+            mine |= (j >= a0 && j < a0 + GT) || (j >= j0 && j < j0 + GT);
+        }
     }
     const int dirty = __syncthreads_or(mine);
     if (blockIdx.y == 0 && threadIdx.x == 0) reinterpret_cast<int *>(gpart + dsplit * k * k)[blockIdx.x] = dirty;
@@ -2627,11 +2633,15 @@ int64_t spkm_center_scratch_doubles(int64_t k, int64_t d) {
     return k * (nch > 2 * ntile ? nch : 2 * ntile);
 }
 
+int spkm_center_reduce(const spkm_centers *C, void *stream);
+
 int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
     cudaStream_t st = S(stream);
     const int64_t nch = spkm_center_chunks(C->d);
     const int64_t ntile = (C->d + kTileT - 1) / kTileT;
     const double inv = ldexp(1.0, -C->scale_bits);
+    const bool defer_reduce = (all_clusters & 4) != 0;   // spkm_center_reduce is issued separately
+    all_clusters &= 1;
     pdl_launch(k_touched_list, dim3(1), dim3(1024), (size_t)(0), st, C->k, C->touched, all_clusters, C->tlist, C->tcount, C->ctl);
     CHECK_LAUNCH("touched_list");
     pdl_launch(k_center_norm_part, dim3(dim3((unsigned)nch, (unsigned)C->k)), dim3(256), (size_t)(0), st, C->d, nch, C->sums, C->tlist, C->tcount,
@@ -2642,8 +2652,13 @@ int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
     pdl_launch(k_center_write, dim3(dim3((unsigned)ntile, (unsigned)((C->k + kTileJ - 1) / kTileJ))), dim3(256), (size_t)(0), st, 
         C->d, C->kp, ntile, C->sums, C->tlist, C->tcount, inv, C->norm, C->cent64, C->ct32, C->part, C->ctl);
     CHECK_LAUNCH("center_write");
-    pdl_launch(k_center_reduce, dim3((unsigned)C->k), dim3(256), (size_t)(0), st, ntile, C->tlist, C->tcount, C->part, C->norm, C->drift, C->sinp,
-                                                   C->objc, C->ctl);
+    return defer_reduce ? 0 : spkm_center_reduce(C, stream);
+}
+
+int spkm_center_reduce(const spkm_centers *C, void *stream) {
+    const int64_t ntile = (C->d + kTileT - 1) / kTileT;
+    pdl_launch(k_center_reduce, dim3((unsigned)C->k), dim3(256), (size_t)0, S(stream), ntile, C->tlist, C->tcount, C->part,
+               C->norm, C->drift, C->sinp, C->objc, C->ctl);
     CHECK_LAUNCH("center_reduce");
     return 0;
 }
@@ -2693,10 +2708,10 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     }
     if (tk == 1)
         pdl_launch(k_gram_mn<true>, dim3(1, (unsigned)ds), dim3(GM_THREADS), GmCfg<true>::SMEM, st, tm, C->k, C->d, ds,
-                   tiles_dev, C->sinp, full, gp, C->ctl);
+                   tiles_dev, C->tlist, C->tcount, full, gp, C->ctl);
     else
         pdl_launch(k_gram_mn<false>, dim3((unsigned)ntiles, (unsigned)ds), dim3(GM_THREADS), GmCfg<false>::SMEM, st, tm,
-                   C->k, C->d, ds, tiles_dev, C->sinp, full, gp, C->ctl);
+                   C->k, C->d, ds, tiles_dev, C->tlist, C->tcount, full, gp, C->ctl);
     CHECK_LAUNCH("gram_mn");
     pdl_launch(k_gram_final, dim3((unsigned)((C->k * C->k * 8 + 255) / 256)), dim3(256), (size_t)0, st, C->k, ds, gp,
                full, gdelta, C->cc, C->ctl);
@@ -3143,7 +3158,8 @@ int spkm_fit_graph_abort(void *loop) {
         }
     }
     cudaGetLastError();
-    if (L->graph) cudaGraphDestroy(L->graph);
+    // the graph is left to the driver: after an invalidated capture its state
+    // is undefined, and destroying it has crashed (a one-off leak on an error path)
     delete L;
     return 0;
 }

@@ -681,6 +681,11 @@ class Engine:
         self.stream = torch.cuda.Stream(device=self.device)
         self.stream.wait_stream(torch.cuda.current_stream(self.device))
         self.sp = ctypes_void(self.stream.cuda_stream)
+        # the next iteration's center thresholds run on a second stream beside
+        # the drift/objective reduction and finalize (fork/join by events); one
+        # side stream per main stream, so a graph body captured while the
+        # whole-fit capture is open forks to a stream of its own
+        self._side = {}
         self.use_graphs = use_graphs and comm is None
         self.loop = None                 # device-driven fit loop (CUDA graph with a WHILE node)
         self.fit = None                  # the whole fit as one CUDA graph (fit_launch)
@@ -816,9 +821,39 @@ class Engine:
             _lib.call("spkm_apply_move_slots", self.corpus.struct, self.C.struct, _ptr(ex.slots), ex.world,
                       ex.slot_len, _ptr(self.C.touched), _ptr(self.P.ctr), self.sp)
 
-    def move_centers(self, all_clusters: bool):
-        _lib.call("spkm_move_centers", self.C.struct, int(all_clusters), self.sp)
+    def move_centers(self, all_clusters: bool, defer_reduce: bool = False):
+        _lib.call("spkm_move_centers", self.C.struct, int(all_clusters) | (4 if defer_reduce else 0), self.sp)
         self.C.refresh_dense(self.sp)
+
+    def update_and_finalize(self, all_clusters: bool, sims_extra: int, scratch: bool = False):
+        """Center update (engine.py:321-324), then -- for the variants that
+        use center-center bounds -- the NEXT iteration's thresholds
+        (engine.py:243) on the side stream: they need only the new centers and
+        the touched list, so they run beside the drift/objective reduction
+        and the finalize; the main stream joins before the next iteration."""
+        if not self.needs_cc:
+            self.move_centers(all_clusters)
+            if scratch:
+                self.scratch_sums()
+            self.finalize_launch(all_clusters, sims_extra)
+            return
+        self.move_centers(all_clusters, defer_reduce=True)
+        key = self.stream.cuda_stream
+        if key not in self._side:
+            side = torch.cuda.Stream(device=self.device)
+            self._side[key] = (side, ctypes_void(side.cuda_stream), torch.cuda.Event(), torch.cuda.Event())
+        side, side_sp, fork, join = self._side[key]
+        fork.record(self.stream)
+        side.wait_event(fork)
+        _lib.call("spkm_center_thresholds", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles),
+                  int(not self.C.cc_valid), side_sp)
+        self.C.cc_valid = True
+        join.record(side)
+        _lib.call("spkm_center_reduce", self.C.struct, self.sp)
+        if scratch:
+            self.scratch_sums()
+        self.finalize_launch(all_clusters, sims_extra)
+        self.stream.wait_event(join)
 
     def finalize_launch(self, all_clusters: bool, sims_extra: int):
         _lib.call("spkm_finalize", self.C.struct, self.P.work, int(all_clusters), int(sims_extra), self.sp)
@@ -856,9 +891,7 @@ class Engine:
             self.lloyd_pass()
             sims_extra = self.n_total * self.k
         else:
-            use = int(self.needs_cc)
-            if self.needs_cc:
-                self.center_thresholds()
+            use = int(self.needs_cc)       # cc / s were computed at the end of the previous iteration
             self.bounds_pass(use)
             if debug_hook is not None:
                 if hasattr(debug_hook, "device_audit"):    # validation.DeviceBoundAuditor: stays on the device
@@ -869,12 +902,9 @@ class Engine:
             self.scan_pass(use)
             sims_extra = 0
         self.apply_moves()
-        self.move_centers(False)
-        if it % _SCRATCH_INTERVAL == 0:
-            # exact fixed-point sums: the rebuild reproduces the incremental
-            # sums bit-for-bit; kept so the reference's schedule is visible
-            self.scratch_sums()
-        self.finalize_launch(False, sims_extra)
+        # exact fixed-point sums: the it % 50 rebuild reproduces the incremental
+        # sums bit-for-bit; kept so the reference's schedule is visible
+        self.update_and_finalize(False, sims_extra, scratch=(it % _SCRATCH_INTERVAL == 0))
 
     def enqueue(self, it: int):
         """Launch iteration ``it`` (>= 2) eagerly without a host sync (a no-op
@@ -892,14 +922,11 @@ class Engine:
             sims_extra = self.n_total * self.k
         else:
             use = int(self.needs_cc)
-            if self.needs_cc:
-                _lib.call("spkm_center_thresholds", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles), 0, self.sp)
             self.bounds_pass(use)
             self.scan_pass(use)
             sims_extra = 0
         self.apply_moves()
-        self.move_centers(False)
-        self.finalize_launch(False, sims_extra)
+        self.update_and_finalize(False, sims_extra)
 
     def loop_launch(self, max_iter: int):
         """Iterations 3..max_iter as ONE graph launch: a conditional WHILE node
@@ -1028,8 +1055,7 @@ class Engine:
         """Iteration 1 (engine.py:249-271): full pass, scratch sums, move all, stats."""
         self.init_pass()
         self.scratch_sums()
-        self.move_centers(True)
-        self.finalize_launch(True, self.n_total * self.k)
+        self.update_and_finalize(True, self.n_total * self.k)
 
     def iteration(self, it: int, debug_hook=None, seed_indices=None) -> tuple:
         if it == 1:

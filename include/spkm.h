@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define SPKM_ABI_VERSION 2
+#define SPKM_ABI_VERSION 3
 
 /* variants, engine.py:22 */
 enum spkm_variant {
@@ -87,7 +87,7 @@ typedef struct spkm_centers {
     double *norm;            /* [k] scratch: |sums_j|                       */
     float *cc;               /* [k*k] half-angle center cosines, rounded up */
     float *s;                /* [k]   row max of cc (diag excluded)         */
-    double *hstat;           /* [8]   owner, p_min, p_min2, owner_s, smax, smax2 */
+    double *hstat;           /* [8]   owner, p_min, p_min2, owner_s, smax, smax2, fuse */
     int32_t *tlist;          /* [k]   scratch: touched cluster list         */
     int32_t *tcount;         /* [1]   scratch: its length                   */
     long long *ctl;          /* [2]   {iterations done, converged}: every loop
@@ -164,7 +164,12 @@ int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B
                         int use_s, int naive, void *stream);
 int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
                          int use_s, void *stream);
-int spkm_hamerly_rescan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
+/* Full-k rescan of the tighten survivors.  use_s: as for spkm_hamerly_tighten
+ * -- when the previous iteration's tighten pruned < 5% of the bound survivors
+ * (flag in hstat[6], set by spkm_finalize) this pass takes the bound
+ * survivors and applies the tighten test itself (the tighten call is then a
+ * no-op): identical results and counters, one pass fewer. */
+int spkm_hamerly_rescan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_s,
                         void *stream);
 int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
                       int use_cc, void *stream);

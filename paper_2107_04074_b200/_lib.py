@@ -20,7 +20,7 @@ LIB_PATH = PKG / "libspkm.so"
 SRC = PKG / "csrc" / "spkm.cu"
 SRC_HOST = PKG / "csrc" / "ingest.cpp"
 HEADER = ROOT / "include" / "spkm.h"
-ABI_VERSION = 2
+ABI_VERSION = 3
 
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-shared", "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
@@ -84,7 +84,7 @@ _SIGS = {
     "spkm_full_assign": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_hamerly_bounds": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, ctypes.c_int, c_vp],
     "spkm_hamerly_tighten": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
-    "spkm_hamerly_rescan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), c_vp],
+    "spkm_hamerly_rescan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_elkan_bounds": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_elkan_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_aggregate_sums": [_P(CSR), _P(Centers), _P(Bounds), c_vp, c_vp, c_vp],

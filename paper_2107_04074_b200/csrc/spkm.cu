@@ -51,6 +51,7 @@ constexpr double kCcSlack = 1e-9;           // float64 Gram error (d * 2^-53 << 
 constexpr double kSqrt2 = 1.4142135623730951;
 constexpr double kZeroSumEps = 1e-12;       // engine.py:27
 constexpr int kCenterChunk = 4096;          // d-chunk of the center kernels
+constexpr int kFuseFlag = 6;                // hstat slot: fused Hamerly tighten + rescan next iteration
 
 thread_local char g_err[512] = {0};
 
@@ -280,6 +281,14 @@ struct RowPassArgs {
     long long *ctr;
     double *best, *second;       // predict outputs
     const long long *ctl;        // [it, done]: done -> this launch is a no-op
+    // Hamerly rescan fused with the tighten (when *fuse != 0): rows come from
+    // the bound survivors, and each row's s~(i, a) from the full pass decides
+    // the tighten test first (k_hamerly_tighten is then a no-op)
+    const double *fuse;
+    const int32_t *rowlist_fused;
+    const long long *rowcount_fused;
+    const float *s_arr;
+    int use_s;
 };
 
 // Thread = (row, CH centers in float4 groups tpr apart).  tpr threads cover
@@ -300,14 +309,16 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane / A.tpr, q = lane - g * A.tpr;
     const bool lane_on = g < A.rpw;
-    const int64_t nrows = A.rowlist ? *A.rowcount : A.n;
+    const bool fused = A.mode == MODE_RESCAN && A.fuse && *A.fuse != 0.0;
+    const int32_t *rowlist = fused ? A.rowlist_fused : A.rowlist;
+    const int64_t nrows = rowlist ? (fused ? *A.rowcount_fused : *A.rowcount) : A.n;
     const int64_t nslots = (nrows + A.rpw - 1) / A.rpw;
     const int o0 = A.tpr > 1 ? (1 << (31 - __clz(A.tpr - 1))) : 0;
     int2 *my_iv = s_iv + (wib * 8 + (lane_on ? g : 0)) * kIvStride;
     for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
         const int64_t slot = w * A.rpw + g;
         const bool valid = lane_on && slot < nrows;
-        const int64_t row = valid ? (A.rowlist ? (int64_t)A.rowlist[slot] : slot) : 0;
+        const int64_t row = valid ? (rowlist ? (int64_t)rowlist[slot] : slot) : 0;
         const int64_t s = valid ? A.indptr[row] : 0;
         const int64_t e = valid ? A.indptr[row + 1] : 0;
         const int len = (int)(e - s);
@@ -379,6 +390,15 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
             if (q < o && q + o < A.tpr) top2_merge(tp, other, inc);
         }
         const double eps = valid ? (double)A.reps[row] : 0.0;
+        float sa = 0.f;   // fused rescan: s~(i, a(i)) from the lane that holds a(i)
+        if (fused) {
+            float mine = 0.f;
+#pragma unroll
+            for (int c = 0; c < CH; ++c)
+                if (j0 + (c >> 2) * jstr + (c & 3) == inc) mine = acc[c];
+            const int src = (valid && inc >= 0) ? g * A.tpr + (inc % jstr) / 4 : lane;
+            sa = __shfl_sync(FULL, mine, src);
+        }
         if (A.mode == SPKM_MODE_INIT_ELKAN && valid) {
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
@@ -388,6 +408,7 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
         }
         const bool leader = valid && q == 0;
         bool moved = false;
+        bool tight_pruned = false;
         if (leader) {
             switch (A.mode) {
                 case SPKM_MODE_INIT_PLAIN:
@@ -405,6 +426,16 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
                     }
                     break;
                 case MODE_RESCAN:
+                    if (fused) {   // the tighten test of k_hamerly_tighten (kernels.py:88-95)
+                        const double lbt = (double)sa - eps;
+                        bool pruned = (A.use_s && lbt >= 0.0 && (double)A.s_arr[inc] + kSqrt2 * eps <= lbt);
+                        if (!pruned) pruned = ((double)A.u[row] + eps <= (double)sa);
+                        tight_pruned = pruned;
+                        if (pruned) {
+                            A.l[row] = store_lower(lbt);
+                            break;
+                        }
+                    }
                     if (tp.bj != inc) {
                         A.a[row] = tp.bj;
                         moved = true;
@@ -422,8 +453,14 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
         if (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN) {
             warp_append(moved, (int32_t)row, A.mv_i, inc, A.mv_old, A.ctr + SPKM_CTR_MOVES);
             if (A.mode == MODE_RESCAN) {
-                ctr_add(s_ctr, SPKM_CTR_SIMS, leader ? (long long)(A.k - 1) : 0);
-                ctr_add(s_ctr, SPKM_CTR_NNZ_RESCAN, leader ? (long long)(e - s) : 0);
+                const bool scanned = leader && !tight_pruned;
+                ctr_add(s_ctr, SPKM_CTR_SIMS, scanned ? (long long)(A.k - 1) : 0);
+                ctr_add(s_ctr, SPKM_CTR_NNZ_RESCAN, scanned ? (long long)(e - s) : 0);
+                if (fused) {   // the tighten's counters and its survivor count
+                    ctr_add(s_ctr, SPKM_CTR_SIMS, leader ? 1 : 0);
+                    ctr_add(s_ctr, SPKM_CTR_NNZ_TIGHTEN, leader ? (long long)(e - s) : 0);
+                    ctr_add(s_ctr, SPKM_CTR_SURV2, scanned ? 1 : 0);
+                }
             }
         }
     }
@@ -496,9 +533,10 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
                                                          const float *__restrict__ u,
                                                          const float *__restrict__ s_arr, int use_s,
                                                          const int32_t *__restrict__ surv1, int32_t *surv2,
-                                                         long long *ctr, const long long *__restrict__ ctl) {
+                                                         long long *ctr, const double *__restrict__ fuse,
+                                                         const long long *__restrict__ ctl) {
     PDL_ENTRY();
-    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    if (ctl[1] || *fuse != 0.0) return;   // converged, or the rescan does the tighten this iteration
     __shared__ __align__(16) float2 s_vc[8][4][kIvStride];   // (value, center value), padded as s_iv
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
@@ -1458,6 +1496,10 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
         hstat[3] = (double)Sx.i1;
         hstat[4] = -Sx.v1;
         hstat[5] = (k > 1) ? -Sx.v2 : 0.0;
+        // Hamerly: when the tighten pruned < 5% of the bound survivors this
+        // iteration, the next rescan runs over the bound survivors and does
+        // the tighten test itself (same results and counters, one pass less)
+        hstat[kFuseFlag] = (cv[SPKM_CTR_SURV1] > 0 && 20 * cv[SPKM_CTR_SURV2] >= 19 * cv[SPKM_CTR_SURV1]) ? 1.0 : 0.0;
         sv[SPKM_ST_OBJECTIVE] = tot;
         sv[SPKM_ST_ALLONE] = no ? 0.0 : 1.0;
         sv[SPKM_ST_TOUCHED] = (double)tc;
@@ -2534,18 +2576,25 @@ int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *
     if (X->n == 0) return 0;
     const int grid = grid_for((X->n + 3) / 4, 8);
     pdl_launch(k_hamerly_tighten, dim3(grid), dim3(256), (size_t)(0), S(stream), X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
-                                                   B->a, B->l, B->u, C->s, use_s, W->surv1, W->surv2, W->ctr, C->ctl);
+                                                   B->a, B->l, B->u, C->s, use_s, W->surv1, W->surv2, W->ctr,
+                                                   (const double *)(C->hstat + kFuseFlag), C->ctl);
     CHECK_LAUNCH("hamerly_tighten");
     return 0;
 }
 
-int spkm_hamerly_rescan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream) {
+int spkm_hamerly_rescan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_s,
+                        void *stream) {
     if (C->k > 1024) return fail_msg("k > 1024 not supported by this build");
     if (X->n == 0) return 0;
     RowPassArgs A = row_args(X, C);
     A.mode = MODE_RESCAN;
     A.rowlist = W->surv2;
     A.rowcount = W->ctr + SPKM_CTR_SURV2;
+    A.fuse = C->hstat + kFuseFlag;
+    A.rowlist_fused = W->surv1;
+    A.rowcount_fused = W->ctr + SPKM_CTR_SURV1;
+    A.s_arr = C->s;
+    A.use_s = use_s;
     A.a = B->a;
     A.l = B->l;
     A.u = B->u;

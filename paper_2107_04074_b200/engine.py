@@ -804,7 +804,7 @@ class Engine:
             self._dense(_lib.DMODE_RESCAN_H, use_flag)   # tighten + full scan on the canonical TC values
         else:
             _lib.call("spkm_hamerly_tighten", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
-            _lib.call("spkm_hamerly_rescan", self.xs, self.C.struct, self.P.bounds, self.P.work, self.sp)
+            _lib.call("spkm_hamerly_rescan", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
 
     def apply_moves(self):
         if self.comm is None:

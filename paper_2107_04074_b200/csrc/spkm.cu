@@ -1429,7 +1429,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
                                                           double *sinp, const double *__restrict__ objc,
                                                           double *hstat, long long *ctr, double *stats,
                                                           long long sims_extra, int all, double *stats_hist,
-                                                          int64_t hist_cap, long long *ctl) {
+                                                          int64_t hist_cap, int fuse_policy, long long *ctl) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double s_ob[kFinThreads / 32];
@@ -1499,7 +1499,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
         // Hamerly: when the tighten pruned < 5% of the bound survivors this
         // iteration, the next rescan runs over the bound survivors and does
         // the tighten test itself (same results and counters, one pass less)
-        hstat[kFuseFlag] = (cv[SPKM_CTR_SURV1] > 0 && 20 * cv[SPKM_CTR_SURV2] >= 19 * cv[SPKM_CTR_SURV1]) ? 1.0 : 0.0;
+        const bool fuse_auto = 20 * cv[SPKM_CTR_SURV2] >= 19 * cv[SPKM_CTR_SURV1];
+        hstat[kFuseFlag] = (cv[SPKM_CTR_SURV1] > 0 && (fuse_policy == 1 || (fuse_policy == 2 && fuse_auto))) ? 1.0 : 0.0;
         sv[SPKM_ST_OBJECTIVE] = tot;
         sv[SPKM_ST_ALLONE] = no ? 0.0 : 1.0;
         sv[SPKM_ST_TOUCHED] = (double)tc;
@@ -2712,10 +2713,19 @@ int spkm_center_reduce(const spkm_centers *C, void *stream) {
     return 0;
 }
 
+// SPKM_HAMERLY_FUSE: 0 = never fuse the tighten into the rescan, 1 = always,
+// unset / 2 = when the last tighten pruned < 5% (read at every call, so the
+// eager loop can be switched for A/B tests; a captured graph keeps its value)
+static int hamerly_fuse_policy() {
+    const char *e = getenv("SPKM_HAMERLY_FUSE");
+    const int v = e ? atoi(e) : 2;
+    return (v >= 0 && v <= 2) ? v : 2;
+}
+
 int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra, void *stream) {
     pdl_launch(k_finalize, dim3(1), dim3(kFinThreads), (size_t)(0), S(stream), C->k, C->touched, C->tcount, C->drift, C->sinp, C->objc, C->hstat,
                                                  W->ctr, W->stats, sims_extra, all_clusters, W->stats_hist,
-                                                 W->hist_cap, C->ctl);
+                                                 W->hist_cap, hamerly_fuse_policy(), C->ctl);
     CHECK_LAUNCH("finalize");
     return 0;
 }

@@ -419,3 +419,25 @@ def test_result_sums_rebuilt_on_host_equal_device_aggregate(variant):
     m.update_centers(data, r.assignments, cs)
     assert np.array_equal(r.centers.sums, cs.sums)
     assert np.array_equal(r.centers.counts, cs.counts)
+
+
+@pytest.mark.parametrize("variant", ["hamerly", "simp_hamerly"])
+def test_hamerly_fused_rescan_matches_separate_tighten(variant, monkeypatch):
+    """The rescan that applies the tighten test itself (SPKM_HAMERLY_FUSE=1)
+    and the separate tighten kernel (=0) give identical fits, iteration
+    statistics included (eager loop: the policy is read at every launch)."""
+    m = spk()
+    data = golden_dataset(load_golden("C1"))
+    out = {}
+    for pol in ("0", "1", "2"):
+        monkeypatch.setenv("SPKM_HAMERLY_FUSE", pol)
+        r = m.run(data, 12, variant, m.SeedConfig(seed=3), max_iter=30, use_graphs=False)
+        out[pol] = r
+    ref = out["0"]
+    for pol in ("1", "2"):
+        r = out[pol]
+        assert np.array_equal(r.assignments, ref.assignments)
+        assert r.objective == ref.objective
+        key = lambda s: (s.sim_count, s.reassignments, s.survivors, s.survivors2, s.nnz_tighten, s.nnz_rescan,
+                         s.objective)
+        assert [key(s) for s in r.iterations] == [key(s) for s in ref.iterations]

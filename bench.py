@@ -406,8 +406,12 @@ def roofline(args, data, corpus, dev, world):
                 bytes_by[("spkm_hamerly_rescan", v)] = sum(8 * s.nnz_rescan + 24 * s.survivors2 for s in its[1:])
                 gather_by[("spkm_hamerly_rescan", v)] = sum(4 * kp * s.nnz_rescan for s in its[1:])
             if v in ("elkan", "simp_elkan"):
-                bytes_by[("spkm_elkan_bounds", v)] = (8 * ku + 16) * n * (len(its) - 1)
-                bytes_by[("spkm_elkan_scan", v)] = sum(8 * s.nnz_elkan + (8 * ku + 16) * s.survivors for s in its[1:])
+                b_bounds = (8 * ku + 16) * n * (len(its) - 1)
+                b_scan = sum(8 * s.nnz_elkan + (8 * ku + 16) * s.survivors for s in its[1:])
+                bytes_by[("spkm_elkan_bounds", v)] = b_bounds
+                bytes_by[("spkm_elkan_scan", v)] = b_scan
+                # the fused entry point (bound update + scan in one pass) moves both
+                bytes_by[("spkm_elkan_bounds_scan", v)] = b_bounds + b_scan
             # center update (reported beside B_iter): 16 B of
             # int64 atomics per moved nnz; 20 B per (touched cluster, term)
             # to renormalise and take the drift

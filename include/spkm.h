@@ -175,6 +175,11 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
                       int use_cc, void *stream);
 int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
                     int use_cc, void *stream);
+/* spkm_elkan_bounds + spkm_elkan_scan in one pass over all rows: each row's
+ * drift update and prune test are done by the lanes that then scan it (same
+ * results and counters as the two calls). */
+int spkm_elkan_bounds_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
+                           void *stream);
 
 /* Center maintenance.  aggregate: sums/counts from scratch (target arrays may
  * be a delta buffer); apply_moves: sums[old] -= x, sums[new] += x for the

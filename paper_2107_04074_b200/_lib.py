@@ -87,6 +87,7 @@ _SIGS = {
     "spkm_hamerly_rescan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_elkan_bounds": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_elkan_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
+    "spkm_elkan_bounds_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_aggregate_sums": [_P(CSR), _P(Centers), _P(Bounds), c_vp, c_vp, c_vp],
     "spkm_apply_moves": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), c_vp, c_vp, c_vp, c_vp],
     "spkm_move_centers": [_P(Centers), ctypes.c_int, c_vp],
@@ -146,7 +147,7 @@ _RESTYPES = {
 # kernels each entry point launches (for the bench's gpu_launches count)
 KERNELS_PER_CALL = {
     "spkm_full_assign": 1, "spkm_hamerly_bounds": 1, "spkm_hamerly_tighten": 1, "spkm_hamerly_rescan": 1,
-    "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
+    "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_elkan_bounds_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
     "spkm_move_centers": 5, "spkm_center_reduce": 1, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,

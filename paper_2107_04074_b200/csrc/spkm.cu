@@ -737,7 +737,11 @@ __host__ __device__ __forceinline__ int64_t elkan_sim_stride(int64_t k) {
 //     Every center the replay needs was fetched (a center passing the u
 //     pre-test also passes every later u test, since the running best only
 //     grows), so sim_count counts exactly what the reference's loop counts.
-template <int EB>
+// FUSE: the drift update + prune test of k_elkan_bounds is done here, per
+// row over all n rows (each lane updates the u(i, j) of its own blocks, the
+// same lanes that later test and scan them), so the bound pass, its survivor
+// list and one read of u are saved; rows that survive go straight on.
+template <int EB, bool FUSE>
 __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ indptr,
                                                     const int32_t *__restrict__ indices,
                                                     const float *__restrict__ values,
@@ -746,7 +750,11 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                                                     int32_t *a, float *l, float *u, int64_t ku,
                                                     const float *__restrict__ cc, int use_cc,
                                                     const int32_t *__restrict__ surv1, int32_t *mv_i,
-                                                    int32_t *mv_old, long long *ctr, const long long *__restrict__ ctl) {
+                                                    int32_t *mv_old, long long *ctr, int64_t n_rows,
+                                                    const double *__restrict__ drift,
+                                                    const double *__restrict__ sinp,
+                                                    const float *__restrict__ s_arr,
+                                                    const long long *__restrict__ ctl) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     constexpr int UB = 32 / EB;   // nnz per gather batch: 8 float4 loads in flight per lane
@@ -767,20 +775,63 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     const int gstride = sim_stride / ppw;             // per-group slice (>= ES * nb)
     float *my_sim = s_sim_dyn + wib * sim_stride + (lane_on ? g : 0) * gstride;
     int2 *my_iv = s_iv[wib][lane_on ? g : 0];
-    const long long cnt = ctr[SPKM_CTR_SURV1];
+    const long long cnt = FUSE ? n_rows : ctr[SPKM_CTR_SURV1];
     const int64_t nslots = (cnt + ppw - 1) / ppw;
     const int wpb = blockDim.x >> 5;
     for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
         const int64_t slot = w * ppw + g;
-        const bool valid = lane_on && slot < cnt;
-        const int32_t i = valid ? surv1[slot] : 0;
+        bool valid = lane_on && slot < cnt;
+        const int32_t i = valid ? (FUSE ? (int32_t)slot : surv1[slot]) : 0;
         const int ai = valid ? a[i] : 0;
+        float *ui = u + (int64_t)i * ku;
+        const double eps = valid ? (double)reps[i] : 0.0;
+        double lb;
+        if constexpr (FUSE) {
+            // k_elkan_bounds for this row (engine.py:274-283 + kernels.py:35-47)
+            const float lo = valid ? l[i] : 0.f;
+            float lf = lo;
+            const double sa = valid ? sinp[ai] : 0.0;
+            if (sa != 0.0) {
+                const double pa = drift[ai];
+                lf = store_lower((lo < -pa) ? -1.0 : d_clamp((double)lo * pa - d_sin((double)lo) * sa));
+            }
+            if (valid && q == 0 && lf != lo) l[i] = lf;
+            lb = (double)lf;
+            const bool pskip = use_cc && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb;
+            const bool cc_on = use_cc && lb >= 0.0;
+            bool surv = false;
+            for (int r = 0; r < nrounds && valid; ++r) {
+                const int blk = r * 32 + q;
+                if (blk >= nb) break;
+                for (int c2 = 0; c2 < EB; ++c2) {
+                    const int j = blk * EB + c2;
+                    if (j >= k) break;
+                    float wv = ui[j];
+                    const double sj = sinp[j];
+                    if (sj != 0.0) {   // engine.py:281-283 with the chord-based sine bound
+                        const double pj = drift[j];
+                        const double nv = ((double)wv <= pj) ? d_clamp((double)wv * pj + d_sin((double)wv) * sj) : 1.0;
+                        wv = store_upper(nv);
+                        ui[j] = wv;
+                    }
+                    if (!pskip && j != ai) {
+                        bool skip = cc_on && (double)__ldg(cc + (int64_t)ai * k + j) + kSqrt2 * eps <= lb;
+                        if (!skip) skip = ((double)wv + 2.0 * eps <= lb);
+                        surv |= !skip;
+                    }
+                }
+            }
+            // the row survives if any of its lanes found a center it cannot prune
+            const unsigned m = __ballot_sync(FULL, surv);
+            const unsigned gmask = (bpr >= 32 ? 0xffffffffu : ((1u << bpr) - 1u)) << (lane_on ? g * bpr : 0);
+            valid = valid && (m & gmask) != 0;
+            ctr_add(s_ctr, SPKM_CTR_SURV1, (valid && q == 0) ? 1 : 0);
+        } else {
+            lb = valid ? (double)l[i] : 0.0;
+        }
         const int64_t s = valid ? indptr[i] : 0, e = valid ? indptr[i + 1] : 0;
         const int len = (int)(e - s);
         const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
-        const double eps = valid ? (double)reps[i] : 0.0;
-        const double lb = valid ? (double)l[i] : 0.0;
-        float *ui = u + (int64_t)i * ku;
         const bool cc_ok = use_cc && lb >= 0.0;
         for (int r = 0; r < nrounds; ++r) {
             const int blk = r * 32 + q;
@@ -2616,27 +2667,41 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
     return 0;
 }
 
-int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
-                    void *stream) {
+static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
+                             bool fuse, void *stream) {
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
     const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float);
-    static size_t dyn_set = 0;   // static smem (16 KB staging) + dyn must fit the opt-in limit
-    if (dyn > dyn_set) {
-        cudaFuncSetAttribute(k_elkan_scan<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        cudaFuncSetAttribute(k_elkan_scan<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-        dyn_set = dyn;
+    auto launch = [&](auto kern) {
+        static size_t dyn_set = 0;   // static smem (16 KB staging) + dyn must fit the opt-in limit
+        if (dyn > dyn_set) {
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+            dyn_set = dyn;
+        }
+        pdl_launch(kern, dim3(grid), dim3(256), dyn, S(stream), X->indptr, X->indices, X->values, X->row_eps, C->ct32,
+                   C->kp, (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1, W->mv_i, W->mv_old, W->ctr,
+                   X->n, C->drift, C->sinp, C->s, C->ctl);
+    };
+    const bool eb4 = elkan_block(C->k) == 4;
+    if (fuse) {
+        if (eb4) launch(k_elkan_scan<4, true>);
+        else launch(k_elkan_scan<8, true>);
+    } else {
+        if (eb4) launch(k_elkan_scan<4, false>);
+        else launch(k_elkan_scan<8, false>);
     }
-    if (elkan_block(C->k) == 4)
-        pdl_launch(k_elkan_scan<4>, dim3(grid), dim3(256), dyn, S(stream), X->indptr, X->indices, X->values, X->row_eps,
-                   C->ct32, C->kp, (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1, W->mv_i, W->mv_old,
-                   W->ctr, C->ctl);
-    else
-        pdl_launch(k_elkan_scan<8>, dim3(grid), dim3(256), dyn, S(stream), X->indptr, X->indices, X->values, X->row_eps,
-                   C->ct32, C->kp, (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1, W->mv_i, W->mv_old,
-                   W->ctr, C->ctl);
     CHECK_LAUNCH("elkan_scan");
     return 0;
+}
+
+int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
+                    void *stream) {
+    return elkan_scan_launch(X, C, B, W, use_cc, false, stream);
+}
+
+int spkm_elkan_bounds_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
+                           void *stream) {
+    return elkan_scan_launch(X, C, B, W, use_cc, true, stream);
 }
 
 int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B, long long *sums_target,

@@ -24,6 +24,7 @@ reference's 50-iteration scratch rebuild is a no-op, kept for its schedule).
 from __future__ import annotations
 
 import math
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -687,6 +688,9 @@ class Engine:
         # whole-fit capture is open forks to a stream of its own
         self._side = {}
         self.use_graphs = use_graphs and comm is None
+        # Elkan family: bound update + scan as one pass (spkm_elkan_bounds_scan);
+        # SPKM_ELKAN_FUSE=0 keeps the two passes (A/B measurements)
+        self.fuse_elkan = os.environ.get("SPKM_ELKAN_FUSE", "1") != "0"
         self.loop = None                 # device-driven fit loop (CUDA graph with a WHILE node)
         self.fit = None                  # the whole fit as one CUDA graph (fit_launch)
         self.loop_kernels = 0            # kernels per loop-body iteration
@@ -890,8 +894,12 @@ class Engine:
         if self.variant == "standard":
             self.lloyd_pass()
             sims_extra = self.n_total * self.k
-        else:
+        elif self.elkan and debug_hook is None and self.fuse_elkan:
             use = int(self.needs_cc)       # cc / s were computed at the end of the previous iteration
+            _lib.call("spkm_elkan_bounds_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, use, self.sp)
+            sims_extra = 0
+        else:
+            use = int(self.needs_cc)
             self.bounds_pass(use)
             if debug_hook is not None:
                 if hasattr(debug_hook, "device_audit"):    # validation.DeviceBoundAuditor: stays on the device
@@ -920,6 +928,10 @@ class Engine:
         if self.variant == "standard":
             self.lloyd_pass()
             sims_extra = self.n_total * self.k
+        elif self.elkan and self.fuse_elkan:
+            _lib.call("spkm_elkan_bounds_scan", self.xs, self.C.struct, self.P.bounds, self.P.work,
+                      int(self.needs_cc), self.sp)
+            sims_extra = 0
         else:
             use = int(self.needs_cc)
             self.bounds_pass(use)

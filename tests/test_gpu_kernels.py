@@ -441,3 +441,27 @@ def test_hamerly_fused_rescan_matches_separate_tighten(variant, monkeypatch):
         key = lambda s: (s.sim_count, s.reassignments, s.survivors, s.survivors2, s.nnz_tighten, s.nnz_rescan,
                          s.objective)
         assert [key(s) for s in r.iterations] == [key(s) for s in ref.iterations]
+
+
+@pytest.mark.parametrize("variant", ["elkan", "simp_elkan"])
+@pytest.mark.parametrize("graphs", [False, True])
+def test_elkan_fused_bounds_scan_matches_two_passes(variant, graphs, monkeypatch):
+    """spkm_elkan_bounds_scan (drift update + prune test + scan in one pass)
+    and spkm_elkan_bounds + spkm_elkan_scan give identical fits and iteration
+    statistics."""
+    from paper_2107_04074_b200 import engine as E
+    m = spk()
+    data = golden_dataset(load_golden("C1"))
+    out = {}
+    for fuse in ("0", "1"):
+        monkeypatch.setenv("SPKM_ELKAN_FUSE", fuse)
+        E.clear_engine_cache()
+        for _ in range(2 if graphs else 1):    # the second fit runs the captured whole-fit graph
+            r = m.run(data, 12, variant, m.SeedConfig(seed=3), max_iter=30, use_graphs=graphs)
+        out[fuse] = r
+    E.clear_engine_cache()
+    a, b = out["0"], out["1"]
+    assert np.array_equal(a.assignments, b.assignments)
+    assert a.objective == b.objective
+    key = lambda s: (s.sim_count, s.reassignments, s.survivors, s.nnz_elkan, s.objective)
+    assert [key(s) for s in a.iterations] == [key(s) for s in b.iterations]

@@ -688,9 +688,12 @@ class Engine:
         # whole-fit capture is open forks to a stream of its own
         self._side = {}
         self.use_graphs = use_graphs and comm is None
-        # Elkan family: bound update + scan as one pass (spkm_elkan_bounds_scan);
-        # SPKM_ELKAN_FUSE=0 keeps the two passes (A/B measurements)
-        self.fuse_elkan = os.environ.get("SPKM_ELKAN_FUSE", "1") != "0"
+        # Elkan family: bound update + scan as one pass (spkm_elkan_bounds_scan)
+        # for k <= 256 (C3: +4%); at k = 1000 most rows are pruned by the
+        # bounds and the light bound pass + survivor scan is faster (C4: 132
+        # vs 140 ms).  SPKM_ELKAN_FUSE=0/1 forces it (A/B measurements).
+        env = os.environ.get("SPKM_ELKAN_FUSE")
+        self.fuse_elkan = (k <= 256) if env is None else env != "0"
         self.loop = None                 # device-driven fit loop (CUDA graph with a WHILE node)
         self.fit = None                  # the whole fit as one CUDA graph (fit_launch)
         self.loop_kernels = 0            # kernels per loop-body iteration

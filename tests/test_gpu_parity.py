@@ -18,12 +18,13 @@ MARGIN = 1e-5
 OBJ_RTOL = 1e-6
 
 
-def check_vs_oracle(r, ref_assign, ref_obj, ref_iters, margin):
+def check_vs_oracle(r, ref_assign, ref_obj, ref_iters, margin, check_iters=True):
     ok = margin > MARGIN
     bad = np.nonzero((r.assignments != ref_assign) & ok)[0]
     assert bad.size == 0, f"{bad.size} confident points differ, e.g. {bad[:5]}"
     assert abs(r.objective - ref_obj) <= OBJ_RTOL * max(1.0, abs(ref_obj)), (r.objective, ref_obj)
-    assert abs(len(r.iterations) - ref_iters) <= 1, (len(r.iterations), ref_iters)
+    if check_iters:
+        assert abs(len(r.iterations) - ref_iters) <= 1, (len(r.iterations), ref_iters)
 
 
 @pytest.mark.parametrize("name", golden_names())
@@ -103,3 +104,67 @@ def test_c5_dense_subsample_parity(oracle_mod):
     assert np.max(np.abs(best - rb)) < 3e-5 and np.max(np.abs(second - rs)) < 3e-5
     with pytest.raises(spk.ConfigError):
         spk.run(data, 10, "elkan", spk.SeedConfig(seed=5), max_iter=3)
+
+
+def _edge_dataset(kind):
+    from paper_2107_04074_b200.sparse import Dataset
+    g = np.random.default_rng(11)
+    if kind == "single_nnz":          # every row has one term: many exact ties between centers
+        n, d = 300, 40
+        ip = np.arange(n + 1, dtype=np.int64)
+        idx = g.integers(0, d, n).astype(np.int64)
+        val = np.ones(n)
+    elif kind == "duplicates":        # blocks of identical rows
+        n, d = 240, 60
+        base = [np.sort(g.choice(d, 5, replace=False)) for _ in range(12)]
+        rows = [base[i % 12] for i in range(n)]
+        ip = np.zeros(n + 1, np.int64)
+        ip[1:] = np.cumsum([r.size for r in rows])
+        idx = np.concatenate(rows).astype(np.int64)
+        val = np.tile(np.arange(1.0, 6.0), n)
+    else:                             # long and short rows mixed (row-length extremes of the kernels)
+        n, d = 200, 3000
+        lens = np.where(np.arange(n) % 17 == 0, 1200, g.integers(1, 4, n))
+        ip = np.zeros(n + 1, np.int64)
+        ip[1:] = np.cumsum(lens)
+        idx = np.concatenate([np.sort(g.choice(d, L, replace=False)) for L in lens]).astype(np.int64)
+        val = g.uniform(0.1, 1.0, idx.size)
+    return Dataset.from_csr(ip, idx, val, d, normalize_rows=True)
+
+
+@pytest.mark.parametrize("kind", ["single_nnz", "duplicates", "long_rows"])
+@pytest.mark.parametrize("k", [1, 7, 40])
+def test_edge_corpora_parity(kind, k, oracle_mod):
+    """Edge cases of the reference's tests (ties, k = 1, duplicate rows, extreme
+    row lengths): every variant equals the GPU Lloyd and the oracle.  With
+    exact ties between identical centers the iteration count is not compared:
+    the GPU keeps the incumbent on ties from iteration 2 where
+    the reference's Lloyd argmax moves tied points to the lowest index, so
+    tie-only reassignments can take the reference extra iterations."""
+    import paper_2107_04074_b200 as spk
+    data = _edge_dataset(kind)
+    X = oracle_mod.CSR(data.indptr, data.indices, data.data, data.dim)
+    ref = oracle_mod.run(X, k, "standard", seed=4, max_iter=30)
+    margin = oracle_mod.margins(X, ref["centers"])
+    base = None
+    for v in VARIANTS:
+        r = spk.run(data, k, v, spk.SeedConfig(seed=4), max_iter=30)
+        if base is None:
+            base = r
+            check_vs_oracle(r, ref["assignments"], ref["objective"][-1], ref["iterations"], margin,
+                            check_iters=kind == "long_rows")
+        else:
+            assert np.array_equal(r.assignments, base.assignments), v
+            assert r.objective == base.objective, v
+            assert [s.reassignments for s in r.iterations] == [s.reassignments for s in base.iterations], v
+
+
+def test_k_equals_n(oracle_mod):
+    """k = n: every point its own seed; one iteration, objective n (unit rows)."""
+    import paper_2107_04074_b200 as spk
+    data = _edge_dataset("duplicates")
+    sub = spk.Dataset.from_csr(data.indptr[:31], data.indices[:data.indptr[30]], data.data[:data.indptr[30]],
+                               data.dim, normalize_rows=False)
+    for v in VARIANTS:
+        r = spk.run(sub, sub.n, v, spk.SeedConfig(seed=1), max_iter=10)
+        assert r.objective == pytest.approx(float(sub.n), rel=1e-6), v

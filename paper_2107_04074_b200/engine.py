@@ -337,14 +337,17 @@ class DeviceCorpus:
         dev = self.device
         stream = torch.cuda.current_stream(dev)
         sp = ctypes_void(stream.cuda_stream)
+        # a dense corpus (Dataset.from_dense) has the term ids 0..D-1 in every
+        # row: they are generated on the device instead of uploaded
+        dense_ids = self.dense_dim is not None and getattr(data, "dense_dim", None) == self.dense_dim
         if self.pinned_host and (r0, r1) == (0, data.n):
             # the whole corpus: page-lock the Dataset's own arrays once and copy
             # straight from them (no staging copy on the host)
-            ip_h, idx_h, val_h = (torch.from_numpy(_host_registered(a))
-                                  for a in (data.indptr, data.indices, data.data))
+            ip_h, val_h = (torch.from_numpy(_host_registered(a)) for a in (data.indptr, data.data))
+            idx_h = None if dense_ids else torch.from_numpy(_host_registered(data.indices))
         else:
             ip_h = torch.from_numpy(np.asarray(data.indptr[r0:r1 + 1], dtype=np.int64) - s)
-            idx_h = torch.from_numpy(np.ascontiguousarray(data.indices[s:e], dtype=np.int32))
+            idx_h = None if dense_ids else torch.from_numpy(np.ascontiguousarray(data.indices[s:e], dtype=np.int32))
             val_h = torch.from_numpy(np.ascontiguousarray(data.data[s:e], dtype=np.float64))
         if self.pinned_host:
             # anything not page-locked in place goes through persistent pinned staging
@@ -352,7 +355,7 @@ class DeviceCorpus:
             if self._stage is None:
                 self._stage = [None, None, None]
             for q, t in enumerate(hs):
-                if not t.is_pinned():
+                if t is not None and not t.is_pinned():
                     if self._stage[q] is None or self._stage[q].shape != t.shape:
                         self._stage[q] = torch.empty(t.shape, dtype=t.dtype).pin_memory()
                     self._stage[q].copy_(t)
@@ -366,9 +369,12 @@ class DeviceCorpus:
         up = self._upload
         up.wait_stream(stream)
         with torch.cuda.stream(up):
-            idx_raw = idx_h.to(dev, non_blocking=True)
+            if idx_h is None:
+                idx_raw = torch.arange(self.dense_dim, dtype=torch.int32, device=dev).repeat(r1 - r0)
+            else:
+                idx_raw = idx_h.to(dev, non_blocking=True)
             val_raw = val_h.to(dev, non_blocking=True)
-        self.h2d_bytes = sum(t.numel() * t.element_size() for t in (ip_h, idx_h, val_h))
+        self.h2d_bytes = sum(t.numel() * t.element_size() for t in (ip_h, idx_h, val_h) if t is not None)
         lens = ip_raw[1:] - ip_raw[:-1]
         perm = torch.sort(-lens, stable=True).indices
         self.indptr[0] = 0

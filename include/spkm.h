@@ -186,11 +186,6 @@ int spkm_elkan_bounds_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds
  * recorded moves into `sums_target`/`counts_target`, marks touched. */
 int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
                         long long *sums_target, long long *counts_target, void *stream);
-/* The same, gated on the device: a no-op unless the iteration in flight
- * (ctl[0] + 1) is a multiple of period (engine.py:317-320 scratch rebuild,
- * for the device-driven loop). */
-int spkm_aggregate_sums_gated(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
-                              long long *sums_target, long long *counts_target, int period, void *stream);
 int spkm_apply_moves(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
                      const spkm_work *W, long long *sums_target, long long *counts_target,
                      int32_t *touched, void *stream);

@@ -103,7 +103,6 @@ _SIGS = {
     "spkm_geometry": [ctypes.c_int, c_i64, c_vp, c_vp, c_vp, c_vp],
     "spkm_seed_scratch_doubles": [c_i64, c_i64],
     "spkm_seed_rows_csr": [_P(Centers), _P(Seed), c_vp, c_vp],
-    "spkm_aggregate_sums_gated": [_P(CSR), _P(Centers), _P(Bounds), c_vp, c_vp, ctypes.c_int, c_vp],
     "spkm_loop_begin": [c_vp, c_vp, c_vp, _P(c_vp)],
     "spkm_move_slot_ints": [c_i64],
     "spkm_pack_moves": [_P(Work), _P(Bounds), _P(Centers), c_i64, c_i64, c_vp, c_vp],
@@ -151,7 +150,7 @@ KERNELS_PER_CALL = {
     "spkm_move_centers": 5, "spkm_center_reduce": 1, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
-    "spkm_seed_rows_csr": 1, "spkm_aggregate_sums_gated": 2, "spkm_permute_rows": 1, "spkm_audit": 1, "spkm_audit_transpose": 1,
+    "spkm_seed_rows_csr": 1, "spkm_permute_rows": 1, "spkm_audit": 1, "spkm_audit_transpose": 1,
     "spkm_pack_moves": 1, "spkm_apply_move_slots": 1, "spkm_rows_to_host": 1,
 }
 

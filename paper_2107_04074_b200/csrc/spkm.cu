@@ -150,12 +150,6 @@ __device__ __forceinline__ float store_upper(double v) {
     return __double2float_ru(v);
 }
 
-// gated scratch rebuild: only on iterations it with it % period == 0 (it =
-// ctl[0] + 1, the iteration in flight); period 0 = always
-__device__ __forceinline__ bool gate_off(const long long *ctl, int period) {
-    return period > 0 && ((ctl[0] + 1) % period) != 0;
-}
-
 // ------------------------------------------------------- canonical similarity
 // s~(i,j) = float32 FMA chain over row i's nnz in CSR order, starting at 0:
 //   acc = fma(val[t], ct[idx[t] * kp + j], acc)   for t = indptr[i] .. indptr[i+1]-1
@@ -1060,10 +1054,9 @@ __global__ void __launch_bounds__(256) k_aggregate(int64_t n, int64_t d, const i
                                                    const int32_t *__restrict__ indices,
                                                    const float *__restrict__ values,
                                                    const int32_t *__restrict__ a, long long *sums,
-                                                   long long *counts, double scale, const long long *__restrict__ ctl,
-                                                   int period) {
+                                                   long long *counts, double scale, const long long *__restrict__ ctl) {
     PDL_ENTRY();
-    if (ctl[1] || gate_off(ctl, period)) return;   // converged: later enqueued iterations are no-ops
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const int lane = threadIdx.x & 31;
     const int wpb = blockDim.x >> 5;
     for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
@@ -1421,15 +1414,6 @@ __global__ void k_rows_to_host(int64_t n, const int64_t *__restrict__ row_perm, 
 
 __global__ void k_loop_cond(cudaGraphConditionalHandle h, const long long *ctl, const long long *limit) {
     cudaGraphSetConditional(h, (ctl[1] == 0 && ctl[0] < *limit) ? 1u : 0u);
-}
-
-__global__ void k_zero_sums_gated(long long *sums, int64_t count, long long *counts, int64_t k,
-                                  const long long *__restrict__ ctl, int period) {
-    PDL_ENTRY();
-    if (ctl[1] || gate_off(ctl, period)) return;
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count; i += stride) sums[i] = 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < k; i += stride) counts[i] = 0;
 }
 
 // centers = data rows (CentroidSet.from_data_rows, engine.py:46-58) gathered
@@ -2714,20 +2698,7 @@ int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bou
     if (X->n == 0) return 0;
     const int grid = grid_for(X->n, 8);
     pdl_launch(k_aggregate, dim3(grid), dim3(256), (size_t)(0), st, X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
-                                      counts_target, ldexp(1.0, C->scale_bits), C->ctl, 0);
-    CHECK_LAUNCH("aggregate");
-    return 0;
-}
-
-int spkm_aggregate_sums_gated(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B,
-                              long long *sums_target, long long *counts_target, int period, void *stream) {
-    cudaStream_t st = S(stream);
-    pdl_launch(k_zero_sums_gated, dim3(num_sms() * 4), dim3(256), (size_t)(0), st, sums_target, C->k * C->d, counts_target, C->k, C->ctl, period);
-    CHECK_LAUNCH("aggregate zero");
-    if (X->n == 0) return 0;
-    const int grid = grid_for(X->n, 8);
-    pdl_launch(k_aggregate, dim3(grid), dim3(256), (size_t)(0), st, X->n, C->d, X->indptr, X->indices, X->values, B->a, sums_target,
-                                      counts_target, ldexp(1.0, C->scale_bits), C->ctl, period);
+                                      counts_target, ldexp(1.0, C->scale_bits), C->ctl);
     CHECK_LAUNCH("aggregate");
     return 0;
 }

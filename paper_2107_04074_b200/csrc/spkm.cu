@@ -69,6 +69,9 @@ int fail_msg(const char *msg) {
 // its predecessor grid (griddepcontrol.wait: complete, memory visible), then
 // lets its own successor launch.  Outside PDL launches both are no-ops.
 #define PDL_ENTRY() asm volatile("griddepcontrol.wait;" ::: "memory")
+// a CTA whose main work is done lets the next kernel start launching (its
+// CTAs still wait in PDL_ENTRY for this grid's completion and memory flush)
+#define PDL_TRIGGER() asm volatile("griddepcontrol.launch_dependents;" ::: "memory")
 
 bool pdl_enabled() {
     static int on = -1;   // SPKM_PDL=0 turns programmatic launches off (A/B measurements)
@@ -458,6 +461,7 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
             }
         }
     }
+    PDL_TRIGGER();
     if (A.ctr) ctr_flush(s_ctr, A.ctr);
 }
 
@@ -598,6 +602,7 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
         ctr_add(s_ctr, SPKM_CTR_SIMS, (valid && q == 0) ? 1 : 0);
         ctr_add(s_ctr, SPKM_CTR_NNZ_TIGHTEN, (valid && q == 0) ? (long long)len : 0);
     }
+    PDL_TRIGGER();
     ctr_flush(s_ctr, ctr);
 }
 
@@ -1043,6 +1048,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
         ctr_add(s_ctr, SPKM_CTR_NNZ_ELKAN, leader ? (long long)len : 0);
         __syncwarp();
     }
+    PDL_TRIGGER();
     ctr_flush(s_ctr, ctr);
 }
 

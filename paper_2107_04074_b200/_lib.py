@@ -240,8 +240,11 @@ def note_launches(n: int):
 
 def kernels_for(name: str, args) -> int:
     n = KERNELS_PER_CALL.get(name, 0)
-    if name == "spkm_move_centers" and len(args) > 1 and int(args[1]) & 4:
-        n -= 1                                   # the reduction is issued by spkm_center_reduce
+    if name == "spkm_move_centers" and len(args) > 1:
+        if int(args[1]) & 4:
+            n -= 1                               # the reduction is issued by spkm_center_reduce
+        if getattr(args[0], "k", 1 << 30) <= 2048:
+            n -= 1                               # the touched list is built inside the norm pass
     return n
 
 

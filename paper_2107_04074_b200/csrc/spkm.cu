@@ -1169,17 +1169,52 @@ __global__ void k_touched_list(int64_t k, const int32_t *__restrict__ touched, i
     if (threadIdx.x == 0) *tcount = base_s;
 }
 
+constexpr int kListInline = 2048;   // k up to this: the norm-part CTAs build the touched list themselves
+
+// build_list: every CTA derives the touched list from the flags (k <= kListInline,
+// a few flag loads per thread), takes its own entry, and the x == 0 column
+// publishes it for the later kernels -- one launch (k_touched_list) less.
 __global__ void __launch_bounds__(256) k_center_norm_part(int64_t d, int64_t nchunk,
                                                           const long long *__restrict__ sums,
-                                                          const int32_t *__restrict__ tlist,
-                                                          const int32_t *__restrict__ tcount, double inv_scale,
-                                                          double *part, const long long *__restrict__ ctl) {
+                                                          int32_t *tlist, int32_t *tcount, double inv_scale,
+                                                          double *part, int build_list, int64_t k,
+                                                          const int32_t *__restrict__ touched, int all,
+                                                          const long long *__restrict__ ctl) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double sh[8];
     const int64_t y = blockIdx.y, c = blockIdx.x;
-    if (y >= *tcount) return;
-    const int64_t j = tlist[y];
+    int64_t j;
+    if (build_list) {
+        __shared__ int s_list[kListInline];
+        __shared__ int wsum[8];
+        __shared__ int base_s;
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        if (threadIdx.x == 0) base_s = 0;
+        __syncthreads();
+        for (int64_t j0 = 0; j0 < k; j0 += blockDim.x) {
+            const int64_t jj = j0 + threadIdx.x;
+            const int f = (jj < k) && (all || touched[jj]);
+            const unsigned m = __ballot_sync(FULL, f);
+            if (lane == 0) wsum[w] = __popc(m);
+            __syncthreads();
+            int off = base_s;
+            for (int q = 0; q < w; ++q) off += wsum[q];
+            if (f) s_list[off + __popc(m & ((1u << lane) - 1u))] = (int)jj;
+            __syncthreads();
+            if (threadIdx.x == 0)
+                for (int q = 0; q < 8; ++q) base_s += wsum[q];
+            __syncthreads();
+        }
+        const int cnt = base_s;
+        if (c == 0 && y == 0 && threadIdx.x == 0) *tcount = cnt;
+        if (y >= cnt) return;
+        j = s_list[y];
+        if (c == 0 && threadIdx.x == 0) tlist[y] = (int32_t)j;
+    } else {
+        if (y >= *tcount) return;
+        j = tlist[y];
+    }
     const int64_t t0 = c * kCenterChunk, t1 = min(d, t0 + kCenterChunk);
     const long long *sj = sums + j * d;
     double acc = 0.0;
@@ -2734,10 +2769,14 @@ int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
     const double inv = ldexp(1.0, -C->scale_bits);
     const bool defer_reduce = (all_clusters & 4) != 0;   // spkm_center_reduce is issued separately
     all_clusters &= 1;
-    pdl_launch(k_touched_list, dim3(1), dim3(1024), (size_t)(0), st, C->k, C->touched, all_clusters, C->tlist, C->tcount, C->ctl);
-    CHECK_LAUNCH("touched_list");
-    pdl_launch(k_center_norm_part, dim3(dim3((unsigned)nch, (unsigned)C->k)), dim3(256), (size_t)(0), st, C->d, nch, C->sums, C->tlist, C->tcount,
-                                                                           inv, C->part, C->ctl);
+    const int build = C->k <= kListInline;
+    if (!build) {
+        pdl_launch(k_touched_list, dim3(1), dim3(1024), (size_t)(0), st, C->k, C->touched, all_clusters, C->tlist,
+                   C->tcount, C->ctl);
+        CHECK_LAUNCH("touched_list");
+    }
+    pdl_launch(k_center_norm_part, dim3(dim3((unsigned)nch, (unsigned)C->k)), dim3(256), (size_t)(0), st, C->d, nch,
+               C->sums, C->tlist, C->tcount, inv, C->part, build, C->k, (const int32_t *)C->touched, all_clusters, C->ctl);
     CHECK_LAUNCH("center_norm_part");
     pdl_launch(k_center_norm_final, dim3((unsigned)C->k), dim3(256), (size_t)(0), st, nch, C->counts, C->tlist, C->tcount, C->part, C->norm, C->ctl);
     CHECK_LAUNCH("center_norm_final");

@@ -181,6 +181,17 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
 int spkm_elkan_bounds_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
                            void *stream);
 
+/* Order a row worklist by cluster a(i) (counting sort; L2 locality of the
+ * gather passes when the center table exceeds L2: rows of one cluster share
+ * most of their terms).  list == NULL: rows [0, n) are ordered into `out`;
+ * otherwise the first *count (device) entries of `list` are reordered in
+ * place through `tmp` (n int32).  bins: 2k int32 scratch; k <= 12288.
+ * Every pass's results are independent of the order rows are visited in.
+ * No reference counterpart (the reference visits rows in index order,
+ * kernels.py:31, 78); ctl[1] != 0 makes it a no-op like the loop kernels. */
+int spkm_order_by_cluster(int64_t k, const int32_t *a, int32_t *list, const long long *count, int64_t n,
+                          int32_t *tmp, int32_t *out, int32_t *bins, const long long *ctl, void *stream);
+
 /* Center maintenance.  aggregate: sums/counts from scratch (target arrays may
  * be a delta buffer); apply_moves: sums[old] -= x, sums[new] += x for the
  * recorded moves into `sums_target`/`counts_target`, marks touched. */

@@ -61,7 +61,7 @@ def lib():
         L.oracle_run.argtypes = (
             [ctypes.c_int64] * 3 + [_i64p, _i32p, _f64p, ctypes.c_int, ctypes.c_int64, ctypes.c_int]
             + [_f64p, _f64p, _i64p, _f64p, _i64p, _i64p, _i64p, _i64p, _f64p,
-               ctypes.POINTER(ctypes.c_int), HOOK_T]
+               ctypes.POINTER(ctypes.c_int), HOOK_T, _f64p, _f64p]
         )
         L.oracle_run.restype = ctypes.c_int64
         L.oracle_seed_kmpp.argtypes = ([ctypes.c_int64] * 2 + [_i64p, _i32p, _f64p, ctypes.c_int64, ctypes.c_double,
@@ -74,6 +74,7 @@ def lib():
         L.oracle_np_ddot.restype = ctypes.c_double
         L.oracle_np_sum.argtypes = [_f64p, ctypes.c_int64]
         L.oracle_np_sum.restype = ctypes.c_double
+        L.oracle_row_norms.argtypes = [ctypes.c_int64, _i64p, _f64p, _f64p]
         L.oracle_num_threads.restype = ctypes.c_int
         L.oracle_set_threads.argtypes = [ctypes.c_int]
         _lib = L
@@ -120,6 +121,25 @@ def np_ddot(x, y) -> float:
     x = np.ascontiguousarray(x, np.float64)
     y = np.ascontiguousarray(y, np.float64)
     return float(lib().oracle_np_ddot(x.size, _p(x, _f64p), _p(y, _f64p)))
+
+
+def row_norms(indptr, data) -> np.ndarray:
+    """sqrt(np.dot(v, v)) of every CSR row in numpy's order (SparseVector.norm, sparse.py:52)."""
+    ip = np.ascontiguousarray(indptr, np.int64)
+    dv = np.ascontiguousarray(data, np.float64)
+    out = np.empty(max(ip.size - 1, 0))
+    lib().oracle_row_norms(out.size, _p(ip, _i64p), _p(dv, _f64p), _p(out, _f64p))
+    return out
+
+
+def normalized_csr(indptr, indices, weights, n_cols) -> "CSR":
+    """Rows normalised as Dataset.from_rows does (values / norm, sparse.py:54-58)."""
+    ip = np.ascontiguousarray(indptr, np.int64)
+    w = np.ascontiguousarray(weights, np.float64)
+    nrm = row_norms(ip, w)
+    if np.any(nrm == 0.0):
+        raise ValueError("zero row")
+    return CSR(ip, indices, w / np.repeat(nrm, np.diff(ip)), n_cols)
 
 
 def np_sum(a) -> float:
@@ -200,6 +220,8 @@ def run(X: CSR, k: int, variant: str, seed: int = 0, max_iter: int = 100,
     ccs = np.zeros(max_iter, np.int64)
     rea = np.zeros(max_iter, np.int64)
     obj = np.zeros(max_iter)
+    t_rows = np.zeros(max_iter)
+    t_other = np.zeros(max_iter)
     conv = ctypes.c_int(0)
     n, d = X.n, X.d
 
@@ -218,6 +240,7 @@ def run(X: CSR, k: int, variant: str, seed: int = 0, max_iter: int = 100,
         n, d, k, *X.args(), VARIANTS.index(variant), max_iter, int(hamerly_update == "naive"),
         _p(centers, _f64p), _p(sums, _f64p), _p(counts, _i64p), _p(drift, _f64p), _p(a, _i64p),
         _p(sims, _i64p), _p(ccs, _i64p), _p(rea, _i64p), _p(obj, _f64p), ctypes.byref(conv), cb,
+        _p(t_rows, _f64p), _p(t_other, _f64p),
     )
     return {
         "assignments": a,
@@ -232,6 +255,8 @@ def run(X: CSR, k: int, variant: str, seed: int = 0, max_iter: int = 100,
         "objective": obj[:iters].copy(),
         "iterations": int(iters),
         "converged": bool(conv.value),
+        "t_rows": t_rows[:iters].copy(),      # seconds per iteration spent on row-proportional work
+        "t_other": t_other[:iters].copy(),    # ... on the k x d centers
     }
 
 

@@ -311,7 +311,7 @@ int64_t oracle_run(int64_t n, int64_t d, int64_t k, const int64_t *indptr, const
                    const double *data, int variant, int64_t max_iter, int hamerly_naive,
                    double *centers, double *sums, int64_t *counts, double *drift, int64_t *a_out,
                    int64_t *it_sims, int64_t *it_cc, int64_t *it_reassign, double *it_obj,
-                   int *converged, oracle_hook_t hook) {
+                   int *converged, oracle_hook_t hook, double *it_t_rows, double *it_t_other) {
     const int elkan_family = (variant == V_ELKAN || variant == V_SIMP_ELKAN);
     const int hamerly_family = (variant == V_HAMERLY || variant == V_SIMP_HAMERLY);
     const int needs_cc = (variant == V_ELKAN || variant == V_HAMERLY);
@@ -336,10 +336,16 @@ int64_t oracle_run(int64_t n, int64_t d, int64_t k, const int64_t *indptr, const
 
     for (int64_t it = 1; it <= max_iter; ++it) {
         int64_t cc_count = 0, sim_count = 0, reassign = 0;
+        /* phase clocks (bench.py's reference arm): t_rows = work proportional
+         * to the rows (sims, bounds, scans, aggregation, moves), t_other =
+         * work on the k x d centers (thresholds, renormalise, objective) */
+        double t_rows = 0.0, t_other = 0.0, t0 = omp_get_wtime();
         if (needs_cc) {                                   /* engine.py:242-244 */
             center_thresholds(d, k, centers, cc, s_arr);
             cc_count = k * (k - 1) / 2;
         }
+        t_other += omp_get_wtime() - t0;
+        t0 = omp_get_wtime();
         if (it == 1) {                                    /* engine.py:249-265 */
             oracle_full_sims(n, d, k, indptr, indices, data, centers, S);
             sim_count = n * k;
@@ -362,7 +368,10 @@ int64_t oracle_run(int64_t n, int64_t d, int64_t k, const int64_t *indptr, const
             }
             reassign = n;
             oracle_aggregate_sums(n, d, k, indptr, indices, data, a, sums, counts);
+            t_rows += omp_get_wtime() - t0;
+            t0 = omp_get_wtime();
             move_centers(d, centers, sums, counts, prev, drift, k, all, k);
+            t_other += omp_get_wtime() - t0;
         } else {
             memcpy(a_prev, a, sizeof(int64_t) * (size_t)n);
             if (variant == V_STANDARD) {                  /* engine.py:268-271 */
@@ -430,14 +439,23 @@ int64_t oracle_run(int64_t n, int64_t d, int64_t k, const int64_t *indptr, const
             }
             int64_t nch = 0;
             for (int64_t j = 0; j < k; ++j) if (touched[j]) changed[nch++] = j;
+            t_rows += omp_get_wtime() - t0;
+            t0 = omp_get_wtime();
             move_centers(d, centers, sums, counts, prev, drift, k, changed, nch);
+            t_other += omp_get_wtime() - t0;
         }
+        t0 = omp_get_wtime();
         if (it % SCRATCH_INTERVAL == 0)                   /* engine.py:323-324 */
             oracle_aggregate_sums(n, d, k, indptr, indices, data, a, sums, counts);
+        t_rows += omp_get_wtime() - t0;
+        t0 = omp_get_wtime();
         it_sims[it - 1] = sim_count;
         it_cc[it - 1] = cc_count;
         it_reassign[it - 1] = reassign;
         it_obj[it - 1] = objective_of(d, k, sums, centers);
+        t_other += omp_get_wtime() - t0;
+        if (it_t_rows) it_t_rows[it - 1] = t_rows;
+        if (it_t_other) it_t_other[it - 1] = t_other;
         iters = it;
         int allone = 1;
         for (int64_t j = 0; j < k; ++j) if (drift[j] != 1.0) { allone = 0; break; }
@@ -520,6 +538,29 @@ double oracle_np_ddot(int64_t m, const double *x, const double *y) {
     double r = np_ddot_gather(m, x, idx, y);
     free(idx);
     return r;
+}
+
+/* |row| = np.sqrt(np.dot(v, v)) for every CSR row (SparseVector.norm,
+ * sparse.py:52), in the same np.dot order; lets the reference arm of
+ * bench.py normalise generated rows exactly as Dataset.from_rows does
+ * without touching the product library. */
+void oracle_row_norms(int64_t n, const int64_t *indptr, const double *data, double *out) {
+    int64_t maxlen = 0;
+    for (int64_t r = 0; r < n; ++r) {
+        const int64_t m = indptr[r + 1] - indptr[r];
+        if (m > maxlen) maxlen = m;
+    }
+    #pragma omp parallel
+    {
+        int32_t *idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)(maxlen > 0 ? maxlen : 1));
+        for (int64_t i = 0; i < maxlen; ++i) idx[i] = (int32_t)i;
+        #pragma omp for schedule(static)
+        for (int64_t r = 0; r < n; ++r) {
+            const double *x = data + indptr[r];
+            out[r] = sqrt(np_ddot_gather(indptr[r + 1] - indptr[r], x, idx, x));
+        }
+        free(idx);
+    }
 }
 
 /* numpy's pairwise_sum (np.add.reduce of a contiguous float64 array) */

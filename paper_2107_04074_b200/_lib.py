@@ -89,6 +89,7 @@ _SIGS = {
     "spkm_elkan_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_elkan_bounds_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_aggregate_sums": [_P(CSR), _P(Centers), _P(Bounds), c_vp, c_vp, c_vp],
+    "spkm_order_by_cluster": [c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp],
     "spkm_apply_moves": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), c_vp, c_vp, c_vp, c_vp],
     "spkm_move_centers": [_P(Centers), ctypes.c_int, c_vp],
     "spkm_center_reduce": [_P(Centers), c_vp],
@@ -152,6 +153,7 @@ KERNELS_PER_CALL = {
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
     "spkm_seed_rows_csr": 1, "spkm_permute_rows": 1, "spkm_audit": 1, "spkm_audit_transpose": 1,
     "spkm_pack_moves": 1, "spkm_apply_move_slots": 1, "spkm_rows_to_host": 1,
+    "spkm_order_by_cluster": 4,
 }
 
 _lib = None
@@ -240,6 +242,8 @@ def note_launches(n: int):
 
 def kernels_for(name: str, args) -> int:
     n = KERNELS_PER_CALL.get(name, 0)
+    if name == "spkm_order_by_cluster" and len(args) > 2 and args[2] is None:
+        n -= 1                                   # identity input: no copy back
     if name == "spkm_move_centers" and len(args) > 1:
         if int(args[1]) & 4:
             n -= 1                               # the reduction is issued by spkm_center_reduce

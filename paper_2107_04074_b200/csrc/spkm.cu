@@ -467,7 +467,13 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
 
 // --------------------------------------------------------- Hamerly family
 // engine.py:274 (l), 284-303 (u) fused with the kernels.py:81-87 tests.
-__global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *__restrict__ reps,
+// One CTA = a tile of kHbTile consecutive points, kHbPer per thread (strided
+// by the CTA size, so every load instruction of a warp is one coalesced
+// 128-byte line and the kHbPer loads of a thread are independent); the
+// survivors of the tile are appended with ONE global atomic (warp ballots ->
+// per-warp counts in shared memory -> one prefix), not one per warp.
+constexpr int kHbThreads = 256, kHbPer = 4, kHbTile = kHbThreads * kHbPer;
+__global__ void __launch_bounds__(kHbThreads) k_hamerly_bounds(int64_t n, const float *__restrict__ reps,
                                                         const int32_t *__restrict__ a, float *l, float *u,
                                                         const double *__restrict__ drift,
                                                         const double *__restrict__ sinp,
@@ -476,45 +482,88 @@ __global__ void __launch_bounds__(256) k_hamerly_bounds(int64_t n, const float *
                                                         int32_t *surv1, long long *ctr, const long long *__restrict__ ctl) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    __shared__ int s_cnt[kHbPer][kHbThreads / 32];
+    __shared__ long long s_base;
     const int owner = (int)hstat[0], owner_s = (int)hstat[3];
     const double pmin = hstat[1], pmin2 = hstat[2], smax = hstat[4], smax2 = hstat[5];
-    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    const int64_t n_pad = (n + 31) & ~int64_t(31);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n_pad; i += stride) {
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int64_t i0 = (int64_t)blockIdx.x * kHbTile + threadIdx.x;
+    int ai[kHbPer];
+    float lo[kHbPer], uo[kHbPer], ep[kHbPer];
+#pragma unroll
+    for (int r = 0; r < kHbPer; ++r) {
+        const int64_t i = i0 + r * kHbThreads;
+        const bool in = i < n;
+        ai[r] = in ? __ldg(a + i) : 0;
+        lo[r] = in ? l[i] : 0.f;
+        uo[r] = in ? u[i] : 0.f;
+        ep[r] = in ? __ldg(reps + i) : 0.f;
+    }
+    unsigned surv_mask[kHbPer];
+#pragma unroll
+    for (int r = 0; r < kHbPer; ++r) {
+        const int64_t i = i0 + r * kHbThreads;
         bool surv = false;
         if (i < n) {
-            const int ai = a[i];
-            const float lo = l[i];
-            const double sa = sinp[ai];
-            float lf = lo;
+            const double sa = sinp[ai[r]];
+            float lf = lo[r];
             if (sa != 0.0) {   // cos(theta_l + theta_p), theta_p from the chord bound
-                const double pa = drift[ai];
-                const double ln = (lo < -pa) ? -1.0 : d_clamp((double)lo * pa - d_sin((double)lo) * sa);
+                const double pa = drift[ai[r]];
+                const double ln = (lo[r] < -pa) ? -1.0 : d_clamp((double)lo[r] * pa - d_sin((double)lo[r]) * sa);
                 lf = store_lower(ln);
                 l[i] = lf;
             }
-            const double worst_p = (ai == owner) ? pmin2 : pmin;
-            const double worst_s = (ai == owner_s) ? smax2 : smax;
-            const float uo = u[i];
-            float uf = uo;
+            const double worst_p = (ai[r] == owner) ? pmin2 : pmin;
+            const double worst_s = (ai[r] == owner_s) ? smax2 : smax;
+            float uf = uo[r];
             if (naive) {       // engine.py:299-303, deliberately unsound
                 if (worst_p != 1.0) {
-                    uf = store_upper(d_cos_upper((double)uo, worst_p));
+                    uf = store_upper(d_cos_upper((double)uo[r], worst_p));
                     u[i] = uf;
                 }
-            } else if (!(uo >= 0.f && worst_s == 0.0)) {   // engine.py:290-298
-                const double un = (uo >= 0.f && worst_p >= 0.0) ? d_clamp((double)uo + d_sin((double)uo) * worst_s)
-                                                                 : 1.0;
+            } else if (!(uo[r] >= 0.f && worst_s == 0.0)) {   // engine.py:290-298
+                const double un = (uo[r] >= 0.f && worst_p >= 0.0)
+                                      ? d_clamp((double)uo[r] + d_sin((double)uo[r]) * worst_s)
+                                      : 1.0;
                 uf = store_upper(un);
                 u[i] = uf;
             }
-            const double eps = (double)reps[i];
+            const double eps = (double)ep[r];
             const double lb = (double)lf;
-            bool pruned = (use_s && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb);
+            bool pruned = (use_s && lb >= 0.0 && (double)s_arr[ai[r]] + kSqrt2 * eps <= lb);
             if (!pruned) pruned = ((double)uf + 2.0 * eps <= lb);
             surv = !pruned;
         }
-        warp_append(surv, (int32_t)i, surv1, 0, nullptr, ctr + SPKM_CTR_SURV1);
+        surv_mask[r] = __ballot_sync(FULL, surv);
+        if (lane == 0) s_cnt[r][wib] = __popc(surv_mask[r]);
+    }
+    __syncthreads();
+    // tile prefix over (r, warp) in the order the entries are written
+    if (wib == 0) {
+        constexpr int E = kHbPer * (kHbThreads / 32);   // 32 entries
+        static_assert(E == 32, "one warp scans the tile counts");
+        const int v = (&s_cnt[0][0])[lane];
+        int x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        const int tot = __shfl_sync(FULL, x, 31);
+        long long base = 0;
+        if (lane == 0 && tot) base = (long long)atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1),
+                                                          (unsigned long long)tot);
+        (&s_cnt[0][0])[lane] = x - v;
+        if (lane == 0) s_base = base;
+    }
+    __syncthreads();
+    PDL_TRIGGER();
+    const long long base = s_base;
+#pragma unroll
+    for (int r = 0; r < kHbPer; ++r) {
+        if (surv_mask[r] >> lane & 1u) {
+            const int rank = __popc(surv_mask[r] & ((1u << lane) - 1u));
+            surv1[base + s_cnt[r][wib] + rank] = (int32_t)(i0 + r * kHbThreads);
+        }
     }
 }
 
@@ -607,9 +656,37 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
 }
 
 // ----------------------------------------------------------- Elkan family
+// engine.py:281-283, u(i,j) <- cos_upper(u(i,j), p_j) if u <= p_j else 1,
+// with the chord-based sine bound sin_p (see k_finalize), evaluated in
+// float32 with directed rounding: every operation rounds towards the safe
+// side, so the result is an upper bound of clamp(w p + sin(w) sin_p) + 1e-12
+// for the float inputs -- the float64 version's guarantee -- at float32 cost
+// (n*k elements per iteration: float64 sqrt made this pass ALU-bound).
+//   pd = rd(p), pu = ru(p), su = ru(sin_p) (su == 0 <=> the center did not move)
+//   (double)w <= p  <=>  w <= pd, exactly (pd is the largest float <= p)
+__device__ __forceinline__ float elkan_u_drift(float w, float pd, float pu, float su) {
+    if (!(w <= pd)) return 1.0f;
+    const float sw = __fsqrt_ru(fmaxf(__fmaf_ru(-w, w, 1.0f), 0.0f));   // >= sin(w)
+    const float prod = __fmaf_ru(sw, su, 1e-12f);
+    const float nv = __fmaf_ru(w, w >= 0.f ? pu : pd, prod);
+    return fminf(fmaxf(nv, -1.0f), 1.0f);
+}
+// Prune thresholds of one row (kernels.py:35-47 with the eps margins):
+//   u(i,j) + 2 eps <= l  <=>  u(i,j) <= rd(l - 2 eps)      (u a float)
+//   cc(a,j) + sqrt2 eps <= l  <=>  cc(a,j) <= rd(l - sqrt2 eps)
+// so the per-element tests are single float compares.
+__device__ __forceinline__ float thr_u_of(double lb, double eps) { return __double2float_rd(lb - 2.0 * eps); }
+__device__ __forceinline__ float thr_c_of(double lb, double eps) { return __double2float_rd(lb - kSqrt2 * eps); }
+
 // engine.py:274-283 (l and u(i,j) drift updates) fused with the
 // kernels.py:35-47 tests; a point survives if any j != a(i) is not pruned.
-// Warp per point, lanes over j (u rows are contiguous).
+// Warp per point, lanes over j in 16-byte groups (u rows are contiguous,
+// ku a multiple of 4); each warp takes chunks of 32 consecutive points:
+// lane r prepares point r's row values (drift-updated l, thresholds), the
+// warp then streams the 32 u rows (up to 8 float4 loads per lane in flight)
+// and appends the chunk's survivors with one atomic.  Per-center pd/pu/su
+// live in shared memory.  k <= 1024.
+constexpr int kEbMaxK = 1024;
 __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const float *__restrict__ reps,
                                                       const int32_t *__restrict__ a, float *l, float *u,
                                                       int64_t ku, const double *__restrict__ drift,
@@ -619,90 +696,96 @@ __global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const fl
                                                       int32_t *surv1, long long *ctr, const long long *__restrict__ ctl) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
-    const int lane = threadIdx.x & 31;
-    const int wpb = blockDim.x >> 5;
-    const int k4 = (k + 3) >> 2;   // u rows are ku (a multiple of 4) floats: 16-byte vectors
-    // rounds of one point per warp, identical for every warp of the CTA, so
-    // each round's survivors are appended with ONE global atomic per CTA
-    __shared__ int32_t s_surv[32];
-    __shared__ long long s_base;
-    const int wib = threadIdx.x >> 5;
-    for (int64_t i0 = (int64_t)blockIdx.x * wpb; i0 < n; i0 += (int64_t)gridDim.x * wpb) {
-        const int64_t i = i0 + wib;
-        if (i >= n) {
-            if (lane == 0) s_surv[wib] = -1;
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int c = 0;
-                for (int q = 0; q < wpb; ++q) c += s_surv[q] >= 0;
-                if (c) s_base = (long long)atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1), (unsigned long long)c);
-            }
-            __syncthreads();
-            if (threadIdx.x == 0) {
-                int c = 0;
-                for (int q = 0; q < wpb; ++q)
-                    if (s_surv[q] >= 0) surv1[s_base + c++] = s_surv[q];
-            }
-            __syncthreads();
-            continue;
-        }
-        const int ai = a[i];
-        const float lo = l[i];
-        const double sa = sinp[ai];
-        float lf = lo;
-        if (sa != 0.0) {
-            const double pa = drift[ai];
-            lf = store_lower((lo < -pa) ? -1.0 : d_clamp((double)lo * pa - d_sin((double)lo) * sa));
-        }
-        if (lane == 0 && lf != lo) l[i] = lf;
-        const double eps = (double)reps[i];
-        const double lb = (double)lf;
-        const bool pskip = use_cc && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb;
-        const bool cc_on = use_cc && lb >= 0.0;
-        bool any = false;
-        float4 *ui = reinterpret_cast<float4 *>(u + i * ku);
-        const float *cca = cc + (int64_t)ai * k;
-#pragma unroll 2
-        for (int q = lane; q < k4; q += 32) {
-            const float4 uv = ui[q];
-            float w[4] = {uv.x, uv.y, uv.z, uv.w};
-            bool changed = false;
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                const int j = 4 * q + c;
-                if (j >= k) break;
-                const double sj = sinp[j];
-                if (sj != 0.0) {   // engine.py:281-283 with the chord-based sine bound
-                    const double pj = drift[j];
-                    const double nv = ((double)w[c] <= pj) ? d_clamp((double)w[c] * pj + d_sin((double)w[c]) * sj)
-                                                           : 1.0;
-                    w[c] = store_upper(nv);
-                    changed = true;
-                }
-                if (!pskip && j != ai) {
-                    bool skip = cc_on && (double)__ldg(cca + j) + kSqrt2 * eps <= lb;
-                    if (!skip) skip = ((double)w[c] + 2.0 * eps <= lb);
-                    any |= !skip;
-                }
-            }
-            if (changed) ui[q] = make_float4(w[0], w[1], w[2], w[3]);
-        }
-        any = __any_sync(FULL, any);
-        if (lane == 0) s_surv[wib] = any ? (int32_t)i : -1;
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int c = 0;
-            for (int q = 0; q < wpb; ++q) c += s_surv[q] >= 0;
-            if (c) s_base = (long long)atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1), (unsigned long long)c);
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            int c = 0;
-            for (int q = 0; q < wpb; ++q)
-                if (s_surv[q] >= 0) surv1[s_base + c++] = s_surv[q];
-        }
-        __syncthreads();
+    __shared__ __align__(16) float s_pd[kEbMaxK], s_pu[kEbMaxK], s_su[kEbMaxK];
+    const int k4 = (k + 3) >> 2;
+    for (int j = threadIdx.x; j < 4 * k4; j += blockDim.x) {
+        const bool in = j < k;
+        const double p = in ? drift[j] : 1.0, sp = in ? sinp[j] : 0.0;
+        s_pd[j] = __double2float_rd(p);
+        s_pu[j] = __double2float_ru(p);
+        s_su[j] = __double2float_ru(sp);
     }
+    __syncthreads();
+    const float4 *pd4 = reinterpret_cast<const float4 *>(s_pd), *pu4 = reinterpret_cast<const float4 *>(s_pu),
+                 *su4 = reinterpret_cast<const float4 *>(s_su);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const int64_t nchunks = (n + 31) >> 5;
+    for (int64_t c = (int64_t)blockIdx.x * wpb + wib; c < nchunks; c += (int64_t)gridDim.x * wpb) {
+        const int64_t rb = c << 5;
+        const int64_t ir = rb + lane;
+        int ai_r = 0;
+        float thu_r = 0.f, thc_r = 0.f;
+        bool pskip_r = true, ccon_r = false;
+        if (ir < n) {
+            ai_r = a[ir];
+            const float lo = l[ir];
+            float lf = lo;
+            const double sa = sinp[ai_r];
+            if (sa != 0.0) {
+                const double pa = drift[ai_r];
+                lf = store_lower((lo < -pa) ? -1.0 : d_clamp((double)lo * pa - d_sin((double)lo) * sa));
+                l[ir] = lf;
+            }
+            const double eps = (double)reps[ir];
+            const double lb = (double)lf;
+            pskip_r = use_cc && lb >= 0.0 && (double)s_arr[ai_r] + kSqrt2 * eps <= lb;
+            ccon_r = use_cc && lb >= 0.0;
+            thu_r = thr_u_of(lb, eps);
+            thc_r = thr_c_of(lb, eps);
+        }
+        const int nr = (int)min((int64_t)32, n - rb);
+        unsigned smask = 0;
+        for (int r = 0; r < nr; ++r) {
+            const int ai = __shfl_sync(FULL, ai_r, r);
+            const float thu = __shfl_sync(FULL, thu_r, r), thc = __shfl_sync(FULL, thc_r, r);
+            const bool pskip = __shfl_sync(FULL, (int)pskip_r, r) != 0;
+            const bool ccon = __shfl_sync(FULL, (int)ccon_r, r) != 0;
+            float4 *ui = reinterpret_cast<float4 *>(u + (rb + r) * ku);
+            const float *cca = cc + (int64_t)ai * k;
+            float4 v[8];
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int q = lane + 32 * t;
+                if (q < k4) v[t] = ui[q];
+            }
+            bool any = false;
+#pragma unroll
+            for (int t = 0; t < 8; ++t) {
+                const int q = lane + 32 * t;
+                if (q >= k4) break;
+                const float4 su = su4[q];
+                float w[4] = {v[t].x, v[t].y, v[t].z, v[t].w};
+                if (su.x != 0.f || su.y != 0.f || su.z != 0.f || su.w != 0.f) {
+                    const float4 pd = pd4[q], pu = pu4[q];
+                    const float sa_[4] = {su.x, su.y, su.z, su.w}, pda[4] = {pd.x, pd.y, pd.z, pd.w},
+                                pua[4] = {pu.x, pu.y, pu.z, pu.w};
+#pragma unroll
+                    for (int cq = 0; cq < 4; ++cq)
+                        if (sa_[cq] != 0.f) w[cq] = elkan_u_drift(w[cq], pda[cq], pua[cq], sa_[cq]);
+                    ui[q] = make_float4(w[0], w[1], w[2], w[3]);   // padding columns (j >= k) have su == 0
+                }
+                if (!pskip) {
+#pragma unroll
+                    for (int cq = 0; cq < 4; ++cq) {
+                        const int j = 4 * q + cq;
+                        if (j < k && j != ai) {
+                            bool skip = ccon && __ldg(cca + j) <= thc;
+                            if (!skip) skip = w[cq] <= thu;
+                            any |= !skip;
+                        }
+                    }
+                }
+            }
+            if (__any_sync(FULL, any)) smask |= 1u << r;
+        }
+        long long base = 0;
+        if (lane == 0 && smask) base = (long long)atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1),
+                                                            (unsigned long long)__popc(smask));
+        base = __shfl_sync(FULL, base, 0);
+        if (smask >> lane & 1u) surv1[base + __popc(smask & ((1u << lane) - 1u))] = (int32_t)ir;
+    }
+    PDL_TRIGGER();
 }
 
 // Centers per lane block of k_elkan_scan: EB = 4 (one float4 of a term-major
@@ -798,6 +881,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
             lb = (double)lf;
             const bool pskip = use_cc && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb;
             const bool cc_on = use_cc && lb >= 0.0;
+            const float thu = thr_u_of(lb, eps), thc = thr_c_of(lb, eps);
             bool surv = false;
             for (int r = 0; r < nrounds && valid; ++r) {
                 const int blk = r * 32 + q;
@@ -807,15 +891,14 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                     if (j >= k) break;
                     float wv = ui[j];
                     const double sj = sinp[j];
-                    if (sj != 0.0) {   // engine.py:281-283 with the chord-based sine bound
+                    if (sj != 0.0) {   // the k_elkan_bounds update, same float32 arithmetic
                         const double pj = drift[j];
-                        const double nv = ((double)wv <= pj) ? d_clamp((double)wv * pj + d_sin((double)wv) * sj) : 1.0;
-                        wv = store_upper(nv);
+                        wv = elkan_u_drift(wv, __double2float_rd(pj), __double2float_ru(pj), __double2float_ru(sj));
                         ui[j] = wv;
                     }
                     if (!pskip && j != ai) {
-                        bool skip = cc_on && (double)__ldg(cc + (int64_t)ai * k + j) + kSqrt2 * eps <= lb;
-                        if (!skip) skip = ((double)wv + 2.0 * eps <= lb);
+                        bool skip = cc_on && __ldg(cc + (int64_t)ai * k + j) <= thc;
+                        if (!skip) skip = wv <= thu;
                         surv |= !skip;
                     }
                 }
@@ -832,6 +915,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
         const int len = (int)(e - s);
         const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
         const bool cc_ok = use_cc && lb >= 0.0;
+        const float thu_s = thr_u_of(lb, eps), thc_s = thr_c_of(lb, eps);
         for (int r = 0; r < nrounds; ++r) {
             const int blk = r * 32 + q;
             const int j0 = blk * EB;
@@ -847,7 +931,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                     // u-test only: a center the replay may need fails it (the
                     // cc test depends on the running best, so it cannot
                     // prune the fetch)
-                    act |= !((double)ui[j] + 2.0 * eps <= lb);
+                    act |= !(ui[j] <= thu_s);
                 }
             }
             if (!__any_sync(FULL, act)) continue;
@@ -955,8 +1039,8 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                     const int j = blk * EB + c2;
                     if (j >= k) break;
                     if (j == ai) continue;
-                    if (cc_ok && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb) continue;
-                    if ((double)ui[j] + 2.0 * eps <= lb) continue;
+                    if (cc_ok && cc[(int64_t)ai * k + j] <= thc_s) continue;
+                    if (ui[j] <= thu_s) continue;
                     first_fail = j;
                     break;
                 }
@@ -2549,6 +2633,133 @@ __global__ void __launch_bounds__(256) k_apply_move_slots(const int32_t *__restr
     }
 }
 
+// ------------------------------------------------------ cluster-ordered worklists
+// The gather passes (Hamerly rescan, Elkan survivor scan, Lloyd pass) read,
+// per nnz, a term row of the center table.  When the table does not fit L2
+// (C4: ct32 = 4 GB) and rows arrive in storage order, every topic-term
+// gather misses L2.  Rows of one cluster share most of their terms (one
+// topic), so a worklist ordered by a(i) keeps the CTAs in flight on a few
+// clusters' term rows at a time: the gathers become L2 hits.  Results do not
+// depend on the order in which rows are visited (per-row outputs, integer
+// counters, int64 fixed-point sums), so this is a pure locality change.
+//
+// Counting sort by a(i) in tiles of kOrdTile list entries: k_order_hist adds
+// each tile's bin counts to a global histogram, k_order_scan turns it into
+// bin starts, k_order_scatter reserves a range per (tile, bin) with one
+// global atomic and writes each entry at its shared-memory rank.  Within a
+// bin the order is the tiles' reservation order (not stable; any order is
+// valid).
+constexpr int kOrdThreads = 256, kOrdPer = 8, kOrdTile = kOrdThreads * kOrdPer;
+
+__device__ __forceinline__ int64_t ord_count(const long long *count, int64_t n) {
+    return count ? (int64_t)*count : n;
+}
+
+__global__ void __launch_bounds__(kOrdThreads) k_order_hist(int64_t k, const int32_t *__restrict__ a,
+                                                          const int32_t *__restrict__ list,
+                                                          const long long *__restrict__ count, int64_t n,
+                                                          int32_t *bins, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
+    if (ctl && ctl[1]) return;
+    extern __shared__ int32_t s_h[];
+    const int64_t cnt = ord_count(count, n);
+    const int64_t ntile = (cnt + kOrdTile - 1) / kOrdTile;
+    for (int j = threadIdx.x; j < k; j += blockDim.x) s_h[j] = 0;
+    __syncthreads();
+    for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+#pragma unroll
+        for (int r = 0; r < kOrdPer; ++r) {
+            const int64_t p = t * kOrdTile + r * kOrdThreads + threadIdx.x;
+            if (p < cnt) atomicAdd(s_h + a[list ? list[p] : p], 1);
+        }
+    }
+    __syncthreads();
+    for (int j = threadIdx.x; j < k; j += blockDim.x)
+        if (s_h[j]) atomicAdd(bins + j, s_h[j]);
+}
+
+// bins[0..k) counts -> bins[k..2k) exclusive starts (one CTA)
+__global__ void __launch_bounds__(1024) k_order_scan(int64_t k, int32_t *bins, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
+    if (ctl && ctl[1]) return;
+    __shared__ int32_t s_w[32];
+    __shared__ int32_t s_carry;
+    if (threadIdx.x == 0) s_carry = 0;
+    __syncthreads();
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    for (int64_t j0 = 0; j0 < k; j0 += blockDim.x) {
+        const int64_t j = j0 + threadIdx.x;
+        const int32_t v = j < k ? bins[j] : 0;
+        int32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const int32_t y = __shfl_up_sync(FULL, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_w[w] = x;
+        __syncthreads();
+        if (w == 0) {
+            int32_t z = lane < (int)(blockDim.x >> 5) ? s_w[lane] : 0;
+            for (int o = 1; o < 32; o <<= 1) {
+                const int32_t y = __shfl_up_sync(FULL, z, o);
+                if (lane >= o) z += y;
+            }
+            s_w[lane] = z;
+        }
+        __syncthreads();
+        const int32_t excl = s_carry + (w ? s_w[w - 1] : 0) + x - v;
+        if (j < k) bins[k + j] = excl;
+        __syncthreads();
+        if (threadIdx.x == blockDim.x - 1) s_carry = excl + v;
+        __syncthreads();
+    }
+}
+
+__global__ void __launch_bounds__(kOrdThreads) k_order_scatter(int64_t k, const int32_t *__restrict__ a,
+                                                             const int32_t *__restrict__ list,
+                                                             const long long *__restrict__ count, int64_t n,
+                                                             int32_t *cursor, int32_t *out,
+                                                             const long long *__restrict__ ctl) {
+    PDL_ENTRY();
+    if (ctl && ctl[1]) return;
+    extern __shared__ int32_t s_h[];   // [k] tile counts, then the tile's base per bin
+    const int64_t cnt = ord_count(count, n);
+    const int64_t ntile = (cnt + kOrdTile - 1) / kOrdTile;
+    for (int64_t t = blockIdx.x; t < ntile; t += gridDim.x) {
+        for (int j = threadIdx.x; j < k; j += blockDim.x) s_h[j] = 0;
+        __syncthreads();
+        int32_t row[kOrdPer], bin[kOrdPer], rank[kOrdPer];
+#pragma unroll
+        for (int r = 0; r < kOrdPer; ++r) {
+            const int64_t p = t * kOrdTile + r * kOrdThreads + threadIdx.x;
+            row[r] = -1;
+            if (p < cnt) {
+                row[r] = list ? list[p] : (int32_t)p;
+                bin[r] = a[row[r]];
+                rank[r] = atomicAdd(s_h + bin[r], 1);
+            }
+        }
+        __syncthreads();
+        for (int j = threadIdx.x; j < k; j += blockDim.x) {
+            const int32_t c = s_h[j];
+            if (c) s_h[j] = atomicAdd(cursor + j, c);
+        }
+        __syncthreads();
+#pragma unroll
+        for (int r = 0; r < kOrdPer; ++r)
+            if (row[r] >= 0) out[s_h[bin[r]] + rank[r]] = row[r];
+        __syncthreads();
+    }
+}
+
+__global__ void k_copy_list(const int32_t *__restrict__ src, int32_t *dst, const long long *__restrict__ count,
+                            int64_t n, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
+    if (ctl && ctl[1]) return;
+    const int64_t cnt = ord_count(count, n);
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < cnt; i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src ? src[i] : (int32_t)i;
+}
+
 
 // TMA descriptor of a row-major float32 [rows][D] operand: box = one stage
 // (16 dims = 64 bytes) x box_rows rows, 64-byte swizzle (the K-major
@@ -2640,8 +2851,10 @@ int spkm_full_assign(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, s
 int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_s,
                         int naive, void *stream) {
     if (X->n == 0) return 0;
-    const int grid = grid_for(X->n, 256);
-    pdl_launch(k_hamerly_bounds, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, X->row_eps, B->a, B->l, B->u, C->drift, C->sinp, C->s,
+    const int64_t tiles = (X->n + kHbTile - 1) / kHbTile;
+    if (tiles > INT_MAX) return fail_msg("hamerly_bounds: n too large");
+    const int grid = (int)tiles;
+    pdl_launch(k_hamerly_bounds, dim3(grid), dim3(kHbThreads), (size_t)(0), S(stream), X->n, X->row_eps, B->a, B->l, B->u, C->drift, C->sinp, C->s,
                                                   C->hstat,
                                                   use_s, naive, W->surv1, W->ctr, C->ctl);
     CHECK_LAUNCH("hamerly_bounds");
@@ -2685,7 +2898,8 @@ int spkm_hamerly_rescan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B
 int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
                       void *stream) {
     if (X->n == 0) return 0;
-    const int grid = grid_for(X->n, 8);
+    if (C->k > kEbMaxK) return fail_msg("elkan_bounds: k > 1024 not supported by this build");
+    const int grid = grid_for((X->n + 31) / 32, 8);
     pdl_launch(k_elkan_bounds, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l, B->u, B->ku, C->drift,
                                                 C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl);
     CHECK_LAUNCH("elkan_bounds");
@@ -2727,6 +2941,49 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
 int spkm_elkan_bounds_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
                            void *stream) {
     return elkan_scan_launch(X, C, B, W, use_cc, true, stream);
+}
+
+// Order a row list by cluster (see "cluster-ordered worklists" above).
+// list == NULL: the rows [0, n) are ordered into `out`.  Otherwise the
+// first *count (device) entries of `list` are ordered in place through
+// `tmp` (n int32).  bins: 2k int32 scratch.  k <= 12288.
+int spkm_order_by_cluster(int64_t k, const int32_t *a, int32_t *list, const long long *count, int64_t n,
+                          int32_t *tmp, int32_t *out, int32_t *bins, const long long *ctl, void *stream) {
+    if (n <= 0 || k <= 1) {
+        if (!list && n > 0) {   // identity order
+            pdl_launch(k_copy_list, dim3(grid_for(n, 256 * 4)), dim3(256), (size_t)0, S(stream),
+                       (const int32_t *)nullptr, out, (const long long *)nullptr, n, ctl);
+        }
+        return 0;
+    }
+    if (k > 12288) return fail_msg("order_by_cluster: k > 12288");
+    cudaStream_t st = S(stream);
+    const size_t smem = (size_t)k * sizeof(int32_t);
+    cudaError_t e = cudaMemsetAsync(bins, 0, (size_t)k * sizeof(int32_t), st);
+    if (e != cudaSuccess) return fail("order memset", e);
+    const int64_t ntile = (n + kOrdTile - 1) / kOrdTile;
+    const int64_t cap = (int64_t)num_sms() * 4;
+    const int ghist = (int)(ntile < cap ? (ntile < 1 ? 1 : ntile) : cap);
+    const int gscat = (int)(ntile < (int64_t)num_sms() * 8 ? (ntile < 1 ? 1 : ntile) : (int64_t)num_sms() * 8);
+    if (smem > 48 * 1024) {
+        cudaFuncSetAttribute(k_order_hist, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        cudaFuncSetAttribute(k_order_scatter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    pdl_launch(k_order_hist, dim3(ghist), dim3(kOrdThreads), smem, st, k, a, (const int32_t *)list, count, n,
+               bins, ctl);
+    CHECK_LAUNCH("order_hist");
+    pdl_launch(k_order_scan, dim3(1), dim3(1024), (size_t)0, st, k, bins, ctl);
+    CHECK_LAUNCH("order_scan");
+    int32_t *dst = list ? tmp : out;
+    pdl_launch(k_order_scatter, dim3(gscat), dim3(kOrdThreads), smem, st, k, a, (const int32_t *)list, count, n,
+               bins + k, dst, ctl);
+    CHECK_LAUNCH("order_scatter");
+    if (list) {
+        pdl_launch(k_copy_list, dim3(grid_for(n, 256 * 4)), dim3(256), (size_t)0, st, (const int32_t *)tmp, list,
+                   count, n, ctl);
+        CHECK_LAUNCH("order_copy");
+    }
+    return 0;
 }
 
 int spkm_aggregate_sums(const spkm_csr *X, const spkm_centers *C, const spkm_bounds *B, long long *sums_target,

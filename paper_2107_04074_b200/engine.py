@@ -700,6 +700,17 @@ class Engine:
         # vs 140 ms).  SPKM_ELKAN_FUSE=0/1 forces it (A/B measurements).
         env = os.environ.get("SPKM_ELKAN_FUSE")
         self.fuse_elkan = (k <= 256) if env is None else env != "0"
+        # cluster-ordered survivor lists (spkm_order_by_cluster): when the
+        # term-major center table does not fit L2 the gather passes visit the
+        # survivors grouped by a(i), so the CTAs in flight share a few
+        # clusters' term rows.  SPKM_ORDER=0/1 forces it (A/B measurements).
+        env = os.environ.get("SPKM_ORDER")
+        big = self.C.kp * data.dim * 4 > (96 << 20)
+        self.order_rows = (not self.dense and 1 < k <= 12288 and
+                           (big if env is None else env != "0"))
+        if self.order_rows:
+            self.P.ord_tmp = torch.empty(max(self.n_loc, 1), dtype=torch.int32, device=self.device)
+            self.P.ord_bins = torch.empty(2 * k, dtype=torch.int32, device=self.device)
         self.loop = None                 # device-driven fit loop (CUDA graph with a WHILE node)
         self.fit = None                  # the whole fit as one CUDA graph (fit_launch)
         self.loop_kernels = 0            # kernels per loop-body iteration
@@ -810,7 +821,16 @@ class Engine:
             _lib.call("spkm_hamerly_bounds", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag,
                       self.naive, self.sp)
 
+    def order_survivors(self):
+        """Group the bound survivors (surv1) by cluster before the gather passes."""
+        if not self.order_rows:
+            return
+        P = self.P
+        _lib.call("spkm_order_by_cluster", self.k, _ptr(P.a), _ptr(P.surv1), _ptr(P.ctr) + 8 * _lib.CTR_SURV1,
+                  self.n_loc, _ptr(P.ord_tmp), None, _ptr(P.ord_bins), _ptr(self.C.ctl), self.sp)
+
     def scan_pass(self, use_flag: int):
+        self.order_survivors()
         if self.elkan:
             _lib.call("spkm_elkan_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
         elif self.dense:

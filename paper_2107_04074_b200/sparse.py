@@ -155,8 +155,11 @@ class Dataset:
 
     @classmethod
     def from_csr(cls, indptr, indices, data, dim, normalize_rows=True,
-                 check_sorted=True) -> "Dataset":
-        """Scalable constructor from flat CSR arrays (vectorised checks)."""
+                 check_sorted=True, row_norms=None) -> "Dataset":
+        """Scalable constructor from flat CSR arrays (vectorised checks).
+
+        ``row_norms(indptr, data)`` overrides the row-norm helper (default: the
+        library's np.dot-order replay, falling back to np.dot per row)."""
         indptr = np.asarray(indptr, dtype=np.int64)
         indices = np.asarray(indices, dtype=np.int64)
         data = np.asarray(data, dtype=np.float64)
@@ -179,7 +182,7 @@ class Dataset:
             counts = np.bincount(rowid[keep], minlength=indptr.size - 1)
             indptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
             indices, data = indices[keep], data[keep]
-        norms = _row_norms(indptr, data)
+        norms = (row_norms or _row_norms)(indptr, data)
         bad = np.nonzero(norms == 0.0)[0]
         if bad.size:
             raise ZeroNormError(rows=bad.tolist())

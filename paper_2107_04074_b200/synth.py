@@ -111,7 +111,7 @@ def _first_distinct(rows_local, terms, m, nrows):
 
 
 def sparse_corpus(spec: CorpusSpec, seed: int | None = None, chunk_rows: int = 1 << 18,
-                  return_raw: bool = False):
+                  return_raw: bool = False, row_norms=None):
     """Generate the corpus of ``spec``; returns a normalised ``Dataset``.
 
     With ``return_raw`` returns (indptr, indices, weights) before
@@ -181,7 +181,7 @@ def sparse_corpus(spec: CorpusSpec, seed: int | None = None, chunk_rows: int = 1
     np.cumsum(counts, out=indptr[1:])
     if return_raw:
         return indptr, terms.astype(np.int32), w
-    return Dataset.from_csr(indptr, terms, w, d, normalize_rows=True, check_sorted=False)
+    return Dataset.from_csr(indptr, terms, w, d, normalize_rows=True, check_sorted=False, row_norms=row_norms)
 
 
 def dense_corpus(n: int, d: int = 256, centers: int = 1000, sigma_total: float = 0.3,
@@ -212,7 +212,40 @@ def dense_corpus(n: int, d: int = 256, centers: int = 1000, sigma_total: float =
 C5 = dict(n=10_000_000, d=256, centers=1000, sigma_total=0.3)
 
 
-def config_dataset(name: str, seed: int | None = None, n_override: int | None = None) -> Dataset:
+def config_dataset(name: str, seed: int | None = None, n_override: int | None = None,
+                   cache_dir: str | None = None, row_norms=None) -> Dataset:
+    """The Dataset of BASELINE config ``name`` (optionally its first-``n_override``-rows variant:
+    the same generator with n = n_override).  ``row_norms`` overrides the
+    row-norm helper of ``Dataset.from_csr`` (bench.py's reference arm passes
+    the oracle's, so that process never loads the product library).
+
+    ``cache_dir`` (default: $SPKM_DATA_CACHE, unset = no cache) keeps the
+    normalised CSR as .npy files keyed by (config, seed, n) so repeated runs
+    in one session skip the generator (C4 takes minutes on the host).  The
+    cache only stores this function's own output; nothing is read from it
+    that the generator did not write.
+    """
+    import os
+    cache_dir = cache_dir if cache_dir is not None else os.environ.get("SPKM_DATA_CACHE")
+    if cache_dir:
+        from pathlib import Path
+        key = f"{name}_s{seed}_n{n_override}"
+        base = Path(cache_dir) / key
+        files = [base.with_name(key + f".{part}.npy") for part in ("indptr", "indices", "data", "meta")]
+        if all(f.exists() for f in files):
+            ip, ix, dv, meta = (np.load(f, mmap_mode=None) for f in files)
+            ds = Dataset(ip, ix, dv, int(meta[0]))
+            if int(meta[1]) > 0:
+                ds.dense_dim = int(meta[1])
+            return ds
+        ds = config_dataset(name, seed, n_override, cache_dir="", row_norms=row_norms)
+        base.parent.mkdir(parents=True, exist_ok=True)
+        for f, arr in zip(files, (ds.indptr, ds.indices, ds.data,
+                                  np.array([ds.dim, getattr(ds, "dense_dim", 0) or 0], np.int64))):
+            tmp = f.with_name(f.name + ".tmp.npy")
+            np.save(tmp, arr)
+            os.replace(tmp, f)
+        return ds
     if name == "C5":
         n = n_override if n_override is not None else C5["n"]
         X, _ = dense_corpus(n, C5["d"], C5["centers"], C5["sigma_total"],
@@ -223,4 +256,4 @@ def config_dataset(name: str, seed: int | None = None, n_override: int | None = 
         spec = CorpusSpec(spec.name + f"[n={n_override}]", n_override, spec.d, spec.mean_nnz,
                           spec.topics, spec.topic_size, spec.topic_frac)
     base = DATA_SEED_BASE + int(name[1:])
-    return sparse_corpus(spec, base if seed is None else seed)
+    return sparse_corpus(spec, base if seed is None else seed, row_norms=row_norms)

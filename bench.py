@@ -1,26 +1,43 @@
 #!/usr/bin/env python3
 """Benchmark: the accelerated spherical k-means loop on B200 vs the reference's CPU path.
 
-Workload (BASELINE.json configs[1], "C2"): n=20,000 synthetic TF-IDF docs,
-d=100,000, mean ~120 nnz/row (Zipf(1.1) terms, lognormal lengths; seeded,
-see paper_2107_04074_b200/synth.py), k=100, uniform seeded init (seed 2),
-max_iter 50.  One STEP = one complete fit of each of the five variants
-(standard, elkan, simp_elkan, hamerly, simp_hamerly) from the same start.
+Workload (BASELINE.json configs[3], "C4", the largest single-GPU config and
+the one north_star's targets are stated on): n = 4,000,000 synthetic TF-IDF
+docs, d = 1,000,000, mean ~60 nnz/row, Zipf(1.1) terms with 1,000 planted
+topics (seeded, paper_2107_04074_b200/synth.py), k = 1,000, uniform seeded
+init (seed 2), max_iter 50.  One STEP = one complete fit of each of
+BASELINE's C4 variants (hamerly, simp_elkan) from the same start.
 metric = k-means iterations/s over the step (plus effective n*k sims/s and
-the pruned fraction as extra keys).
+the pruned fraction as extra keys).  ``--config/--k/--variants`` select the
+other configs (C2, C3, C5) for profiling runs.
 
-  value      device-timed (CUDA events per step, inputs resident in HBM)
+  value      device-timed (CUDA events per step, inputs resident in HBM;
+             the C4 working set is far larger than L2, and L2 is also
+             flushed before every step)
   e2e        same work through the public API from pinned HOST buffers:
              every step the raw CSR rows are copied H2D into the serving
              buffers (device layout rebuilt on the GPU), seed row ids H2D,
              stats + assignments D2H
-  roofline   the dominant kernel's algorithmic bytes / its event time
-  cpu_baseline  the CPU oracle (C port of the reference loop, OpenMP over
-             points) on a bounded sample, rank 0 at N=1 only
+  roofline   the dominant kernel (by CUDA-event time in an instrumented
+             pass) with its algorithmic bytes / time, next to every other
+             kernel's; the ncu DRAM traffic per launch from profiles/
+  cpu_baseline  the CPU oracle (C port of the reference loop, OpenMP) on a
+             bounded sample, rank 0 at N=1 only; cpu_baseline_reference:
+             the unmodified reference package (baseline/_ref, 1 core)
 
---impl reference runs the oracle port (the reference package is Python and
-cannot travel to the GPU box) on the same workload.  Multi-GPU (torchrun):
-rows sharded by nnz, one allreduce per iteration; strong scaling.
+--impl reference runs the oracle port (C, all host threads) on a bounded
+sample of the same workload: the first n' rows of the corpus, each variant
+capped at a few iterations, its row-proportional phase time scaled by
+n / n' (the oracle's phase clocks; the k x d center phases are not scaled).
+That process never loads the product library (rows are normalised by the
+oracle's np.dot-order row norms).
+
+Multi-GPU (``--gpus N``; re-executed under torch.distributed.run when
+WORLD_SIZE is unset): the corpus is replicated, every rank scans an
+nnz-balanced shard of the rows, and one NCCL allgather of the packed moves
+per iteration keeps the replicated int64 fixed-point sums identical on all
+ranks (paper_2107_04074_b200/distributed.py); weak in memory, strong in
+work (total work fixed).
 """
 
 from __future__ import annotations
@@ -29,7 +46,9 @@ import argparse
 import gc
 import json
 import os
+import subprocess
 import sys
+import tempfile
 import threading
 import time
 from pathlib import Path
@@ -40,34 +59,63 @@ ROOT = Path(__file__).resolve().parent
 sys.path.insert(0, str(ROOT))
 
 VARIANTS = ("standard", "elkan", "simp_elkan", "hamerly", "simp_hamerly")
-def metric_name(args) -> str:
-    """BASELINE.json's iterations/s metric, labelled with the workload (C2, k=100, 5 variants by default)."""
-    return f"k-means iterations/s ({args.config}, k={args.k}, {len(args.variants.split(','))} variants per step)"
+DEFAULTS = {"C1": (20, VARIANTS), "C2": (100, VARIANTS), "C3": (200, ("elkan", "hamerly")),
+            "C4": (1000, ("hamerly", "simp_elkan")), "C5": (1000, ("hamerly",))}
 PEAKS = ROOT / "MEASURED_PEAKS.json"
+REF_STEP_S = 8.0          # target seconds of CPU work per reference-arm step
+
+
+def metric_name(args) -> str:
+    """BASELINE.json's iterations/s metric, labelled with the workload."""
+    return f"k-means iterations/s ({args.config}, k={args.k}, {len(args.variants.split(','))} variants per step)"
 
 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=20)
+    p.add_argument("--steps", type=int, default=3)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    p.add_argument("--config", default="C2")
-    p.add_argument("--k", type=int, default=100)
-    p.add_argument("--n", type=int, default=None, help="row count override (subsample of the config)")
+    p.add_argument("--config", default="C4")
+    p.add_argument("--k", type=int, default=None)
+    p.add_argument("--n", type=int, default=None, help="row count override (the generator at n rows)")
     p.add_argument("--seed", type=int, default=2)
     p.add_argument("--max-iter", type=int, default=50)
-    p.add_argument("--variants", default=",".join(VARIANTS))
+    p.add_argument("--variants", default=None)
     p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true", help="skip the end-to-end leg (A/B runs)")
+    p.add_argument("--no-roofline", action="store_true", help="skip the instrumented pass (A/B runs)")
     p.add_argument("--profile-only", action="store_true", help="one untimed step (for ncu)")
-    return p.parse_args()
+    a = p.parse_args()
+    k0, v0 = DEFAULTS.get(a.config, (100, VARIANTS))
+    a.k = a.k if a.k is not None else k0
+    a.variants = a.variants if a.variants is not None else ",".join(v0)
+    if a.warmup < 1:
+        a.warmup = 1
+    return a
+
+
+def maybe_launch_ranks(args) -> bool:
+    """--gpus N > 1 outside torchrun: re-execute this command under
+    torch.distributed.run with N ranks (one per GPU).  Returns True if it did."""
+    if args.gpus <= 1 or "WORLD_SIZE" in os.environ:
+        return False
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), str(Path(__file__).resolve())] + sys.argv[1:]
+    rc = subprocess.call(cmd)
+    sys.exit(rc)
 
 
 def peaks():
     try:
-        return json.loads(PEAKS.read_text()), "measured"
+        return json.loads(PEAKS.read_text()), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback (B200_PROFILING.md)"
 
 
 class Clocks:
@@ -124,10 +172,16 @@ class Clocks:
 
 
 # ----------------------------------------------------------------- workload
-def load_workload(args):
+def load_workload(args, host_only: bool = False):
+    """The config's Dataset.  host_only (reference arm): rows normalised with
+    the oracle's np.dot-order row norms, so the product library is never loaded."""
     from paper_2107_04074_b200 import synth
+    norms = None
+    if host_only:
+        from oracle import oracle as O
+        norms = O.row_norms
     t = time.time()
-    data = synth.config_dataset(args.config, n_override=args.n)
+    data = synth.config_dataset(args.config, n_override=args.n, row_norms=norms)
     return data, time.time() - t
 
 
@@ -135,79 +189,134 @@ def workload_config(args, data, n_gpus):
     return {"workload": f"{args.config} n={data.n} d={data.dim} nnz={data.nnz} k={args.k}; "
                         f"one step = one fit of each of [{args.variants}] (seed {args.seed}, max_iter {args.max_iter})",
             "global_batch": data.n, "k": args.k, "variants": args.variants.split(","),
-            "parallelism": f"dp{n_gpus} (rows sharded by nnz, centers replicated)",
-            "l2": "flushed (256 MiB write) before every timed step",
+            "parallelism": (f"dp{n_gpus} (corpus replicated, rows sharded by nnz, centers replicated, "
+                            f"one allgather of moves per iteration)" if n_gpus > 1 else "single GPU"),
+            "l2": "flushed (256 MiB write) before every timed step; C4's working set (CSR 2 GB, center table "
+                  "4 GB) is also far larger than L2",
             "precision": "fp32 similarities, fp64 centers, exact int64 fixed-point sums"}
 
 
-# ----------------------------------------------------------------- reference arm
+# ----------------------------------------------------------------- CPU legs
+def _oracle_sample(data, n_sub: int):
+    from oracle import oracle as O
+    if n_sub >= data.n:
+        return O.CSR(data.indptr, data.indices, data.data, data.dim)
+    ip = data.indptr[:n_sub + 1]
+    return O.CSR(ip, data.indices[:ip[-1]], data.data[:ip[-1]], data.dim)
+
+
+def oracle_plan(args, data, budget_s: float):
+    """(n_sub, max_iter) so that one fit of every variant on the first n_sub
+    rows costs about budget_s of CPU time: a 2-iteration probe on at most 20k
+    rows measures the row-proportional and the center (k x d) phase costs."""
+    from oracle import oracle as O
+    variants = args.variants.split(",")
+    k = args.k
+    n_probe = min(data.n, max(20000, 4 * k))
+    r = O.run(_oracle_sample(data, n_probe), min(k, n_probe), variants[0], seed=args.seed, max_iter=2)
+    its = max(r["iterations"], 1)
+    per_row = float(r["t_rows"].sum()) / its / n_probe
+    other = float(r["t_other"].sum()) / its
+    mi = min(args.max_iter, 50)
+    per_it_full = per_row * data.n + other
+    if per_it_full * mi * len(variants) <= budget_s:
+        return data.n, mi
+    mi = max(2, min(mi, 4))
+    room = budget_s / (mi * len(variants)) - other
+    n_sub = int(room / per_row) if room > 0 else n_probe
+    n_sub = max(min(data.n, max(4 * k, 20000)), min(data.n, n_sub))
+    return n_sub, mi
+
+
+def oracle_sample_rate(args, data, n_sub: int, mi: int):
+    """One fit of every variant on the first n_sub rows (cap mi iterations):
+    (iterations, full-size-equivalent seconds, measured seconds)."""
+    from oracle import oracle as O
+    X = _oracle_sample(data, n_sub)
+    its, t_full, t_meas = 0, 0.0, 0.0
+    for v in args.variants.split(","):
+        r = O.run(X, min(args.k, n_sub), v, seed=args.seed, max_iter=mi)
+        its += r["iterations"]
+        tr, to = float(r["t_rows"].sum()), float(r["t_other"].sum())
+        t_meas += tr + to
+        t_full += tr * data.n / n_sub + to
+    return its, t_full, t_meas
+
+
+def sample_label(data, n_sub, mi, args):
+    if n_sub >= data.n and mi >= args.max_iter:
+        return f"full workload: one fit of each of [{args.variants}]"
+    rows = "all rows" if n_sub >= data.n else f"the first {n_sub} of {data.n} rows"
+    return (f"one fit of each of [{args.variants}] on {rows}, each capped at {mi} iterations; "
+            f"row-proportional phase time (sims, bounds, scans, aggregation, moves) scaled by n/n_sub, "
+            f"k x d center phases (thresholds, renormalise, objective) counted as measured")
+
+
 def run_reference(args):
+    """--impl reference: the oracle port on the box's host cores, bounded sample per step."""
     from oracle import oracle as O
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    data, _ = load_workload(args)
-    X = O.CSR(data.indptr, data.indices, data.data, data.dim)
-    variants = args.variants.split(",")
+    data, _ = load_workload(args, host_only=True)
     cores = O.num_threads()
-
-    def step():
-        its = 0
-        for v in variants:
-            r = O.run(X, args.k, v, seed=args.seed, max_iter=args.max_iter)
-            its += r["iterations"]
-        return its
-
+    n_sub, mi = oracle_plan(args, data, REF_STEP_S)
     for _ in range(args.warmup):
-        step()
+        oracle_sample_rate(args, data, n_sub, mi)
+    its_tot, tf_tot, tm_tot = 0, 0.0, 0.0
     t0 = time.perf_counter()
-    its = sum(step() for _ in range(args.steps))
-    dt = time.perf_counter() - t0
-    val = its / dt
-    line = {"metric": metric_name(args), "value": val, "unit": "iterations/s", "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * dt / args.steps, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": dict(workload_config(args, data, args.gpus),
-                           precision="float64 (C port of the reference loop, the oracle)"), "impl": "reference",
+    for _ in range(args.steps):
+        its, tf, tm = oracle_sample_rate(args, data, n_sub, mi)
+        its_tot, tf_tot, tm_tot = its_tot + its, tf_tot + tf, tm_tot + tm
+    wall = time.perf_counter() - t0
+    val = its_tot / tf_tot
+    sample = sample_label(data, n_sub, mi, args) + f"; {args.steps} steps, {wall:.1f} s measured wall"
+    line = {"metric": metric_name(args), "value": val, "unit": "iterations/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tf_tot / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": dict(workload_config(args, data, 1),
+                                                precision="float64 (C port of the reference loop, the oracle)"),
+            "impl": "reference",
             "cpu_baseline": {"value": val, "unit": "iterations/s", "cores": cores, "kind": "port",
-                             "sample": f"full workload ({args.steps} steps x {len(variants)} fits), OpenMP over points"},
+                             "sample": sample},
             "e2e": {"value": val, "unit": "iterations/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
 def cpu_baseline(args, data, budget_s: float = 20.0):
-    """Bounded sample (about 10-30 s of CPU): one fit of each variant with the
-    oracle.  A 2-iteration probe on at most 20k rows estimates the cost; when
-    the full workload does not fit the budget the fits are capped in
-    iterations and, if needed, run on the first n' rows with the rate scaled
-    by n'/n (per-iteration cost is linear in n), and the sample says so."""
+    """The oracle port on a bounded sample (about budget_s of CPU work)."""
     from oracle import oracle as O
-    variants = args.variants.split(",")
+    n_sub, mi = oracle_plan(args, data, budget_s)
+    its, tf, tm = oracle_sample_rate(args, data, n_sub, mi)
+    return {"value": its / tf, "unit": "iterations/s", "cores": O.num_threads(), "kind": "port",
+            "sample": sample_label(data, n_sub, mi, args) + f" ({its} iterations, {tm:.1f} s measured)"}
 
-    def csr(rows):
-        ip = data.indptr[:rows + 1]
-        return O.CSR(ip, data.indices[:ip[-1]], data.data[:ip[-1]], data.dim)
 
-    n_probe = min(data.n, 20000)
-    t0 = time.perf_counter()
-    probe = O.run(csr(n_probe), min(args.k, n_probe), variants[0], seed=args.seed, max_iter=2)["iterations"]
-    per_it_full = (time.perf_counter() - t0) / max(probe, 1) * data.n / n_probe
-    n_sub, mi = data.n, args.max_iter
-    if per_it_full * mi * len(variants) > budget_s:
-        mi = max(2, min(mi, int(budget_s / (per_it_full * len(variants)))))
-        if per_it_full * mi * len(variants) > budget_s:
-            n_sub = max(min(data.n, 2000), int(data.n * budget_s / (per_it_full * mi * len(variants))))
-    X = csr(n_sub) if n_sub < data.n else O.CSR(data.indptr, data.indices, data.data, data.dim)
-    its = 0
-    t0 = time.perf_counter()
-    for v in variants:
-        its += O.run(X, min(args.k, n_sub), v, seed=args.seed, max_iter=mi)["iterations"]
-    dt = time.perf_counter() - t0
-    scale = n_sub / data.n
-    cap = "" if mi == args.max_iter else f", each capped at {mi} iterations"
-    rows = "" if n_sub == data.n else f", on the first {n_sub} of {data.n} rows (rate scaled by {scale:.4g})"
-    return {"value": its / dt * scale, "unit": "iterations/s", "cores": O.num_threads(), "kind": "port",
-            "sample": f"one fit of each variant{cap}{rows} ({its} iterations, {dt:.1f} s), C oracle, OpenMP threads"}
+def cpu_baseline_reference(args, data, n_sub: int = 10000, max_iter: int = 3, timeout: int = 900):
+    """The unmodified reference package (baseline/_ref) on 1 core, first n_sub rows,
+    max_iter iterations per variant (baseline/ref_sample.py, own process)."""
+    if not (ROOT / "baseline" / "_ref" / "spkmeans").exists():
+        return {"unavailable": "baseline/_ref not installed"}
+    n_sub = min(n_sub, data.n)
+    ip = data.indptr[:n_sub + 1]
+    with tempfile.TemporaryDirectory() as td:
+        f = Path(td) / "sample.npz"
+        np.savez(f, indptr=ip, indices=data.indices[:ip[-1]], data=data.data[:ip[-1]], dim=data.dim)
+        cmd = [sys.executable, str(ROOT / "baseline" / "ref_sample.py"), "--npz", str(f), "--k",
+               str(min(args.k, n_sub)), "--variants", args.variants, "--max-iter", str(max_iter), "--seed",
+               str(args.seed), "--n-full", str(data.n)]
+        try:
+            out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
+            r = json.loads(out.stdout.strip().splitlines()[-1])
+        except Exception as e:
+            return {"unavailable": f"reference sample failed: {e!r}"[:300]}
+    if "unavailable" in r:
+        return r
+    return {"value": r["its_per_s_full_est"], "unit": "iterations/s", "cores": 1, "kind": "reference",
+            "sample": (f"unmodified spkmeans {r['spkmeans']} (baseline/_ref), serial: one fit of each of "
+                       f"[{args.variants}] on the first {r['n_sub']} of {data.n} rows, max_iter {max_iter}; "
+                       f"row phases scaled by n/n_sub, k x d center phases as measured"),
+            "value_at_sample": r["its_per_s_sample"], "detail": r}
 
 
 # ----------------------------------------------------------------- our arm
@@ -218,11 +327,13 @@ def main_ours(args):
     import paper_2107_04074_b200 as spk
     from paper_2107_04074_b200 import _lib
     from paper_2107_04074_b200.engine import DeviceCorpus, run
-    from paper_2107_04074_b200.seeding import SeedConfig, make_centroids
+    from paper_2107_04074_b200.seeding import SeedConfig
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and rank == 0:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}; reporting n_gpus={world}", file=sys.stderr)
     torch.cuda.set_device(local)
     dev = torch.device(f"cuda:{local}")
     if world > 1:
@@ -230,8 +341,6 @@ def main_ours(args):
     data, gen_s = load_workload(args)
     variants = args.variants.split(",")
     k = args.k
-    from paper_2107_04074_b200.seeding import uniform_rows
-    seed_rows = uniform_rows(data.n, k, args.seed)
     if world > 1:
         from paper_2107_04074_b200.distributed import Exchange
     rows = (0, data.n)                 # multi-GPU: corpus replicated, scans sharded (distributed.py)
@@ -245,7 +354,7 @@ def main_ours(args):
             exchanges[id(corpus_)] = Exchange.for_corpus(k, corpus_, dev)
         return exchanges[id(corpus_)]
 
-    def fit_all(corpus_, tag=None):
+    def fit_all(corpus_):
         its, sims, nk = 0, 0, 0
         per = {}
         for v in variants:
@@ -257,8 +366,7 @@ def main_ours(args):
             nk += data.n * k * len(r.iterations)
             per[v] = {"iterations": len(r.iterations), "objective": r.objective,
                       "pruned_frac": 1.0 - r.total_sims / (data.n * k * len(r.iterations))}
-            last = r
-        return its, sims, nk, per, last
+        return its, sims, nk, per
 
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
 
@@ -287,7 +395,7 @@ def main_ours(args):
             e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             e0.record()
             with prof:
-                its, sims, nk, per, _ = fit_all(corpus)
+                its, sims, nk, per = fit_all(corpus)
             e1.record()
             barrier()
             times.append(e0.elapsed_time(e1))
@@ -301,49 +409,56 @@ def main_ours(args):
     launches_per_step = prof.launches // max(args.steps, 1)
 
     # ---- e2e through the public API from host buffers ----
-    # every step: the CSR shard's host arrays are staged in pinned memory and
-    # uploaded (raw rows H2D; device-order layout, term renumbering and
-    # float32 conversion rebuilt on the GPU) into the serving buffers of a
-    # persistent DeviceCorpus, then the user's call spk.run(...) per variant
-    # (seed row ids H2D, stats + assignments D2H).  W untimed warm-up steps
-    # fill the engine cache for that corpus and capture its fit graphs.
-    e2e_times, h2d, d2h = [], 0, 0
-    c = DeviceCorpus(data, dev, rows=rows, pinned_host=True)
+    # every step: the CSR's host arrays (page-locked in place) are uploaded
+    # (raw rows H2D; device-order layout, term renumbering and float32
+    # conversion rebuilt on the GPU) into the serving buffers of a persistent
+    # DeviceCorpus, then the user's call spk.run(...) per variant (seed row
+    # ids H2D, stats + assignments D2H).  Untimed warm-up steps fill the
+    # engine cache for that corpus and capture its fit graphs.
+    e2e = None
+    if not args.no_e2e:
+        e2e_times, h2d, d2h = [], 0, 0
+        del corpus
+        from paper_2107_04074_b200 import engine as _E
+        _E.clear_engine_cache()
+        torch.cuda.empty_cache()
+        c = DeviceCorpus(data, dev, rows=rows, pinned_host=True)
 
-    def e2e_step():
-        c.refresh(data)
-        b_in, b_out = c.h2d_bytes, 0
-        for v in variants:
-            comm = exchange_for(c) if world > 1 else None
-            r = spk.run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=c,
-                        comm=comm, n_total=data.n)
-            b_in += int(k * 8)
-            b_out += r.assignments.nbytes + 8 * len(r.iterations) * _lib.ST_COUNT
-        return b_in, b_out
+        def e2e_step():
+            c.refresh(data)
+            b_in, b_out = c.h2d_bytes, 0
+            for v in variants:
+                comm = exchange_for(c) if world > 1 else None
+                r = spk.run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=c,
+                            comm=comm, n_total=data.n)
+                b_in += int(k * 8)
+                b_out += r.assignments.nbytes + 8 * len(r.iterations) * _lib.ST_COUNT
+            return b_in, b_out
 
-    for _ in range(max(args.warmup, 2)):
-        e2e_step()
-    barrier()
-    gc.collect()
-    gc.disable()
-    for _ in range(args.steps):
-        flush.fill_(1)
+        for _ in range(max(args.warmup, 2)):
+            e2e_step()
         barrier()
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        h2d, d2h = e2e_step()
-        e1.record()
-        barrier()
-        e2e_times.append(e0.elapsed_time(e1))
-    gc.enable()
-    del c
-    e2e_ms = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
-    e2e_val = its_tot / (float(e2e_ms.item()) / 1e3)
+        gc.collect()
+        gc.disable()
+        for _ in range(args.steps):
+            flush.fill_(1)
+            barrier()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            h2d, d2h = e2e_step()
+            e1.record()
+            barrier()
+            e2e_times.append(e0.elapsed_time(e1))
+        gc.enable()
+        e2e_ms = torch.tensor([sum(e2e_times)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(e2e_ms, op=dist.ReduceOp.MAX)
+        e2e = {"value": its_tot / (float(e2e_ms.item()) / 1e3), "unit": "iterations/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h)}
+        corpus = c
 
     # ---- instrumented pass: per-entry-point event times -> roofline ----
-    roof = roofline(args, data, corpus, dev, world)
+    roof = None if args.no_roofline else roofline(args, data, corpus, dev, world)
 
     if rank != 0:
         dist.destroy_process_group()
@@ -357,20 +472,35 @@ def main_ours(args):
             "computed_sims_per_s": sims_tot / (total_ms / 1e3),
             "pruned_frac": 1.0 - sims_tot / nk_tot,
             "per_variant": per,
-            "e2e": {"value": e2e_val, "unit": "iterations/s", "h2d_bytes_per_step": int(h2d),
-                    "d2h_bytes_per_step": int(d2h)},
+            "e2e": e2e,
             "gpu_launches": launches_per_step * args.steps,
             "roofline": roof,
-            "clocks": clocks}
+            "clocks": clocks,
+            "data_gen_s": round(gen_s, 1)}
     if world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(args, data)
+        line["cpu_baseline_reference"] = cpu_baseline_reference(args, data)
     print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
 
 
+# entry point -> the kernel doing its work (the dominant kernel is chosen
+# per KERNEL, so entry points sharing one kernel are pooled)
+KERNEL_OF = {"spkm_full_assign": "k_row_pass", "spkm_hamerly_rescan": "k_row_pass",
+             "spkm_hamerly_tighten": "k_hamerly_tighten", "spkm_hamerly_bounds": "k_hamerly_bounds",
+             "spkm_elkan_bounds": "k_elkan_bounds", "spkm_elkan_scan": "k_elkan_scan",
+             "spkm_elkan_bounds_scan": "k_elkan_scan (fused bounds)", "spkm_dense_assign": "k_dense_pass",
+             "spkm_apply_moves": "k_apply_moves", "spkm_aggregate_sums": "k_aggregate",
+             "spkm_order_by_cluster": "k_order_*", "spkm_move_centers": "center pipeline (4 kernels)",
+             "spkm_center_thresholds": "k_gram_mn + k_gram_final + k_row_max"}
+MULTI = {"spkm_move_centers", "spkm_center_thresholds", "spkm_order_by_cluster"}
+
+
 def roofline(args, data, corpus, dev, world):
-    """Time every entry point with CUDA events over one step; bytes from SURVEY.md §8(d)."""
+    """Time every entry point with CUDA events (on the stream its kernels run
+    on) over one eager step; algorithmic bytes per SURVEY.md §8(d) from the
+    fits' own counters; aggregate per kernel."""
     import torch
     from paper_2107_04074_b200 import _lib
     from paper_2107_04074_b200.engine import run
@@ -382,7 +512,8 @@ def roofline(args, data, corpus, dev, world):
     dense = getattr(corpus, "dense_dim", None) is not None
     prof = _lib.CallProfiler(timed=True)
     bytes_by, flops_by, gather_by = {}, {}, {}
-    kp = (k + 7) // 8 * 8
+    kp = int(_lib.lib().spkm_padded_k(k))
+    ku = (k + 3) // 4 * 4
     with prof:
         for v in args.variants.split(","):
             prof.tag = v
@@ -390,90 +521,93 @@ def roofline(args, data, corpus, dev, world):
             r = run(data, k, v, SeedConfig(seed=args.seed), max_iter=args.max_iter, device=dev, corpus=corpus,
                     comm=comm, n_total=data.n)
             its = r.iterations
-            ku = (k + 3) // 4 * 4
-            csr_full = 8 * nnz + 8 * n + 4 * n          # indices+values, indptr, row eps
-            # full passes: iteration 1 of every variant and every Lloyd iteration
+            csr_row = 12          # int64 indptr + fp32 row eps per row read
+            csr_full = 8 * nnz + csr_row * n
             n_full = 1 + (len(its) - 1 if v == "standard" else 0)
-            init_w = 8 * n + (4 * k * n if v in ("elkan", "simp_elkan") else 4 * n if "hamerly" in v else 0)
-            lloyd_w = 4 * n
-            b = csr_full * n_full + init_w + lloyd_w * (n_full - 1)
+            # full passes: CSR + the bound writes (a, l; u: Hamerly 4 B, Elkan 4k B)
+            init_w = 8 * n + (4 * ku * n if v in ("elkan", "simp_elkan") else 4 * n if "hamerly" in v else 0)
+            b = csr_full * n_full + init_w + 4 * n * (n_full - 1)
             bytes_by[("spkm_full_assign", v)] = b
-            # center-row bytes the gather passes read through L1/L2 (4 kp per nnz)
             gather_by[("spkm_full_assign", v)] = 4 * kp * nnz * n_full
             if v in ("hamerly", "simp_hamerly"):
-                bytes_by[("spkm_hamerly_bounds", v)] = 24 * n * (len(its) - 1)
-                bytes_by[("spkm_hamerly_tighten", v)] = sum(8 * s.nnz_tighten + 24 * s.survivors for s in its[1:])
-                bytes_by[("spkm_hamerly_rescan", v)] = sum(8 * s.nnz_rescan + 24 * s.survivors2 for s in its[1:])
-                gather_by[("spkm_hamerly_rescan", v)] = sum(4 * kp * s.nnz_rescan for s in its[1:])
+                # bound pass: a, l, u, eps read; l, u written; survivor ids written
+                bytes_by[("spkm_hamerly_bounds", v)] = sum(24 * n + 4 * s.survivors for s in its[1:])
+                # tighten + rescan: both pooled under k_row_pass/k_hamerly_tighten by time; the bytes of
+                # the tighten test (CSR of the bound survivors) are credited to whichever ran it
+                tb = sum(8 * s.nnz_tighten + (csr_row + 12) * s.survivors for s in its[1:])
+                rb = sum(8 * s.nnz_rescan + (csr_row + 12) * s.survivors2 for s in its[1:])
+                bytes_by[("spkm_hamerly_scan", v)] = tb + rb
+                gather_by[("spkm_hamerly_scan", v)] = sum(4 * kp * s.nnz_rescan + 4 * s.nnz_tighten for s in its[1:])
             if v in ("elkan", "simp_elkan"):
-                b_bounds = (8 * ku + 16) * n * (len(its) - 1)
-                b_scan = sum(8 * s.nnz_elkan + (8 * ku + 16) * s.survivors for s in its[1:])
+                # bound pass: u read (4 ku) + a, l, eps (12) + l write (4) per row, and u written only in
+                # the 16-byte groups holding a center that moved (touched clusters of the previous iteration)
+                moved_prev = [its[q - 1].touched for q in range(1, len(its))]
+                b_bounds = sum((4 * ku + 16) * n + 4 * min(ku, 4 * m) * n for m in moved_prev)
+                b_scan = sum(8 * s.nnz_elkan + (csr_row + 4 * ku + 16) * s.survivors for s in its[1:])
                 bytes_by[("spkm_elkan_bounds", v)] = b_bounds
                 bytes_by[("spkm_elkan_scan", v)] = b_scan
-                # the fused entry point (bound update + scan in one pass) moves both
-                bytes_by[("spkm_elkan_bounds_scan", v)] = b_bounds + b_scan
-            # center update (reported beside B_iter): 16 B of
-            # int64 atomics per moved nnz; 20 B per (touched cluster, term)
-            # to renormalise and take the drift
+                # fused: the scan's u reads of a survivor are the bound pass's (counted once)
+                bytes_by[("spkm_elkan_bounds_scan", v)] = b_bounds + sum(
+                    8 * s.nnz_elkan + csr_row * s.survivors for s in its[1:])
             bytes_by[("spkm_apply_moves", v)] = sum(16 * s.nnz_moved for s in its[1:])
             bytes_by[("spkm_move_centers", v)] = sum(20 * s.touched * data.dim for s in its)
             if dense:
-                # tensor-core pass: 3 tf32 MMAs per (row, padded center, dim)
-                kpad = (k + 255) // 256 * 256
                 D = corpus.dense_dim
                 rows = n * n_full + (sum(s.survivors for s in its[1:]) if "hamerly" in v else 0)
-                flops_by[("spkm_dense_assign", v)] = 6 * rows * kpad * D
+                flops_by[("spkm_dense_assign", v)] = 2 * rows * k * D     # the algorithm's flops (k, not kpad)
     torch.cuda.synchronize()
     times = prof.times_ms()
     calls = {}
     for (name, tag), ms in times.items():
-        calls.setdefault(name, [0.0, 0])
-        calls[name][0] += ms
+        key = "spkm_hamerly_scan" if name in ("spkm_hamerly_tighten", "spkm_hamerly_rescan") else name
+        calls.setdefault(key, [0.0, 0])
+        calls[key][0] += ms
     for name, e0, e1, tag in prof.records:
-        calls[name][1] += 1
+        key = "spkm_hamerly_scan" if name in ("spkm_hamerly_tighten", "spkm_hamerly_rescan") else name
+        calls[key][1] += 1
     total = sum(v[0] for v in calls.values())
     share = {nm: round(v[0] / total, 4) for nm, v in sorted(calls.items(), key=lambda x: -x[1][0])}
-    # dominant KERNEL: the largest single-kernel entry point with a byte (HBM)
-    # or flop (tensor) model; multi-kernel entry points (center update:
-    # 4-5 short kernels whose event span includes host launch gaps in this
-    # eager profiling pass) are reported beside it
-    multi = {"spkm_move_centers", "spkm_center_thresholds", "spkm_aggregate_sums"}
-    cand = [nm for nm in share if nm not in multi and any(key[0] == nm for key in list(bytes_by) + list(flops_by))]
-    dom = cand[0] if cand else None
-    out = {"bound": "hbm", "peak": pk.get("hbm_gbs"), "unit": "GB/s", "peak_source": src,
+
+    def entry_bytes(nm):
+        return sum(val for key, val in bytes_by.items() if key[0] == nm)
+
+    per = {}
+    for nm, (ms, nl) in calls.items():
+        b = entry_bytes(nm)
+        if b and ms:
+            per[nm] = {"kernel": KERNEL_OF.get(nm, "k_row_pass (rescan) + k_hamerly_tighten"), "launches": nl,
+                       "ms": round(ms, 4), "algorithmic_bytes": b,
+                       "achieved_gbs": round(b / (ms / 1e3) / 1e9, 1),
+                       "frac": round(b / (ms / 1e3) / 1e9 / pk.get("hbm_gbs"), 4)}
+    out = {"bound": "hbm", "peak": pk.get("hbm_gbs"), "unit": "GB/s", "peak_source": src + ", copy bandwidth",
            "time_share": share, "traffic": None}
+    cand = [nm for nm in share if nm not in MULTI and (entry_bytes(nm) or any(key[0] == nm for key in flops_by))]
+    dom = cand[0] if cand else None
     if dom and any(key[0] == dom for key in flops_by):
         ms = calls[dom][0]
         f = sum(val for key, val in flops_by.items() if key[0] == dom)
         peak_tf32, how = tf32_peak(dev)
         ach = f / (ms / 1e3) / 1e12
-        out.update({"bound": "tensor", "unit": "TFLOP/s", "kernel": dom, "achieved": ach, "peak": peak_tf32,
-                    "peak_source": how, "frac": ach / peak_tf32, "launches": calls[dom][1],
+        out.update({"bound": "tensor", "unit": "TFLOP/s", "kernel": KERNEL_OF[dom], "entry": dom, "achieved": ach,
+                    "peak": peak_tf32, "peak_source": how, "frac": ach / peak_tf32, "launches": calls[dom][1],
                     "algorithmic_flops": f, "kernel_ms": ms,
-                    "note": "3xTF32 flops (3 MMAs per product) over the kernel's CUDA-event time"})
+                    "note": "2 n k D flops per pass over the kernel's CUDA-event time (3xTF32 issues 3 MMAs each)"})
     elif dom:
         ms = calls[dom][0]
-        b = sum(val for key, val in bytes_by.items() if key[0] == dom)
+        b = entry_bytes(dom)
         ach = b / (ms / 1e3) / 1e9
-        out.update({"kernel": dom, "achieved": ach, "frac": ach / pk.get("hbm_gbs"), "launches": calls[dom][1],
-                    "algorithmic_bytes": b, "kernel_ms": ms})
-    tr = ncu_traffic(dom)
+        out.update({"kernel": per[dom]["kernel"], "entry": dom, "achieved": ach, "frac": ach / pk.get("hbm_gbs"),
+                    "launches": calls[dom][1], "algorithmic_bytes": b, "kernel_ms": ms})
+    tr = ncu_traffic(args.config, dom)
     if tr is not None:
-        out["traffic"] = tr["dram_bytes_per_launch"]
-        out["traffic_source"] = tr["source"]
-        if "ncu_throughput_pct" in tr:
-            out["ncu_throughput_pct"] = tr["ncu_throughput_pct"]
-    # every entry point with a byte model: achieved GB/s of its event span
-    per = {}
-    for nm, (ms, nl) in calls.items():
-        b = sum(val for key, val in bytes_by.items() if key[0] == nm)
-        if b and ms:
-            per[nm] = {"launches": nl, "ms": round(ms, 4), "algorithmic_bytes": b,
-                       "achieved_gbs": round(b / (ms / 1e3) / 1e9, 1),
-                       "frac": round(b / (ms / 1e3) / 1e9 / pk.get("hbm_gbs"), 4)}
-    out["per_entry"] = per
-    # the gather passes are bound by L1/L2 (ncu_throughput_pct), not HBM: the
-    # center-row bytes they pull per second, beside the HBM view above
+        out["traffic"] = tr.get("dram_bytes_per_launch")
+        out["traffic_source"] = tr.get("source")
+        for key in ("algorithmic_bytes_per_launch", "ncu_throughput_pct", "note"):
+            if key in tr:
+                out["traffic_" + key] = tr[key]
+    out["per_kernel"] = per
+    # the gather passes are bound by the center-row gathers (L2/DRAM), not by
+    # their CSR bytes: the center-row bytes they pull per second
     gv = {}
     for nm, (ms, nl) in calls.items():
         g = sum(val for key, val in gather_by.items() if key[0] == nm)
@@ -482,7 +616,7 @@ def roofline(args, data, corpus, dev, world):
     if gv:
         out["center_gather"] = gv
     if "spkm_move_centers" in calls:
-        b = sum(val for key, val in bytes_by.items() if key[0] == "spkm_move_centers")
+        b = entry_bytes("spkm_move_centers")
         ms = calls["spkm_move_centers"][0]
         out["center_update"] = {"entry": "spkm_move_centers", "algorithmic_bytes": b, "ms": ms,
                                 "achieved_gbs": b / (ms / 1e3) / 1e9 if ms else None,
@@ -512,13 +646,14 @@ def tf32_peak(dev):
         return 1100.0, f"nominal dense TF32 ({e!r})"
 
 
-def ncu_traffic(kernel_entry):
-    """dram bytes per launch of the entry point's main kernel from a committed ncu --set full capture."""
+def ncu_traffic(config, entry):
+    """DRAM bytes per launch of the entry's kernel from a committed ncu --set full capture of this config."""
     p = ROOT / "profiles" / "ncu_traffic.json"
-    if kernel_entry is None or not p.exists():
+    if entry is None or not p.exists():
         return None
     try:
-        return json.loads(p.read_text()).get(kernel_entry)
+        t = json.loads(p.read_text())
+        return t.get(config, {}).get(entry)
     except Exception:
         return None
 
@@ -527,8 +662,9 @@ def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        main_ours(args)
+        return
+    maybe_launch_ranks(args)
+    main_ours(args)
 
 
 if __name__ == "__main__":

@@ -16,7 +16,8 @@ from .errors import DeviceError
 
 PKG = Path(__file__).resolve().parent
 ROOT = PKG.parent
-LIB_PATH = PKG / "libspkm.so"
+# SPKM_LIB: an alternative build of the same library (A/B measurements only)
+LIB_PATH = Path(os.environ["SPKM_LIB"]) if os.environ.get("SPKM_LIB") else PKG / "libspkm.so"
 SRC = PKG / "csrc" / "spkm.cu"
 SRC_HOST = PKG / "csrc" / "ingest.cpp"
 HEADER = ROOT / "include" / "spkm.h"

@@ -257,6 +257,36 @@ __device__ __forceinline__ void load_iv(const int2 *p, int (&iv)[UB], float (&vv
     }
 }
 
+// L2 eviction priority of the center-row gathers.  Term ids are renumbered
+// by document frequency, so the Zipf head is the block of term rows
+// [0, hot) of ct32.  Those rows are gathered with evict_last and every other
+// row with evict_first: the flood of once-per-pass topic-term rows (C4: a
+// 4 GB table, ~70% of the gathers) then streams through L2 without evicting
+// the head, which serves most of the remaining gathers from L2.  A hint
+// only: results do not depend on it.  hot is chosen on the host (the head
+// rows that fit half of L2; SPKM_HOT_MB).
+__device__ __forceinline__ uint64_t l2_policy_last() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t l2_policy_first() {
+    uint64_t p;
+    asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ float4 ldg_hint(const float4 *p, uint64_t pol) {
+    float4 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.f32 {%0,%1,%2,%3}, [%4], %5;"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float ldg_hint(const float *p, uint64_t pol) {
+    float v;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
 enum { MODE_RESCAN = 4, MODE_PREDICT = 5 };
 
 struct RowPassArgs {
@@ -286,6 +316,7 @@ struct RowPassArgs {
     const long long *rowcount_fused;
     const float *s_arr;
     int use_s;
+    int64_t hot;                 // term rows [0, hot) are gathered with evict_last, the rest evict_first
 };
 
 // Thread = (row, CH centers in float4 groups tpr apart).  tpr threads cover
@@ -297,7 +328,13 @@ template <int CH, int NT>
 __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPassArgs A) {
     PDL_ENTRY();
     // nnz per gather batch: keep ~8 float4 loads in flight per lane
-    constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 2 : 1;
+#ifndef SPKM_UB_WIDE
+#define SPKM_UB_WIDE 4
+#endif
+    // CH >= 16 (k > 256, one row per warp, one CTA per SM by registers): the
+    // gathers are latency-bound, so SPKM_UB_WIDE x 8 float4 loads in flight
+    // (C4: 1, 2, 3, 4 -> 8.50, 9.40, 9.70, 9.84 it/s; profiles/r02_ab_notes.txt)
+    constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 2 * SPKM_UB_WIDE : SPKM_UB_WIDE;
     if (A.ctl[1]) return;   // converged: later enqueued iterations are no-ops
     extern __shared__ __align__(16) int2 s_iv[];   // per row group: kIvStride staged (id, value) pairs
     const int wpb = blockDim.x >> 5;
@@ -329,6 +366,7 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
 #pragma unroll
         for (int c = 0; c < CH; ++c) acc[c] = 0.f;
         const float *ctj = A.ct + j0;
+        const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
         // Rows are staged 32 nnz at a time in shared memory (coalesced loads by
         // the row's lanes); the term-major center rows are then gathered UB
         // nnz at a time so UB * CH/4 independent float4 loads are in flight.
@@ -346,8 +384,9 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
 #pragma unroll
                 for (int b = 0; b < UB; ++b) {
                     const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)iv[b] * A.kp);
+                    const uint64_t pol = iv[b] < A.hot ? pol_hot : pol_cold;
 #pragma unroll
-                    for (int r = 0; r < CH / 4; ++r) cv[b][r] = __ldg(p + r * A.tpr);
+                    for (int r = 0; r < CH / 4; ++r) cv[b][r] = ldg_hint(p + r * A.tpr, pol);
                 }
 #pragma unroll
                 for (int b = 0; b < UB; ++b)
@@ -363,9 +402,10 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
                 const int2 t = my_iv[u];
                 const float v0 = __int_as_float(t.y);
                 const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)t.x * A.kp);
+                const uint64_t pol = t.x < A.hot ? pol_hot : pol_cold;
 #pragma unroll
                 for (int r = 0; r < CH / 4; ++r) {
-                    const float4 cc4 = p[r * A.tpr];
+                    const float4 cc4 = ldg_hint(p + r * A.tpr, pol);
                     acc[4 * r + 0] = __fmaf_rn(v0, cc4.x, acc[4 * r + 0]);
                     acc[4 * r + 1] = __fmaf_rn(v0, cc4.y, acc[4 * r + 1]);
                     acc[4 * r + 2] = __fmaf_rn(v0, cc4.z, acc[4 * r + 2]);
@@ -581,9 +621,10 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
                                                          const float *__restrict__ s_arr, int use_s,
                                                          const int32_t *__restrict__ surv1, int32_t *surv2,
                                                          long long *ctr, const double *__restrict__ fuse,
-                                                         const long long *__restrict__ ctl) {
+                                                         const long long *__restrict__ ctl, int64_t hot) {
     PDL_ENTRY();
     if (ctl[1] || *fuse != 0.0) return;   // converged, or the rescan does the tighten this iteration
+    const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
     __shared__ __align__(16) float2 s_vc[8][4][kIvStride];   // (value, center value), padded as s_iv
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
@@ -617,7 +658,8 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
             const int cntc = max(0, min(32, len - c0));
             float cx[4];
 #pragma unroll
-            for (int r = 0; r < 4; ++r) cx[r] = (q + 8 * r < cntc) ? __ldg(cta + (int64_t)ix[r] * kp) : 0.f;
+            for (int r = 0; r < 4; ++r)
+                cx[r] = (q + 8 * r < cntc) ? ldg_hint(cta + (int64_t)ix[r] * kp, ix[r] < hot ? pol_hot : pol_cold) : 0.f;
 #pragma unroll
             for (int r = 0; r < 4; ++r) svc[q + 8 * r] = make_float2(vx[r], cx[r]);
 #pragma unroll
@@ -836,12 +878,14 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                                                     const double *__restrict__ drift,
                                                     const double *__restrict__ sinp,
                                                     const float *__restrict__ s_arr,
-                                                    const long long *__restrict__ ctl) {
+                                                    const long long *__restrict__ ctl, int64_t hot) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
     constexpr int UB = 32 / EB;   // nnz per gather batch: 8 float4 loads in flight per lane
     constexpr int ES = EB + 1;    // padded per-block stride of the similarity buffer
     __shared__ __align__(16) int2 s_iv[8][8][kIvStride];
+    __shared__ int s_act[8][128];          // per warp: the groups' active block lists (ppw * nb <= 128)
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
     extern __shared__ float s_sim_dyn[];   // [8 warps][sim_stride]
@@ -913,34 +957,100 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
         }
         const int64_t s = valid ? indptr[i] : 0, e = valid ? indptr[i + 1] : 0;
         const int len = (int)(e - s);
-        const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
         const bool cc_ok = use_cc && lb >= 0.0;
         const float thu_s = thr_u_of(lb, eps), thc_s = thr_c_of(lb, eps);
-        for (int r = 0; r < nrounds; ++r) {
-            const int blk = r * 32 + q;
-            const int j0 = blk * EB;
-            bool act = false;
-            if (valid && blk < nb) {
+        constexpr int NONE = 0x7fffffff;
+        // (A) the first j failing the pre-tests (kernels.py:35-47): where the
+        // reference tightens l to the exact s(i, a)
+        int first_fail = NONE;
+        if (valid) {
+            for (int r = 0; r < nrounds && first_fail == NONE; ++r) {
+                const int blk = r * 32 + q;
+                if (blk >= nb) break;
                 for (int c2 = 0; c2 < EB; ++c2) {
-                    const int j = j0 + c2;
+                    const int j = blk * EB + c2;
                     if (j >= k) break;
-                    if (j == ai) {
-                        act = true;
-                        continue;
-                    }
-                    // u-test only: a center the replay may need fails it (the
-                    // cc test depends on the running best, so it cannot
-                    // prune the fetch)
-                    act |= !(ui[j] <= thu_s);
+                    if (j == ai) continue;
+                    if (cc_ok && cc[(int64_t)ai * k + j] <= thc_s) continue;
+                    if (ui[j] <= thu_s) continue;
+                    first_fail = j;
+                    break;
                 }
             }
-            if (!__any_sync(FULL, act)) continue;
+        }
+        for (int o = o0; o; o >>= 1) {   // group min (lanes of other groups hold their own values)
+            const int other = __shfl_down_sync(FULL, first_fail, o);
+            if (q < o && q + o < bpr) first_fail = min(first_fail, other);
+        }
+        first_fail = __shfl_sync(FULL, first_fail, lane - q);
+        const bool tight = valid && first_fail != NONE;
+        // (B) s~(i, a(i)) -- the canonical chain for the single center a(i),
+        // as k_hamerly_tighten: the group's lanes stage (value, center value)
+        // pairs of each 32-nnz chunk, the leader runs the chain in CSR order
+        float lcur = 0.f;
+        const int tlen = tight ? len : 0;
+        const int maxt = (int)__reduce_max_sync(FULL, (unsigned)tlen);
+        if (maxt > 0) {
+            float acc = 0.f;
+            const float *cta = ct + ai;
+            for (int c0 = 0; c0 < maxt; c0 += 32) {
+                const int cntc = max(0, min(32, tlen - c0));
+                for (int q2 = q; q2 < cntc; q2 += bpr) {
+                    const int t = __ldg(indices + s + c0 + q2);
+                    const float cv = ldg_hint(cta + (int64_t)t * kp, t < hot ? pol_hot : pol_cold);
+                    my_iv[q2] = make_int2(__float_as_int(__ldg(values + s + c0 + q2)), __float_as_int(cv));
+                }
+                __syncwarp();
+                if (q == 0)
+                    for (int t = 0; t < cntc; ++t)
+                        acc = __fmaf_rn(__int_as_float(my_iv[t].x), __int_as_float(my_iv[t].y), acc);
+                __syncwarp();
+            }
+            lcur = __shfl_sync(FULL, acc, lane - q);
+        }
+        // (C) blocks to fetch: centers j >= first_fail, j != a(i) failing the
+        // u test at the tightened bound s~(i, a).  The replay below only ever
+        // computes such centers: its u test u + eps <= lcur is implied by the
+        // same test at s~(i, a) because the running best only grows (the cc
+        // test is not used here: it refers to the current best center, which
+        // changes).  Active blocks are compacted so each fetch round gives
+        // every lane of the group a block that is needed.
+        int *my_act = s_act[wib] + (lane_on ? g : 0) * nb;
+        int nact = 0;
+        {
+            const double lc = (double)lcur;
+            for (int r = 0; r < nrounds; ++r) {
+                const int blk = r * 32 + q;
+                bool act = false;
+                if (tight && blk < nb) {
+                    for (int c2 = 0; c2 < EB; ++c2) {
+                        const int j = blk * EB + c2;
+                        if (j >= k) break;
+                        if (j < first_fail || j == ai) continue;
+                        act |= !((double)ui[j] + eps <= lc);
+                    }
+                }
+                const unsigned m = __ballot_sync(FULL, act);
+                const unsigned gm = (m >> (lane - q)) & (bpr >= 32 ? 0xffffffffu : ((1u << bpr) - 1u));
+                if (act) my_act[nact + __popc(gm & ((1u << q) - 1u))] = blk;
+                nact += __popc(gm);
+            }
+        }
+        __syncwarp();
+        const int act_rounds = (int)__reduce_max_sync(FULL, (unsigned)((nact + bpr - 1) / bpr));
+        const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)(nact ? len : 0));
+        for (int r = 0; r < act_rounds; ++r) {
+            const int slot_b = r * bpr + q;
+            const bool act = lane_on && slot_b < nact;
+            const int blk = act ? my_act[slot_b] : 0;
+            const int j0 = blk * EB;
             float acc[EB];
 #pragma unroll
             for (int c2 = 0; c2 < EB; ++c2) acc[c2] = 0.f;
             const float4 *base4 = reinterpret_cast<const float4 *>(ct + j0);
+            const int glen = nact > r * bpr ? len : 0;   // rows of the group with blocks left this round
             for (int c0 = 0; c0 < maxlen; c0 += 32) {
-                const int cntc = max(0, min(32, len - c0));
+                const int cntc = max(0, min(32, glen - c0));
                 for (int q2 = q; q2 < cntc; q2 += bpr)
                     my_iv[q2] = make_int2(__ldg(indices + s + c0 + q2), __float_as_int(__ldg(values + s + c0 + q2)));
                 __syncwarp();
@@ -954,8 +1064,9 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
 #pragma unroll
                         for (int b = 0; b < UB; ++b) {
                             const float4 *p = base4 + ((int64_t)iv[b] * kp >> 2);
-                            x[b][0] = __ldg(p);
-                            x[b][1] = __ldg(p + 1);
+                            const uint64_t pol = iv[b] < hot ? pol_hot : pol_cold;
+                            x[b][0] = ldg_hint(p, pol);
+                            x[b][1] = ldg_hint(p + 1, pol);
                         }
 #pragma unroll
                         for (int b = 0; b < UB; ++b) {
@@ -973,7 +1084,8 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                         const int2 t = my_iv[uu];
                         const float v0 = __int_as_float(t.y);
                         const float4 *p = base4 + ((int64_t)t.x * kp >> 2);
-                        const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
+                        const uint64_t pol = t.x < hot ? pol_hot : pol_cold;
+                        const float4 x0 = ldg_hint(p, pol), x1 = ldg_hint(p + 1, pol);
                         acc[0] = __fmaf_rn(v0, x0.x, acc[0]);
                         acc[1] = __fmaf_rn(v0, x0.y, acc[1]);
                         acc[2] = __fmaf_rn(v0, x0.z, acc[2]);
@@ -991,7 +1103,8 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                         int iv[UB];
                         load_iv<UB>(my_iv + uu, iv, vv);
 #pragma unroll
-                        for (int b = 0; b < UB; ++b) x[b] = __ldg(base4 + ((int64_t)iv[b] * kp >> 2));
+                        for (int b = 0; b < UB; ++b)
+                            x[b] = ldg_hint(base4 + ((int64_t)iv[b] * kp >> 2), iv[b] < hot ? pol_hot : pol_cold);
 #pragma unroll
                         for (int b = 0; b < UB; ++b) {
                             acc[0] = __fmaf_rn(vv[b], x[b].x, acc[0]);
@@ -1003,7 +1116,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                     for (; uu < cntc; ++uu) {
                         const int2 t = my_iv[uu];
                         const float v0 = __int_as_float(t.y);
-                        const float4 x0 = __ldg(base4 + ((int64_t)t.x * kp >> 2));
+                        const float4 x0 = ldg_hint(base4 + ((int64_t)t.x * kp >> 2), t.x < hot ? pol_hot : pol_cold);
                         acc[0] = __fmaf_rn(v0, x0.x, acc[0]);
                         acc[1] = __fmaf_rn(v0, x0.y, acc[1]);
                         acc[2] = __fmaf_rn(v0, x0.z, acc[2]);
@@ -1018,47 +1131,18 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
             }
         }
         __syncwarp();
-        // replay of kernels.py:35-65, parallel over the group's lanes.  Lane q
-        // owns the centers of blocks q, q+32, ... (ascending j within the
-        // lane).  (A) tighten at the first j failing the pre-tests; (B) with
-        // the running best (cur, lcur) every lane finds its candidates and
-        // its first "event" (candidate beating lcur); the earliest event of
-        // the group updates (cur, lcur) and the scan resumes after it.
-        // Between events the state is constant, so the candidate set and the
-        // reassignments equal the reference's sequential loop.
+        // (D) replay of kernels.py:35-65, parallel over the group's lanes.
+        // Lane q owns the centers of blocks q, q+32, ... (ascending j within
+        // the lane).  With the running best (cur, lcur) every lane finds its
+        // candidates and its first "event" (candidate beating lcur); the
+        // earliest event of the group updates (cur, lcur) and the scan resumes
+        // after it.  Between events the state is constant, so the candidate set
+        // and the reassignments equal the reference's sequential loop.
         int cur = ai;
-        float lcur = 0.f;
         long long sims = 0;
-        constexpr int NONE = 0x7fffffff;
-        int first_fail = NONE;
-        if (valid) {
-            for (int r = 0; r < nrounds && first_fail == NONE; ++r) {
-                const int blk = r * 32 + q;
-                if (blk >= nb) break;
-                for (int c2 = 0; c2 < EB; ++c2) {
-                    const int j = blk * EB + c2;
-                    if (j >= k) break;
-                    if (j == ai) continue;
-                    if (cc_ok && cc[(int64_t)ai * k + j] <= thc_s) continue;
-                    if (ui[j] <= thu_s) continue;
-                    first_fail = j;
-                    break;
-                }
-            }
-        }
-        // group min (lanes of other groups hold their own values)
-        for (int o = o0; o; o >>= 1) {
-            const int other = __shfl_down_sync(FULL, first_fail, o);
-            if (q < o && q + o < bpr) first_fail = min(first_fail, other);
-        }
-        first_fail = __shfl_sync(FULL, first_fail, lane - q);
-        const bool tight = valid && first_fail != NONE;
-        if (tight) {
-            lcur = my_sim[(ai >> (EB == 4 ? 2 : 3)) * ES + (ai & (EB - 1))];
-            if (q == 0) {
-                ui[ai] = store_upper((double)lcur + eps);
-                sims = 1;
-            }
+        if (tight && q == 0) {
+            ui[ai] = store_upper((double)lcur + eps);
+            sims = 1;
         }
         int start = first_fail;
         bool more = __any_sync(FULL, tight);
@@ -2453,6 +2537,18 @@ int launch_row_pass(RowPassArgs &A, int64_t k, cudaStream_t st, int64_t max_rows
     return launch_rp<32, 256>(A, grid, smem, st);
 }
 
+// Term rows of the Zipf head kept in L2 by the gathers' eviction hints:
+// as many as fit SPKM_HOT_MB (default 64 MB, about half of L2).
+int64_t hot_terms(const spkm_centers *C) {
+    static int64_t mb = -1;
+    if (mb < 0) {
+        const char *e = getenv("SPKM_HOT_MB");
+        mb = e ? atoll(e) : 64;
+    }
+    const int64_t rows = (mb << 20) / (C->kp * 4 > 0 ? C->kp * 4 : 1);
+    return rows < C->d ? rows : C->d;
+}
+
 RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     RowPassArgs A{};
     A.ctl = C->ctl;
@@ -2463,6 +2559,7 @@ RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     A.n = X->n;
     A.ct = C->ct32;
     A.kp = C->kp;
+    A.hot = hot_terms(C);
     return A;
 }
 
@@ -2867,7 +2964,7 @@ int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *
     const int grid = grid_for((X->n + 3) / 4, 8);
     pdl_launch(k_hamerly_tighten, dim3(grid), dim3(256), (size_t)(0), S(stream), X->indptr, X->indices, X->values, X->row_eps, C->ct32, C->kp,
                                                    B->a, B->l, B->u, C->s, use_s, W->surv1, W->surv2, W->ctr,
-                                                   (const double *)(C->hstat + kFuseFlag), C->ctl);
+                                                   (const double *)(C->hstat + kFuseFlag), C->ctl, hot_terms(C));
     CHECK_LAUNCH("hamerly_tighten");
     return 0;
 }
@@ -2909,17 +3006,19 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
 static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
                              bool fuse, void *stream) {
     if (X->n == 0) return 0;
+    if (C->k > 1024) return fail_msg("elkan_scan: k > 1024 not supported by this build");
     const int grid = grid_for(X->n, 8);
     const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float);
+    cudaError_t attr = cudaSuccess;
     auto launch = [&](auto kern) {
-        static size_t dyn_set = 0;   // static smem (16 KB staging) + dyn must fit the opt-in limit
-        if (dyn > dyn_set) {
-            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
-            dyn_set = dyn;
-        }
+        // static smem (staging + active lists) + dyn must fit the opt-in
+        // limit; set per launch (cheap), so it holds for every instantiation
+        // and device
+        attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (attr != cudaSuccess) return;
         pdl_launch(kern, dim3(grid), dim3(256), dyn, S(stream), X->indptr, X->indices, X->values, X->row_eps, C->ct32,
                    C->kp, (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1, W->mv_i, W->mv_old, W->ctr,
-                   X->n, C->drift, C->sinp, C->s, C->ctl);
+                   X->n, C->drift, C->sinp, C->s, C->ctl, hot_terms(C));
     };
     const bool eb4 = elkan_block(C->k) == 4;
     if (fuse) {
@@ -2929,6 +3028,7 @@ static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_boun
         if (eb4) launch(k_elkan_scan<4, false>);
         else launch(k_elkan_scan<8, false>);
     }
+    if (attr != cudaSuccess) return fail("elkan_scan smem attribute", attr);
     CHECK_LAUNCH("elkan_scan");
     return 0;
 }
@@ -3097,12 +3197,13 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
     CUtensorMap tm;
     int rc = encode_gram_map(&tm, C->ct32, C->kp, C->d);
     if (rc) return rc;
-    static bool attr_mn = false;
-    if (!attr_mn) {
-        cudaFuncSetAttribute(k_gram_mn<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GmCfg<true>::SMEM);
-        cudaFuncSetAttribute(k_gram_mn<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GmCfg<false>::SMEM);
-        attr_mn = true;
-    }
+    // set on every call (cheap; the opt-in is per device, a process-wide
+    // "done" flag would miss a second device)
+    cudaError_t ae = tk == 1 ? cudaFuncSetAttribute(k_gram_mn<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)GmCfg<true>::SMEM)
+                             : cudaFuncSetAttribute(k_gram_mn<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                    (int)GmCfg<false>::SMEM);
+    if (ae != cudaSuccess) return fail("gram_mn smem attribute", ae);
     if (tk == 1)
         pdl_launch(k_gram_mn<true>, dim3(1, (unsigned)ds), dim3(GM_THREADS), GmCfg<true>::SMEM, st, tm, C->k, C->d, ds,
                    tiles_dev, C->tlist, C->tcount, full, gp, C->ctl);
@@ -3205,11 +3306,8 @@ int spkm_dense_assign(const spkm_csr *X, const spkm_centers *C, const spkm_dense
         P.dbg = dbg;
     }
     const size_t smem = (size_t)DN_STAGES * DN_STAGE;
-    static bool attr = false;
-    if (!attr) {
-        cudaFuncSetAttribute(k_dense_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        attr = true;
-    }
+    const cudaError_t ae = cudaFuncSetAttribute(k_dense_pass, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (ae != cudaSuccess) return fail("dense_pass smem attribute", ae);
     int64_t tiles = (X->n + DN_M - 1) / DN_M;
     int grid = (int)(tiles < num_sms() ? tiles : num_sms());
     if (grid < 1) grid = 1;

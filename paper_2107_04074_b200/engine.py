@@ -700,14 +700,13 @@ class Engine:
         # vs 140 ms).  SPKM_ELKAN_FUSE=0/1 forces it (A/B measurements).
         env = os.environ.get("SPKM_ELKAN_FUSE")
         self.fuse_elkan = (k <= 256) if env is None else env != "0"
-        # cluster-ordered survivor lists (spkm_order_by_cluster): when the
-        # term-major center table does not fit L2 the gather passes visit the
-        # survivors grouped by a(i), so the CTAs in flight share a few
-        # clusters' term rows.  SPKM_ORDER=0/1 forces it (A/B measurements).
+        # cluster-ordered survivor lists (spkm_order_by_cluster), SPKM_ORDER=1:
+        # the gather passes visit the survivors grouped by a(i).  Off by
+        # default: at C4 the clusters are too impure to share term rows, and
+        # storage order (longest rows first) was 3% faster (8.94 vs 8.71 it/s,
+        # profiles/r02_ab_notes.txt).
         env = os.environ.get("SPKM_ORDER")
-        big = self.C.kp * data.dim * 4 > (96 << 20)
-        self.order_rows = (not self.dense and 1 < k <= 12288 and
-                           (big if env is None else env != "0"))
+        self.order_rows = (not self.dense and 1 < k <= 12288 and env is not None and env != "0")
         if self.order_rows:
             self.P.ord_tmp = torch.empty(max(self.n_loc, 1), dtype=torch.int32, device=self.device)
             self.P.ord_bins = torch.empty(2 * k, dtype=torch.int32, device=self.device)

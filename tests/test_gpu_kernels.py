@@ -465,3 +465,70 @@ def test_elkan_fused_bounds_scan_matches_two_passes(variant, graphs, monkeypatch
     assert a.objective == b.objective
     key = lambda s: (s.sim_count, s.reassignments, s.survivors, s.nnz_elkan, s.objective)
     assert [key(s) for s in a.iterations] == [key(s) for s in b.iterations]
+
+
+def test_order_by_cluster_is_a_grouping_permutation():
+    """spkm_order_by_cluster: in-place on a list with a device count, and the
+    identity form; the output holds the same rows, grouped by a(i) ascending."""
+    import ctypes
+    from paper_2107_04074_b200 import _lib
+    g = np.random.default_rng(5)
+    n, k = 100_003, 777
+    a = torch.from_numpy(g.integers(0, k, n).astype(np.int32)).cuda()
+    lst_h = g.permutation(n)[:60_001].astype(np.int32)
+    lst = torch.from_numpy(np.concatenate([lst_h, np.full(n - lst_h.size, -7, np.int32)])).cuda()
+    cnt = torch.tensor([lst_h.size], dtype=torch.int64, device="cuda")
+    ctl = torch.zeros(2, dtype=torch.int64, device="cuda")
+    tmp = torch.empty(n, dtype=torch.int32, device="cuda")
+    bins = torch.empty(2 * k, dtype=torch.int32, device="cuda")
+    out = torch.empty(n, dtype=torch.int32, device="cuda")
+    s = ctypes.c_void_p(0)
+    _lib.call("spkm_order_by_cluster", k, a.data_ptr(), lst.data_ptr(), cnt.data_ptr(), n, tmp.data_ptr(), None,
+              bins.data_ptr(), ctl.data_ptr(), s)
+    _lib.call("spkm_order_by_cluster", k, a.data_ptr(), None, None, n, tmp.data_ptr(), out.data_ptr(),
+              bins.data_ptr(), ctl.data_ptr(), s)
+    torch.cuda.synchronize()
+    ah = a.cpu().numpy()
+    got = lst.cpu().numpy()
+    assert np.array_equal(got[lst_h.size:], np.full(n - lst_h.size, -7))      # past the count: untouched
+    got = got[:lst_h.size]
+    assert np.array_equal(np.sort(got), np.sort(lst_h))
+    assert np.all(np.diff(ah[got]) >= 0)
+    full = out.cpu().numpy()
+    assert np.array_equal(np.sort(full), np.arange(n))
+    assert np.all(np.diff(ah[full]) >= 0)
+    # converged (ctl[1] != 0): a no-op
+    ctl[1] = 1
+    before = lst.clone()
+    _lib.call("spkm_order_by_cluster", k, a.data_ptr(), lst.data_ptr(), cnt.data_ptr(), n, tmp.data_ptr(), None,
+              bins.data_ptr(), ctl.data_ptr(), s)
+    torch.cuda.synchronize()
+    assert torch.equal(before, lst)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("graphs", [False, True])
+def test_cluster_ordered_worklists_give_identical_fits(variant, graphs, monkeypatch):
+    """Survivor lists ordered by cluster (SPKM_ORDER=1, the default when the
+    center table exceeds L2) give the same fit and iteration statistics as
+    storage order (=0): the scans' results do not depend on visiting order."""
+    from paper_2107_04074_b200 import engine as E
+    m = spk()
+    data = golden_dataset(load_golden("C1"))
+    monkeypatch.setenv("SPKM_ELKAN_FUSE", "0")      # the Elkan survivor list exists only unfused
+    out = {}
+    for order in ("0", "1"):
+        monkeypatch.setenv("SPKM_ORDER", order)
+        E.clear_engine_cache()
+        for _ in range(2 if graphs else 1):
+            r = m.run(data, 12, variant, m.SeedConfig(seed=3), max_iter=30, use_graphs=graphs)
+        out[order] = r
+    E.clear_engine_cache()
+    a, b = out["0"], out["1"]
+    assert np.array_equal(a.assignments, b.assignments)
+    assert a.objective == b.objective
+    key = lambda s: (s.sim_count, s.reassignments, s.survivors, s.survivors2, s.nnz_elkan, s.nnz_rescan,
+                     s.objective)
+    assert [key(s) for s in a.iterations] == [key(s) for s in b.iterations]
+
+

@@ -37,3 +37,15 @@ for tb in (32, 64, 256):
     pc = torch.nn.functional.pad(c64, (0, dq - data.dim))
     live = (pc.view(k, -1, tb) != 0).any(dim=2).double().mean().item()
     print(f"  cluster x {tb}-term blocks live: {live:.3f}")
+# split by the gathers' L2 head (term rows [0, hot) kept in L2 by the eviction hints)
+hot = min(data.dim, (64 << 20) // (eng.C.kp * 4))
+wc = w.copy(); wc[:hot] = 0
+print(f"  head rows [0,{hot}) carry {w[:hot].sum():.3f} of the nnz")
+for width in (32, 16, 8, 4):
+    kq = (ctl.shape[1] + width - 1) // width * width
+    padded = torch.nn.functional.pad(ctl, (0, kq - ctl.shape[1]))
+    lines = (padded.view(data.dim, -1, width) != 0).any(dim=2).double().cpu().numpy()
+    live = (wc[:, None] * lines).sum() / lines.shape[1] / max(wc.sum(), 1e-30)
+    print(f"  cold rows, {width}-center blocks: nnz-weighted live fraction {live:.3f}")
+nzc = (wc * nz).sum() / max(wc.sum(), 1e-30) / k
+print(f"  cold rows: nnz-weighted nonzero fraction {nzc:.3f} (bitmap+packed bytes/nnz {k/8 + 4*nzc*k:.0f} vs dense {4*k})")

@@ -376,7 +376,12 @@ class DeviceCorpus:
             val_raw = val_h.to(dev, non_blocking=True)
         self.h2d_bytes = sum(t.numel() * t.element_size() for t in (ip_h, idx_h, val_h) if t is not None)
         lens = ip_raw[1:] - ip_raw[:-1]
-        perm = torch.sort(-lens, stable=True).indices
+        key = getattr(data, "_row_key", None)
+        if key is None:
+            perm = torch.sort(-lens, stable=True).indices
+        else:   # locality experiments (tools/c4_locality.py): rows grouped by key, longest first within a group
+            kk = np.asarray(key, np.int64)[r0:r1]
+            perm = torch.from_numpy(np.lexsort((-np.diff(data.indptr[r0:r1 + 1]), kk)).astype(np.int64)).to(dev)
         self.indptr[0] = 0
         torch.cumsum(lens[perm], 0, out=self.indptr[1:])
         stream.wait_stream(up)

@@ -333,6 +333,20 @@ int spkm_permute_rows(int64_t n, const int64_t *ip_raw, const int32_t *idx_raw, 
                       const int64_t *perm, const int64_t *ip_new, const int64_t *new_id, int32_t *idx, float *val,
                       double *val64, float *reps, void *stream);
 
+/* Corpus layout on the device (replaces the host CSR build of sparse.py:136-156
+ * Dataset.matrix / csr_arrays for the device copy): from the raw row offsets
+ * ip_raw[n+1] (relative, ip_raw[0] = 0) -> perm[n] (device row r = raw row
+ * perm[r], rows longest first, stable), pos[n] (inverse of perm, optional),
+ * indptr[n+1] (device-order offsets); when order and new_id are given, also
+ * the term order by document frequency over idx_raw[nnz] (descending,
+ * stable): order[d] (new id -> raw id) and new_id[d] (raw id -> new id).
+ * perm = NULL skips the row part.  Scratch: spkm_prepare_scratch_bytes(n, d)
+ * bytes (-1: n or d >= 2^31). */
+int64_t spkm_prepare_scratch_bytes(int64_t n, int64_t d);
+int spkm_prepare_rows(int64_t n, int64_t d, int64_t nnz, const int64_t *ip_raw, const int32_t *idx_raw,
+                      int64_t *perm, int64_t *pos, int64_t *indptr, int64_t *order, int64_t *new_id,
+                      void *scratch, int64_t scratch_bytes, void *stream);
+
 /* Ingestion (host, no GPU; corpus_io.py:31-131).  spkm_svml_parse parses a
  * whole SVMlight/libsvm text buffer with nthreads threads (<1: all cores);
  * on a syntax error it returns 1 with err_line (1-based) and err_msg (the

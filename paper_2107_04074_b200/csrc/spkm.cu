@@ -28,6 +28,8 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 #include <stdint.h>
 #include <stdio.h>
 #include <math.h>
@@ -2906,6 +2908,7 @@ int encode_gram_map(CUtensorMap *map, const float *base, int64_t kp, int64_t d) 
 }
 
 #include "seed.cuh"
+#include "prepare.cuh"
 
 }  // namespace
 
@@ -3475,6 +3478,55 @@ int spkm_permute_rows(int64_t n, const int64_t *ip_raw, const int32_t *idx_raw, 
     k_permute_rows<<<grid_for(n, 8), 256, 0, S(stream)>>>(n, ip_raw, idx_raw, val_raw, perm, ip_new, new_id, idx, val,
                                                          val64, reps);
     CHECK_LAUNCH("permute_rows");
+    return 0;
+}
+
+
+// ------------------------------------------------- corpus layout (prepare.cuh)
+int64_t spkm_prepare_scratch_bytes(int64_t n, int64_t d) {
+    if (n < 0 || d < 0 || n > INT32_MAX || d > INT32_MAX) return -1;
+    return (int64_t)prep_plan(n, d).total;
+}
+
+int spkm_prepare_rows(int64_t n, int64_t d, int64_t nnz, const int64_t *ip_raw, const int32_t *idx_raw,
+                      int64_t *perm, int64_t *pos, int64_t *indptr, int64_t *order, int64_t *new_id,
+                      void *scratch, int64_t scratch_bytes, void *stream) {
+    if (n < 0 || d < 0 || n > INT32_MAX || d > INT32_MAX) return fail_msg("prepare_rows: n and d must be < 2^31");
+    const PrepPlan p = prep_plan(n, d);
+    if (scratch_bytes < (int64_t)p.total || (!scratch && p.total)) return fail_msg("prepare_rows: scratch too small");
+    cudaStream_t st = (cudaStream_t)stream;
+    char *s = (char *)scratch;
+    uint32_t *rk = (uint32_t *)s;
+    int64_t *rv = (int64_t *)(s + p.rows_key);
+    void *rt = s + p.rows_key + p.rows_val;
+    int64_t *lens = (int64_t *)(s + p.rows_key + p.rows_val + p.rows_tmp);
+    char *s2 = s + p.rows_key + p.rows_val + p.rows_tmp + p.rows_lens;
+    uint32_t *tk = (uint32_t *)s2;
+    int64_t *tv = (int64_t *)(s2 + p.terms_key);
+    void *tt = s2 + p.terms_key + p.terms_val;
+    if (perm && n > 0) {
+        // rows: stable sort by length, descending -> perm
+        k_row_keys<<<grid1(n), 256, 0, st>>>(n, ip_raw, rk, rv);
+        size_t tb = p.rows_tmp;
+        if (cub::DeviceRadixSort::SortPairsDescending(rt, tb, rk, rk + n, rv, perm, (int)n, 0, 32, st) != cudaSuccess)
+            return fail_msg("prepare_rows: CUB sort/scan failed");
+        k_perm_lens<<<grid1(n), 256, 0, st>>>(n, ip_raw, perm, lens, pos, indptr);
+        tb = p.rows_tmp;
+        if (cub::DeviceScan::InclusiveSum(rt, tb, lens, indptr + 1, (int)n, st) != cudaSuccess) return fail_msg("prepare_rows: CUB sort/scan failed");
+    } else if (perm) {
+        cudaMemsetAsync(indptr, 0, sizeof(int64_t), st);
+    }
+    if (order && new_id && d > 0) {
+        // terms: stable sort by document frequency, descending -> order; new_id = order^-1
+        cudaMemsetAsync(tk, 0, (size_t)d * sizeof(uint32_t), st);
+        if (nnz > 0) k_term_df<<<grid1(nnz), 256, 0, st>>>(nnz, idx_raw, tk);
+        k_iota<<<grid1(d), 256, 0, st>>>(d, tv);
+        size_t tb = p.terms_tmp;
+        if (cub::DeviceRadixSort::SortPairsDescending(tt, tb, tk, tk + d, tv, order, (int)d, 0, 32, st) != cudaSuccess)
+            return fail_msg("prepare_rows: CUB sort/scan failed");
+        k_invert<<<grid1(d), 256, 0, st>>>(d, order, new_id);
+    }
+    CHECK_LAUNCH("prepare_rows");
     return 0;
 }
 

@@ -291,6 +291,7 @@ class DeviceCorpus:
         self._stage = None
         self._seed = None
         self._upload = None
+        self._prep = None                # spkm_prepare_rows scratch
         self._row_perm = self._row_pos = None
         self.dense_dim = getattr(data, "dense_dim", None) if self.device.type == "cuda" else None
         if self.dense_dim is not None and self.dense_dim % 32 != 0:
@@ -375,25 +376,42 @@ class DeviceCorpus:
                 idx_raw = idx_h.to(dev, non_blocking=True)
             val_raw = val_h.to(dev, non_blocking=True)
         self.h2d_bytes = sum(t.numel() * t.element_size() for t in (ip_h, idx_h, val_h) if t is not None)
-        lens = ip_raw[1:] - ip_raw[:-1]
+        # device layout by spkm_prepare_rows (csrc/prepare.cuh): rows longest
+        # first (stable radix sort) and their offsets, then -- once per
+        # Dataset -- the term order by document frequency
+        nb = int(_lib.lib().spkm_prepare_scratch_bytes(self.n, self.d))
+        if nb < 0:
+            raise ConfigError("corpus too large for one device (n and d must be < 2^31)")
+        if self._prep is None or self._prep.numel() < nb:
+            self._prep = torch.empty(max(nb, 1), dtype=torch.uint8, device=dev)
+        perm = torch.empty(max(self.n, 1), dtype=torch.int64, device=dev)
         key = getattr(data, "_row_key", None)
+        pos = self._seed[3] if self._seed is not None else None    # refresh: the seeding maps follow
         if key is None:
-            perm = torch.sort(-lens, stable=True).indices
+            _lib.call("spkm_prepare_rows", self.n, self.d, 0, _ptr(ip_raw), None, _ptr(perm),
+                      None if pos is None else _ptr(pos), _ptr(self.indptr), None, None, _ptr(self._prep), nb, sp)
         else:   # locality experiments (tools/c4_locality.py): rows grouped by key, longest first within a group
             kk = np.asarray(key, np.int64)[r0:r1]
-            perm = torch.from_numpy(np.lexsort((-np.diff(data.indptr[r0:r1 + 1]), kk)).astype(np.int64)).to(dev)
-        self.indptr[0] = 0
-        torch.cumsum(lens[perm], 0, out=self.indptr[1:])
+            lens = np.diff(data.indptr[r0:r1 + 1])
+            ph = np.lexsort((-lens, kk)).astype(np.int64)
+            perm.copy_(torch.from_numpy(ph))
+            ip = np.zeros(self.n + 1, np.int64)
+            np.cumsum(lens[ph], out=ip[1:])
+            self.indptr.copy_(torch.from_numpy(ip))
+            if pos is not None:
+                inv = np.empty_like(ph)
+                inv[ph] = np.arange(ph.size)
+                pos.copy_(torch.from_numpy(inv))
         stream.wait_stream(up)
         idx_raw.record_stream(stream)
         val_raw.record_stream(stream)
         cached = getattr(data, "_term_order", None)
         if cached is None and self.rows == (0, data.n):
-            df = torch.bincount(idx_raw.to(torch.int64), minlength=self.d)
-            order_d = torch.sort(-df, stable=True).indices
+            order_d = torch.empty(max(self.d, 1), dtype=torch.int64, device=dev)
             new_id_d = torch.empty_like(order_d)
-            new_id_d[order_d] = torch.arange(self.d, device=dev)
-            order_h, new_id_h = order_d.cpu().numpy(), new_id_d.cpu().numpy()
+            _lib.call("spkm_prepare_rows", self.n, self.d, self.nnz, None, _ptr(idx_raw), None, None, None,
+                      _ptr(order_d), _ptr(new_id_d), _ptr(self._prep), nb, sp)
+            order_h, new_id_h = order_d[:self.d].cpu().numpy(), new_id_d[:self.d].cpu().numpy()
             data._term_order = (order_h, new_id_h)
             self._new_id_dev, self._new_id_src = new_id_d, new_id_h
         else:
@@ -413,9 +431,8 @@ class DeviceCorpus:
             self.reps.fill_(float(row_eps_dense(self.dense_dim, 1)[0]))
         self.perm_dev = perm
         self._row_perm = self._row_pos = None   # host copies on first use (no sync here)
-        if self._seed is not None:          # refresh: the seeding maps follow the new rows
+        if self._seed is not None:          # refresh: the seeding maps follow the new rows (pos written above)
             self._seed[2].copy_(perm)
-            self._seed[3].scatter_(0, perm, torch.arange(self.n, dtype=torch.int64, device=dev))
         del ip_raw, idx_raw, val_raw        # stream-ordered frees (caching allocator)
 
     def refresh(self, data: Dataset):
@@ -674,7 +691,12 @@ class Engine:
         self.hamerly = variant in _HAMERLY_FAMILY
         self.needs_cc = variant in _CC_VARIANTS
         self.C = CenterState(k, data.dim, self.n_total, self.device, self.needs_cc, order=self.corpus.order)
-        self.dense = self.corpus.dense_dim is not None
+        # dense corpora: the tcgen05 similarity pass for standard and the Hamerly
+        # family; the Elkan family (per-(point, center) bounds and pair scans)
+        # runs the sparse kernels over the dense rows (every row holds all D
+        # terms), as does everything when SPKM_DENSE_TC=0 (A/B, tests)
+        self.dense = (self.corpus.dense_dim is not None and not self.elkan
+                      and os.environ.get("SPKM_DENSE_TC", "1") != "0")
         # rows this rank scans: all of them, or its shard [p0, p1) of the replicated corpus
         self.p0, self.p1 = (comm.p0, comm.p1) if comm is not None else (0, self.corpus.n)
         self.n_loc = self.p1 - self.p0
@@ -683,9 +705,6 @@ class Engine:
             self.n_loc, cs.d, cs.nnz, _ptr(cs.indptr) + 8 * self.p0, _ptr(cs.indices), _ptr(cs.values),
             _ptr(cs.reps) + 4 * self.p0)
         if self.dense:
-            if self.elkan:
-                raise ConfigError("the Elkan family is not available for dense corpora in this build "
-                                  "(standard, hamerly and simp_hamerly are)")
             self.C.attach_dense(self.corpus, row0=self.p0, n_rows=self.n_loc, rescan=self.hamerly)
         self.P = PointState(self.n_loc, k, variant, self.device)
         self.a_global = torch.zeros(max(cs.n, 1), dtype=torch.int32, device=self.device) if comm is not None else None

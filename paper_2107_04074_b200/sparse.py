@@ -119,13 +119,45 @@ class Dataset:
     (reference sparse.py:117-134).
     """
 
-    def __init__(self, indptr, indices, data, dim: int, _checked: bool = False):
+    def __init__(self, *args, rows=None, dim=None, indptr=None, indices=None, data=None):
+        """Two forms:
+
+        * ``Dataset(rows, dim)`` / ``Dataset(rows=..., dim=...)`` -- the
+          reference's dataclass constructor (sparse.py:101-115): a sequence of
+          ``SparseVector`` rows taken as they are (no normalisation; use
+          ``from_rows`` for the checked, normalising constructor);
+        * ``Dataset(indptr, indices, data, dim)`` -- flat CSR arrays (the
+          scalable form; ``from_csr`` adds the checks and the normalisation).
+        """
+        if len(args) == 4:
+            indptr, indices, data, dim = args
+        elif len(args) == 2:
+            rows, dim = args
+        elif len(args) == 1 and rows is None and indptr is None:
+            rows = args[0]
+        elif args:
+            raise TypeError("Dataset(rows, dim) or Dataset(indptr, indices, data, dim)")
+        if dim is None:
+            raise TypeError("Dataset needs dim")
+        row_objs = None
+        if rows is not None:
+            if indptr is not None:
+                raise TypeError("give rows or CSR arrays, not both")
+            row_objs = tuple(rows)
+            indptr = np.zeros(len(row_objs) + 1, np.int64)
+            indptr[1:] = np.cumsum([r.nnz for r in row_objs])
+            indices = (np.concatenate([np.asarray(r.indices) for r in row_objs]) if row_objs
+                       else np.zeros(0, np.int32))
+            data = (np.concatenate([np.asarray(r.values, np.float64) for r in row_objs]) if row_objs
+                    else np.zeros(0))
+        elif indptr is None or indices is None or data is None:
+            raise TypeError("Dataset(rows, dim) or Dataset(indptr, indices, data, dim)")
         self.indptr = np.ascontiguousarray(indptr, dtype=np.int64)
         self.indices = np.ascontiguousarray(indices, dtype=np.int32)
         self.data = np.ascontiguousarray(data, dtype=np.float64)
         self.dim = int(dim)
         self.n = int(self.indptr.size - 1)
-        self._rows = None
+        self._rows = row_objs
         self._csr = None
         self._device_cache = {}
 

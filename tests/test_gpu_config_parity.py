@@ -67,7 +67,7 @@ def _check_same(r, base, v):
 @pytest.mark.parametrize("name,variants", [
     ("C3", VARIANTS),                                   # n = 500k, d = 250k, k = 200: full size
     ("C4s", VARIANTS),                                  # C4 generator at n = 250k, d = 1M, k = 1000
-    ("C5s", ("standard", "hamerly", "simp_hamerly")),   # dense C5 at n = 100k, k = 1000 (tensor cores)
+    ("C5s", VARIANTS),      # dense C5 at n = 100k, k = 1000 (tensor cores; the Elkan family on the sparse kernels)
 ])
 def test_config_parity_vs_oracle(name, variants):
     import paper_2107_04074_b200 as spk
@@ -79,7 +79,7 @@ def test_config_parity_vs_oracle(name, variants):
         _check_oracle(r, z, conf)
         if base is None:
             base = r
-        else:
+        elif not (name == "C5s" and v in ("elkan", "simp_elkan")):   # other similarity path: oracle check only
             _check_same(r, base, v)
         assert sum(s.sim_count for s in r.iterations) <= len(r.iterations) * ds.n * k
 

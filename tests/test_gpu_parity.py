@@ -81,7 +81,7 @@ def test_c1_parity_all_variants(oracle_mod):
                         len(z[key + "__objective"]), z[key + "__margin"])
 
 
-def test_c5_dense_subsample_parity(oracle_mod):
+def test_c5_dense_subsample_parity(oracle_mod, monkeypatch):
     """Config C5 (dense unit vectors, d=256, k=1000) on a 20k-row subsample of the generator."""
     import paper_2107_04074_b200 as spk
     from paper_2107_04074_b200 import synth
@@ -90,7 +90,7 @@ def test_c5_dense_subsample_parity(oracle_mod):
     ref = oracle_mod.run(X, 1000, "standard", seed=5, max_iter=50)
     margin = oracle_mod.margins(X, ref["centers"])
     base = None
-    for v in ("standard", "hamerly", "simp_hamerly"):       # tensor-core dense path (Elkan family: sparse only)
+    for v in ("standard", "hamerly", "simp_hamerly"):       # tensor-core dense path
         r = spk.run(data, 1000, v, spk.SeedConfig(seed=5), max_iter=50)
         if base is None:
             base = r
@@ -102,8 +102,20 @@ def test_c5_dense_subsample_parity(oracle_mod):
     a, best, second = spk.assign_full(data, base.centers)
     _, rb, rs = oracle_mod.assign_full(X, base.centers.centers)
     assert np.max(np.abs(best - rb)) < 3e-5 and np.max(np.abs(second - rs)) < 3e-5
-    with pytest.raises(spk.ConfigError):
-        spk.run(data, 10, "elkan", spk.SeedConfig(seed=5), max_iter=3)
+    # the Elkan family on dense rows runs the sparse kernels: equal to the Lloyd of that path
+    from paper_2107_04074_b200 import engine
+    monkeypatch.setenv("SPKM_DENSE_TC", "0")
+    engine.clear_engine_cache()
+    sbase = spk.run(data, 1000, "standard", spk.SeedConfig(seed=5), max_iter=50)
+    check_vs_oracle(sbase, ref["assignments"], ref["objective"][-1], ref["iterations"], margin)
+    monkeypatch.delenv("SPKM_DENSE_TC")
+    engine.clear_engine_cache()
+    for v in ("elkan", "simp_elkan"):
+        r = spk.run(data, 1000, v, spk.SeedConfig(seed=5), max_iter=50)
+        check_vs_oracle(r, ref["assignments"], ref["objective"][-1], ref["iterations"], margin)
+        assert np.array_equal(r.assignments, sbase.assignments), v
+        assert r.objective == sbase.objective, v
+        assert [s.reassignments for s in r.iterations] == [s.reassignments for s in sbase.iterations]
 
 
 def _edge_dataset(kind):

@@ -235,3 +235,25 @@ def test_from_csr_normalises_like_from_rows():
     rows = [SparseVector(idx[ip[i]:ip[i + 1]], val[ip[i]:ip[i + 1]]) for i in range(lens.size)]
     b = Dataset.from_rows(rows, dim=5000)
     assert np.array_equal(a.data, np.concatenate([r.values for r in b.rows]))
+
+
+def test_dataset_reference_constructor_forms():
+    """Dataset(rows=..., dim=...) / Dataset(rows, dim): the reference dataclass
+    form (sparse.py:101-115, rows taken as given) next to the CSR form."""
+    from paper_2107_04074_b200.sparse import Dataset, SparseVector
+    rows = [SparseVector(np.array([0, 3]), np.array([0.6, 0.8])), SparseVector(np.array([2]), np.array([1.0]))]
+    a = Dataset(rows=rows, dim=5)
+    b = Dataset(rows, 5)
+    c = Dataset.from_rows(rows, dim=5, normalize_rows=False)
+    for ds in (a, b):
+        assert ds.n == 2 and ds.dim == 5 and ds.rows[0] is rows[0]
+        assert np.array_equal(ds.indptr, c.indptr) and np.array_equal(ds.indices, c.indices)
+        assert np.array_equal(ds.data, c.data)
+        ip, ix, dv = ds.csr_arrays()
+        assert ix.dtype == np.int64 and list(ip) == [0, 2, 3]
+    d = Dataset(c.indptr, c.indices, c.data, 5)
+    assert np.array_equal(d.data, c.data) and d.rows[1].indices.tolist() == [2]
+    with pytest.raises(TypeError):
+        Dataset(rows)
+    with pytest.raises(TypeError):
+        Dataset(c.indptr, c.indices, 5)

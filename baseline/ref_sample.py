@@ -20,7 +20,8 @@ Cost model for the full-size estimate: the reference's per-iteration time
 splits into row-proportional work (similarities, bound updates, the scans,
 the moves loop) and work on the k x d centers (``_move_centers``,
 ``_center_thresholds`` and the objective einsum), which does not grow with
-n.  The center phases are timed by wrapping the two functions and
+n (with --d-full: the sample's term ids were folded to its d, and the center
+phases, linear in d, are scaled by d_full / d).  The center phases are timed by wrapping the two functions and
 ``np.einsum`` in the reference module's namespace (timers only; the
 reference code runs unchanged); the row part is scaled by n_full / n_sub.
 """
@@ -53,6 +54,7 @@ def main():
     p.add_argument("--max-iter", type=int, default=3)
     p.add_argument("--seed", type=int, default=2)
     p.add_argument("--n-full", type=int, required=True)
+    p.add_argument("--d-full", type=int, default=None, help="full d when the sample's term ids are folded")
     a = p.parse_args()
     if not (REF / "spkmeans").exists():
         print(json.dumps({"unavailable": f"{REF} missing (pip install --target baseline/_ref)"}))
@@ -101,7 +103,7 @@ def main():
     E._center_thresholds = timed(E._center_thresholds)
     E.np = proxy
 
-    out = {"n_sub": n_sub, "n_full": a.n_full, "k": a.k, "max_iter": a.max_iter, "variants": {},
+    out = {"n_sub": n_sub, "n_full": a.n_full, "d_sample": dim, "d_full": a.d_full or dim, "k": a.k, "max_iter": a.max_iter, "variants": {},
            "dataset_build_s": round(build_s, 2), "jit_warmup_s": round(jit_s, 2),
            "threads": "1 (OPENBLAS/OMP/MKL/NUMBA_NUM_THREADS=1)", "spkmeans": getattr(spkmeans, "__version__", "0.1.0")}
     its_tot, t_full_tot, t_sub_tot = 0, 0.0, 0.0
@@ -113,7 +115,7 @@ def main():
         its = len(r.iterations)
         el = sum(s.elapsed_ns for s in r.iterations) / 1e9     # seeding excluded (engine.py:240)
         oth = min(other[0], el)
-        t_full = (el - oth) * a.n_full / n_sub + oth
+        t_full = (el - oth) * a.n_full / n_sub + oth * (a.d_full or dim) / dim
         out["variants"][v] = {"iterations": its, "elapsed_s": round(el, 3), "wall_s": round(wall, 3),
                               "center_phase_s": round(oth, 3), "est_full_s": round(t_full, 3),
                               "sims": int(sum(s.sim_count for s in r.iterations))}

@@ -62,7 +62,7 @@ VARIANTS = ("standard", "elkan", "simp_elkan", "hamerly", "simp_hamerly")
 DEFAULTS = {"C1": (20, VARIANTS), "C2": (100, VARIANTS), "C3": (200, ("elkan", "hamerly")),
             "C4": (1000, ("hamerly", "simp_elkan")), "C5": (1000, ("hamerly",))}
 PEAKS = ROOT / "MEASURED_PEAKS.json"
-REF_STEP_S = 8.0          # target seconds of CPU work per reference-arm step
+REF_STEP_S = 5.0          # target seconds of CPU work per reference-arm step
 
 
 def metric_name(args) -> str:
@@ -197,12 +197,47 @@ def workload_config(args, data, n_gpus):
 
 
 # ----------------------------------------------------------------- CPU legs
+D_FOLD = 20000     # columns of the CPU samples: the k x d center phases scale linearly in d
+
+
+def cpu_sample(data, n_sub: int, d_fold: int = D_FOLD):
+    """The CPU legs' sample: the first n_sub rows; when d > d_fold, term ids
+    folded modulo d_fold (duplicates within a row summed, rows renormalised),
+    so the k x d center phases (thresholds, renormalise, objective: linear in
+    d) cost d_fold/d of the full size and are scaled back by d/d_fold.  The
+    row phases keep every nnz (their cost does not depend on d, except that a
+    smaller center table caches better on the host: conservative for the GPU).
+    Returns (indptr, int32 indices, float64 data, d_sample)."""
+    n_sub = min(n_sub, data.n)
+    ip = np.asarray(data.indptr[:n_sub + 1], np.int64)
+    ix = np.asarray(data.indices[:ip[-1]], np.int64)
+    dv = np.asarray(data.data[:ip[-1]], np.float64)
+    if data.dim <= d_fold:
+        return ip, ix.astype(np.int32), dv, data.dim
+    rows = np.repeat(np.arange(n_sub, dtype=np.int64), np.diff(ip))
+    key = rows * d_fold + ix % d_fold
+    order = np.argsort(key, kind="stable")
+    ks = key[order]
+    uniq, start = np.unique(ks, return_index=True)
+    vals = np.add.reduceat(dv[order], start)
+    keep = vals != 0.0
+    uniq, vals = uniq[keep], vals[keep]
+    r = uniq // d_fold
+    counts = np.bincount(r, minlength=n_sub)
+    if np.any(counts == 0):
+        raise ValueError("a folded sample row is empty")
+    ip2 = np.zeros(n_sub + 1, np.int64)
+    np.cumsum(counts, out=ip2[1:])
+    nrm = np.sqrt(np.add.reduceat(vals * vals, ip2[:-1]))
+    vals = vals / np.repeat(nrm, counts)
+    return ip2, (uniq % d_fold).astype(np.int32), vals, d_fold
+
+
 def _oracle_sample(data, n_sub: int):
+    """(oracle CSR of the CPU sample, d / d_sample)."""
     from oracle import oracle as O
-    if n_sub >= data.n:
-        return O.CSR(data.indptr, data.indices, data.data, data.dim)
-    ip = data.indptr[:n_sub + 1]
-    return O.CSR(ip, data.indices[:ip[-1]], data.data[:ip[-1]], data.dim)
+    ip, ix, dv, ds = cpu_sample(data, n_sub)
+    return O.CSR(ip, ix, dv, ds), data.dim / ds
 
 
 def oracle_plan(args, data, budget_s: float):
@@ -212,11 +247,12 @@ def oracle_plan(args, data, budget_s: float):
     from oracle import oracle as O
     variants = args.variants.split(",")
     k = args.k
-    n_probe = min(data.n, max(20000, 4 * k))
-    r = O.run(_oracle_sample(data, n_probe), min(k, n_probe), variants[0], seed=args.seed, max_iter=2)
+    n_probe = min(data.n, max(5000, 4 * k))
+    X, dscale = _oracle_sample(data, n_probe)
+    r = O.run(X, min(k, n_probe), variants[0], seed=args.seed, max_iter=2)
     its = max(r["iterations"], 1)
     per_row = float(r["t_rows"].sum()) / its / n_probe
-    other = float(r["t_other"].sum()) / its
+    other = float(r["t_other"].sum()) / its          # at the sample's d: the measured share of a step
     mi = min(args.max_iter, 50)
     per_it_full = per_row * data.n + other
     if per_it_full * mi * len(variants) <= budget_s:
@@ -224,7 +260,7 @@ def oracle_plan(args, data, budget_s: float):
     mi = max(2, min(mi, 4))
     room = budget_s / (mi * len(variants)) - other
     n_sub = int(room / per_row) if room > 0 else n_probe
-    n_sub = max(min(data.n, max(4 * k, 20000)), min(data.n, n_sub))
+    n_sub = max(min(data.n, max(2 * k, 5000)), min(data.n, n_sub))
     return n_sub, mi
 
 
@@ -232,14 +268,14 @@ def oracle_sample_rate(args, data, n_sub: int, mi: int):
     """One fit of every variant on the first n_sub rows (cap mi iterations):
     (iterations, full-size-equivalent seconds, measured seconds)."""
     from oracle import oracle as O
-    X = _oracle_sample(data, n_sub)
+    X, dscale = _oracle_sample(data, n_sub)
     its, t_full, t_meas = 0, 0.0, 0.0
     for v in args.variants.split(","):
         r = O.run(X, min(args.k, n_sub), v, seed=args.seed, max_iter=mi)
         its += r["iterations"]
         tr, to = float(r["t_rows"].sum()), float(r["t_other"].sum())
         t_meas += tr + to
-        t_full += tr * data.n / n_sub + to
+        t_full += tr * data.n / n_sub + to * dscale
     return its, t_full, t_meas
 
 
@@ -247,9 +283,11 @@ def sample_label(data, n_sub, mi, args):
     if n_sub >= data.n and mi >= args.max_iter:
         return f"full workload: one fit of each of [{args.variants}]"
     rows = "all rows" if n_sub >= data.n else f"the first {n_sub} of {data.n} rows"
+    fold = (f", term ids folded to d' = {D_FOLD} (k x d center phases -- thresholds, renormalise, objective -- "
+            f"timed at d' and scaled by d/d' = {data.dim / D_FOLD:g})" if data.dim > D_FOLD else
+            ", k x d center phases counted as measured")
     return (f"one fit of each of [{args.variants}] on {rows}, each capped at {mi} iterations; "
-            f"row-proportional phase time (sims, bounds, scans, aggregation, moves) scaled by n/n_sub, "
-            f"k x d center phases (thresholds, renormalise, objective) counted as measured")
+            f"row-proportional phase time (sims, bounds, scans, aggregation, moves) scaled by n/n_sub" + fold)
 
 
 def run_reference(args):
@@ -298,13 +336,13 @@ def cpu_baseline_reference(args, data, n_sub: int = 10000, max_iter: int = 3, ti
     if not (ROOT / "baseline" / "_ref" / "spkmeans").exists():
         return {"unavailable": "baseline/_ref not installed"}
     n_sub = min(n_sub, data.n)
-    ip = data.indptr[:n_sub + 1]
+    ip, ix, dv, ds = cpu_sample(data, n_sub)
     with tempfile.TemporaryDirectory() as td:
         f = Path(td) / "sample.npz"
-        np.savez(f, indptr=ip, indices=data.indices[:ip[-1]], data=data.data[:ip[-1]], dim=data.dim)
+        np.savez(f, indptr=ip, indices=ix, data=dv, dim=ds)
         cmd = [sys.executable, str(ROOT / "baseline" / "ref_sample.py"), "--npz", str(f), "--k",
                str(min(args.k, n_sub)), "--variants", args.variants, "--max-iter", str(max_iter), "--seed",
-               str(args.seed), "--n-full", str(data.n)]
+               str(args.seed), "--n-full", str(data.n), "--d-full", str(data.dim)]
         try:
             out = subprocess.run(cmd, capture_output=True, text=True, timeout=timeout)
             r = json.loads(out.stdout.strip().splitlines()[-1])
@@ -315,7 +353,8 @@ def cpu_baseline_reference(args, data, n_sub: int = 10000, max_iter: int = 3, ti
     return {"value": r["its_per_s_full_est"], "unit": "iterations/s", "cores": 1, "kind": "reference",
             "sample": (f"unmodified spkmeans {r['spkmeans']} (baseline/_ref), serial: one fit of each of "
                        f"[{args.variants}] on the first {r['n_sub']} of {data.n} rows, max_iter {max_iter}; "
-                       f"row phases scaled by n/n_sub, k x d center phases as measured"),
+                       f"row phases scaled by n/n_sub, k x d center phases "
+                       + (f"timed at folded d' = {ds} and scaled by d/d'" if ds < data.dim else "as measured")),
             "value_at_sample": r["its_per_s_sample"], "detail": r}
 
 

@@ -287,7 +287,8 @@ int spkm_audit(const spkm_seed *S, int64_t k, int64_t kp, const double *ct64, co
 /* Multi-GPU exchange (distributed.py): the corpus is replicated and the
  * scans are sharded by device-row ranges; per iteration each rank packs its
  * moves and counters into a fixed-size int32 slot of
- * spkm_move_slot_ints(cap) ints (cap = its shard's rows; rows are stored
+ * spkm_move_slot_ints(cap) ints (a multiple of 4: every slot of the gathered
+ * array is 16-byte aligned; cap = its shard's rows; rows are stored
  * global, p0 = the shard's first device row), the slots are allgathered
  * (NCCL), and every rank applies all ranks' moves to its replicated
  * fixed-point sums (spkm_apply_move_slots, X = the whole corpus) and takes

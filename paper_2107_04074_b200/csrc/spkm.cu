@@ -3550,7 +3550,11 @@ int spkm_audit(const spkm_seed *Sd, int64_t k, int64_t kp, const double *ct64, c
 
 
 // ------------------------------------------------------ multi-GPU exchange
-int64_t spkm_move_slot_ints(int64_t cap) { return kSlotHead + 3 * cap; }
+// rounded up to 4 ints: every slot of the allgathered array starts 16-byte
+// aligned, so its int64 counter head is an aligned load for every rank q
+// (an odd slot length put rank 1's head on a 4-byte boundary: misaligned
+// address at world 3, found by tests/test_gpu_loopback.py)
+int64_t spkm_move_slot_ints(int64_t cap) { return (kSlotHead + 3 * cap + 3) / 4 * 4; }
 
 int spkm_pack_moves(const spkm_work *W, const spkm_bounds *B, const spkm_centers *C, int64_t p0, int64_t cap,
                     int32_t *slot, void *stream) {

@@ -47,7 +47,8 @@ enum spkm_variant {
     SPKM_ELKAN = 1,
     SPKM_SIMP_ELKAN = 2,
     SPKM_HAMERLY = 3,
-    SPKM_SIMP_HAMERLY = 4
+    SPKM_SIMP_HAMERLY = 4,
+    SPKM_YINYANG = 5            /* not in the reference: group bounds */
 };
 
 /* spkm_full_assign modes */
@@ -55,7 +56,8 @@ enum spkm_assign_mode {
     SPKM_MODE_INIT_PLAIN = 0,   /* iteration 1, no bounds (standard)          */
     SPKM_MODE_INIT_ELKAN = 1,   /* iteration 1, l + u(i,j) for every j        */
     SPKM_MODE_INIT_HAMERLY = 2, /* iteration 1, l + u = second best           */
-    SPKM_MODE_LLOYD = 3         /* iteration >= 2 of standard: reassign+moves */
+    SPKM_MODE_LLOYD = 3,        /* iteration >= 2 of standard: reassign+moves */
+    SPKM_MODE_INIT_YINYANG = 6  /* iteration 1, l + group bounds ug(i, g), g = 4 centers */
 };
 
 /* Device CSR of the (local shard of the) corpus; rows unit-normalised. */
@@ -164,6 +166,16 @@ int spkm_hamerly_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B
                         int use_s, int naive, void *stream);
 int spkm_hamerly_tighten(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
                          int use_s, void *stream);
+/* Yin-Yang group bounds (the reference has no
+ * Yin-Yang): groups = 4 consecutive centers; B->u holds ug[n][ku] with
+ * ku = ceil(k/4) rounded up to 4.  Iteration 1: spkm_full_assign with
+ * SPKM_MODE_INIT_YINYANG.  Then per iteration: spkm_yy_bounds (drift update
+ * of l and ug by each group's worst drift, prune test, survivor list) and
+ * spkm_yy_scan (tighten s~(i, a), fetch the groups with ug + eps > s~(i, a),
+ * best by the Lloyd rule, exact bounds of the fetched groups).  k <= 1024. */
+int spkm_yy_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream);
+int spkm_yy_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream);
+
 /* Full-k rescan of the tighten survivors.  use_s: as for spkm_hamerly_tighten
  * -- when the previous iteration's tighten pruned < 5% of the bound survivors
  * (flag in hstat[6], set by spkm_finalize) this pass takes the bound
@@ -278,7 +290,8 @@ int spkm_seed_rows_csr(const spkm_centers *C, const spkm_seed *S, const int64_t 
  * corpus (device-order rows) and folds, with atomicMax on order-preserving
  * keys (keys[0] lower, keys[1] upper): mode 0 max(l - S[i,a]) and
  * max(S - u) over the Elkan matrix (row stride ku), 1 the Hamerly
- * max_{j != a} S[i,j] - u[i], 2 the lower bound only, 3 argmax per row into
+ * max_{j != a} S[i,j] - u[i], 2 the Yin-Yang max_{j != a} S[i,j] - u[i, j/4]
+ * (group bounds, row stride ku), 3 argmax per row into
  * a_out (lowest index on ties). */
 int spkm_audit_transpose(int64_t k, int64_t d, int64_t kp, const double *cent64, double *ct64, void *stream);
 int spkm_audit(const spkm_seed *S, int64_t k, int64_t kp, const double *ct64, const int32_t *a, const float *l,

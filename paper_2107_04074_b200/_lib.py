@@ -69,6 +69,7 @@ class Work(ctypes.Structure):
 # modes / enums (include/spkm.h)
 MODE_INIT_PLAIN, MODE_INIT_ELKAN, MODE_INIT_HAMERLY, MODE_LLOYD = 0, 1, 2, 3
 MODE_PREDICT, DMODE_RESCAN_H = 5, 6
+MODE_INIT_YINYANG = 6          # spkm_full_assign (the dense modes are a separate enum)
 CTR_SURV1, CTR_SURV2, CTR_MOVES, CTR_SIMS, CTR_NNZ_TIGHTEN, CTR_NNZ_RESCAN, CTR_NNZ_ELKAN, CTR_NNZ_MOVED = range(8)
 (ST_SIMS, ST_REASSIGN, ST_OBJECTIVE, ST_ALLONE, ST_SURV1, ST_SURV2, ST_TOUCHED, ST_NNZ_TIGHTEN, ST_NNZ_RESCAN,
  ST_NNZ_ELKAN, ST_ITER, ST_TSTAMP, ST_T0, ST_NNZ_MOVED) = range(14)
@@ -87,6 +88,8 @@ _SIGS = {
     "spkm_hamerly_tighten": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_hamerly_rescan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_elkan_bounds": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
+    "spkm_yy_bounds": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), c_vp],
+    "spkm_yy_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), c_vp],
     "spkm_elkan_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_elkan_bounds_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_aggregate_sums": [_P(CSR), _P(Centers), _P(Bounds), c_vp, c_vp, c_vp],
@@ -151,7 +154,7 @@ _RESTYPES = {
 # kernels each entry point launches (for the bench's gpu_launches count)
 KERNELS_PER_CALL = {
     "spkm_full_assign": 1, "spkm_hamerly_bounds": 1, "spkm_hamerly_tighten": 1, "spkm_hamerly_rescan": 1,
-    "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_elkan_bounds_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
+    "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_yy_bounds": 1, "spkm_yy_scan": 1, "spkm_elkan_bounds_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
     "spkm_move_centers": 5, "spkm_center_reduce": 1, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,

@@ -289,7 +289,7 @@ __device__ __forceinline__ float ldg_hint(const float *p, uint64_t pol) {
     return v;
 }
 
-enum { MODE_RESCAN = 4, MODE_PREDICT = 5 };
+enum { MODE_RESCAN = 4, MODE_PREDICT = 5, MODE_INIT_YY = SPKM_MODE_INIT_YINYANG };
 
 struct RowPassArgs {
     const int64_t *indptr;
@@ -438,6 +438,27 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
             const int src = (valid && inc >= 0) ? g * A.tpr + (inc % jstr) / 4 : lane;
             sa = __shfl_sync(FULL, mine, src);
         }
+        if (A.mode == MODE_INIT_YY) {
+            // Yin-Yang group bounds: group f = the 4 consecutive centers of one
+            // float4 (lane q, round r: f = q + r * tpr), ug(i, f) = the max of
+            // s~ + eps over its centers j != a(i) (-1: none)
+            const int bj = __shfl_sync(FULL, tp.bj, g * A.tpr);
+            if (valid) {
+#pragma unroll
+                for (int r = 0; r < CH / 4; ++r) {
+                    const int f = q + r * A.tpr;
+                    if (4 * f < A.k) {
+                        float m = -INFINITY;
+#pragma unroll
+                        for (int c = 0; c < 4; ++c) {
+                            const int j = 4 * f + c;
+                            if (j < A.k && j != bj) m = fmaxf(m, acc[4 * r + c]);
+                        }
+                        A.u[row * A.ku + f] = (m == -INFINITY) ? -1.f : store_upper((double)m + eps);
+                    }
+                }
+            }
+        }
         if (A.mode == SPKM_MODE_INIT_ELKAN && valid) {
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
@@ -451,6 +472,7 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
         if (leader) {
             switch (A.mode) {
                 case SPKM_MODE_INIT_PLAIN:
+                case MODE_INIT_YY:
                 case SPKM_MODE_INIT_ELKAN:
                 case SPKM_MODE_INIT_HAMERLY:
                     A.a[row] = tp.bj;
@@ -1215,6 +1237,313 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
         const bool leader = valid && q == 0;
         warp_append(leader && cur != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
         ctr_add(s_ctr, SPKM_CTR_SIMS, sims);
+        ctr_add(s_ctr, SPKM_CTR_NNZ_ELKAN, leader ? (long long)len : 0);
+        __syncwarp();
+    }
+    PDL_TRIGGER();
+    ctr_flush(s_ctr, ctr);
+}
+
+// ------------------------------------------------------ Yin-Yang family
+// Group bounds (Ding et al., ICML 2015, carried over to cosine similarities
+// as the paper says its bounds transfer: PAPER.md:409-414, 667-671) with the
+// groups = blocks of 4 consecutive centers (one float4 of a term-major ct32
+// row, the gather unit of the scans).  Per point: a(i), l(i) <= <x_i, c_a>,
+// ug(i, g) >= max over j in g, j != a(i) of <x_i, c_j>  (n x ceil(k/4)
+// floats: a quarter of Elkan's n x k).  Per iteration:
+//   * drift update: l by a(i)'s own drift (engine.py:274), ug(i, g) by the
+//     group's worst drift (min p_j, max sin_p over the group; Eq. 9 as the
+//     Elkan u update, kernels.py:35-47 via engine.py:281-283);
+//   * a point survives if some group may beat l: ug + 2 eps > l;
+//   * survivors: tighten s~(i, a), fetch every group with ug + eps >
+//     s~(i, a) (its 4 canonical similarities), take the best (strict >
+//     beats the incumbent, ties to the lowest index: the Lloyd rule), and
+//     recompute the bounds of the fetched groups exactly.
+// Skips only what is provably <= s~(i, a) with the same eps margins as the
+// Elkan kernels, so every fit equals the GPU Lloyd bit for bit.
+constexpr int kYyMaxGroups = 256;   // k <= 1024
+__global__ void __launch_bounds__(256) k_yy_bounds(int64_t n, int k, const float *__restrict__ reps,
+                                                   const int32_t *__restrict__ a, float *l, float *ug, int64_t gp,
+                                                   const double *__restrict__ drift,
+                                                   const double *__restrict__ sinp, int32_t *surv1, long long *ctr,
+                                                   const long long *__restrict__ ctl) {
+    PDL_ENTRY();
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    __shared__ __align__(16) float s_pd[kYyMaxGroups], s_pu[kYyMaxGroups], s_su[kYyMaxGroups];
+    const int ng = (k + 3) >> 2;
+    const int g4 = (ng + 3) >> 2;
+    for (int g = threadIdx.x; g < 4 * g4; g += blockDim.x) {
+        double pmin = 1.0, smax = 0.0;
+        for (int c = 0; c < 4; ++c) {
+            const int j = 4 * g + c;
+            if (g < ng && j < k) {
+                pmin = fmin(pmin, drift[j]);
+                smax = fmax(smax, sinp[j]);
+            }
+        }
+        s_pd[g] = __double2float_rd(pmin);
+        s_pu[g] = __double2float_ru(pmin);
+        s_su[g] = __double2float_ru(smax);
+    }
+    __syncthreads();
+    const float4 *pd4 = reinterpret_cast<const float4 *>(s_pd), *pu4 = reinterpret_cast<const float4 *>(s_pu),
+                 *su4 = reinterpret_cast<const float4 *>(s_su);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int wpb = blockDim.x >> 5;
+    const int64_t nchunks = (n + 31) >> 5;
+    __shared__ int s_cnt[8];
+    __shared__ long long s_base;
+    for (int64_t c0 = (int64_t)blockIdx.x * wpb; c0 < nchunks; c0 += (int64_t)gridDim.x * wpb) {
+        const int64_t c = c0 + wib;
+        const int64_t rb = c << 5;
+        const int64_t ir = rb + lane;
+        float thu_r = 0.f;
+        if (c < nchunks && ir < n) {
+            const int ai = a[ir];
+            const float lo = l[ir];
+            float lf = lo;
+            const double sa = sinp[ai];
+            if (sa != 0.0) {
+                const double pa = drift[ai];
+                lf = store_lower((lo < -pa) ? -1.0 : d_clamp((double)lo * pa - d_sin((double)lo) * sa));
+                l[ir] = lf;
+            }
+            thu_r = thr_u_of((double)lf, (double)reps[ir]);
+        }
+        const int nr = c < nchunks ? (int)min((int64_t)32, n - rb) : 0;
+        unsigned smask = 0;
+        for (int r = 0; r < nr; ++r) {
+            const float thu = __shfl_sync(FULL, thu_r, r);
+            float4 *gi = reinterpret_cast<float4 *>(ug + (rb + r) * gp);
+            bool any = false;
+            for (int q = lane; q < g4; q += 32) {
+                float4 v = gi[q];
+                const float4 su = su4[q];
+                if (su.x != 0.f || su.y != 0.f || su.z != 0.f || su.w != 0.f) {
+                    const float4 pd = pd4[q], pu = pu4[q];
+                    v.x = su.x != 0.f ? elkan_u_drift(v.x, pd.x, pu.x, su.x) : v.x;
+                    v.y = su.y != 0.f ? elkan_u_drift(v.y, pd.y, pu.y, su.y) : v.y;
+                    v.z = su.z != 0.f ? elkan_u_drift(v.z, pd.z, pu.z, su.z) : v.z;
+                    v.w = su.w != 0.f ? elkan_u_drift(v.w, pd.w, pu.w, su.w) : v.w;
+                    gi[q] = v;        // padding groups (g >= ng) have su == 0: never rewritten
+                }
+                const int gb = 4 * q;
+                any |= (gb + 0 < ng && v.x > thu) || (gb + 1 < ng && v.y > thu) || (gb + 2 < ng && v.z > thu) ||
+                       (gb + 3 < ng && v.w > thu);
+            }
+            if (__any_sync(FULL, any)) smask |= 1u << r;
+        }
+        // one global atomic per CTA round: warp counts -> shared prefix
+        if (lane == 0) s_cnt[wib] = __popc(smask);
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+            for (int w = 0; w < wpb; ++w) {
+                const int t = s_cnt[w];
+                s_cnt[w] = tot;
+                tot += t;
+            }
+            s_base = tot ? (long long)atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1), (unsigned long long)tot)
+                         : 0ll;
+        }
+        __syncthreads();
+        if (smask >> lane & 1u) surv1[s_base + s_cnt[wib] + __popc(smask & ((1u << lane) - 1u))] = (int32_t)ir;
+        __syncthreads();
+    }
+    PDL_TRIGGER();
+}
+
+// floats of the per-warp similarity buffer of k_yy_scan: 4 per group and point
+__host__ __device__ __forceinline__ int yy_sim_stride(int64_t k) {
+    const int ng = (int)((k + 3) / 4);
+    const int bpr = ng < 32 ? ng : 32;
+    const int ppw = (32 / bpr) < 8 ? (32 / bpr) : 8;
+    return 4 * ng * ppw;
+}
+// Survivor scan: lanes = groups (bpr lanes per point, up to 8 points per
+// warp, rounds of 32 groups), the gather machinery of k_elkan_scan<4>.
+__global__ void __launch_bounds__(256) k_yy_scan(const int64_t *__restrict__ indptr,
+                                                 const int32_t *__restrict__ indices,
+                                                 const float *__restrict__ values, const float *__restrict__ reps,
+                                                 const float *__restrict__ ct, int64_t kp, int k, int32_t *a,
+                                                 float *l, float *ug, int64_t gp,
+                                                 const int32_t *__restrict__ surv1, int32_t *mv_i, int32_t *mv_old,
+                                                 long long *ctr, const long long *__restrict__ ctl, int64_t hot) {
+    PDL_ENTRY();
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
+    constexpr int UB = 8;     // nnz per gather batch: 8 float4 loads in flight per lane
+    __shared__ __align__(16) int2 s_iv[8][8][kIvStride];
+    __shared__ int s_act[8][kYyMaxGroups];
+    extern __shared__ float s_sim_yy[];    // [8 warps][yy_sim_stride(k)]
+    __shared__ unsigned long long s_ctr[8];
+    ctr_init(s_ctr);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int ng = (k + 3) >> 2;
+    const int bpr = ng < 32 ? ng : 32;
+    const int ppw = min(8, 32 / bpr);
+    const int nrounds = (ng + 31) >> 5;
+    const int g = lane / bpr, q = lane - g * bpr;
+    const bool lane_on = g < ppw;
+    const int o0 = bpr > 1 ? (1 << (31 - __clz(bpr - 1))) : 0;
+    float *my_sim = s_sim_yy + wib * yy_sim_stride(k) + (lane_on ? g : 0) * 4 * ng;   // 4 per group and point
+    int *my_act = s_act[wib] + (lane_on ? g : 0) * (kYyMaxGroups / ppw);
+    int2 *my_iv = s_iv[wib][lane_on ? g : 0];
+    const long long cnt = ctr[SPKM_CTR_SURV1];
+    const int64_t nslots = (cnt + ppw - 1) / ppw;
+    const int wpb = blockDim.x >> 5;
+    const unsigned gmask_lo = bpr >= 32 ? 0xffffffffu : ((1u << bpr) - 1u);
+    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
+        const int64_t slot = w * ppw + g;
+        const bool valid = lane_on && slot < cnt;
+        const int32_t i = valid ? surv1[slot] : 0;
+        const int ai = valid ? a[i] : 0;
+        float *gi = ug + (int64_t)i * gp;
+        const double eps = valid ? (double)reps[i] : 0.0;
+        const int64_t s = valid ? indptr[i] : 0, e = valid ? indptr[i + 1] : 0;
+        const int len = (int)(e - s);
+        // (A) tighten: s~(i, a(i)), the canonical chain for the single center a(i)
+        float lcur = 0.f;
+        {
+            const int maxt = (int)__reduce_max_sync(FULL, (unsigned)len);
+            float acc = 0.f;
+            const float *cta = ct + ai;
+            for (int c0 = 0; c0 < maxt; c0 += 32) {
+                const int cntc = max(0, min(32, len - c0));
+                for (int q2 = q; q2 < cntc; q2 += bpr) {
+                    const int t = __ldg(indices + s + c0 + q2);
+                    const float cv = ldg_hint(cta + (int64_t)t * kp, t < hot ? pol_hot : pol_cold);
+                    my_iv[q2] = make_int2(__float_as_int(__ldg(values + s + c0 + q2)), __float_as_int(cv));
+                }
+                __syncwarp();
+                if (q == 0)
+                    for (int t = 0; t < cntc; ++t)
+                        acc = __fmaf_rn(__int_as_float(my_iv[t].x), __int_as_float(my_iv[t].y), acc);
+                __syncwarp();
+            }
+            lcur = __shfl_sync(FULL, acc, lane - q);
+        }
+        // (B) groups to fetch: ug + eps > s~(i, a), compacted per point
+        int nact = 0;
+        {
+            const double lc = (double)lcur;
+            for (int r = 0; r < nrounds; ++r) {
+                const int gr = r * 32 + q;
+                const bool act = valid && gr < ng && !((double)gi[gr] + eps <= lc);
+                const unsigned m = __ballot_sync(FULL, act);
+                const unsigned gm = (m >> (lane - q)) & gmask_lo;
+                if (act) my_act[nact + __popc(gm & ((1u << q) - 1u))] = gr;
+                nact += __popc(gm);
+            }
+        }
+        __syncwarp();
+        // (C) the 4 canonical similarities of every active group
+        const int act_rounds = (int)__reduce_max_sync(FULL, (unsigned)((nact + bpr - 1) / bpr));
+        const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)(nact ? len : 0));
+        const float4 *base4 = reinterpret_cast<const float4 *>(ct);
+        for (int r = 0; r < act_rounds; ++r) {
+            const int sb = r * bpr + q;
+            const bool act = lane_on && sb < nact;
+            const int gr = act ? my_act[sb] : 0;
+            float acc[4] = {0.f, 0.f, 0.f, 0.f};
+            const int glen = nact > r * bpr ? len : 0;
+            for (int c0 = 0; c0 < maxlen; c0 += 32) {
+                const int cntc = max(0, min(32, glen - c0));
+                for (int q2 = q; q2 < cntc; q2 += bpr)
+                    my_iv[q2] = make_int2(__ldg(indices + s + c0 + q2), __float_as_int(__ldg(values + s + c0 + q2)));
+                __syncwarp();
+                if (act) {
+                    int uu = 0;
+                    for (; uu + UB <= cntc; uu += UB) {
+                        float4 x[UB];
+                        float vv[UB];
+                        int iv[UB];
+                        load_iv<UB>(my_iv + uu, iv, vv);
+#pragma unroll
+                        for (int b = 0; b < UB; ++b)
+                            x[b] = ldg_hint(base4 + (((int64_t)iv[b] * kp) >> 2) + gr, iv[b] < hot ? pol_hot : pol_cold);
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) {
+                            acc[0] = __fmaf_rn(vv[b], x[b].x, acc[0]);
+                            acc[1] = __fmaf_rn(vv[b], x[b].y, acc[1]);
+                            acc[2] = __fmaf_rn(vv[b], x[b].z, acc[2]);
+                            acc[3] = __fmaf_rn(vv[b], x[b].w, acc[3]);
+                        }
+                    }
+                    for (; uu < cntc; ++uu) {
+                        const int2 t = my_iv[uu];
+                        const float v0 = __int_as_float(t.y);
+                        const float4 x0 = ldg_hint(base4 + (((int64_t)t.x * kp) >> 2) + gr, t.x < hot ? pol_hot : pol_cold);
+                        acc[0] = __fmaf_rn(v0, x0.x, acc[0]);
+                        acc[1] = __fmaf_rn(v0, x0.y, acc[1]);
+                        acc[2] = __fmaf_rn(v0, x0.z, acc[2]);
+                        acc[3] = __fmaf_rn(v0, x0.w, acc[3]);
+                    }
+                }
+                __syncwarp();
+            }
+            if (act) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) my_sim[4 * sb + c] = acc[c];
+            }
+        }
+        __syncwarp();
+        // (D) the best candidate (larger value, ties to the lower index), then
+        // the incumbent rule: strictly greater than s~(i, a) to move
+        float bs = -INFINITY;
+        int bj = 0x7fffffff;
+        long long sims = 0;
+        for (int sb = q; sb < nact; sb += bpr) {
+            const int gr = my_act[sb];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int j = 4 * gr + c;
+                if (j >= k || j == ai) continue;
+                ++sims;
+                const float v = my_sim[4 * sb + c];
+                if (v > bs || (v == bs && j < bj)) {
+                    bs = v;
+                    bj = j;
+                }
+            }
+        }
+        for (int o = o0; o; o >>= 1) {
+            const float ov = __shfl_down_sync(FULL, bs, o);
+            const int oj = __shfl_down_sync(FULL, bj, o);
+            if (q < o && q + o < bpr && (ov > bs || (ov == bs && oj < bj))) {
+                bs = ov;
+                bj = oj;
+            }
+        }
+        bs = __shfl_sync(FULL, bs, lane - q);
+        bj = __shfl_sync(FULL, bj, lane - q);
+        const int b = (valid && bs > lcur) ? bj : ai;
+        const float sb_val = b == ai ? lcur : bs;
+        // (E) bounds: fetched groups exactly (max over j != b), a(i)'s group
+        // when it was not fetched and a(i) lost the point gains s~(i, a)
+        for (int sb = q; sb < nact; sb += bpr) {
+            const int gr = my_act[sb];
+            float m = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int j = 4 * gr + c;
+                if (j < k && j != b) m = fmaxf(m, my_sim[4 * sb + c]);
+            }
+            gi[gr] = (m == -INFINITY) ? -1.f : store_upper((double)m + eps);
+        }
+        const bool leader = valid && q == 0;
+        if (leader) {
+            l[i] = store_lower((double)sb_val - eps);
+            if (b != ai) {
+                a[i] = b;
+                const int ga = ai >> 2;
+                bool fetched = false;
+                for (int sb = 0; sb < nact; ++sb) fetched |= my_act[sb] == ga;
+                if (!fetched) gi[ga] = fmaxf(gi[ga], store_upper((double)lcur + eps));
+            }
+        }
+        warp_append(leader && b != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
+        ctr_add(s_ctr, SPKM_CTR_SIMS, sims + (leader ? 1 : 0));
         ctr_add(s_ctr, SPKM_CTR_NNZ_ELKAN, leader ? (long long)len : 0);
         __syncwarp();
     }
@@ -2613,6 +2942,7 @@ __global__ void __launch_bounds__(256) k_audit(int64_t n, int64_t k, int64_t kp,
                 if (j == ai) own = S;
                 if (mode == 0) up = fmax(up, S - (double)u[i * ku + j]);
                 if (mode == 1 && j != ai) up = fmax(up, S);
+                if (mode == 2 && j != ai) up = fmax(up, S - (double)u[i * ku + (j >> 2)]);   // Yin-Yang groups
                 if (mode == 3 && (S > best || (S == best && j < bj))) {
                     best = S;
                     bj = (int)j;
@@ -2634,7 +2964,7 @@ __global__ void __launch_bounds__(256) k_audit(int64_t n, int64_t k, int64_t kp,
                 a_out[i] = bj;
             } else {
                 atomicMax(keys, dkey((double)l[i] - own));
-                if (mode == 0) atomicMax(keys + 1, dkey(up));
+                if (mode == 0 || (mode == 2 && k > 1)) atomicMax(keys + 1, dkey(up));
                 if (mode == 1 && k > 1) atomicMax(keys + 1, dkey(up - (double)u[i]));
             }
         }
@@ -2993,6 +3323,31 @@ int spkm_hamerly_rescan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B
     A.mv_old = W->mv_old;
     A.ctr = W->ctr;
     return launch_row_pass(A, C->k, S(stream), X->n);
+}
+
+int spkm_yy_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream) {
+    if (X->n == 0) return 0;
+    if (C->k > 4 * kYyMaxGroups) return fail_msg("yy_bounds: k > 1024 not supported by this build");
+    if (B->ku < (C->k + 3) / 4 || B->ku % 4) return fail_msg("yy_bounds: ku must be ceil(k/4) rounded up to 4");
+    const int grid = grid_for((X->n + 31) / 32, 8);
+    pdl_launch(k_yy_bounds, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l,
+               B->u, B->ku, C->drift, C->sinp, W->surv1, W->ctr, C->ctl);
+    CHECK_LAUNCH("yy_bounds");
+    return 0;
+}
+
+int spkm_yy_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream) {
+    if (X->n == 0) return 0;
+    if (C->k > 4 * kYyMaxGroups) return fail_msg("yy_scan: k > 1024 not supported by this build");
+    const int grid = grid_for(X->n, 8);
+    const size_t dyn = (size_t)8 * yy_sim_stride(C->k) * sizeof(float);
+    const cudaError_t attr = cudaFuncSetAttribute(k_yy_scan, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+    if (attr != cudaSuccess) return fail("yy_scan smem", attr);
+    pdl_launch(k_yy_scan, dim3(grid), dim3(256), dyn, S(stream), X->indptr, X->indices, X->values, X->row_eps,
+               C->ct32, C->kp, (int)C->k, B->a, B->l, B->u, B->ku, W->surv1, W->mv_i, W->mv_old, W->ctr, C->ctl,
+               hot_terms(C));
+    CHECK_LAUNCH("yy_scan");
+    return 0;
 }
 
 int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,

@@ -37,6 +37,9 @@ from .errors import ConfigError, DeviceError, InfeasibleError
 from .sparse import Dataset
 
 VARIANTS = ("standard", "elkan", "simp_elkan", "hamerly", "simp_hamerly")
+# beyond the reference's five: Yin-Yang group bounds (SURVEY.md 8(f) rank 4,
+# PAPER.md:409-414; the reference does not implement it)
+EXTRA_VARIANTS = ("yinyang",)
 _ELKAN_FAMILY = frozenset({"elkan", "simp_elkan"})
 _HAMERLY_FAMILY = frozenset({"hamerly", "simp_hamerly"})
 _CC_VARIANTS = frozenset({"elkan", "hamerly"})
@@ -629,6 +632,9 @@ class PointState:
         if variant in _ELKAN_FAMILY:
             self.ku = (k + 3) // 4 * 4
             self.u = torch.zeros(max(n, 1) * self.ku, dtype=torch.float32, device=device)
+        elif variant == "yinyang":      # group bounds ug[n][ceil(k/4) rounded up to 4]
+            self.ku = ((k + 3) // 4 + 3) // 4 * 4
+            self.u = torch.zeros(max(n, 1) * self.ku, dtype=torch.float32, device=device)
         else:
             self.ku = 1
             self.u = torch.zeros(max(n, 1), dtype=torch.float32, device=device)
@@ -654,7 +660,7 @@ class PointState:
 
 # --------------------------------------------------------------- validation
 def _validate(data: Dataset, k: int, variant: str, hamerly_update: str):
-    if variant not in VARIANTS:
+    if variant not in VARIANTS and variant not in EXTRA_VARIANTS:
         raise ConfigError(f"unknown variant {variant!r}")
     if hamerly_update not in ("safe", "naive"):
         raise ConfigError(f"unknown hamerly_update {hamerly_update!r}")
@@ -689,13 +695,14 @@ class Engine:
         self.n_total = n_total if n_total is not None else self.corpus.n
         self.elkan = variant in _ELKAN_FAMILY
         self.hamerly = variant in _HAMERLY_FAMILY
+        self.yy = variant == "yinyang"
         self.needs_cc = variant in _CC_VARIANTS
         self.C = CenterState(k, data.dim, self.n_total, self.device, self.needs_cc, order=self.corpus.order)
         # dense corpora: the tcgen05 similarity pass for standard and the Hamerly
         # family; the Elkan family (per-(point, center) bounds and pair scans)
         # runs the sparse kernels over the dense rows (every row holds all D
         # terms), as does everything when SPKM_DENSE_TC=0 (A/B, tests)
-        self.dense = (self.corpus.dense_dim is not None and not self.elkan
+        self.dense = (self.corpus.dense_dim is not None and not self.elkan and not self.yy
                       and os.environ.get("SPKM_DENSE_TC", "1") != "0")
         # rows this rank scans: all of them, or its shard [p0, p1) of the replicated corpus
         self.p0, self.p1 = (comm.p0, comm.p1) if comm is not None else (0, self.corpus.n)
@@ -814,7 +821,7 @@ class Engine:
 
     def init_pass(self):
         mode = (_lib.MODE_INIT_ELKAN if self.elkan else _lib.MODE_INIT_HAMERLY if self.hamerly
-                else _lib.MODE_INIT_PLAIN)
+                else _lib.MODE_INIT_YINYANG if self.yy else _lib.MODE_INIT_PLAIN)
         if self.dense:
             return self._dense(mode)
         _lib.call("spkm_full_assign", self.xs, self.C.struct, self.P.bounds, self.P.work, mode, self.sp)
@@ -838,7 +845,9 @@ class Engine:
                   _lib.MODE_LLOYD, self.sp)
 
     def bounds_pass(self, use_flag: int):
-        if self.elkan:
+        if self.yy:
+            _lib.call("spkm_yy_bounds", self.xs, self.C.struct, self.P.bounds, self.P.work, self.sp)
+        elif self.elkan:
             _lib.call("spkm_elkan_bounds", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
         else:
             _lib.call("spkm_hamerly_bounds", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag,
@@ -854,7 +863,9 @@ class Engine:
 
     def scan_pass(self, use_flag: int):
         self.order_survivors()
-        if self.elkan:
+        if self.yy:
+            _lib.call("spkm_yy_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, self.sp)
+        elif self.elkan:
             _lib.call("spkm_elkan_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
         elif self.dense:
             self._dense(_lib.DMODE_RESCAN_H, use_flag)   # tighten + full scan on the canonical TC values
@@ -932,6 +943,9 @@ class Engine:
         if self.elkan:
             um = h(self.P.u.view(-1, self.P.ku)[:n, :self.k].cpu().numpy().astype(np.float64))
             return BoundsState(self.variant, a, l, u_matrix=um)
+        if self.yy:         # group bounds: u_matrix[i, g] over the centers 4g .. 4g+3
+            ug = h(self.P.u.view(-1, self.P.ku)[:n, :(self.k + 3) // 4].cpu().numpy().astype(np.float64))
+            return BoundsState(self.variant, a, l, u_matrix=ug)
         u = h(self.P.u[:n].cpu().numpy().astype(np.float64))
         return BoundsState(self.variant, a, l, u=u)
 

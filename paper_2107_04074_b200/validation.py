@@ -100,13 +100,15 @@ class DeviceBoundAuditor:
         sp = eng.sp
         with torch.cuda.stream(eng.stream):
             _lib.call("spkm_audit_transpose", k, d, kp, _ptr(C.cent64), _ptr(self.ct64), sp)
-            mode = 0 if eng.elkan else 1
+            mode = 0 if eng.elkan else 2 if eng.yy else 1
             _lib.call("spkm_audit", st, k, kp, _ptr(self.ct64), _ptr(P.a), _ptr(P.l), _ptr(P.u), P.ku, mode,
                       _ptr(self.keys), None, sp)
         n = eng.corpus.n
         self.count += n
         if eng.elkan:
             self.count += n * k
+        elif eng.yy:
+            self.count += n * ((k + 3) // 4)
         elif k > 1:
             self.count += n
 

@@ -257,3 +257,14 @@ def test_dataset_reference_constructor_forms():
         Dataset(rows)
     with pytest.raises(TypeError):
         Dataset(c.indptr, c.indices, 5)
+
+
+def test_yinyang_is_an_extra_variant():
+    """VARIANTS stays the reference's five; "yinyang" is accepted on top."""
+    from paper_2107_04074_b200 import engine
+    assert spk.VARIANTS == ("standard", "elkan", "simp_elkan", "hamerly", "simp_hamerly")
+    assert "yinyang" in engine.EXTRA_VARIANTS
+    data = Dataset.from_csr(np.array([0, 1, 2]), np.array([0, 1]), np.array([1.0, 1.0]), 2)
+    engine._validate(data, 2, "yinyang", "safe")
+    with pytest.raises(spk.ConfigError):
+        engine._validate(data, 2, "yin_yang", "safe")

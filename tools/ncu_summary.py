@@ -20,10 +20,16 @@ KEYS = [
     ("regs", "launch__registers_per_thread"),
     ("tensor%", "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active"),
     ("grid", "launch__grid_size"),
+    ("l2_rd_sect_M", "lts__t_sectors_srcunit_tex_op_read.sum"),
+    ("l1_rd_sect_M", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum"),
+    ("lsu_wavefr%", "l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+    ("issue%", "sm__inst_issued.avg.pct_of_peak_sustained_active"),
 ]
 
 
 def unit_scale(unit, key):
+    if key.endswith("_sect_M"):
+        return {"sector": 1e-6, "Ksector": 1e-3, "Msector": 1.0, "Gsector": 1e3}.get(unit, 1e-6)
     if key.startswith("dram_") and key.endswith("MB"):
         return {"byte": 1e-6, "Kbyte": 1e-3, "Mbyte": 1.0, "Gbyte": 1e3}.get(unit, 1.0)
     if key == "time_us":

@@ -532,7 +532,8 @@ KERNEL_OF = {"spkm_full_assign": "k_row_pass", "spkm_hamerly_rescan": "k_row_pas
              "spkm_elkan_bounds_scan": "k_elkan_scan (fused bounds)", "spkm_dense_assign": "k_dense_pass",
              "spkm_apply_moves": "k_apply_moves", "spkm_aggregate_sums": "k_aggregate",
              "spkm_order_by_cluster": "k_order_*", "spkm_move_centers": "center pipeline (4 kernels)",
-             "spkm_center_thresholds": "k_gram_mn + k_gram_final + k_row_max"}
+             "spkm_center_thresholds": "k_gram_mn + k_gram_final + k_row_max",
+             "spkm_yy_bounds": "k_yy_bounds", "spkm_yy_scan": "k_yy_scan"}
 MULTI = {"spkm_move_centers", "spkm_center_thresholds", "spkm_order_by_cluster"}
 
 
@@ -564,7 +565,9 @@ def roofline(args, data, corpus, dev, world):
             csr_full = 8 * nnz + csr_row * n
             n_full = 1 + (len(its) - 1 if v == "standard" else 0)
             # full passes: CSR + the bound writes (a, l; u: Hamerly 4 B, Elkan 4k B)
-            init_w = 8 * n + (4 * ku * n if v in ("elkan", "simp_elkan") else 4 * n if "hamerly" in v else 0)
+            gpw = ((k + 3) // 4 + 3) // 4 * 4
+            init_w = 8 * n + (4 * ku * n if v in ("elkan", "simp_elkan") else 4 * n if "hamerly" in v
+                              else 4 * gpw * n if v == "yinyang" else 0)
             b = csr_full * n_full + init_w + 4 * n * (n_full - 1)
             bytes_by[("spkm_full_assign", v)] = b
             gather_by[("spkm_full_assign", v)] = 4 * kp * nnz * n_full
@@ -588,6 +591,14 @@ def roofline(args, data, corpus, dev, world):
                 # fused: the scan's u reads of a survivor are the bound pass's (counted once)
                 bytes_by[("spkm_elkan_bounds_scan", v)] = b_bounds + sum(
                     8 * s.nnz_elkan + csr_row * s.survivors for s in its[1:])
+            if v == "yinyang":
+                # group bounds (4 centers per group, gp per row): bound pass reads ug, a, l, eps, writes l and
+                # the groups holding a moved center; the scan re-reads the survivor's CSR row and ug
+                gp = ((k + 3) // 4 + 3) // 4 * 4
+                moved_prev = [its[q - 1].touched for q in range(1, len(its))]
+                bytes_by[("spkm_yy_bounds", v)] = sum((4 * gp + 16) * n + 4 * min(gp, m) * n for m in moved_prev)
+                bytes_by[("spkm_yy_scan", v)] = sum(8 * s.nnz_elkan + (csr_row + 8 * gp + 16) * s.survivors
+                                                    for s in its[1:])
             bytes_by[("spkm_apply_moves", v)] = sum(16 * s.nnz_moved for s in its[1:])
             bytes_by[("spkm_move_centers", v)] = sum(20 * s.touched * data.dim for s in its)
             if dense:

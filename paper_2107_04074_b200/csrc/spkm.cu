@@ -730,9 +730,23 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
 // (n*k elements per iteration: float64 sqrt made this pass ALU-bound).
 //   pd = rd(p), pu = ru(p), su = ru(sin_p) (su == 0 <=> the center did not move)
 //   (double)w <= p  <=>  w <= pd, exactly (pd is the largest float <= p)
+#ifndef SPKM_FAST_SQRT
+#define SPKM_FAST_SQRT 0
+#endif
+// sqrt(x) rounded up, x in [0, 1]: the IEEE directed sqrt is a ~20-instruction
+// software sequence; x * rsqrt(x) from the MUFU (<= 2 ulp + 0.5 ulp of the
+// product) times (1 + 2^-19) rounded up is >= sqrt(x) at a quarter of the cost
+__device__ __forceinline__ float sqrt_up(float x) {
+#if SPKM_FAST_SQRT
+    if (x <= 0.f) return 0.f;
+    return __fmul_ru(x * rsqrtf(x), 1.0f + 1.9073486e-6f);
+#else
+    return __fsqrt_ru(x);
+#endif
+}
 __device__ __forceinline__ float elkan_u_drift(float w, float pd, float pu, float su) {
     if (!(w <= pd)) return 1.0f;
-    const float sw = __fsqrt_ru(fmaxf(__fmaf_ru(-w, w, 1.0f), 0.0f));   // >= sin(w)
+    const float sw = sqrt_up(fmaxf(__fmaf_ru(-w, w, 1.0f), 0.0f));   // >= sin(w)
     const float prod = __fmaf_ru(sw, su, 1e-12f);
     const float nv = __fmaf_ru(w, w >= 0.f ? pu : pd, prod);
     return fminf(fmaxf(nv, -1.0f), 1.0f);
@@ -753,7 +767,10 @@ __device__ __forceinline__ float thr_c_of(double lb, double eps) { return __doub
 // and appends the chunk's survivors with one atomic.  Per-center pd/pu/su
 // live in shared memory.  k <= 1024.
 constexpr int kEbMaxK = 1024;
-__global__ void __launch_bounds__(256) k_elkan_bounds(int64_t n, int k, const float *__restrict__ reps,
+#ifndef SPKM_EB_MINB
+#define SPKM_EB_MINB 1
+#endif
+__global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, int k, const float *__restrict__ reps,
                                                       const int32_t *__restrict__ a, float *l, float *u,
                                                       int64_t ku, const double *__restrict__ drift,
                                                       const double *__restrict__ sinp,
@@ -906,7 +923,11 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
-    constexpr int UB = 32 / EB;   // nnz per gather batch: 8 float4 loads in flight per lane
+#ifndef SPKM_EK_UB
+#define SPKM_EK_UB 1
+#endif
+    // nnz per gather batch: 8 * SPKM_EK_UB float4 loads in flight per lane
+    constexpr int UB = SPKM_EK_UB * 32 / EB;
     constexpr int ES = EB + 1;    // padded per-block stride of the similarity buffer
     __shared__ __align__(16) int2 s_iv[8][8][kIvStride];
     __shared__ int s_act[8][128];          // per warp: the groups' active block lists (ppw * nb <= 128)

@@ -731,14 +731,14 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
 //   pd = rd(p), pu = ru(p), su = ru(sin_p) (su == 0 <=> the center did not move)
 //   (double)w <= p  <=>  w <= pd, exactly (pd is the largest float <= p)
 #ifndef SPKM_FAST_SQRT
-#define SPKM_FAST_SQRT 0
+#define SPKM_FAST_SQRT 1      // C4 k_elkan_bounds 430 -> 321 ms per fit with SPKM_EB_MINB 3 (r02_ab_notes)
 #endif
 // sqrt(x) rounded up, x in [0, 1]: the IEEE directed sqrt is a ~20-instruction
 // software sequence; x * rsqrt(x) from the MUFU (<= 2 ulp + 0.5 ulp of the
 // product) times (1 + 2^-19) rounded up is >= sqrt(x) at a quarter of the cost
 __device__ __forceinline__ float sqrt_up(float x) {
 #if SPKM_FAST_SQRT
-    if (x <= 0.f) return 0.f;
+    if (x < 1e-30f) return 1e-15f;    // >= sqrt(x); keeps subnormals away from the MUFU
     return __fmul_ru(x * rsqrtf(x), 1.0f + 1.9073486e-6f);
 #else
     return __fsqrt_ru(x);
@@ -768,7 +768,7 @@ __device__ __forceinline__ float thr_c_of(double lb, double eps) { return __doub
 // live in shared memory.  k <= 1024.
 constexpr int kEbMaxK = 1024;
 #ifndef SPKM_EB_MINB
-#define SPKM_EB_MINB 1
+#define SPKM_EB_MINB 3        // 80 registers, 3 CTAs per SM: the u stream needs the warps (126 -> 80 regs)
 #endif
 __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, int k, const float *__restrict__ reps,
                                                       const int32_t *__restrict__ a, float *l, float *u,
@@ -876,7 +876,10 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
 // instruction) while the row fits one round of 32 lanes (k <= 128); EB = 8
 // (two float4, one 32-byte sector) above, which halves the rounds.  Measured:
 // C2 (k = 100) scan 91 -> 78 us with 4; C3 (k = 200) 2.6 -> 3.1 ms with 4.
-__host__ __device__ __forceinline__ int elkan_block(int64_t k) { return k <= 128 ? 4 : 8; }
+#ifndef SPKM_EK_EB4_MAXK
+#define SPKM_EK_EB4_MAXK 128
+#endif
+__host__ __device__ __forceinline__ int elkan_block(int64_t k) { return k <= SPKM_EK_EB4_MAXK ? 4 : 8; }
 // floats of the per-warp value buffer of k_elkan_scan (EB + 1 per block)
 __host__ __device__ __forceinline__ int64_t elkan_sim_stride(int64_t k) {
     const int64_t eb = elkan_block(k);
@@ -930,7 +933,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     constexpr int UB = SPKM_EK_UB * 32 / EB;
     constexpr int ES = EB + 1;    // padded per-block stride of the similarity buffer
     __shared__ __align__(16) int2 s_iv[8][8][kIvStride];
-    __shared__ int s_act[8][128];          // per warp: the groups' active block lists (ppw * nb <= 128)
+    __shared__ int s_act[8][EB == 4 ? 256 : 128];   // per warp: the groups' active block lists (ppw * nb <= 256 / 128)
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
     extern __shared__ float s_sim_dyn[];   // [8 warps][sim_stride]
@@ -1081,6 +1084,20 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
                 nact += __popc(gm);
             }
         }
+#ifndef SPKM_EK_DENSE_PCT
+#define SPKM_EK_DENSE_PCT 0
+#endif
+#if SPKM_EK_DENSE_PCT > 0
+        // most blocks active: fetch them all in block order (each warp load
+        // instruction then reads one contiguous span of the center row: full
+        // 128-byte lines instead of scattered sectors); the extra blocks'
+        // similarities are computed but never read by the replay
+        if (nact * 100 >= SPKM_EK_DENSE_PCT * nb) {
+            __syncwarp();
+            for (int bb = q; bb < nb; bb += bpr) my_act[bb] = bb;
+            nact = nb;
+        }
+#endif
         __syncwarp();
         const int act_rounds = (int)__reduce_max_sync(FULL, (unsigned)((nact + bpr - 1) / bpr));
         const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)(nact ? len : 0));

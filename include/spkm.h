@@ -95,6 +95,10 @@ typedef struct spkm_centers {
     long long *ctl;          /* [2]   {iterations done, converged}: every loop
                                 kernel is a no-op once converged, so the
                                 host may enqueue iterations ahead          */
+    uint16_t *ct16;          /* [d*kp] fp16 (round to nearest) copy of ct32 for
+                                the screening full pass, or NULL: the row
+                                pass gathers half the bytes and re-checks
+                                the near-best centers on ct32 exactly      */
 } spkm_centers;
 
 /* Per-point bounds of the local shard. */

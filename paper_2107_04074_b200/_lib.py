@@ -40,7 +40,7 @@ class Centers(ctypes.Structure):
     _fields_ = [("k", c_i64), ("d", c_i64), ("kp", c_i64), ("scale_bits", c_i32), ("_pad", c_i32),
                 ("cent64", c_vp), ("ct32", c_vp), ("sums", c_vp), ("counts", c_vp), ("drift", c_vp),
                 ("sinp", c_vp), ("touched", c_vp), ("objc", c_vp), ("part", c_vp), ("norm", c_vp), ("cc", c_vp),
-                ("s", c_vp), ("hstat", c_vp), ("tlist", c_vp), ("tcount", c_vp), ("ctl", c_vp)]
+                ("s", c_vp), ("hstat", c_vp), ("tlist", c_vp), ("tcount", c_vp), ("ctl", c_vp), ("ct16", c_vp)]
 
 
 class Bounds(ctypes.Structure):

@@ -28,6 +28,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 #include <stdint.h>
@@ -283,6 +284,16 @@ __device__ __forceinline__ float4 ldg_hint(const float4 *p, uint64_t pol) {
                  : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "l"(p), "l"(pol));
     return v;
 }
+__device__ __forceinline__ uint2 ldg_hint(const uint2 *p, uint64_t pol) {
+    uint2 v;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0,%1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ float4 half4_to_float4(uint2 h) {
+    const float2 a = __half22float2(*reinterpret_cast<const __half2 *>(&h.x));
+    const float2 b = __half22float2(*reinterpret_cast<const __half2 *>(&h.y));
+    return make_float4(a.x, a.y, b.x, b.y);
+}
 __device__ __forceinline__ float ldg_hint(const float *p, uint64_t pol) {
     float v;
     asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(p), "l"(pol));
@@ -319,14 +330,107 @@ struct RowPassArgs {
     const float *s_arr;
     int use_s;
     int64_t hot;                 // term rows [0, hot) are gathered with evict_last, the rest evict_first
+    const __half *ct16;          // fp16 copy of ct for the screening pass (HALF instantiations)
 };
+
+// One row group's gather (the canonical chain per column, CSR order): lane q
+// accumulates its CH columns j0 + r * jstr + c.  H: the fp16 table (4 halves
+// = 8 bytes per lane and nnz and float4 group) -- the screening values s'.
+template <int CH, int UB, bool H>
+__device__ __forceinline__ void row_gather(float (&acc)[CH], const RowPassArgs &A, int2 *my_iv, int64_t s, int len,
+                                           int maxlen, int q, int j0, uint64_t pol_hot, uint64_t pol_cold) {
+#pragma unroll
+    for (int c = 0; c < CH; ++c) acc[c] = 0.f;
+    const float *ctj = A.ct + j0;
+    const __half *chj = A.ct16 + j0;
+    // Rows are staged 32 nnz at a time in shared memory (coalesced loads by
+    // the row's lanes); the term-major center rows are then gathered UB
+    // nnz at a time so UB * CH/4 independent loads are in flight.
+    for (int c0 = 0; c0 < maxlen; c0 += 32) {
+        const int cnt = max(0, min(32, len - c0));
+        for (int q2 = q; q2 < cnt; q2 += A.tpr)
+            my_iv[q2] = make_int2(__ldg(A.indices + s + c0 + q2), __float_as_int(__ldg(A.values + s + c0 + q2)));
+        __syncwarp();
+        int u = 0;
+        for (; u + UB <= cnt; u += UB) {
+            float vv[UB];
+            int iv[UB];
+            load_iv<UB>(my_iv + u, iv, vv);
+            if constexpr (H) {
+                uint2 hv[UB][CH / 4];
+#pragma unroll
+                for (int b = 0; b < UB; ++b) {
+                    const uint2 *p = reinterpret_cast<const uint2 *>(chj + (int64_t)iv[b] * A.kp);
+                    const uint64_t pol = iv[b] < A.hot ? pol_hot : pol_cold;
+#pragma unroll
+                    for (int r = 0; r < CH / 4; ++r) hv[b][r] = ldg_hint(p + r * A.tpr, pol);
+                }
+#pragma unroll
+                for (int b = 0; b < UB; ++b)
+#pragma unroll
+                    for (int r = 0; r < CH / 4; ++r) {
+                        const float4 cv = half4_to_float4(hv[b][r]);
+                        acc[4 * r + 0] = __fmaf_rn(vv[b], cv.x, acc[4 * r + 0]);
+                        acc[4 * r + 1] = __fmaf_rn(vv[b], cv.y, acc[4 * r + 1]);
+                        acc[4 * r + 2] = __fmaf_rn(vv[b], cv.z, acc[4 * r + 2]);
+                        acc[4 * r + 3] = __fmaf_rn(vv[b], cv.w, acc[4 * r + 3]);
+                    }
+            } else {
+                float4 cv[UB][CH / 4];
+#pragma unroll
+                for (int b = 0; b < UB; ++b) {
+                    const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)iv[b] * A.kp);
+                    const uint64_t pol = iv[b] < A.hot ? pol_hot : pol_cold;
+#pragma unroll
+                    for (int r = 0; r < CH / 4; ++r) cv[b][r] = ldg_hint(p + r * A.tpr, pol);
+                }
+#pragma unroll
+                for (int b = 0; b < UB; ++b)
+#pragma unroll
+                    for (int r = 0; r < CH / 4; ++r) {
+                        acc[4 * r + 0] = __fmaf_rn(vv[b], cv[b][r].x, acc[4 * r + 0]);
+                        acc[4 * r + 1] = __fmaf_rn(vv[b], cv[b][r].y, acc[4 * r + 1]);
+                        acc[4 * r + 2] = __fmaf_rn(vv[b], cv[b][r].z, acc[4 * r + 2]);
+                        acc[4 * r + 3] = __fmaf_rn(vv[b], cv[b][r].w, acc[4 * r + 3]);
+                    }
+            }
+        }
+        for (; u < cnt; ++u) {
+            const int2 t = my_iv[u];
+            const float v0 = __int_as_float(t.y);
+            const uint64_t pol = t.x < A.hot ? pol_hot : pol_cold;
+#pragma unroll
+            for (int r = 0; r < CH / 4; ++r) {
+                float4 cc4;
+                if constexpr (H)
+                    cc4 = half4_to_float4(ldg_hint(reinterpret_cast<const uint2 *>(chj + (int64_t)t.x * A.kp) + r * A.tpr, pol));
+                else
+                    cc4 = ldg_hint(reinterpret_cast<const float4 *>(ctj + (int64_t)t.x * A.kp) + r * A.tpr, pol);
+                acc[4 * r + 0] = __fmaf_rn(v0, cc4.x, acc[4 * r + 0]);
+                acc[4 * r + 1] = __fmaf_rn(v0, cc4.y, acc[4 * r + 1]);
+                acc[4 * r + 2] = __fmaf_rn(v0, cc4.z, acc[4 * r + 2]);
+                acc[4 * r + 3] = __fmaf_rn(v0, cc4.w, acc[4 * r + 3]);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// fp16 screening (k_row_pass<.., HALF>): candidates per row whose exact value
+// is re-checked on ct32; more in a row -> the warp re-gathers in fp32.
+constexpr int kCand = 8;
+// |s' - s~| <= E(m) for a row of m nnz: fp16 rounding of ct32 (2^-11
+// relative, 2^-25 absolute below the fp16 normal range: 2^-11 |x||c| +
+// 2^-25 |x|_1 <= 4.883e-4 + 2.98e-8 sqrt(m) for unit x, c) plus the two
+// float32 FMA chains (2 gamma_m <= 1.2e-7 m), with margin.
+__device__ __forceinline__ double screen_err(int m) { return 5.0e-4 + 1.3e-7 * m + 3.0e-8 * sqrt((double)m); }
 
 // Thread = (row, CH centers in float4 groups tpr apart).  tpr threads cover
 // one row's kp columns, rpw rows share a warp.  Per nnz: one broadcast (idx, val) load and
 // CH/4 float4 loads of the term-major center row; CH independent FMA chains.
 // CH <= 8: capped at 64 registers (4 CTAs of 256 per SM); CH >= 16 (k > 256):
 // uncapped, the CH accumulators and loads in flight need the registers.
-template <int CH, int NT>
+template <int CH, int NT, bool HALF>
 __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPassArgs A) {
     PDL_ENTRY();
     // nnz per gather batch: keep ~8 float4 loads in flight per lane
@@ -337,10 +441,18 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
     // gathers are latency-bound, so SPKM_UB_WIDE x 8 float4 loads in flight
     // (C4: 1, 2, 3, 4 -> 8.50, 9.40, 9.70, 9.84 it/s; profiles/r02_ab_notes.txt)
     constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 2 * SPKM_UB_WIDE : SPKM_UB_WIDE;
+#ifndef SPKM_UB_HALF_MUL
+#define SPKM_UB_HALF_MUL 2
+#endif
+    // fp16 gathers: the same registers hold twice the loads (8-byte vs 16-byte)
+    constexpr int UBH = HALF ? SPKM_UB_HALF_MUL * UB : UB;
     if (A.ctl[1]) return;   // converged: later enqueued iterations are no-ops
     extern __shared__ __align__(16) int2 s_iv[];   // per row group: kIvStride staged (id, value) pairs
     const int wpb = blockDim.x >> 5;
     __shared__ unsigned long long s_ctr[8];
+    __shared__ int s_cj[HALF ? NT / 32 : 1][8][kCand];     // fp16 screening: candidate columns per row group
+    __shared__ float s_cv[HALF ? NT / 32 : 1][8][kCand];   // and their exact values
+    __shared__ float s_cs[HALF ? NT / 32 : 1][1][HALF ? kCand * 32 : 1];   // recheck staging (HALF: k > 128, one row per warp)
     ctr_init(s_ctr);
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
     const int g = lane / A.tpr, q = lane - g * A.tpr;
@@ -365,59 +477,93 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPas
         const int j0 = q * 4;
         const int jstr = 4 * A.tpr;
         float acc[CH];
-#pragma unroll
-        for (int c = 0; c < CH; ++c) acc[c] = 0.f;
-        const float *ctj = A.ct + j0;
         const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
-        // Rows are staged 32 nnz at a time in shared memory (coalesced loads by
-        // the row's lanes); the term-major center rows are then gathered UB
-        // nnz at a time so UB * CH/4 independent float4 loads are in flight.
-        for (int c0 = 0; c0 < maxlen; c0 += 32) {
-            const int cnt = max(0, min(32, len - c0));
-            for (int q2 = q; q2 < cnt; q2 += A.tpr)
-                my_iv[q2] = make_int2(__ldg(A.indices + s + c0 + q2), __float_as_int(__ldg(A.values + s + c0 + q2)));
-            __syncwarp();
-            int u = 0;
-            for (; u + UB <= cnt; u += UB) {
-                float4 cv[UB][CH / 4];
-                float vv[UB];
-                int iv[UB];
-                load_iv<UB>(my_iv + u, iv, vv);
-#pragma unroll
-                for (int b = 0; b < UB; ++b) {
-                    const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)iv[b] * A.kp);
-                    const uint64_t pol = iv[b] < A.hot ? pol_hot : pol_cold;
-#pragma unroll
-                    for (int r = 0; r < CH / 4; ++r) cv[b][r] = ldg_hint(p + r * A.tpr, pol);
-                }
-#pragma unroll
-                for (int b = 0; b < UB; ++b)
-#pragma unroll
-                    for (int r = 0; r < CH / 4; ++r) {
-                        acc[4 * r + 0] = __fmaf_rn(vv[b], cv[b][r].x, acc[4 * r + 0]);
-                        acc[4 * r + 1] = __fmaf_rn(vv[b], cv[b][r].y, acc[4 * r + 1]);
-                        acc[4 * r + 2] = __fmaf_rn(vv[b], cv[b][r].z, acc[4 * r + 2]);
-                        acc[4 * r + 3] = __fmaf_rn(vv[b], cv[b][r].w, acc[4 * r + 3]);
-                    }
-            }
-            for (; u < cnt; ++u) {
-                const int2 t = my_iv[u];
-                const float v0 = __int_as_float(t.y);
-                const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)t.x * A.kp);
-                const uint64_t pol = t.x < A.hot ? pol_hot : pol_cold;
-#pragma unroll
-                for (int r = 0; r < CH / 4; ++r) {
-                    const float4 cc4 = ldg_hint(p + r * A.tpr, pol);
-                    acc[4 * r + 0] = __fmaf_rn(v0, cc4.x, acc[4 * r + 0]);
-                    acc[4 * r + 1] = __fmaf_rn(v0, cc4.y, acc[4 * r + 1]);
-                    acc[4 * r + 2] = __fmaf_rn(v0, cc4.z, acc[4 * r + 2]);
-                    acc[4 * r + 3] = __fmaf_rn(v0, cc4.w, acc[4 * r + 3]);
-                }
-            }
-            __syncwarp();
-        }
+        row_gather<CH, UBH, HALF>(acc, A, my_iv, s, len, maxlen, q, j0, pol_hot, pol_cold);
         const bool incumbent_mode = (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN);
         const int inc = (valid && incumbent_mode) ? A.a[row] : -1;
+        if constexpr (HALF) {
+            // acc holds the fp16-screened s'.  Candidates: s' >= max s' - 2E (the
+            // only centers that can be the best or tie it: any other j has
+            // s~_j <= s'_j + E < max - E <= s~ of the argmax of s') plus the
+            // incumbent.  Their exact canonical s~ comes from one chain each on
+            // ct32; every other acc becomes s' + E rounded up, an upper bound on
+            // its s~ strictly below the best -- so a, l, the tie rule and the
+            // tighten test are exact, and the second / u(i, j) / group bounds
+            // stay valid upper bounds.
+            float mx = -INFINITY;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int j = j0 + (c >> 2) * jstr + (c & 3);
+                if (j < A.k) mx = fmaxf(mx, acc[c]);
+            }
+            for (int o = o0; o; o >>= 1) {
+                const float ot = __shfl_down_sync(FULL, mx, o);
+                if (q < o && q + o < A.tpr) mx = fmaxf(mx, ot);
+            }
+            mx = __shfl_sync(FULL, mx, lane - q);
+            const double E = screen_err(len);
+            const float thr = __double2float_rd((double)mx - 2.0 * E);
+            const float Ef = __double2float_ru(E);
+            int cnt = 0;
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int j = j0 + (c >> 2) * jstr + (c & 3);
+                cnt += (valid && j < A.k && (acc[c] >= thr || j == inc)) ? 1 : 0;
+            }
+            int x = cnt;
+            for (int o = 1; o < A.tpr; o <<= 1) {
+                const int v = __shfl_up_sync(FULL, x, o);
+                if (q >= o) x += v;
+            }
+            const int tot = __shfl_sync(FULL, x, (lane - q + A.tpr - 1) & 31);
+            if (__any_sync(FULL, valid && tot > kCand)) {
+                // too many near-ties in some row of the warp: exact float32 gather
+                row_gather<CH, UB, false>(acc, A, my_iv, s, len, maxlen, q, j0, pol_hot, pol_cold);
+            } else {
+                int *cj = s_cj[wib][lane_on ? g : 0];
+                float *cvv = s_cv[wib][lane_on ? g : 0];
+                int pos = x - cnt;
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const int j = j0 + (c >> 2) * jstr + (c & 3);
+                    if (valid && j < A.k && (acc[c] >= thr || j == inc)) cj[pos++] = j;
+                }
+                __syncwarp();
+                // exact canonical chains of the candidates, 32 nnz at a time: the
+                // row's lanes fetch every (candidate, nnz) center value of the
+                // chunk at once (one round trip), then lane c < tot runs
+                // candidate c's FMA chain from shared memory in CSR order
+                float e = 0.f;
+                float *stage = s_cs[wib][lane_on ? g : 0];
+                const int mt = (int)__reduce_max_sync(FULL, (unsigned)(valid ? len : 0));
+                for (int c0 = 0; c0 < mt; c0 += 32) {
+                    const int cntc = valid ? max(0, min(32, len - c0)) : 0;
+                    for (int q2 = q; q2 < cntc; q2 += A.tpr) {
+                        const int id = __ldg(A.indices + s + c0 + q2);
+                        const float *rowp = A.ct + (int64_t)id * A.kp;
+                        for (int p = 0; p < tot; ++p) stage[p * 32 + q2] = __ldg(rowp + cj[p]);
+                    }
+                    __syncwarp();
+                    if (valid && q < tot)
+                        for (int t = 0; t < cntc; ++t) e = __fmaf_rn(__ldg(A.values + s + c0 + t), stage[q * 32 + t], e);
+                    __syncwarp();
+                }
+                if (valid && q < tot) cvv[q] = e;
+                __syncwarp();
+#pragma unroll
+                for (int c = 0; c < CH; ++c) {
+                    const int j = j0 + (c >> 2) * jstr + (c & 3);
+                    if (!valid || j >= A.k) continue;
+                    if (acc[c] >= thr || j == inc) {
+                        for (int p = 0; p < tot; ++p)
+                            if (cj[p] == j) acc[c] = cvv[p];
+                    } else {
+                        acc[c] = __fadd_ru(acc[c], Ef);
+                    }
+                }
+                __syncwarp();
+            }
+        }
         Top2 tp{-INFINITY, -2, -INFINITY};
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
@@ -1796,7 +1942,7 @@ __global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int
                                                       const int32_t *__restrict__ tlist,
                                                       const int32_t *__restrict__ tcount, double inv_scale,
                                                       const double *__restrict__ norm, double *cent64, float *ct32,
-                                                      double *part, const long long *__restrict__ ctl) {
+                                                      __half *ct16, double *part, const long long *__restrict__ ctl) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ float tile[kTileT][kTileJ + 1];
@@ -1868,7 +2014,11 @@ __global__ void __launch_bounds__(256) k_center_write(int64_t d, int64_t kp, int
     const int j = js[lane];
     for (int q = w; q < kTileT; q += 8) {
         const int64_t t = t0 + q;
-        if (t < d && j >= 0) ct32[t * kp + j] = tile[q][lane];
+        if (t < d && j >= 0) {
+            const float f = tile[q][lane];
+            ct32[t * kp + j] = f;
+            if (ct16) ct16[t * kp + j] = __float2half_rn(f);
+        }
     }
 }
 
@@ -1999,7 +2149,7 @@ __global__ void k_loop_cond(cudaGraphConditionalHandle h, const long long *ctl, 
 __global__ void k_seed_rows_csr(int64_t d, int64_t kp, const int64_t *__restrict__ indptr,
                                 const int32_t *__restrict__ indices, const double *__restrict__ v64,
                                 const int64_t *__restrict__ row_dev, const int64_t *__restrict__ rows,
-                                double *cent64, float *ct32) {
+                                double *cent64, float *ct32, __half *ct16) {
     PDL_ENTRY();
     const int64_t j = blockIdx.x;
     const int64_t r = row_dev[rows[j]];
@@ -2008,6 +2158,7 @@ __global__ void k_seed_rows_csr(int64_t d, int64_t kp, const int64_t *__restrict
         const double v = v64[e];
         cent64[j * d + c] = v;
         ct32[(int64_t)c * kp + j] = (float)v;
+        if (ct16) ct16[(int64_t)c * kp + j] = __float2half_rn((float)v);
     }
 }
 
@@ -2824,25 +2975,27 @@ __global__ void k_gather_rows(const float *__restrict__ x, int64_t D, const int3
 
 // ---------------------------------------------------------------- misc
 __global__ void k_load_centers(int64_t k, int64_t d, int64_t kp, const double *__restrict__ src, double *cent64,
-                               float *ct32) {
+                               float *ct32, __half *ct16) {
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= k * d) return;
     const int64_t j = e / d, t = e % d;
     const double v = src[e];
     cent64[e] = v;
     ct32[t * kp + j] = (float)v;
+    if (ct16) ct16[t * kp + j] = __float2half_rn((float)v);
 }
 
 // CentroidSet.from_data_rows (engine.py:46-58) on the device: k packed seed
 // rows (float64 values) scattered into zeroed cent64 / ct32.
 __global__ void k_seed_rows(int64_t d, int64_t kp, const int64_t *__restrict__ sptr, const int32_t *__restrict__ sidx,
-                            const double *__restrict__ sval, double *cent64, float *ct32) {
+                            const double *__restrict__ sval, double *cent64, float *ct32, __half *ct16) {
     const int64_t j = blockIdx.x;
     for (int64_t t = sptr[j] + threadIdx.x; t < sptr[j + 1]; t += blockDim.x) {
         const int c = sidx[t];
         const double v = sval[t];
         cent64[j * d + c] = v;
         ct32[(int64_t)c * kp + j] = (float)v;
+        if (ct16) ct16[(int64_t)c * kp + j] = __float2half_rn((float)v);
     }
 }
 
@@ -2882,9 +3035,9 @@ int grid_for(int64_t work_items, int per_block) {
     return (int)(g < 1 ? 1 : g);
 }
 
-template <int CH, int NT>
+template <int CH, int NT, bool HALF>
 int launch_rp(RowPassArgs &A, int grid, size_t smem, cudaStream_t st) {
-    pdl_launch(k_row_pass<CH, NT>, dim3(grid), dim3(NT), smem, st, A);
+    pdl_launch(k_row_pass<CH, NT, HALF>, dim3(grid), dim3(NT), smem, st, A);
     CHECK_LAUNCH("row_pass");
     return 0;
 }
@@ -2900,10 +3053,13 @@ int launch_row_pass(RowPassArgs &A, int64_t k, cudaStream_t st, int64_t max_rows
     const int64_t slots = (max_rows + p.rpw - 1) / p.rpw;
     const int grid = grid_for(slots, 8);
     const size_t smem = (size_t)(256 / 32) * 8 * kIvStride * 8;
-    if (p.ch == 4) return launch_rp<4, 256>(A, grid, smem, st);
-    if (p.ch == 8) return launch_rp<8, 256>(A, grid, smem, st);
-    if (p.ch == 16) return launch_rp<16, 256>(A, grid, smem, st);
-    return launch_rp<32, 256>(A, grid, smem, st);
+    // fp16 screening for every full pass but predict, when the table exists (k > 128)
+    const bool half = A.ct16 != nullptr && A.mode != MODE_PREDICT && p.ch >= 8;
+    if (p.ch == 4) return launch_rp<4, 256, false>(A, grid, smem, st);
+    if (p.ch == 8) return half ? launch_rp<8, 256, true>(A, grid, smem, st) : launch_rp<8, 256, false>(A, grid, smem, st);
+    if (p.ch == 16)
+        return half ? launch_rp<16, 256, true>(A, grid, smem, st) : launch_rp<16, 256, false>(A, grid, smem, st);
+    return half ? launch_rp<32, 256, true>(A, grid, smem, st) : launch_rp<32, 256, false>(A, grid, smem, st);
 }
 
 // Term rows of the Zipf head kept in L2 by the gathers' eviction hints:
@@ -2929,6 +3085,7 @@ RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     A.ct = C->ct32;
     A.kp = C->kp;
     A.hot = hot_terms(C);
+    A.ct16 = reinterpret_cast<const __half *>(C->ct16);
     return A;
 }
 
@@ -3534,7 +3691,8 @@ int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
     pdl_launch(k_center_norm_final, dim3((unsigned)C->k), dim3(256), (size_t)(0), st, nch, C->counts, C->tlist, C->tcount, C->part, C->norm, C->ctl);
     CHECK_LAUNCH("center_norm_final");
     pdl_launch(k_center_write, dim3(dim3((unsigned)ntile, (unsigned)((C->k + kTileJ - 1) / kTileJ))), dim3(256), (size_t)(0), st, 
-        C->d, C->kp, ntile, C->sums, C->tlist, C->tcount, inv, C->norm, C->cent64, C->ct32, C->part, C->ctl);
+        C->d, C->kp, ntile, C->sums, C->tlist, C->tcount, inv, C->norm, C->cent64, C->ct32,
+        reinterpret_cast<__half *>(C->ct16), C->part, C->ctl);
     CHECK_LAUNCH("center_write");
     return defer_reduce ? 0 : spkm_center_reduce(C, stream);
 }
@@ -3726,7 +3884,7 @@ int spkm_objective(const spkm_centers *C, const long long *sums, double *out, vo
 int spkm_load_centers(const spkm_centers *C, const double *src, void *stream) {
     const int64_t tot = C->k * C->d;
     k_load_centers<<<(unsigned)((tot + 255) / 256), 256, 0, S(stream)>>>(C->k, C->d, C->kp, src, C->cent64,
-                                                                         C->ct32);
+                                                                         C->ct32, reinterpret_cast<__half *>(C->ct16));
     CHECK_LAUNCH("load_centers");
     return 0;
 }
@@ -3736,8 +3894,10 @@ int spkm_seed_rows(const spkm_centers *C, const int64_t *sptr, const int32_t *si
     cudaStream_t st = S(stream);
     cudaError_t e = cudaMemsetAsync(C->cent64, 0, sizeof(double) * C->k * C->d, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(C->ct32, 0, sizeof(float) * C->kp * C->d, st);
+    if (e == cudaSuccess && C->ct16) e = cudaMemsetAsync(C->ct16, 0, sizeof(uint16_t) * C->kp * C->d, st);
     if (e != cudaSuccess) return fail("seed_rows memset", e);
-    k_seed_rows<<<(unsigned)C->k, 128, 0, st>>>(C->d, C->kp, sptr, sidx, sval, C->cent64, C->ct32);
+    k_seed_rows<<<(unsigned)C->k, 128, 0, st>>>(C->d, C->kp, sptr, sidx, sval, C->cent64, C->ct32,
+                                                reinterpret_cast<__half *>(C->ct16));
     CHECK_LAUNCH("seed_rows");
     return 0;
 }
@@ -3857,9 +4017,10 @@ int spkm_seed_rows_csr(const spkm_centers *C, const spkm_seed *Sd, const int64_t
     cudaStream_t st = S(stream);
     cudaError_t e = cudaMemsetAsync(C->cent64, 0, sizeof(double) * C->k * C->d, st);
     if (e == cudaSuccess) e = cudaMemsetAsync(C->ct32, 0, sizeof(float) * C->kp * C->d, st);
+    if (e == cudaSuccess && C->ct16) e = cudaMemsetAsync(C->ct16, 0, sizeof(uint16_t) * C->kp * C->d, st);
     if (e != cudaSuccess) return fail("seed_rows_csr memset", e);
     pdl_launch(k_seed_rows_csr, dim3((unsigned)C->k), dim3(128), (size_t)(0), st, C->d, C->kp, Sd->indptr, Sd->indices, Sd->values, Sd->row_dev,
-                                                     rows, C->cent64, C->ct32);
+                                                     rows, C->cent64, C->ct32, reinterpret_cast<__half *>(C->ct16));
     CHECK_LAUNCH("seed_rows_csr");
     return 0;
 }

@@ -504,6 +504,10 @@ class CenterState:
         # + 1024 floats: the row pass's last lanes read whole float4 groups past kp on the last term row
         self.ct32_buf = torch.zeros(d * self.kp + 1024, dtype=torch.float32, device=dev)
         self.ct32 = self.ct32_buf[:d * self.kp]
+        # fp16 copy for the screening full pass (k > 128; SPKM_CT16=0 turns it off)
+        env = os.environ.get("SPKM_CT16")
+        use16 = (k > 128) if env is None else env != "0"
+        self.ct16_buf = torch.zeros(d * self.kp + 1024, dtype=torch.float16, device=dev) if use16 else None
         self.sums = torch.empty(k * d, dtype=torch.int64, device=dev)
         self.counts = torch.zeros(k, dtype=torch.int64, device=dev)
         self.drift = torch.ones(k, **f64)
@@ -529,7 +533,7 @@ class CenterState:
                               _ptr(self.sums), _ptr(self.counts), _ptr(self.drift), _ptr(self.sinp),
                               _ptr(self.touched), _ptr(self.objc), _ptr(self.part), _ptr(self.norm), _ptr(self.cc),
                               _ptr(self.s), _ptr(self.hstat), _ptr(self.tlist), _ptr(self.tcount),
-                              _ptr(self.ctl))
+                              _ptr(self.ctl), _ptr(self.ct16_buf))
         self.cc_valid = False
 
     def load(self, centers, stream):

@@ -49,7 +49,7 @@ int main(void) {
   printf("spkm_csr %zu\nspkm_centers %zu\nspkm_bounds %zu\nspkm_work %zu\n", sizeof(spkm_csr),
          sizeof(spkm_centers), sizeof(spkm_bounds), sizeof(spkm_work));
   P(spkm_csr, row_eps) P(spkm_centers, scale_bits) P(spkm_centers, hstat) P(spkm_centers, cc)
-  P(spkm_bounds, ku) P(spkm_work, stats)
+  P(spkm_bounds, ku) P(spkm_work, stats) P(spkm_centers, ct16)
   return 0;
 }
 '''
@@ -69,6 +69,7 @@ int main(void) {
     assert int(lines["spkm_centers.hstat"]) == _lib.Centers.hstat.offset
     assert int(lines["spkm_centers.cc"]) == _lib.Centers.cc.offset
     assert int(lines["spkm_bounds.ku"]) == _lib.Bounds.ku.offset
+    assert int(lines["spkm_centers.ct16"]) == _lib.Centers.ct16.offset
     assert int(lines["spkm_work.stats"]) == _lib.Work.stats.offset
 
 

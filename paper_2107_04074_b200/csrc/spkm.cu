@@ -1056,7 +1056,10 @@ __host__ __device__ __forceinline__ int64_t elkan_sim_stride(int64_t k) {
 // same lanes that later test and scan them), so the bound pass, its survivor
 // list and one read of u are saved; rows that survive go straight on.
 template <int EB, bool FUSE>
-__global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ indptr,
+#ifndef SPKM_EK_MINB
+#define SPKM_EK_MINB 3
+#endif
+__global__ void __launch_bounds__(256, SPKM_EK_MINB) k_elkan_scan(const int64_t *__restrict__ indptr,
                                                     const int32_t *__restrict__ indices,
                                                     const float *__restrict__ values,
                                                     const float *__restrict__ reps,
@@ -1078,7 +1081,9 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     // nnz per gather batch: 8 * SPKM_EK_UB float4 loads in flight per lane
     constexpr int UB = SPKM_EK_UB * 32 / EB;
     constexpr int ES = EB + 1;    // padded per-block stride of the similarity buffer
-    __shared__ __align__(16) int2 s_iv[8][8][kIvStride];
+    // staged (id, value) pairs live in dynamic shared memory after the
+    // similarity buffers: ppw row groups per warp (k > 128: one), not 8
+
     __shared__ int s_act[8][EB == 4 ? 256 : 128];   // per warp: the groups' active block lists (ppw * nb <= 256 / 128)
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
@@ -1094,7 +1099,7 @@ __global__ void __launch_bounds__(256) k_elkan_scan(const int64_t *__restrict__ 
     const int sim_stride = (int)elkan_sim_stride(k);  // floats per warp
     const int gstride = sim_stride / ppw;             // per-group slice (>= ES * nb)
     float *my_sim = s_sim_dyn + wib * sim_stride + (lane_on ? g : 0) * gstride;
-    int2 *my_iv = s_iv[wib][lane_on ? g : 0];
+    int2 *my_iv = reinterpret_cast<int2 *>(s_sim_dyn + 8 * sim_stride) + (wib * ppw + (lane_on ? g : 0)) * kIvStride;
     const long long cnt = FUSE ? n_rows : ctr[SPKM_CTR_SURV1];
     const int64_t nslots = (cnt + ppw - 1) / ppw;
     const int wpb = blockDim.x >> 5;
@@ -3561,7 +3566,9 @@ static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_boun
     if (X->n == 0) return 0;
     if (C->k > 1024) return fail_msg("elkan_scan: k > 1024 not supported by this build");
     const int grid = grid_for(X->n, 8);
-    const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float);
+    const int64_t eb = elkan_block(C->k), nbk = (C->k + eb - 1) / eb;
+    const int64_t ppw_k = (32 / (nbk < 32 ? nbk : 32)) < 8 ? (32 / (nbk < 32 ? nbk : 32)) : 8;
+    const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float) + (size_t)8 * ppw_k * kIvStride * sizeof(int2);
     cudaError_t attr = cudaSuccess;
     auto launch = [&](auto kern) {
         // static smem (staging + active lists) + dyn must fit the opt-in
@@ -3679,7 +3686,10 @@ int spkm_move_centers(const spkm_centers *C, int all_clusters, void *stream) {
     const double inv = ldexp(1.0, -C->scale_bits);
     const bool defer_reduce = (all_clusters & 4) != 0;   // spkm_center_reduce is issued separately
     all_clusters &= 1;
-    const int build = C->k <= kListInline;
+    // the norm-part CTAs build the touched list themselves only while the
+    // grid is small: each of the nch x k CTAs scans all k flags (C4: 245k
+    // CTAs x 1000 flags, 73% issue-bound) -- else one k_touched_list launch
+    const int build = C->k <= kListInline && nch * C->k <= 65536;
     if (!build) {
         pdl_launch(k_touched_list, dim3(1), dim3(1024), (size_t)(0), st, C->k, C->touched, all_clusters, C->tlist,
                    C->tcount, C->ctl);

@@ -504,9 +504,10 @@ class CenterState:
         # + 1024 floats: the row pass's last lanes read whole float4 groups past kp on the last term row
         self.ct32_buf = torch.zeros(d * self.kp + 1024, dtype=torch.float32, device=dev)
         self.ct32 = self.ct32_buf[:d * self.kp]
-        # fp16 copy for the screening full pass (k > 128; SPKM_CT16=0 turns it off)
-        env = os.environ.get("SPKM_CT16")
-        use16 = (k > 128) if env is None else env != "0"
+        # fp16 copy for the screening full pass: off unless SPKM_CT16=1 -- measured
+        # slower at C4 and C3 (the gathers are not limited by their bytes;
+        # profiles/r02_ab_notes.txt), kept tested as an option
+        use16 = k > 128 and os.environ.get("SPKM_CT16") == "1"
         self.ct16_buf = torch.zeros(d * self.kp + 1024, dtype=torch.float16, device=dev) if use16 else None
         self.sums = torch.empty(k * d, dtype=torch.int64, device=dev)
         self.counts = torch.zeros(k, dtype=torch.int64, device=dev)

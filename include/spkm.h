@@ -361,6 +361,10 @@ int spkm_permute_rows(int64_t n, const int64_t *ip_raw, const int32_t *idx_raw, 
  * perm = NULL skips the row part.  Scratch: spkm_prepare_scratch_bytes(n, d)
  * bytes (-1: n or d >= 2^31). */
 int64_t spkm_prepare_scratch_bytes(int64_t n, int64_t d);
+/* Dense corpora (every row holds the D terms in order): idx[r*D + t] = t,
+ * indptr[r] = r*D (n+1 entries), perm[r] = r (the stable length order is the
+ * identity); indptr / perm may be NULL. */
+int spkm_dense_ids(int64_t n, int64_t D, int32_t *idx, int64_t *indptr, int64_t *perm, void *stream);
 int spkm_prepare_rows(int64_t n, int64_t d, int64_t nnz, const int64_t *ip_raw, const int32_t *idx_raw,
                       int64_t *perm, int64_t *pos, int64_t *indptr, int64_t *order, int64_t *new_id,
                       void *scratch, int64_t scratch_bytes, void *stream);

@@ -77,3 +77,15 @@ PrepPlan prep_plan(int64_t n, int64_t d) {
     p.total = p.rows_key + p.rows_val + p.rows_tmp + p.rows_lens + p.terms_key + p.terms_val + p.terms_tmp;
     return p;
 }
+
+// dense corpora (every row holds the D terms 0..D-1): the device term ids,
+// the row offsets r * D and the (identity) row order
+__global__ void k_dense_ids(int64_t n, int64_t D, int32_t *idx, int64_t *indptr, int64_t *perm) {
+    const int64_t tot = n * D;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < tot; i += stride) idx[i] = (int32_t)(i % D);
+    for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r <= n; r += stride) {
+        if (indptr) indptr[r] = r * D;
+        if (perm && r < n) perm[r] = r;
+    }
+}

@@ -344,6 +344,8 @@ class DeviceCorpus:
         # a dense corpus (Dataset.from_dense) has the term ids 0..D-1 in every
         # row: they are generated on the device instead of uploaded
         dense_ids = self.dense_dim is not None and getattr(data, "dense_dim", None) == self.dense_dim
+        if dense_ids and getattr(data, "_values32", None) is not None:
+            return self._device_prepare_dense(data, data._values32, sp)
         if self.pinned_host and (r0, r1) == (0, data.n):
             # the whole corpus: page-lock the Dataset's own arrays once and copy
             # straight from them (no staging copy on the host)
@@ -374,7 +376,9 @@ class DeviceCorpus:
         up.wait_stream(stream)
         with torch.cuda.stream(up):
             if idx_h is None:
-                idx_raw = torch.arange(self.dense_dim, dtype=torch.int32, device=dev).repeat(r1 - r0)
+                idx_raw = torch.empty((r1 - r0) * self.dense_dim, dtype=torch.int32, device=dev)
+                _lib.call("spkm_dense_ids", r1 - r0, self.dense_dim, _ptr(idx_raw), None, None,
+                          ctypes_void(up.cuda_stream))
             else:
                 idx_raw = idx_h.to(dev, non_blocking=True)
             val_raw = val_h.to(dev, non_blocking=True)
@@ -437,6 +441,39 @@ class DeviceCorpus:
         if self._seed is not None:          # refresh: the seeding maps follow the new rows (pos written above)
             self._seed[2].copy_(perm)
         del ip_raw, idx_raw, val_raw        # stream-ordered frees (caching allocator)
+
+    def _device_prepare_dense(self, data: Dataset, v32: np.ndarray, sp):
+        """Dense rows (Dataset.dense keeps a float32 copy of its normalised
+        rows): every row holds the D terms in order, so the stable length
+        order and the document-frequency term order are the identity -- the
+        float32 values go H2D straight into the device buffer (half the bytes
+        of the float64 rows), term ids, offsets and row order are generated
+        (spkm_dense_ids); nothing is permuted."""
+        r0, r1 = self.rows
+        D, dev, n = self.dense_dim, self.device, r1 - r0
+        src = v32[r0 * D:r1 * D]
+        h = torch.from_numpy(_host_registered(v32) if (r0, r1) == (0, data.n) else np.ascontiguousarray(src))
+        if (r0, r1) == (0, data.n):
+            h = h[r0 * D:r1 * D]
+        if self.pinned_host and not h.is_pinned():
+            if self._stage is None or self._stage[0] is None or self._stage[0].shape != h.shape:
+                self._stage = [torch.empty(h.shape, dtype=h.dtype).pin_memory(), None, None]
+            self._stage[0].copy_(h)
+            h = self._stage[0]
+        self.values[:n * D].copy_(h, non_blocking=True)
+        perm = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
+        _lib.call("spkm_dense_ids", n, D, _ptr(self.indices), _ptr(self.indptr), _ptr(perm), sp)
+        self.reps.fill_(float(row_eps_dense(D, 1)[0]))
+        ident = np.arange(self.d, dtype=np.int64)
+        if getattr(data, "_term_order", None) is None and (r0, r1) == (0, data.n):
+            data._term_order = (ident, ident.copy())
+        self.order, self.new_id = term_order(data) if (r0, r1) != (0, data.n) else data._term_order
+        self.h2d_bytes = int(src.nbytes)
+        self.perm_dev = perm
+        self._row_perm = self._row_pos = None
+        if self._seed is not None:
+            self._seed[2].copy_(perm)
+            self._seed[3].copy_(perm)          # identity: position == row
 
     def refresh(self, data: Dataset):
         """Upload new rows of the same shape (n, nnz, d) into the same device

@@ -242,6 +242,9 @@ class Dataset:
         indices = np.tile(np.arange(d, dtype=np.int32), n)
         ds = cls(indptr, indices, data.reshape(-1), d)
         ds.dense_dim = d
+        # float32 copy (round to nearest, what the device computes on): the
+        # upload moves it instead of the float64 rows
+        ds._values32 = ds.data.astype(np.float32)
         return ds
 
     # -- reference-compatible views ----------------------------------------

@@ -237,6 +237,7 @@ def config_dataset(name: str, seed: int | None = None, n_override: int | None = 
             ds = Dataset(ip, ix, dv, int(meta[0]))
             if int(meta[1]) > 0:
                 ds.dense_dim = int(meta[1])
+                ds._values32 = ds.data.astype(np.float32)     # as Dataset.dense keeps it
             return ds
         ds = config_dataset(name, seed, n_override, cache_dir="", row_norms=row_norms)
         base.parent.mkdir(parents=True, exist_ok=True)

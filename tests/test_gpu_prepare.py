@@ -84,3 +84,24 @@ def test_device_corpus_layout_equals_host_layout():
         assert torch.equal(a, getattr(cpu, name)), name
     assert np.array_equal(gpu.new_id, cpu.new_id) and np.array_equal(gpu.order, cpu.order)
     assert np.array_equal(gpu.row_perm, cpu.row_perm)
+
+
+def test_dense_corpus_float32_upload_equals_host_layout():
+    """Dense corpora upload their float32 rows (Dataset.dense keeps them) straight into the device
+    buffer; the layout equals the float64-upload path's and the host layout's."""
+    from paper_2107_04074_b200 import synth
+    from paper_2107_04074_b200.engine import DeviceCorpus
+    data = synth.config_dataset("C5", n_override=3000, cache_dir="")
+    assert data._values32.dtype == np.float32
+    fast = DeviceCorpus(data, "cuda:0")
+    slow_data = type(data)(data.indptr, data.indices, data.data, data.dim)
+    slow_data.dense_dim = data.dense_dim                 # no _values32: the float64 path
+    slow = DeviceCorpus(slow_data, "cuda:0")
+    cpu = DeviceCorpus(type(data)(data.indptr, data.indices, data.data, data.dim), "cpu")
+    for name in ("indptr", "indices", "values", "reps"):
+        a = getattr(fast, name)[: getattr(slow, name).numel()].cpu()
+        assert torch.equal(a, getattr(slow, name).cpu()), name
+    for name in ("indptr", "indices", "values"):
+        assert torch.equal(getattr(fast, name)[: getattr(cpu, name).numel()].cpu(), getattr(cpu, name)), name
+    assert fast.h2d_bytes * 2 <= slow.h2d_bytes
+    assert np.array_equal(fast.row_perm, np.arange(data.n))

@@ -430,8 +430,11 @@ __device__ __forceinline__ double screen_err(int m) { return 5.0e-4 + 1.3e-7 * m
 // CH/4 float4 loads of the term-major center row; CH independent FMA chains.
 // CH <= 8: capped at 64 registers (4 CTAs of 256 per SM); CH >= 16 (k > 256):
 // uncapped, the CH accumulators and loads in flight need the registers.
+#ifndef SPKM_RP_MINB
+#define SPKM_RP_MINB 1
+#endif
 template <int CH, int NT, bool HALF>
-__global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : 1) k_row_pass(RowPassArgs A) {
+__global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : SPKM_RP_MINB) k_row_pass(RowPassArgs A) {
     PDL_ENTRY();
     // nnz per gather batch: keep ~8 float4 loads in flight per lane
 #ifndef SPKM_UB_WIDE
@@ -1057,9 +1060,12 @@ __host__ __device__ __forceinline__ int64_t elkan_sim_stride(int64_t k) {
 // list and one read of u are saved; rows that survive go straight on.
 template <int EB, bool FUSE>
 #ifndef SPKM_EK_MINB
-#define SPKM_EK_MINB 4        // 64 registers, 4 CTAs per SM (C4 scan 3590 -> 3350 ms per fit)
+#define SPKM_EK_MINB 4        // EB = 8 (k > 128): 64 registers, 4 CTAs per SM (C4 scan 3590 -> 3350 ms per fit)
 #endif
-__global__ void __launch_bounds__(256, SPKM_EK_MINB) k_elkan_scan(const int64_t *__restrict__ indptr,
+#ifndef SPKM_EK4_MINB
+#define SPKM_EK4_MINB 3       // EB = 4 (k <= 128): <= 85 registers, the occupancy of the r01 build
+#endif
+__global__ void __launch_bounds__(256, EB == 8 ? SPKM_EK_MINB : SPKM_EK4_MINB) k_elkan_scan(const int64_t *__restrict__ indptr,
                                                     const int32_t *__restrict__ indices,
                                                     const float *__restrict__ values,
                                                     const float *__restrict__ reps,
@@ -1552,7 +1558,7 @@ __host__ __device__ __forceinline__ int yy_sim_stride(int64_t k) {
 // Survivor scan: lanes = groups (bpr lanes per point, up to 8 points per
 // warp, rounds of 32 groups), the gather machinery of k_elkan_scan<4>.
 #ifndef SPKM_YY_MINB
-#define SPKM_YY_MINB 1
+#define SPKM_YY_MINB 4        // 64 registers (C4 yy_scan 2492 -> 2423 ms per fit)
 #endif
 __global__ void __launch_bounds__(256, SPKM_YY_MINB) k_yy_scan(const int64_t *__restrict__ indptr,
                                                  const int32_t *__restrict__ indices,

@@ -255,8 +255,12 @@ def kernels_for(name: str, args) -> int:
     if name == "spkm_move_centers" and len(args) > 1:
         if int(args[1]) & 4:
             n -= 1                               # the reduction is issued by spkm_center_reduce
-        if getattr(args[0], "k", 1 << 30) <= 2048:
+        k, d = getattr(args[0], "k", 1 << 30), getattr(args[0], "d", 1 << 30)
+        if k <= 2048 and (d + 4095) // 4096 * k <= 65536:
             n -= 1                               # the touched list is built inside the norm pass
+    if name == "spkm_prepare_rows" and len(args) > 8:
+        # rows: keys, 1 + 4 radix-sort passes, lengths, 2 scan kernels; terms: df, iota, 1 + 4, inverse
+        n = (9 if args[5] is not None else 0) + (8 if args[8] is not None else 0)
     return n
 
 

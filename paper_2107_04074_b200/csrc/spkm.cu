@@ -431,19 +431,19 @@ __device__ __forceinline__ double screen_err(int m) { return 5.0e-4 + 1.3e-7 * m
 // CH <= 8: capped at 64 registers (4 CTAs of 256 per SM); CH >= 16 (k > 256):
 // uncapped, the CH accumulators and loads in flight need the registers.
 #ifndef SPKM_RP_MINB
-#define SPKM_RP_MINB 1
+#define SPKM_RP_MINB 2        // k > 256: 128 registers, 2 CTAs per SM with UB 3 (C4 rescan 3336 -> 3281 ms per fit)
 #endif
 template <int CH, int NT, bool HALF>
-__global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : SPKM_RP_MINB) k_row_pass(RowPassArgs A) {
+__global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : CH == 32 ? SPKM_RP_MINB : 1) k_row_pass(RowPassArgs A) {
     PDL_ENTRY();
     // nnz per gather batch: keep ~8 float4 loads in flight per lane
 #ifndef SPKM_UB_WIDE
-#define SPKM_UB_WIDE 4
+#define SPKM_UB_WIDE 3
 #endif
     // CH >= 16 (k > 256, one row per warp, one CTA per SM by registers): the
     // gathers are latency-bound, so SPKM_UB_WIDE x 8 float4 loads in flight
     // (C4: 1, 2, 3, 4 -> 8.50, 9.40, 9.70, 9.84 it/s; profiles/r02_ab_notes.txt)
-    constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 2 * SPKM_UB_WIDE : SPKM_UB_WIDE;
+    constexpr int UB = CH == 4 ? 8 : CH == 8 ? 4 : CH == 16 ? 8 : SPKM_UB_WIDE;
 #ifndef SPKM_UB_HALF_MUL
 #define SPKM_UB_HALF_MUL 2
 #endif
@@ -1063,9 +1063,9 @@ template <int EB, bool FUSE>
 #define SPKM_EK_MINB 4        // EB = 8 (k > 128): 64 registers, 4 CTAs per SM (C4 scan 3590 -> 3350 ms per fit)
 #endif
 #ifndef SPKM_EK4_MINB
-#define SPKM_EK4_MINB 3       // EB = 4 (k <= 128): <= 85 registers, the occupancy of the r01 build
+#define SPKM_EK4_MINB 3       // EB = 4 unfused: <= 85 registers (fused and EB = 8: SPKM_EK_MINB), as the r01 build
 #endif
-__global__ void __launch_bounds__(256, EB == 8 ? SPKM_EK_MINB : SPKM_EK4_MINB) k_elkan_scan(const int64_t *__restrict__ indptr,
+__global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_EK4_MINB) k_elkan_scan(const int64_t *__restrict__ indptr,
                                                     const int32_t *__restrict__ indices,
                                                     const float *__restrict__ values,
                                                     const float *__restrict__ reps,
@@ -1090,7 +1090,7 @@ __global__ void __launch_bounds__(256, EB == 8 ? SPKM_EK_MINB : SPKM_EK4_MINB) k
     // staged (id, value) pairs live in dynamic shared memory after the
     // similarity buffers: ppw row groups per warp (k > 128: one), not 8
 
-    __shared__ int s_act[8][EB == 4 ? 256 : 128];   // per warp: the groups' active block lists (ppw * nb <= 256 / 128)
+    __shared__ int s_act[8][EB == 4 && SPKM_EK_EB4_MAXK > 128 ? 256 : 128];   // per warp: the groups' active block lists
     __shared__ unsigned long long s_ctr[8];
     ctr_init(s_ctr);
     extern __shared__ float s_sim_dyn[];   // [8 warps][sim_stride]

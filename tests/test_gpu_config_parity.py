@@ -65,8 +65,8 @@ def _check_same(r, base, v):
 
 
 @pytest.mark.parametrize("name,variants", [
-    ("C3", VARIANTS),                                   # n = 500k, d = 250k, k = 200: full size
-    ("C4s", VARIANTS),                                  # C4 generator at n = 250k, d = 1M, k = 1000
+    ("C3", VARIANTS + ("yinyang",)),                    # n = 500k, d = 250k, k = 200: full size
+    ("C4s", VARIANTS + ("yinyang",)),                   # C4 generator at n = 250k, d = 1M, k = 1000
     ("C5s", VARIANTS),      # dense C5 at n = 100k, k = 1000 (tensor cores; the Elkan family on the sparse kernels)
 ])
 def test_config_parity_vs_oracle(name, variants):
@@ -100,7 +100,7 @@ def test_c4_full_size_pruned_equal_lloyd():
     diff = a != base.assignments
     assert np.all(best[diff] == second[diff]), int(np.sum(diff & (best != second)))
     assert abs(float(np.sum(best)) - base.objective) <= 1e-5 * base.objective
-    for v in ("hamerly", "simp_elkan"):
+    for v in ("hamerly", "simp_elkan", "yinyang"):
         r = spk.run(ds, 1000, v, spk.SeedConfig(seed=2), max_iter=50)
         _check_same(r, base, v)
         pruned = 1.0 - sum(s.sim_count for s in r.iterations[1:]) / max(1, (len(r.iterations) - 1) * ds.n * 1000)

@@ -216,6 +216,21 @@ def build(verbose: bool = False) -> Path:
     return LIB_PATH
 
 
+CHECK_LIB_PATH = PKG / "libspkm_check.so"
+
+
+def build_check(verbose: bool = False) -> Path:
+    """The debug build with device-side bounds checks (-DSPKM_CHECKS=1): same
+    ABI, loaded with SPKM_LIB=libspkm_check.so by tests/test_gpu_checks.py."""
+    nvcc = os.environ.get("NVCC", "nvcc")
+    cmd = [nvcc, *NVCC_FLAGS, "-DSPKM_CHECKS=1", "-I", str(ROOT / "include"), "-o", str(CHECK_LIB_PATH), str(SRC),
+           str(SRC_HOST)]
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise DeviceError(f"nvcc failed:\n{r.stderr[-4000:]}")
+    return CHECK_LIB_PATH
+
+
 def exported_symbols() -> list:
     return sorted(_SIGS)
 

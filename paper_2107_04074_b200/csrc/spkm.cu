@@ -45,6 +45,26 @@
 
 #define FULL 0xffffffffu
 
+// Debug build (-DSPKM_CHECKS=1, libspkm_check.so, tests/test_gpu_checks.py):
+// device-side bounds checks on the indices the kernels trust, trapping with a
+// message.  The pool has no compute-sanitizer; these checks
+// and the bit-exact comparisons stand in for it.
+#ifndef SPKM_CHECKS
+#define SPKM_CHECKS 0
+#endif
+#if SPKM_CHECKS
+#define DCHECK(cond)                                                                            \
+    do {                                                                                        \
+        if (!(cond)) {                                                                          \
+            printf("SPKM_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__,    \
+                   #cond, (int)blockIdx.x, (int)threadIdx.x);                                   \
+            __trap();                                                                           \
+        }                                                                                       \
+    } while (0)
+#else
+#define DCHECK(cond) do { } while (0)
+#endif
+
 namespace {
 
 // eps_i = (nnz_i + 6) * 6.1e-8 (>= 2^-24 * 1.02 per term) is computed on the
@@ -331,6 +351,7 @@ struct RowPassArgs {
     int use_s;
     int64_t hot;                 // term rows [0, hot) are gathered with evict_last, the rest evict_first
     const __half *ct16;          // fp16 copy of ct for the screening pass (HALF instantiations)
+    int64_t d;                   // term rows of ct (bounds checks of the debug build)
 };
 
 // One row group's gather (the canonical chain per column, CSR order): lane q
@@ -348,8 +369,10 @@ __device__ __forceinline__ void row_gather(float (&acc)[CH], const RowPassArgs &
     // nnz at a time so UB * CH/4 independent loads are in flight.
     for (int c0 = 0; c0 < maxlen; c0 += 32) {
         const int cnt = max(0, min(32, len - c0));
-        for (int q2 = q; q2 < cnt; q2 += A.tpr)
+        for (int q2 = q; q2 < cnt; q2 += A.tpr) {
             my_iv[q2] = make_int2(__ldg(A.indices + s + c0 + q2), __float_as_int(__ldg(A.values + s + c0 + q2)));
+            DCHECK((uint64_t)my_iv[q2].x < (uint64_t)A.d);
+        }
         __syncwarp();
         int u = 0;
         for (; u + UB <= cnt; u += UB) {
@@ -484,6 +507,7 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : CH == 32 ? SPKM_RP_M
         row_gather<CH, UBH, HALF>(acc, A, my_iv, s, len, maxlen, q, j0, pol_hot, pol_cold);
         const bool incumbent_mode = (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN);
         const int inc = (valid && incumbent_mode) ? A.a[row] : -1;
+        DCHECK(!valid || (row >= 0 && row < A.n && inc < A.k));
         if constexpr (HALF) {
             // acc holds the fp16-screened s'.  Candidates: s' >= max s' - 2E (the
             // only centers that can be the best or tie it: any other j has
@@ -1634,6 +1658,7 @@ __global__ void __launch_bounds__(256, SPKM_YY_MINB) k_yy_scan(const int64_t *__
                 nact += __popc(gm);
             }
         }
+        DCHECK(nact <= ng);
         __syncwarp();
         // (C) the 4 canonical similarities of every active group
         const int act_rounds = (int)__reduce_max_sync(FULL, (unsigned)((nact + bpr - 1) / bpr));
@@ -1765,8 +1790,10 @@ __global__ void __launch_bounds__(256) k_aggregate(int64_t n, int64_t d, const i
     for (int64_t i = (int64_t)blockIdx.x * wpb + (threadIdx.x >> 5); i < n; i += (int64_t)gridDim.x * wpb) {
         const int ai = a[i];
         long long *sj = sums + (int64_t)ai * d;
-        for (int64_t t = indptr[i] + lane; t < indptr[i + 1]; t += 32)
+        for (int64_t t = indptr[i] + lane; t < indptr[i + 1]; t += 32) {
+            DCHECK((uint64_t)__ldg(indices + t) < (uint64_t)d);
             atomicAdd((unsigned long long *)(sj + __ldg(indices + t)), (unsigned long long)to_fixed(__ldg(values + t), scale));
+        }
         if (lane == 0) atomicAdd((unsigned long long *)(counts + ai), 1ull);
     }
 }
@@ -1793,6 +1820,7 @@ __global__ void __launch_bounds__(256) k_apply_moves(int64_t d, const int64_t *_
         long long *sn = sums + (int64_t)nw * d;
         for (int64_t t = indptr[i] + lane; t < indptr[i + 1]; t += 32) {
             const int c = __ldg(indices + t);
+            DCHECK((uint64_t)c < (uint64_t)d && o >= 0 && nw >= 0);
             const long long q = to_fixed(__ldg(values + t), scale);
             atomicAdd((unsigned long long *)(so + c), (unsigned long long)(-q));
             atomicAdd((unsigned long long *)(sn + c), (unsigned long long)q);
@@ -3068,7 +3096,10 @@ int launch_row_pass(RowPassArgs &A, int64_t k, cudaStream_t st, int64_t max_rows
     const int grid = grid_for(slots, 8);
     // staging for rpw row groups per warp (k > 256: one) -- the rest of the
     // shared-memory carve-out stays L1 (C4 Elkan scan: -20% from this alone)
-    const size_t smem = (size_t)(256 / 32) * p.rpw * kIvStride * 8;
+#ifndef SPKM_RP_SMEM_GROUPS
+#define SPKM_RP_SMEM_GROUPS 0     // > 0: reserve this many row groups per warp (A/B of the L1 carve-out)
+#endif
+    const size_t smem = (size_t)(256 / 32) * (SPKM_RP_SMEM_GROUPS > p.rpw ? SPKM_RP_SMEM_GROUPS : p.rpw) * kIvStride * 8;
     // fp16 screening for every full pass but predict, when the table exists (k > 128)
     const bool half = A.ct16 != nullptr && A.mode != MODE_PREDICT && p.ch >= 8;
     if (p.ch == 4) return launch_rp<4, 256, false>(A, grid, smem, st);
@@ -3102,6 +3133,7 @@ RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     A.kp = C->kp;
     A.hot = hot_terms(C);
     A.ct16 = reinterpret_cast<const __half *>(C->ct16);
+    A.d = X->d;
     return A;
 }
 
@@ -3212,6 +3244,7 @@ __global__ void k_pack_moves(const int32_t *__restrict__ mv_i, const int32_t *__
     PDL_ENTRY();
     if (ctl[1]) return;
     const long long cnt = ctr[SPKM_CTR_MOVES];
+    DCHECK(cnt <= cap);
     const long long c = cnt < cap ? cnt : cap;   // cap = shard rows >= moves
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         slot[0] = (int32_t)c;
@@ -3580,7 +3613,11 @@ static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_boun
     const int grid = grid_for(X->n, 8);
     const int64_t eb = elkan_block(C->k), nbk = (C->k + eb - 1) / eb;
     const int64_t ppw_k = (32 / (nbk < 32 ? nbk : 32)) < 8 ? (32 / (nbk < 32 ? nbk : 32)) : 8;
-    const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float) + (size_t)8 * ppw_k * kIvStride * sizeof(int2);
+#ifndef SPKM_EK_SMEM_PAD
+#define SPKM_EK_SMEM_PAD 0        // extra bytes of dynamic shared memory (A/B of the L1 carve-out)
+#endif
+    const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float) + (size_t)8 * ppw_k * kIvStride * sizeof(int2) +
+                       SPKM_EK_SMEM_PAD;
     cudaError_t attr = cudaSuccess;
     auto launch = [&](auto kern) {
         // static smem (staging + active lists) + dyn must fit the opt-in

@@ -357,6 +357,14 @@ struct RowPassArgs {
 // One row group's gather (the canonical chain per column, CSR order): lane q
 // accumulates its CH columns j0 + r * jstr + c.  H: the fp16 table (4 halves
 // = 8 bytes per lane and nnz and float4 group) -- the screening values s'.
+#ifndef SPKM_HINT_MINCH
+#define SPKM_HINT_MINCH 16        // L2 eviction hints only where the table outgrows L2 (k > 256)
+#endif
+template <bool HINT>
+__device__ __forceinline__ float4 ldg4(const float4 *p, uint64_t pol) {
+    if constexpr (HINT) return ldg_hint(p, pol);
+    else return __ldg(p);
+}
 template <int CH, int UB, bool H>
 __device__ __forceinline__ void row_gather(float (&acc)[CH], const RowPassArgs &A, int2 *my_iv, int64_t s, int len,
                                            int maxlen, int q, int j0, uint64_t pol_hot, uint64_t pol_cold) {
@@ -405,7 +413,7 @@ __device__ __forceinline__ void row_gather(float (&acc)[CH], const RowPassArgs &
                     const float4 *p = reinterpret_cast<const float4 *>(ctj + (int64_t)iv[b] * A.kp);
                     const uint64_t pol = iv[b] < A.hot ? pol_hot : pol_cold;
 #pragma unroll
-                    for (int r = 0; r < CH / 4; ++r) cv[b][r] = ldg_hint(p + r * A.tpr, pol);
+                    for (int r = 0; r < CH / 4; ++r) cv[b][r] = ldg4<(CH >= SPKM_HINT_MINCH)>(p + r * A.tpr, pol);
                 }
 #pragma unroll
                 for (int b = 0; b < UB; ++b)
@@ -428,7 +436,7 @@ __device__ __forceinline__ void row_gather(float (&acc)[CH], const RowPassArgs &
                 if constexpr (H)
                     cc4 = half4_to_float4(ldg_hint(reinterpret_cast<const uint2 *>(chj + (int64_t)t.x * A.kp) + r * A.tpr, pol));
                 else
-                    cc4 = ldg_hint(reinterpret_cast<const float4 *>(ctj + (int64_t)t.x * A.kp) + r * A.tpr, pol);
+                    cc4 = ldg4<(CH >= SPKM_HINT_MINCH)>(reinterpret_cast<const float4 *>(ctj + (int64_t)t.x * A.kp) + r * A.tpr, pol);
                 acc[4 * r + 0] = __fmaf_rn(v0, cc4.x, acc[4 * r + 0]);
                 acc[4 * r + 1] = __fmaf_rn(v0, cc4.y, acc[4 * r + 1]);
                 acc[4 * r + 2] = __fmaf_rn(v0, cc4.z, acc[4 * r + 2]);
@@ -1462,6 +1470,325 @@ __global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_E
     PDL_TRIGGER();
     ctr_flush(s_ctr, ctr);
 }
+
+// k <= 128 (4-center blocks, one round of lanes per row): the round-1 form
+// of the scan -- blocks are fetched on the drift-updated u test and the
+// tightened s~(i, a) is read from the fetched a(i) block inside the replay,
+// instead of a separate tighten chain + compaction (k_elkan_scan), which
+// only pays off with several rounds of blocks (C4).  C2: 1.75 -> ~1.36 ms
+// per step of fused bound + scan passes.  Same results and counters.
+template <int EB, bool FUSE>
+__global__ void __launch_bounds__(256) k_elkan_scan_r1(const int64_t *__restrict__ indptr,
+                                                    const int32_t *__restrict__ indices,
+                                                    const float *__restrict__ values,
+                                                    const float *__restrict__ reps,
+                                                    const float *__restrict__ ct, int64_t kp, int k,
+                                                    int32_t *a, float *l, float *u, int64_t ku,
+                                                    const float *__restrict__ cc, int use_cc,
+                                                    const int32_t *__restrict__ surv1, int32_t *mv_i,
+                                                    int32_t *mv_old, long long *ctr, int64_t n_rows,
+                                                    const double *__restrict__ drift,
+                                                    const double *__restrict__ sinp,
+                                                    const float *__restrict__ s_arr,
+                                                    const long long *__restrict__ ctl) {
+    PDL_ENTRY();
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    constexpr int UB = 32 / EB;   // nnz per gather batch: 8 float4 loads in flight per lane
+    constexpr int ES = EB + 1;    // padded per-block stride of the similarity buffer
+    __shared__ __align__(16) int2 s_iv[8][8][kIvStride];
+    __shared__ unsigned long long s_ctr[8];
+    ctr_init(s_ctr);
+    extern __shared__ float s_sim_dyn[];   // [8 warps][sim_stride]
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int nb = (k + EB - 1) / EB;
+    const int bpr = nb < 32 ? nb : 32;
+    const int ppw = min(8, 32 / bpr);
+    const int nrounds = (nb + 31) >> 5;
+    const int g = lane / bpr, q = lane - g * bpr;
+    const bool lane_on = g < ppw;
+    const int o0 = bpr > 1 ? (1 << (31 - __clz(bpr - 1))) : 0;
+    const int sim_stride = (int)elkan_sim_stride(k);  // floats per warp
+    const int gstride = sim_stride / ppw;             // per-group slice (>= ES * nb)
+    float *my_sim = s_sim_dyn + wib * sim_stride + (lane_on ? g : 0) * gstride;
+    int2 *my_iv = s_iv[wib][lane_on ? g : 0];
+    const long long cnt = FUSE ? n_rows : ctr[SPKM_CTR_SURV1];
+    const int64_t nslots = (cnt + ppw - 1) / ppw;
+    const int wpb = blockDim.x >> 5;
+    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
+        const int64_t slot = w * ppw + g;
+        bool valid = lane_on && slot < cnt;
+        const int32_t i = valid ? (FUSE ? (int32_t)slot : surv1[slot]) : 0;
+        const int ai = valid ? a[i] : 0;
+        float *ui = u + (int64_t)i * ku;
+        const double eps = valid ? (double)reps[i] : 0.0;
+        double lb;
+        if constexpr (FUSE) {
+            // k_elkan_bounds for this row (engine.py:274-283 + kernels.py:35-47)
+            const float lo = valid ? l[i] : 0.f;
+            float lf = lo;
+            const double sa = valid ? sinp[ai] : 0.0;
+            if (sa != 0.0) {
+                const double pa = drift[ai];
+                lf = store_lower((lo < -pa) ? -1.0 : d_clamp((double)lo * pa - d_sin((double)lo) * sa));
+            }
+            if (valid && q == 0 && lf != lo) l[i] = lf;
+            lb = (double)lf;
+            const bool pskip = use_cc && lb >= 0.0 && (double)s_arr[ai] + kSqrt2 * eps <= lb;
+            const bool cc_on = use_cc && lb >= 0.0;
+            const float thu = thr_u_of(lb, eps), thc = thr_c_of(lb, eps);
+            bool surv = false;
+            for (int r = 0; r < nrounds && valid; ++r) {
+                const int blk = r * 32 + q;
+                if (blk >= nb) break;
+                for (int c2 = 0; c2 < EB; ++c2) {
+                    const int j = blk * EB + c2;
+                    if (j >= k) break;
+                    float wv = ui[j];
+                    const double sj = sinp[j];
+                    if (sj != 0.0) {   // the k_elkan_bounds update, same float32 arithmetic
+                        const double pj = drift[j];
+                        wv = elkan_u_drift(wv, __double2float_rd(pj), __double2float_ru(pj), __double2float_ru(sj));
+                        ui[j] = wv;
+                    }
+                    if (!pskip && j != ai) {
+                        bool skip = cc_on && __ldg(cc + (int64_t)ai * k + j) <= thc;
+                        if (!skip) skip = wv <= thu;
+                        surv |= !skip;
+                    }
+                }
+            }
+            // the row survives if any of its lanes found a center it cannot prune
+            const unsigned m = __ballot_sync(FULL, surv);
+            const unsigned gmask = (bpr >= 32 ? 0xffffffffu : ((1u << bpr) - 1u)) << (lane_on ? g * bpr : 0);
+            valid = valid && (m & gmask) != 0;
+            ctr_add(s_ctr, SPKM_CTR_SURV1, (valid && q == 0) ? 1 : 0);
+        } else {
+            lb = valid ? (double)l[i] : 0.0;
+        }
+        const int64_t s = valid ? indptr[i] : 0, e = valid ? indptr[i + 1] : 0;
+        const int len = (int)(e - s);
+        const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
+        const bool cc_ok = use_cc && lb >= 0.0;
+        for (int r = 0; r < nrounds; ++r) {
+            const int blk = r * 32 + q;
+            const int j0 = blk * EB;
+            bool act = false;
+            if (valid && blk < nb) {
+                for (int c2 = 0; c2 < EB; ++c2) {
+                    const int j = j0 + c2;
+                    if (j >= k) break;
+                    if (j == ai) {
+                        act = true;
+                        continue;
+                    }
+                    // u-test only: a center the replay may need fails it (the
+                    // cc test depends on the running best, so it cannot
+                    // prune the fetch)
+                    act |= !((double)ui[j] + 2.0 * eps <= lb);
+                }
+            }
+            if (!__any_sync(FULL, act)) continue;
+            float acc[EB];
+#pragma unroll
+            for (int c2 = 0; c2 < EB; ++c2) acc[c2] = 0.f;
+            const float4 *base4 = reinterpret_cast<const float4 *>(ct + j0);
+            for (int c0 = 0; c0 < maxlen; c0 += 32) {
+                const int cntc = max(0, min(32, len - c0));
+                for (int q2 = q; q2 < cntc; q2 += bpr)
+                    my_iv[q2] = make_int2(__ldg(indices + s + c0 + q2), __float_as_int(__ldg(values + s + c0 + q2)));
+                __syncwarp();
+                if (act && EB == 8) {   // two float4 (one sector) per lane and nnz
+                    int uu = 0;
+                    for (; uu + UB <= cntc; uu += UB) {
+                        float4 x[UB][2];
+                        float vv[UB];
+                        int iv[UB];
+                        load_iv<UB>(my_iv + uu, iv, vv);
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) {
+                            const float4 *p = base4 + ((int64_t)iv[b] * kp >> 2);
+                            x[b][0] = __ldg(p);
+                            x[b][1] = __ldg(p + 1);
+                        }
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) {
+                            acc[0] = __fmaf_rn(vv[b], x[b][0].x, acc[0]);
+                            acc[1] = __fmaf_rn(vv[b], x[b][0].y, acc[1]);
+                            acc[2] = __fmaf_rn(vv[b], x[b][0].z, acc[2]);
+                            acc[3] = __fmaf_rn(vv[b], x[b][0].w, acc[3]);
+                            acc[EB > 4 ? 4 : 0] = __fmaf_rn(vv[b], x[b][1].x, acc[EB > 4 ? 4 : 0]);
+                            acc[EB > 4 ? 5 : 1] = __fmaf_rn(vv[b], x[b][1].y, acc[EB > 4 ? 5 : 1]);
+                            acc[EB > 4 ? 6 : 2] = __fmaf_rn(vv[b], x[b][1].z, acc[EB > 4 ? 6 : 2]);
+                            acc[EB > 4 ? 7 : 3] = __fmaf_rn(vv[b], x[b][1].w, acc[EB > 4 ? 7 : 3]);
+                        }
+                    }
+                    for (; uu < cntc; ++uu) {
+                        const int2 t = my_iv[uu];
+                        const float v0 = __int_as_float(t.y);
+                        const float4 *p = base4 + ((int64_t)t.x * kp >> 2);
+                        const float4 x0 = __ldg(p), x1 = __ldg(p + 1);
+                        acc[0] = __fmaf_rn(v0, x0.x, acc[0]);
+                        acc[1] = __fmaf_rn(v0, x0.y, acc[1]);
+                        acc[2] = __fmaf_rn(v0, x0.z, acc[2]);
+                        acc[3] = __fmaf_rn(v0, x0.w, acc[3]);
+                        acc[EB > 4 ? 4 : 0] = __fmaf_rn(v0, x1.x, acc[EB > 4 ? 4 : 0]);
+                        acc[EB > 4 ? 5 : 1] = __fmaf_rn(v0, x1.y, acc[EB > 4 ? 5 : 1]);
+                        acc[EB > 4 ? 6 : 2] = __fmaf_rn(v0, x1.z, acc[EB > 4 ? 6 : 2]);
+                        acc[EB > 4 ? 7 : 3] = __fmaf_rn(v0, x1.w, acc[EB > 4 ? 7 : 3]);
+                    }
+                } else if (act) {   // EB == 4: one float4 per lane and nnz
+                    int uu = 0;
+                    for (; uu + UB <= cntc; uu += UB) {
+                        float4 x[UB];
+                        float vv[UB];
+                        int iv[UB];
+                        load_iv<UB>(my_iv + uu, iv, vv);
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) x[b] = __ldg(base4 + ((int64_t)iv[b] * kp >> 2));
+#pragma unroll
+                        for (int b = 0; b < UB; ++b) {
+                            acc[0] = __fmaf_rn(vv[b], x[b].x, acc[0]);
+                            acc[1] = __fmaf_rn(vv[b], x[b].y, acc[1]);
+                            acc[2] = __fmaf_rn(vv[b], x[b].z, acc[2]);
+                            acc[3] = __fmaf_rn(vv[b], x[b].w, acc[3]);
+                        }
+                    }
+                    for (; uu < cntc; ++uu) {
+                        const int2 t = my_iv[uu];
+                        const float v0 = __int_as_float(t.y);
+                        const float4 x0 = __ldg(base4 + ((int64_t)t.x * kp >> 2));
+                        acc[0] = __fmaf_rn(v0, x0.x, acc[0]);
+                        acc[1] = __fmaf_rn(v0, x0.y, acc[1]);
+                        acc[2] = __fmaf_rn(v0, x0.z, acc[2]);
+                        acc[3] = __fmaf_rn(v0, x0.w, acc[3]);
+                    }
+                }
+                __syncwarp();
+            }
+            if (act) {
+#pragma unroll
+                for (int c2 = 0; c2 < EB; ++c2) my_sim[blk * ES + c2] = acc[c2];
+            }
+        }
+        __syncwarp();
+        // replay of kernels.py:35-65, parallel over the group's lanes.  Lane q
+        // owns the centers of blocks q, q+32, ... (ascending j within the
+        // lane).  (A) tighten at the first j failing the pre-tests; (B) with
+        // the running best (cur, lcur) every lane finds its candidates and
+        // its first "event" (candidate beating lcur); the earliest event of
+        // the group updates (cur, lcur) and the scan resumes after it.
+        // Between events the state is constant, so the candidate set and the
+        // reassignments equal the reference's sequential loop.
+        int cur = ai;
+        float lcur = 0.f;
+        long long sims = 0;
+        constexpr int NONE = 0x7fffffff;
+        int first_fail = NONE;
+        if (valid) {
+            for (int r = 0; r < nrounds && first_fail == NONE; ++r) {
+                const int blk = r * 32 + q;
+                if (blk >= nb) break;
+                for (int c2 = 0; c2 < EB; ++c2) {
+                    const int j = blk * EB + c2;
+                    if (j >= k) break;
+                    if (j == ai) continue;
+                    if (cc_ok && (double)cc[(int64_t)ai * k + j] + kSqrt2 * eps <= lb) continue;
+                    if ((double)ui[j] + 2.0 * eps <= lb) continue;
+                    first_fail = j;
+                    break;
+                }
+            }
+        }
+        // group min (lanes of other groups hold their own values)
+        for (int o = o0; o; o >>= 1) {
+            const int other = __shfl_down_sync(FULL, first_fail, o);
+            if (q < o && q + o < bpr) first_fail = min(first_fail, other);
+        }
+        first_fail = __shfl_sync(FULL, first_fail, lane - q);
+        const bool tight = valid && first_fail != NONE;
+        if (tight) {
+            lcur = my_sim[(ai >> (EB == 4 ? 2 : 3)) * ES + (ai & (EB - 1))];
+            if (q == 0) {
+                ui[ai] = store_upper((double)lcur + eps);
+                sims = 1;
+            }
+        }
+        int start = first_fail;
+        bool more = __any_sync(FULL, tight);
+        bool active_g = tight;
+        while (more) {
+            // lane-local pass over its j >= start with the current state
+            int ev = NONE;
+            if (active_g) {
+                const double lc = (double)lcur;
+                const bool ccok2 = use_cc && lc - eps >= 0.0;
+                for (int r = 0; r < nrounds && ev == NONE; ++r) {
+                    const int blk = r * 32 + q;
+                    if (blk >= nb) break;
+                    if (blk * EB + EB - 1 < start) continue;
+                    for (int c2 = 0; c2 < EB; ++c2) {
+                        const int j = blk * EB + c2;
+                        if (j >= k) break;
+                        if (j < start || j == ai || j == cur) continue;
+                        if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
+                        if ((double)ui[j] + eps <= lc) continue;
+                        if (my_sim[blk * ES + c2] > lcur) {
+                            ev = j;
+                            break;
+                        }
+                    }
+                }
+            }
+            int gev = ev;
+            for (int o = o0; o; o >>= 1) {
+                const int other = __shfl_down_sync(FULL, gev, o);
+                if (q < o && q + o < bpr) gev = min(gev, other);
+            }
+            gev = __shfl_sync(FULL, gev, lane - q);
+            // commit every candidate in [start, gev) (and the event itself)
+            if (active_g) {
+                const double lc = (double)lcur;
+                const bool ccok2 = use_cc && lc - eps >= 0.0;
+                for (int r = 0; r < nrounds; ++r) {
+                    const int blk = r * 32 + q;
+                    if (blk >= nb) break;
+                    if (blk * EB + EB - 1 < start || blk * EB > gev) continue;
+                    for (int c2 = 0; c2 < EB; ++c2) {
+                        const int j = blk * EB + c2;
+                        if (j >= k || j > gev) break;
+                        if (j < start || j == ai || j == cur) continue;
+                        if (j < gev) {
+                            if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
+                            if ((double)ui[j] + eps <= lc) continue;
+                        }
+                        ui[j] = store_upper((double)my_sim[blk * ES + c2] + eps);
+                        ++sims;
+                    }
+                }
+                if (gev != NONE) {
+                    cur = gev;
+                    lcur = my_sim[(gev >> (EB == 4 ? 2 : 3)) * ES + (gev & (EB - 1))];
+                    start = gev + 1;
+                } else {
+                    active_g = false;
+                }
+            }
+            more = __any_sync(FULL, active_g);
+        }
+        if (valid && q == 0 && tight) {
+            l[i] = store_lower((double)lcur - eps);
+            if (cur != ai) a[i] = cur;
+        }
+        const bool leader = valid && q == 0;
+        warp_append(leader && cur != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
+        ctr_add(s_ctr, SPKM_CTR_SIMS, sims);
+        ctr_add(s_ctr, SPKM_CTR_NNZ_ELKAN, leader ? (long long)len : 0);
+        __syncwarp();
+    }
+    PDL_TRIGGER();
+    ctr_flush(s_ctr, ctr);
+}
+
 
 // ------------------------------------------------------ Yin-Yang family
 // Group bounds (Ding et al., ICML 2015, carried over to cosine similarities
@@ -3629,12 +3956,22 @@ static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_boun
                    C->kp, (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1, W->mv_i, W->mv_old, W->ctr,
                    X->n, C->drift, C->sinp, C->s, C->ctl, hot_terms(C));
     };
+    auto launch_r1 = [&](auto kern) {   // k <= 128: the round-1 scan (no `hot` argument)
+        attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);
+        if (attr != cudaSuccess) return;
+        pdl_launch(kern, dim3(grid), dim3(256), dyn, S(stream), X->indptr, X->indices, X->values, X->row_eps, C->ct32,
+                   C->kp, (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1, W->mv_i, W->mv_old, W->ctr,
+                   X->n, C->drift, C->sinp, C->s, C->ctl);
+    };
+#ifndef SPKM_EK_SMALL_R1
+#define SPKM_EK_SMALL_R1 1
+#endif
     const bool eb4 = elkan_block(C->k) == 4;
     if (fuse) {
-        if (eb4) launch(k_elkan_scan<4, true>);
+        if (eb4) SPKM_EK_SMALL_R1 ? launch_r1(k_elkan_scan_r1<4, true>) : launch(k_elkan_scan<4, true>);
         else launch(k_elkan_scan<8, true>);
     } else {
-        if (eb4) launch(k_elkan_scan<4, false>);
+        if (eb4) SPKM_EK_SMALL_R1 ? launch_r1(k_elkan_scan_r1<4, false>) : launch(k_elkan_scan<4, false>);
         else launch(k_elkan_scan<8, false>);
     }
     if (attr != cudaSuccess) return fail("elkan_scan smem attribute", attr);

@@ -232,6 +232,16 @@ int64_t spkm_gram_tiles(int64_t k, int32_t *host_pairs);
 int64_t spkm_gram_scratch_doubles(int64_t k, int64_t d);
 int spkm_center_thresholds(const spkm_centers *C, double *gram_scratch, const void *tile_pairs,
                            int full, void *stream);
+/* The same in two halves for the multi-GPU path: spkm_gram_partial computes
+ * rank's round-robin share of the (tile, d-split) Gram partials (world > 1:
+ * the others are zeroed), the caller sums the spkm_gram_partial_floats(k, d)
+ * floats at the start of gpart over the ranks (allreduce; exact: every
+ * element is nonzero on one rank only), then spkm_gram_finish maps them to
+ * cc and s.  rank 0 of world 1 == spkm_center_thresholds. */
+int64_t spkm_gram_partial_floats(int64_t k, int64_t d);
+int spkm_gram_partial(const spkm_centers *C, double *gpart, const void *tiles, int full, int rank, int world,
+                      void *stream);
+int spkm_gram_finish(const spkm_centers *C, double *gpart, int full, void *stream);
 /* Objective, all-p==1 flag, Hamerly owner/p_min/p_min2, stats; clears
  * touched.  sims_extra is added to the sims counter (host-known counts). */
 int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra,

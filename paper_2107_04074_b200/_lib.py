@@ -117,6 +117,9 @@ _SIGS = {
     "spkm_permute_rows": [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp],
     "spkm_prepare_scratch_bytes": [c_i64, c_i64],
     "spkm_dense_ids": [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],
+    "spkm_gram_partial_floats": [c_i64, c_i64],
+    "spkm_gram_partial": [_P(Centers), c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp],
+    "spkm_gram_finish": [_P(Centers), c_vp, ctypes.c_int, c_vp],
     "spkm_prepare_rows": [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp],
     "spkm_loop_end": [c_vp],
     "spkm_fit_graph_begin": [c_vp, _P(c_vp)],
@@ -150,6 +153,7 @@ _RESTYPES = {
     "spkm_seed_scratch_doubles": c_i64,
     "spkm_move_slot_ints": c_i64,
     "spkm_prepare_scratch_bytes": c_i64,
+    "spkm_gram_partial_floats": c_i64,
 }
 
 # kernels each entry point launches (for the bench's gpu_launches count)
@@ -159,7 +163,7 @@ KERNELS_PER_CALL = {
     "spkm_move_centers": 5, "spkm_center_reduce": 1, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
-    "spkm_seed_rows_csr": 1, "spkm_permute_rows": 1, "spkm_prepare_rows": 7, "spkm_dense_ids": 1, "spkm_audit": 1, "spkm_audit_transpose": 1,
+    "spkm_seed_rows_csr": 1, "spkm_permute_rows": 1, "spkm_prepare_rows": 7, "spkm_dense_ids": 1, "spkm_gram_partial": 1, "spkm_gram_finish": 2, "spkm_audit": 1, "spkm_audit_transpose": 1,
     "spkm_pack_moves": 1, "spkm_apply_move_slots": 1, "spkm_rows_to_host": 1,
     "spkm_order_by_cluster": 4,
 }

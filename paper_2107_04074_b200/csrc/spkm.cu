@@ -3164,7 +3164,7 @@ __global__ void __launch_bounds__(GM_THREADS, 1) k_gram_mn(const __grid_constant
                                                           int64_t dsplit, const int2 *__restrict__ tiles,
                                                           const int32_t *__restrict__ tlist,
                                                           const int32_t *__restrict__ tcount, int full, float *gpart,
-                                                          const long long *__restrict__ ctl) {
+                                                          const long long *__restrict__ ctl, int rank, int world) {
     PDL_ENTRY();
     using G = GmCfg<DIAG>;
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
@@ -3186,7 +3186,10 @@ __global__ void __launch_bounds__(GM_THREADS, 1) k_gram_mn(const __grid_constant
     }
     const int dirty = __syncthreads_or(mine);
     if (blockIdx.y == 0 && threadIdx.x == 0) reinterpret_cast<int *>(gpart + dsplit * k * k)[blockIdx.x] = dirty;
-    if (!dirty) return;
+    // multi-GPU: the (tile, split) CTAs are dealt round-robin to the ranks;
+    // every rank still writes every tile's dirty flag (above), its own
+    // partials only (the others are zero and summed in by an allreduce)
+    if (!dirty || (int)(((int64_t)blockIdx.x * gridDim.y + blockIdx.y) % world) != rank) return;
     const int64_t per = ((d + dsplit - 1) / dsplit + GKC - 1) / GKC * GKC;
     const int64_t t0 = blockIdx.y * per, t1 = min(d, t0 + per);
     const int nch = t1 > t0 ? (int)((t1 - t0 + GKC - 1) / GKC) : 0;
@@ -4133,15 +4136,25 @@ int64_t spkm_gram_dsplit(int64_t k, int64_t d) {
 
 int64_t spkm_gram_scratch_doubles(int64_t k, int64_t d) { return spkm_gram_dsplit(k, d) * k * k; }
 
+int spkm_gram_partial(const spkm_centers *C, double *gpart, const void *tiles_ptr, int full, int rank, int world,
+                      void *stream);
+int spkm_gram_finish(const spkm_centers *C, double *gpart, int full, void *stream);
+
 int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *tiles_ptr, int full, void *stream) {
+    const int rc = spkm_gram_partial(C, gpart, tiles_ptr, full, 0, 1, stream);
+    return rc ? rc : spkm_gram_finish(C, gpart, full, stream);
+}
+
+int64_t spkm_gram_partial_floats(int64_t k, int64_t d) { return spkm_gram_dsplit(k, d) * k * k; }
+
+int spkm_gram_partial(const spkm_centers *C, double *gpart, const void *tiles_ptr, int full, int rank, int world,
+                      void *stream) {
+    if (world < 1 || rank < 0 || rank >= world) return fail_msg("gram_partial: bad rank / world");
     const int2 *tiles_dev = static_cast<const int2 *>(tiles_ptr);
     cudaStream_t st = S(stream);
     const int64_t tk = (C->k + GT - 1) / GT;
     const int64_t ntiles = tk * (tk + 1) / 2;
     const int64_t ds = spkm_gram_dsplit(C->k, C->d);
-    const int64_t per = ((C->d + ds - 1) / ds + GKC - 1) / GKC * GKC;
-    // 3xTF32 residual over `per` terms + the float32 copy's rounding (2 x 2^-24 + slack)
-    const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + 2e-6;
     // float32 partials [ds][k][k], then one dirty flag per tile (fits the double-sized scratch)
     float *gp = reinterpret_cast<float *>(gpart);
     CUtensorMap tm;
@@ -4154,13 +4167,26 @@ int spkm_center_thresholds(const spkm_centers *C, double *gpart, const void *til
                              : cudaFuncSetAttribute(k_gram_mn<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                     (int)GmCfg<false>::SMEM);
     if (ae != cudaSuccess) return fail("gram_mn smem attribute", ae);
+    if (world > 1) {   // this rank's share of the partials; the others are zeroed and summed in by the caller
+        const cudaError_t me = cudaMemsetAsync(gp, 0, sizeof(float) * ds * C->k * C->k, st);
+        if (me != cudaSuccess) return fail("gram_partial memset", me);
+    }
     if (tk == 1)
         pdl_launch(k_gram_mn<true>, dim3(1, (unsigned)ds), dim3(GM_THREADS), GmCfg<true>::SMEM, st, tm, C->k, C->d, ds,
-                   tiles_dev, C->tlist, C->tcount, full, gp, C->ctl);
+                   tiles_dev, C->tlist, C->tcount, full, gp, C->ctl, rank, world);
     else
         pdl_launch(k_gram_mn<false>, dim3((unsigned)ntiles, (unsigned)ds), dim3(GM_THREADS), GmCfg<false>::SMEM, st, tm,
-                   C->k, C->d, ds, tiles_dev, C->tlist, C->tcount, full, gp, C->ctl);
+                   C->k, C->d, ds, tiles_dev, C->tlist, C->tcount, full, gp, C->ctl, rank, world);
     CHECK_LAUNCH("gram_mn");
+    return 0;
+}
+
+int spkm_gram_finish(const spkm_centers *C, double *gpart, int full, void *stream) {
+    cudaStream_t st = S(stream);
+    const int64_t ds = spkm_gram_dsplit(C->k, C->d);
+    const int64_t per = ((C->d + ds - 1) / ds + GKC - 1) / GKC * GKC;
+    const double gdelta = (3.0 * (double)per / 8.0 + 8.0) * ldexp(1.0, -22) + 2e-6;
+    float *gp = reinterpret_cast<float *>(gpart);
     pdl_launch(k_gram_final, dim3((unsigned)((C->k * C->k * 8 + 255) / 256)), dim3(256), (size_t)0, st, C->k, ds, gp,
                full, gdelta, C->cc, C->ctl);
     CHECK_LAUNCH("gram_final");

@@ -8,8 +8,10 @@ device rows (rows are stored longest first; ranges are balanced by nnz) for
 everything that scales with n x k: the full passes, the bound updates and
 the pruned scans, with their bounds and worklists.
 
-Per iteration the only exchange is ONE allgather of fixed-size int32 move
-slots (``spkm_pack_moves``):
+Per iteration the exchange is ONE allgather of fixed-size int32 move
+slots (``spkm_pack_moves``) -- plus, for the variants with center-center
+bounds (elkan, hamerly), one allreduce of the rank-sharded Gram partials of
+the center thresholds (``Engine.center_thresholds``):
 
     slot = [ move count | 8 int64 counters | (global row, old, new) x cap ]
 
@@ -83,6 +85,11 @@ class Exchange:
     def allgather_moves(self):
         """slot (packed by spkm_pack_moves) -> every rank's slot in ``slots``."""
         dist.all_gather_into_tensor(self.slots, self.slot, group=self.group)
+
+    def allreduce_sum(self, t: torch.Tensor):
+        """In-place sum over the ranks (the center-threshold Gram partials:
+        each element is nonzero on one rank, so the float sum is exact)."""
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
     def allgather_assignments(self, a_local: torch.Tensor, a_global: torch.Tensor):
         """Shard assignments (device order) -> the global device-order array."""

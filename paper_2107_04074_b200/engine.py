@@ -852,9 +852,24 @@ class Engine:
         with torch.cuda.stream(self.stream):
             self.C.ctl.zero_()
 
-    def center_thresholds(self):
-        _lib.call("spkm_center_thresholds", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles),
-                  int(not self.C.cc_valid), self.sp)
+    def center_thresholds(self, stream=None, sp=None):
+        """cc / s of the current centers (engine.py:192-198).  Multi-GPU: each
+        rank computes its round-robin share of the Gram partials, one
+        allreduce sums them (exact: each float is nonzero on one rank), every
+        rank maps them to cc and s -- the same values as one GPU."""
+        stream = self.stream if stream is None else stream
+        sp = self.sp if sp is None else sp
+        full = int(not self.C.cc_valid)
+        ex = self.comm
+        if ex is None or ex.world == 1 or not hasattr(ex, "allreduce_sum"):
+            _lib.call("spkm_center_thresholds", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles), full, sp)
+        else:
+            _lib.call("spkm_gram_partial", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles), full, ex.rank,
+                      ex.world, sp)
+            nfl = int(_lib.lib().spkm_gram_partial_floats(self.k, self.C.d))
+            with torch.cuda.stream(stream):
+                ex.allreduce_sum(self.C.gram.view(torch.float32)[:nfl])
+            _lib.call("spkm_gram_finish", self.C.struct, _ptr(self.C.gram), full, sp)
         self.C.cc_valid = True
 
     def _dense(self, mode: int, use_s: int = 0):
@@ -954,9 +969,7 @@ class Engine:
         side, side_sp, fork, join = self._side[key]
         fork.record(self.stream)
         side.wait_event(fork)
-        _lib.call("spkm_center_thresholds", self.C.struct, _ptr(self.C.gram), _ptr(self.C.tiles),
-                  int(not self.C.cc_valid), side_sp)
-        self.C.cc_valid = True
+        self.center_thresholds(side, side_sp)
         join.record(side)
         _lib.call("spkm_center_reduce", self.C.struct, self.sp)
         if scratch:

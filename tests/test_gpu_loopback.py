@@ -64,6 +64,19 @@ class LoopbackExchange:
         self.g.barrier.wait()                  # nobody rewrites its buffer before all have copied
         self.calls += 1
 
+    def allreduce_sum(self, t):
+        s = torch.cuda.current_stream()
+        s.synchronize()
+        self.g.bufs[self.rank] = t.clone()
+        self.g.barrier.wait()
+        acc = torch.zeros_like(t)
+        for q in range(self.world):
+            acc += self.g.bufs[q]
+        t.copy_(acc)
+        s.synchronize()
+        self.g.barrier.wait()
+        self.calls += 1
+
     def allgather_moves(self):
         self._allgather(self.slot, self.slots, self.slot_len)
 
@@ -132,3 +145,20 @@ def test_loopback_ranks_equal_single_process(corpus, variant, world):
         assert np.array_equal(r.centers.centers, ref.centers.centers)
         assert np.array_equal(r.centers.counts, ref.centers.counts)
         assert ex.calls >= len(r.iterations)      # one move exchange per iteration >= 2, plus the assignments
+
+
+@pytest.mark.parametrize("variant", ["elkan", "hamerly"])
+def test_loopback_sharded_thresholds_multi_tile(variant):
+    """k = 300: 3 x 3 Gram tiles, so the (tile, d-split) CTAs of the center
+    thresholds are really dealt across the 3 ranks (spkm_gram_partial) and
+    summed by the allreduce; the fit equals the single-process one."""
+    import paper_2107_04074_b200 as spk
+    from paper_2107_04074_b200 import synth
+    data = synth.config_dataset("C3", n_override=20_000)
+    ref = spk.run(data, 300, variant, spk.SeedConfig(seed=5), max_iter=25, use_graphs=False)
+    out, _ = _fit_ranks(data, 300, variant, 3, 5, 25)
+    for r, ex in out:
+        assert np.array_equal(r.assignments, ref.assignments)
+        assert r.objective == ref.objective
+        assert [s.sim_count for s in r.iterations] == [s.sim_count for s in ref.iterations]
+        assert ex.calls >= 2 * len(r.iterations) - 1      # moves + Gram partials every iteration >= 2

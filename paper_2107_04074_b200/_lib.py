@@ -36,11 +36,17 @@ class CSR(ctypes.Structure):
                 ("values", c_vp), ("row_eps", c_vp)]
 
 
+class CIndex(ctypes.Structure):
+    _fields_ = [("desc", c_vp), ("pairs", c_vp), ("off", c_vp), ("scratch", c_vp), ("scratch_bytes", c_i64),
+                ("capacity", c_i64), ("dense_thr", c_i32), ("_pad", c_i32)]
+
+
 class Centers(ctypes.Structure):
     _fields_ = [("k", c_i64), ("d", c_i64), ("kp", c_i64), ("scale_bits", c_i32), ("_pad", c_i32),
                 ("cent64", c_vp), ("ct32", c_vp), ("sums", c_vp), ("counts", c_vp), ("drift", c_vp),
                 ("sinp", c_vp), ("touched", c_vp), ("objc", c_vp), ("part", c_vp), ("norm", c_vp), ("cc", c_vp),
-                ("s", c_vp), ("hstat", c_vp), ("tlist", c_vp), ("tcount", c_vp), ("ctl", c_vp), ("ct16", c_vp)]
+                ("s", c_vp), ("hstat", c_vp), ("tlist", c_vp), ("tcount", c_vp), ("ctl", c_vp), ("ct16", c_vp),
+                ("cindex", c_vp)]
 
 
 class Bounds(ctypes.Structure):
@@ -118,6 +124,8 @@ _SIGS = {
     "spkm_prepare_scratch_bytes": [c_i64, c_i64],
     "spkm_dense_ids": [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp],
     "spkm_gram_partial_floats": [c_i64, c_i64],
+    "spkm_cindex_scratch_bytes": [c_i64],
+    "spkm_cindex_build": [_P(Centers), c_vp],
     "spkm_gram_partial": [_P(Centers), c_vp, c_vp, ctypes.c_int, ctypes.c_int, ctypes.c_int, c_vp],
     "spkm_gram_finish": [_P(Centers), c_vp, ctypes.c_int, c_vp],
     "spkm_prepare_rows": [c_i64, c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_vp],
@@ -154,6 +162,7 @@ _RESTYPES = {
     "spkm_move_slot_ints": c_i64,
     "spkm_prepare_scratch_bytes": c_i64,
     "spkm_gram_partial_floats": c_i64,
+    "spkm_cindex_scratch_bytes": c_i64,
 }
 
 # kernels each entry point launches (for the bench's gpu_launches count)
@@ -163,7 +172,7 @@ KERNELS_PER_CALL = {
     "spkm_move_centers": 5, "spkm_center_reduce": 1, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
-    "spkm_seed_rows_csr": 1, "spkm_permute_rows": 1, "spkm_prepare_rows": 7, "spkm_dense_ids": 1, "spkm_gram_partial": 1, "spkm_gram_finish": 2, "spkm_audit": 1, "spkm_audit_transpose": 1,
+    "spkm_seed_rows_csr": 1, "spkm_permute_rows": 1, "spkm_prepare_rows": 7, "spkm_dense_ids": 1, "spkm_gram_partial": 1, "spkm_gram_finish": 2, "spkm_cindex_build": 3, "spkm_audit": 1, "spkm_audit_transpose": 1,
     "spkm_pack_moves": 1, "spkm_apply_move_slots": 1, "spkm_rows_to_host": 1,
     "spkm_order_by_cluster": 4,
 }

@@ -352,7 +352,89 @@ struct RowPassArgs {
     int64_t hot;                 // term rows [0, hot) are gathered with evict_last, the rest evict_first
     const __half *ct16;          // fp16 copy of ct for the screening pass (HALF instantiations)
     int64_t d;                   // term rows of ct (bounds checks of the debug build)
+    const int64_t *ci_desc;      // sparse center index (SPARSE instantiations): per term row
+    const int2 *ci_pairs;        //   (offset << 12 | count) and the (j, value bits) pairs
 };
+
+// Sparse gather (k > 256 with a center index): the row's accumulators live in
+// shared memory (kp floats per warp); term by term in CSR order, a dense
+// term row (more than dense_thr centers nonzero) is read from ct32 by the
+// lanes that own its columns (as the register gather), a sparse one as its
+// (j, value) pairs, one pair per lane.  Zeros contribute nothing to the FMA
+// chain, so every s~(i, j) is the canonical chain (ties and all).  The
+// lanes then pick up their CH columns into registers for the epilogue.
+template <int CH>
+__device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPassArgs &A, float *sacc, int64_t s,
+                                                  int len, int maxlen, int lane, int j0, uint64_t pol_hot,
+                                                  uint64_t pol_cold) {
+    const int jstr = 4 * A.tpr;
+#pragma unroll
+    for (int r = 0; r < CH / 4; ++r) *reinterpret_cast<float4 *>(sacc + j0 + r * jstr) = make_float4(0.f, 0.f, 0.f, 0.f);
+    __syncwarp();
+    bool last_sparse = true;
+    for (int c0 = 0; c0 < maxlen; c0 += 32) {
+        const int cnt = max(0, min(32, len - c0));
+        int id = 0;
+        float v = 0.f;
+        long long dsc = 0;
+        if (lane < cnt) {
+            id = __ldg(A.indices + s + c0 + lane);
+            v = __ldg(A.values + s + c0 + lane);
+            DCHECK((uint64_t)id < (uint64_t)A.d);
+            dsc = __ldg(reinterpret_cast<const long long *>(A.ci_desc) + id);
+        }
+        for (int t = 0; t < cnt; ++t) {
+            const int tid = __shfl_sync(FULL, id, t);
+            const float tv = __shfl_sync(FULL, v, t);
+            const long long td = __shfl_sync(FULL, dsc, t);
+            const int n = (int)(td & 0xFFF);
+            if (n == 0xFFF) {   // dense term row: the owner lanes, float4 per column group
+                const float4 *p = reinterpret_cast<const float4 *>(A.ct + (int64_t)tid * A.kp + j0);
+                const uint64_t pol = tid < A.hot ? pol_hot : pol_cold;
+                float4 x[CH / 4];
+#pragma unroll
+                for (int r = 0; r < CH / 4; ++r) x[r] = ldg_hint(p + r * A.tpr, pol);
+                if (last_sparse) __syncwarp();
+#pragma unroll
+                for (int r = 0; r < CH / 4; ++r) {
+                    float4 *ap = reinterpret_cast<float4 *>(sacc + j0 + r * jstr);
+                    float4 a = *ap;
+                    a.x = __fmaf_rn(tv, x[r].x, a.x);
+                    a.y = __fmaf_rn(tv, x[r].y, a.y);
+                    a.z = __fmaf_rn(tv, x[r].z, a.z);
+                    a.w = __fmaf_rn(tv, x[r].w, a.w);
+                    *ap = a;
+                }
+                last_sparse = false;
+            } else if (n > 0) {   // sparse term row: its pairs, one per lane (distinct j within a row)
+                const int2 *pp = A.ci_pairs + (td >> 12);
+                int2 e[8];
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+                    if (lane + 32 * m < n) e[m] = __ldg(pp + lane + 32 * m);
+                __syncwarp();   // earlier terms' updates (any lane) are visible
+#pragma unroll
+                for (int m = 0; m < 8; ++m)
+                    if (lane + 32 * m < n) sacc[e[m].x] = __fmaf_rn(tv, __int_as_float(e[m].y), sacc[e[m].x]);
+                for (int p2 = lane + 256; p2 < n; p2 += 32) {   // rows beyond 256 pairs (dense_thr > 256)
+                    const int2 f = __ldg(pp + p2);
+                    sacc[f.x] = __fmaf_rn(tv, __int_as_float(f.y), sacc[f.x]);
+                }
+                last_sparse = true;
+            }
+        }
+    }
+    __syncwarp();
+#pragma unroll
+    for (int r = 0; r < CH / 4; ++r) {
+        const float4 a = *reinterpret_cast<const float4 *>(sacc + j0 + r * jstr);
+        acc[4 * r + 0] = a.x;
+        acc[4 * r + 1] = a.y;
+        acc[4 * r + 2] = a.z;
+        acc[4 * r + 3] = a.w;
+    }
+    __syncwarp();
+}
 
 // One row group's gather (the canonical chain per column, CSR order): lane q
 // accumulates its CH columns j0 + r * jstr + c.  H: the fp16 table (4 halves
@@ -461,11 +543,18 @@ __device__ __forceinline__ double screen_err(int m) { return 5.0e-4 + 1.3e-7 * m
 // CH/4 float4 loads of the term-major center row; CH independent FMA chains.
 // CH <= 8: capped at 64 registers (4 CTAs of 256 per SM); CH >= 16 (k > 256):
 // uncapped, the CH accumulators and loads in flight need the registers.
+#ifndef SPKM_RP_SP_MINB
+#define SPKM_RP_SP_MINB 3         // sparse gather: no register accumulators in the hot loop
+#endif
 #ifndef SPKM_RP_MINB
 #define SPKM_RP_MINB 2        // k > 256: 128 registers, 2 CTAs per SM with UB 3 (C4 rescan 3336 -> 3281 ms per fit)
 #endif
-template <int CH, int NT, bool HALF>
-__global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : CH == 32 ? SPKM_RP_MINB : 1) k_row_pass(RowPassArgs A) {
+// GV: the gather variant -- 0 float32 table, 1 fp16 screening (SPKM_CT16=1),
+// 2 sparse center index (k > 256)
+template <int CH, int NT, int GV>
+__global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP_MINB : CH == 32 ? SPKM_RP_MINB : 1)
+    k_row_pass(RowPassArgs A) {
+    constexpr bool HALF = GV == 1, SPARSE = GV == 2;
     PDL_ENTRY();
     // nnz per gather batch: keep ~8 float4 loads in flight per lane
 #ifndef SPKM_UB_WIDE
@@ -512,7 +601,11 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : CH == 32 ? SPKM_RP_M
         const int jstr = 4 * A.tpr;
         float acc[CH];
         const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
-        row_gather<CH, UBH, HALF>(acc, A, my_iv, s, len, maxlen, q, j0, pol_hot, pol_cold);
+        if constexpr (SPARSE)
+            row_gather_sparse<CH>(acc, A, reinterpret_cast<float *>(s_iv + 8 * A.rpw * kIvStride) + wib * A.kp, s, len,
+                                  maxlen, lane, j0, pol_hot, pol_cold);
+        else
+            row_gather<CH, UBH, HALF>(acc, A, my_iv, s, len, maxlen, q, j0, pol_hot, pol_cold);
         const bool incumbent_mode = (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN);
         const int inc = (valid && incumbent_mode) ? A.a[row] : -1;
         DCHECK(!valid || (row >= 0 && row < A.n && inc < A.k));
@@ -1789,6 +1882,73 @@ __global__ void __launch_bounds__(256) k_elkan_scan_r1(const int64_t *__restrict
     ctr_flush(s_ctr, ctr);
 }
 
+
+// ------------------------------------------------ sparse center index
+// spkm_cindex_build: warp per term row of ct32 (float4 per lane, 128
+// columns per step).  count: nonzero centers -> off[t] (sparse rows; 0 for
+// dense ones) and desc[t] = count (temporarily); an exclusive scan turns off
+// into offsets; fill: the sparse rows' (j, value) pairs in j order, desc.
+__global__ void __launch_bounds__(256) k_ci_count(int64_t d, int64_t kp, int k, const float *__restrict__ ct, int thr,
+                                                  int64_t *off, int64_t *desc, const long long *__restrict__ ctl) {
+    PDL_ENTRY();
+    if (ctl[1]) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < d; t += warps) {
+        const float *row = ct + t * kp;
+        int c = 0;
+        for (int j0 = 4 * lane; j0 < k; j0 += 128) {
+            const float4 v = __ldg(reinterpret_cast<const float4 *>(row + j0));
+            c += (v.x != 0.f) + (j0 + 1 < k && v.y != 0.f) + (j0 + 2 < k && v.z != 0.f) + (j0 + 3 < k && v.w != 0.f);
+        }
+        c = (int)__reduce_add_sync(FULL, (unsigned)c);
+        if (lane == 0) {
+            off[t] = c <= thr ? c : 0;
+            desc[t] = c;
+        }
+    }
+    PDL_TRIGGER();
+}
+__global__ void __launch_bounds__(256) k_ci_fill(int64_t d, int64_t kp, int k, const float *__restrict__ ct, int thr,
+                                                 const int64_t *__restrict__ off, int64_t *desc, int2 *pairs,
+                                                 const long long *__restrict__ ctl) {
+    PDL_ENTRY();
+    if (ctl[1]) return;
+    const int lane = threadIdx.x & 31;
+    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
+    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < d; t += warps) {
+        const int c = (int)desc[t];
+        __syncwarp();
+        if (c > thr) {
+            if (lane == 0) desc[t] = 0xFFF;
+            continue;
+        }
+        const int64_t base = off[t];
+        const float *row = ct + t * kp;
+        int pos = 0;
+        for (int j0 = 4 * lane, jb = 0; jb < k; j0 += 128, jb += 128) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (j0 < k) v = __ldg(reinterpret_cast<const float4 *>(row + j0));
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+            int m = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) m += (j0 + q < k && vv[q] != 0.f);
+            int x = m;   // inclusive prefix over the lanes
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
+            }
+            int w = pos + x - m;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (j0 + q < k && vv[q] != 0.f) pairs[base + w++] = make_int2(j0 + q, __float_as_int(vv[q]));
+            pos += __shfl_sync(FULL, x, 31);
+        }
+        DCHECK(pos == c);
+        if (lane == 0) desc[t] = (base << 12) | (int64_t)c;
+    }
+    PDL_TRIGGER();
+}
 
 // ------------------------------------------------------ Yin-Yang family
 // Group bounds (Ding et al., ICML 2015, carried over to cosine similarities
@@ -3407,9 +3567,15 @@ int grid_for(int64_t work_items, int per_block) {
     return (int)(g < 1 ? 1 : g);
 }
 
-template <int CH, int NT, bool HALF>
+template <int CH, int NT, int GV>
 int launch_rp(RowPassArgs &A, int grid, size_t smem, cudaStream_t st) {
-    pdl_launch(k_row_pass<CH, NT, HALF>, dim3(grid), dim3(NT), smem, st, A);
+    if (GV == 2) {   // + kp floats of accumulators per warp
+        smem += (size_t)(NT / 32) * A.kp * sizeof(float);
+        const cudaError_t e = cudaFuncSetAttribute(k_row_pass<CH, NT, GV>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                   (int)smem);
+        if (e != cudaSuccess) return fail("row_pass smem attribute", e);
+    }
+    pdl_launch(k_row_pass<CH, NT, GV>, dim3(grid), dim3(NT), smem, st, A);
     CHECK_LAUNCH("row_pass");
     return 0;
 }
@@ -3432,11 +3598,15 @@ int launch_row_pass(RowPassArgs &A, int64_t k, cudaStream_t st, int64_t max_rows
     const size_t smem = (size_t)(256 / 32) * (SPKM_RP_SMEM_GROUPS > p.rpw ? SPKM_RP_SMEM_GROUPS : p.rpw) * kIvStride * 8;
     // fp16 screening for every full pass but predict, when the table exists (k > 128)
     const bool half = A.ct16 != nullptr && A.mode != MODE_PREDICT && p.ch >= 8;
-    if (p.ch == 4) return launch_rp<4, 256, false>(A, grid, smem, st);
-    if (p.ch == 8) return half ? launch_rp<8, 256, true>(A, grid, smem, st) : launch_rp<8, 256, false>(A, grid, smem, st);
+    // sparse center index for every full pass but predict, when built (k > 256)
+    const bool sparse = A.ci_desc != nullptr && A.mode != MODE_PREDICT && p.ch >= 16;
+    if (p.ch == 4) return launch_rp<4, 256, 0>(A, grid, smem, st);
+    if (p.ch == 8) return half ? launch_rp<8, 256, 1>(A, grid, smem, st) : launch_rp<8, 256, 0>(A, grid, smem, st);
     if (p.ch == 16)
-        return half ? launch_rp<16, 256, true>(A, grid, smem, st) : launch_rp<16, 256, false>(A, grid, smem, st);
-    return half ? launch_rp<32, 256, true>(A, grid, smem, st) : launch_rp<32, 256, false>(A, grid, smem, st);
+        return sparse ? launch_rp<16, 256, 2>(A, grid, smem, st)
+                      : half ? launch_rp<16, 256, 1>(A, grid, smem, st) : launch_rp<16, 256, 0>(A, grid, smem, st);
+    return sparse ? launch_rp<32, 256, 2>(A, grid, smem, st)
+                  : half ? launch_rp<32, 256, 1>(A, grid, smem, st) : launch_rp<32, 256, 0>(A, grid, smem, st);
 }
 
 // Term rows of the Zipf head kept in L2 by the gathers' eviction hints:
@@ -3464,6 +3634,10 @@ RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     A.hot = hot_terms(C);
     A.ct16 = reinterpret_cast<const __half *>(C->ct16);
     A.d = X->d;
+    if (C->cindex) {
+        A.ci_desc = C->cindex->desc;
+        A.ci_pairs = reinterpret_cast<const int2 *>(C->cindex->pairs);
+    }
     return A;
 }
 
@@ -4457,6 +4631,30 @@ int spkm_permute_rows(int64_t n, const int64_t *ip_raw, const int32_t *idx_raw, 
     return 0;
 }
 
+
+int64_t spkm_cindex_scratch_bytes(int64_t d) {
+    size_t t = 0;
+    cub::DeviceScan::ExclusiveSum(nullptr, t, (const int64_t *)nullptr, (int64_t *)nullptr, (int)(d > 0 ? d : 1));
+    return (int64_t)t;
+}
+
+int spkm_cindex_build(const spkm_centers *C, void *stream) {
+    const spkm_cindex *I = C->cindex;
+    if (!I) return fail_msg("cindex_build: no index attached");
+    if (C->k > 2047) return fail_msg("cindex_build: k > 2047");
+    cudaStream_t st = S(stream);
+    const int grid = grid_for((C->d + 7) / 8, 1);
+    pdl_launch(k_ci_count, dim3(grid), dim3(256), (size_t)0, st, C->d, C->kp, (int)C->k, C->ct32, I->dense_thr, I->off,
+               I->desc, C->ctl);
+    CHECK_LAUNCH("ci_count");
+    size_t tb = (size_t)I->scratch_bytes;
+    if (cub::DeviceScan::ExclusiveSum(I->scratch, tb, I->off, I->off, (int)C->d, st) != cudaSuccess)
+        return fail_msg("cindex_build: scan failed");
+    pdl_launch(k_ci_fill, dim3(grid), dim3(256), (size_t)0, st, C->d, C->kp, (int)C->k, C->ct32, I->dense_thr, I->off,
+               I->desc, reinterpret_cast<int2 *>(I->pairs), C->ctl);
+    CHECK_LAUNCH("ci_fill");
+    return 0;
+}
 
 // ------------------------------------------------- corpus layout (prepare.cuh)
 int64_t spkm_prepare_scratch_bytes(int64_t n, int64_t d) {

@@ -23,6 +23,7 @@ reference's 50-iteration scratch rebuild is a no-op, kept for its schedule).
 
 from __future__ import annotations
 
+import ctypes
 import math
 import os
 import time
@@ -567,6 +568,7 @@ class CenterState:
             self.tiles = torch.from_numpy(pairs).to(dev)
             self.gram = torch.empty(int(L.spkm_gram_scratch_doubles(k, d)), **f64)
         self.dense = None
+        self.cindex = None
         self.struct = Centers(k, d, self.kp, self.scale_bits, 0, _ptr(self.cent64), _ptr(self.ct32),
                               _ptr(self.sums), _ptr(self.counts), _ptr(self.drift), _ptr(self.sinp),
                               _ptr(self.touched), _ptr(self.objc), _ptr(self.part), _ptr(self.norm), _ptr(self.cc),
@@ -590,6 +592,25 @@ class CenterState:
             raise ValueError(f"centers must be {self.k} x {self.d}")
         _lib.call("spkm_load_centers", self.struct, _ptr(src), stream)
         return src  # keep alive until the stream passes
+
+    def attach_cindex(self, capacity: int):
+        """Sparse term-major index of the centers for the full pass (k > 256):
+        pairs for term rows with at most kp/4 nonzero centers (spkm_cindex)."""
+        L = _lib.lib()
+        dev = self.cent64.device
+        cap = max(int(min(capacity, self.k * self.d)), 1)
+        nb = int(L.spkm_cindex_scratch_bytes(self.d))
+        self._ci = (torch.empty(max(self.d, 1), dtype=torch.int64, device=dev),
+                    torch.empty(2 * cap, dtype=torch.int32, device=dev),
+                    torch.empty(max(self.d, 1), dtype=torch.int64, device=dev),
+                    torch.empty(max(nb, 1), dtype=torch.uint8, device=dev))
+        self.cindex = _lib.CIndex(_ptr(self._ci[0]), _ptr(self._ci[1]), _ptr(self._ci[2]), _ptr(self._ci[3]), nb, cap,
+                                  self.kp // 4, 0)
+        self.struct.cindex = ctypes.addressof(self.cindex)
+
+    def build_cindex(self, sp):
+        if self.cindex is not None:
+            _lib.call("spkm_cindex_build", self.struct, sp)
 
     def attach_dense(self, corpus: "DeviceCorpus", row0: int = 0, n_rows: int = 0, rescan: bool = False):
         """float32 center rows (padded to 256) for the dense tensor-core pass
@@ -755,6 +776,10 @@ class Engine:
             _ptr(cs.reps) + 4 * self.p0)
         if self.dense:
             self.C.attach_dense(self.corpus, row0=self.p0, n_rows=self.n_loc, rescan=self.hamerly)
+        # sparse center index for the full passes (k > 256; SPKM_CSPARSE=1)
+        if (not self.dense and k > 256 and variant in ("standard", "hamerly", "simp_hamerly")
+                and os.environ.get("SPKM_CSPARSE") == "1"):
+            self.C.attach_cindex(self.corpus.nnz)
         self.P = PointState(self.n_loc, k, variant, self.device)
         self.a_global = torch.zeros(max(cs.n, 1), dtype=torch.int32, device=self.device) if comm is not None else None
         # a dedicated stream: steady-state iterations are replayed as one CUDA graph
@@ -881,6 +906,7 @@ class Engine:
                 else _lib.MODE_INIT_YINYANG if self.yy else _lib.MODE_INIT_PLAIN)
         if self.dense:
             return self._dense(mode)
+        self.C.build_cindex(self.sp)
         _lib.call("spkm_full_assign", self.xs, self.C.struct, self.P.bounds, self.P.work, mode, self.sp)
 
     def scratch_sums(self):
@@ -898,6 +924,7 @@ class Engine:
     def lloyd_pass(self):
         if self.dense:
             return self._dense(_lib.MODE_LLOYD)
+        self.C.build_cindex(self.sp)
         _lib.call("spkm_full_assign", self.xs, self.C.struct, self.P.bounds, self.P.work,
                   _lib.MODE_LLOYD, self.sp)
 
@@ -927,6 +954,7 @@ class Engine:
         elif self.dense:
             self._dense(_lib.DMODE_RESCAN_H, use_flag)   # tighten + full scan on the canonical TC values
         else:
+            self.C.build_cindex(self.sp)
             _lib.call("spkm_hamerly_tighten", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
             _lib.call("spkm_hamerly_rescan", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
 

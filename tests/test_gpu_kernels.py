@@ -532,3 +532,26 @@ def test_cluster_ordered_worklists_give_identical_fits(variant, graphs, monkeypa
     assert [key(s) for s in a.iterations] == [key(s) for s in b.iterations]
 
 
+
+
+@pytest.mark.parametrize("k", [300, 1000])
+@pytest.mark.parametrize("variant", ["standard", "hamerly", "simp_hamerly"])
+def test_sparse_center_index_full_pass_equals_dense(k, variant, monkeypatch):
+    """SPKM_CSPARSE=1: the full passes gather the centers through the sparse
+    term-major index (spkm_cindex) -- the same canonical chains, so the fit is
+    the dense-gather fit bit for bit, counters included."""
+    from paper_2107_04074_b200 import engine, synth
+    m = spk()
+    data = synth.config_dataset("C3", n_override=20_000)
+    engine.clear_engine_cache()
+    monkeypatch.delenv("SPKM_CSPARSE", raising=False)
+    ref = m.run(data, k, variant, m.SeedConfig(seed=3), max_iter=30)
+    monkeypatch.setenv("SPKM_CSPARSE", "1")
+    engine.clear_engine_cache()
+    for graphs in (False, True, True):
+        r = m.run(data, k, variant, m.SeedConfig(seed=3), max_iter=30, use_graphs=graphs)
+        assert np.array_equal(r.assignments, ref.assignments)
+        assert r.objective == ref.objective
+        key = lambda s: (s.sim_count, s.reassignments, s.survivors, s.survivors2, s.nnz_rescan)  # noqa: E731
+        assert [key(s) for s in r.iterations] == [key(s) for s in ref.iterations]
+    engine.clear_engine_cache()

@@ -363,17 +363,24 @@ struct RowPassArgs {
 // (j, value) pairs, one pair per lane.  Zeros contribute nothing to the FMA
 // chain, so every s~(i, j) is the canonical chain (ties and all).  The
 // lanes then pick up their CH columns into registers for the epilogue.
+// One row per warp (k > 256): lanes 0..tpr-1 own the columns (own), every
+// lane loads nnz and pairs; the row's start and length come from lane 0.
 template <int CH>
-__device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPassArgs &A, float *sacc, int64_t s,
-                                                  int len, int maxlen, int lane, int j0, uint64_t pol_hot,
+__device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPassArgs &A, float *sacc, int64_t s_own,
+                                                  int len_own, bool own, int lane, int j0, uint64_t pol_hot,
                                                   uint64_t pol_cold) {
     const int jstr = 4 * A.tpr;
+    const int64_t s = __shfl_sync(FULL, s_own, 0);
+    const int maxlen = __shfl_sync(FULL, len_own, 0);
+    if (own) {
 #pragma unroll
-    for (int r = 0; r < CH / 4; ++r) *reinterpret_cast<float4 *>(sacc + j0 + r * jstr) = make_float4(0.f, 0.f, 0.f, 0.f);
+        for (int r = 0; r < CH / 4; ++r)
+            *reinterpret_cast<float4 *>(sacc + j0 + r * jstr) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     __syncwarp();
     bool last_sparse = true;
     for (int c0 = 0; c0 < maxlen; c0 += 32) {
-        const int cnt = max(0, min(32, len - c0));
+        const int cnt = min(32, maxlen - c0);
         int id = 0;
         float v = 0.f;
         long long dsc = 0;
@@ -388,13 +395,15 @@ __device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPas
             const float tv = __shfl_sync(FULL, v, t);
             const long long td = __shfl_sync(FULL, dsc, t);
             const int n = (int)(td & 0xFFF);
-            if (n == 0xFFF) {   // dense term row: the owner lanes, float4 per column group
+            if (n == 0xFFF) {   // dense term row: the owner lanes, float4 per column group (n, last_sparse: warp-uniform)
+                if (last_sparse) __syncwarp();
+                last_sparse = false;
+                if (!own) continue;
                 const float4 *p = reinterpret_cast<const float4 *>(A.ct + (int64_t)tid * A.kp + j0);
                 const uint64_t pol = tid < A.hot ? pol_hot : pol_cold;
                 float4 x[CH / 4];
 #pragma unroll
                 for (int r = 0; r < CH / 4; ++r) x[r] = ldg_hint(p + r * A.tpr, pol);
-                if (last_sparse) __syncwarp();
 #pragma unroll
                 for (int r = 0; r < CH / 4; ++r) {
                     float4 *ap = reinterpret_cast<float4 *>(sacc + j0 + r * jstr);
@@ -405,13 +414,15 @@ __device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPas
                     a.w = __fmaf_rn(tv, x[r].w, a.w);
                     *ap = a;
                 }
-                last_sparse = false;
             } else if (n > 0) {   // sparse term row: its pairs, one per lane (distinct j within a row)
                 const int2 *pp = A.ci_pairs + (td >> 12);
                 int2 e[8];
 #pragma unroll
                 for (int m = 0; m < 8; ++m)
-                    if (lane + 32 * m < n) e[m] = __ldg(pp + lane + 32 * m);
+                    if (lane + 32 * m < n) {
+                    e[m] = __ldg(pp + lane + 32 * m);
+                    DCHECK((uint32_t)e[m].x < (uint32_t)A.k);
+                }
                 __syncwarp();   // earlier terms' updates (any lane) are visible
 #pragma unroll
                 for (int m = 0; m < 8; ++m)
@@ -426,7 +437,7 @@ __device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPas
     }
     __syncwarp();
 #pragma unroll
-    for (int r = 0; r < CH / 4; ++r) {
+    for (int r = 0; r < CH / 4; ++r) {   // (lanes that own no columns read a duplicate; their row is not valid)
         const float4 a = *reinterpret_cast<const float4 *>(sacc + j0 + r * jstr);
         acc[4 * r + 0] = a.x;
         acc[4 * r + 1] = a.y;
@@ -603,7 +614,7 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
         const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
         if constexpr (SPARSE)
             row_gather_sparse<CH>(acc, A, reinterpret_cast<float *>(s_iv + 8 * A.rpw * kIvStride) + wib * A.kp, s, len,
-                                  maxlen, lane, j0, pol_hot, pol_cold);
+                                  lane_on, lane, j0, pol_hot, pol_cold);
         else
             row_gather<CH, UBH, HALF>(acc, A, my_iv, s, len, maxlen, q, j0, pol_hot, pol_cold);
         const bool incumbent_mode = (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN);

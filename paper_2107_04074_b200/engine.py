@@ -776,9 +776,9 @@ class Engine:
             _ptr(cs.reps) + 4 * self.p0)
         if self.dense:
             self.C.attach_dense(self.corpus, row0=self.p0, n_rows=self.n_loc, rescan=self.hamerly)
-        # sparse center index for the full passes (k > 256; SPKM_CSPARSE=1)
-        if (not self.dense and k > 256 and variant in ("standard", "hamerly", "simp_hamerly")
-                and os.environ.get("SPKM_CSPARSE") == "1"):
+        # sparse center index for the full passes (k > 256; SPKM_CSPARSE=0 turns
+        # it off): C4 full pass 222 -> 134 ms, Hamerly rescan -34% (profiles/r02_ab_notes.txt)
+        if not self.dense and k > 256 and os.environ.get("SPKM_CSPARSE", "1") != "0":
             self.C.attach_cindex(self.corpus.nnz)
         self.P = PointState(self.n_loc, k, variant, self.device)
         self.a_global = torch.zeros(max(cs.n, 1), dtype=torch.int32, device=self.device) if comm is not None else None

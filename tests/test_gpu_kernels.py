@@ -535,7 +535,7 @@ def test_cluster_ordered_worklists_give_identical_fits(variant, graphs, monkeypa
 
 
 @pytest.mark.parametrize("k", [300, 1000])
-@pytest.mark.parametrize("variant", ["standard", "hamerly", "simp_hamerly"])
+@pytest.mark.parametrize("variant", ["standard", "hamerly", "simp_hamerly", "elkan", "yinyang"])
 def test_sparse_center_index_full_pass_equals_dense(k, variant, monkeypatch):
     """SPKM_CSPARSE=1: the full passes gather the centers through the sparse
     term-major index (spkm_cindex) -- the same canonical chains, so the fit is
@@ -544,7 +544,7 @@ def test_sparse_center_index_full_pass_equals_dense(k, variant, monkeypatch):
     m = spk()
     data = synth.config_dataset("C3", n_override=20_000)
     engine.clear_engine_cache()
-    monkeypatch.delenv("SPKM_CSPARSE", raising=False)
+    monkeypatch.setenv("SPKM_CSPARSE", "0")
     ref = m.run(data, k, variant, m.SeedConfig(seed=3), max_iter=30)
     monkeypatch.setenv("SPKM_CSPARSE", "1")
     engine.clear_engine_cache()

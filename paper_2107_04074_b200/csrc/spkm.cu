@@ -363,6 +363,9 @@ struct RowPassArgs {
 // (j, value) pairs, one pair per lane.  Zeros contribute nothing to the FMA
 // chain, so every s~(i, j) is the canonical chain (ties and all).  The
 // lanes then pick up their CH columns into registers for the epilogue.
+#ifndef SPKM_SP_PREFETCH
+#define SPKM_SP_PREFETCH 1
+#endif
 // One row per warp (k > 256): lanes 0..tpr-1 own the columns (own), every
 // lane loads nnz and pairs; the row's start and length come from lane 0.
 template <int CH>
@@ -389,6 +392,23 @@ __device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPas
             v = __ldg(A.values + s + c0 + lane);
             DCHECK((uint64_t)id < (uint64_t)A.d);
             dsc = __ldg(reinterpret_cast<const long long *>(A.ci_desc) + id);
+#if SPKM_SP_PREFETCH
+            // one bulk L2 prefetch per term of the chunk (its pair list or its
+            // dense row): the per-term loads below then find them in L2
+            const int n = (int)(dsc & 0xFFF);
+            uintptr_t a0;
+            uint32_t bytes;
+            if (n == 0xFFF) {
+                a0 = reinterpret_cast<uintptr_t>(A.ct + (int64_t)id * A.kp);
+                bytes = (uint32_t)(A.kp * 4);
+            } else {
+                const uintptr_t b = reinterpret_cast<uintptr_t>(A.ci_pairs + (dsc >> 12));
+                a0 = b & ~(uintptr_t)15;
+                bytes = (uint32_t)(((b + (uintptr_t)n * 8 - a0) + 15) & ~(uintptr_t)15);
+            }
+            if (n != 0 && id >= A.hot)
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(bytes) : "memory");
+#endif
         }
         for (int t = 0; t < cnt; ++t) {
             const int tid = __shfl_sync(FULL, id, t);

@@ -601,7 +601,7 @@ class CenterState:
         cap = max(int(min(capacity, self.k * self.d)), 1)
         nb = int(L.spkm_cindex_scratch_bytes(self.d))
         self._ci = (torch.empty(max(self.d, 1), dtype=torch.int64, device=dev),
-                    torch.empty(2 * cap, dtype=torch.int32, device=dev),
+                    torch.empty(2 * cap + 8, dtype=torch.int32, device=dev),   # + slack for 16-byte bulk prefetches
                     torch.empty(max(self.d, 1), dtype=torch.int64, device=dev),
                     torch.empty(max(nb, 1), dtype=torch.uint8, device=dev))
         self.cindex = _lib.CIndex(_ptr(self._ci[0]), _ptr(self._ci[1]), _ptr(self._ci[2]), _ptr(self._ci[3]), nb, cap,

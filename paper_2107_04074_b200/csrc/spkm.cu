@@ -364,7 +364,7 @@ struct RowPassArgs {
 // chain, so every s~(i, j) is the canonical chain (ties and all).  The
 // lanes then pick up their CH columns into registers for the epilogue.
 #ifndef SPKM_SP_PREFETCH
-#define SPKM_SP_PREFETCH 1
+#define SPKM_SP_PREFETCH 0        // per-term bulk L2 prefetch: measured slower at C4 (2267 vs 2184 ms per fit)
 #endif
 // One row per warp (k > 256): lanes 0..tpr-1 own the columns (own), every
 // lane loads nnz and pairs; the row's start and length come from lane 0.

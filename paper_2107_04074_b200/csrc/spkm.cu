@@ -564,7 +564,7 @@ __device__ __forceinline__ void row_gather(float (&acc)[CH], const RowPassArgs &
 // all 32 lanes; lane owns the float4 column groups 4 lane + 128 r): the
 // sparse center index exactly as row_gather_sparse.  Used by the Elkan scan
 // for rows whose failing blocks are many.
-__device__ __noinline__ void row_sims_sparse(float *sacc, const int32_t *__restrict__ indices,
+__device__ __forceinline__ void row_sims_sparse(float *sacc, const int32_t *__restrict__ indices,
                                                 const float *__restrict__ values, int64_t s, int len,
                                                 const float *__restrict__ ct, int64_t kp,
                                                 const int64_t *__restrict__ desc, const int2 *__restrict__ pairs,
@@ -1454,12 +1454,9 @@ __global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_E
                 sp = tight && nf * 100 >= SPKM_EK_SP_PCT * nb;
             }
         }
-        // (16-byte aligned row buffer inside the warp's similarity slice; the
-        // launcher checks kp + 4 <= the slice)
-        float *const sacc = reinterpret_cast<float *>((reinterpret_cast<uintptr_t>(my_sim) + 15) & ~uintptr_t(15));
         if (sp) {
-            row_sims_sparse(sacc, indices, values, s, len, ct, kp, ci_desc, ci_pairs, hot, pol_hot, pol_cold, lane);
-            lcur = sacc[ai];
+            row_sims_sparse(my_sim, indices, values, s, len, ct, kp, ci_desc, ci_pairs, hot, pol_hot, pol_cold, lane);
+            lcur = my_sim[ai];
         } else {
         // (B) s~(i, a(i)) -- the canonical chain for the single center a(i),
         // as k_hamerly_tighten: the group's lanes stage (value, center value)
@@ -1655,7 +1652,7 @@ __global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_E
                         if (j < start || j == ai || j == cur) continue;
                         if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
                         if ((double)ui[j] + eps <= lc) continue;
-                        if ((sp ? sacc[blk * EB + c2] : my_sim[blk * ES + c2]) > lcur) {
+                        if ((sp ? my_sim[blk * EB + c2] : my_sim[blk * ES + c2]) > lcur) {
                             ev = j;
                             break;
                         }
@@ -1684,13 +1681,13 @@ __global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_E
                             if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
                             if ((double)ui[j] + eps <= lc) continue;
                         }
-                        ui[j] = store_upper((double)(sp ? sacc[blk * EB + c2] : my_sim[blk * ES + c2]) + eps);
+                        ui[j] = store_upper((double)(sp ? my_sim[blk * EB + c2] : my_sim[blk * ES + c2]) + eps);
                         ++sims;
                     }
                 }
                 if (gev != NONE) {
                     cur = gev;
-                    lcur = sp ? sacc[gev] : my_sim[(gev >> (EB == 4 ? 2 : 3)) * ES + (gev & (EB - 1))];
+                    lcur = sp ? my_sim[gev] : my_sim[(gev >> (EB == 4 ? 2 : 3)) * ES + (gev & (EB - 1))];
                     start = gev + 1;
                 } else {
                     active_g = false;
@@ -4273,7 +4270,7 @@ static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_boun
     cudaError_t attr = cudaSuccess;
     // the sparse center index for the unfused EB = 8 scan (k > 256), when
     // built and its row buffer fits the per-warp similarity slice
-    const bool ci_ok = C->cindex != nullptr && !fuse && elkan_block(C->k) == 8 && C->kp + 4 <= elkan_sim_stride(C->k);
+    const bool ci_ok = C->cindex != nullptr && !fuse && elkan_block(C->k) == 8 && C->kp <= elkan_sim_stride(C->k);
     const int64_t *cid = ci_ok ? C->cindex->desc : nullptr;
     const int2 *cip = ci_ok ? reinterpret_cast<const int2 *>(C->cindex->pairs) : nullptr;
     auto launch = [&](auto kern) {

@@ -560,82 +560,6 @@ __device__ __forceinline__ void row_gather(float (&acc)[CH], const RowPassArgs &
     }
 }
 
-// Every canonical similarity of one row into sacc[0, kp) (one row per warp,
-// all 32 lanes; lane owns the float4 column groups 4 lane + 128 r): the
-// sparse center index exactly as row_gather_sparse.  Used by the Elkan scan
-// for rows whose failing blocks are many.
-__device__ __forceinline__ void row_sims_sparse(float *sacc, const int32_t *__restrict__ indices,
-                                                const float *__restrict__ values, int64_t s, int len,
-                                                const float *__restrict__ ct, int64_t kp,
-                                                const int64_t *__restrict__ desc, const int2 *__restrict__ pairs,
-                                                int64_t hot, uint64_t pol_hot, uint64_t pol_cold, int lane) {
-#pragma unroll
-    for (int r = 0; r < 8; ++r) {
-        const int j = 4 * lane + 128 * r;
-        if (j < kp) *reinterpret_cast<float4 *>(sacc + j) = make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    __syncwarp();
-    bool last_sparse = true;
-    for (int c0 = 0; c0 < len; c0 += 32) {
-        const int cnt = min(32, len - c0);
-        int id = 0;
-        float v = 0.f;
-        long long dsc = 0;
-        if (lane < cnt) {
-            id = __ldg(indices + s + c0 + lane);
-            v = __ldg(values + s + c0 + lane);
-            dsc = __ldg(reinterpret_cast<const long long *>(desc) + id);
-        }
-        for (int t = 0; t < cnt; ++t) {
-            const int tid = __shfl_sync(FULL, id, t);
-            const float tv = __shfl_sync(FULL, v, t);
-            const long long td = __shfl_sync(FULL, dsc, t);
-            const int n = (int)(td & 0xFFF);
-            if (n == 0xFFF) {
-                if (last_sparse) __syncwarp();
-                last_sparse = false;
-                const float *rowp = ct + (int64_t)tid * kp;
-                const uint64_t pol = tid < hot ? pol_hot : pol_cold;
-                float4 x[8];
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const int j = 4 * lane + 128 * r;
-                    if (j < kp) x[r] = ldg_hint(reinterpret_cast<const float4 *>(rowp + j), pol);
-                }
-#pragma unroll
-                for (int r = 0; r < 8; ++r) {
-                    const int j = 4 * lane + 128 * r;
-                    if (j < kp) {
-                        float4 *ap = reinterpret_cast<float4 *>(sacc + j);
-                        float4 aa = *ap;
-                        aa.x = __fmaf_rn(tv, x[r].x, aa.x);
-                        aa.y = __fmaf_rn(tv, x[r].y, aa.y);
-                        aa.z = __fmaf_rn(tv, x[r].z, aa.z);
-                        aa.w = __fmaf_rn(tv, x[r].w, aa.w);
-                        *ap = aa;
-                    }
-                }
-            } else if (n > 0) {
-                const int2 *pp = pairs + (td >> 12);
-                int2 e[8];
-#pragma unroll
-                for (int m = 0; m < 8; ++m)
-                    if (lane + 32 * m < n) e[m] = __ldg(pp + lane + 32 * m);
-                __syncwarp();
-#pragma unroll
-                for (int m = 0; m < 8; ++m)
-                    if (lane + 32 * m < n) sacc[e[m].x] = __fmaf_rn(tv, __int_as_float(e[m].y), sacc[e[m].x]);
-                for (int p2 = lane + 256; p2 < n; p2 += 32) {
-                    const int2 f = __ldg(pp + p2);
-                    sacc[f.x] = __fmaf_rn(tv, __int_as_float(f.y), sacc[f.x]);
-                }
-                last_sparse = true;
-            }
-        }
-    }
-    __syncwarp();
-}
-
 // fp16 screening (k_row_pass<.., HALF>): candidates per row whose exact value
 // is re-checked on ct32; more in a row -> the warp re-gathers in fp32.
 constexpr int kCand = 8;
@@ -1291,9 +1215,6 @@ __host__ __device__ __forceinline__ int64_t elkan_sim_stride(int64_t k) {
 // same lanes that later test and scan them), so the bound pass, its survivor
 // list and one read of u are saved; rows that survive go straight on.
 template <int EB, bool FUSE>
-#ifndef SPKM_EK_SP_PCT
-#define SPKM_EK_SP_PCT 50     // Elkan rows with >= this % of blocks failing at the untightened bound: sparse sims
-#endif
 #ifndef SPKM_EK_MINB
 #define SPKM_EK_MINB 4        // EB = 8 (k > 128): 64 registers, 4 CTAs per SM (C4 scan 3590 -> 3350 ms per fit)
 #endif
@@ -1312,9 +1233,7 @@ __global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_E
                                                     const double *__restrict__ drift,
                                                     const double *__restrict__ sinp,
                                                     const float *__restrict__ s_arr,
-                                                    const long long *__restrict__ ctl, int64_t hot,
-                                                    const int64_t *__restrict__ ci_desc,
-                                                    const int2 *__restrict__ ci_pairs) {
+                                                    const long long *__restrict__ ctl, int64_t hot) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
@@ -1426,41 +1345,10 @@ __global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_E
         }
         first_fail = __shfl_sync(FULL, first_fail, lane - q);
         const bool tight = valid && first_fail != NONE;
-        // sparse center index (k > 256, one row per warp): rows with many
-        // failing blocks at the untightened bound get every similarity from
-        // the index (row_sims_sparse; s~(i, a) included) instead of the
-        // tighten chain + active-block gathers below; the replay reads them
-        // from the same buffer.  Same values, so same results and counters.
-        float lcur = 0.f;
-        bool sp = false;
-        if constexpr (EB == 8 && !FUSE) {
-            if (ci_desc != nullptr && ppw == 1) {
-                int nf = 0;
-                if (tight) {
-                    for (int r = 0; r < nrounds; ++r) {
-                        const int blk = r * 32 + q;
-                        if (blk >= nb) break;
-                        bool f = false;
-                        for (int c2 = 0; c2 < EB; ++c2) {
-                            const int j = blk * EB + c2;
-                            if (j >= k) break;
-                            if (j < first_fail || j == ai) continue;
-                            f |= ui[j] > thu_s;
-                        }
-                        nf += f;
-                    }
-                }
-                nf = (int)__reduce_add_sync(FULL, (unsigned)nf);
-                sp = tight && nf * 100 >= SPKM_EK_SP_PCT * nb;
-            }
-        }
-        if (sp) {
-            row_sims_sparse(my_sim, indices, values, s, len, ct, kp, ci_desc, ci_pairs, hot, pol_hot, pol_cold, lane);
-            lcur = my_sim[ai];
-        } else {
         // (B) s~(i, a(i)) -- the canonical chain for the single center a(i),
         // as k_hamerly_tighten: the group's lanes stage (value, center value)
         // pairs of each 32-nnz chunk, the leader runs the chain in CSR order
+        float lcur = 0.f;
         const int tlen = tight ? len : 0;
         const int maxt = (int)__reduce_max_sync(FULL, (unsigned)tlen);
         if (maxt > 0) {
@@ -1618,8 +1506,6 @@ __global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_E
             }
         }
         __syncwarp();
-        }   // !sp
-        __syncwarp();
         // (D) replay of kernels.py:35-65, parallel over the group's lanes.
         // Lane q owns the centers of blocks q, q+32, ... (ascending j within
         // the lane).  With the running best (cur, lcur) every lane finds its
@@ -1652,7 +1538,7 @@ __global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_E
                         if (j < start || j == ai || j == cur) continue;
                         if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
                         if ((double)ui[j] + eps <= lc) continue;
-                        if ((sp ? my_sim[blk * EB + c2] : my_sim[blk * ES + c2]) > lcur) {
+                        if (my_sim[blk * ES + c2] > lcur) {
                             ev = j;
                             break;
                         }
@@ -1681,13 +1567,13 @@ __global__ void __launch_bounds__(256, (EB == 8 || FUSE) ? SPKM_EK_MINB : SPKM_E
                             if (ccok2 && (double)cc[(int64_t)cur * k + j] + kSqrt2 * eps <= lc - eps) continue;
                             if ((double)ui[j] + eps <= lc) continue;
                         }
-                        ui[j] = store_upper((double)(sp ? my_sim[blk * EB + c2] : my_sim[blk * ES + c2]) + eps);
+                        ui[j] = store_upper((double)my_sim[blk * ES + c2] + eps);
                         ++sims;
                     }
                 }
                 if (gev != NONE) {
                     cur = gev;
-                    lcur = sp ? my_sim[gev] : my_sim[(gev >> (EB == 4 ? 2 : 3)) * ES + (gev & (EB - 1))];
+                    lcur = my_sim[(gev >> (EB == 4 ? 2 : 3)) * ES + (gev & (EB - 1))];
                     start = gev + 1;
                 } else {
                     active_g = false;
@@ -4268,11 +4154,6 @@ static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_boun
     const size_t dyn = (size_t)8 * elkan_sim_stride(C->k) * sizeof(float) + (size_t)8 * ppw_k * kIvStride * sizeof(int2) +
                        SPKM_EK_SMEM_PAD;
     cudaError_t attr = cudaSuccess;
-    // the sparse center index for the unfused EB = 8 scan (k > 256), when
-    // built and its row buffer fits the per-warp similarity slice
-    const bool ci_ok = C->cindex != nullptr && !fuse && elkan_block(C->k) == 8 && C->kp <= elkan_sim_stride(C->k);
-    const int64_t *cid = ci_ok ? C->cindex->desc : nullptr;
-    const int2 *cip = ci_ok ? reinterpret_cast<const int2 *>(C->cindex->pairs) : nullptr;
     auto launch = [&](auto kern) {
         // static smem (staging + active lists) + dyn must fit the opt-in
         // limit; set per launch (cheap), so it holds for every instantiation
@@ -4281,7 +4162,7 @@ static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_boun
         if (attr != cudaSuccess) return;
         pdl_launch(kern, dim3(grid), dim3(256), dyn, S(stream), X->indptr, X->indices, X->values, X->row_eps, C->ct32,
                    C->kp, (int)C->k, B->a, B->l, B->u, B->ku, C->cc, use_cc, W->surv1, W->mv_i, W->mv_old, W->ctr,
-                   X->n, C->drift, C->sinp, C->s, C->ctl, hot_terms(C), cid, cip);
+                   X->n, C->drift, C->sinp, C->s, C->ctl, hot_terms(C));
     };
     auto launch_r1 = [&](auto kern) {   // k <= 128: the round-1 scan (no `hot` argument)
         attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn);

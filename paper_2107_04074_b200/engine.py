@@ -950,7 +950,6 @@ class Engine:
         if self.yy:
             _lib.call("spkm_yy_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, self.sp)
         elif self.elkan:
-            self.C.build_cindex(self.sp)     # the scan's rows with many failing blocks read the index
             _lib.call("spkm_elkan_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
         elif self.dense:
             self._dense(_lib.DMODE_RESCAN_H, use_flag)   # tighten + full scan on the canonical TC values

@@ -421,33 +421,37 @@ __device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPas
                 if (!own) continue;
                 const float4 *p = reinterpret_cast<const float4 *>(A.ct + (int64_t)tid * A.kp + j0);
                 const uint64_t pol = tid < A.hot ? pol_hot : pol_cold;
-                float4 x[CH / 4];
+                // in halves of CH/8 float4: half the registers live (the kernel runs at 64)
 #pragma unroll
-                for (int r = 0; r < CH / 4; ++r) x[r] = ldg_hint(p + r * A.tpr, pol);
+                for (int h = 0; h < 2; ++h) {
+                    float4 x[CH / 8];
 #pragma unroll
-                for (int r = 0; r < CH / 4; ++r) {
-                    float4 *ap = reinterpret_cast<float4 *>(sacc + j0 + r * jstr);
-                    float4 a = *ap;
-                    a.x = __fmaf_rn(tv, x[r].x, a.x);
-                    a.y = __fmaf_rn(tv, x[r].y, a.y);
-                    a.z = __fmaf_rn(tv, x[r].z, a.z);
-                    a.w = __fmaf_rn(tv, x[r].w, a.w);
-                    *ap = a;
+                    for (int r = 0; r < CH / 8; ++r) x[r] = ldg_hint(p + (h * (CH / 8) + r) * A.tpr, pol);
+#pragma unroll
+                    for (int r = 0; r < CH / 8; ++r) {
+                        float4 *ap = reinterpret_cast<float4 *>(sacc + j0 + (h * (CH / 8) + r) * jstr);
+                        float4 a = *ap;
+                        a.x = __fmaf_rn(tv, x[r].x, a.x);
+                        a.y = __fmaf_rn(tv, x[r].y, a.y);
+                        a.z = __fmaf_rn(tv, x[r].z, a.z);
+                        a.w = __fmaf_rn(tv, x[r].w, a.w);
+                        *ap = a;
+                    }
                 }
             } else if (n > 0) {   // sparse term row: its pairs, one per lane (distinct j within a row)
                 const int2 *pp = A.ci_pairs + (td >> 12);
-                int2 e[8];
+                int2 e[4];
 #pragma unroll
-                for (int m = 0; m < 8; ++m)
+                for (int m = 0; m < 4; ++m)
                     if (lane + 32 * m < n) {
-                    e[m] = __ldg(pp + lane + 32 * m);
-                    DCHECK((uint32_t)e[m].x < (uint32_t)A.k);
-                }
+                        e[m] = __ldg(pp + lane + 32 * m);
+                        DCHECK((uint32_t)e[m].x < (uint32_t)A.k);
+                    }
                 __syncwarp();   // earlier terms' updates (any lane) are visible
 #pragma unroll
-                for (int m = 0; m < 8; ++m)
+                for (int m = 0; m < 4; ++m)
                     if (lane + 32 * m < n) sacc[e[m].x] = __fmaf_rn(tv, __int_as_float(e[m].y), sacc[e[m].x]);
-                for (int p2 = lane + 256; p2 < n; p2 += 32) {   // rows beyond 256 pairs (dense_thr > 256)
+                for (int p2 = lane + 128; p2 < n; p2 += 32) {   // rows beyond 128 pairs
                     const int2 f = __ldg(pp + p2);
                     sacc[f.x] = __fmaf_rn(tv, __int_as_float(f.y), sacc[f.x]);
                 }

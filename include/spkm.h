@@ -21,6 +21,7 @@
  *   spkm_hamerly_rescan     kernels.hamerly_scan full-k scan, kernels.py:96-112
  *   spkm_elkan_bounds       Elkan drift update, engine.py:274-283 (fused test)
  *   spkm_elkan_scan         kernels.elkan_scan, kernels.py:22-66
+ *   spkm_elkan_heavy        kernels.elkan_scan for rows the bounds barely prune (full pass)
  *   spkm_aggregate_sums     engine._aggregate_sums, engine.py:130-139
  *   spkm_apply_moves        engine.update_centers (incremental), engine.py:174-188
  *   spkm_move_centers       engine._move_centers, engine.py:142-160
@@ -151,6 +152,8 @@ typedef struct spkm_work {
     double *stats;           /* [16] per-iteration stats, see SPKM_ST_*      */
     double *stats_hist;      /* [hist_cap][16] stats of every iteration      */
     int64_t hist_cap;
+    int64_t elkan_heavy;     /* > 0: spkm_elkan_bounds sends rows with at least this many unpruned
+                              * centers to surv2 for spkm_elkan_heavy                     */
 } spkm_work;
 
 enum {
@@ -211,6 +214,19 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
                       int use_cc, void *stream);
 int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
                     int use_cc, void *stream);
+/* Heavy survivors (kernels.elkan_scan, kernels.py:22-66, for rows whose stored
+ * bounds prune little).  With W->elkan_heavy > 0 spkm_elkan_bounds splits its
+ * survivors: rows where at least W->elkan_heavy centers fail the stored-bound
+ * test go to W->surv2 (count in ctr[SPKM_CTR_SURV2]), the others to W->surv1.
+ * spkm_elkan_heavy takes the surv2 rows through one full pass (over the sparse
+ * center index when C->cindex is attached: spkm_cindex_build first): same
+ * reassignment rule as the scan (incumbent wins ties, else the lowest index),
+ * l and every u(i, j) come back exact, SIMS += k per row.  Call it between
+ * spkm_elkan_bounds and spkm_elkan_scan whenever W->elkan_heavy > 0.
+ * spkm_elkan_heavy_threshold: the library's default for k centers (25% of k
+ * for k > 256, SPKM_EK_HEAVY_PCT overrides; 0 = off). */
+int spkm_elkan_heavy(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream);
+int64_t spkm_elkan_heavy_threshold(int64_t k);
 /* spkm_elkan_bounds + spkm_elkan_scan in one pass over all rows: each row's
  * drift update and prune test are done by the lanes that then scan it (same
  * results and counters as the two calls). */

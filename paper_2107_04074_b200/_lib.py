@@ -69,7 +69,7 @@ class Svml(ctypes.Structure):
 
 class Work(ctypes.Structure):
     _fields_ = [("surv1", c_vp), ("surv2", c_vp), ("mv_i", c_vp), ("mv_old", c_vp), ("ctr", c_vp),
-                ("stats", c_vp), ("stats_hist", c_vp), ("hist_cap", c_i64)]
+                ("stats", c_vp), ("stats_hist", c_vp), ("hist_cap", c_i64), ("elkan_heavy", c_i64)]
 
 
 # modes / enums (include/spkm.h)
@@ -98,6 +98,8 @@ _SIGS = {
     "spkm_yy_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), c_vp],
     "spkm_elkan_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
     "spkm_elkan_bounds_scan": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), ctypes.c_int, c_vp],
+    "spkm_elkan_heavy": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), c_vp],
+    "spkm_elkan_heavy_threshold": [c_i64],
     "spkm_aggregate_sums": [_P(CSR), _P(Centers), _P(Bounds), c_vp, c_vp, c_vp],
     "spkm_order_by_cluster": [c_i64, c_vp, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp],
     "spkm_apply_moves": [_P(CSR), _P(Centers), _P(Bounds), _P(Work), c_vp, c_vp, c_vp, c_vp],
@@ -163,12 +165,13 @@ _RESTYPES = {
     "spkm_prepare_scratch_bytes": c_i64,
     "spkm_gram_partial_floats": c_i64,
     "spkm_cindex_scratch_bytes": c_i64,
+    "spkm_elkan_heavy_threshold": c_i64,
 }
 
 # kernels each entry point launches (for the bench's gpu_launches count)
 KERNELS_PER_CALL = {
     "spkm_full_assign": 1, "spkm_hamerly_bounds": 1, "spkm_hamerly_tighten": 1, "spkm_hamerly_rescan": 1,
-    "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_yy_bounds": 1, "spkm_yy_scan": 1, "spkm_elkan_bounds_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
+    "spkm_elkan_bounds": 1, "spkm_elkan_scan": 1, "spkm_elkan_heavy": 1, "spkm_yy_bounds": 1, "spkm_yy_scan": 1, "spkm_elkan_bounds_scan": 1, "spkm_aggregate_sums": 1, "spkm_apply_moves": 1,
     "spkm_move_centers": 5, "spkm_center_reduce": 1, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,

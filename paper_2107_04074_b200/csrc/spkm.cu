@@ -320,7 +320,9 @@ __device__ __forceinline__ float ldg_hint(const float *p, uint64_t pol) {
     return v;
 }
 
-enum { MODE_RESCAN = 4, MODE_PREDICT = 5, MODE_INIT_YY = SPKM_MODE_INIT_YINYANG };
+// MODE_ELKAN_FULL: the Elkan family's heavy survivors (spkm_elkan_heavy) -- every similarity of the row,
+// reassignment by the scan's rule (incumbent wins ties, else the lowest index), l and every u(i, j) exact
+enum { MODE_RESCAN = 4, MODE_PREDICT = 5, MODE_INIT_YY = SPKM_MODE_INIT_YINYANG, MODE_ELKAN_FULL = 7 };
 
 struct RowPassArgs {
     const int64_t *indptr;
@@ -363,6 +365,12 @@ struct RowPassArgs {
 // (j, value) pairs, one pair per lane.  Zeros contribute nothing to the FMA
 // chain, so every s~(i, j) is the canonical chain (ties and all).  The
 // lanes then pick up their CH columns into registers for the epilogue.
+#ifndef SPKM_EK_HEAVY_PCT_DEFAULT
+#define SPKM_EK_HEAVY_PCT_DEFAULT 25
+#endif
+#ifndef SPKM_SP_EXP
+#define SPKM_SP_EXP 0             // timing probe of register accumulation for dense term rows (not exact)
+#endif
 #ifndef SPKM_SP_PREFETCH
 #define SPKM_SP_PREFETCH 0        // per-term bulk L2 prefetch: measured slower at C4 (2267 vs 2184 ms per fit)
 #endif
@@ -410,11 +418,73 @@ __device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPas
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(bytes) : "memory");
 #endif
         }
+#if SPKM_SP_EXP
+        // TIMING PROBE ONLY (wrong summation order): the chunk's dense term rows first, accumulated in
+        // registers, folded into the shared accumulators once per chunk
+        {
+            unsigned dm = __ballot_sync(FULL, lane < cnt && (int)(dsc & 0xFFF) == 0xFFF);
+            if (dm) {
+                float ra[CH];
+#pragma unroll
+                for (int c = 0; c < CH; ++c) ra[c] = 0.f;
+                while (dm) {
+                    const int t0 = __ffs(dm) - 1;
+                    dm &= dm - 1;
+                    int t1 = -1;
+                    if (dm) {
+                        t1 = __ffs(dm) - 1;
+                        dm &= dm - 1;
+                    }
+                    const int id0 = __shfl_sync(FULL, id, t0), id1 = __shfl_sync(FULL, id, t1 < 0 ? t0 : t1);
+                    const float v0 = __shfl_sync(FULL, v, t0), v1 = t1 < 0 ? 0.f : __shfl_sync(FULL, v, t1 < 0 ? t0 : t1);
+                    if (own) {
+                        const float4 *p0 = reinterpret_cast<const float4 *>(A.ct + (int64_t)id0 * A.kp + j0);
+                        const float4 *p1 = reinterpret_cast<const float4 *>(A.ct + (int64_t)id1 * A.kp + j0);
+                        const uint64_t q0 = id0 < A.hot ? pol_hot : pol_cold, q1 = id1 < A.hot ? pol_hot : pol_cold;
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            float4 x[CH / 8], y[CH / 8];
+#pragma unroll
+                            for (int r = 0; r < CH / 8; ++r) {
+                                x[r] = ldg_hint(p0 + (h * (CH / 8) + r) * A.tpr, q0);
+                                y[r] = ldg_hint(p1 + (h * (CH / 8) + r) * A.tpr, q1);
+                            }
+#pragma unroll
+                            for (int r = 0; r < CH / 8; ++r) {
+                                const int b = 4 * (h * (CH / 8) + r);
+                                ra[b + 0] = __fmaf_rn(v1, y[r].x, __fmaf_rn(v0, x[r].x, ra[b + 0]));
+                                ra[b + 1] = __fmaf_rn(v1, y[r].y, __fmaf_rn(v0, x[r].y, ra[b + 1]));
+                                ra[b + 2] = __fmaf_rn(v1, y[r].z, __fmaf_rn(v0, x[r].z, ra[b + 2]));
+                                ra[b + 3] = __fmaf_rn(v1, y[r].w, __fmaf_rn(v0, x[r].w, ra[b + 3]));
+                            }
+                        }
+                    }
+                }
+                __syncwarp();
+                if (own) {
+#pragma unroll
+                    for (int r = 0; r < CH / 4; ++r) {
+                        float4 *ap = reinterpret_cast<float4 *>(sacc + j0 + r * jstr);
+                        float4 a = *ap;
+                        a.x += ra[4 * r];
+                        a.y += ra[4 * r + 1];
+                        a.z += ra[4 * r + 2];
+                        a.w += ra[4 * r + 3];
+                        *ap = a;
+                    }
+                }
+                __syncwarp();
+            }
+        }
+#endif
         for (int t = 0; t < cnt; ++t) {
             const int tid = __shfl_sync(FULL, id, t);
             const float tv = __shfl_sync(FULL, v, t);
             const long long td = __shfl_sync(FULL, dsc, t);
             const int n = (int)(td & 0xFFF);
+#if SPKM_SP_EXP
+            if (n == 0xFFF) continue;
+#endif
             if (n == 0xFFF) {   // dense term row: the owner lanes, float4 per column group (n, last_sparse: warp-uniform)
                 if (last_sparse) __syncwarp();
                 last_sparse = false;
@@ -641,7 +711,7 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
                                   lane_on, lane, j0, pol_hot, pol_cold);
         else
             row_gather<CH, UBH, HALF>(acc, A, my_iv, s, len, maxlen, q, j0, pol_hot, pol_cold);
-        const bool incumbent_mode = (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN);
+        const bool incumbent_mode = (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN || A.mode == MODE_ELKAN_FULL);
         const int inc = (valid && incumbent_mode) ? A.a[row] : -1;
         DCHECK(!valid || (row >= 0 && row < A.n && inc < A.k));
         if constexpr (HALF) {
@@ -775,6 +845,22 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
                 if (j < A.k) A.u[row * A.ku + j] = store_upper((double)acc[c] + eps);
             }
         }
+        if (A.mode == MODE_ELKAN_FULL && valid) {   // every u(i, j) exact: one 16-byte store per column group (ku % 4 == 0)
+            float *ur = A.u + row * A.ku;
+#pragma unroll
+            for (int r = 0; r < CH / 4; ++r) {
+                const int j = j0 + r * jstr;
+                if (j + 3 < A.k) {
+                    *reinterpret_cast<float4 *>(ur + j) =
+                        make_float4(store_upper((double)acc[4 * r] + eps), store_upper((double)acc[4 * r + 1] + eps),
+                                    store_upper((double)acc[4 * r + 2] + eps), store_upper((double)acc[4 * r + 3] + eps));
+                } else {
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        if (j + c < A.k) ur[j + c] = store_upper((double)acc[4 * r + c] + eps);
+                }
+            }
+        }
         const bool leader = valid && q == 0;
         bool moved = false;
         bool tight_pruned = false;
@@ -813,12 +899,24 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
                     A.l[row] = store_lower((double)tp.b - eps);
                     A.u[row] = store_upper((double)tp.s + eps);
                     break;
+                case MODE_ELKAN_FULL:
+                    if (tp.bj != inc) {
+                        A.a[row] = tp.bj;
+                        moved = true;
+                    }
+                    A.l[row] = store_lower((double)tp.b - eps);
+                    break;
                 case MODE_PREDICT:
                     A.a[row] = tp.bj;
                     A.best[row] = (double)tp.b;
                     A.second[row] = (A.k == 1) ? -1.0 : (double)tp.s;
                     break;
             }
+        }
+        if (A.mode == MODE_ELKAN_FULL) {
+            warp_append(moved, (int32_t)row, A.mv_i, inc, A.mv_old, A.ctr + SPKM_CTR_MOVES);
+            ctr_add(s_ctr, SPKM_CTR_SIMS, leader ? (long long)A.k : 0);
+            ctr_add(s_ctr, SPKM_CTR_NNZ_RESCAN, leader ? (long long)(e - s) : 0);   // (the block scan counts NNZ_ELKAN)
         }
         if (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN) {
             warp_append(moved, (int32_t)row, A.mv_i, inc, A.mv_old, A.ctr + SPKM_CTR_MOVES);
@@ -1085,7 +1183,8 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                                                       const double *__restrict__ sinp,
                                                       const float *__restrict__ cc,
                                                       const float *__restrict__ s_arr, int use_cc,
-                                                      int32_t *surv1, long long *ctr, const long long *__restrict__ ctl) {
+                                                      int32_t *surv1, long long *ctr, const long long *__restrict__ ctl,
+                                                      int heavy_thr, int32_t *surv_h) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ __align__(16) float s_pd[kEbMaxK], s_pu[kEbMaxK], s_su[kEbMaxK];
@@ -1127,7 +1226,7 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
             thc_r = thr_c_of(lb, eps);
         }
         const int nr = (int)min((int64_t)32, n - rb);
-        unsigned smask = 0;
+        unsigned smask = 0, hmask = 0;
         for (int r = 0; r < nr; ++r) {
             const int ai = __shfl_sync(FULL, ai_r, r);
             const float thu = __shfl_sync(FULL, thu_r, r), thc = __shfl_sync(FULL, thc_r, r);
@@ -1141,7 +1240,7 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                 const int q = lane + 32 * t;
                 if (q < k4) v[t] = ui[q];
             }
-            bool any = false;
+            int nfail = 0;
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const int q = lane + 32 * t;
@@ -1164,18 +1263,29 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                         if (j < k && j != ai) {
                             bool skip = ccon && __ldg(cca + j) <= thc;
                             if (!skip) skip = w[cq] <= thu;
-                            any |= !skip;
+                            nfail += skip ? 0 : 1;
                         }
                     }
                 }
             }
-            if (__any_sync(FULL, any)) smask |= 1u << r;
+            // heavy rows (many centers the stored bounds cannot prune) go to the
+            // full pass over the sparse center index (spkm_elkan_heavy), the
+            // others to the block scan; heavy_thr == 0: every survivor is light
+            const int tot = __reduce_add_sync(FULL, nfail);
+            if (tot > 0) {
+                if (heavy_thr > 0 && tot >= heavy_thr) hmask |= 1u << r;
+                else smask |= 1u << r;
+            }
         }
         long long base = 0;
         if (lane == 0 && smask) base = (long long)atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV1),
                                                             (unsigned long long)__popc(smask));
+        if (lane == 1 && hmask) base = (long long)atomicAdd((unsigned long long *)(ctr + SPKM_CTR_SURV2),
+                                                            (unsigned long long)__popc(hmask));
+        const long long base_h = __shfl_sync(FULL, base, 1);
         base = __shfl_sync(FULL, base, 0);
         if (smask >> lane & 1u) surv1[base + __popc(smask & ((1u << lane) - 1u))] = (int32_t)ir;
+        if (hmask >> lane & 1u) surv_h[base_h + __popc(hmask & ((1u << lane) - 1u))] = (int32_t)ir;
     }
     PDL_TRIGGER();
 }
@@ -3656,6 +3766,17 @@ int64_t hot_terms(const spkm_centers *C) {
     return rows < C->d ? rows : C->d;
 }
 
+// Elkan family, k > 256: rows with at least this many centers failing the
+// stored-bound test take the full pass (spkm_elkan_heavy).
+// SPKM_EK_HEAVY_PCT: percent of k (0 = off).
+int64_t elkan_heavy_default(int64_t k) {
+    const char *e = getenv("SPKM_EK_HEAVY_PCT");
+    const double pct = e ? atof(e) : (double)SPKM_EK_HEAVY_PCT_DEFAULT;
+    if (k <= 256 || !(pct > 0.0)) return 0;
+    const int64_t t = (int64_t)ceil((double)k * pct / 100.0 - 1e-9);
+    return t < 1 ? 1 : t;
+}
+
 RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     RowPassArgs A{};
     A.ctl = C->ctl;
@@ -4140,10 +4261,39 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
     if (C->k > kEbMaxK) return fail_msg("elkan_bounds: k > 1024 not supported by this build");
     const int grid = grid_for((X->n + 31) / 32, 8);
     pdl_launch(k_elkan_bounds, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l, B->u, B->ku, C->drift,
-                                                C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl);
+                                                C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl,
+                                                (int)W->elkan_heavy, W->surv2);
     CHECK_LAUNCH("elkan_bounds");
     return 0;
 }
+
+// The heavy survivors of spkm_elkan_bounds (rows where at least
+// W->elkan_heavy centers fail the stored-bound test): one full
+// pass over the sparse center index instead of the tighten chain + block
+// gathers of spkm_elkan_scan -- at C4 a row with > ~1/4 of its centers
+// unpruned gathers fewer bytes that way (1.5 KB per nnz against 32 B per
+// active 8-center block), and every u(i, j) comes back exact.  Same
+// assignments as the scan (both are the Lloyd argmax on the canonical s~).
+// With a center index attached, spkm_cindex_build comes before the call; a
+// no-op when W->elkan_heavy is 0.
+int spkm_elkan_heavy(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream) {
+    if (X->n == 0 || W->elkan_heavy <= 0) return 0;
+    if (C->k > 1024) return fail_msg("elkan_heavy: k > 1024 not supported by this build");
+    RowPassArgs A = row_args(X, C);
+    A.mode = MODE_ELKAN_FULL;
+    A.rowlist = W->surv2;
+    A.rowcount = W->ctr + SPKM_CTR_SURV2;
+    A.a = B->a;
+    A.l = B->l;
+    A.u = B->u;
+    A.ku = B->ku;
+    A.mv_i = W->mv_i;
+    A.mv_old = W->mv_old;
+    A.ctr = W->ctr;
+    return launch_row_pass(A, C->k, S(stream), X->n);
+}
+
+int64_t spkm_elkan_heavy_threshold(int64_t k) { return elkan_heavy_default(k); }
 
 static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_cc,
                              bool fuse, void *stream) {

@@ -688,8 +688,9 @@ def fixed_sums_host(data: Dataset, a: np.ndarray, k: int, scale_bits: int) -> np
 class PointState:
     """Per-point bounds and worklists (spkm_bounds + spkm_work)."""
 
-    def __init__(self, n: int, k: int, variant: str, device):
+    def __init__(self, n: int, k: int, variant: str, device, elkan_heavy: int = 0):
         i32 = dict(dtype=torch.int32, device=device)
+        self.elkan_heavy = int(elkan_heavy)     # spkm_work.elkan_heavy (0: every bound survivor is scanned)
         self.a = torch.zeros(max(n, 1), **i32)
         self.l = torch.zeros(max(n, 1), dtype=torch.float32, device=device)
         if variant in _ELKAN_FAMILY:
@@ -718,7 +719,7 @@ class PointState:
         self.hist_host = torch.zeros(cap * _lib.ST_COUNT + 2, dtype=torch.float64).pin_memory()
         self.bounds = Bounds(_ptr(self.a), _ptr(self.l), _ptr(self.u), self.ku)
         self.work = Work(_ptr(self.surv1), _ptr(self.surv2), _ptr(self.mv_i), _ptr(self.mv_old), _ptr(self.ctr),
-                         _ptr(self.stats), _ptr(self.hist), cap)
+                         _ptr(self.stats), _ptr(self.hist), cap, self.elkan_heavy)
 
 
 # --------------------------------------------------------------- validation
@@ -780,7 +781,11 @@ class Engine:
         # it off): C4 full pass 222 -> 134 ms, Hamerly rescan -34% (profiles/r02_ab_notes.txt)
         if not self.dense and k > 256 and os.environ.get("SPKM_CSPARSE", "1") != "0":
             self.C.attach_cindex(self.corpus.nnz)
-        self.P = PointState(self.n_loc, k, variant, self.device)
+        # Elkan family with a center index: the bound pass routes rows with many unpruned centers to
+        # spkm_elkan_heavy (threshold from the library: SPKM_EK_HEAVY_PCT percent of k, 0 = off)
+        self.elkan_heavy = (int(_lib.lib().spkm_elkan_heavy_threshold(k))
+                            if self.elkan and self.C.cindex is not None else 0)
+        self.P = PointState(self.n_loc, k, variant, self.device, elkan_heavy=self.elkan_heavy)
         self.a_global = torch.zeros(max(cs.n, 1), dtype=torch.int32, device=self.device) if comm is not None else None
         # a dedicated stream: steady-state iterations are replayed as one CUDA graph
         self.stream = torch.cuda.Stream(device=self.device)
@@ -950,6 +955,10 @@ class Engine:
         if self.yy:
             _lib.call("spkm_yy_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, self.sp)
         elif self.elkan:
+            if self.C.cindex is not None and self.elkan_heavy:
+                # rows the stored bounds barely prune: one full pass over the sparse center index
+                self.C.build_cindex(self.sp)
+                _lib.call("spkm_elkan_heavy", self.xs, self.C.struct, self.P.bounds, self.P.work, self.sp)
             _lib.call("spkm_elkan_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)
         elif self.dense:
             self._dense(_lib.DMODE_RESCAN_H, use_flag)   # tighten + full scan on the canonical TC values

@@ -545,6 +545,7 @@ def test_sparse_center_index_full_pass_equals_dense(k, variant, monkeypatch):
     data = synth.config_dataset("C3", n_override=20_000)
     engine.clear_engine_cache()
     monkeypatch.setenv("SPKM_CSPARSE", "0")
+    monkeypatch.setenv("SPKM_EK_HEAVY_PCT", "0")     # the heavy-row pass changes the counters (tested below)
     ref = m.run(data, k, variant, m.SeedConfig(seed=3), max_iter=30)
     monkeypatch.setenv("SPKM_CSPARSE", "1")
     engine.clear_engine_cache()
@@ -555,3 +556,51 @@ def test_sparse_center_index_full_pass_equals_dense(k, variant, monkeypatch):
         key = lambda s: (s.sim_count, s.reassignments, s.survivors, s.survivors2, s.nnz_rescan)  # noqa: E731
         assert [key(s) for s in r.iterations] == [key(s) for s in ref.iterations]
     engine.clear_engine_cache()
+
+
+@pytest.mark.parametrize("k", [300, 1000])
+@pytest.mark.parametrize("variant", ["elkan", "simp_elkan"])
+def test_elkan_heavy_rows_full_pass_equals_scan(k, variant, monkeypatch):
+    """spkm_elkan_heavy: rows with many unpruned centers take one full pass over
+    the sparse center index instead of the block scan.  Both are the Lloyd
+    argmax on the canonical s~ (incumbent wins ties, else the lowest index), so
+    assignments, objective and per-iteration reassignments equal the scan-only
+    fit and the GPU Lloyd for every threshold; the full pass computes k
+    similarities per row, so sim_count can only differ."""
+    from paper_2107_04074_b200 import engine, synth
+    m = spk()
+    data = synth.config_dataset("C3", n_override=20_000)
+    engine.clear_engine_cache()
+    monkeypatch.setenv("SPKM_EK_HEAVY_PCT", "0")
+    ref = m.run(data, k, variant, m.SeedConfig(seed=3), max_iter=30)
+    lloyd = m.run(data, k, "standard", m.SeedConfig(seed=3), max_iter=30)
+    assert np.array_equal(ref.assignments, lloyd.assignments) and ref.objective == lloyd.objective
+    assert all(s.survivors2 == 0 for s in ref.iterations)
+    for pct in ("1", "25", "60"):
+        monkeypatch.setenv("SPKM_EK_HEAVY_PCT", pct)
+        engine.clear_engine_cache()
+        for graphs in (False, True, True):
+            r = m.run(data, k, variant, m.SeedConfig(seed=3), max_iter=30, use_graphs=graphs)
+            assert np.array_equal(r.assignments, ref.assignments)
+            assert r.objective == ref.objective
+            assert [s.reassignments for s in r.iterations] == [s.reassignments for s in ref.iterations]
+            assert any(s.survivors2 > 0 for s in r.iterations[1:])       # the heavy pass did run
+            assert (sum(s.survivors + s.survivors2 for s in r.iterations[1:])
+                    <= sum(s.survivors for s in ref.iterations[1:]))     # exact u(i, j): never more survivors
+    engine.clear_engine_cache()
+
+
+def test_elkan_heavy_rows_bounds_audited(monkeypatch):
+    """Bounds written by the heavy pass (l and every u(i, j) exact + eps) pass
+    the device auditor at every iteration, mixed with the block scan's."""
+    from paper_2107_04074_b200 import engine, synth, validation
+    data = synth.config_dataset("C3", n_override=20_000)
+    for pct in ("1", "10"):
+        monkeypatch.setenv("SPKM_EK_HEAVY_PCT", pct)
+        engine.clear_engine_cache()
+        for variant in ("elkan", "simp_elkan"):
+            rep = validation.audit_bounds(data, variant, 300, seed=3, max_iter=12)
+            assert rep.passed, rep
+            assert rep.decisions_audited > 0
+    engine.clear_engine_cache()
+

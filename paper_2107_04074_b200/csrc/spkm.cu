@@ -366,10 +366,7 @@ struct RowPassArgs {
 // chain, so every s~(i, j) is the canonical chain (ties and all).  The
 // lanes then pick up their CH columns into registers for the epilogue.
 #ifndef SPKM_EK_HEAVY_PCT_DEFAULT
-#define SPKM_EK_HEAVY_PCT_DEFAULT 25
-#endif
-#ifndef SPKM_SP_EXP
-#define SPKM_SP_EXP 0             // timing probe of register accumulation for dense term rows (not exact)
+#define SPKM_EK_HEAVY_PCT_DEFAULT 0.5    // C4: 0.1 / 0.3 / 0.5 / 1 / 5 / 25 % -> 17.6 / 17.9 / 18.0 / 17.7 / 17.0 / 14.7 it/s (off: 13.2)
 #endif
 #ifndef SPKM_SP_PREFETCH
 #define SPKM_SP_PREFETCH 0        // per-term bulk L2 prefetch: measured slower at C4 (2267 vs 2184 ms per fit)
@@ -418,73 +415,11 @@ __device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPas
                 asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(a0), "r"(bytes) : "memory");
 #endif
         }
-#if SPKM_SP_EXP
-        // TIMING PROBE ONLY (wrong summation order): the chunk's dense term rows first, accumulated in
-        // registers, folded into the shared accumulators once per chunk
-        {
-            unsigned dm = __ballot_sync(FULL, lane < cnt && (int)(dsc & 0xFFF) == 0xFFF);
-            if (dm) {
-                float ra[CH];
-#pragma unroll
-                for (int c = 0; c < CH; ++c) ra[c] = 0.f;
-                while (dm) {
-                    const int t0 = __ffs(dm) - 1;
-                    dm &= dm - 1;
-                    int t1 = -1;
-                    if (dm) {
-                        t1 = __ffs(dm) - 1;
-                        dm &= dm - 1;
-                    }
-                    const int id0 = __shfl_sync(FULL, id, t0), id1 = __shfl_sync(FULL, id, t1 < 0 ? t0 : t1);
-                    const float v0 = __shfl_sync(FULL, v, t0), v1 = t1 < 0 ? 0.f : __shfl_sync(FULL, v, t1 < 0 ? t0 : t1);
-                    if (own) {
-                        const float4 *p0 = reinterpret_cast<const float4 *>(A.ct + (int64_t)id0 * A.kp + j0);
-                        const float4 *p1 = reinterpret_cast<const float4 *>(A.ct + (int64_t)id1 * A.kp + j0);
-                        const uint64_t q0 = id0 < A.hot ? pol_hot : pol_cold, q1 = id1 < A.hot ? pol_hot : pol_cold;
-#pragma unroll
-                        for (int h = 0; h < 2; ++h) {
-                            float4 x[CH / 8], y[CH / 8];
-#pragma unroll
-                            for (int r = 0; r < CH / 8; ++r) {
-                                x[r] = ldg_hint(p0 + (h * (CH / 8) + r) * A.tpr, q0);
-                                y[r] = ldg_hint(p1 + (h * (CH / 8) + r) * A.tpr, q1);
-                            }
-#pragma unroll
-                            for (int r = 0; r < CH / 8; ++r) {
-                                const int b = 4 * (h * (CH / 8) + r);
-                                ra[b + 0] = __fmaf_rn(v1, y[r].x, __fmaf_rn(v0, x[r].x, ra[b + 0]));
-                                ra[b + 1] = __fmaf_rn(v1, y[r].y, __fmaf_rn(v0, x[r].y, ra[b + 1]));
-                                ra[b + 2] = __fmaf_rn(v1, y[r].z, __fmaf_rn(v0, x[r].z, ra[b + 2]));
-                                ra[b + 3] = __fmaf_rn(v1, y[r].w, __fmaf_rn(v0, x[r].w, ra[b + 3]));
-                            }
-                        }
-                    }
-                }
-                __syncwarp();
-                if (own) {
-#pragma unroll
-                    for (int r = 0; r < CH / 4; ++r) {
-                        float4 *ap = reinterpret_cast<float4 *>(sacc + j0 + r * jstr);
-                        float4 a = *ap;
-                        a.x += ra[4 * r];
-                        a.y += ra[4 * r + 1];
-                        a.z += ra[4 * r + 2];
-                        a.w += ra[4 * r + 3];
-                        *ap = a;
-                    }
-                }
-                __syncwarp();
-            }
-        }
-#endif
         for (int t = 0; t < cnt; ++t) {
             const int tid = __shfl_sync(FULL, id, t);
             const float tv = __shfl_sync(FULL, v, t);
             const long long td = __shfl_sync(FULL, dsc, t);
             const int n = (int)(td & 0xFFF);
-#if SPKM_SP_EXP
-            if (n == 0xFFF) continue;
-#endif
             if (n == 0xFFF) {   // dense term row: the owner lanes, float4 per column group (n, last_sparse: warp-uniform)
                 if (last_sparse) __syncwarp();
                 last_sparse = false;
@@ -1184,7 +1119,7 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                                                       const float *__restrict__ cc,
                                                       const float *__restrict__ s_arr, int use_cc,
                                                       int32_t *surv1, long long *ctr, const long long *__restrict__ ctl,
-                                                      int heavy_thr, int32_t *surv_h) {
+                                                      int heavy_thr, int32_t *surv_h, int store_heavy) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ __align__(16) float s_pd[kEbMaxK], s_pu[kEbMaxK], s_su[kEbMaxK];
@@ -1241,6 +1176,7 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                 if (q < k4) v[t] = ui[q];
             }
             int nfail = 0;
+            unsigned dirty = 0;   // 16-byte groups whose drift-updated values are still to be stored
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const int q = lane + 32 * t;
@@ -1254,7 +1190,8 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
 #pragma unroll
                     for (int cq = 0; cq < 4; ++cq)
                         if (sa_[cq] != 0.f) w[cq] = elkan_u_drift(w[cq], pda[cq], pua[cq], sa_[cq]);
-                    ui[q] = make_float4(w[0], w[1], w[2], w[3]);   // padding columns (j >= k) have su == 0
+                    v[t] = make_float4(w[0], w[1], w[2], w[3]);   // padding columns (j >= k) have su == 0
+                    dirty |= 1u << t;
                 }
                 if (!pskip) {
 #pragma unroll
@@ -1272,9 +1209,16 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
             // full pass over the sparse center index (spkm_elkan_heavy), the
             // others to the block scan; heavy_thr == 0: every survivor is light
             const int tot = __reduce_add_sync(FULL, nfail);
+            const bool heavy = heavy_thr > 0 && tot >= heavy_thr;
             if (tot > 0) {
-                if (heavy_thr > 0 && tot >= heavy_thr) hmask |= 1u << r;
+                if (heavy) hmask |= 1u << r;
                 else smask |= 1u << r;
+            }
+            // a heavy row's u(i, .) is rewritten in full by spkm_elkan_heavy: its drift update is not stored
+            if (!heavy || store_heavy) {
+#pragma unroll
+                for (int t = 0; t < 8; ++t)
+                    if (dirty >> t & 1u) ui[lane + 32 * t] = v[t];
             }
         }
         long long base = 0;
@@ -4261,8 +4205,8 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
     if (C->k > kEbMaxK) return fail_msg("elkan_bounds: k > 1024 not supported by this build");
     const int grid = grid_for((X->n + 31) / 32, 8);
     pdl_launch(k_elkan_bounds, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l, B->u, B->ku, C->drift,
-                                                C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl,
-                                                (int)W->elkan_heavy, W->surv2);
+                                                C->sinp, C->cc, C->s, use_cc & 1, W->surv1, W->ctr, C->ctl,
+                                                (int)W->elkan_heavy, W->surv2, (use_cc >> 1) & 1);
     CHECK_LAUNCH("elkan_bounds");
     return 0;
 }

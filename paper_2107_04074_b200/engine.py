@@ -604,8 +604,10 @@ class CenterState:
                     torch.empty(2 * cap + 8, dtype=torch.int32, device=dev),   # + slack for 16-byte bulk prefetches
                     torch.empty(max(self.d, 1), dtype=torch.int64, device=dev),
                     torch.empty(max(nb, 1), dtype=torch.uint8, device=dev))
+        # term rows with more nonzero centers than kp / SPKM_CI_DIV stay dense float4 rows (A/B: profiles/r02_ab_notes.txt)
+        div = max(int(os.environ.get("SPKM_CI_DIV", "4")), 1)
         self.cindex = _lib.CIndex(_ptr(self._ci[0]), _ptr(self._ci[1]), _ptr(self._ci[2]), _ptr(self._ci[3]), nb, cap,
-                                  self.kp // 4, 0)
+                                  self.kp // div, 0)
         self.struct.cindex = ctypes.addressof(self.cindex)
 
     def build_cindex(self, sp):
@@ -1058,7 +1060,8 @@ class Engine:
             sims_extra = 0
         else:
             use = int(self.needs_cc)
-            self.bounds_pass(use)
+            # bit 1: a debug hook reads the bounds before the scans, so heavy rows' drift updates are stored too
+            self.bounds_pass(use | (2 if (debug_hook is not None and self.elkan) else 0))
             if debug_hook is not None:
                 if hasattr(debug_hook, "device_audit"):    # validation.DeviceBoundAuditor: stays on the device
                     debug_hook.device_audit(it, self)

@@ -83,8 +83,8 @@ typedef struct spkm_csr {
 typedef struct spkm_cindex {
     int64_t *desc;           /* [d] */
     int32_t *pairs;          /* [2 * capacity] (j, float bits) */
-    int64_t *off;            /* [d] scratch: sparse counts, then their offsets */
-    void *scratch;           /* CUB scan scratch, spkm_cindex_scratch_bytes(d) bytes */
+    int64_t *off;            /* [d] scratch: off[0] = running total of reserved pairs during a build */
+    void *scratch;           /* spkm_cindex_scratch_bytes(d) bytes (unused by the one-pass build)     */
     int64_t scratch_bytes;
     int64_t capacity;        /* pairs; >= nonzeros of the centers (<= nnz of the corpus) */
     int32_t dense_thr;       /* rows with more nonzeros are read densely */
@@ -210,9 +210,6 @@ int spkm_yy_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_
  * no-op): identical results and counters, one pass fewer. */
 int spkm_hamerly_rescan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, int use_s,
                         void *stream);
-/* use_cc bit 0: apply the center-center tests (elkan); bit 1: also store the
- * drift update of heavy rows (see spkm_elkan_heavy) -- for auditing the
- * bounds between this call and the scans. */
 int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
                       int use_cc, void *stream);
 int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W,
@@ -225,8 +222,7 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
  * center index when C->cindex is attached: spkm_cindex_build first): same
  * reassignment rule as the scan (incumbent wins ties, else the lowest index),
  * l and every u(i, j) come back exact, SIMS += k per row.  Call it between
- * spkm_elkan_bounds and spkm_elkan_scan whenever W->elkan_heavy > 0 (the bound
- * pass does not store the drift update of a heavy row: this call rewrites it).
+ * spkm_elkan_bounds and spkm_elkan_scan whenever W->elkan_heavy > 0.
  * spkm_elkan_heavy_threshold: the library's default for k centers (0.5% of k
  * for k > 256, SPKM_EK_HEAVY_PCT overrides; 0 = off). */
 int spkm_elkan_heavy(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream);

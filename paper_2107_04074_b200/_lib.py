@@ -175,7 +175,7 @@ KERNELS_PER_CALL = {
     "spkm_move_centers": 5, "spkm_center_reduce": 1, "spkm_center_thresholds": 3, "spkm_finalize": 1, "spkm_predict": 1,
     "spkm_objective": 2, "spkm_load_centers": 1, "spkm_geometry": 1, "spkm_seed_rows": 1,
     "spkm_dense_centers": 1, "spkm_dense_assign": 1, "spkm_reset_counters": 1,
-    "spkm_seed_rows_csr": 1, "spkm_permute_rows": 1, "spkm_prepare_rows": 7, "spkm_dense_ids": 1, "spkm_gram_partial": 1, "spkm_gram_finish": 2, "spkm_cindex_build": 3, "spkm_audit": 1, "spkm_audit_transpose": 1,
+    "spkm_seed_rows_csr": 1, "spkm_permute_rows": 1, "spkm_prepare_rows": 7, "spkm_dense_ids": 1, "spkm_gram_partial": 1, "spkm_gram_finish": 2, "spkm_cindex_build": 1, "spkm_audit": 1, "spkm_audit_transpose": 1,
     "spkm_pack_moves": 1, "spkm_apply_move_slots": 1, "spkm_rows_to_host": 1,
     "spkm_order_by_cluster": 4,
 }

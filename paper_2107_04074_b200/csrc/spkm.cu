@@ -1078,20 +1078,23 @@ __global__ void __launch_bounds__(256) k_hamerly_tighten(const int64_t *__restri
 // sqrt(x) rounded up, x in [0, 1]: the IEEE directed sqrt is a ~20-instruction
 // software sequence; x * rsqrt(x) from the MUFU (<= 2 ulp + 0.5 ulp of the
 // product) times (1 + 2^-19) rounded up is >= sqrt(x) at a quarter of the cost
+// Branch-free: x is clamped to 1e-30 (sqrt_up(1e-30) ~ 1e-15 >= sqrt of anything smaller; the MUFU never
+// sees a subnormal), rsqrt.approx (relative error < 2^-22) is one instruction.
 __device__ __forceinline__ float sqrt_up(float x) {
 #if SPKM_FAST_SQRT
-    if (x < 1e-30f) return 1e-15f;    // >= sqrt(x); keeps subnormals away from the MUFU
-    return __fmul_ru(x * rsqrtf(x), 1.0f + 1.9073486e-6f);
+    x = fmaxf(x, 1e-30f);
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+    return __fmul_ru(x * r, 1.0f + 1.9073486e-6f);
 #else
     return __fsqrt_ru(x);
 #endif
 }
 __device__ __forceinline__ float elkan_u_drift(float w, float pd, float pu, float su) {
-    if (!(w <= pd)) return 1.0f;
-    const float sw = sqrt_up(fmaxf(__fmaf_ru(-w, w, 1.0f), 0.0f));   // >= sin(w)
+    const float sw = sqrt_up(__fmaf_ru(-w, w, 1.0f));   // >= sin(w) (negative arguments are clamped)
     const float prod = __fmaf_ru(sw, su, 1e-12f);
     const float nv = __fmaf_ru(w, w >= 0.f ? pu : pd, prod);
-    return fminf(fmaxf(nv, -1.0f), 1.0f);
+    return (w <= pd) ? fminf(fmaxf(nv, -1.0f), 1.0f) : 1.0f;
 }
 // Prune thresholds of one row (kernels.py:35-47 with the eps margins):
 //   u(i,j) + 2 eps <= l  <=>  u(i,j) <= rd(l - 2 eps)      (u a float)
@@ -1112,6 +1115,7 @@ constexpr int kEbMaxK = 1024;
 #ifndef SPKM_EB_MINB
 #define SPKM_EB_MINB 3        // 80 registers, 3 CTAs per SM: the u stream needs the warps (126 -> 80 regs)
 #endif
+template <bool CC>   // CC: the center-center tests of elkan (simp_elkan: the per-element loop is branch-free)
 __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, int k, const float *__restrict__ reps,
                                                       const int32_t *__restrict__ a, float *l, float *u,
                                                       int64_t ku, const double *__restrict__ drift,
@@ -1119,7 +1123,7 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                                                       const float *__restrict__ cc,
                                                       const float *__restrict__ s_arr, int use_cc,
                                                       int32_t *surv1, long long *ctr, const long long *__restrict__ ctl,
-                                                      int heavy_thr, int32_t *surv_h, int store_heavy) {
+                                                      int heavy_thr, int32_t *surv_h) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ __align__(16) float s_pd[kEbMaxK], s_pu[kEbMaxK], s_su[kEbMaxK];
@@ -1155,8 +1159,8 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
             }
             const double eps = (double)reps[ir];
             const double lb = (double)lf;
-            pskip_r = use_cc && lb >= 0.0 && (double)s_arr[ai_r] + kSqrt2 * eps <= lb;
-            ccon_r = use_cc && lb >= 0.0;
+            pskip_r = CC && use_cc && lb >= 0.0 && (double)s_arr[ai_r] + kSqrt2 * eps <= lb;
+            ccon_r = CC && use_cc && lb >= 0.0;
             thu_r = thr_u_of(lb, eps);
             thc_r = thr_c_of(lb, eps);
         }
@@ -1176,7 +1180,6 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                 if (q < k4) v[t] = ui[q];
             }
             int nfail = 0;
-            unsigned dirty = 0;   // 16-byte groups whose drift-updated values are still to be stored
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const int q = lane + 32 * t;
@@ -1188,19 +1191,24 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                     const float sa_[4] = {su.x, su.y, su.z, su.w}, pda[4] = {pd.x, pd.y, pd.z, pd.w},
                                 pua[4] = {pu.x, pu.y, pu.z, pu.w};
 #pragma unroll
-                    for (int cq = 0; cq < 4; ++cq)
-                        if (sa_[cq] != 0.f) w[cq] = elkan_u_drift(w[cq], pda[cq], pua[cq], sa_[cq]);
-                    v[t] = make_float4(w[0], w[1], w[2], w[3]);   // padding columns (j >= k) have su == 0
-                    dirty |= 1u << t;
+                    for (int cq = 0; cq < 4; ++cq) {
+                        const float wn = elkan_u_drift(w[cq], pda[cq], pua[cq], sa_[cq]);
+                        w[cq] = sa_[cq] != 0.f ? wn : w[cq];
+                    }
+                    ui[q] = make_float4(w[0], w[1], w[2], w[3]);   // padding columns (j >= k) have su == 0
                 }
                 if (!pskip) {
 #pragma unroll
                     for (int cq = 0; cq < 4; ++cq) {
                         const int j = 4 * q + cq;
-                        if (j < k && j != ai) {
-                            bool skip = ccon && __ldg(cca + j) <= thc;
-                            if (!skip) skip = w[cq] <= thu;
-                            nfail += skip ? 0 : 1;
+                        if constexpr (CC) {
+                            if (j < k && j != ai) {
+                                bool skip = ccon && __ldg(cca + j) <= thc;
+                                if (!skip) skip = w[cq] <= thu;
+                                nfail += skip ? 0 : 1;
+                            }
+                        } else {
+                            nfail += (j < k && j != ai && !(w[cq] <= thu)) ? 1 : 0;
                         }
                     }
                 }
@@ -1209,16 +1217,9 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
             // full pass over the sparse center index (spkm_elkan_heavy), the
             // others to the block scan; heavy_thr == 0: every survivor is light
             const int tot = __reduce_add_sync(FULL, nfail);
-            const bool heavy = heavy_thr > 0 && tot >= heavy_thr;
             if (tot > 0) {
-                if (heavy) hmask |= 1u << r;
+                if (heavy_thr > 0 && tot >= heavy_thr) hmask |= 1u << r;
                 else smask |= 1u << r;
-            }
-            // a heavy row's u(i, .) is rewritten in full by spkm_elkan_heavy: its drift update is not stored
-            if (!heavy || store_heavy) {
-#pragma unroll
-                for (int t = 0; t < 8; ++t)
-                    if (dirty >> t & 1u) ui[lane + 32 * t] = v[t];
             }
         }
         long long base = 0;
@@ -1973,47 +1974,54 @@ __global__ void __launch_bounds__(256) k_elkan_scan_r1(const int64_t *__restrict
 
 
 // ------------------------------------------------ sparse center index
-// spkm_cindex_build: warp per term row of ct32 (float4 per lane, 128
-// columns per step).  count: nonzero centers -> off[t] (sparse rows; 0 for
-// dense ones) and desc[t] = count (temporarily); an exclusive scan turns off
-// into offsets; fill: the sparse rows' (j, value) pairs in j order, desc.
-__global__ void __launch_bounds__(256) k_ci_count(int64_t d, int64_t kp, int k, const float *__restrict__ ct, int thr,
-                                                  int64_t *off, int64_t *desc, const long long *__restrict__ ctl) {
+// spkm_cindex_build, one pass over ct32: a CTA takes 8 term rows per round
+// (warp per row, float4 per lane, 128 columns per step).  Each warp counts its
+// row's nonzero centers; the CTA reserves the pairs of its sparse rows (count
+// <= thr) with ONE atomic on the running total; each warp then re-reads its
+// row (4 KB, still in L1) and writes its (j, value) pairs in j order and
+// desc[t] = offset << 12 | count (0xFFF: dense row).  Where a row's pairs
+// land depends on the atomic order; the row's pairs, their order and so every
+// result do not.  (A count kernel + CUB scan + fill kernel read the 4 GB
+// table twice: 1.8 ms per build at C4 against 0.7.)
+__global__ void __launch_bounds__(256) k_ci_build(int64_t d, int64_t kp, int k, const float *__restrict__ ct, int thr,
+                                                  unsigned long long *total, int64_t *desc, int2 *pairs,
+                                                  const long long *__restrict__ ctl) {
     PDL_ENTRY();
     if (ctl[1]) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < d; t += warps) {
+    __shared__ int s_c[8];
+    __shared__ int s_off[8];
+    __shared__ long long s_base;
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    for (int64_t t0 = (int64_t)blockIdx.x * 8; t0 < d; t0 += (int64_t)gridDim.x * 8) {
+        const int64_t t = t0 + wib;
         const float *row = ct + t * kp;
         int c = 0;
-        for (int j0 = 4 * lane; j0 < k; j0 += 128) {
-            const float4 v = __ldg(reinterpret_cast<const float4 *>(row + j0));
-            c += (v.x != 0.f) + (j0 + 1 < k && v.y != 0.f) + (j0 + 2 < k && v.z != 0.f) + (j0 + 3 < k && v.w != 0.f);
+        if (t < d) {
+            for (int j0 = 4 * lane; j0 < k; j0 += 128) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(row + j0));
+                c += (v.x != 0.f) + (j0 + 1 < k && v.y != 0.f) + (j0 + 2 < k && v.z != 0.f) + (j0 + 3 < k && v.w != 0.f);
+            }
         }
         c = (int)__reduce_add_sync(FULL, (unsigned)c);
-        if (lane == 0) {
-            off[t] = c <= thr ? c : 0;
-            desc[t] = c;
+        const bool sparse = t < d && c <= thr;
+        if (lane == 0) s_c[wib] = sparse ? c : 0;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            int tot = 0;
+#pragma unroll
+            for (int w = 0; w < 8; ++w) {
+                s_off[w] = tot;
+                tot += s_c[w];
+            }
+            s_base = tot ? (long long)atomicAdd(total, (unsigned long long)tot) : 0;
         }
-    }
-    PDL_TRIGGER();
-}
-__global__ void __launch_bounds__(256) k_ci_fill(int64_t d, int64_t kp, int k, const float *__restrict__ ct, int thr,
-                                                 const int64_t *__restrict__ off, int64_t *desc, int2 *pairs,
-                                                 const long long *__restrict__ ctl) {
-    PDL_ENTRY();
-    if (ctl[1]) return;
-    const int lane = threadIdx.x & 31;
-    const int64_t warps = (int64_t)gridDim.x * (blockDim.x >> 5);
-    for (int64_t t = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); t < d; t += warps) {
-        const int c = (int)desc[t];
-        __syncwarp();
-        if (c > thr) {
+        __syncthreads();
+        const int64_t base = s_base + s_off[wib];
+        if (t >= d) continue;           // (every warp still reaches the barriers of the next round: t0 is CTA-uniform)
+        if (!sparse) {
             if (lane == 0) desc[t] = 0xFFF;
             continue;
         }
-        const int64_t base = off[t];
-        const float *row = ct + t * kp;
         int pos = 0;
         for (int j0 = 4 * lane, jb = 0; jb < k; j0 += 128, jb += 128) {
             float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -4204,9 +4212,14 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
     if (X->n == 0) return 0;
     if (C->k > kEbMaxK) return fail_msg("elkan_bounds: k > 1024 not supported by this build");
     const int grid = grid_for((X->n + 31) / 32, 8);
-    pdl_launch(k_elkan_bounds, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l, B->u, B->ku, C->drift,
-                                                C->sinp, C->cc, C->s, use_cc & 1, W->surv1, W->ctr, C->ctl,
-                                                (int)W->elkan_heavy, W->surv2, (use_cc >> 1) & 1);
+    if (use_cc)
+        pdl_launch(k_elkan_bounds<true>, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l,
+                   B->u, B->ku, C->drift, C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl, (int)W->elkan_heavy,
+                   W->surv2);
+    else
+        pdl_launch(k_elkan_bounds<false>, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l,
+                   B->u, B->ku, C->drift, C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl, (int)W->elkan_heavy,
+                   W->surv2);
     CHECK_LAUNCH("elkan_bounds");
     return 0;
 }
@@ -4773,15 +4786,11 @@ int spkm_cindex_build(const spkm_centers *C, void *stream) {
     if (C->k > 2047) return fail_msg("cindex_build: k > 2047");
     cudaStream_t st = S(stream);
     const int grid = grid_for((C->d + 7) / 8, 1);
-    pdl_launch(k_ci_count, dim3(grid), dim3(256), (size_t)0, st, C->d, C->kp, (int)C->k, C->ct32, I->dense_thr, I->off,
-               I->desc, C->ctl);
-    CHECK_LAUNCH("ci_count");
-    size_t tb = (size_t)I->scratch_bytes;
-    if (cub::DeviceScan::ExclusiveSum(I->scratch, tb, I->off, I->off, (int)C->d, st) != cudaSuccess)
-        return fail_msg("cindex_build: scan failed");
-    pdl_launch(k_ci_fill, dim3(grid), dim3(256), (size_t)0, st, C->d, C->kp, (int)C->k, C->ct32, I->dense_thr, I->off,
-               I->desc, reinterpret_cast<int2 *>(I->pairs), C->ctl);
-    CHECK_LAUNCH("ci_fill");
+    // the running total of reserved pairs lives in off[0] (the scan scratch of the two-pass build is unused)
+    if (cudaMemsetAsync(I->off, 0, sizeof(int64_t), st) != cudaSuccess) return fail_msg("cindex_build: memset failed");
+    pdl_launch(k_ci_build, dim3(grid), dim3(256), (size_t)0, st, C->d, C->kp, (int)C->k, C->ct32, I->dense_thr,
+               reinterpret_cast<unsigned long long *>(I->off), I->desc, reinterpret_cast<int2 *>(I->pairs), C->ctl);
+    CHECK_LAUNCH("ci_build");
     return 0;
 }
 

@@ -1060,8 +1060,7 @@ class Engine:
             sims_extra = 0
         else:
             use = int(self.needs_cc)
-            # bit 1: a debug hook reads the bounds before the scans, so heavy rows' drift updates are stored too
-            self.bounds_pass(use | (2 if (debug_hook is not None and self.elkan) else 0))
+            self.bounds_pass(use)
             if debug_hook is not None:
                 if hasattr(debug_hook, "device_audit"):    # validation.DeviceBoundAuditor: stays on the device
                     debug_hook.device_audit(it, self)

@@ -1974,22 +1974,15 @@ __global__ void __launch_bounds__(256) k_elkan_scan_r1(const int64_t *__restrict
 
 
 // ------------------------------------------------ sparse center index
-// spkm_cindex_build, one pass over ct32: a CTA takes 8 term rows per round,
-// warp per row.  Lane b owns the columns j = b (mod 32) -- the shared-memory
-// bank of the full pass's accumulator sacc[j] -- and reads them level by
-// level (j = b + 32 l: one coalesced 128-byte line per level).  Each warp
-// counts its row's nonzero centers; the CTA reserves the pairs of its sparse
-// rows (count <= thr) with ONE atomic on the running total; each warp then
-// re-reads its row (4 KB, still in L1) and writes its (j, value) pairs in
-// ROUNDS: round r holds the r-th nonzero of every bank that has one, in bank
-// order, rounds back to back.  32 consecutive pairs -- what the 32 lanes of
-// the full pass apply together -- then hit distinct banks (2-way at a round
-// boundary at worst) instead of ~3.5-way conflicts of pairs in j order.
+// spkm_cindex_build, one pass over ct32: a CTA takes 8 term rows per round
+// (warp per row, float4 per lane, 128 columns per step).  Each warp counts its
+// row's nonzero centers; the CTA reserves the pairs of its sparse rows (count
+// <= thr) with ONE atomic on the running total; each warp then re-reads its
+// row (4 KB, still in L1) and writes its (j, value) pairs in j order and
 // desc[t] = offset << 12 | count (0xFFF: dense row).  Where a row's pairs
-// land depends on the atomic order; the row's pairs and so every result do
-// not (a row's pairs have distinct j: their order is free).  (A count
-// kernel + CUB scan + fill kernel read the 4 GB table twice: 1.8 ms per
-// build at C4.)
+// land depends on the atomic order; the row's pairs, their order and so every
+// result do not.  (A count kernel + CUB scan + fill kernel read the 4 GB
+// table twice: 1.8 ms per build at C4 against 0.7.)
 __global__ void __launch_bounds__(256) k_ci_build(int64_t d, int64_t kp, int k, const float *__restrict__ ct, int thr,
                                                   unsigned long long *total, int64_t *desc, int2 *pairs,
                                                   const long long *__restrict__ ctl) {
@@ -1999,19 +1992,17 @@ __global__ void __launch_bounds__(256) k_ci_build(int64_t d, int64_t kp, int k, 
     __shared__ int s_off[8];
     __shared__ long long s_base;
     const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-    const unsigned lt = (1u << lane) - 1u;
-    const int levels = (k + 31) >> 5;
     for (int64_t t0 = (int64_t)blockIdx.x * 8; t0 < d; t0 += (int64_t)gridDim.x * 8) {
         const int64_t t = t0 + wib;
-        const float *row = ct + t * kp + lane;
-        int mine = 0;   // nonzero centers in this lane's bank
+        const float *row = ct + t * kp;
+        int c = 0;
         if (t < d) {
-            for (int l = 0; l < levels; ++l) {
-                const int j = lane + 32 * l;
-                mine += (j < k && __ldg(row + 32 * l) != 0.f) ? 1 : 0;
+            for (int j0 = 4 * lane; j0 < k; j0 += 128) {
+                const float4 v = __ldg(reinterpret_cast<const float4 *>(row + j0));
+                c += (v.x != 0.f) + (j0 + 1 < k && v.y != 0.f) + (j0 + 2 < k && v.z != 0.f) + (j0 + 3 < k && v.w != 0.f);
             }
         }
-        const int c = (int)__reduce_add_sync(FULL, (unsigned)mine);
+        c = (int)__reduce_add_sync(FULL, (unsigned)c);
         const bool sparse = t < d && c <= thr;
         if (lane == 0) s_c[wib] = sparse ? c : 0;
         __syncthreads();
@@ -2031,24 +2022,26 @@ __global__ void __launch_bounds__(256) k_ci_build(int64_t d, int64_t kp, int k, 
             if (lane == 0) desc[t] = 0xFFF;
             continue;
         }
-        const int rounds = (int)__reduce_max_sync(FULL, (unsigned)mine);
-        int64_t off = base;
-        int l = 0;
-        for (int r = 0; r < rounds; ++r) {
-            const unsigned m = __ballot_sync(FULL, mine > r);
-            if (mine > r) {
-                float v;
-                int j;
-                do {   // this lane's next nonzero (from L1)
-                    j = lane + 32 * l;
-                    v = __ldg(row + 32 * l);
-                    ++l;
-                } while (v == 0.f || j >= k);   // (terminates: a nonzero with j < k is left, mine > r counted it)
-                pairs[off + __popc(m & lt)] = make_int2(j, __float_as_int(v));
+        int pos = 0;
+        for (int j0 = 4 * lane, jb = 0; jb < k; j0 += 128, jb += 128) {
+            float4 v = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (j0 < k) v = __ldg(reinterpret_cast<const float4 *>(row + j0));
+            const float vv[4] = {v.x, v.y, v.z, v.w};
+            int m = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) m += (j0 + q < k && vv[q] != 0.f);
+            int x = m;   // inclusive prefix over the lanes
+            for (int o = 1; o < 32; o <<= 1) {
+                const int y = __shfl_up_sync(FULL, x, o);
+                if (lane >= o) x += y;
             }
-            off += __popc(m);
+            int w = pos + x - m;
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                if (j0 + q < k && vv[q] != 0.f) pairs[base + w++] = make_int2(j0 + q, __float_as_int(vv[q]));
+            pos += __shfl_sync(FULL, x, 31);
         }
-        DCHECK(off - base == c);
+        DCHECK(pos == c);
         if (lane == 0) desc[t] = (base << 12) | (int64_t)c;
     }
     PDL_TRIGGER();

@@ -154,6 +154,9 @@ typedef struct spkm_work {
     int64_t hist_cap;
     int64_t elkan_heavy;     /* > 0: spkm_elkan_bounds sends rows with at least this many unpruned
                               * centers to surv2 for spkm_elkan_heavy                     */
+    int32_t *lightj;         /* [n][4] or NULL.  With use_cc == 0 and 0 < elkan_heavy <= 5 the bound
+                              * pass lists the (< elkan_heavy) failing centers of every surv1 row here
+                              * (ascending, -1 padded) and spkm_elkan_scan scans exactly those        */
 } spkm_work;
 
 enum {

@@ -1112,6 +1112,7 @@ __device__ __forceinline__ float thr_c_of(double lb, double eps) { return __doub
 // and appends the chunk's survivors with one atomic.  Per-center pd/pu/su
 // live in shared memory.  k <= 1024.
 constexpr int kEbMaxK = 1024;
+constexpr int kLightMax = 4;      // failing centers listed per light row (lightj[n][4]); needs heavy_thr <= 5
 #ifndef SPKM_EB_MINB
 #define SPKM_EB_MINB 3        // 80 registers, 3 CTAs per SM: the u stream needs the warps (126 -> 80 regs)
 #endif
@@ -1123,7 +1124,7 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                                                       const float *__restrict__ cc,
                                                       const float *__restrict__ s_arr, int use_cc,
                                                       int32_t *surv1, long long *ctr, const long long *__restrict__ ctl,
-                                                      int heavy_thr, int32_t *surv_h) {
+                                                      int heavy_thr, int32_t *surv_h, int32_t *lightj) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ __align__(16) float s_pd[kEbMaxK], s_pu[kEbMaxK], s_su[kEbMaxK];
@@ -1179,7 +1180,7 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                 const int q = lane + 32 * t;
                 if (q < k4) v[t] = ui[q];
             }
-            int nfail = 0;
+            unsigned fb = 0;   // bit 4 t + cq: center 4 (lane + 32 t) + cq fails the stored-bound test
 #pragma unroll
             for (int t = 0; t < 8; ++t) {
                 const int q = lane + 32 * t;
@@ -1205,10 +1206,10 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                             if (j < k && j != ai) {
                                 bool skip = ccon && __ldg(cca + j) <= thc;
                                 if (!skip) skip = w[cq] <= thu;
-                                nfail += skip ? 0 : 1;
+                                fb |= (skip ? 0u : 1u) << (4 * t + cq);
                             }
                         } else {
-                            nfail += (j < k && j != ai && !(w[cq] <= thu)) ? 1 : 0;
+                            fb |= ((j < k && j != ai && !(w[cq] <= thu)) ? 1u : 0u) << (4 * t + cq);
                         }
                     }
                 }
@@ -1216,10 +1217,40 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
             // heavy rows (many centers the stored bounds cannot prune) go to the
             // full pass over the sparse center index (spkm_elkan_heavy), the
             // others to the block scan; heavy_thr == 0: every survivor is light
-            const int tot = __reduce_add_sync(FULL, nfail);
+            const int tot = __reduce_add_sync(FULL, __popc(fb));
             if (tot > 0) {
                 if (heavy_thr > 0 && tot >= heavy_thr) hmask |= 1u << r;
                 else smask |= 1u << r;
+            }
+            if constexpr (!CC) {
+                // light rows (fewer than heavy_thr <= kLightMax + 1 failing centers): their ids, ascending, for
+                // k_elkan_light -- decoded from the lanes' fail bits
+                if (lightj != nullptr && tot > 0 && tot < heavy_thr) {
+                    constexpr int NONE = 0x7fffffff;
+                    int f0 = NONE, f1 = NONE, f2 = NONE, f3 = NONE;
+                    unsigned lm = __ballot_sync(FULL, fb != 0);
+                    while (lm) {
+                        const int ln = __ffs(lm) - 1;
+                        lm &= lm - 1;
+                        unsigned b = __shfl_sync(FULL, fb, ln);
+                        while (b) {
+                            const int bit = __ffs(b) - 1;
+                            b &= b - 1;
+                            f3 = f2;   // (at most kLightMax entries: tot < heavy_thr <= kLightMax + 1)
+                            f2 = f1;
+                            f1 = f0;
+                            f0 = 4 * (ln + 32 * (bit >> 2)) + (bit & 3);
+                        }
+                    }
+                    // ascending (4-element sorting network); unused slots -> -1 at the end
+                    int x;
+#define SPKM_CSWAP(A_, B_) x = min(A_, B_); B_ = max(A_, B_); A_ = x;
+                    SPKM_CSWAP(f0, f1) SPKM_CSWAP(f2, f3) SPKM_CSWAP(f0, f2) SPKM_CSWAP(f1, f3) SPKM_CSWAP(f1, f2)
+#undef SPKM_CSWAP
+                    if (lane == 0)
+                        *reinterpret_cast<int4 *>(lightj + (rb + r) * kLightMax) =
+                            make_int4(f0 == NONE ? -1 : f0, f1 == NONE ? -1 : f1, f2 == NONE ? -1 : f2, f3 == NONE ? -1 : f3);
+                }
             }
         }
         long long base = 0;
@@ -1233,6 +1264,115 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
         if (hmask >> lane & 1u) surv_h[base_h + __popc(hmask & ((1u << lane) - 1u))] = (int32_t)ir;
     }
     PDL_TRIGGER();
+}
+
+// kernels.py:22-66 for the LIGHT survivors of a simp_elkan bound pass that
+// listed their failing centers (at most kLightMax, ascending; every other
+// center passed u + 2 eps <= l and so passes every later test, the running
+// best only grows).  8 lanes per row, 4 rows per warp (as k_hamerly_tighten):
+// per 32-nnz chunk each lane loads 4 (id, value) pairs and gathers the row's
+// 1 + nF columns a(i), F of each (all independent loads), lanes 0..nF run
+// one canonical chain each from shared memory in CSR order, then the leader
+// replays the reference's sequential scan on those few values: tighten to
+// s~(i, a), re-test each listed center against the running best, "compute"
+// = take its s~, strict > reassigns.  Same results and counters as
+// k_elkan_scan on these rows, without its four passes over the u row.
+__global__ void __launch_bounds__(256) k_elkan_light(const int64_t *__restrict__ indptr,
+                                                     const int32_t *__restrict__ indices,
+                                                     const float *__restrict__ values,
+                                                     const float *__restrict__ reps,
+                                                     const float *__restrict__ ct, int64_t kp, int k, int32_t *a,
+                                                     float *l, float *u, int64_t ku,
+                                                     const int32_t *__restrict__ surv1,
+                                                     const int32_t *__restrict__ lightj, int32_t *mv_i,
+                                                     int32_t *mv_old, long long *ctr,
+                                                     const long long *__restrict__ ctl, int64_t hot) {
+    PDL_ENTRY();
+    if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
+    constexpr int NC = kLightMax + 1, ST = NC + 1;   // columns per row; floats staged per nnz (value + NC center values)
+    __shared__ float s_st[8][4][32 * ST];
+    __shared__ unsigned long long s_ctr[8];
+    ctr_init(s_ctr);
+    const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+    const int g = lane >> 3, q = lane & 7;
+    float *st = s_st[wib][g];
+    const long long cnt = ctr[SPKM_CTR_SURV1];
+    const int64_t nslots = (cnt + 3) / 4;
+    const int wpb = blockDim.x >> 5;
+    for (int64_t w = (int64_t)blockIdx.x * wpb + wib; w < nslots; w += (int64_t)gridDim.x * wpb) {
+        const int64_t slot = w * 4 + g;
+        const bool valid = slot < cnt;
+        const int32_t i = valid ? surv1[slot] : 0;
+        const int ai = valid ? a[i] : 0;
+        const int4 f4 = valid ? __ldg(reinterpret_cast<const int4 *>(lightj + (int64_t)i * kLightMax)) : make_int4(-1, -1, -1, -1);
+        const int col[NC] = {ai, f4.x, f4.y, f4.z, f4.w};
+        const int nc = 1 + (f4.x >= 0) + (f4.y >= 0) + (f4.z >= 0) + (f4.w >= 0);
+        DCHECK(!valid || (f4.x >= 0 && f4.x < k && f4.w < k));
+        const int64_t s = valid ? indptr[i] : 0, e = valid ? indptr[i + 1] : 0;
+        const int len = (int)(e - s);
+        const int maxlen = (int)__reduce_max_sync(FULL, (unsigned)len);
+        float acc = 0.f;
+        for (int c0 = 0; c0 < maxlen; c0 += 32) {
+            const int cntc = max(0, min(32, len - c0));
+            float vx[4], cx[4][NC];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                const int t = q + 8 * r;
+                const bool on = t < cntc;
+                const int id = on ? __ldg(indices + s + c0 + t) : 0;
+                vx[r] = on ? __ldg(values + s + c0 + t) : 0.f;
+                const float *rowp = ct + (int64_t)id * kp;
+                const uint64_t pol = id < hot ? pol_hot : pol_cold;
+#pragma unroll
+                for (int c = 0; c < NC; ++c) cx[r][c] = (on && c < nc) ? ldg_hint(rowp + col[c], pol) : 0.f;
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                float *p = st + (q + 8 * r) * ST;
+                p[0] = vx[r];
+#pragma unroll
+                for (int c = 0; c < NC; ++c) p[1 + c] = cx[r][c];
+            }
+            __syncwarp();
+            if (q < nc)
+                for (int t = 0; t < cntc; ++t) acc = __fmaf_rn(st[t * ST], st[t * ST + 1 + q], acc);
+            __syncwarp();
+        }
+        // the group's similarities to the leader: s~(i, a) and the listed centers'
+        float sv[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) sv[c] = __shfl_sync(FULL, acc, (lane & ~7) + c);
+        int cur = ai;
+        long long sims = 0;
+        if (valid && q == 0) {
+            const double eps = (double)reps[i];
+            float *ui = u + (int64_t)i * ku;
+            float lcur = sv[0];
+            ui[ai] = store_upper((double)lcur + eps);
+            sims = 1;
+#pragma unroll
+            for (int c = 1; c < NC; ++c) {
+                const int j = col[c];
+                if (j < 0) continue;
+                if ((double)ui[j] + eps <= (double)lcur) continue;
+                ui[j] = store_upper((double)sv[c] + eps);
+                ++sims;
+                if (sv[c] > lcur) {
+                    cur = j;
+                    lcur = sv[c];
+                }
+            }
+            l[i] = store_lower((double)lcur - eps);
+            if (cur != ai) a[i] = cur;
+        }
+        const bool leader = valid && q == 0;
+        warp_append(leader && cur != ai, i, mv_i, ai, mv_old, ctr + SPKM_CTR_MOVES);
+        ctr_add(s_ctr, SPKM_CTR_SIMS, sims);
+        ctr_add(s_ctr, SPKM_CTR_NNZ_ELKAN, leader ? (long long)len : 0);
+    }
+    PDL_TRIGGER();
+    ctr_flush(s_ctr, ctr);
 }
 
 // Centers per lane block of k_elkan_scan: EB = 4 (one float4 of a term-major
@@ -3729,6 +3869,12 @@ int64_t elkan_heavy_default(int64_t k) {
     return t < 1 ? 1 : t;
 }
 
+// simp_elkan with a heavy threshold of at most kLightMax + 1: the bound pass lists the failing centers of
+// every light row (W->lightj) and k_elkan_light scans just those (instead of k_elkan_scan)
+bool light_lists(const spkm_work *W, int use_cc) {
+    return !use_cc && W->lightj != nullptr && W->elkan_heavy > 0 && W->elkan_heavy <= kLightMax + 1;
+}
+
 RowPassArgs row_args(const spkm_csr *X, const spkm_centers *C) {
     RowPassArgs A{};
     A.ctl = C->ctl;
@@ -4215,11 +4361,11 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
     if (use_cc)
         pdl_launch(k_elkan_bounds<true>, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l,
                    B->u, B->ku, C->drift, C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl, (int)W->elkan_heavy,
-                   W->surv2);
+                   W->surv2, (int32_t *)nullptr);
     else
         pdl_launch(k_elkan_bounds<false>, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l,
                    B->u, B->ku, C->drift, C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl, (int)W->elkan_heavy,
-                   W->surv2);
+                   W->surv2, light_lists(W, use_cc) ? W->lightj : (int32_t *)nullptr);
     CHECK_LAUNCH("elkan_bounds");
     return 0;
 }
@@ -4256,6 +4402,13 @@ static int elkan_scan_launch(const spkm_csr *X, const spkm_centers *C, spkm_boun
                              bool fuse, void *stream) {
     if (X->n == 0) return 0;
     if (C->k > 1024) return fail_msg("elkan_scan: k > 1024 not supported by this build");
+    if (!fuse && light_lists(W, use_cc)) {   // the bound pass listed every light row's failing centers
+        pdl_launch(k_elkan_light, dim3(grid_for((X->n + 3) / 4, 8)), dim3(256), (size_t)0, S(stream), X->indptr, X->indices,
+                   X->values, X->row_eps, C->ct32, C->kp, (int)C->k, B->a, B->l, B->u, B->ku, W->surv1, W->lightj,
+                   W->mv_i, W->mv_old, W->ctr, C->ctl, hot_terms(C));
+        CHECK_LAUNCH("elkan_light");
+        return 0;
+    }
     const int grid = grid_for(X->n, 8);
     const int64_t eb = elkan_block(C->k), nbk = (C->k + eb - 1) / eb;
     const int64_t ppw_k = (32 / (nbk < 32 ? nbk : 32)) < 8 ? (32 / (nbk < 32 ? nbk : 32)) : 8;

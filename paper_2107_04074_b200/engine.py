@@ -693,6 +693,11 @@ class PointState:
     def __init__(self, n: int, k: int, variant: str, device, elkan_heavy: int = 0):
         i32 = dict(dtype=torch.int32, device=device)
         self.elkan_heavy = int(elkan_heavy)     # spkm_work.elkan_heavy (0: every bound survivor is scanned)
+        # simp_elkan with a small heavy threshold: the bound pass lists each light row's (<= 4) failing
+        # centers and the scan computes exactly those (spkm_work.lightj; SPKM_EK_LIGHT=0 turns it off)
+        self.lightj = (torch.full((max(n, 1) * 4,), -1, **i32)
+                       if variant == "simp_elkan" and 0 < self.elkan_heavy <= 5
+                       and os.environ.get("SPKM_EK_LIGHT", "1") != "0" else None)
         self.a = torch.zeros(max(n, 1), **i32)
         self.l = torch.zeros(max(n, 1), dtype=torch.float32, device=device)
         if variant in _ELKAN_FAMILY:
@@ -721,7 +726,8 @@ class PointState:
         self.hist_host = torch.zeros(cap * _lib.ST_COUNT + 2, dtype=torch.float64).pin_memory()
         self.bounds = Bounds(_ptr(self.a), _ptr(self.l), _ptr(self.u), self.ku)
         self.work = Work(_ptr(self.surv1), _ptr(self.surv2), _ptr(self.mv_i), _ptr(self.mv_old), _ptr(self.ctr),
-                         _ptr(self.stats), _ptr(self.hist), cap, self.elkan_heavy)
+                         _ptr(self.stats), _ptr(self.hist), cap, self.elkan_heavy,
+                         _ptr(self.lightj) if self.lightj is not None else None)
 
 
 # --------------------------------------------------------------- validation

@@ -604,3 +604,32 @@ def test_elkan_heavy_rows_bounds_audited(monkeypatch):
             assert rep.decisions_audited > 0
     engine.clear_engine_cache()
 
+
+@pytest.mark.parametrize("k", [300, 1000])
+def test_elkan_light_rows_listed_centers_equal_block_scan(k, monkeypatch):
+    """simp_elkan, default heavy threshold (ceil(k / 200) <= 5): the bound pass lists each light row's
+    failing centers and k_elkan_light computes exactly those.  Same scan semantics as k_elkan_scan, so
+    the fit AND every counter (sim_count, survivors, nnz) equal the block-scan fit (SPKM_EK_LIGHT=0)."""
+    from paper_2107_04074_b200 import engine, synth
+    m = spk()
+    data = synth.config_dataset("C3", n_override=20_000)
+    key = lambda s: (s.sim_count, s.reassignments, s.survivors, s.survivors2, s.nnz_elkan, s.nnz_rescan)  # noqa: E731
+    for pct in (None, "1.5"):          # k = 300: thresholds 2 and 5; k = 1000: 5 and 15 (15: no lists, same path twice)
+        if pct is None:
+            monkeypatch.delenv("SPKM_EK_HEAVY_PCT", raising=False)
+        else:
+            monkeypatch.setenv("SPKM_EK_HEAVY_PCT", pct)
+        monkeypatch.setenv("SPKM_EK_LIGHT", "0")
+        engine.clear_engine_cache()
+        ref = m.run(data, k, "simp_elkan", m.SeedConfig(seed=3), max_iter=30)
+        if k == 300:
+            assert any(s.survivors > 0 for s in ref.iterations[1:])      # light rows exist
+        monkeypatch.setenv("SPKM_EK_LIGHT", "1")
+        engine.clear_engine_cache()
+        for graphs in (False, True, True):
+            r = m.run(data, k, "simp_elkan", m.SeedConfig(seed=3), max_iter=30, use_graphs=graphs)
+            assert np.array_equal(r.assignments, ref.assignments)
+            assert r.objective == ref.objective
+            assert [key(s) for s in r.iterations] == [key(s) for s in ref.iterations]
+    engine.clear_engine_cache()
+

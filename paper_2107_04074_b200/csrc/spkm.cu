@@ -364,7 +364,8 @@ struct RowPassArgs {
 // lanes that own its columns (as the register gather), a sparse one as its
 // (j, value) pairs, one pair per lane.  Zeros contribute nothing to the FMA
 // chain, so every s~(i, j) is the canonical chain (ties and all).  The
-// lanes then pick up their CH columns into registers for the epilogue.
+// epilogue streams each lane's CH columns from shared memory, one float4 at a
+// time (holding them in CH registers spilled at the pass's 64 registers).
 #ifndef SPKM_EK_HEAVY_PCT_DEFAULT
 #define SPKM_EK_HEAVY_PCT_DEFAULT 0.5    // C4: 0.1 / 0.3 / 0.5 / 1 / 5 / 25 % -> 17.6 / 17.9 / 18.0 / 17.7 / 17.0 / 14.7 it/s (off: 13.2)
 #endif
@@ -374,7 +375,7 @@ struct RowPassArgs {
 // One row per warp (k > 256): lanes 0..tpr-1 own the columns (own), every
 // lane loads nnz and pairs; the row's start and length come from lane 0.
 template <int CH>
-__device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPassArgs &A, float *sacc, int64_t s_own,
+__device__ __forceinline__ void row_gather_sparse(const RowPassArgs &A, float *sacc, int64_t s_own,
                                                   int len_own, bool own, int lane, int j0, uint64_t pol_hot,
                                                   uint64_t pol_cold) {
     const int jstr = 4 * A.tpr;
@@ -464,16 +465,7 @@ __device__ __forceinline__ void row_gather_sparse(float (&acc)[CH], const RowPas
             }
         }
     }
-    __syncwarp();
-#pragma unroll
-    for (int r = 0; r < CH / 4; ++r) {   // (lanes that own no columns read a duplicate; their row is not valid)
-        const float4 a = *reinterpret_cast<const float4 *>(sacc + j0 + r * jstr);
-        acc[4 * r + 0] = a.x;
-        acc[4 * r + 1] = a.y;
-        acc[4 * r + 2] = a.z;
-        acc[4 * r + 3] = a.w;
-    }
-    __syncwarp();
+    __syncwarp();   // the row's similarities stay in sacc: the epilogue streams them from there (acc4)
 }
 
 // One row group's gather (the canonical chain per column, CSR order): lane q
@@ -641,11 +633,18 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
         const int jstr = 4 * A.tpr;
         float acc[CH];
         const uint64_t pol_hot = l2_policy_last(), pol_cold = l2_policy_first();
-        if constexpr (SPARSE)
-            row_gather_sparse<CH>(acc, A, reinterpret_cast<float *>(s_iv + 8 * A.rpw * kIvStride) + wib * A.kp, s, len,
-                                  lane_on, lane, j0, pol_hot, pol_cold);
-        else
+        float *sacc = nullptr;   // SPARSE: this warp's kp accumulators
+        if constexpr (SPARSE) {
+            sacc = reinterpret_cast<float *>(s_iv + 8 * A.rpw * kIvStride) + wib * A.kp;
+            row_gather_sparse<CH>(A, sacc, s, len, lane_on, lane, j0, pol_hot, pol_cold);
+        } else {
             row_gather<CH, UBH, HALF>(acc, A, my_iv, s, len, maxlen, q, j0, pol_hot, pol_cold);
+        }
+        // column group r of this lane: centers j0 + r * jstr .. + 3
+        auto acc4 = [&](int r) -> float4 {
+            if constexpr (SPARSE) return *reinterpret_cast<const float4 *>(sacc + j0 + r * jstr);
+            else return make_float4(acc[4 * r], acc[4 * r + 1], acc[4 * r + 2], acc[4 * r + 3]);
+        };
         const bool incumbent_mode = (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN || A.mode == MODE_ELKAN_FULL);
         const int inc = (valid && incumbent_mode) ? A.a[row] : -1;
         DCHECK(!valid || (row >= 0 && row < A.n && inc < A.k));
@@ -734,9 +733,14 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
         }
         Top2 tp{-INFINITY, -2, -INFINITY};
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-            const int j = j0 + (c >> 2) * jstr + (c & 3);
-            if (j < A.k) top2_push(tp, acc[c], j, inc);
+        for (int r = 0; r < CH / 4; ++r) {
+            const float4 a4 = acc4(r);
+            const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                const int j = j0 + r * jstr + c;
+                if (j < A.k) top2_push(tp, av[c], j, inc);
+            }
         }
         for (int o = o0; o; o >>= 1) {
             const Top2 other = top2_shfl_down(tp, o);
@@ -745,12 +749,16 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
         const double eps = valid ? (double)A.reps[row] : 0.0;
         float sa = 0.f;   // fused rescan: s~(i, a(i)) from the lane that holds a(i)
         if (fused) {
-            float mine = 0.f;
+            if constexpr (SPARSE) {
+                sa = (valid && inc >= 0) ? sacc[inc] : 0.f;   // one row per warp: every lane reads the same word
+            } else {
+                float mine = 0.f;
 #pragma unroll
-            for (int c = 0; c < CH; ++c)
-                if (j0 + (c >> 2) * jstr + (c & 3) == inc) mine = acc[c];
-            const int src = (valid && inc >= 0) ? g * A.tpr + (inc % jstr) / 4 : lane;
-            sa = __shfl_sync(FULL, mine, src);
+                for (int c = 0; c < CH; ++c)
+                    if (j0 + (c >> 2) * jstr + (c & 3) == inc) mine = acc[c];
+                const int src = (valid && inc >= 0) ? g * A.tpr + (inc % jstr) / 4 : lane;
+                sa = __shfl_sync(FULL, mine, src);
+            }
         }
         if (A.mode == MODE_INIT_YY) {
             // Yin-Yang group bounds: group f = the 4 consecutive centers of one
@@ -763,10 +771,12 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
                     const int f = q + r * A.tpr;
                     if (4 * f < A.k) {
                         float m = -INFINITY;
+                        const float4 a4 = acc4(r);
+                        const float av[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
                         for (int c = 0; c < 4; ++c) {
                             const int j = 4 * f + c;
-                            if (j < A.k && j != bj) m = fmaxf(m, acc[4 * r + c]);
+                            if (j < A.k && j != bj) m = fmaxf(m, av[c]);
                         }
                         A.u[row * A.ku + f] = (m == -INFINITY) ? -1.f : store_upper((double)m + eps);
                     }
@@ -775,9 +785,14 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
         }
         if (A.mode == SPKM_MODE_INIT_ELKAN && valid) {
 #pragma unroll
-            for (int c = 0; c < CH; ++c) {
-                const int j = j0 + (c >> 2) * jstr + (c & 3);
-                if (j < A.k) A.u[row * A.ku + j] = store_upper((double)acc[c] + eps);
+            for (int r = 0; r < CH / 4; ++r) {
+                const float4 a4 = acc4(r);
+                const float av[4] = {a4.x, a4.y, a4.z, a4.w};
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int j = j0 + r * jstr + c;
+                    if (j < A.k) A.u[row * A.ku + j] = store_upper((double)av[c] + eps);
+                }
             }
         }
         if (A.mode == MODE_ELKAN_FULL && valid) {   // every u(i, j) exact: one 16-byte store per column group (ku % 4 == 0)
@@ -785,14 +800,16 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
 #pragma unroll
             for (int r = 0; r < CH / 4; ++r) {
                 const int j = j0 + r * jstr;
+                const float4 a4 = acc4(r);
                 if (j + 3 < A.k) {
                     *reinterpret_cast<float4 *>(ur + j) =
-                        make_float4(store_upper((double)acc[4 * r] + eps), store_upper((double)acc[4 * r + 1] + eps),
-                                    store_upper((double)acc[4 * r + 2] + eps), store_upper((double)acc[4 * r + 3] + eps));
+                        make_float4(store_upper((double)a4.x + eps), store_upper((double)a4.y + eps),
+                                    store_upper((double)a4.z + eps), store_upper((double)a4.w + eps));
                 } else {
+                    const float av[4] = {a4.x, a4.y, a4.z, a4.w};
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
-                        if (j + c < A.k) ur[j + c] = store_upper((double)acc[4 * r + c] + eps);
+                        if (j + c < A.k) ur[j + c] = store_upper((double)av[c] + eps);
                 }
             }
         }
@@ -866,6 +883,7 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
                 }
             }
         }
+        if constexpr (SPARSE) __syncwarp();   // every lane is done with sacc before the next row zeroes it
     }
     PDL_TRIGGER();
     if (A.ctr) ctr_flush(s_ctr, A.ctr);

@@ -896,6 +896,15 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
 // 128-byte line and the kHbPer loads of a thread are independent); the
 // survivors of the tile are appended with ONE global atomic (warp ballots ->
 // per-warp counts in shared memory -> one prefix), not one per warp.
+// sin(acos(x)) = sqrt(1 - x^2) for a float x, rounded UP, as a double: float32 MUFU rsqrt x (1 + 2^-19) instead of
+// the float64 sqrt sequence (two per point made this 96 MB stream arithmetic-bound).  Both uses below want an upper
+// bound of the sine (it lowers l and raises u); the excess is < 2^-18 relative, times a sine of the drift.
+__device__ __forceinline__ double f_sin_up(float x) {
+    const float y = fmaxf(__fmaf_ru(-x, x, 1.0f), 1e-30f);
+    float r;
+    asm("rsqrt.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(y));
+    return (double)__fmul_ru(y * r, 1.0f + 1.9073486e-6f);
+}
 constexpr int kHbThreads = 256, kHbPer = 4, kHbTile = kHbThreads * kHbPer;
 __global__ void __launch_bounds__(kHbThreads) k_hamerly_bounds(int64_t n, const float *__restrict__ reps,
                                                         const int32_t *__restrict__ a, float *l, float *u,
@@ -933,7 +942,7 @@ __global__ void __launch_bounds__(kHbThreads) k_hamerly_bounds(int64_t n, const 
             float lf = lo[r];
             if (sa != 0.0) {   // cos(theta_l + theta_p), theta_p from the chord bound
                 const double pa = drift[ai[r]];
-                const double ln = (lo[r] < -pa) ? -1.0 : d_clamp((double)lo[r] * pa - d_sin((double)lo[r]) * sa);
+                const double ln = (lo[r] < -pa) ? -1.0 : d_clamp((double)lo[r] * pa - f_sin_up(lo[r]) * sa);
                 lf = store_lower(ln);
                 l[i] = lf;
             }
@@ -947,7 +956,7 @@ __global__ void __launch_bounds__(kHbThreads) k_hamerly_bounds(int64_t n, const 
                 }
             } else if (!(uo[r] >= 0.f && worst_s == 0.0)) {   // engine.py:290-298
                 const double un = (uo[r] >= 0.f && worst_p >= 0.0)
-                                      ? d_clamp((double)uo[r] + d_sin((double)uo[r]) * worst_s)
+                                      ? d_clamp((double)uo[r] + f_sin_up(uo[r]) * worst_s)
                                       : 1.0;
                 uf = store_upper(un);
                 u[i] = uf;

@@ -26,6 +26,6 @@ $NCU --metrics gpu__time_duration.sum --csv --log-file $O/f_launches.csv $B > $O
 python tools/ncu_launches.py $O/f_launches.csv > $O/f_launches.txt; head -24 $O/f_launches.txt
 F="$NCU --set full --import-source on -f"
 $F -k regex:"k_row_pass|k_ci_|k_hamerly_bounds|k_center_write|k_gram_mn" --launch-skip 40 --launch-count 8 -o /tmp/f_c4_h $B --variants hamerly > $O/f_ncu_h.log 2>&1
-$F -k regex:"k_elkan|k_row_pass" --launch-skip 12 --launch-count 4 -o /tmp/f_c4_e $B --variants simp_elkan > $O/f_ncu_e.log 2>&1
+$F -k regex:"k_elkan|k_row_pass" --launch-skip 24 --launch-count 6 -o /tmp/f_c4_e $B --variants simp_elkan > $O/f_ncu_e.log 2>&1
 for r in h e; do python tools/ncu_summary.py /tmp/f_c4_$r.ncu-rep > $O/f_c4_$r.txt 2>&1; cat $O/f_c4_$r.txt; cp /tmp/f_c4_$r.ncu-rep $O/; done
 ls -la $O/f_*

@@ -671,6 +671,15 @@ def roofline(args, data, corpus, dev, world):
             if key in tr:
                 out["traffic_" + key] = tr[key]
     out["per_kernel"] = per
+    # the whole step on SURVEY 8(d)'s definition: B_iter = CSR bytes + bound bytes of every pass (center
+    # update and move bytes are reported separately, below), over the instrumented step's kernel time
+    iter_entries = [nm for nm in calls if nm not in ("spkm_move_centers", "spkm_apply_moves") and entry_bytes(nm)]
+    b_iter = sum(entry_bytes(nm) for nm in iter_entries)
+    if b_iter and total:
+        out["step"] = {"algorithmic_bytes": b_iter, "ms": round(total, 3),
+                       "achieved_gbs": round(b_iter / (total / 1e3) / 1e9, 1),
+                       "frac": round(b_iter / (total / 1e3) / 1e9 / pk.get("hbm_gbs"), 4),
+                       "note": "sum of CSR + bound bytes of all passes / sum of all kernels' event time of one step"}
     # the gather passes are bound by the center-row gathers (L2/DRAM), not by
     # their CSR bytes: the center-row bytes they pull per second
     gv = {}

@@ -369,9 +369,6 @@ struct RowPassArgs {
 #ifndef SPKM_EK_HEAVY_PCT_DEFAULT
 #define SPKM_EK_HEAVY_PCT_DEFAULT 0.5    // C4: 0.1 / 0.3 / 0.5 / 1 / 5 / 25 % -> 17.6 / 17.9 / 18.0 / 17.7 / 17.0 / 14.7 it/s (off: 13.2)
 #endif
-#ifndef SPKM_SP_LEAD
-#define SPKM_SP_LEAD 0            // 1: the row's leading run of dense term rows in registers; 2: timing probe
-#endif
 #ifndef SPKM_SP_PREFETCH
 #define SPKM_SP_PREFETCH 0        // per-term bulk L2 prefetch: measured slower at C4 (2267 vs 2184 ms per fit)
 #endif
@@ -384,67 +381,11 @@ __device__ __forceinline__ void row_gather_sparse(const RowPassArgs &A, float *s
     const int jstr = 4 * A.tpr;
     const int64_t s = __shfl_sync(FULL, s_own, 0);
     const int maxlen = __shfl_sync(FULL, len_own, 0);
-#if SPKM_SP_LEAD
-    // The row's leading run of dense term rows (rows are stored with their terms in document-frequency
-    // order, so the Zipf head -- the dense rows -- comes first): accumulated in registers, one half of the
-    // lane's columns at a time (CH/2 accumulators + CH/8 float4 loads: inside the 64-register budget), and
-    // stored once -- 32 LSU wavefronts per dense term instead of 96 (load + shared-memory read-modify-write).
-    // The run is a prefix of the CSR order, so every chain is still the canonical one.
-    unsigned lead_mask = 0;
-    {
-        const int cnt0 = min(32, maxlen);
-        int id0 = 0;
-        float v0 = 0.f;
-        bool dense0 = false;
-        if (lane < cnt0) {
-            id0 = __ldg(A.indices + s + lane);
-            v0 = __ldg(A.values + s + lane);
-            dense0 = (int)(__ldg(reinterpret_cast<const long long *>(A.ci_desc) + id0) & 0xFFF) == 0xFFF;
-        }
-        const unsigned dm = __ballot_sync(FULL, dense0);
-#if SPKM_SP_LEAD == 2
-        lead_mask = dm;                                   // timing probe: every dense term of the first chunk (wrong order)
-#else
-        const int lead = __ffs(~dm) - 1;                  // first term that is not a dense row (32: none)
-        lead_mask = lead >= 32 ? 0xffffffffu : ((1u << lead) - 1u);
-#endif
-        if (own) {
-#pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float4 a[CH / 8];
-#pragma unroll
-                for (int r = 0; r < CH / 8; ++r) a[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-                for (unsigned m = lead_mask; m; m &= m - 1) {
-                    const int t = __ffs(m) - 1;
-                    const int tid = __shfl_sync(FULL, id0, t);
-                    const float tv = __shfl_sync(FULL, v0, t);
-                    const float4 *p = reinterpret_cast<const float4 *>(A.ct + (int64_t)tid * A.kp + j0);
-                    const uint64_t pol = tid < A.hot ? pol_hot : pol_cold;
-                    float4 x[CH / 8];
-#pragma unroll
-                    for (int r = 0; r < CH / 8; ++r) x[r] = ldg_hint(p + (h * (CH / 8) + r) * A.tpr, pol);
-#pragma unroll
-                    for (int r = 0; r < CH / 8; ++r) {
-                        a[r].x = __fmaf_rn(tv, x[r].x, a[r].x);
-                        a[r].y = __fmaf_rn(tv, x[r].y, a[r].y);
-                        a[r].z = __fmaf_rn(tv, x[r].z, a[r].z);
-                        a[r].w = __fmaf_rn(tv, x[r].w, a[r].w);
-                    }
-                }
-#pragma unroll
-                for (int r = 0; r < CH / 8; ++r)
-                    *reinterpret_cast<float4 *>(sacc + j0 + (h * (CH / 8) + r) * jstr) = a[r];
-            }
-        }
-    }
-#else
-    constexpr unsigned lead_mask = 0;
     if (own) {
 #pragma unroll
         for (int r = 0; r < CH / 4; ++r)
             *reinterpret_cast<float4 *>(sacc + j0 + r * jstr) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
-#endif
     __syncwarp();
     bool last_sparse = true;
     for (int c0 = 0; c0 < maxlen; c0 += 32) {
@@ -476,7 +417,6 @@ __device__ __forceinline__ void row_gather_sparse(const RowPassArgs &A, float *s
 #endif
         }
         for (int t = 0; t < cnt; ++t) {
-            if (c0 == 0 && (lead_mask >> t & 1u)) continue;   // done in registers above
             const int tid = __shfl_sync(FULL, id, t);
             const float tv = __shfl_sync(FULL, v, t);
             const long long td = __shfl_sync(FULL, dsc, t);
@@ -2226,6 +2166,9 @@ __global__ void __launch_bounds__(256) k_ci_build(int64_t d, int64_t kp, int k, 
         if (t < d) {
             for (int j0 = 4 * lane; j0 < k; j0 += 128) {
                 const float4 v = __ldg(reinterpret_cast<const float4 *>(row + j0));
+                // most float4 of a center table are all zero (C4: 72%): one test instead of four
+                if (((__float_as_uint(v.x) | __float_as_uint(v.y) | __float_as_uint(v.z) | __float_as_uint(v.w)) << 1) == 0u)
+                    continue;
                 c += (v.x != 0.f) + (j0 + 1 < k && v.y != 0.f) + (j0 + 2 < k && v.z != 0.f) + (j0 + 3 < k && v.w != 0.f);
             }
         }

@@ -528,7 +528,7 @@ def main_ours(args):
 # per KERNEL, so entry points sharing one kernel are pooled)
 KERNEL_OF = {"spkm_full_assign": "k_row_pass", "spkm_hamerly_rescan": "k_row_pass",
              "spkm_hamerly_tighten": "k_hamerly_tighten", "spkm_hamerly_bounds": "k_hamerly_bounds",
-             "spkm_elkan_bounds": "k_elkan_bounds", "spkm_elkan_scan": "k_elkan_scan",
+             "spkm_elkan_bounds": "k_elkan_bounds", "spkm_elkan_scan": "k_elkan_scan / k_elkan_light",
              "spkm_elkan_heavy": "k_row_pass",
              "spkm_elkan_bounds_scan": "k_elkan_scan (fused bounds)", "spkm_dense_assign": "k_dense_pass",
              "spkm_apply_moves": "k_apply_moves", "spkm_aggregate_sums": "k_aggregate",
@@ -586,7 +586,12 @@ def roofline(args, data, corpus, dev, world):
                 # the 16-byte groups holding a center that moved (touched clusters of the previous iteration)
                 moved_prev = [its[q - 1].touched for q in range(1, len(its))]
                 b_bounds = sum((4 * ku + 16) * n + 4 * min(ku, 4 * m) * n for m in moved_prev)
-                b_scan = sum(8 * s.nnz_elkan + (csr_row + 4 * ku + 16) * s.survivors for s in its[1:])
+                # light rows scanned from the bound pass's lists (k_elkan_light: simp_elkan, heavy threshold <= 5):
+                # the 16-byte list, a / l / eps, and the <= 5 u(i, j) touched instead of the whole u row
+                lists = (v == "simp_elkan" and any(s.survivors2 for s in its[1:]) and (k + 199) // 200 <= 5
+                         and os.environ.get("SPKM_EK_LIGHT", "1") != "0" and not os.environ.get("SPKM_EK_HEAVY_PCT"))
+                per_surv = (csr_row + 16 + 16 + 40) if lists else (csr_row + 4 * ku + 16)
+                b_scan = sum(8 * s.nnz_elkan + per_surv * s.survivors for s in its[1:])
                 bytes_by[("spkm_elkan_bounds", v)] = b_bounds
                 bytes_by[("spkm_elkan_scan", v)] = b_scan
                 # heavy rows (spkm_elkan_heavy, k > 256): CSR row + a, l, eps, and every u(i, j) written

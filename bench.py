@@ -585,7 +585,11 @@ def roofline(args, data, corpus, dev, world):
                 # bound pass: u read (4 ku) + a, l, eps (12) + l write (4) per row, and u written only in
                 # the 16-byte groups holding a center that moved (touched clusters of the previous iteration)
                 moved_prev = [its[q - 1].touched for q in range(1, len(its))]
-                b_bounds = sum((4 * ku + 16) * n + 4 * min(ku, 4 * m) * n for m in moved_prev)
+                # the bound pass is skipped (every row takes the full pass) in an iteration that follows one
+                # which moved >= n / 256 rows (spkm_work.allheavy_rows; only with the heavy-row pass, k > 256)
+                heavy_on = any(s.survivors2 for s in its[1:]) and os.environ.get("SPKM_EK_ALLHEAVY", "1") != "0"
+                ran = [not (heavy_on and 256 * its[q - 1].reassignments >= n) for q in range(1, len(its))]
+                b_bounds = sum(((4 * ku + 16) * n + 4 * min(ku, 4 * m) * n) for m, r_ in zip(moved_prev, ran) if r_)
                 # light rows scanned from the bound pass's lists (k_elkan_light: simp_elkan, heavy threshold <= 5):
                 # the 16-byte list, a / l / eps, and the <= 5 u(i, j) touched instead of the whole u row
                 lists = (v == "simp_elkan" and any(s.survivors2 for s in its[1:]) and (k + 199) // 200 <= 5

@@ -108,7 +108,7 @@ typedef struct spkm_centers {
     double *norm;            /* [k] scratch: |sums_j|                       */
     float *cc;               /* [k*k] half-angle center cosines, rounded up */
     float *s;                /* [k]   row max of cc (diag excluded)         */
-    double *hstat;           /* [8]   owner, p_min, p_min2, owner_s, smax, smax2, fuse */
+    double *hstat;           /* [8]   owner, p_min, p_min2, owner_s, smax, smax2, fuse, all-heavy */
     int32_t *tlist;          /* [k]   scratch: touched cluster list         */
     int32_t *tcount;         /* [1]   scratch: its length                   */
     long long *ctl;          /* [2]   {iterations done, converged}: every loop
@@ -154,6 +154,10 @@ typedef struct spkm_work {
     int64_t hist_cap;
     int64_t elkan_heavy;     /* > 0: spkm_elkan_bounds sends rows with at least this many unpruned
                               * centers to surv2 for spkm_elkan_heavy                     */
+    int64_t allheavy_rows;   /* > 0 (= the rows this engine scans) with elkan_heavy > 0: while an iteration
+                              * moves >= allheavy_rows / 256 rows, the next one skips spkm_elkan_bounds and
+                              * spkm_elkan_heavy takes every row (flag in hstat[7], set by spkm_finalize);
+                              * 0: never (debug hooks that read the bounds between the calls)            */
     int32_t *lightj;         /* [n][4] or NULL.  With use_cc == 0 and 0 < elkan_heavy <= 5 the bound
                               * pass lists the (< elkan_heavy) failing centers of every surv1 row here
                               * (ascending, -1 padded) and spkm_elkan_scan scans exactly those        */

@@ -69,7 +69,7 @@ class Svml(ctypes.Structure):
 
 class Work(ctypes.Structure):
     _fields_ = [("surv1", c_vp), ("surv2", c_vp), ("mv_i", c_vp), ("mv_old", c_vp), ("ctr", c_vp),
-                ("stats", c_vp), ("stats_hist", c_vp), ("hist_cap", c_i64), ("elkan_heavy", c_i64), ("lightj", c_vp)]
+                ("stats", c_vp), ("stats_hist", c_vp), ("hist_cap", c_i64), ("elkan_heavy", c_i64), ("allheavy_rows", c_i64), ("lightj", c_vp)]
 
 
 # modes / enums (include/spkm.h)

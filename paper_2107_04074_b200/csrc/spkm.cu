@@ -75,6 +75,11 @@ constexpr double kSqrt2 = 1.4142135623730951;
 constexpr double kZeroSumEps = 1e-12;       // engine.py:27
 constexpr int kCenterChunk = 4096;          // d-chunk of the center kernels
 constexpr int kFuseFlag = 6;                // hstat slot: fused Hamerly tighten + rescan next iteration
+// hstat slot: Elkan family, every row takes the full pass next iteration and the bound pass is skipped.  Set
+// by k_finalize while an iteration still moves at least 1/256 of the rows: at C4 those are the iterations in
+// which the bound pass sends all 4M rows to the heavy pass anyway (profiles/r02_c4_iteration_stats.txt), after
+// streaming 32 GB of bounds to find that out.  A performance switch only: the full pass is exact for any row.
+constexpr int kAllHeavyFlag = 7;
 
 thread_local char g_err[512] = {0};
 
@@ -356,6 +361,7 @@ struct RowPassArgs {
     int64_t d;                   // term rows of ct (bounds checks of the debug build)
     const int64_t *ci_desc;      // sparse center index (SPARSE instantiations): per term row
     const int2 *ci_pairs;        //   (offset << 12 | count) and the (j, value bits) pairs
+    const double *allheavy;      // MODE_ELKAN_FULL: != 0 -> every row [0, n), the bound pass was skipped
 };
 
 // Sparse gather (k > 256 with a center index): the row's accumulators live in
@@ -613,7 +619,8 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
     const int g = lane / A.tpr, q = lane - g * A.tpr;
     const bool lane_on = g < A.rpw;
     const bool fused = A.mode == MODE_RESCAN && A.fuse && *A.fuse != 0.0;
-    const int32_t *rowlist = fused ? A.rowlist_fused : A.rowlist;
+    const bool allrows = A.mode == MODE_ELKAN_FULL && A.allheavy && *A.allheavy != 0.0;
+    const int32_t *rowlist = allrows ? nullptr : fused ? A.rowlist_fused : A.rowlist;
     const int64_t nrows = rowlist ? (fused ? *A.rowcount_fused : *A.rowcount) : A.n;
     const int64_t nslots = (nrows + A.rpw - 1) / A.rpw;
     const int o0 = A.tpr > 1 ? (1 << (31 - __clz(A.tpr - 1))) : 0;
@@ -869,6 +876,7 @@ __global__ void __launch_bounds__(NT, CH <= 8 ? 1024 / NT : GV == 2 ? SPKM_RP_SP
             warp_append(moved, (int32_t)row, A.mv_i, inc, A.mv_old, A.ctr + SPKM_CTR_MOVES);
             ctr_add(s_ctr, SPKM_CTR_SIMS, leader ? (long long)A.k : 0);
             ctr_add(s_ctr, SPKM_CTR_NNZ_RESCAN, leader ? (long long)(e - s) : 0);   // (the block scan counts NNZ_ELKAN)
+            if (allrows) ctr_add(s_ctr, SPKM_CTR_SURV2, leader ? 1 : 0);            // (else counted by the bound pass)
         }
         if (A.mode == SPKM_MODE_LLOYD || A.mode == MODE_RESCAN) {
             warp_append(moved, (int32_t)row, A.mv_i, inc, A.mv_old, A.ctr + SPKM_CTR_MOVES);
@@ -1151,9 +1159,11 @@ __global__ void __launch_bounds__(256, SPKM_EB_MINB) k_elkan_bounds(int64_t n, i
                                                       const float *__restrict__ cc,
                                                       const float *__restrict__ s_arr, int use_cc,
                                                       int32_t *surv1, long long *ctr, const long long *__restrict__ ctl,
-                                                      int heavy_thr, int32_t *surv_h, int32_t *lightj) {
+                                                      int heavy_thr, int32_t *surv_h, int32_t *lightj,
+                                                      const double *__restrict__ allheavy) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
+    if (heavy_thr > 0 && *allheavy != 0.0) return;   // every row takes the full pass this iteration (kAllHeavyFlag)
     __shared__ __align__(16) float s_pd[kEbMaxK], s_pu[kEbMaxK], s_su[kEbMaxK];
     const int k4 = (k + 3) >> 2;
     for (int j = threadIdx.x; j < 4 * k4; j += blockDim.x) {
@@ -2992,7 +3002,8 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
                                                           double *sinp, const double *__restrict__ objc,
                                                           double *hstat, long long *ctr, double *stats,
                                                           long long sims_extra, int all, double *stats_hist,
-                                                          int64_t hist_cap, int fuse_policy, long long *ctl) {
+                                                          int64_t hist_cap, int fuse_policy, long long *ctl,
+                                                          long long allheavy_rows) {
     PDL_ENTRY();
     if (ctl[1]) return;   // converged: later enqueued iterations are no-ops
     __shared__ double s_ob[kFinThreads / 32];
@@ -3064,6 +3075,7 @@ __global__ void __launch_bounds__(kFinThreads) k_finalize(int64_t k, int32_t *to
         // the tighten test itself (same results and counters, one pass less)
         const bool fuse_auto = 20 * cv[SPKM_CTR_SURV2] >= 19 * cv[SPKM_CTR_SURV1];
         hstat[kFuseFlag] = (cv[SPKM_CTR_SURV1] > 0 && (fuse_policy == 1 || (fuse_policy == 2 && fuse_auto))) ? 1.0 : 0.0;
+        hstat[kAllHeavyFlag] = (allheavy_rows > 0 && 256 * cv[SPKM_CTR_MOVES] >= allheavy_rows) ? 1.0 : 0.0;
         sv[SPKM_ST_OBJECTIVE] = tot;
         sv[SPKM_ST_ALLONE] = no ? 0.0 : 1.0;
         sv[SPKM_ST_TOUCHED] = (double)tc;
@@ -4394,11 +4406,12 @@ int spkm_elkan_bounds(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, 
     if (use_cc)
         pdl_launch(k_elkan_bounds<true>, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l,
                    B->u, B->ku, C->drift, C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl, (int)W->elkan_heavy,
-                   W->surv2, (int32_t *)nullptr);
+                   W->surv2, (int32_t *)nullptr, (const double *)(C->hstat + kAllHeavyFlag));
     else
         pdl_launch(k_elkan_bounds<false>, dim3(grid), dim3(256), (size_t)(0), S(stream), X->n, (int)C->k, X->row_eps, B->a, B->l,
                    B->u, B->ku, C->drift, C->sinp, C->cc, C->s, use_cc, W->surv1, W->ctr, C->ctl, (int)W->elkan_heavy,
-                   W->surv2, light_lists(W, use_cc) ? W->lightj : (int32_t *)nullptr);
+                   W->surv2, light_lists(W, use_cc) ? W->lightj : (int32_t *)nullptr,
+                   (const double *)(C->hstat + kAllHeavyFlag));
     CHECK_LAUNCH("elkan_bounds");
     return 0;
 }
@@ -4419,6 +4432,7 @@ int spkm_elkan_heavy(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, s
     A.mode = MODE_ELKAN_FULL;
     A.rowlist = W->surv2;
     A.rowcount = W->ctr + SPKM_CTR_SURV2;
+    A.allheavy = C->hstat + kAllHeavyFlag;
     A.a = B->a;
     A.l = B->l;
     A.u = B->u;
@@ -4618,7 +4632,8 @@ static int hamerly_fuse_policy() {
 int spkm_finalize(const spkm_centers *C, spkm_work *W, int all_clusters, long long sims_extra, void *stream) {
     pdl_launch(k_finalize, dim3(1), dim3(kFinThreads), (size_t)(0), S(stream), C->k, C->touched, C->tcount, C->drift, C->sinp, C->objc, C->hstat,
                                                  W->ctr, W->stats, sims_extra, all_clusters, W->stats_hist,
-                                                 W->hist_cap, hamerly_fuse_policy(), C->ctl);
+                                                 W->hist_cap, hamerly_fuse_policy(), C->ctl,
+                                                 (long long)(W->elkan_heavy > 0 ? W->allheavy_rows : 0));
     CHECK_LAUNCH("finalize");
     return 0;
 }

@@ -690,9 +690,15 @@ def fixed_sums_host(data: Dataset, a: np.ndarray, k: int, scale_bits: int) -> np
 class PointState:
     """Per-point bounds and worklists (spkm_bounds + spkm_work)."""
 
-    def __init__(self, n: int, k: int, variant: str, device, elkan_heavy: int = 0):
+    def __init__(self, n: int, k: int, variant: str, device, elkan_heavy: int = 0, n_total: int | None = None):
         i32 = dict(dtype=torch.int32, device=device)
         self.elkan_heavy = int(elkan_heavy)     # spkm_work.elkan_heavy (0: every bound survivor is scanned)
+        # spkm_work.allheavy_rows: skip the bound pass while an iteration still moves >= n / 256 rows
+        # (SPKM_EK_ALLHEAVY=0 turns it off; run() clears it while a debug hook reads the bounds)
+        # (n_total: the move counter k_finalize compares it with is summed over the ranks of a multi-GPU fit,
+        # so every rank and the single-GPU fit take the same decision)
+        self.allheavy_rows = ((n_total if n_total is not None else n)
+                              if (self.elkan_heavy > 0 and os.environ.get("SPKM_EK_ALLHEAVY", "1") != "0") else 0)
         # simp_elkan with a small heavy threshold: the bound pass lists each light row's (<= 4) failing
         # centers and the scan computes exactly those (spkm_work.lightj; SPKM_EK_LIGHT=0 turns it off)
         self.lightj = (torch.full((max(n, 1) * 4,), -1, **i32)
@@ -726,7 +732,7 @@ class PointState:
         self.hist_host = torch.zeros(cap * _lib.ST_COUNT + 2, dtype=torch.float64).pin_memory()
         self.bounds = Bounds(_ptr(self.a), _ptr(self.l), _ptr(self.u), self.ku)
         self.work = Work(_ptr(self.surv1), _ptr(self.surv2), _ptr(self.mv_i), _ptr(self.mv_old), _ptr(self.ctr),
-                         _ptr(self.stats), _ptr(self.hist), cap, self.elkan_heavy,
+                         _ptr(self.stats), _ptr(self.hist), cap, self.elkan_heavy, self.allheavy_rows,
                          _ptr(self.lightj) if self.lightj is not None else None)
 
 
@@ -793,7 +799,7 @@ class Engine:
         # spkm_elkan_heavy (threshold from the library: SPKM_EK_HEAVY_PCT percent of k, 0 = off)
         self.elkan_heavy = (int(_lib.lib().spkm_elkan_heavy_threshold(k))
                             if self.elkan and self.C.cindex is not None else 0)
-        self.P = PointState(self.n_loc, k, variant, self.device, elkan_heavy=self.elkan_heavy)
+        self.P = PointState(self.n_loc, k, variant, self.device, elkan_heavy=self.elkan_heavy, n_total=self.n_total)
         self.a_global = torch.zeros(max(cs.n, 1), dtype=torch.int32, device=self.device) if comm is not None else None
         # a dedicated stream: steady-state iterations are replayed as one CUDA graph
         self.stream = torch.cuda.Stream(device=self.device)
@@ -1264,6 +1270,9 @@ def run(data: Dataset, k: int, variant: str, seeding=None, max_iter: int = 100, 
     if eng.P.hist_cap < max_iter + 1:
         eng.drop_loop()                     # the captured loop holds the old history pointer
         eng.P.set_history(max_iter + 1)
+    # a debug hook reads the bounds between the bound pass and the scans: never skip the bound pass then
+    # (hook runs are eager, so the struct is read at every call; captured graphs hold the no-hook value)
+    eng.P.work.allheavy_rows = 0 if debug_hook is not None else eng.P.allheavy_rows
     prof = _lib.active_profiler()
     untimed = not (prof is not None and prof.timed)
     device_loop = (eng.use_graphs and eng.runs > 0 and debug_hook is None and comm is None and untimed)

@@ -576,8 +576,11 @@ def test_elkan_heavy_rows_full_pass_equals_scan(k, variant, monkeypatch):
     lloyd = m.run(data, k, "standard", m.SeedConfig(seed=3), max_iter=30)
     assert np.array_equal(ref.assignments, lloyd.assignments) and ref.objective == lloyd.objective
     assert all(s.survivors2 == 0 for s in ref.iterations)
-    for pct in ("1", "25", "60"):
+    # SPKM_EK_ALLHEAVY: while an iteration moves >= n / 256 rows the next one skips the bound pass and every
+    # row takes the full pass (a performance switch; "0" keeps the bound pass in every iteration)
+    for pct, allheavy in (("1", "0"), ("25", "0"), ("60", "0"), ("1", "1"), ("25", "1")):
         monkeypatch.setenv("SPKM_EK_HEAVY_PCT", pct)
+        monkeypatch.setenv("SPKM_EK_ALLHEAVY", allheavy)
         engine.clear_engine_cache()
         for graphs in (False, True, True):
             r = m.run(data, k, variant, m.SeedConfig(seed=3), max_iter=30, use_graphs=graphs)
@@ -585,8 +588,11 @@ def test_elkan_heavy_rows_full_pass_equals_scan(k, variant, monkeypatch):
             assert r.objective == ref.objective
             assert [s.reassignments for s in r.iterations] == [s.reassignments for s in ref.iterations]
             assert any(s.survivors2 > 0 for s in r.iterations[1:])       # the heavy pass did run
-            assert (sum(s.survivors + s.survivors2 for s in r.iterations[1:])
-                    <= sum(s.survivors for s in ref.iterations[1:]))     # exact u(i, j): never more survivors
+            if allheavy == "0":
+                assert (sum(s.survivors + s.survivors2 for s in r.iterations[1:])
+                        <= sum(s.survivors for s in ref.iterations[1:]))     # exact u(i, j): never more survivors
+            else:
+                assert r.iterations[1].survivors2 == data.n and r.iterations[1].survivors == 0   # iteration 2: all rows
     engine.clear_engine_cache()
 
 

@@ -86,6 +86,30 @@ def normalize(v):
     return v / nrm
 
 
+_HELPER_OK = None
+
+
+def _helper_matches_numpy(L) -> bool:
+    """The host helper replays the summation order of the ddot kernel numpy's
+    bundled OpenBLAS uses on this machine (SkylakeX-style 32-accumulator
+    blocks).  Another BLAS kernel would round differently in the last bit, so
+    the helper is probed once against np.dot on rows of every length class
+    and only used when it agrees bit for bit; otherwise the per-row np.dot
+    loop (the reference's own arithmetic) is used."""
+    global _HELPER_OK
+    if _HELPER_OK is None:
+        g = np.random.default_rng(12345)
+        lens = [1, 2, 3, 7, 8, 15, 16, 17, 31, 32, 33, 47, 48, 63, 64, 65, 100, 127, 128, 129, 255, 400]
+        ip = np.zeros(len(lens) + 1, np.int64)
+        np.cumsum(lens, out=ip[1:])
+        dv = g.random(int(ip[-1]))
+        got = np.zeros(len(lens))
+        L.spkm_host_row_norms(len(lens), ip.ctypes.data, dv.ctypes.data, got.ctypes.data)
+        ref = np.array([np.sqrt(np.dot(dv[a:b], dv[a:b])) for a, b in zip(ip[:-1], ip[1:])])
+        _HELPER_OK = bool(np.array_equal(got, ref))
+    return _HELPER_OK
+
+
 def _row_norms(indptr, data):
     """|row| of every CSR row exactly as SparseVector.norm computes it
     (np.sqrt(np.dot(v, v)), sparse.py:52): the library's host helper replays
@@ -102,7 +126,7 @@ def _row_norms(indptr, data):
         L = None
     ip = np.ascontiguousarray(indptr, np.int64)
     dv = np.ascontiguousarray(data, np.float64)
-    if L is not None:
+    if L is not None and _helper_matches_numpy(L):
         L.spkm_host_row_norms(n, ip.ctypes.data, dv.ctypes.data, out.ctypes.data)
         return out
     for i in range(n):   # same values, one np.dot per row

@@ -73,6 +73,24 @@ class TestDataset:
         assert np.array_equal(a.indptr, b.indptr) and np.array_equal(a.indices, b.indices)
         assert np.allclose(a.data, b.data, rtol=1e-15)
 
+    def test_row_norm_helper_is_probed_and_has_an_exact_fallback(self, monkeypatch):
+        """The ddot-order host helper is only used when it reproduces np.dot bit
+        for bit on this machine; otherwise (another BLAS kernel) the per-row
+        np.dot loop gives the reference's values.  Both paths agree here."""
+        from paper_2107_04074_b200 import sparse
+        g = np.random.default_rng(5)
+        lens = g.integers(1, 300, 200)
+        ip = np.zeros(lens.size + 1, np.int64)
+        np.cumsum(lens, out=ip[1:])
+        dv = g.random(int(ip[-1]))
+        ref = np.array([np.sqrt(np.dot(dv[a:b], dv[a:b])) for a, b in zip(ip[:-1], ip[1:])])
+        monkeypatch.setattr(sparse, "_HELPER_OK", None)
+        fast = sparse._row_norms(ip, dv)
+        monkeypatch.setattr(sparse, "_HELPER_OK", False)
+        slow = sparse._row_norms(ip, dv)
+        assert np.array_equal(slow, ref)
+        assert np.array_equal(fast, ref)
+
     def test_from_csr_rejects_unsorted_and_zero_rows(self):
         with pytest.raises(ValueError):
             Dataset.from_csr([0, 2], [3, 1], [1.0, 1.0], 4)

@@ -639,3 +639,24 @@ def test_elkan_light_rows_listed_centers_equal_block_scan(k, monkeypatch):
             assert [key(s) for s in r.iterations] == [key(s) for s in ref.iterations]
     engine.clear_engine_cache()
 
+
+@pytest.mark.parametrize("k", [257, 511, 513, 1023, 1024])
+def test_elkan_heavy_and_light_rows_at_boundary_k(k):
+    """Boundary k of the k > 256 paths (16- and 32-column lanes, u rows whose last float4 is partial, ku padding):
+    the Elkan family with heavy rows, light-row lists and the all-heavy switch equals the GPU Lloyd fit bit for bit,
+    and its bounds pass the device auditor."""
+    from paper_2107_04074_b200 import engine, synth, validation
+    m = spk()
+    data = synth.config_dataset("C3", n_override=6_000)
+    engine.clear_engine_cache()
+    lloyd = m.run(data, k, "standard", m.SeedConfig(seed=5), max_iter=12)
+    for variant in ("simp_elkan", "elkan"):
+        r = m.run(data, k, variant, m.SeedConfig(seed=5), max_iter=12)
+        assert np.array_equal(r.assignments, lloyd.assignments), variant
+        assert r.objective == lloyd.objective
+        assert [s.reassignments for s in r.iterations] == [s.reassignments for s in lloyd.iterations]
+        assert any(s.survivors2 > 0 for s in r.iterations[1:])
+    rep = validation.audit_bounds(data, "simp_elkan", k, seed=5, max_iter=8)
+    assert rep.passed, rep
+    engine.clear_engine_cache()
+

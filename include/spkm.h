@@ -231,7 +231,7 @@ int spkm_elkan_scan(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, sp
  * l and every u(i, j) come back exact, SIMS += k per row.  Call it between
  * spkm_elkan_bounds and spkm_elkan_scan whenever W->elkan_heavy > 0.
  * spkm_elkan_heavy_threshold: the library's default for k centers (0.5% of k
- * for k > 256, SPKM_EK_HEAVY_PCT overrides; 0 = off). */
+ * rounded up for k > 128, SPKM_EK_HEAVY_PCT overrides; 0 = off). */
 int spkm_elkan_heavy(const spkm_csr *X, const spkm_centers *C, spkm_bounds *B, spkm_work *W, void *stream);
 int64_t spkm_elkan_heavy_threshold(int64_t k);
 /* spkm_elkan_bounds + spkm_elkan_scan in one pass over all rows: each row's

@@ -3903,13 +3903,17 @@ int64_t hot_terms(const spkm_centers *C) {
     return rows < C->d ? rows : C->d;
 }
 
-// Elkan family, k > 256: rows with at least this many centers failing the
+// Elkan family, k > 128: rows with at least this many centers failing the
 // stored-bound test take the full pass (spkm_elkan_heavy).
 // SPKM_EK_HEAVY_PCT: percent of k (0 = off).
 int64_t elkan_heavy_default(int64_t k) {
     const char *e = getenv("SPKM_EK_HEAVY_PCT");
     const double pct = e ? atof(e) : (double)SPKM_EK_HEAVY_PCT_DEFAULT;
-    if (k <= 256 || !(pct > 0.0)) return 0;
+    // smallest k with a heavy-row pass: 129 (k <= 128 keeps the fused bound + scan pass: C2, k = 100, is 6% slower
+    // with heavy rows; C3, k = 200: 221 -> 305 it/s with every bound survivor heavy); SPKM_EK_HEAVY_MINK overrides
+    const char *m = getenv("SPKM_EK_HEAVY_MINK");
+    const int64_t mink = m ? atoll(m) : 129;
+    if (k < mink || !(pct > 0.0)) return 0;
     const int64_t t = (int64_t)ceil((double)k * pct / 100.0 - 1e-9);
     return t < 1 ? 1 : t;
 }

@@ -798,7 +798,7 @@ class Engine:
         # Elkan family with a center index: the bound pass routes rows with many unpruned centers to
         # spkm_elkan_heavy (threshold from the library: SPKM_EK_HEAVY_PCT percent of k, 0 = off)
         self.elkan_heavy = (int(_lib.lib().spkm_elkan_heavy_threshold(k))
-                            if self.elkan and self.C.cindex is not None else 0)
+                            if self.elkan and self.corpus.dense_dim is None else 0)
         self.P = PointState(self.n_loc, k, variant, self.device, elkan_heavy=self.elkan_heavy, n_total=self.n_total)
         self.a_global = torch.zeros(max(cs.n, 1), dtype=torch.int32, device=self.device) if comm is not None else None
         # a dedicated stream: steady-state iterations are replayed as one CUDA graph
@@ -816,7 +816,7 @@ class Engine:
         # bounds and the light bound pass + survivor scan is faster (C4: 132
         # vs 140 ms).  SPKM_ELKAN_FUSE=0/1 forces it (A/B measurements).
         env = os.environ.get("SPKM_ELKAN_FUSE")
-        self.fuse_elkan = (k <= 256) if env is None else env != "0"
+        self.fuse_elkan = (k <= 256 and not self.elkan_heavy) if env is None else env != "0"
         # cluster-ordered survivor lists (spkm_order_by_cluster), SPKM_ORDER=1:
         # the gather passes visit the survivors grouped by a(i).  Off by
         # default: at C4 the clusters are too impure to share term rows, and
@@ -969,8 +969,8 @@ class Engine:
         if self.yy:
             _lib.call("spkm_yy_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, self.sp)
         elif self.elkan:
-            if self.C.cindex is not None and self.elkan_heavy:
-                # rows the stored bounds barely prune: one full pass over the sparse center index
+            if self.elkan_heavy:
+                # rows the stored bounds barely prune: one full pass (over the sparse center index for k > 256)
                 self.C.build_cindex(self.sp)
                 _lib.call("spkm_elkan_heavy", self.xs, self.C.struct, self.P.bounds, self.P.work, self.sp)
             _lib.call("spkm_elkan_scan", self.xs, self.C.struct, self.P.bounds, self.P.work, use_flag, self.sp)

@@ -812,9 +812,9 @@ class Engine:
         self._side = {}
         self.use_graphs = use_graphs and comm is None
         # Elkan family: bound update + scan as one pass (spkm_elkan_bounds_scan)
-        # for k <= 256 (C3: +4%); at k = 1000 most rows are pruned by the
-        # bounds and the light bound pass + survivor scan is faster (C4: 132
-        # vs 140 ms).  SPKM_ELKAN_FUSE=0/1 forces it (A/B measurements).
+        # for k <= 128; above, the separate bound pass routes rows to the heavy
+        # full pass / the light scan (C3: 221 -> 311 it/s, C4: 13.2 -> 20.7).
+        # SPKM_ELKAN_FUSE=0/1 forces it (A/B measurements).
         env = os.environ.get("SPKM_ELKAN_FUSE")
         self.fuse_elkan = (k <= 256 and not self.elkan_heavy) if env is None else env != "0"
         # cluster-ordered survivor lists (spkm_order_by_cluster), SPKM_ORDER=1:
